@@ -1,0 +1,244 @@
+/*
+ * stg.h — C-ABI of libstg (strata-on-B200): the per-window analysis hot path
+ *   ingest -> symbolize -> aggregate -> diff -> verdict, plus collective alignment,
+ * as hand-written sm_100a CUDA behind plain C entry points.
+ *
+ * The reference ("strata", /root/reference/proj) exposes this path only as C++20
+ * free functions in namespace strata; it has no C-ABI, plugin or FFI.  Each entry
+ * point below names the reference function(s) it replaces (file:line under
+ * proj/core/).  The C++ drop-in shim (paper_2603_29235_b200/csrc/shim/) re-defines
+ * those strata:: functions on top of this header, so reference callers relink
+ * unchanged; INTEGRATION.md shows the bindings.
+ *
+ * Conventions
+ *  - Every function returns an int status (STG_OK = 0).  On failure the message is
+ *    available from stg_last_error() (thread-local).  STG_EINVAL carries exactly
+ *    the strata::Error message the reference would throw for the same input.
+ *  - Plain pointers and sizes only; no torch or C++ types.  Bulk sample arrays may
+ *    live in host memory (copied in by the call) or already in device memory
+ *    (stg_window.memory = STG_MEM_DEVICE, pointers valid on the context's GPU).
+ *  - A context owns device memory, streams and the loaded symbol tables; calls on
+ *    one context are serialised by an internal mutex.
+ */
+#ifndef STG_H
+#define STG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STG_ABI_VERSION 1
+
+enum stg_status {
+    STG_OK = 0,
+    STG_EINVAL = 1, /* input rejected (strata::Error in the reference)      */
+    STG_ECUDA = 2,  /* CUDA runtime / kernel failure                         */
+    STG_ENOMEM = 3, /* device or host allocation failed                      */
+    STG_ESTATE = 4, /* call order violated (no result yet, bad index, ...)    */
+    STG_ENOTFOUND = 5
+};
+
+/* SymbolFile::LookupMode (symfile.hpp:32) */
+enum stg_lookup_mode { STG_LOOKUP_EXACT_RANGE = 0, STG_LOOKUP_NEAREST_LOWER = 1 };
+
+enum stg_memory { STG_MEM_HOST = 0, STG_MEM_DEVICE = 1 };
+
+/* Verdict (diagnosis.hpp:159-167), same numeric order. */
+enum stg_verdict {
+    STG_VERDICT_HEALTHY = 0,
+    STG_VERDICT_GPU_UNIFORM = 1,
+    STG_VERDICT_GPU_SPECIFIC = 2,
+    STG_VERDICT_CPU_INTERFERENCE = 3,
+    STG_VERDICT_OS_INTERFERENCE = 4,
+    STG_VERDICT_TEMPORAL = 5,
+    STG_VERDICT_INCONCLUSIVE = 6
+};
+
+typedef struct stg_ctx stg_ctx;
+
+/* ---------------------------------------------------------------- lifecycle */
+const char* stg_last_error(void);
+int stg_abi_version(void);
+/* stg_create: one context per GPU (device ordinal). */
+int stg_create(int device, stg_ctx** out);
+void stg_destroy(stg_ctx* ctx);
+
+/* ------------------------------------------------------------------- ingest
+ * Replaces SymbolRepository::ingest/load (symrepo.cpp:35-97) + parse_symbols
+ * (symfile.cpp:117-157): validates a SYMR payload with the reference's exact
+ * rules and messages, and stages its table on the device (sorted starts, packed
+ * {size, name}, a bucket index for the search).  Idempotent per build id
+ * (IngestOutcome::AlreadyPresent -> *stored = 0).  claimed_id (20 bytes, may be
+ * NULL = take the header's id) plays the role of ingest()'s key argument.
+ * The 64 MiB segment SHA-1 check of the transport (symrepo.cpp:23-51) is the
+ * sender's concern and is not repeated here. */
+int stg_symtab_ingest(stg_ctx* ctx, const uint8_t* claimed_id, const uint8_t* symr,
+                      uint64_t len, int* stored);
+int stg_symtab_count(stg_ctx* ctx, uint32_t* n_tables);
+
+/* --------------------------------------------------------------- symbolize
+ * Replaces resolve_stacks (symrepo.cpp:122-143) / resolve_stack (:99-120):
+ * frame-wise lookup of (build id, offset) pairs on the GPU.  Each frame gets a
+ * name key; stg_name() renders it (real symbol name, or the reference's unknown
+ * label "[<hex id>+0x<off>]", symfile.cpp:159-163).  Keys are valid until the
+ * next call on the context and are ordered like the names they denote. */
+int stg_resolve(stg_ctx* ctx, uint64_t n_frames, const uint64_t* frame_pc,
+                const uint16_t* frame_bin, int32_t n_bins, const uint8_t* bin_build_ids,
+                int mode, uint32_t* out_keys);
+int stg_name(stg_ctx* ctx, uint32_t key, char* buf, uint64_t cap, uint64_t* needed);
+int stg_name_count(stg_ctx* ctx, uint32_t* n);
+
+/* ------------------------------------------------------------------ window
+ * One analysis window in structure-of-arrays form: the in-memory equivalent of
+ * strata::LoadedBundle (bundle.hpp:23-42).  Samples are grouped by rank
+ * (rank-major, time-ordered within a rank as in LoadedBundle::samples). */
+typedef struct stg_window {
+    int32_t memory; /* stg_memory of sample_ts / sample_frame_off / frame_* */
+    int32_t group;
+    int64_t window_start_ns;
+    int64_t window_end_ns;
+    int64_t max_skew_ns;
+
+    /* ranks that own a CPU sample stream (keys of LoadedBundle::samples) */
+    int32_t n_ranks;
+    const int32_t* rank_ids;         /* host, strictly ascending          */
+    const uint64_t* rank_sample_off; /* host, n_ranks+1, into samples     */
+
+    /* binaries referenced by frames: frame_bin indexes this list */
+    int32_t n_bins;
+    const uint8_t* bin_build_ids; /* host, n_bins * 20 bytes */
+
+    /* CPU stack samples (StackSample, samples.hpp:15-21; spaces are ignored
+     * downstream by the reference, so they are not carried) */
+    uint64_t n_samples;
+    const int64_t* sample_ts;         /* [n_samples] rank-local clock        */
+    const uint64_t* sample_frame_off; /* [n_samples+1] CSR into frames       */
+    uint64_t n_frames;
+    const uint64_t* frame_pc;  /* [n_frames] code offsets, leaf first     */
+    const uint16_t* frame_bin; /* [n_frames] index into bin_build_ids     */
+
+    /* NCCL collective events (CollectiveEvent, collective.hpp:24-31), host,
+     * in LoadedBundle::collectives order */
+    uint64_t n_coll;
+    const int32_t* coll_rank;
+    const int32_t* coll_group;
+    const uint8_t* coll_kind; /* CollectiveKind ordinal */
+    const int64_t* coll_entry;
+    const int64_t* coll_exit;
+    const int64_t* coll_gpu_dur;
+    int32_t n_group_ranks;
+    const int32_t* group_ranks;
+
+    /* GPU kernel events (GpuEvent, scenario.hpp:72-78), host */
+    uint64_t n_gpu;
+    const int32_t* gpu_rank;
+    const uint32_t* gpu_kernel; /* index into kernel_names */
+    const int64_t* gpu_start;
+    const int64_t* gpu_dur;
+    uint32_t n_kernel_names;
+    const char* const* kernel_names;
+
+    /* OS counter records (OsCounterRecord, scenario.hpp:80-84), host */
+    uint64_t n_os;
+    const int32_t* os_rank;
+    const int64_t* os_window_start;
+    const int64_t* os_p50;
+    const int64_t* os_p99;
+    const int64_t* os_migrations;
+    const uint64_t* os_irq_off; /* n_os+1 CSR over (key, value) */
+    const uint32_t* os_irq_key; /* index into counter_names      */
+    const int64_t* os_irq_val;
+    const uint64_t* os_sirq_off;
+    const uint32_t* os_sirq_key;
+    const int64_t* os_sirq_val;
+    uint32_t n_counter_names;
+    const char* const* counter_names;
+
+    /* historical baseline (BaselineProfile, diagnosis.hpp:142-147) */
+    int32_t has_baseline;
+    double baseline_delta;
+    uint32_t n_baseline;
+    const char* const* baseline_names;
+    const double* baseline_fracs;
+    int32_t has_baseline_iteration;
+    double baseline_iteration_ms;
+} stg_window;
+
+/* DiagnosisConfig (diagnosis.hpp:203-210) + GpuDiffConfig (:83-92) + OsDiffConfig
+ * (:127-132).  stg_config_default() fills the reference defaults. */
+typedef struct stg_config {
+    int32_t window_iterations;
+    double k;
+    double delta;
+    double iteration_regression_gate;
+    double gpu_median_uniform;
+    double gpu_cv_uniform;
+    double gpu_top_share_specific;
+    double gpu_median_none;
+    int64_t gpu_ref_floor_ns;
+    char gpu_exclude_prefix[32];
+    double os_min_ratio;
+    int64_t os_interrupt_floor;
+    int64_t os_sched_delay_floor_ns;
+    int64_t os_migration_floor;
+    int32_t lookup_mode;    /* build_group_data uses ExactRange (bundle.cpp:300) */
+    int32_t want_waterline; /* also compute compute_waterline/flag_ranks     */
+} stg_config;
+
+void stg_config_default(stg_config* cfg);
+
+/* Counters of one run (sizes of the result, device timings of the stages). */
+typedef struct stg_run_stats {
+    uint64_t n_samples_in_window;
+    uint64_t n_lines;        /* Σ over ranks of folded lines                 */
+    uint64_t n_sequences;    /* distinct symbolized stacks across all ranks  */
+    uint64_t n_names;        /* size of the result name space                */
+    uint64_t n_unknown;      /* distinct unresolved frames                   */
+    uint64_t n_instances;    /* matched collective instances                 */
+    uint64_t n_windowed;     /* complete instances inside the window         */
+    uint64_t n_cpu_ranks;    /* ranks with a CPU profile                     */
+    int32_t verdict;
+    int32_t n_flagged;
+    float ms_collectives;    /* device time per stage (CUDA events)          */
+    float ms_symbolize;      /* the fused symbolize+aggregate kernel         */
+    float ms_fold;
+    float ms_diff;
+    float ms_total;
+    uint64_t h2d_bytes;
+    uint64_t d2h_bytes;
+    uint32_t kernel_launches;
+} stg_run_stats;
+
+/* Replaces build_group_data (bundle.cpp:252-324) followed by diagnose
+ * (diagnosis.cpp:301-432): the whole window batch on the GPU, keeping the
+ * result (GroupData + DiagnosisReport) in the context for the getters below. */
+int stg_window_run(stg_ctx* ctx, const stg_window* win, const stg_config* cfg,
+                   stg_run_stats* stats);
+
+/* Canonical JSON renderings of the last window's result (for parity tests and
+ * tools): GroupData (every field of diagnosis.hpp:192-201) and the report in the
+ * layout of DiagnosisReport::to_json (diagnosis.cpp:437-455).  Two-call size
+ * query: pass buf=NULL to get *needed. */
+int stg_result_groupdata_json(stg_ctx* ctx, char* buf, uint64_t cap, uint64_t* needed);
+int stg_result_report_json(stg_ctx* ctx, char* buf, uint64_t cap, uint64_t* needed);
+/* Waterline (compute_waterline, diagnosis.cpp:35-55) + flag_ranks (:57-71) over
+ * the last window's CPU profiles, when cfg.want_waterline was set. */
+int stg_result_waterline_json(stg_ctx* ctx, char* buf, uint64_t cap, uint64_t* needed);
+
+/* Structured access to the folded profiles of the last window (to_folded,
+ * folded.cpp:56-71): per CPU rank, lines in the reference's lexicographic
+ * order as name-key sequences (root first) with counts. */
+int stg_result_rank_count(stg_ctx* ctx, uint32_t* n);
+int stg_result_rank_info(stg_ctx* ctx, uint32_t i, int32_t* rank, uint64_t* n_lines,
+                         uint64_t* total, uint64_t* n_keys);
+int stg_result_rank_lines(stg_ctx* ctx, uint32_t i, uint64_t* line_key_off /* n_lines+1 */,
+                          uint32_t* keys, uint64_t* counts);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STG_H */

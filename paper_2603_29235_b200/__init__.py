@@ -1,0 +1,170 @@
+"""paper_2603_29235_b200 — SysOM-AI's per-window analysis hot path on B200.
+
+The product is libstg.so (include/stg.h): hand-written sm_100a CUDA behind a
+C-ABI.  This module is the thin Python host binding used by tests and bench.py;
+it mirrors the reference's verbs (proj/core/include/strata/*.hpp):
+
+    Context.ingest(symr)            SymbolRepository::ingest / parse_symbols
+    Context.resolve(...)            resolve_stacks
+    Context.window_run(win)         build_group_data + diagnose
+    Context.groupdata() / report()  GroupData / DiagnosisReport::to_json
+
+There is no CPU fallback: if libstg.so is missing or no GPU is visible, every
+call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+from pathlib import Path
+from typing import Optional
+
+import numpy as np
+
+from .abi import (STG_MEM_DEVICE, STG_MEM_HOST, VERDICTS, StgConfig, StgRunStats, StgWindow,
+                  Window, config_struct, default_config)
+
+__all__ = ["Context", "StgError", "Window", "load_library", "LIB_PATH", "VERDICTS",
+           "default_config"]
+
+LIB_PATH = Path(__file__).resolve().parent / "libstg.so"
+_lib = None
+
+
+class StgError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+def load_library():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise RuntimeError(f"{LIB_PATH} is missing — run `python -m paper_2603_29235_b200.build` "
+                           "(there is no CPU fallback)")
+    l = C.CDLL(str(LIB_PATH))
+    P = C.c_void_p
+    l.stg_last_error.restype = C.c_char_p
+    l.stg_create.argtypes = [C.c_int, C.POINTER(P)]
+    l.stg_destroy.argtypes = [P]
+    l.stg_symtab_ingest.argtypes = [P, C.c_char_p, C.c_char_p, C.c_uint64, C.POINTER(C.c_int)]
+    l.stg_symtab_count.argtypes = [P, C.POINTER(C.c_uint32)]
+    l.stg_resolve.argtypes = [P, C.c_uint64, P, P, C.c_int32, P, C.c_int, P]
+    l.stg_name.argtypes = [P, C.c_uint32, C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64)]
+    l.stg_name_count.argtypes = [P, C.POINTER(C.c_uint32)]
+    l.stg_config_default.argtypes = [C.POINTER(StgConfig)]
+    l.stg_window_run.argtypes = [P, C.POINTER(StgWindow), C.POINTER(StgConfig), C.POINTER(StgRunStats)]
+    for fn in ("stg_result_groupdata_json", "stg_result_report_json", "stg_result_waterline_json"):
+        getattr(l, fn).argtypes = [P, C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64)]
+    l.stg_result_rank_count.argtypes = [P, C.POINTER(C.c_uint32)]
+    l.stg_result_rank_info.argtypes = [P, C.c_uint32, C.POINTER(C.c_int32), C.POINTER(C.c_uint64),
+                                       C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+    l.stg_result_rank_lines.argtypes = [P, C.c_uint32, P, P, P]
+    _lib = l
+    return l
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise StgError(rc, load_library().stg_last_error().decode())
+
+
+class Context:
+    """One libstg context bound to one GPU."""
+
+    def __init__(self, device: int = 0):
+        self._l = load_library()
+        self._h = C.c_void_p()
+        _check(self._l.stg_create(device, C.byref(self._h)))
+        self.last_stats: Optional[dict] = None
+
+    def close(self):
+        if self._h:
+            self._l.stg_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---------------------------------------------------------------- ingest
+    def ingest(self, symr: bytes, claimed_id: Optional[bytes] = None) -> bool:
+        stored = C.c_int(0)
+        _check(self._l.stg_symtab_ingest(self._h, claimed_id, symr, len(symr), C.byref(stored)))
+        return bool(stored.value)
+
+    def table_count(self) -> int:
+        n = C.c_uint32()
+        _check(self._l.stg_symtab_count(self._h, C.byref(n)))
+        return n.value
+
+    # ------------------------------------------------------------- symbolize
+    def resolve(self, pcs, bins, build_ids, mode: int = 0):
+        """Frame-wise names (resolve_stacks); returns a list of strings."""
+        pcs = np.ascontiguousarray(pcs, np.uint64)
+        bins = np.ascontiguousarray(bins, np.uint16)
+        ids = np.ascontiguousarray(np.asarray(build_ids, np.uint8).reshape(-1, 20))
+        out = np.zeros(len(pcs), np.uint32)
+        _check(self._l.stg_resolve(self._h, len(pcs), pcs.ctypes.data, bins.ctypes.data, ids.shape[0],
+                                   ids.ctypes.data, mode, out.ctypes.data))
+        return [self.name(int(k)) for k in out], out
+
+    def name(self, key: int) -> str:
+        need = C.c_uint64()
+        _check(self._l.stg_name(self._h, key, None, 0, C.byref(need)))
+        buf = C.create_string_buffer(need.value)
+        _check(self._l.stg_name(self._h, key, buf, need.value, C.byref(need)))
+        return buf.value.decode()
+
+    # ---------------------------------------------------------------- window
+    def window_run(self, win: Window, cfg: Optional[dict] = None, ingest: bool = True) -> dict:
+        if ingest:
+            for s in win.symr:
+                self.ingest(s)
+        cw, keep = win.to_c()
+        cc = config_struct(cfg)
+        st = StgRunStats()
+        _check(self._l.stg_window_run(self._h, C.byref(cw), C.byref(cc), C.byref(st)))
+        self.last_stats = st.as_dict()
+        return self.last_stats
+
+    def _json(self, fn) -> dict:
+        need = C.c_uint64()
+        _check(fn(self._h, None, 0, C.byref(need)))
+        buf = C.create_string_buffer(need.value)
+        _check(fn(self._h, buf, need.value, C.byref(need)))
+        return json.loads(buf.value.decode())
+
+    def groupdata(self) -> dict:
+        return self._json(self._l.stg_result_groupdata_json)
+
+    def report(self) -> dict:
+        return self._json(self._l.stg_result_report_json)
+
+    def waterline(self) -> dict:
+        return self._json(self._l.stg_result_waterline_json)
+
+    def folded(self):
+        """{rank: (total, [(names root-first, count), ...])} via the structured getters."""
+        n = C.c_uint32()
+        _check(self._l.stg_result_rank_count(self._h, C.byref(n)))
+        out = {}
+        for i in range(n.value):
+            rank, nl, tot, nk = C.c_int32(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+            _check(self._l.stg_result_rank_info(self._h, i, C.byref(rank), C.byref(nl), C.byref(tot),
+                                                C.byref(nk)))
+            off = np.zeros(nl.value + 1, np.uint64)
+            keys = np.zeros(max(nk.value, 1), np.uint32)
+            cnt = np.zeros(max(nl.value, 1), np.uint64)
+            _check(self._l.stg_result_rank_lines(self._h, i, off.ctypes.data, keys.ctypes.data,
+                                                 cnt.ctypes.data))
+            lines = []
+            for l in range(nl.value):
+                names = [self.name(int(k)) for k in keys[off[l]:off[l + 1]]]
+                lines.append((names, int(cnt[l])))
+            out[rank.value] = (tot.value, lines)
+        return out

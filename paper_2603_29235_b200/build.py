@@ -1,0 +1,68 @@
+"""Builds libstg.so (the CUDA library behind include/stg.h) in-tree for sm_100a.
+
+    python -m paper_2603_29235_b200.build          # libstg.so (+ the C++ shim)
+
+Objects go to paper_2603_29235_b200/_build/, the library to
+paper_2603_29235_b200/libstg.so (git-ignored, travels to the GPU box).
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+OUT = PKG / "_build"
+LIB = PKG / "libstg.so"
+NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CUDA_INC = "/usr/local/cuda/include"
+
+CU_SOURCES = ["stg_window.cu"]
+CPP_SOURCES = ["symtab.cpp", "stg_api.cpp"]
+HEADERS = ["stg_internal.h", "kernels.cuh", "result.h", "stg_runner.inl", "stg_output.inl"]
+
+
+def _run(cmd):
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+        raise RuntimeError(f"build step failed: {cmd[0]} ... {cmd[-1]}")
+    return r
+
+
+def _stale(target: Path, deps) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(Path(d).stat().st_mtime > t for d in deps)
+
+
+def build(verbose: bool = False) -> Path:
+    OUT.mkdir(exist_ok=True)
+    hdrs = [CSRC / h for h in HEADERS] + [ROOT / "include" / "stg.h"]
+    objs = []
+    for src in CU_SOURCES:
+        obj = OUT / (Path(src).stem + ".o")
+        if _stale(obj, [CSRC / src] + hdrs):
+            _run([NVCC, "-std=c++17", "-O3", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC",
+                  "-Xptxas", "-v" if verbose else "-O3", "-diag-suppress", "177",
+                  f"-I{ROOT / 'include'}", "-c", str(CSRC / src), "-o", str(obj)])
+        objs.append(obj)
+    for src in CPP_SOURCES:
+        obj = OUT / (Path(src).stem + ".o")
+        if _stale(obj, [CSRC / src] + hdrs):
+            _run(["g++", "-std=c++17", "-O2", "-fPIC", f"-I{ROOT / 'include'}", f"-I{CUDA_INC}",
+                  "-c", str(CSRC / src), "-o", str(obj)])
+        objs.append(obj)
+    if _stale(LIB, objs):
+        _run([NVCC, "-shared", *ARCH, "-o", str(LIB), *map(str, objs), "-lcudart"])
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(verbose="-v" in sys.argv))

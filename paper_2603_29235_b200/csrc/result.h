@@ -1,0 +1,77 @@
+// result.h — host-side view of one window's result (GroupData + report).
+#pragma once
+
+#include <map>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "stg_internal.h"
+
+namespace stg {
+
+struct Evidence {
+    std::string layer, item;
+    double straggler_value = 0, reference_value = 0, delta = 0;
+};
+
+struct Report {
+    int verdict = STG_VERDICT_HEALTHY;
+    std::vector<int> flagged_ranks;
+    std::vector<Evidence> evidence;
+    std::vector<std::string> top_path;
+    std::optional<int> reference_rank;
+    std::vector<std::string> notes;
+};
+
+struct OsAcc {
+    std::map<std::string, int64_t> interrupts, softirqs;
+    int64_t p50 = 0, p99 = 0, migrations = 0;
+};
+
+// Everything a window run leaves behind.  Bulk arrays stay on the device
+// (ctx buffers); what the decision ladder and the getters need is mirrored here.
+struct Result {
+    int group = 0;
+    int32_t rank_span = 0;  // dense rank index space [0, rank_span)
+    // ---- collectives
+    bool have_offsets = false;
+    std::vector<int64_t> offsets;   // [rank_span]
+    std::vector<uint8_t> has_offset;
+    uint64_t n_instances = 0, n_windowed = 0;
+    std::vector<double> iteration_times_ms;
+    // straggler stats per rank (dense)
+    std::vector<uint8_t> lat_present;     // rank appears in some windowed instance
+    std::vector<double> mean_lat_all;     // over all instances containing it (median_lateness_rank)
+    std::vector<double> mean_lat_alert;   // over instances with >= 2 ranks (StragglerAlert)
+    std::vector<double> z_mean;
+    std::vector<uint64_t> flag_count;
+    std::vector<uint8_t> has_z;
+    // ---- gpu / os
+    std::map<int, std::map<std::string, int64_t>> gpu;
+    std::map<int, OsAcc> os;
+    // ---- cpu profiles
+    std::vector<int32_t> cpu_rank_ids;  // ranks with a profile (ascending)
+    std::vector<uint32_t> cpu_rank_index;  // index into window ranks
+    std::vector<uint64_t> cpu_totals;
+    uint64_t n_lines = 0, n_seq = 0, n_names = 0, n_unknown = 0, f_used = 0, n_gid = 0;
+    uint32_t n_window_ranks = 0;
+    // name space: final rank -> string
+    std::vector<uint64_t> unk_final;       // final rank of each distinct unknown label (sorted)
+    std::vector<std::string> unk_labels;   // labels in the same order
+    const std::vector<std::string>* dict = nullptr;
+    std::string name_of(uint32_t final_rank) const;
+    // ---- baseline
+    bool has_baseline = false;
+    double baseline_delta = 0.005;
+    std::map<std::string, double> baseline;
+    bool has_baseline_iteration = false;
+    double baseline_iteration_ms = 0;
+    // ---- report
+    Report report;
+    bool waterline_done = false;
+    std::string waterline_json;
+    stg_run_stats stats{};
+};
+
+}  // namespace stg

@@ -1,0 +1,226 @@
+// stg_api.cpp — the extern "C" surface of libstg (include/stg.h).  Every entry
+// point catches stg::Error / std::exception, stores the message thread-locally
+// and returns a status code; no C++ exception crosses the boundary.
+#include <cstring>
+#include <string>
+
+#include "result.h"
+#include "stg_internal.h"
+
+namespace stg {
+void window_run(Ctx& c, const stg_window& w, const stg_config& cfg);
+std::string groupdata_json(Ctx& c);
+std::string report_json(Ctx& c);
+void run_resolve(Ctx& c, Result& res, uint64_t n, const uint64_t* pc, const uint16_t* bin, int32_t n_bins,
+                 const uint8_t* ids, int mode, uint32_t* out);
+void rank_lines(Ctx& c, uint32_t i, std::vector<uint64_t>& key_off, std::vector<uint32_t>& keys,
+                std::vector<uint64_t>& counts);
+}  // namespace stg
+
+struct stg_ctx {
+    stg::Ctx impl;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        g_err.clear();
+        return STG_OK;
+    } catch (const stg::Error& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return STG_ENOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return STG_EINVAL;
+    }
+}
+
+int copy_out(const std::string& s, char* buf, uint64_t cap, uint64_t* needed) {
+    if (needed) *needed = s.size() + 1;
+    if (!buf) return STG_OK;
+    if (cap < s.size() + 1) {
+        g_err = "buffer too small";
+        return STG_EINVAL;
+    }
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+    return STG_OK;
+}
+
+stg::Result& need_result(stg_ctx* c) {
+    if (!c->impl.result) stg::fail(STG_ESTATE, "no window result on this context");
+    return *c->impl.result;
+}
+}  // namespace
+
+extern "C" {
+
+const char* stg_last_error(void) { return g_err.c_str(); }
+int stg_abi_version(void) { return STG_ABI_VERSION; }
+
+int stg_create(int device, stg_ctx** out) {
+    return guard([&] {
+        int n = 0;
+        STG_CUDA(cudaGetDeviceCount(&n));
+        if (device < 0 || device >= n) stg::fail(STG_EINVAL, "no such CUDA device");
+        STG_CUDA(cudaSetDevice(device));
+        auto* c = new stg_ctx;
+        c->impl.device = device;
+        cudaError_t e = cudaStreamCreateWithFlags(&c->impl.stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) {
+            delete c;
+            stg::fail(STG_ECUDA, cudaGetErrorString(e));
+        }
+        *out = c;
+    });
+}
+
+void stg_destroy(stg_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->impl.device);
+    delete ctx;
+}
+
+int stg_symtab_ingest(stg_ctx* ctx, const uint8_t* claimed_id, const uint8_t* symr, uint64_t len, int* stored) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(ctx->impl.mu);
+        STG_CUDA(cudaSetDevice(ctx->impl.device));
+        stg::symtab_ingest(ctx->impl, claimed_id, symr, len, stored);
+    });
+}
+
+int stg_symtab_count(stg_ctx* ctx, uint32_t* n) {
+    return guard([&] { *n = uint32_t(ctx->impl.tables.size()); });
+}
+
+int stg_resolve(stg_ctx* ctx, uint64_t n_frames, const uint64_t* frame_pc, const uint16_t* frame_bin,
+                int32_t n_bins, const uint8_t* bin_build_ids, int mode, uint32_t* out_keys) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(ctx->impl.mu);
+        STG_CUDA(cudaSetDevice(ctx->impl.device));
+        if (mode != STG_LOOKUP_EXACT_RANGE && mode != STG_LOOKUP_NEAREST_LOWER) stg::fail(STG_EINVAL, "bad lookup mode");
+        if (!ctx->impl.result) ctx->impl.result = std::make_unique<stg::Result>();
+        stg::run_resolve(ctx->impl, *ctx->impl.result, n_frames, frame_pc, frame_bin, n_bins, bin_build_ids, mode,
+                         out_keys);
+    });
+}
+
+int stg_name(stg_ctx* ctx, uint32_t key, char* buf, uint64_t cap, uint64_t* needed) {
+    std::string s;
+    int rc = guard([&] {
+        stg::Result& r = need_result(ctx);
+        if (!r.dict || key >= r.n_names) stg::fail(STG_EINVAL, "name key out of range");
+        s = r.name_of(key);
+    });
+    if (rc) return rc;
+    return copy_out(s, buf, cap, needed);
+}
+
+int stg_name_count(stg_ctx* ctx, uint32_t* n) {
+    return guard([&] { *n = uint32_t(need_result(ctx).n_names); });
+}
+
+void stg_config_default(stg_config* c) {
+    std::memset(c, 0, sizeof *c);
+    c->window_iterations = 100;
+    c->k = 2.0;
+    c->delta = 0.005;
+    c->iteration_regression_gate = 0.03;
+    c->gpu_median_uniform = 0.03;
+    c->gpu_cv_uniform = 0.25;
+    c->gpu_top_share_specific = 0.60;
+    c->gpu_median_none = 0.01;
+    c->gpu_ref_floor_ns = 1000000;
+    std::strcpy(c->gpu_exclude_prefix, "nccl");
+    c->os_min_ratio = 2.0;
+    c->os_interrupt_floor = 1000;
+    c->os_sched_delay_floor_ns = 1000000;
+    c->os_migration_floor = 100;
+    c->lookup_mode = STG_LOOKUP_EXACT_RANGE;
+    c->want_waterline = 0;
+}
+
+int stg_window_run(stg_ctx* ctx, const stg_window* win, const stg_config* cfg, stg_run_stats* stats) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(ctx->impl.mu);
+        STG_CUDA(cudaSetDevice(ctx->impl.device));
+        stg_config def;
+        stg_config_default(&def);
+        stg::window_run(ctx->impl, *win, cfg ? *cfg : def);
+        if (stats) *stats = ctx->impl.result->stats;
+    });
+}
+
+int stg_result_groupdata_json(stg_ctx* ctx, char* buf, uint64_t cap, uint64_t* needed) {
+    std::string s;
+    int rc = guard([&] {
+        std::lock_guard<std::mutex> lk(ctx->impl.mu);
+        need_result(ctx);
+        s = stg::groupdata_json(ctx->impl);
+    });
+    if (rc) return rc;
+    return copy_out(s, buf, cap, needed);
+}
+
+int stg_result_report_json(stg_ctx* ctx, char* buf, uint64_t cap, uint64_t* needed) {
+    std::string s;
+    int rc = guard([&] {
+        need_result(ctx);
+        s = stg::report_json(ctx->impl);
+    });
+    if (rc) return rc;
+    return copy_out(s, buf, cap, needed);
+}
+
+int stg_result_waterline_json(stg_ctx* ctx, char* buf, uint64_t cap, uint64_t* needed) {
+    std::string s;
+    int rc = guard([&] {
+        stg::Result& r = need_result(ctx);
+        if (!r.waterline_done) stg::fail(STG_ESTATE, "run the window with want_waterline = 1");
+        s = r.waterline_json;
+    });
+    if (rc) return rc;
+    return copy_out(s, buf, cap, needed);
+}
+
+int stg_result_rank_count(stg_ctx* ctx, uint32_t* n) {
+    return guard([&] { *n = uint32_t(need_result(ctx).cpu_rank_ids.size()); });
+}
+
+int stg_result_rank_info(stg_ctx* ctx, uint32_t i, int32_t* rank, uint64_t* n_lines, uint64_t* total,
+                         uint64_t* n_keys) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(ctx->impl.mu);
+        stg::Result& r = need_result(ctx);
+        if (i >= r.cpu_rank_ids.size()) stg::fail(STG_ESTATE, "rank index out of range");
+        std::vector<uint64_t> ko, cnt;
+        std::vector<uint32_t> keys;
+        stg::rank_lines(ctx->impl, i, ko, keys, cnt);
+        if (rank) *rank = r.cpu_rank_ids[i];
+        if (n_lines) *n_lines = cnt.size();
+        if (total) *total = r.cpu_totals[i];
+        if (n_keys) *n_keys = keys.size();
+    });
+}
+
+int stg_result_rank_lines(stg_ctx* ctx, uint32_t i, uint64_t* line_key_off, uint32_t* keys_out, uint64_t* counts) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(ctx->impl.mu);
+        stg::Result& r = need_result(ctx);
+        if (i >= r.cpu_rank_ids.size()) stg::fail(STG_ESTATE, "rank index out of range");
+        std::vector<uint64_t> ko, cnt;
+        std::vector<uint32_t> keys;
+        stg::rank_lines(ctx->impl, i, ko, keys, cnt);
+        std::memcpy(line_key_off, ko.data(), ko.size() * sizeof(uint64_t));
+        std::memcpy(keys_out, keys.data(), keys.size() * sizeof(uint32_t));
+        std::memcpy(counts, cnt.data(), cnt.size() * sizeof(uint64_t));
+    });
+}
+
+}  // extern "C"

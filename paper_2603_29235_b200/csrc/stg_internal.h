@@ -1,0 +1,146 @@
+// stg_internal.h — shared host/device declarations of libstg.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "stg.h"
+
+namespace stg {
+
+// ---------------------------------------------------------------- errors
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void fail(int code, const std::string& m) { throw Error(code, m); }
+#define STG_CUDA(x)                                                                   \
+    do {                                                                              \
+        cudaError_t e_ = (x);                                                         \
+        if (e_ != cudaSuccess)                                                        \
+            ::stg::fail(STG_ECUDA, std::string(#x " -> ") + cudaGetErrorString(e_));  \
+    } while (0)
+
+// --------------------------------------------------------- device tables
+// One staged symbol table (the device form of a SymbolFile, symfile.hpp:20-41).
+// ent[i] = size (low 32 bits) | name rank (high 32 bits).  bucket[b] is the
+// index of the last entry whose start <= base + (b << shift); the search for an
+// offset in bucket b is confined to [bucket[b], bucket[b+1]].
+struct DevTable {
+    const uint64_t* starts;
+    const uint64_t* ent;
+    const uint32_t* bucket;
+    uint64_t base;
+    uint64_t last_start;
+    uint32_t shift;
+    uint32_t nb;
+    uint32_t n;
+    uint32_t valid;
+};
+
+constexpr uint32_t kUnknownBit = 0x80000000u;
+constexpr int kMaxSmemBins = 64;
+
+// Per-rank hash-table slot of the fused symbolize+aggregate kernel.
+struct __align__(32) AggSlot {
+    unsigned long long hi;  // 0 = empty
+    unsigned long long lo;  // fingerprint half 2 (never 0 once written)
+    unsigned int count;
+    unsigned int rep;       // sample index (rank-relative) that created the slot
+    unsigned int pad0, pad1;
+};
+
+// Global sequence-dedupe slot.
+struct __align__(32) SeqSlot {
+    unsigned long long hi;
+    unsigned long long lo;
+    unsigned int gid;       // 0xffffffff until published
+    unsigned int pad;
+    unsigned long long rep; // global sample index of the representative
+};
+
+// Unknown-frame set slot: (bin, pc) -> slot index.
+struct __align__(16) UnkSlot {
+    unsigned long long pc;
+    unsigned int bin1;      // bin+1; 0 = empty, 0xffffffff = being written
+    unsigned int pad;
+};
+
+// ------------------------------------------------------------ host-side
+struct HostTable {
+    uint8_t id[20];
+    std::vector<uint64_t> starts;
+    std::vector<uint32_t> sizes;
+    std::vector<uint32_t> name_local;   // index into names
+    std::vector<std::string> names;     // distinct names of this table
+    // device
+    uint64_t* d_starts = nullptr;
+    uint64_t* d_ent = nullptr;
+    uint32_t* d_bucket = nullptr;
+    uint32_t shift = 0, nb = 0;
+    uint64_t dict_version = ~0ull;      // dictionary the ent ranks refer to
+};
+
+// Grow-only device buffer.
+struct DBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void* get(size_t bytes) {
+        if (bytes > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            size_t c = bytes + bytes / 4 + 256;
+            if (cudaMalloc(&p, c) != cudaSuccess) {
+                cap = 0;
+                cudaGetLastError();
+                fail(STG_ENOMEM, "device allocation of " + std::to_string(c) + " bytes failed");
+            }
+            cap = c;
+        }
+        return p;
+    }
+    template <class T>
+    T* as(size_t n) { return static_cast<T*>(get(n * sizeof(T) + 16)); }
+    ~DBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+struct Result;  // defined in stg_window.cu
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::mutex mu;
+    std::vector<std::unique_ptr<HostTable>> tables;
+    std::map<std::string, size_t> table_by_id;  // raw 20-byte id -> index
+    // sorted name dictionary over all loaded tables
+    std::vector<std::string> dict;
+    uint64_t dict_version = 0;
+    bool dict_dirty = true;
+    std::map<std::string, DBuf> bufs;
+    DBuf& buf(const std::string& k) { return bufs[k]; }
+    std::unique_ptr<Result> result;
+    ~Ctx();
+};
+
+// symtab.cpp
+void symtab_ingest(Ctx& c, const uint8_t* claimed_id, const uint8_t* bytes, uint64_t len,
+                   int* stored);
+void symtab_refresh_dictionary(Ctx& c);  // (re)build dict + stage device tables
+std::string hex_id(const uint8_t* id);
+std::string unknown_label(const uint8_t* id, uint64_t off);
+
+// device helpers implemented in stg_window.cu
+void launch_build_buckets(const uint64_t* starts, uint32_t n, uint64_t base, uint32_t shift,
+                          uint32_t nb, uint32_t* bucket, cudaStream_t s);
+
+}  // namespace stg

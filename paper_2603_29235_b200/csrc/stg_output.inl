@@ -1,0 +1,315 @@
+// stg_output.inl — resolve verb and result renderings (included by stg_window.cu).
+namespace stg {
+
+static const char* kVerdictNames[] = {"healthy",        "gpu-uniform-slowdown", "gpu-specific-kernel",
+                                      "cpu-interference", "os-interference",   "temporal-degradation",
+                                      "inconclusive"};
+
+// resolve_stacks (symrepo.cpp:122-143) as one batched GPU lookup.
+void run_resolve(Ctx& c, Result& res, uint64_t n, const uint64_t* pc, const uint16_t* bin, int32_t n_bins,
+                 const uint8_t* ids, int mode, uint32_t* out) {
+    stg_window w{};
+    w.n_bins = n_bins;
+    w.bin_build_ids = ids;
+    stg_config cfg{};
+    stg_config_default(&cfg);
+    cfg.lookup_mode = mode;
+    Runner rn(c, w, cfg, res);
+    symtab_refresh_dictionary(c);
+    std::vector<DevTable> tabs(std::max<int32_t>(n_bins, 1));
+    for (int32_t b = 0; b < n_bins; ++b) {
+        DevTable& t = tabs[size_t(b)];
+        std::memset(&t, 0, sizeof t);
+        auto it = c.table_by_id.find(std::string(reinterpret_cast<const char*>(ids + 20 * b), 20));
+        if (it == c.table_by_id.end()) continue;
+        HostTable& h = *c.tables[it->second];
+        if (h.starts.empty()) continue;
+        t = DevTable{h.d_starts, h.d_ent, h.d_bucket, h.starts.front(), h.starts.back(), h.shift, h.nb,
+                     uint32_t(h.starts.size()), 1};
+    }
+    DevTable* d_tabs = rn.up<DevTable>("rv_tabs", tabs.data(), tabs.size());
+    const uint64_t* d_pc = rn.up<uint64_t>("rv_pc", pc, n);
+    const uint16_t* d_bin = rn.up<uint16_t>("rv_bin", bin, n);
+    uint32_t* d_out = rn.dev<uint32_t>("rv_out", n);
+    uint32_t cap = uint32_t(std::max<uint64_t>(1024, next_pow2(2 * n + 2)));
+    UnkSlot* unk = rn.dev<UnkSlot>("rv_unk", cap);
+    rn.zero(unk, size_t(cap) * sizeof(UnkSlot));
+    unsigned* used = rn.dev<unsigned>("rv_used", 1);
+    int* ovf = rn.dev<int>("rv_ovf", 1);
+    int* ebin = rn.dev<int>("rv_ebin", 1);
+    rn.zero(used, 4);
+    rn.zero(ovf, 4);
+    rn.zero(ebin, 4);
+    cudaStream_t st = c.stream;
+    uint32_t& launches = rn.launches;
+    if (n) LAUNCH(k_resolve, grid_for(n), kThreads, n, d_pc, d_bin, d_tabs, uint32_t(n_bins), mode,
+                  UnkSet{unk, cap - 1, cap, used, ovf}, ebin, d_out);
+    if (rn.get1(ebin)) fail(STG_EINVAL, "frame binary index out of range");
+    if (rn.get1(ovf)) fail(STG_ENOMEM, "unknown-frame set overflow");
+    uint32_t* u_slot = rn.dev<uint32_t>("rv_uslot", cap);
+    uint32_t* u_bin = rn.dev<uint32_t>("rv_ubin", cap);
+    uint64_t* u_pc = rn.dev<uint64_t>("rv_upc", cap);
+    unsigned* nu = rn.dev<unsigned>("rv_nu", 1);
+    rn.zero(nu, 4);
+    LAUNCH(k_unk_compact, grid_for(cap), kThreads, cap, unk, u_slot, u_bin, u_pc, nu);
+    uint32_t NU = rn.get1(nu);
+    std::vector<uint32_t> hs(NU), hb(NU);
+    std::vector<uint64_t> hp(NU);
+    rn.down(hs.data(), u_slot, NU);
+    rn.down(hb.data(), u_bin, NU);
+    rn.down(hp.data(), u_pc, NU);
+    rn.merge_labels(NU, hs, hb, hp, cap);
+    if (n) {
+        LAUNCH(k_remap, grid_for(n), kThreads, n, d_out, static_cast<const uint32_t*>(c.buf("u_final").p),
+               static_cast<const uint32_t*>(c.buf("u_pos").p), uint32_t(rn.n_pos));
+        rn.down(out, d_out, n);
+    }
+    res.n_names = c.dict.size() + res.unk_labels.size();
+}
+
+static void render_report(const Result& r, JsonW& j) {
+    const Report& p = r.report;
+    j.raw("{\"verdict\": ");
+    j.str(kVerdictNames[p.verdict]);
+    j.raw(", \"flagged_ranks\": [");
+    for (size_t i = 0; i < p.flagged_ranks.size(); ++i) {
+        if (i) j.raw(", ");
+        j.num(p.flagged_ranks[i]);
+    }
+    j.raw("], \"evidence\": [");
+    for (size_t i = 0; i < p.evidence.size(); ++i) {
+        const Evidence& e = p.evidence[i];
+        if (i) j.raw(", ");
+        j.raw("{\"layer\": ");
+        j.str(e.layer);
+        j.raw(", \"item\": ");
+        j.str(e.item);
+        j.raw(", \"straggler_value\": ");
+        j.num(e.straggler_value);
+        j.raw(", \"reference_value\": ");
+        j.num(e.reference_value);
+        j.raw(", \"delta\": ");
+        j.num(e.delta);
+        j.raw("}");
+    }
+    j.raw("], \"top_path\": [");
+    for (size_t i = 0; i < p.top_path.size(); ++i) {
+        if (i) j.raw(", ");
+        j.str(p.top_path[i]);
+    }
+    j.raw("], \"notes\": [");
+    for (size_t i = 0; i < p.notes.size(); ++i) {
+        if (i) j.raw(", ");
+        j.str(p.notes[i]);
+    }
+    j.raw("], \"reference_rank\": ");
+    if (p.reference_rank)
+        j.num(*p.reference_rank);
+    else
+        j.raw("null");
+    j.raw("}");
+}
+
+std::string report_json(Ctx& c) {
+    JsonW j;
+    render_report(*c.result, j);
+    return j.s;
+}
+
+template <class T>
+static void d2h(Ctx& c, T* host, const char* name, size_t n, size_t offset = 0) {
+    if (!n) return;
+    const T* d = static_cast<const T*>(c.buf(name).p) + offset;
+    STG_CUDA(cudaMemcpyAsync(host, d, n * sizeof(T), cudaMemcpyDeviceToHost, c.stream));
+    STG_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+// Lines of CPU rank i: (sequence name keys, count), in folded order.
+void rank_lines(Ctx& c, uint32_t i, std::vector<uint64_t>& key_off, std::vector<uint32_t>& keys,
+                std::vector<uint64_t>& counts) {
+    Result& r = *c.result;
+    uint32_t row = r.cpu_rank_index.at(i);
+    uint64_t lo[2];
+    d2h(c, lo, "line_off", 2, row);
+    uint64_t n = lo[1] - lo[0];
+    std::vector<uint64_t> lk(n);
+    counts.resize(n);
+    d2h(c, lk.data(), "lkey_s", n, lo[0]);
+    d2h(c, counts.data(), "lcount_s", n, lo[0]);
+    key_off.assign(1, 0);
+    keys.clear();
+    for (uint64_t l = 0; l < n; ++l) {
+        uint32_t s = uint32_t(lk[l]);
+        uint32_t g;
+        d2h(c, &g, "dense_rep", 1, s);
+        uint64_t so[2];
+        d2h(c, so, "seq_off", 2, g);
+        size_t base = keys.size();
+        keys.resize(base + (so[1] - so[0]));
+        d2h(c, keys.data() + base, "arena", so[1] - so[0], so[0]);
+        key_off.push_back(keys.size());
+    }
+}
+
+std::string groupdata_json(Ctx& c) {
+    Result& r = *c.result;
+    JsonW j;
+    j.raw("{\"group\": ");
+    j.num(r.group);
+    j.raw(", \"cpu_profiles\": [");
+    // bulk-copy what the lines need once
+    std::vector<uint64_t> lk(r.n_lines), lc(r.n_lines), seq_off, line_off;
+    std::vector<uint32_t> dense_rep(r.n_seq), arena;
+    if (r.n_lines) {
+        d2h(c, lk.data(), "lkey_s", r.n_lines);
+        d2h(c, lc.data(), "lcount_s", r.n_lines);
+        d2h(c, dense_rep.data(), "dense_rep", r.n_seq);
+        size_t G = c.buf("seq_off").cap / sizeof(uint64_t);
+        (void)G;
+    }
+    uint64_t G = 0;
+    if (r.n_lines) {
+        // number of gids = size of gids buffer in use; recover from seq_off's last entry
+        G = r.n_gid;
+        seq_off.resize(G + 1);
+        d2h(c, seq_off.data(), "seq_off", G + 1);
+        arena.resize(seq_off[G]);
+        d2h(c, arena.data(), "arena", seq_off[G]);
+        line_off.resize(r.n_window_ranks + 1);
+        d2h(c, line_off.data(), "line_off", r.n_window_ranks + 1);
+    }
+    std::vector<std::string> names_cache;
+    for (size_t i = 0; i < r.cpu_rank_ids.size(); ++i) {
+        if (i) j.raw(", ");
+        uint32_t row = r.cpu_rank_index[i];
+        j.raw("{\"rank\": ");
+        j.num(r.cpu_rank_ids[i]);
+        j.raw(", \"total\": ");
+        j.num(r.cpu_totals[i]);
+        j.raw(", \"lines\": [");
+        for (uint64_t l = line_off[row]; l < line_off[row + 1]; ++l) {
+            if (l > line_off[row]) j.raw(", ");
+            uint32_t g = dense_rep[uint32_t(lk[l])];
+            j.raw("[[");
+            for (uint64_t k = seq_off[g]; k < seq_off[g + 1]; ++k) {
+                if (k > seq_off[g]) j.raw(", ");
+                j.str(r.name_of(arena[k]));
+            }
+            j.raw("], ");
+            j.num(lc[l]);
+            j.raw("]");
+        }
+        j.raw("]}");
+    }
+    j.raw("], \"gpu_profiles\": [");
+    bool first = true;
+    for (const auto& [rank, m] : r.gpu) {
+        if (!first) j.raw(", ");
+        first = false;
+        j.raw("{\"rank\": ");
+        j.num(rank);
+        j.raw(", \"kernels\": [");
+        bool f2 = true;
+        for (const auto& [k, v] : m) {
+            if (!f2) j.raw(", ");
+            f2 = false;
+            j.raw("[");
+            j.str(k);
+            j.raw(", ");
+            j.num(v);
+            j.raw("]");
+        }
+        j.raw("]}");
+    }
+    j.raw("], \"os_snapshots\": [");
+    first = true;
+    for (const auto& [rank, a] : r.os) {
+        if (!first) j.raw(", ");
+        first = false;
+        j.raw("{\"rank\": ");
+        j.num(rank);
+        for (int pass = 0; pass < 2; ++pass) {
+            j.raw(pass ? ", \"softirqs\": [" : ", \"interrupts\": [");
+            bool f2 = true;
+            for (const auto& [k, v] : pass ? a.softirqs : a.interrupts) {
+                if (!f2) j.raw(", ");
+                f2 = false;
+                j.raw("[");
+                j.str(k);
+                j.raw(", ");
+                j.num(v);
+                j.raw("]");
+            }
+            j.raw("]");
+        }
+        j.raw(", \"p50\": ");
+        j.num(a.p50);
+        j.raw(", \"p99\": ");
+        j.num(a.p99);
+        j.raw(", \"migrations\": ");
+        j.num(a.migrations);
+        j.raw("}");
+    }
+    j.raw("], \"lateness_per_instance\": [");
+    if (r.n_windowed) {
+        std::vector<double> lat(uint64_t(r.rank_span) * r.n_windowed);
+        d2h(c, lat.data(), "lat", lat.size());
+        for (uint64_t wi = 0; wi < r.n_windowed; ++wi) {
+            if (wi) j.raw(", ");
+            j.raw("[");
+            bool f2 = true;
+            for (int32_t rk = 0; rk < r.rank_span; ++rk) {
+                double v = lat[uint64_t(rk) * r.n_windowed + wi];
+                if (!(v == v)) continue;
+                if (!f2) j.raw(", ");
+                f2 = false;
+                j.raw("[");
+                j.num(rk);
+                j.raw(", ");
+                j.num(v);
+                j.raw("]");
+            }
+            j.raw("]");
+        }
+    }
+    j.raw("], \"iteration_times_ms\": [");
+    for (size_t i = 0; i < r.iteration_times_ms.size(); ++i) {
+        if (i) j.raw(", ");
+        j.num(r.iteration_times_ms[i]);
+    }
+    j.raw("], \"baseline\": ");
+    if (r.has_baseline) {
+        j.raw("{\"delta\": ");
+        j.num(r.baseline_delta);
+        j.raw(", \"fractions\": [");
+        bool f2 = true;
+        for (const auto& [k, v] : r.baseline) {
+            if (!f2) j.raw(", ");
+            f2 = false;
+            j.raw("[");
+            j.str(k);
+            j.raw(", ");
+            j.num(v);
+            j.raw("]");
+        }
+        j.raw("]}");
+    } else {
+        j.raw("null");
+    }
+    j.raw(", \"baseline_iteration_ms\": ");
+    if (r.has_baseline_iteration)
+        j.num(r.baseline_iteration_ms);
+    else
+        j.raw("null");
+    j.raw("}");
+    return j.s;
+}
+
+void window_run(Ctx& c, const stg_window& w, const stg_config& cfg) {
+    if (!c.result) c.result = std::make_unique<Result>();
+    Result& r = *c.result;
+    Runner rn(c, w, cfg, r);
+    rn.run();
+}
+
+}  // namespace stg

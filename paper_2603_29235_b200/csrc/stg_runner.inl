@@ -1,0 +1,1315 @@
+// stg_runner.inl — host orchestration of one window (included by stg_window.cu).
+// Stage order follows build_group_data (bundle.cpp:252-324): collectives first
+// (their errors surface first, and the clock offsets feed every other stream),
+// then GPU/OS sums, then CPU samples, then the diagnose ladder.
+namespace stg {
+
+// Minimal JSON writer (numbers with 17 significant digits: round-trip exact).
+struct JsonW {
+    std::string s;
+    void raw(const char* t) { s += t; }
+    void raw(const std::string& t) { s += t; }
+    void num(double v) {
+        if (!std::isfinite(v)) {
+            s += "null";
+            return;
+        }
+        char b[40];
+        std::snprintf(b, sizeof b, "%.17g", v);
+        s += b;
+    }
+    void num(int64_t v) { s += std::to_string(v); }
+    void num(uint64_t v) { s += std::to_string(v); }
+    void num(int v) { s += std::to_string(v); }
+    void str(const std::string& t) {
+        s += '"';
+        for (unsigned char ch : t) {
+            switch (ch) {
+                case '"': s += "\\\""; break;
+                case '\\': s += "\\\\"; break;
+                case '\n': s += "\\n"; break;
+                case '\t': s += "\\t"; break;
+                case '\r': s += "\\r"; break;
+                default:
+                    if (ch < 0x20) {
+                        char b[8];
+                        std::snprintf(b, sizeof b, "\\u%04x", ch);
+                        s += b;
+                    } else {
+                        s += char(ch);
+                    }
+            }
+        }
+        s += '"';
+    }
+};
+
+#define LAUNCH(kern, grid, block, ...)                                   \
+    do {                                                                 \
+        kern<<<(grid), (block), 0, st>>>(__VA_ARGS__);                   \
+        STG_CUDA(cudaGetLastError());                                    \
+        ++launches;                                                      \
+    } while (0)
+
+struct Runner {
+    Ctx& c;
+    const stg_window& w;
+    const stg_config& cfg;
+    Result& res;
+    cudaStream_t st;
+    uint32_t launches = 0;
+    uint64_t h2d = 0, d2h = 0;
+    int32_t span = 0;
+    // device state shared between stages
+    int64_t* d_off = nullptr;
+    uint8_t* d_has_off = nullptr;
+    double* d_lat = nullptr;
+    // samples
+    int R = 0;
+    uint64_t S = 0;  // dense sequences
+    uint64_t L = 0;  // lines
+    uint64_t F = 0;  // used names
+    uint64_t* d_lkey = nullptr;
+    unsigned long long* d_lcount = nullptr;
+    uint64_t* d_line_off = nullptr;
+    uint64_t* d_seq_off = nullptr;
+    uint32_t* d_arena = nullptr;
+    uint32_t* d_dense_rep = nullptr;
+    uint64_t* d_dn_off = nullptr;
+    uint32_t* d_dn = nullptr;
+    uint32_t* d_dense_final = nullptr;
+    unsigned long long* d_incl = nullptr;
+    uint64_t* d_totals = nullptr;
+    std::vector<uint64_t> h_n_in;
+    std::vector<uint32_t> h_dense_final;
+    cudaEvent_t ev[8];
+
+    Runner(Ctx& c_, const stg_window& w_, const stg_config& cfg_, Result& r_)
+        : c(c_), w(w_), cfg(cfg_), res(r_), st(c_.stream) {
+        for (auto& e : ev) STG_CUDA(cudaEventCreate(&e));
+    }
+    ~Runner() {
+        for (auto& e : ev) cudaEventDestroy(e);
+    }
+
+    template <class T>
+    T* dev(const char* name, size_t n) { return c.buf(name).as<T>(n); }
+    template <class T>
+    T* up(const char* name, const T* host, size_t n) {
+        T* d = dev<T>(name, n);
+        if (n) {
+            STG_CUDA(cudaMemcpyAsync(d, host, n * sizeof(T), cudaMemcpyHostToDevice, st));
+            h2d += n * sizeof(T);
+        }
+        return d;
+    }
+    template <class T, class U>
+    void down(T* host, const U* d, size_t n) {
+        static_assert(sizeof(T) == sizeof(U), "size mismatch");
+        if (!n) return;
+        STG_CUDA(cudaMemcpyAsync(host, d, n * sizeof(T), cudaMemcpyDeviceToHost, st));
+        STG_CUDA(cudaStreamSynchronize(st));
+        d2h += n * sizeof(T);
+    }
+    template <class T>
+    T get1(const T* d) {
+        T v;
+        down(&v, d, 1);
+        return v;
+    }
+    void zero(void* p, size_t bytes) {
+        if (bytes) STG_CUDA(cudaMemsetAsync(p, 0, bytes, st));
+    }
+    void* temp(size_t bytes) { return c.buf("cub_temp").get(bytes + 16); }
+
+    // ---------------------------------------------------------------- cub
+    template <class K, class V>
+    void sort_pairs(const K* kin, K* kout, const V* vin, V* vout, uint64_t n, int end_bit = sizeof(K) * 8) {
+        if (!n) return;
+        size_t tb = 0;
+        STG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, vin, vout, n, 0, end_bit, st));
+        STG_CUDA(cub::DeviceRadixSort::SortPairs(temp(tb), tb, kin, kout, vin, vout, n, 0, end_bit, st));
+        ++launches;
+    }
+    template <class K>
+    void sort_keys(const K* kin, K* kout, uint64_t n, int end_bit = sizeof(K) * 8) {
+        if (!n) return;
+        size_t tb = 0;
+        STG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, kin, kout, n, 0, end_bit, st));
+        STG_CUDA(cub::DeviceRadixSort::SortKeys(temp(tb), tb, kin, kout, n, 0, end_bit, st));
+        ++launches;
+    }
+    template <class I, class O>
+    void excl_sum(const I* in, O* out, uint64_t n) {
+        if (!n) return;
+        size_t tb = 0;
+        STG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, n, st));
+        STG_CUDA(cub::DeviceScan::ExclusiveSum(temp(tb), tb, in, out, n, st));
+        ++launches;
+    }
+    template <class I, class O>
+    void incl_sum(const I* in, O* out, uint64_t n) {
+        if (!n) return;
+        size_t tb = 0;
+        STG_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, in, out, n, st));
+        STG_CUDA(cub::DeviceScan::InclusiveSum(temp(tb), tb, in, out, n, st));
+        ++launches;
+    }
+    uint64_t select_flagged(const uint32_t* flags, uint32_t* out, uint64_t n) {
+        uint32_t* iota = dev<uint32_t>("sel_iota", n);
+        LAUNCH(k_iota, grid_for(n), kThreads, iota, n);
+        unsigned long long* nsel = dev<unsigned long long>("sel_n", 1);
+        size_t tb = 0;
+        STG_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, iota, flags, out, nsel, n, st));
+        STG_CUDA(cub::DeviceSelect::Flagged(temp(tb), tb, iota, flags, out, nsel, n, st));
+        ++launches;
+        return get1(nsel);
+    }
+
+    // ------------------------------------------------------------ ranks
+    void rank_space() {
+        int mx = -1, mn = 0;
+        for (int32_t i = 0; i < w.n_ranks; ++i) {
+            mx = std::max(mx, w.rank_ids[i]);
+            mn = std::min(mn, w.rank_ids[i]);
+            if (i && w.rank_ids[i] <= w.rank_ids[i - 1])
+                fail(STG_EINVAL, "stg_window.rank_ids must be strictly ascending");
+        }
+        for (int32_t i = 0; i < w.n_group_ranks; ++i) {
+            mx = std::max(mx, w.group_ranks[i]);
+            mn = std::min(mn, w.group_ranks[i]);
+        }
+        int* d_mm = dev<int>("mm", 2);
+        int init[2] = {mx, mn};
+        STG_CUDA(cudaMemcpyAsync(d_mm, init, sizeof init, cudaMemcpyHostToDevice, st));
+        auto scan = [&](const int32_t* host, uint64_t n, const char* nm) {
+            if (!n) return;
+            const int32_t* d = up<int32_t>(nm, host, n);
+            LAUNCH(k_max_rank, grid_for(n), kThreads, n, d, d_mm, d_mm + 1);
+        };
+        scan(w.coll_rank, w.n_coll, "coll_rank");
+        scan(w.gpu_rank, w.n_gpu, "gpu_rank");
+        scan(w.os_rank, w.n_os, "os_rank");
+        int out[2];
+        down(out, d_mm, 2);
+        if (out[1] < 0) fail(STG_EINVAL, "negative rank ids are not supported");
+        if (out[0] >= (1 << 24)) fail(STG_EINVAL, "rank ids must be below 2^24");
+        span = out[0] + 1;
+        res.rank_span = span;
+    }
+
+    // ------------------------------------------------------ collectives
+    void collectives() {
+        d_off = dev<int64_t>("off", span);
+        d_has_off = dev<uint8_t>("has_off", span);
+        zero(d_off, span * sizeof(int64_t));
+        zero(d_has_off, span);
+        res.n_instances = res.n_windowed = 0;
+        res.iteration_times_ms.clear();
+        res.offsets.assign(span, 0);
+        res.has_offset.assign(span, 0);
+        res.lat_present.assign(span, 0);
+        res.mean_lat_all.assign(span, 0);
+        res.mean_lat_alert.assign(span, 0);
+        res.z_mean.assign(span, 0);
+        res.flag_count.assign(span, 0);
+        res.has_z.assign(span, 0);
+        res.have_offsets = false;
+        const uint64_t n = w.n_coll;
+        if (n == 0) return;
+        if (n >= 0xffffffffull) fail(STG_EINVAL, "too many collective events");
+        const int32_t* d_rank = static_cast<const int32_t*>(c.buf("coll_rank").p);  // uploaded in rank_space
+        const int32_t* d_group = up<int32_t>("coll_group", w.coll_group, n);
+        const uint8_t* d_kind = up<uint8_t>("coll_kind", w.coll_kind, n);
+        const int64_t* d_entry = up<int64_t>("coll_entry", w.coll_entry, n);
+        const int64_t* d_exit = up<int64_t>("coll_exit", w.coll_exit, n);
+        uint64_t* key = dev<uint64_t>("c_key", n);
+        uint64_t* key_s = dev<uint64_t>("c_key_s", n);
+        uint32_t* idx = dev<uint32_t>("c_idx", n);
+        uint32_t* idx_s = dev<uint32_t>("c_idx_s", n);
+        int* d_err = dev<int>("c_err", 1);
+        zero(d_err, sizeof(int));
+        LAUNCH(k_coll_keys, grid_for(n), kThreads, n, d_rank, d_group, d_kind, key, idx, d_err);
+        sort_pairs(key, key_s, idx, idx_s, n);
+        int64_t* s_entry = dev<int64_t>("c_sentry", n);
+        int64_t* s_exit = dev<int64_t>("c_sexit", n);
+        unsigned long long* errs = dev<unsigned long long>("c_errs", 2);
+        STG_CUDA(cudaMemsetAsync(errs, 0xff, 2 * sizeof(unsigned long long), st));
+        uint32_t* seg_flag = dev<uint32_t>("c_segflag", n);
+        uint32_t* stream_flag = dev<uint32_t>("c_stflag", n);
+        LAUNCH(k_coll_gather, grid_for(n), kThreads, n, key_s, idx_s, d_entry, d_exit, s_entry, s_exit, errs,
+               errs + 1, seg_flag, stream_flag);
+        unsigned long long he[2];
+        down(he, errs, 2);
+        if (he[0] != ~0ull || he[1] != ~0ull) {
+            if (he[0] <= he[1]) fail(STG_EINVAL, "collective event with entry >= exit");
+            fail(STG_EINVAL, "collective events not time-ordered within rank");
+        }
+        // segments (stream, rank) and streams (group, kind)
+        uint32_t* seg_pos = dev<uint32_t>("c_segpos", n + 1);
+        uint64_t n_seg = select_flagged(seg_flag, seg_pos, n);
+        uint32_t* st_pos = dev<uint32_t>("c_stpos", n + 1);
+        uint64_t n_st = select_flagged(stream_flag, st_pos, n);
+        std::vector<uint32_t> h_seg(n_seg + 1), h_st(n_st);
+        down(h_seg.data(), seg_pos, n_seg);
+        down(h_st.data(), st_pos, n_st);
+        h_seg[n_seg] = uint32_t(n);
+        std::vector<uint32_t> st_seg(n_st + 1), seg_stream(n_seg);
+        for (uint64_t s = 0, j = 0; s < n_st; ++s) {
+            while (h_seg[j] != h_st[s]) ++j;
+            st_seg[s] = uint32_t(j);
+        }
+        st_seg[n_st] = uint32_t(n_seg);
+        for (uint64_t s = 0; s < n_st; ++s)
+            for (uint32_t j = st_seg[s]; j < st_seg[s + 1]; ++j) seg_stream[j] = uint32_t(s);
+        seg_pos = up<uint32_t>("c_segpos2", h_seg.data(), n_seg + 1);
+        uint32_t* d_st_seg = up<uint32_t>("c_stseg", st_seg.data(), n_st + 1);
+        uint32_t* d_seg_stream = up<uint32_t>("c_segstream", seg_stream.data(), n_seg);
+        uint32_t* stream_of_pos = dev<uint32_t>("c_streamofpos", n);
+        incl_sum(stream_flag, stream_of_pos, n);  // 1-based
+        // coarse offsets + counts
+        int64_t* coarse = dev<int64_t>("c_coarse", n_seg);
+        uint32_t* kmin = dev<uint32_t>("c_kmin", n_st);
+        uint32_t* kmax = dev<uint32_t>("c_kmax", n_st);
+        LAUNCH(k_coll_streams, unsigned(n_st), kThreads, int(n_st), d_st_seg, seg_pos, s_entry, coarse, kmin, kmax);
+        std::vector<uint32_t> h_kmin(n_st), h_kmax(n_st);
+        down(h_kmin.data(), kmin, n_st);
+        down(h_kmax.data(), kmax, n_st);
+        std::vector<uint64_t> k_base(n_st + 1, 0);
+        for (uint64_t s = 0; s < n_st; ++s) k_base[s + 1] = k_base[s] + h_kmin[s];
+        uint64_t* d_kbase = up<uint64_t>("c_kbase", k_base.data(), n_st + 1);
+        uint32_t* first_fail = up<uint32_t>("c_ffail", h_kmin.data(), n_st);
+        if (k_base[n_st])
+            LAUNCH(k_coll_regular, grid_for(k_base[n_st]), kThreads, int(n_st), d_st_seg, seg_pos, coarse, s_entry,
+                   s_exit, kmin, d_kbase, k_base[n_st], w.max_skew_ns, first_fail);
+        std::vector<uint32_t> k0(n_st);
+        down(k0.data(), first_fail, n_st);
+        uint32_t* inst_local = dev<uint32_t>("c_instlocal", n);
+        uint32_t* d_k0 = up<uint32_t>("c_k0", k0.data(), n_st);
+        LAUNCH(k_coll_assign_regular, unsigned(std::min<uint64_t>(n_seg, 65535)), 128, int(n_st), d_st_seg, seg_pos,
+               d_seg_stream, uint32_t(n_seg), d_k0, inst_local);
+        std::vector<int> irregular;
+        std::vector<uint32_t> n_inst(n_st);
+        for (uint64_t s = 0; s < n_st; ++s) {
+            if (k0[s] < h_kmax[s])
+                irregular.push_back(int(s));
+            else
+                n_inst[s] = k0[s];
+        }
+        if (!irregular.empty()) {
+            int* d_irr = up<int>("c_irr", irregular.data(), irregular.size());
+            uint32_t* head = dev<uint32_t>("c_head", n_seg);
+            uint32_t* d_ninst = dev<uint32_t>("c_ninst", n_st);
+            LAUNCH(k_coll_sequential, unsigned(irregular.size()), 1024, d_irr, d_st_seg, seg_pos, coarse, s_entry,
+                   s_exit, d_k0, w.max_skew_ns, head, inst_local, d_ninst);
+            std::vector<uint32_t> tmp(n_st);
+            down(tmp.data(), d_ninst, n_st);
+            for (int s : irregular) n_inst[size_t(s)] = tmp[size_t(s)];
+        }
+        // stream_of_pos is 1-based (inclusive scan): shift the base table
+        std::vector<uint64_t> inst_base(n_st + 1, 0);
+        for (uint64_t s = 0; s < n_st; ++s) inst_base[s + 1] = inst_base[s] + n_inst[s];
+        std::vector<uint64_t> base1(n_st + 1, 0);
+        for (uint64_t s = 0; s < n_st; ++s) base1[s + 1] = inst_base[s];
+        uint64_t I = inst_base[n_st];
+        res.n_instances = I;
+        uint64_t* d_ibase = up<uint64_t>("c_ibase", base1.data(), n_st + 1);
+        // group membership
+        std::vector<uint8_t> member(span, 0);
+        unsigned n_group = 0;
+        for (int32_t i = 0; i < w.n_group_ranks; ++i)
+            if (!member[size_t(w.group_ranks[i])]) {
+                member[size_t(w.group_ranks[i])] = 1;
+                ++n_group;
+            }
+        uint8_t* d_member = up<uint8_t>("c_member", member.data(), span);
+        uint32_t* inst_of = dev<uint32_t>("c_instof", n);
+        unsigned long long* imax = dev<unsigned long long>("c_imax", I);
+        unsigned* isize = dev<unsigned>("c_isize", I);
+        unsigned* iing = dev<unsigned>("c_iing", I);
+        LAUNCH(k_fill_i64, grid_for(I), kThreads, (long long*)imax, I, LLONG_MIN);
+        zero(isize, I * sizeof(unsigned));
+        zero(iing, I * sizeof(unsigned));
+        LAUNCH(k_coll_inst, grid_for(n), kThreads, n, key_s, nullptr, stream_of_pos, d_ibase, inst_local, s_exit,
+               d_member, inst_of, imax, isize, iing);
+        // align_clocks
+        uint64_t* dkey = dev<uint64_t>("c_dkey", n);
+        uint64_t* dkey_s = dev<uint64_t>("c_dkey_s", n);
+        unsigned long long* nd = dev<unsigned long long>("c_nd", 1);
+        int* rerr = dev<int>("c_rerr", 1);
+        zero(nd, 8);
+        zero(rerr, 4);
+        LAUNCH(k_coll_deltas, grid_for(n), kThreads, n, key_s, inst_of, s_exit, imax, iing, n_group, dkey, nd, rerr);
+        uint64_t n_d = get1(nd);
+        if (get1(rerr)) fail(STG_EINVAL, "barrier-exit spread beyond 2^39 ns is not supported");
+        sort_keys(dkey, dkey_s, n_d);
+        LAUNCH(k_coll_median, grid_for(span), kThreads, span, dkey_s, n_d, d_off, d_has_off);
+        res.have_offsets = n_d > 0;
+        // windowed complete instances ordered by max aligned exit
+        unsigned long long* aexit = dev<unsigned long long>("c_aexit", I);
+        zero(aexit, I * 8);  // int64 0: build_group_data initialises max_exit to 0
+        LAUNCH(k_coll_aligned_exit, grid_for(n), kThreads, n, key_s, inst_of, s_exit, iing, n_group, d_off, aexit);
+        uint64_t* wkey = dev<uint64_t>("c_wkey", I);
+        uint64_t* wkey_s = dev<uint64_t>("c_wkey_s", I);
+        uint32_t* winst = dev<uint32_t>("c_winst", I);
+        uint32_t* winst_s = dev<uint32_t>("c_winst_s", I);
+        unsigned long long* nw = dev<unsigned long long>("c_nw", 1);
+        zero(nw, 8);
+        LAUNCH(k_coll_window_select, grid_for(I), kThreads, I, iing, n_group, aexit, w.window_start_ns, wkey, winst,
+               nw);
+        uint64_t n_w = get1(nw);
+        res.n_windowed = n_w;
+        sort_pairs(wkey, wkey_s, winst, winst_s, n_w);
+        uint32_t* inst_w = dev<uint32_t>("c_instw", I);
+        STG_CUDA(cudaMemsetAsync(inst_w, 0xff, I * sizeof(uint32_t), st));
+        LAUNCH(k_coll_winv, grid_for(n_w), kThreads, n_w, winst_s, inst_w);
+        long long* wmin = dev<long long>("c_wmin", n_w);
+        LAUNCH(k_fill_i64, grid_for(n_w), kThreads, wmin, n_w, LLONG_MAX);
+        LAUNCH(k_coll_minadj, grid_for(n), kThreads, n, key_s, inst_of, inst_w, s_entry, d_off, wmin);
+        d_lat = dev<double>("lat", uint64_t(span) * n_w);
+        LAUNCH(k_fill_f64, grid_for(uint64_t(span) * n_w), kThreads, d_lat, uint64_t(span) * n_w, nan(""));
+        LAUNCH(k_coll_lateness, grid_for(n), kThreads, n, key_s, inst_of, inst_w, s_entry, d_off, wmin, n_w, d_lat);
+        if (n_w > 1) {
+            double* it = dev<double>("c_it", n_w);
+            LAUNCH(k_coll_itertimes, grid_for(n_w), kThreads, n_w, wkey_s, it);
+            res.iteration_times_ms.resize(n_w - 1);
+            down(res.iteration_times_ms.data(), it, n_w - 1);
+        }
+        // detect_straggler statistics
+        if (n_w) {
+            double* mu = dev<double>("s_mu", n_w);
+            double* sg = dev<double>("s_sg", n_w);
+            uint32_t* m = dev<uint32_t>("s_m", n_w);
+            LAUNCH(k_straggler_inst, grid_for(n_w, 128), 128, n_w, span, d_lat, cfg.k, mu, sg, m);
+            uint8_t* pres = dev<uint8_t>("s_pres", span);
+            double* ma = dev<double>("s_ma", span);
+            double* ml = dev<double>("s_ml", span);
+            double* zm = dev<double>("s_zm", span);
+            uint64_t* fl = dev<uint64_t>("s_fl", span);
+            uint8_t* hz = dev<uint8_t>("s_hz", span);
+            LAUNCH(k_straggler_rank, grid_for(span, 64), 64, n_w, span, d_lat, cfg.k, mu, sg, m, pres, ma, ml, zm, fl,
+                   hz);
+            down(res.lat_present.data(), pres, span);
+            down(res.mean_lat_all.data(), ma, span);
+            down(res.mean_lat_alert.data(), ml, span);
+            down(res.z_mean.data(), zm, span);
+            down(res.flag_count.data(), fl, span);
+            down(res.has_z.data(), hz, span);
+        }
+        down(res.offsets.data(), d_off, span);
+        down(res.has_offset.data(), d_has_off, span);
+    }
+
+    // ------------------------------------------------------------ gpu/os
+    void gpu_os() {
+        res.gpu.clear();
+        res.os.clear();
+        if (w.n_gpu) {
+            const uint64_t n = w.n_gpu, K = w.n_kernel_names;
+            const int32_t* d_rank = static_cast<const int32_t*>(c.buf("gpu_rank").p);
+            const uint32_t* d_k = up<uint32_t>("gpu_k", w.gpu_kernel, n);
+            const int64_t* d_s = up<int64_t>("gpu_s", w.gpu_start, n);
+            const int64_t* d_d = up<int64_t>("gpu_d", w.gpu_dur, n);
+            unsigned long long* sums = dev<unsigned long long>("gpu_sums", span * K);
+            uint8_t* pres = dev<uint8_t>("gpu_pres", span * K);
+            int* err = dev<int>("gpu_err", 1);
+            zero(sums, span * K * 8);
+            zero(pres, span * K);
+            zero(err, 4);
+            LAUNCH(k_gpu_sums, grid_for(n), kThreads, n, d_rank, d_k, d_s, d_d, d_off, w.window_start_ns, uint32_t(K),
+                   sums, pres, err);
+            if (get1(err)) fail(STG_EINVAL, "gpu event kernel index out of range");
+            std::vector<unsigned long long> hs(span * K);
+            std::vector<uint8_t> hp(span * K);
+            down(hs.data(), sums, span * K);
+            down(hp.data(), pres, span * K);
+            for (int32_t r = 0; r < span; ++r)
+                for (uint64_t k = 0; k < K; ++k)
+                    if (hp[r * K + k]) res.gpu[r][w.kernel_names[k]] += int64_t(hs[r * K + k]);
+        }
+        if (w.n_os) {
+            const uint64_t n = w.n_os, C = std::max<uint32_t>(w.n_counter_names, 1);
+            const int32_t* d_rank = static_cast<const int32_t*>(c.buf("os_rank").p);
+            auto ws = up<int64_t>("os_ws", w.os_window_start, n);
+            auto p50 = up<int64_t>("os_p50", w.os_p50, n);
+            auto p99 = up<int64_t>("os_p99", w.os_p99, n);
+            auto mig = up<int64_t>("os_mig", w.os_migrations, n);
+            auto ioff = up<uint64_t>("os_ioff", w.os_irq_off, n + 1);
+            uint64_t ni = w.os_irq_off[n], ns = w.os_sirq_off[n];
+            auto ikey = up<uint32_t>("os_ikey", w.os_irq_key, ni);
+            auto ival = up<int64_t>("os_ival", w.os_irq_val, ni);
+            auto soff = up<uint64_t>("os_soff", w.os_sirq_off, n + 1);
+            auto skey = up<uint32_t>("os_skey", w.os_sirq_key, ns);
+            auto sval = up<int64_t>("os_sval", w.os_sirq_val, ns);
+            auto irq = dev<unsigned long long>("os_irq", span * C);
+            auto irqp = dev<uint8_t>("os_irqp", span * C);
+            auto sirq = dev<unsigned long long>("os_sirq", span * C);
+            auto sirqp = dev<uint8_t>("os_sirqp", span * C);
+            auto mp50 = dev<long long>("os_mp50", span);
+            auto mp99 = dev<long long>("os_mp99", span);
+            auto migs = dev<unsigned long long>("os_migs", span);
+            auto pres = dev<uint8_t>("os_pres", span);
+            int* err = dev<int>("os_err", 1);
+            zero(irq, span * C * 8);
+            zero(irqp, span * C);
+            zero(sirq, span * C * 8);
+            zero(sirqp, span * C);
+            zero(mp50, span * 8);
+            zero(mp99, span * 8);
+            zero(migs, span * 8);
+            zero(pres, span);
+            zero(err, 4);
+            LAUNCH(k_os_sums, grid_for(n), kThreads, n, d_rank, ws, p50, p99, mig, ioff, ikey, ival, soff, skey, sval,
+                   d_off, w.window_start_ns, uint32_t(w.n_counter_names), irq, irqp, sirq, sirqp, mp50, mp99, migs,
+                   pres, err);
+            if (get1(err)) fail(STG_EINVAL, "os counter key index out of range");
+            std::vector<unsigned long long> hi(span * C), hs(span * C), hm(span);
+            std::vector<uint8_t> hip(span * C), hsp(span * C), hp(span);
+            std::vector<long long> h50(span), h99(span);
+            down(hi.data(), irq, span * C);
+            down(hs.data(), sirq, span * C);
+            down(hip.data(), irqp, span * C);
+            down(hsp.data(), sirqp, span * C);
+            down(hp.data(), pres, span);
+            down(h50.data(), mp50, span);
+            down(h99.data(), mp99, span);
+            down(hm.data(), migs, span);
+            for (int32_t r = 0; r < span; ++r) {
+                if (!hp[r]) continue;
+                OsAcc& a = res.os[r];
+                for (uint32_t k = 0; k < w.n_counter_names; ++k) {
+                    if (hip[r * C + k]) a.interrupts[w.counter_names[k]] += int64_t(hi[r * C + k]);
+                    if (hsp[r * C + k]) a.softirqs[w.counter_names[k]] += int64_t(hs[r * C + k]);
+                }
+                a.p50 = h50[r];
+                a.p99 = h99[r];
+                a.migrations = int64_t(hm[r]);
+            }
+        }
+    }
+
+    // ---------------------------------------------------------- samples
+    void samples() {
+        R = w.n_ranks;
+        res.n_window_ranks = uint32_t(R);
+        res.n_gid = 0;
+        res.cpu_rank_ids.clear();
+        res.cpu_rank_index.clear();
+        res.cpu_totals.clear();
+        L = S = F = 0;
+        res.n_lines = res.n_seq = res.n_unknown = res.f_used = 0;
+        res.unk_final.clear();
+        res.unk_labels.clear();
+        if (R == 0) return;
+        const uint64_t n_s = w.n_samples, n_f = w.n_frames;
+        if (w.rank_sample_off[0] != 0 || w.rank_sample_off[R] != n_s)
+            fail(STG_EINVAL, "stg_window.rank_sample_off does not cover the samples");
+        symtab_refresh_dictionary(c);
+        // bulk arrays
+        const int64_t *ts;
+        const uint64_t *foff, *pc;
+        const uint16_t* bin;
+        if (w.memory == STG_MEM_DEVICE) {
+            ts = w.sample_ts;
+            foff = w.sample_frame_off;
+            pc = w.frame_pc;
+            bin = w.frame_bin;
+        } else {
+            ts = up<int64_t>("in_ts", w.sample_ts, n_s);
+            foff = up<uint64_t>("in_foff", w.sample_frame_off, n_s + 1);
+            pc = up<uint64_t>("in_pc", w.frame_pc, n_f);
+            bin = up<uint16_t>("in_bin", w.frame_bin, n_f);
+        }
+        // tables for the window's binaries (missing build id -> every frame unknown)
+        std::vector<DevTable> tabs(std::max<int32_t>(w.n_bins, 1));
+        for (int32_t b = 0; b < w.n_bins; ++b) {
+            DevTable& t = tabs[size_t(b)];
+            std::memset(&t, 0, sizeof t);
+            auto it = c.table_by_id.find(std::string(reinterpret_cast<const char*>(w.bin_build_ids + 20 * b), 20));
+            if (it == c.table_by_id.end()) continue;
+            HostTable& h = *c.tables[it->second];
+            if (h.starts.empty()) continue;
+            t.starts = h.d_starts;
+            t.ent = h.d_ent;
+            t.bucket = h.d_bucket;
+            t.base = h.starts.front();
+            t.last_start = h.starts.back();
+            t.shift = h.shift;
+            t.nb = h.nb;
+            t.n = uint32_t(h.starts.size());
+            t.valid = 1;
+        }
+        DevTable* d_tabs = up<DevTable>("tabs", tabs.data(), tabs.size());
+        uint64_t* d_rsoff = up<uint64_t>("rsoff", w.rank_sample_off, R + 1);
+        int32_t* d_rids = up<int32_t>("rids", w.rank_ids, R);
+        int64_t* d_clk = dev<int64_t>("clk", R);
+        LAUNCH(k_clk_of_cpu, grid_for(R), kThreads, R, d_rids, d_off, d_clk);
+        std::vector<uint8_t> active(R, 1);
+        uint8_t* d_active = up<uint8_t>("active", active.data(), R);
+        // per-rank table capacities (remembered across windows)
+        std::vector<uint32_t> caps(R);
+        for (int r = 0; r < R; ++r) {
+            uint64_t nr = w.rank_sample_off[r + 1] - w.rank_sample_off[r];
+            uint64_t want = c_cap_hint(r, nr);
+            caps[r] = uint32_t(std::max<uint64_t>(64, next_pow2(want)));
+        }
+        uint32_t unk_cap = uint32_t(std::max<uint64_t>(4096, next_pow2(c_unk_hint())));
+        int G = 32;
+        double avg = n_s ? double(n_f) / double(n_s) : 1;
+        if (avg <= 4) G = 4;
+        else if (avg <= 8) G = 8;
+        else if (avg <= 16) G = 16;
+        int dev_sms = 148;
+        STG_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c.device));
+        unsigned long long* d_nin = dev<unsigned long long>("nin", R);
+        int* d_uns = dev<int>("uns", R);
+        unsigned long long* d_eempty = dev<unsigned long long>("eempty", R);
+        int* d_ebin = dev<int>("ebin", 1);
+        unsigned* d_used = dev<unsigned>("tused", R);
+        int* d_ovf = dev<int>("tovf", R);
+        unsigned* d_unk_used = dev<unsigned>("unk_used", 1);
+        int* d_unk_ovf = dev<int>("unk_ovf", 1);
+        std::vector<uint64_t> tab_off(R);
+        AggSlot* slots = nullptr;
+        UnkSlot* unk = nullptr;
+        std::vector<int> ovf(R);
+        std::vector<unsigned> used(R);
+        cudaEventRecord(ev[2], st);
+        for (int attempt = 0;; ++attempt) {
+            uint64_t tot = 0;
+            for (int r = 0; r < R; ++r) {
+                tab_off[r] = tot;
+                tot += caps[r];
+            }
+            slots = dev<AggSlot>("slots", tot);
+            zero(slots, tot * sizeof(AggSlot));
+            uint64_t* d_toff = up<uint64_t>("toff", tab_off.data(), R);
+            std::vector<uint32_t> masks(R);
+            for (int r = 0; r < R; ++r) masks[r] = caps[r] - 1;
+            uint32_t* d_mask = up<uint32_t>("tmask", masks.data(), R);
+            unk = dev<UnkSlot>("unk", unk_cap);
+            zero(unk, size_t(unk_cap) * sizeof(UnkSlot));
+            zero(d_nin, R * 8);
+            zero(d_uns, R * 4);
+            STG_CUDA(cudaMemsetAsync(d_eempty, 0xff, R * 8, st));
+            zero(d_ebin, 4);
+            zero(d_used, R * 4);
+            zero(d_ovf, R * 4);
+            zero(d_unk_used, 4);
+            zero(d_unk_ovf, 4);
+            AggParams p{};
+            p.ts = ts;
+            p.foff = foff;
+            p.pc = pc;
+            p.bin = bin;
+            p.rank_soff = d_rsoff;
+            p.rank_clk = d_clk;
+            p.active = d_active;
+            p.R = R;
+            p.ws = w.window_start_ns;
+            p.tabs = d_tabs;
+            p.n_bins = uint32_t(w.n_bins);
+            p.mode = cfg.lookup_mode;
+            p.slots = slots;
+            p.tab_off = d_toff;
+            p.tab_mask = d_mask;
+            p.tab_used = d_used;
+            p.tab_overflow = d_ovf;
+            p.unk = UnkSet{unk, unk_cap - 1, unk_cap / 2, d_unk_used, d_unk_ovf};
+            p.n_in = d_nin;
+            p.unsorted = d_uns;
+            p.err_empty = d_eempty;
+            p.err_bin = d_ebin;
+            p.n_samples = n_s;
+            p.chunk = 32;
+            unsigned grid = unsigned(dev_sms) * 8;
+            uint64_t chunks = (n_s + p.chunk - 1) / p.chunk;
+            uint64_t need = (chunks + (kThreads / 32) - 1) / (kThreads / 32);
+            if (need < grid) grid = unsigned(std::max<uint64_t>(need, 1));
+            switch (G) {
+                case 4: LAUNCH(k_sym_agg<4>, grid, kThreads, p); break;
+                case 8: LAUNCH(k_sym_agg<8>, grid, kThreads, p); break;
+                case 16: LAUNCH(k_sym_agg<16>, grid, kThreads, p); break;
+                default: LAUNCH(k_sym_agg<32>, grid, kThreads, p); break;
+            }
+            down(ovf.data(), d_ovf, R);
+            down(used.data(), d_used, R);
+            bool any = false;
+            for (int r = 0; r < R; ++r)
+                if (ovf[r]) {
+                    caps[r] = caps[r] >= (1u << 30) ? caps[r] : caps[r] * 4;
+                    any = true;
+                }
+            bool unk_over = get1(d_unk_ovf) != 0;
+            if (unk_over) unk_cap = unk_cap >= (1u << 30) ? unk_cap : unk_cap * 4;
+            if (!any && !unk_over) break;
+            if (attempt > 6) fail(STG_ENOMEM, "aggregation tables kept overflowing");
+        }
+        cudaEventRecord(ev[3], st);
+        c_set_hints(used, get1(d_unk_used));
+        if (get1(d_ebin)) fail(STG_EINVAL, "frame binary index out of range");
+        h_n_in.resize(R);
+        down(h_n_in.data(), d_nin, R);
+        // validation in aggregate_samples order (samples.cpp:32-58), ranks ascending
+        std::vector<unsigned long long> eempty(R), ereg(R, ~0ull);
+        down(eempty.data(), d_eempty, R);
+        std::vector<int> uns(R);
+        down(uns.data(), d_uns, R);
+        std::vector<int> flagged;
+        for (int r = 0; r < R; ++r)
+            if (uns[r] && h_n_in[r]) flagged.push_back(r);
+        if (!flagged.empty()) {
+            int* d_fl = up<int>("regr_r", flagged.data(), flagged.size());
+            unsigned long long* d_o = dev<unsigned long long>("regr_o", flagged.size());
+            LAUNCH(k_regress_exact, grid_for(flagged.size(), 64), 64, int(flagged.size()), d_fl, d_rsoff, ts, d_clk,
+                   w.window_start_ns, d_o);
+            std::vector<unsigned long long> o(flagged.size());
+            down(o.data(), d_o, flagged.size());
+            for (size_t i = 0; i < flagged.size(); ++i) ereg[size_t(flagged[i])] = o[i];
+        }
+        int64_t drain = w.window_end_ns - w.window_start_ns + 2 * w.max_skew_ns;
+        for (int r = 0; r < R; ++r) {
+            if (!h_n_in[r]) continue;
+            if (drain <= 0) fail(STG_EINVAL, "drain interval must be positive");
+            if (eempty[r] != ~0ull || ereg[r] != ~0ull) {
+                if (eempty[r] <= ereg[r]) fail(STG_EINVAL, "empty sample stack");
+                fail(STG_EINVAL, "aggregate_samples: timestamps regressed");
+            }
+        }
+        for (int r = 0; r < R; ++r)
+            if (h_n_in[r]) {
+                res.cpu_rank_ids.push_back(w.rank_ids[r]);
+                res.cpu_rank_index.push_back(uint32_t(r));
+                res.cpu_totals.push_back(h_n_in[r]);
+            }
+        d_totals = up<uint64_t>("totals", h_n_in.data(), R);
+        fold(slots, tab_off, caps, unk, unk_cap, d_rsoff, foff, pc, bin, d_tabs);
+    }
+
+    // table-capacity hints kept on the context between windows
+    uint64_t c_cap_hint(int r, uint64_t nr) {
+        auto& v = c_hints();
+        uint64_t base = std::min<uint64_t>(2 * nr + 2, 1u << 15);
+        if (size_t(r) < v.size() && v[size_t(r)]) base = std::min<uint64_t>(2 * nr + 2, uint64_t(v[size_t(r)]) * 2 + 64);
+        return base;
+    }
+    uint64_t c_unk_hint() {
+        auto& v = c_hints();
+        return v.empty() ? 4096 : uint64_t(c_unk_last()) * 2 + 1024;
+    }
+    std::vector<uint32_t>& c_hints() {
+        static std::map<Ctx*, std::vector<uint32_t>> m;
+        return m[&c];
+    }
+    uint32_t& c_unk_last() {
+        static std::map<Ctx*, uint32_t> m;
+        return m[&c];
+    }
+    void c_set_hints(const std::vector<unsigned>& used, unsigned unk_used) {
+        auto& v = c_hints();
+        v.assign(used.begin(), used.end());
+        c_unk_last() = unk_used;
+    }
+
+    // Unknown labels (symfile.cpp:159-163) merged into the sorted name space.
+    // Real name i moves to i + #{non-name labels < name i}; a label that equals a
+    // real name shares its rank, so folding merges them exactly like strings.
+    uint64_t n_pos = 0;
+    void merge_labels(uint32_t NU, const std::vector<uint32_t>& hs, const std::vector<uint32_t>& hb,
+                      const std::vector<uint64_t>& hp, uint32_t unk_cap) {
+        const auto& dict = c.dict;
+        res.dict = &c.dict;
+        res.unk_final.clear();
+        res.unk_labels.clear();
+        std::vector<std::pair<std::string, uint32_t>> labels(NU);
+        for (uint32_t i = 0; i < NU; ++i) labels[i] = {unknown_label(w.bin_build_ids + 20 * hb[i], hp[i]), hs[i]};
+        std::sort(labels.begin(), labels.end());
+        std::vector<uint32_t> unk_final_by_slot(unk_cap, 0), pos_sorted;
+        uint64_t ne_before = 0;
+        uint64_t last_final = 0;
+        for (uint32_t i = 0; i < NU; ++i) {
+            const std::string& lab = labels[i].first;
+            if (i > 0 && lab == labels[i - 1].first) {  // same label from two slots
+                unk_final_by_slot[labels[i].second] = uint32_t(last_final);
+                continue;
+            }
+            uint64_t pos = uint64_t(std::lower_bound(dict.begin(), dict.end(), lab) - dict.begin());
+            bool eq = pos < dict.size() && dict[pos] == lab;
+            uint64_t fr = pos + ne_before;
+            unk_final_by_slot[labels[i].second] = uint32_t(fr);
+            last_final = fr;
+            if (!eq) {
+                pos_sorted.push_back(uint32_t(pos));
+                res.unk_final.push_back(fr);
+                res.unk_labels.push_back(lab);
+                ++ne_before;
+            }
+        }
+        up<uint32_t>("u_final", unk_final_by_slot.data(), unk_cap);
+        n_pos = pos_sorted.size();
+        uint32_t zero32 = 0;
+        up<uint32_t>("u_pos", n_pos ? pos_sorted.data() : &zero32, std::max<uint64_t>(n_pos, 1));
+    }
+
+    // -------------------------------------------------------------- fold
+    void fold(AggSlot* slots, const std::vector<uint64_t>& tab_off, const std::vector<uint32_t>& caps, UnkSlot* unk,
+              uint32_t unk_cap, const uint64_t* d_rsoff, const uint64_t* foff, const uint64_t* pc,
+              const uint16_t* bin, const DevTable* d_tabs) {
+        cudaEventRecord(ev[4], st);
+        uint64_t tot = 0;
+        uint32_t maxcap = 0;
+        for (int r = 0; r < R; ++r) {
+            tot += caps[r];
+            maxcap = std::max(maxcap, caps[r]);
+        }
+        uint64_t* d_toff = static_cast<uint64_t*>(c.buf("toff").p);
+        uint32_t* d_mask = static_cast<uint32_t*>(c.buf("tmask").p);
+        uint64_t Lmax = 0;
+        for (int r = 0; r < R; ++r) Lmax += std::min<uint64_t>(caps[r], w.rank_sample_off[r + 1] - w.rank_sample_off[r]);
+        Lmax = std::max<uint64_t>(Lmax, 1);
+        uint32_t* l_rank = dev<uint32_t>("l_rank", Lmax);
+        uint64_t* l_hi = dev<uint64_t>("l_hi", Lmax);
+        uint64_t* l_lo = dev<uint64_t>("l_lo", Lmax);
+        uint32_t* l_cnt32 = dev<uint32_t>("l_cnt32", Lmax);
+        uint64_t* l_rep = dev<uint64_t>("l_rep", Lmax);
+        unsigned long long* nl = dev<unsigned long long>("nl", 1);
+        zero(nl, 8);
+        dim3 g(std::max(1u, std::min(64u, (maxcap + kThreads - 1) / kThreads)), unsigned(R));
+        k_compact_lines<<<g, kThreads, 0, st>>>(R, d_toff, d_mask, slots, d_rsoff, l_rank, l_hi, l_lo, l_cnt32,
+                                                 l_rep, nl);
+        STG_CUDA(cudaGetLastError());
+        ++launches;
+        L = get1(nl);
+        res.n_lines = L;
+        if (L == 0) return;
+        // global dedupe -> sequence ids
+        uint64_t scap = next_pow2(2 * L);
+        SeqSlot* sslots = dev<SeqSlot>("sslots", scap);
+        zero(sslots, scap * sizeof(SeqSlot));
+        STG_CUDA(cudaMemsetAsync(sslots, 0, scap * sizeof(SeqSlot), st));
+        // gid field must start at 0xffffffff
+        {
+            std::vector<SeqSlot> tmp;  // set gid via a memset pattern pass
+        }
+        LAUNCH(k_fill_gid, grid_for(scap), kThreads, sslots, scap);
+        unsigned* nseq = dev<unsigned>("nseq", 1);
+        int* sovf = dev<int>("sovf", 1);
+        zero(nseq, 4);
+        zero(sovf, 4);
+        uint32_t* l_gid = dev<uint32_t>("l_gid", L);
+        uint64_t* seq_rep = dev<uint64_t>("seq_rep", L);
+        LAUNCH(k_seq_dedupe, grid_for(L), kThreads, L, l_hi, l_lo, l_rep, sslots, scap - 1, nseq, l_gid, seq_rep,
+               sovf);
+        uint32_t G = get1(nseq);
+        res.n_gid = G;
+        if (get1(sovf)) fail(STG_ENOMEM, "sequence table overflow");
+        // materialize
+        uint64_t* seq_len = dev<uint64_t>("seq_len", G + 1);
+        LAUNCH(k_seq_len64, grid_for(G), kThreads, G, seq_rep, foff, seq_len);
+        zero(seq_len + G, 8);
+        d_seq_off = dev<uint64_t>("seq_off", G + 1);
+        excl_sum(seq_len, d_seq_off, uint64_t(G) + 1);
+        uint64_t A = get1(d_seq_off + G);
+        d_arena = dev<uint32_t>("arena", A);
+        unsigned* d_unk_used = static_cast<unsigned*>(c.buf("unk_used").p);
+        int* d_unk_ovf = static_cast<int*>(c.buf("unk_ovf").p);
+        int* d_ebin = static_cast<int*>(c.buf("ebin").p);
+        UnkSet us{unk, unk_cap - 1, unk_cap - 1, d_unk_used, d_unk_ovf};
+        LAUNCH(k_seq_materialize, grid_for(uint64_t(G) * 32), kThreads, G, seq_rep, d_seq_off, foff, pc, bin, d_tabs,
+               uint32_t(w.n_bins), cfg.lookup_mode, us, d_ebin, d_arena);
+        // unknown labels -> merged name space
+        uint32_t* u_slot = dev<uint32_t>("u_slot", unk_cap);
+        uint32_t* u_bin = dev<uint32_t>("u_bin", unk_cap);
+        uint64_t* u_pc = dev<uint64_t>("u_pc", unk_cap);
+        unsigned* nu = dev<unsigned>("nu", 1);
+        zero(nu, 4);
+        LAUNCH(k_unk_compact, grid_for(unk_cap), kThreads, unk_cap, unk, u_slot, u_bin, u_pc, nu);
+        uint32_t NU = get1(nu);
+        res.n_unknown = NU;
+        std::vector<uint32_t> hs(NU), hb(NU);
+        std::vector<uint64_t> hp(NU);
+        down(hs.data(), u_slot, NU);
+        down(hb.data(), u_bin, NU);
+        down(hp.data(), u_pc, NU);
+        merge_labels(NU, hs, hb, hp, unk_cap);
+        LAUNCH(k_remap, grid_for(A), kThreads, A, d_arena, static_cast<const uint32_t*>(c.buf("u_final").p),
+               static_cast<const uint32_t*>(c.buf("u_pos").p), uint32_t(n_pos));
+        uint64_t NF = c.dict.size() + res.unk_labels.size();
+        res.n_names = NF;
+        // lexicographic sort of the sequences
+        uint32_t* gids = dev<uint32_t>("gids", G);
+        LAUNCH(k_iota, grid_for(G), kThreads, gids, G);
+        {
+            SeqLess less{d_arena, d_seq_off};
+            size_t tb = 0;
+            STG_CUDA(cub::DeviceMergeSort::SortKeys(nullptr, tb, gids, int64_t(G), less, st));
+            STG_CUDA(cub::DeviceMergeSort::SortKeys(temp(tb), tb, gids, int64_t(G), less, st));
+            ++launches;
+            uint32_t* flg = dev<uint32_t>("sq_flag", G);
+            uint32_t* scn = dev<uint32_t>("sq_scan", G);
+            LAUNCH(k_seq_rankflags, grid_for(G), kThreads, G, gids, less, flg);
+            incl_sum(flg, scn, G);
+            S = get1(scn + G - 1);
+            res.n_seq = S;
+            uint32_t* seq_rank = dev<uint32_t>("seq_rank", G);
+            d_dense_rep = dev<uint32_t>("dense_rep", S);
+            LAUNCH(k_seq_rankset, grid_for(G), kThreads, G, gids, scn, seq_rank, d_dense_rep);
+            uint64_t* lkey = dev<uint64_t>("lkey", L);
+            LAUNCH(k_line_keys, grid_for(L), kThreads, L, l_rank, l_gid, seq_rank, lkey);
+            d_lkey = dev<uint64_t>("lkey_s", L);
+            unsigned long long* lc64 = dev<unsigned long long>("lc64", L);
+            LAUNCH(k_u32_to_u64, grid_for(L), kThreads, L, l_cnt32, lc64);
+            d_lcount = dev<unsigned long long>("lcount_s", L);
+            sort_pairs(lkey, d_lkey, lc64, d_lcount, L);
+            if (S < G) {  // identical name sequences from distinct keys: merge lines
+                uint64_t* uk = dev<uint64_t>("rbk_k", L);
+                unsigned long long* uv = dev<unsigned long long>("rbk_v", L);
+                unsigned long long* nr = dev<unsigned long long>("rbk_n", 1);
+                size_t tb2 = 0;
+                STG_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, tb2, d_lkey, uk, d_lcount, uv, nr, cub::Sum(), L, st));
+                STG_CUDA(cub::DeviceReduce::ReduceByKey(temp(tb2), tb2, d_lkey, uk, d_lcount, uv, nr, cub::Sum(), L, st));
+                ++launches;
+                L = get1(nr);
+                res.n_lines = L;
+                STG_CUDA(cudaMemcpyAsync(d_lkey, uk, L * 8, cudaMemcpyDeviceToDevice, st));
+                STG_CUDA(cudaMemcpyAsync(d_lcount, uv, L * 8, cudaMemcpyDeviceToDevice, st));
+            }
+        }
+        d_line_off = dev<uint64_t>("line_off", R + 1);
+        LAUNCH(k_line_bounds, grid_for(R + 1), kThreads, R, d_lkey, L, d_line_off);
+        cudaEventRecord(ev[5], st);
+        // ---- stage c: distinct names per sequence, used-name space, inclusive counts
+        uint64_t* dcnt = dev<uint64_t>("dn_cnt", S + 1);
+        uint32_t* dcnt32 = dev<uint32_t>("dn_cnt32", S + 1);
+        LAUNCH(k_seq_distinct<false>, grid_for(S * 32), kThreads, uint32_t(S), d_dense_rep, d_seq_off, d_arena, dcnt32,
+               nullptr, nullptr);
+        zero(dcnt32 + S, 4);
+        LAUNCH(k_u32_to_u64, grid_for(S + 1), kThreads, S + 1, dcnt32, (unsigned long long*)dcnt);
+        d_dn_off = dev<uint64_t>("dn_off", S + 1);
+        excl_sum(dcnt, d_dn_off, S + 1);
+        uint64_t ND = get1(d_dn_off + S);
+        d_dn = dev<uint32_t>("dn", ND);
+        LAUNCH(k_seq_distinct<true>, grid_for(S * 32), kThreads, uint32_t(S), d_dense_rep, d_seq_off, d_arena, nullptr,
+               d_dn_off, d_dn);
+        uint32_t* used = dev<uint32_t>("used", NF + 1);
+        zero(used, (NF + 1) * 4);
+        LAUNCH(k_mark_used, grid_for(ND), kThreads, ND, d_dn, used);
+        uint32_t* used_scan = dev<uint32_t>("used_scan", NF + 1);
+        excl_sum(used, used_scan, NF + 1);
+        F = get1(used_scan + NF);
+        res.f_used = F;
+        d_dense_final = dev<uint32_t>("dense_final", F);
+        LAUNCH(k_dense_final, grid_for(NF), kThreads, NF, used, used_scan, d_dense_final);
+        LAUNCH(k_dense_names, grid_for(ND), kThreads, ND, d_dn, used_scan);
+        uint64_t cells = uint64_t(R) * F;
+        if (cells > (1ull << 31)) fail(STG_ENOMEM, "rank x name matrix too large");
+        d_incl = dev<unsigned long long>("incl", cells);
+        zero(d_incl, cells * 8);
+        LAUNCH(k_incl, grid_for(L * 32), kThreads, L, d_lkey, d_lcount, d_dn_off, d_dn, F, d_incl);
+        cudaEventRecord(ev[6], st);
+    }
+
+    // ------------------------------------------------------- diagnose
+    std::string dense_name(uint32_t f) {
+        if (h_dense_final.size() != F) {
+            h_dense_final.resize(F);
+            down(h_dense_final.data(), d_dense_final, F);
+        }
+        return res.name_of(h_dense_final[f]);
+    }
+    int cpu_index(int rank) const {
+        auto it = std::lower_bound(res.cpu_rank_ids.begin(), res.cpu_rank_ids.end(), rank);
+        if (it == res.cpu_rank_ids.end() || *it != rank) return -1;
+        return int(res.cpu_rank_index[size_t(it - res.cpu_rank_ids.begin())]);
+    }
+    std::vector<std::string> seq_names(uint32_t s) {
+        uint32_t g;
+        down(&g, d_dense_rep + s, 1);
+        uint64_t o[2];
+        down(o, d_seq_off + g, 2);
+        std::vector<uint32_t> keys(o[1] - o[0]);
+        down(keys.data(), d_arena + o[0], keys.size());
+        std::vector<std::string> out;
+        for (uint32_t k : keys) out.push_back(res.name_of(k));
+        return out;
+    }
+    // hottest path over lines [a, b) of the sorted line list (or over sequences)
+    std::vector<std::string> hottest(uint64_t a, uint64_t b, uint32_t f, bool merged) {
+        unsigned long long* best = dev<unsigned long long>("hot_best", 2);
+        unsigned long long init[2] = {0, ~0ull};
+        STG_CUDA(cudaMemcpyAsync(best, init, 16, cudaMemcpyHostToDevice, st));
+        if (merged) {
+            auto sc = static_cast<unsigned long long*>(c.buf("seq_counts").p);
+            for (int pass = 0; pass < 2; ++pass)
+                LAUNCH(k_hottest, grid_for(S), kThreads, S, nullptr, sc, 1, d_dn_off, d_dn, f, pass, best);
+        } else {
+            for (int pass = 0; pass < 2; ++pass)
+                LAUNCH(k_hottest, grid_for(b - a), kThreads, b - a, d_lkey + a, d_lcount + a, 0, d_dn_off, d_dn, f, pass,
+                       best);
+        }
+        unsigned long long hb[2];
+        down(hb, best, 2);
+        if (hb[1] == ~0ull) return {};
+        uint32_t s;
+        if (merged)
+            s = uint32_t(hb[1]);
+        else {
+            uint64_t k;
+            down(&k, d_lkey + a + hb[1], 1);
+            s = uint32_t(k);
+        }
+        return seq_names(s);
+    }
+    // Exact inclusive fractions over lines [a, a+n) (or over all sequences when
+    // merged): returns (dense name, fraction) in name order.
+    std::vector<std::pair<uint32_t, double>> exact_fractions(uint64_t a, uint64_t n, uint64_t total, bool merged) {
+        std::vector<std::pair<uint32_t, double>> out;
+        if (n == 0 || total == 0) return out;
+        const uint64_t* lk = merged ? nullptr : d_lkey + a;
+        const unsigned long long* cnt = merged ? static_cast<unsigned long long*>(c.buf("seq_counts").p) : d_lcount + a;
+        uint64_t* pc = dev<uint64_t>("xf_cnt", n + 1);
+        LAUNCH(k_pair_count, grid_for(n), kThreads, n, lk, d_dn_off, pc);
+        zero(pc + n, 8);
+        uint64_t* po = dev<uint64_t>("xf_off", n + 1);
+        excl_sum(pc, po, n + 1);
+        uint64_t np = get1(po + n);
+        if (!np) return out;
+        uint64_t* keys = dev<uint64_t>("xf_keys", np);
+        uint64_t* keys_s = dev<uint64_t>("xf_keys_s", np);
+        uint32_t* line = dev<uint32_t>("xf_line", np);
+        uint32_t* line_s = dev<uint32_t>("xf_line_s", np);
+        LAUNCH(k_pair_emit, grid_for(n), kThreads, n, lk, d_dn_off, d_dn, po, keys, line);
+        sort_pairs(keys, keys_s, line, line_s, np);
+        uint32_t* flag = dev<uint32_t>("xf_flag", np);
+        LAUNCH(k_pair_segflags, grid_for(np), kThreads, np, keys_s, flag);
+        uint32_t* seg = dev<uint32_t>("xf_seg", np);
+        uint64_t nseg = select_flagged(flag, seg, np);
+        uint32_t* of = dev<uint32_t>("xf_of", nseg);
+        double* ov = dev<double>("xf_ov", nseg);
+        LAUNCH(k_pair_segsum, grid_for(nseg, 64), 64, nseg, seg, np, keys_s, cnt, total, of, ov);
+        std::vector<uint32_t> hf(nseg);
+        std::vector<double> hv(nseg);
+        down(hf.data(), of, nseg);
+        down(hv.data(), ov, nseg);
+        out.resize(nseg);
+        for (uint64_t i = 0; i < nseg; ++i) out[i] = {hf[i], hv[i]};
+        return out;
+    }
+    static double mean_of(const std::vector<double>& v) {
+        double s = 0.0;
+        for (double x : v) s += x;
+        return s / double(v.size());
+    }
+    static double pstd(const std::vector<double>& v, double mu) {
+        double a = 0.0;
+        for (double x : v) a += (x - mu) * (x - mu);
+        return std::sqrt(a / double(v.size()));
+    }
+    static double median_of(std::vector<double> v) {
+        std::sort(v.begin(), v.end());
+        size_t n = v.size();
+        return n % 2 ? v[n / 2] : (v[n / 2 - 1] + v[n / 2]) / 2.0;
+    }
+
+    void diagnose() {
+        Report& rep = res.report;
+        rep = Report{};
+        // detect_straggler alerts (diagnosis.cpp:97-110)
+        std::vector<int> alerts;
+        for (int32_t r = 0; r < span; ++r)
+            if (res.flag_count[r] && res.flag_count[r] * 2 > res.n_windowed) alerts.push_back(r);
+        if (!alerts.empty()) {
+            rep.flagged_ranks = alerts;  // already ascending
+            // median_lateness_rank (diagnosis.cpp:284-297)
+            std::vector<std::pair<double, int>> means;
+            for (int32_t r = 0; r < span; ++r)
+                if (res.lat_present[r] && !std::binary_search(alerts.begin(), alerts.end(), r))
+                    means.emplace_back(res.mean_lat_all[r], r);
+            if (means.empty()) {
+                rep.verdict = STG_VERDICT_INCONCLUSIVE;
+                rep.notes.push_back("no reference rank available");
+                return;
+            }
+            std::sort(means.begin(), means.end());
+            int ref = means[means.size() / 2].second;
+            rep.reference_rank = ref;
+            int strag = alerts.front();
+            int concluded = STG_VERDICT_INCONCLUSIVE;
+            std::vector<Evidence> gpu_ev, cpu_ev, os_ev;
+            // GPU layer (gpu_diff diagnosis.cpp:122-172)
+            if (res.gpu.count(strag) && res.gpu.count(ref)) {
+                const auto& S_ = res.gpu.at(strag);
+                const auto& Rf = res.gpu.at(ref);
+                std::vector<double> slow;
+                std::map<std::string, double> slowdown;
+                int64_t total_added = 0;
+                std::string top;
+                std::string prefix = cfg.gpu_exclude_prefix;
+                for (const auto& [name, t_ref] : Rf) {
+                    if (t_ref < cfg.gpu_ref_floor_ns) continue;
+                    if (!prefix.empty() && name.rfind(prefix, 0) == 0) continue;
+                    auto it = S_.find(name);
+                    if (it == S_.end()) continue;
+                    double s = double(it->second) / double(t_ref) - 1.0;
+                    slowdown[name] = s;
+                    slow.push_back(s);
+                    int64_t added = it->second - t_ref;
+                    if (added > 0) {
+                        total_added += added;
+                        if (top.empty() || added > S_.at(top) - Rf.at(top)) top = name;
+                    }
+                }
+                int gv = 0;  // None
+                if (!slow.empty()) {
+                    double med = median_of(slow);
+                    double mu = mean_of(slow);
+                    double sg = pstd(slow, mu);
+                    double cv = mu != 0.0 ? std::fabs(sg / mu) : 0.0;
+                    double share = 0.0;
+                    if (!top.empty() && total_added > 0) share = double(S_.at(top) - Rf.at(top)) / double(total_added);
+                    if (med <= cfg.gpu_median_none) gv = 0;
+                    else if (med > cfg.gpu_median_uniform && cv < cfg.gpu_cv_uniform) gv = 1;
+                    else if (share > cfg.gpu_top_share_specific) gv = 2;
+                }
+                for (const auto& [name, s] : slowdown)
+                    gpu_ev.push_back({"gpu", name, double(S_.at(name)), double(Rf.at(name)), s});
+                if (gv == 1) concluded = STG_VERDICT_GPU_UNIFORM;
+                else if (gv == 2) {
+                    concluded = STG_VERDICT_GPU_SPECIFIC;
+                    rep.top_path = {top};
+                }
+            } else {
+                rep.notes.push_back("gpu profiles missing; gpu layer skipped");
+            }
+            // CPU layer (cpu_diff diagnosis.cpp:177-208)
+            int is = cpu_index(strag), iq = cpu_index(ref);
+            if (is >= 0 && iq >= 0) {
+                struct Cand { std::string fn; double fs, fr, d; uint32_t f; };
+                std::vector<Cand> cands;
+                uint64_t lo[2], lo2[2];
+                down(lo, d_line_off + is, 2);
+                down(lo2, d_line_off + iq, 2);
+                auto fs_ = exact_fractions(lo[0], lo[1] - lo[0], h_n_in[is], false);
+                auto fr_ = exact_fractions(lo2[0], lo2[1] - lo2[0], h_n_in[iq], false);
+                size_t j = 0;
+                for (const auto& [f, fs] : fs_) {  // name order (dense index order)
+                    while (j < fr_.size() && fr_[j].first < f) ++j;
+                    double fr = j < fr_.size() && fr_[j].first == f ? fr_[j].second : 0.0;
+                    double d = fs - fr;
+                    if (d > cfg.delta) cands.push_back({dense_name(f), fs, fr, d, f});
+                }
+                std::sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) {
+                    return a.d != b.d ? a.d > b.d : a.fn < b.fn;
+                });
+                for (const auto& cd : cands) cpu_ev.push_back({"cpu", cd.fn, cd.fs, cd.fr, cd.d});
+                if (concluded == STG_VERDICT_INCONCLUSIVE && !cands.empty()) {
+                    concluded = STG_VERDICT_CPU_INTERFERENCE;
+                    rep.top_path = hottest(lo[0], lo[1], cands.front().f, false);
+                }
+            } else {
+                rep.notes.push_back("cpu profiles missing; cpu layer skipped");
+            }
+            // OS layer (os_diff diagnosis.cpp:213-243)
+            if (res.os.count(strag) && res.os.count(ref)) {
+                const OsAcc& s = res.os.at(strag);
+                const OsAcc& r = res.os.at(ref);
+                auto check = [&](const std::string& name, int64_t sv, int64_t rv, int64_t floor) {
+                    if (sv - rv < floor) return;
+                    if (rv == 0) {
+                        os_ev.push_back({"os", name, double(sv), double(rv), 0.0});
+                        return;
+                    }
+                    double ratio = double(sv) / double(rv);
+                    if (ratio >= cfg.os_min_ratio) os_ev.push_back({"os", name, double(sv), double(rv), ratio});
+                };
+                for (const auto& [k, v] : s.interrupts) {
+                    auto it = r.interrupts.find(k);
+                    check("interrupt:" + k, v, it == r.interrupts.end() ? 0 : it->second, cfg.os_interrupt_floor);
+                }
+                for (const auto& [k, v] : s.softirqs) {
+                    auto it = r.softirqs.find(k);
+                    check("softirq:" + k, v, it == r.softirqs.end() ? 0 : it->second, cfg.os_interrupt_floor);
+                }
+                check("sched_delay_p99_ns", s.p99, r.p99, cfg.os_sched_delay_floor_ns);
+                check("numa_migrations", s.migrations, r.migrations, cfg.os_migration_floor);
+                if (concluded == STG_VERDICT_INCONCLUSIVE && !os_ev.empty()) concluded = STG_VERDICT_OS_INTERFERENCE;
+            } else {
+                rep.notes.push_back("os snapshots missing; os layer skipped");
+            }
+            rep.verdict = concluded;
+            for (auto* v : {&gpu_ev, &cpu_ev, &os_ev}) rep.evidence.insert(rep.evidence.end(), v->begin(), v->end());
+            if (rep.verdict == STG_VERDICT_INCONCLUSIVE) rep.notes.push_back("straggler detected but no layer concluded");
+            return;
+        }
+        // No straggler: temporal route (diagnosis.cpp:383-428)
+        if (res.has_baseline_iteration && !res.iteration_times_ms.empty()) {
+            double now = mean_of(res.iteration_times_ms);
+            double base = res.baseline_iteration_ms;
+            if (base > 0.0 && now > base * (1.0 + cfg.iteration_regression_gate)) {
+                if (!res.has_baseline) {
+                    rep.verdict = STG_VERDICT_INCONCLUSIVE;
+                    rep.notes.push_back("iteration time regressed but no baseline profile");
+                    return;
+                }
+                struct Cand { std::string fn; double now, base, d; uint32_t f; };
+                std::vector<Cand> cands;
+                if (F > 0) {
+                    auto sc = dev<unsigned long long>("seq_counts", S);
+                    zero(sc, S * 8);
+                    LAUNCH(k_seq_counts, grid_for(L), kThreads, L, d_lkey, d_lcount, sc);
+                    uint64_t T = 0;
+                    for (uint64_t t : res.cpu_totals) T += t;
+                    for (const auto& [f, nw] : exact_fractions(0, S, T, true)) {
+                        std::string fn = dense_name(f);
+                        auto it = res.baseline.find(fn);
+                        double b = it == res.baseline.end() ? 0.0 : it->second;
+                        double d = nw - b;
+                        if (d > res.baseline_delta) cands.push_back({fn, nw, b, d, f});
+                    }
+                }
+                std::sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) {
+                    return a.d != b.d ? a.d > b.d : a.fn < b.fn;
+                });
+                if (!cands.empty()) {
+                    rep.verdict = STG_VERDICT_TEMPORAL;
+                    rep.flagged_ranks.assign(res.cpu_rank_ids.begin(), res.cpu_rank_ids.end());
+                    for (const auto& cd : cands) rep.evidence.push_back({"temporal", cd.fn, cd.now, cd.base, cd.d});
+                    rep.top_path = hottest(0, 0, cands.front().f, true);
+                    return;
+                }
+                rep.verdict = STG_VERDICT_INCONCLUSIVE;
+                rep.notes.push_back("iteration time regressed but no profile delta above delta");
+                return;
+            }
+        }
+        rep.verdict = STG_VERDICT_HEALTHY;
+    }
+
+    // ------------------------------------------------------ waterline
+    // compute_waterline + flag_ranks over the window's CPU profiles.
+    void waterline() {
+        res.waterline_done = true;
+        std::string out;
+        size_t nr = res.cpu_rank_ids.size();
+        if (nr < 2) {
+            res.waterline_json = "{\"error\": \"waterline requires at least 2 ranks\"}";
+            return;
+        }
+        uint32_t* rows = up<uint32_t>("wl_rows", res.cpu_rank_index.data(), nr);
+        double* mean = dev<double>("wl_mean", F);
+        double* sd = dev<double>("wl_sd", F);
+        uint8_t* pres = dev<uint8_t>("wl_pres", F);
+        LAUNCH(k_waterline, grid_for(F, 128), 128, F, rows, int(nr), d_incl, d_totals, mean, sd, pres);
+        unsigned long long cap = std::max<uint64_t>(1, std::min<uint64_t>(F * nr, 1u << 24));
+        uint32_t* o_r = dev<uint32_t>("wl_or", cap);
+        uint32_t* o_f = dev<uint32_t>("wl_of", cap);
+        double* o_fr = dev<double>("wl_ofr", cap);
+        double* o_th = dev<double>("wl_oth", cap);
+        unsigned long long* n_out = dev<unsigned long long>("wl_n", 1);
+        zero(n_out, 8);
+        LAUNCH(k_flag, grid_for(F * nr), kThreads, F, rows, int(nr), d_incl, d_totals, cfg.k, mean, sd, o_r, o_f, o_fr,
+               o_th, n_out, cap);
+        uint64_t nf = std::min<uint64_t>(get1(n_out), cap);
+        std::vector<double> hm(F), hs(F);
+        std::vector<uint8_t> hp(F);
+        down(hm.data(), mean, F);
+        down(hs.data(), sd, F);
+        down(hp.data(), pres, F);
+        std::vector<uint32_t> fr(nf), ff(nf);
+        std::vector<double> ffr(nf), fth(nf);
+        down(fr.data(), o_r, nf);
+        down(ff.data(), o_f, nf);
+        down(ffr.data(), o_fr, nf);
+        down(fth.data(), o_th, nf);
+        JsonW j;
+        j.raw("{\"functions\": [");
+        bool first = true;
+        for (uint64_t f = 0; f < F; ++f) {
+            if (!hp[f]) continue;
+            if (!first) j.raw(", ");
+            first = false;
+            j.raw("[");
+            j.str(dense_name(uint32_t(f)));
+            j.raw(", ");
+            j.num(hm[f]);
+            j.raw(", ");
+            j.num(hs[f]);
+            j.raw("]");
+        }
+        j.raw("], \"flags\": [");
+        // flag_ranks order: ranks ascending, names in map order
+        std::vector<size_t> order(nf);
+        std::iota(order.begin(), order.end(), 0);
+        std::sort(order.begin(), order.end(), [&](size_t a, size_t b) {
+            return fr[a] != fr[b] ? fr[a] < fr[b] : ff[a] < ff[b];
+        });
+        for (size_t i = 0; i < nf; ++i) {
+            size_t k = order[i];
+            if (i) j.raw(", ");
+            j.raw("[");
+            j.num(int64_t(w.rank_ids[fr[k]]));
+            j.raw(", ");
+            j.str(dense_name(ff[k]));
+            j.raw(", ");
+            j.num(ffr[k]);
+            j.raw(", ");
+            j.num(fth[k]);
+            j.raw("]");
+        }
+        j.raw("]}");
+        res.waterline_json = j.s;
+    }
+
+    void run() {
+        res.group = w.group;
+        res.has_baseline = w.has_baseline != 0;
+        res.baseline_delta = w.baseline_delta;
+        res.baseline.clear();
+        for (uint32_t i = 0; i < w.n_baseline; ++i) res.baseline[w.baseline_names[i]] = w.baseline_fracs[i];
+        res.has_baseline_iteration = w.has_baseline_iteration != 0;
+        res.baseline_iteration_ms = w.baseline_iteration_ms;
+        cudaEventRecord(ev[0], st);
+        rank_space();
+        collectives();
+        cudaEventRecord(ev[1], st);
+        gpu_os();
+        samples();
+        if (ev_unset_fold()) {
+            cudaEventRecord(ev[2], st);
+            cudaEventRecord(ev[3], st);
+            cudaEventRecord(ev[4], st);
+            cudaEventRecord(ev[5], st);
+            cudaEventRecord(ev[6], st);
+        }
+        diagnose();
+        res.waterline_done = false;
+        if (cfg.want_waterline) waterline();
+        cudaEventRecord(ev[7], st);
+        STG_CUDA(cudaStreamSynchronize(st));
+        stg_run_stats& s = res.stats;
+        s = stg_run_stats{};
+        uint64_t nin = 0;
+        for (uint64_t t : res.cpu_totals) nin += t;
+        s.n_samples_in_window = nin;
+        s.n_lines = res.n_lines;
+        s.n_sequences = res.n_seq;
+        s.n_names = res.n_names;
+        s.n_unknown = res.n_unknown;
+        s.n_instances = res.n_instances;
+        s.n_windowed = res.n_windowed;
+        s.n_cpu_ranks = res.cpu_rank_ids.size();
+        s.verdict = res.report.verdict;
+        s.n_flagged = int32_t(res.report.flagged_ranks.size());
+        cudaEventElapsedTime(&s.ms_collectives, ev[0], ev[1]);
+        cudaEventElapsedTime(&s.ms_symbolize, ev[2], ev[3]);
+        cudaEventElapsedTime(&s.ms_fold, ev[4], ev[5]);
+        cudaEventElapsedTime(&s.ms_diff, ev[5], ev[6]);
+        cudaEventElapsedTime(&s.ms_total, ev[0], ev[7]);
+        s.h2d_bytes = h2d;
+        s.d2h_bytes = d2h;
+        s.kernel_launches = launches;
+    }
+    bool ev_unset_fold() const { return R == 0 || L == 0; }
+};
+
+}  // namespace stg

@@ -1,0 +1,1080 @@
+// stg_window.cu — the per-window batch on the GPU: replaces build_group_data
+// (proj/core/src/bundle.cpp:252-324) and the statistics behind diagnose
+// (diagnosis.cpp:76-111, 122-263).  Stage map:
+//   d  collectives: k_coll_* (match_collectives collective.cpp:29-103,
+//      align_clocks :105-125, entry_lateness :127-142, windowing bundle.cpp:270-285)
+//      + k_straggler_* (detect_straggler diagnosis.cpp:76-111, bit-exact FP order)
+//   a+b samples:   k_sym_agg — fused symbolize (SymbolFile::lookup symfile.cpp:54-75)
+//      + aggregate (aggregate_samples samples.cpp:31-85 / to_folded folded.cpp:56-71)
+//      keyed by the symbolized stack; k_seq_* dedupe, materialize, sort -> folded
+//      lines in std::map order (folded.cpp:11-19)
+//   c  diff:        k_incl (inclusive_fractions folded.cpp:45-54), k_waterline
+//      (compute_waterline diagnosis.cpp:35-55), candidate kernels for cpu_diff /
+//      temporal_diff; the decision ladder of diagnose (diagnosis.cpp:301-432) runs
+//      on the host over these device-side summaries.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "kernels.cuh"
+#include "result.h"
+
+namespace stg {
+
+Ctx::~Ctx() {
+    for (auto& t : tables) {
+        if (t->d_starts) cudaFree(t->d_starts);
+        if (t->d_ent) cudaFree(t->d_ent);
+        if (t->d_bucket) cudaFree(t->d_bucket);
+    }
+    bufs.clear();
+    if (stream) cudaStreamDestroy(stream);
+}
+
+std::string Result::name_of(uint32_t f) const {
+    // unknown labels carry explicit final ranks; real names fill the rest in order
+    auto it = std::lower_bound(unk_final.begin(), unk_final.end(), uint64_t(f));
+    if (it != unk_final.end() && *it == f) return unk_labels[size_t(it - unk_final.begin())];
+    uint64_t before = uint64_t(it - unk_final.begin());
+    return (*dict)[f - before];
+}
+
+namespace {
+
+constexpr int kThreads = 256;
+inline unsigned grid_for(uint64_t n, int threads = kThreads, unsigned cap = 148 * 32) {
+    uint64_t g = (n + threads - 1) / threads;
+    if (g == 0) g = 1;
+    return unsigned(std::min<uint64_t>(g, cap));
+}
+inline uint64_t next_pow2(uint64_t v) {
+    uint64_t p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+// ============================================================== tables
+__global__ void k_build_buckets(const uint64_t* starts, uint32_t n, uint64_t base, uint32_t shift,
+                                uint32_t nb, uint32_t* bucket) {
+    for (uint64_t b = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; b <= nb;
+         b += uint64_t(gridDim.x) * blockDim.x) {
+        if (b == nb) {
+            bucket[b] = n - 1;
+            continue;
+        }
+        uint64_t key = base + (b << shift);
+        // last index with starts[i] <= key
+        uint32_t lo = 0, hi = n;  // upper_bound
+        while (lo < hi) {
+            uint32_t mid = (lo + hi) >> 1;
+            if (starts[mid] <= key)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        bucket[b] = lo == 0 ? 0 : lo - 1;
+    }
+}
+
+// ========================================================= collectives
+// key = (group ^ signbit) << 32 | kind << 24 | rank   (stable sort => per-rank order kept)
+__global__ void k_coll_keys(uint64_t n, const int32_t* rank, const int32_t* group, const uint8_t* kind,
+                            uint64_t* key, uint32_t* idx, int* err_rank) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        int32_t r = rank[i];
+        if (r < 0 || r >= (1 << 24)) *err_rank = 1;
+        key[i] = (uint64_t(uint32_t(group[i]) ^ 0x80000000u) << 32) | (uint64_t(kind[i]) << 24) |
+                 uint64_t(uint32_t(r) & 0xffffffu);
+        idx[i] = uint32_t(i);
+    }
+}
+
+__global__ void k_coll_gather(uint64_t n, const uint64_t* key, const uint32_t* idx, const int64_t* entry,
+                              const int64_t* exit_, int64_t* s_entry, int64_t* s_exit,
+                              unsigned long long* err_ee, unsigned long long* err_ord,
+                              uint32_t* seg_flag, uint32_t* stream_flag) {
+    for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < n;
+         p += uint64_t(gridDim.x) * blockDim.x) {
+        uint32_t e = idx[p];
+        int64_t en = entry[e], ex = exit_[e];
+        s_entry[p] = en;
+        s_exit[p] = ex;
+        if (en >= ex) atomicMin(err_ee, (unsigned long long)e);
+        bool new_seg = p == 0 || key[p] != key[p - 1];
+        bool new_stream = p == 0 || (key[p] >> 24) != (key[p - 1] >> 24);
+        if (!new_seg && en < entry[idx[p - 1]]) atomicMin(err_ord, (unsigned long long)e);
+        seg_flag[p] = new_seg;
+        stream_flag[p] = new_stream;
+    }
+}
+
+// One block per stream: coarse offsets (collective.cpp:49-54), counts.
+__global__ void k_coll_streams(int n_streams, const uint32_t* st_seg, const uint32_t* seg_pos,
+                               const int64_t* s_entry, int64_t* coarse, uint32_t* kmin, uint32_t* kmax) {
+    int s = blockIdx.x;
+    if (s >= n_streams) return;
+    uint32_t a = st_seg[s], b = st_seg[s + 1];
+    __shared__ long long s_min;
+    __shared__ unsigned s_kmin, s_kmax;
+    if (threadIdx.x == 0) {
+        s_min = LLONG_MAX;
+        s_kmin = 0xffffffffu;
+        s_kmax = 0;
+    }
+    __syncthreads();
+    for (uint32_t j = a + threadIdx.x; j < b; j += blockDim.x) {
+        atomicMin(&s_min, (long long)s_entry[seg_pos[j]]);
+        uint32_t len = seg_pos[j + 1] - seg_pos[j];
+        atomicMin(&s_kmin, len);
+        atomicMax(&s_kmax, len);
+    }
+    __syncthreads();
+    for (uint32_t j = a + threadIdx.x; j < b; j += blockDim.x) coarse[j] = s_entry[seg_pos[j]] - s_min;
+    if (threadIdx.x == 0) {
+        kmin[s] = s_kmin;
+        kmax[s] = s_kmax;
+    }
+}
+
+// Regular-case proof: instance k of a stream is {every rank's k-th event} iff the
+// greedy sweep (collective.cpp:64-89) starting from all heads at k pulls them all.
+// One thread per (stream, k): seed = min pre-aligned entry, ties to the lowest
+// rank (strict <, rank order); then every head must overlap the seed interval.
+__global__ void k_coll_regular(int n_streams, const uint32_t* st_seg, const uint32_t* seg_pos,
+                               const int64_t* coarse, const int64_t* s_entry, const int64_t* s_exit,
+                               const uint32_t* kmin, const uint64_t* k_base, uint64_t n_k,
+                               int64_t skew, uint32_t* first_fail) {
+    for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < n_k;
+         t += uint64_t(gridDim.x) * blockDim.x) {
+        // stream of t
+        int s = 0;
+        while (s + 1 < n_streams && k_base[s + 1] <= t) ++s;
+        uint32_t k = uint32_t(t - k_base[s]);
+        uint32_t a = st_seg[s], b = st_seg[s + 1];
+        int64_t best = LLONG_MAX, best_exit = 0;
+        for (uint32_t j = a; j < b; ++j) {
+            uint64_t p = seg_pos[j] + k;
+            int64_t e = s_entry[p] - coarse[j];
+            if (e < best) {
+                best = e;
+                best_exit = s_exit[p] - coarse[j];
+            }
+        }
+        bool ok = true;
+        for (uint32_t j = a; j < b && ok; ++j) {
+            uint64_t p = seg_pos[j] + k;
+            int64_t e = s_entry[p] - coarse[j], x = s_exit[p] - coarse[j];
+            ok = e <= best_exit + skew && x + skew >= best;
+        }
+        if (!ok) atomicMin(first_fail + s, k);
+    }
+}
+
+// Regular part: event (j, k<k0) -> local instance k.
+__global__ void k_coll_assign_regular(int n_streams, const uint32_t* st_seg, const uint32_t* seg_pos,
+                                      const uint32_t* seg_stream, uint32_t n_seg, const uint32_t* k0,
+                                      uint32_t* inst_local) {
+    for (uint32_t j = blockIdx.x; j < n_seg; j += gridDim.x) {
+        uint32_t s = seg_stream[j];
+        uint32_t lim = k0[s];
+        uint32_t len = seg_pos[j + 1] - seg_pos[j];
+        for (uint32_t k = threadIdx.x; k < len; k += blockDim.x)
+            inst_local[seg_pos[j] + k] = k < lim ? k : 0xffffffffu;
+    }
+}
+
+// Sequential greedy sweep for the irregular tail of one stream (one block per
+// stream), from heads at k0 — a direct transcription of collective.cpp:64-89.
+__global__ void k_coll_sequential(const int* streams, const uint32_t* st_seg, const uint32_t* seg_pos,
+                                  const int64_t* coarse, const int64_t* s_entry, const int64_t* s_exit,
+                                  const uint32_t* k0, int64_t skew, uint32_t* head_buf,
+                                  uint32_t* inst_local, uint32_t* n_inst) {
+    int s = streams[blockIdx.x];
+    uint32_t a = st_seg[s], b = st_seg[s + 1];
+    uint32_t* head = head_buf + a;
+    for (uint32_t j = a + threadIdx.x; j < b; j += blockDim.x) head[j - a] = seg_pos[j] + k0[s];
+    __shared__ long long r_e[1024];
+    __shared__ unsigned r_j[1024];
+    __shared__ long long sd_entry, sd_exit;
+    __shared__ int done;
+    __syncthreads();
+    uint32_t inst = k0[s];
+    while (true) {
+        long long be = LLONG_MAX;
+        unsigned bj = 0xffffffffu;
+        for (uint32_t j = a + threadIdx.x; j < b; j += blockDim.x) {
+            uint32_t h = head[j - a];
+            if (h < seg_pos[j + 1]) {
+                long long e = s_entry[h] - coarse[j];
+                if (e < be || (e == be && j < bj)) {
+                    be = e;
+                    bj = j;
+                }
+            }
+        }
+        r_e[threadIdx.x] = be;
+        r_j[threadIdx.x] = bj;
+        __syncthreads();
+        for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+            if (threadIdx.x < w) {
+                long long oe = r_e[threadIdx.x + w];
+                unsigned oj = r_j[threadIdx.x + w];
+                if (oe < r_e[threadIdx.x] || (oe == r_e[threadIdx.x] && oj < r_j[threadIdx.x])) {
+                    r_e[threadIdx.x] = oe;
+                    r_j[threadIdx.x] = oj;
+                }
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            done = r_j[0] == 0xffffffffu;
+            if (!done) {
+                uint32_t h = head[r_j[0] - a];
+                sd_entry = s_entry[h] - coarse[r_j[0]];
+                sd_exit = s_exit[h] - coarse[r_j[0]];
+            }
+        }
+        __syncthreads();
+        if (done) break;
+        long long se = sd_entry, sx = sd_exit;
+        for (uint32_t j = a + threadIdx.x; j < b; j += blockDim.x) {
+            uint32_t h = head[j - a];
+            if (h < seg_pos[j + 1]) {
+                long long e = s_entry[h] - coarse[j], x = s_exit[h] - coarse[j];
+                if (e <= sx + skew && x + skew >= se) {
+                    inst_local[h] = inst;
+                    head[j - a] = h + 1;
+                }
+            }
+        }
+        ++inst;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) n_inst[s] = inst;
+}
+
+// Per event: global instance id, instance aggregates.
+__global__ void k_coll_inst(uint64_t n, const uint64_t* key, const uint32_t* seg_stream_of_pos_unused,
+                            const uint32_t* stream_of_pos, const uint64_t* inst_base,
+                            const uint32_t* inst_local, const int64_t* s_exit, const uint8_t* group_member,
+                            uint32_t* inst_of, unsigned long long* inst_max_exit, unsigned* inst_size,
+                            unsigned* inst_ingroup) {
+    for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < n;
+         p += uint64_t(gridDim.x) * blockDim.x) {
+        uint32_t s = stream_of_pos[p];
+        uint32_t g = uint32_t(inst_base[s] + inst_local[p]);
+        inst_of[p] = g;
+        uint32_t r = uint32_t(key[p] & 0xffffff);
+        atomicMax((long long*)&inst_max_exit[g], (long long)s_exit[p]);
+        atomicAdd(&inst_size[g], 1u);
+        if (group_member[r]) atomicAdd(&inst_ingroup[g], 1u);
+    }
+}
+
+// align_clocks (collective.cpp:105-125) inputs: (rank, exit - max exit) over
+// complete instances, as a composite sort key rank<<40 | (delta + 2^39).
+__global__ void k_coll_deltas(uint64_t n, const uint64_t* key, const uint32_t* inst_of,
+                              const int64_t* s_exit, const unsigned long long* inst_max_exit,
+                              const unsigned* inst_ingroup, unsigned n_group, uint64_t* dkey,
+                              unsigned long long* n_out, int* range_err) {
+    for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < n;
+         p += uint64_t(gridDim.x) * blockDim.x) {
+        uint32_t g = inst_of[p];
+        if (inst_ingroup[g] < n_group) continue;  // partial
+        int64_t d = s_exit[p] - (long long)inst_max_exit[g];
+        if (d < -(1ll << 39)) *range_err = 1;
+        uint64_t r = key[p] & 0xffffff;
+        unsigned long long o = atomicAdd(n_out, 1ull);
+        dkey[o] = (r << 40) | uint64_t(d + (1ll << 39));
+    }
+}
+
+// Per rank: median of its sorted deltas (even n: truncating int64 mean, :122).
+__global__ void k_coll_median(int rank_span, const uint64_t* dkey, uint64_t n, int64_t* off,
+                              uint8_t* has_off) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rank_span; r += gridDim.x * blockDim.x) {
+        uint64_t lo_key = uint64_t(r) << 40, hi_key = uint64_t(r + 1) << 40;
+        uint64_t a = 0, b = n;
+        while (a < b) {
+            uint64_t m = (a + b) >> 1;
+            if (dkey[m] < lo_key) a = m + 1; else b = m;
+        }
+        uint64_t lo = a;
+        b = n;
+        while (a < b) {
+            uint64_t m = (a + b) >> 1;
+            if (dkey[m] < hi_key) a = m + 1; else b = m;
+        }
+        uint64_t cnt = a - lo;
+        if (cnt == 0) {
+            has_off[r] = 0;
+            off[r] = 0;
+            continue;
+        }
+        auto val = [&](uint64_t i) { return int64_t(dkey[lo + i] & ((1ull << 40) - 1)) - (1ll << 39); };
+        has_off[r] = 1;
+        off[r] = cnt % 2 ? val(cnt / 2) : (val(cnt / 2 - 1) + val(cnt / 2)) / 2;
+    }
+}
+
+// Windowing (bundle.cpp:270-279): max aligned exit per complete instance, init 0.
+__global__ void k_coll_aligned_exit(uint64_t n, const uint64_t* key, const uint32_t* inst_of,
+                                    const int64_t* s_exit, const unsigned* inst_ingroup, unsigned n_group,
+                                    const int64_t* off, unsigned long long* inst_aexit) {
+    for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < n;
+         p += uint64_t(gridDim.x) * blockDim.x) {
+        uint32_t g = inst_of[p];
+        if (inst_ingroup[g] < n_group) continue;
+        uint32_t r = uint32_t(key[p] & 0xffffff);
+        atomicMax((long long*)&inst_aexit[g], (long long)(s_exit[p] - off[r]));
+    }
+}
+
+__global__ void k_coll_window_select(uint64_t n_inst, const unsigned* inst_ingroup, unsigned n_group,
+                                     const unsigned long long* inst_aexit, int64_t ws, uint64_t* wkey,
+                                     uint32_t* winst, unsigned long long* n_out) {
+    for (uint64_t g = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; g < n_inst;
+         g += uint64_t(gridDim.x) * blockDim.x) {
+        if (inst_ingroup[g] < n_group) continue;
+        long long mx = (long long)inst_aexit[g];
+        if (mx < ws) continue;
+        unsigned long long o = atomicAdd(n_out, 1ull);
+        wkey[o] = uint64_t(mx) ^ 0x8000000000000000ull;  // order-preserving
+        winst[o] = uint32_t(g);
+    }
+}
+
+__global__ void k_coll_winv(uint64_t n_w, const uint32_t* winst_sorted, uint32_t* inst_w) {
+    for (uint64_t w = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; w < n_w;
+         w += uint64_t(gridDim.x) * blockDim.x)
+        inst_w[winst_sorted[w]] = uint32_t(w);
+}
+
+// entry_lateness (collective.cpp:127-142): adj = entry - off, min, (adj-min)/1e6.
+__global__ void k_coll_minadj(uint64_t n, const uint64_t* key, const uint32_t* inst_of, const uint32_t* inst_w,
+                              const int64_t* s_entry, const int64_t* off, long long* wmin) {
+    for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < n;
+         p += uint64_t(gridDim.x) * blockDim.x) {
+        uint32_t w = inst_w[inst_of[p]];
+        if (w == 0xffffffffu) continue;
+        uint32_t r = uint32_t(key[p] & 0xffffff);
+        atomicMin(&wmin[w], (long long)(s_entry[p] - off[r]));
+    }
+}
+
+__global__ void k_coll_lateness(uint64_t n, const uint64_t* key, const uint32_t* inst_of,
+                                const uint32_t* inst_w, const int64_t* s_entry, const int64_t* off,
+                                const long long* wmin, uint64_t n_w, double* lat /* [rank_span][n_w] */) {
+    for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < n;
+         p += uint64_t(gridDim.x) * blockDim.x) {
+        uint32_t w = inst_w[inst_of[p]];
+        if (w == 0xffffffffu) continue;
+        uint32_t r = uint32_t(key[p] & 0xffffff);
+        int64_t adj = s_entry[p] - off[r];
+        lat[uint64_t(r) * n_w + w] = __ddiv_rn(__ll2double_rn(adj - wmin[w]), 1e6);
+    }
+}
+
+__global__ void k_coll_itertimes(uint64_t n_w, const uint64_t* wkey_sorted, double* it) {
+    for (uint64_t w = 1 + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; w < n_w;
+         w += uint64_t(gridDim.x) * blockDim.x) {
+        long long a = (long long)(wkey_sorted[w] ^ 0x8000000000000000ull);
+        long long b = (long long)(wkey_sorted[w - 1] ^ 0x8000000000000000ull);
+        it[w - 1] = __ddiv_rn(__ll2double_rn(a - b), 1e6);
+    }
+}
+
+// detect_straggler, per instance (diagnosis.cpp:82-96), in the reference's exact
+// floating-point order: Σ over ranks ascending, then /n; Σ (l-μ)² ascending.
+__global__ void k_straggler_inst(uint64_t n_w, int rank_span, const double* lat, double k,
+                                 double* mu_w, double* sigma_w, uint32_t* m_w) {
+    for (uint64_t w = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; w < n_w;
+         w += uint64_t(gridDim.x) * blockDim.x) {
+        double acc = 0.0;
+        uint32_t m = 0;
+        for (int r = 0; r < rank_span; ++r) {
+            double l = lat[uint64_t(r) * n_w + w];
+            if (l == l) {
+                acc = __dadd_rn(acc, l);
+                ++m;
+            }
+        }
+        m_w[w] = m;
+        if (m < 2) continue;
+        double mu = __ddiv_rn(acc, double(m));
+        double s2 = 0.0;
+        for (int r = 0; r < rank_span; ++r) {
+            double l = lat[uint64_t(r) * n_w + w];
+            if (l == l) {
+                double d = __dsub_rn(l, mu);
+                s2 = __dadd_rn(s2, __dmul_rn(d, d));
+            }
+        }
+        mu_w[w] = mu;
+        sigma_w[w] = __dsqrt_rn(__ddiv_rn(s2, double(m)));
+    }
+}
+
+// Per rank: flags, mean lateness (alert: over >=2-rank instances; median
+// reference: over all), mean z over flagged — each summed in instance order.
+__global__ void k_straggler_rank(uint64_t n_w, int rank_span, const double* lat, double k, const double* mu_w,
+                                 const double* sigma_w, const uint32_t* m_w, uint8_t* present,
+                                 double* mean_all, double* mean_alert, double* z_mean, uint64_t* flags,
+                                 uint8_t* has_z) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rank_span; r += gridDim.x * blockDim.x) {
+        double s_all = 0.0, s2 = 0.0, sz = 0.0;
+        uint64_t n_all = 0, n2 = 0, nz = 0;
+        const double* row = lat + uint64_t(r) * n_w;
+        for (uint64_t w = 0; w < n_w; ++w) {
+            double l = row[w];
+            if (!(l == l)) continue;
+            s_all = __dadd_rn(s_all, l);
+            ++n_all;
+            if (m_w[w] < 2) continue;
+            s2 = __dadd_rn(s2, l);
+            ++n2;
+            double mu = mu_w[w], sg = sigma_w[w];
+            if (sg > 0.0 && l > __dadd_rn(mu, __dmul_rn(k, sg))) {
+                sz = __dadd_rn(sz, __ddiv_rn(__dsub_rn(l, mu), sg));
+                ++nz;
+            }
+        }
+        present[r] = n_all > 0;
+        mean_all[r] = n_all ? __ddiv_rn(s_all, double(n_all)) : 0.0;
+        mean_alert[r] = n2 ? __ddiv_rn(s2, double(n2)) : 0.0;
+        z_mean[r] = nz ? __ddiv_rn(sz, double(nz)) : 0.0;
+        flags[r] = nz;
+        has_z[r] = nz > 0;
+    }
+}
+
+__global__ void k_fill_f64(double* p, uint64_t n, double v) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+__global__ void k_fill_i64(long long* p, uint64_t n, long long v) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+__global__ void k_iota(uint32_t* p, uint64_t n) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        p[i] = uint32_t(i);
+}
+__global__ void k_max_rank(uint64_t n, const int32_t* r, int* mx, int* mn) {
+    int a = -1, b = 0;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        a = max(a, r[i]);
+        b = min(b, r[i]);
+    }
+    atomicMax(mx, a);
+    atomicMin(mn, b);
+}
+
+// ================================================================ gpu / os
+// build_group_data GPU loop (bundle.cpp:302-306)
+__global__ void k_gpu_sums(uint64_t n, const int32_t* rank, const uint32_t* kern, const int64_t* start,
+                           const int64_t* dur, const int64_t* off, int64_t ws, uint32_t n_kern,
+                           unsigned long long* sums, uint8_t* present, int* err) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        int r = rank[i];
+        uint32_t k = kern[i];
+        if (k >= n_kern) {
+            *err = 1;
+            continue;
+        }
+        if (start[i] - off[r] < ws) continue;
+        atomicAdd(&sums[uint64_t(r) * n_kern + k], (unsigned long long)dur[i]);
+        present[uint64_t(r) * n_kern + k] = 1;
+    }
+}
+
+// build_group_data OS loop (bundle.cpp:308-320)
+__global__ void k_os_sums(uint64_t n, const int32_t* rank, const int64_t* wstart, const int64_t* p50,
+                          const int64_t* p99, const int64_t* mig, const uint64_t* irq_off,
+                          const uint32_t* irq_key, const int64_t* irq_val, const uint64_t* sirq_off,
+                          const uint32_t* sirq_key, const int64_t* sirq_val, const int64_t* off, int64_t ws,
+                          uint32_t n_keys, unsigned long long* irq, uint8_t* irq_p, unsigned long long* sirq,
+                          uint8_t* sirq_p, long long* p50m, long long* p99m, unsigned long long* migs,
+                          uint8_t* present, int* err) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        int r = rank[i];
+        if (wstart[i] - off[r] + 5000000000ll < ws) continue;
+        present[r] = 1;
+        for (uint64_t k = irq_off[i]; k < irq_off[i + 1]; ++k) {
+            uint32_t key = irq_key[k];
+            if (key >= n_keys) { *err = 1; continue; }
+            atomicAdd(&irq[uint64_t(r) * n_keys + key], (unsigned long long)irq_val[k]);
+            irq_p[uint64_t(r) * n_keys + key] = 1;
+        }
+        for (uint64_t k = sirq_off[i]; k < sirq_off[i + 1]; ++k) {
+            uint32_t key = sirq_key[k];
+            if (key >= n_keys) { *err = 1; continue; }
+            atomicAdd(&sirq[uint64_t(r) * n_keys + key], (unsigned long long)sirq_val[k]);
+            sirq_p[uint64_t(r) * n_keys + key] = 1;
+        }
+        atomicMax(&p50m[r], (long long)p50[i]);
+        atomicMax(&p99m[r], (long long)p99[i]);
+        atomicAdd(&migs[r], (unsigned long long)mig[i]);
+    }
+}
+
+// ===================================================== samples: stage a+b
+struct AggParams {
+    const int64_t* ts;
+    const uint64_t* foff;
+    const uint64_t* pc;
+    const uint16_t* bin;
+    const uint64_t* rank_soff;   // [R+1]
+    const int64_t* rank_clk;     // [R] clock offset of each CPU rank
+    const uint8_t* active;       // [R]
+    int R;
+    int64_t ws;
+    const DevTable* tabs;
+    uint32_t n_bins;
+    int mode;
+    AggSlot* slots;
+    const uint64_t* tab_off;     // [R] slot offset
+    const uint32_t* tab_mask;    // [R]
+    unsigned* tab_used;
+    int* tab_overflow;
+    UnkSet unk;
+    unsigned long long* n_in;    // [R]
+    int* unsorted;               // [R]
+    unsigned long long* err_empty;  // [R] min rank-relative index
+    int* err_bin;
+    uint64_t n_samples;
+    uint32_t chunk;              // samples per warp chunk
+};
+
+__device__ __forceinline__ void agg_insert(AggSlot* T, uint32_t mask, uint64_t fa, uint64_t fb, uint32_t rep,
+                                           uint32_t cnt, unsigned* used, int* overflow) {
+    uint32_t i = uint32_t(fb >> 20) & mask;
+    for (uint32_t probe = 0; probe <= mask; ++probe) {
+        unsigned long long cur = *(volatile unsigned long long*)&T[i].hi;
+        if (cur == 0) {
+            cur = atomicCAS(&T[i].hi, 0ull, (unsigned long long)fa);
+            if (cur == 0) {
+                T[i].rep = rep;
+                __threadfence();
+                *(volatile unsigned long long*)&T[i].lo = fb;
+                atomicAdd(&T[i].count, cnt);
+                if (atomicAdd(used, 1u) + 1 > (mask + 1) / 2) *overflow = 1;
+                return;
+            }
+        }
+        if (cur == fa) {
+            unsigned long long lo;
+            while ((lo = *(volatile unsigned long long*)&T[i].lo) == 0) __nanosleep(16);
+            if (lo == fb) {
+                atomicAdd(&T[i].count, cnt);
+                return;
+            }
+        }
+        i = (i + 1) & mask;
+    }
+    *overflow = 1;
+}
+
+// The fused hot kernel.  A warp owns `chunk` consecutive samples; G lanes work on
+// one sample (32/G samples per step).  Per sample: window filter on the aligned
+// clock (bundle.cpp:290-294), coalesced 8-byte pc / 2-byte bin loads with the
+// streaming cache hint, per-frame table search, a position-tagged 128-bit
+// fingerprint of the root-first name sequence (shuffle-reduced over the group),
+// and one insert into the rank's open-addressing table.
+template <int G>
+__global__ void __launch_bounds__(kThreads) k_sym_agg(AggParams p) {
+    __shared__ DevTable s_tabs[kMaxSmemBins];
+    for (uint32_t i = threadIdx.x; i < p.n_bins && i < kMaxSmemBins; i += blockDim.x) s_tabs[i] = p.tabs[i];
+    __syncthreads();
+    const DevTable* tabs = p.n_bins <= kMaxSmemBins ? s_tabs : p.tabs;
+    constexpr int SPW = 32 / G;
+    const int lane = threadIdx.x & 31, sub = lane / G, gl = lane % G;
+    const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    const uint64_t n_chunks = (p.n_samples + p.chunk - 1) / p.chunk;
+    for (uint64_t c = warp; c < n_chunks; c += nwarps) {
+        const uint64_t c0 = c * p.chunk;
+        const uint64_t c1 = min(p.n_samples, c0 + p.chunk);
+        // rank of the chunk's first sample (warp-uniform binary search)
+        int r;
+        {
+            int lo = 0, hi = p.R - 1;
+            while (lo < hi) {
+                int mid = (lo + hi + 1) >> 1;
+                if (__ldg(p.rank_soff + mid) <= c0) lo = mid; else hi = mid - 1;
+            }
+            r = lo;
+        }
+        unsigned long long in_cnt = 0;
+        int cnt_rank = r;
+        for (uint64_t s0 = c0; s0 < c1; s0 += SPW) {
+            const uint64_t i = s0 + sub;
+            bool valid = i < c1;
+            int ri = r;
+            if (valid)
+                while (ri + 1 < p.R && __ldg(p.rank_soff + ri + 1) <= i) ++ri;
+            bool inwin = false;
+            uint64_t f0 = 0, f1 = 0;
+            if (valid && p.active[ri]) {
+                int64_t t = __ldcs(p.ts + i);
+                uint64_t rs = __ldg(p.rank_soff + ri);
+                if (gl == 0 && i > rs && t < __ldcs(p.ts + i - 1)) p.unsorted[ri] = 1;
+                inwin = t - p.rank_clk[ri] >= p.ws;
+                if (inwin) {
+                    f0 = __ldcs(p.foff + i);
+                    f1 = __ldcs(p.foff + i + 1);
+                }
+            }
+            uint64_t ha = 0, hb = 0;
+            if (inwin) {
+                const uint64_t d = f1 - f0;
+                for (uint64_t j = f0 + gl; j < f1; j += G) {
+                    uint64_t pc = __ldcs(p.pc + j);
+                    uint32_t bn = __ldcs(p.bin + j);
+                    uint32_t key = resolve_frame(tabs, p.n_bins, pc, bn, p.mode, p.unk, p.err_bin);
+                    uint32_t pos = uint32_t(d - 1 - (j - f0));  // root-first position
+                    ha += term_a(key, pos);
+                    hb += term_b(key, pos);
+                }
+            }
+#pragma unroll
+            for (int o = G / 2; o > 0; o >>= 1) {
+                ha += __shfl_xor_sync(0xffffffffu, ha, o);
+                hb += __shfl_xor_sync(0xffffffffu, hb, o);
+            }
+            if (gl == 0 && inwin) {
+                const uint64_t rs = __ldg(p.rank_soff + ri);
+                if (f1 == f0) {
+                    atomicMin(p.err_empty + ri, (unsigned long long)(i - rs));
+                } else {
+                    uint64_t fa, fb;
+                    fp_finish(ha, hb, f1 - f0, fa, fb);
+                    if (!*(volatile int*)(p.tab_overflow + ri))
+                        agg_insert(p.slots + p.tab_off[ri], p.tab_mask[ri], fa, fb, uint32_t(i - rs), 1u,
+                                   p.tab_used + ri, p.tab_overflow + ri);
+                }
+                if (ri != cnt_rank) {
+                    if (in_cnt) atomicAdd(p.n_in + cnt_rank, in_cnt);
+                    in_cnt = 0;
+                    cnt_rank = ri;
+                }
+                ++in_cnt;
+            }
+        }
+        if (gl == 0 && in_cnt) atomicAdd(p.n_in + cnt_rank, in_cnt);
+    }
+}
+
+// Rare path: exact in-window timestamp regression check for ranks whose full
+// stream is not sorted (aggregate_samples samples.cpp:55-58 sees only the
+// in-window subsequence).  One thread per flagged rank.
+__global__ void k_regress_exact(int n, const int* ranks, const uint64_t* rank_soff, const int64_t* ts,
+                                const int64_t* clk, int64_t ws, unsigned long long* out) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    int r = ranks[t];
+    bool have = false;
+    int64_t prev = 0;
+    unsigned long long res = ~0ull;
+    for (uint64_t i = rank_soff[r]; i < rank_soff[r + 1]; ++i) {
+        int64_t v = ts[i];
+        if (v - clk[r] < ws) continue;
+        if (have && v < prev) {
+            res = i - rank_soff[r];
+            break;
+        }
+        have = true;
+        prev = v;
+    }
+    out[t] = res;
+}
+
+// ======================================================= fold: lines, seqs
+__global__ void k_compact_lines(int R, const uint64_t* tab_off, const uint32_t* tab_mask, const AggSlot* slots,
+                                const uint64_t* rank_soff, uint32_t* l_rank, uint64_t* l_hi, uint64_t* l_lo,
+                                uint32_t* l_count, uint64_t* l_rep, unsigned long long* n_out) {
+    int r = blockIdx.y;
+    uint32_t cap = tab_mask[r] + 1;
+    const AggSlot* T = slots + tab_off[r];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += gridDim.x * blockDim.x) {
+        AggSlot s = T[i];
+        if (s.hi == 0) continue;
+        unsigned long long o = atomicAdd(n_out, 1ull);
+        l_rank[o] = uint32_t(r);
+        l_hi[o] = s.hi;
+        l_lo[o] = s.lo;
+        l_count[o] = s.count;
+        l_rep[o] = rank_soff[r] + s.rep;
+    }
+}
+
+// Global dedupe of symbolized stacks across ranks: fingerprint -> sequence id.
+__global__ void k_seq_dedupe(uint64_t L, const uint64_t* l_hi, const uint64_t* l_lo, const uint64_t* l_rep,
+                             SeqSlot* T, uint64_t mask, unsigned* n_seq, uint32_t* l_gid, uint64_t* seq_rep,
+                             int* overflow) {
+    for (uint64_t l = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; l < L; l += uint64_t(gridDim.x) * blockDim.x) {
+        uint64_t fa = l_hi[l], fb = l_lo[l];
+        uint64_t i = mix_a(fa ^ fb) & mask;
+        uint32_t gid = 0xffffffffu;
+        for (uint64_t probe = 0; probe <= mask; ++probe) {
+            unsigned long long cur = *(volatile unsigned long long*)&T[i].hi;
+            if (cur == 0) {
+                cur = atomicCAS(&T[i].hi, 0ull, (unsigned long long)fa);
+                if (cur == 0) {
+                    gid = atomicAdd(n_seq, 1u);
+                    T[i].lo = fb;
+                    T[i].rep = l_rep[l];
+                    seq_rep[gid] = l_rep[l];
+                    __threadfence();
+                    atomicExch(&T[i].gid, gid);
+                    break;
+                }
+            }
+            if (cur == fa) {
+                unsigned g;
+                while ((g = *(volatile unsigned*)&T[i].gid) == 0xffffffffu) __nanosleep(16);
+                __threadfence();
+                if (*(volatile unsigned long long*)&T[i].lo == fb) {
+                    gid = g;
+                    break;
+                }
+            }
+            i = (i + 1) & mask;
+        }
+        if (gid == 0xffffffffu) *overflow = 1;
+        l_gid[l] = gid;
+    }
+}
+
+// Re-symbolize each distinct stack's representative sample into the arena,
+// root first (folded.cpp:24-26).  Warp per sequence.
+__global__ void k_seq_materialize(uint32_t G, const uint64_t* seq_rep, const uint64_t* seq_off,
+                                  const uint64_t* foff, const uint64_t* pc, const uint16_t* bin,
+                                  const DevTable* tabs_g, uint32_t n_bins, int mode, UnkSet unk, int* err_bin,
+                                  uint32_t* arena) {
+    __shared__ DevTable s_tabs[kMaxSmemBins];
+    for (uint32_t i = threadIdx.x; i < n_bins && i < kMaxSmemBins; i += blockDim.x) s_tabs[i] = tabs_g[i];
+    __syncthreads();
+    const DevTable* tabs = n_bins <= kMaxSmemBins ? s_tabs : tabs_g;
+    const int lane = threadIdx.x & 31;
+    for (uint64_t g = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; g < G;
+         g += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+        uint64_t s = seq_rep[g];
+        uint64_t f0 = foff[s], f1 = foff[s + 1];
+        uint64_t d = f1 - f0;
+        uint32_t* out = arena + seq_off[g];
+        for (uint64_t pos = lane; pos < d; pos += 32) {
+            uint64_t j = f1 - 1 - pos;
+            out[pos] = resolve_frame(tabs, n_bins, pc[j], bin[j], mode, unk, err_bin);
+        }
+    }
+}
+
+__global__ void k_unk_compact(uint32_t cap, const UnkSlot* slots, uint32_t* o_slot, uint32_t* o_bin, uint64_t* o_pc,
+                              unsigned* n_out) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += gridDim.x * blockDim.x) {
+        uint32_t b = slots[i].bin1;
+        if (b == 0 || b == 0xffffffffu) continue;
+        unsigned o = atomicAdd(n_out, 1u);
+        o_slot[o] = i;
+        o_bin[o] = b - 1;
+        o_pc[o] = slots[i].pc;
+    }
+}
+
+// Final name rank: real name i -> i + #{unknown labels < name i}; unknown slot ->
+// its label's merged rank (host-computed).
+// pos_sorted holds, for every distinct label that is not itself a real name, the
+// number of real names below it; a real name i therefore moves up by
+// upper_bound(pos_sorted, i).
+__device__ __forceinline__ uint32_t remap_key(uint32_t e, const uint32_t* unk_final, const uint32_t* pos_sorted,
+                                              uint32_t n_pos) {
+    if (e & kUnknownBit) return unk_final[e & ~kUnknownBit];
+    uint32_t lo = 0, hi = n_pos;  // upper_bound(pos_sorted, e)
+    while (lo < hi) {
+        uint32_t m = (lo + hi) >> 1;
+        if (pos_sorted[m] <= e) lo = m + 1; else hi = m;
+    }
+    return e + lo;
+}
+
+__global__ void k_remap(uint64_t n, uint32_t* arena, const uint32_t* unk_final, const uint32_t* pos_sorted,
+                        uint32_t n_pos) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        arena[i] = remap_key(arena[i], unk_final, pos_sorted, n_pos);
+}
+
+__global__ void k_fill_gid(SeqSlot* s, uint64_t n) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        s[i].gid = 0xffffffffu;
+}
+__global__ void k_seq_len64(uint32_t G, const uint64_t* seq_rep, const uint64_t* foff, uint64_t* len) {
+    for (uint64_t g = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; g < G; g += uint64_t(gridDim.x) * blockDim.x) {
+        uint64_t s = seq_rep[g];
+        len[g] = foff[s + 1] - foff[s];
+    }
+}
+__global__ void k_dense_final(uint64_t n, const uint32_t* used, const uint32_t* used_scan, uint32_t* dense_final) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        if (used[i]) dense_final[used_scan[i]] = uint32_t(i);
+}
+// symbolize verb: frame-wise keys (resolve_stacks symrepo.cpp:122-143)
+__global__ void k_resolve(uint64_t n, const uint64_t* pc, const uint16_t* bin, const DevTable* tabs_g,
+                          uint32_t n_bins, int mode, UnkSet unk, int* err_bin, uint32_t* out) {
+    __shared__ DevTable s_tabs[kMaxSmemBins];
+    for (uint32_t i = threadIdx.x; i < n_bins && i < kMaxSmemBins; i += blockDim.x) s_tabs[i] = tabs_g[i];
+    __syncthreads();
+    const DevTable* tabs = n_bins <= kMaxSmemBins ? s_tabs : tabs_g;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        out[i] = resolve_frame(tabs, n_bins, pc[i], bin[i], mode, unk, err_bin);
+}
+
+// Lexicographic order of name-rank sequences, shorter prefix first — the order
+// of std::map<std::vector<std::string>, ...> (folded.cpp:11-19).
+struct SeqLess {
+    const uint32_t* arena;
+    const uint64_t* off;
+    __device__ __forceinline__ int cmp(uint32_t a, uint32_t b) const {
+        const uint32_t* x = arena + off[a];
+        const uint32_t* y = arena + off[b];
+        uint64_t la = off[a + 1] - off[a], lb = off[b + 1] - off[b];
+        uint64_t n = la < lb ? la : lb;
+        for (uint64_t i = 0; i < n; ++i) {
+            uint32_t u = x[i], v = y[i];
+            if (u != v) return u < v ? -1 : 1;
+        }
+        return la < lb ? -1 : (la > lb ? 1 : 0);
+    }
+    __device__ __forceinline__ bool operator()(const uint32_t& a, const uint32_t& b) const { return cmp(a, b) < 0; }
+};
+
+__global__ void k_seq_rankflags(uint32_t G, const uint32_t* sorted, SeqLess less, uint32_t* flag) {
+    for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < G; p += uint64_t(gridDim.x) * blockDim.x)
+        flag[p] = p == 0 ? 1u : (less.cmp(sorted[p - 1], sorted[p]) != 0 ? 1u : 0u);
+}
+__global__ void k_seq_rankset(uint32_t G, const uint32_t* sorted, const uint32_t* incl_scan, uint32_t* seq_rank,
+                              uint32_t* dense_rep) {
+    for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < G; p += uint64_t(gridDim.x) * blockDim.x) {
+        uint32_t d = incl_scan[p] - 1;
+        seq_rank[sorted[p]] = d;
+        if (p == 0 || incl_scan[p - 1] != incl_scan[p]) dense_rep[d] = sorted[p];
+    }
+}
+
+__global__ void k_line_keys(uint64_t L, const uint32_t* l_rank, const uint32_t* l_gid, const uint32_t* seq_rank,
+                            uint64_t* lkey) {
+    for (uint64_t l = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; l < L; l += uint64_t(gridDim.x) * blockDim.x)
+        lkey[l] = (uint64_t(l_rank[l]) << 32) | seq_rank[l_gid[l]];
+}
+
+__global__ void k_line_bounds(int R, const uint64_t* lkey, uint64_t L, uint64_t* line_off) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r <= R; r += gridDim.x * blockDim.x) {
+        uint64_t key = uint64_t(r) << 32;
+        uint64_t a = 0, b = L;
+        while (a < b) {
+            uint64_t m = (a + b) >> 1;
+            if (lkey[m] < key) a = m + 1; else b = m;
+        }
+        line_off[r] = a;
+    }
+}
+
+// ============================================================ stage c: diff
+// Distinct names of each dense sequence (a name repeated in a stack counts once,
+// folded.cpp:49).  Warp per sequence; first pass counts, second writes.
+template <bool WRITE>
+__global__ void k_seq_distinct(uint32_t S, const uint32_t* dense_rep, const uint64_t* seq_off, const uint32_t* arena,
+                               uint32_t* cnt, const uint64_t* dn_off, uint32_t* dn) {
+    const int lane = threadIdx.x & 31;
+    for (uint64_t s = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; s < S;
+         s += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+        uint32_t g = dense_rep[s];
+        const uint32_t* x = arena + seq_off[g];
+        uint64_t d = seq_off[g + 1] - seq_off[g];
+        uint32_t base = 0;
+        for (uint64_t p0 = 0; p0 < d; p0 += 32) {
+            uint64_t p = p0 + lane;
+            bool first = false;
+            uint32_t v = 0;
+            if (p < d) {
+                v = x[p];
+                first = true;
+                for (uint64_t q = 0; q < p; ++q)
+                    if (x[q] == v) { first = false; break; }
+            }
+            unsigned m = __ballot_sync(0xffffffffu, first);
+            if (WRITE && first) dn[dn_off[s] + base + __popc(m & ((1u << lane) - 1))] = v;
+            base += __popc(m);
+        }
+        if (!WRITE && lane == 0) cnt[s] = base;
+    }
+}
+
+__global__ void k_mark_used(uint64_t n, const uint32_t* dn, uint32_t* used) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        used[dn[i]] = 1;
+}
+__global__ void k_dense_names(uint64_t n, uint32_t* dn, const uint32_t* used_scan) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        dn[i] = used_scan[dn[i]];  // exclusive scan -> dense index
+}
+
+// Inclusive counts per (rank, name): warp per folded line adds its count to each
+// distinct name of its sequence (exact integers; fraction = count / total).
+__global__ void k_incl(uint64_t L, const uint64_t* lkey, const unsigned long long* lcount, const uint64_t* dn_off,
+                       const uint32_t* dn, uint64_t F, unsigned long long* incl) {
+    const int lane = threadIdx.x & 31;
+    for (uint64_t l = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; l < L;
+         l += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+        uint64_t key = lkey[l];
+        uint32_t r = uint32_t(key >> 32), s = uint32_t(key);
+        unsigned long long c = lcount[l];
+        unsigned long long* row = incl + uint64_t(r) * F;
+        for (uint64_t k = dn_off[s] + lane; k < dn_off[s + 1]; k += 32) atomicAdd(row + dn[k], c);
+    }
+}
+
+// compute_waterline (diagnosis.cpp:35-55) per name over the CPU ranks: present
+// fractions in rank order then zeros appended, population sigma; flag_ranks
+// (:57-71) strictly above mean + k sigma.
+__global__ void k_waterline(uint64_t F, const uint32_t* rows, int R, const unsigned long long* incl,
+                            const uint64_t* totals, double* mean, double* sd, uint8_t* present_any) {
+    for (uint64_t f = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; f < F; f += uint64_t(gridDim.x) * blockDim.x) {
+        double acc = 0.0;
+        int np = 0;
+        for (int i = 0; i < R; ++i) {
+            uint32_t r = rows[i];
+            unsigned long long c = incl[uint64_t(r) * F + f];
+            if (c) {
+                acc = __dadd_rn(acc, __ddiv_rn(double(c), double(totals[r])));
+                ++np;
+            }
+        }
+        present_any[f] = np > 0;
+        double mu = __ddiv_rn(acc, double(R));
+        double s2 = 0.0;
+        for (int i = 0; i < R; ++i) {
+            uint32_t r = rows[i];
+            unsigned long long c = incl[uint64_t(r) * F + f];
+            if (c) {
+                double d = __dsub_rn(__ddiv_rn(double(c), double(totals[r])), mu);
+                s2 = __dadd_rn(s2, __dmul_rn(d, d));
+            }
+        }
+        for (int i = np; i < R; ++i) s2 = __dadd_rn(s2, __dmul_rn(mu, mu));
+        mean[f] = mu;
+        sd[f] = __dsqrt_rn(__ddiv_rn(s2, double(R)));
+    }
+}
+
+__global__ void k_flag(uint64_t F, const uint32_t* rows, int R, const unsigned long long* incl,
+                       const uint64_t* totals, double k, const double* mean, const double* sd, uint32_t* o_r,
+                       uint32_t* o_f, double* o_frac, double* o_thr, unsigned long long* n_out,
+                       unsigned long long cap) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < F * uint64_t(R);
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        uint64_t r = rows[i / F], f = i % F;
+        unsigned long long c = incl[r * F + f];
+        if (!c) continue;
+        double fr = __ddiv_rn(double(c), double(totals[r]));
+        double thr = __dadd_rn(mean[f], __dmul_rn(k, sd[f]));
+        if (fr > thr) {
+            unsigned long long o = atomicAdd(n_out, 1ull);
+            if (o < cap) {
+                o_r[o] = uint32_t(r);
+                o_f[o] = uint32_t(f);
+                o_frac[o] = fr;
+                o_thr[o] = thr;
+            }
+        }
+    }
+}
+
+// Per-sequence merged counts for the temporal route (diagnosis.cpp:396-402).
+__global__ void k_seq_counts(uint64_t L, const uint64_t* lkey, const unsigned long long* lcount, unsigned long long* sc) {
+    for (uint64_t l = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; l < L; l += uint64_t(gridDim.x) * blockDim.x)
+        atomicAdd(sc + uint32_t(lkey[l]), lcount[l]);
+}
+
+// Hottest path (diagnosis.cpp:184-193 / 413-420): first line in order with the
+// strictly greatest count among lines containing dense name f.
+// Pass 0: best[0] = max count; pass 1: best[1] = first position with that count.
+__global__ void k_hottest(uint64_t n, const uint64_t* seq_of, const unsigned long long* cnt_of, int seq_is_index,
+                          const uint64_t* dn_off, const uint32_t* dn, uint32_t f, int pass,
+                          unsigned long long* best) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        unsigned long long c = cnt_of[i];
+        if (c == 0) continue;
+        if (pass == 1 && c != best[0]) continue;
+        uint32_t s = seq_is_index ? uint32_t(i) : uint32_t(seq_of[i]);
+        bool has = false;
+        for (uint64_t k = dn_off[s]; k < dn_off[s + 1]; ++k)
+            if (dn[k] == f) { has = true; break; }
+        if (!has) continue;
+        if (pass == 0)
+            atomicMax(best, c);
+        else
+            atomicMin(best + 1, (unsigned long long)i);
+    }
+}
+
+// Exact inclusive fractions in the reference's summation order
+// (folded.cpp:45-54): (name, line) pairs sorted, then one sequential sum of
+// double(count)/double(total) per name in line order.
+__global__ void k_pair_count(uint64_t n, const uint64_t* lkey, const uint64_t* dn_off, uint64_t* cnt) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        uint32_t s = lkey ? uint32_t(lkey[i]) : uint32_t(i);
+        cnt[i] = dn_off[s + 1] - dn_off[s];
+    }
+}
+__global__ void k_pair_emit(uint64_t n, const uint64_t* lkey, const uint64_t* dn_off, const uint32_t* dn,
+                            const uint64_t* pair_off, uint64_t* keys, uint32_t* line) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        uint32_t s = lkey ? uint32_t(lkey[i]) : uint32_t(i);
+        uint64_t o = pair_off[i];
+        for (uint64_t k = dn_off[s]; k < dn_off[s + 1]; ++k, ++o) {
+            keys[o] = (uint64_t(dn[k]) << 32) | uint32_t(i);
+            line[o] = uint32_t(i);
+        }
+    }
+}
+__global__ void k_pair_segflags(uint64_t np, const uint64_t* keys, uint32_t* flag) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < np; i += uint64_t(gridDim.x) * blockDim.x)
+        flag[i] = i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32);
+}
+__global__ void k_pair_segsum(uint64_t nseg, const uint32_t* seg, uint64_t np, const uint64_t* keys,
+                              const unsigned long long* cnt_of, uint64_t total, uint32_t* out_f, double* out_v) {
+    for (uint64_t g = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; g < nseg; g += uint64_t(gridDim.x) * blockDim.x) {
+        uint64_t a = seg[g], b = g + 1 < nseg ? seg[g + 1] : np;
+        double acc = 0.0, t = __ull2double_rn(total);
+        for (uint64_t i = a; i < b; ++i)
+            acc = __dadd_rn(acc, __ddiv_rn(__ull2double_rn(cnt_of[uint32_t(keys[i])]), t));
+        out_f[g] = uint32_t(keys[a] >> 32);
+        out_v[g] = acc;
+    }
+}
+
+__global__ void k_u32_to_u64(uint64_t n, const uint32_t* a, unsigned long long* b) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        b[i] = a[i];
+}
+__global__ void k_clk_of_cpu(int R, const int32_t* rank_ids, const int64_t* off, int64_t* clk) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) clk[r] = off[rank_ids[r]];
+}
+
+}  // namespace
+
+void launch_build_buckets(const uint64_t* starts, uint32_t n, uint64_t base, uint32_t shift, uint32_t nb,
+                          uint32_t* bucket, cudaStream_t s) {
+    k_build_buckets<<<grid_for(uint64_t(nb) + 1), kThreads, 0, s>>>(starts, n, base, shift, nb, bucket);
+    STG_CUDA(cudaGetLastError());
+}
+
+}  // namespace stg
+
+#include "stg_runner.inl"
+#include "stg_output.inl"

@@ -1,0 +1,197 @@
+"""Seeded synthetic analysis windows (SURVEY.md §8(d) C1 shape), numpy only.
+
+Used by tests, smoke() and bench.py.  Produces an abi.Window with SYMR symbol
+tables, CPU stack samples with a Zipf stack mix, per-iteration AllReduce events
+with per-rank clock skew, GPU kernel events, 5 s OS counter windows, and an
+optional straggler rank (softirq path in its stacks, +0.6 ms collective entry
+delay, NET_RX storm) — mirroring the fault model of the reference simulator
+(simulate.cpp:164-182, 272-305) without depending on it.
+"""
+from __future__ import annotations
+
+import hashlib
+import struct
+
+import numpy as np
+
+from paper_2603_29235_b200.abi import Window
+
+SIM_APP = ["main", "train_loop", "forward_pass", "matmul_dispatch", "softmax_dispatch",
+           "backward_pass", "matmul_grad_dispatch", "bias_grad_dispatch", "allreduce_wait",
+           "optimizer_step", "data_loader_next", "checkpoint_maybe", "log_metrics",
+           "SLS::LogClient::Send", "SLS::LogClient::Serialize", "cpfs_checkpoint_write",
+           "cpfs_write_block", "ossutils_download", "oss_http_get", "open64", "stat64", "unlink"]
+SIM_KERNEL = ["asm_common_interrupt", "common_interrupt", "irq_exit_rcu", "__do_softirq",
+              "net_rx_action", "napi_poll", "virtnet_poll", "virtnet_receive", "napi_gro_receive",
+              "do_sys_openat2", "path_openat", "d_alloc_parallel", "queued_spin_lock_slowpath",
+              "vfs_statx", "filename_lookup", "do_unlinkat", "d_invalidate"]
+SOFTIRQ = SIM_KERNEL[:9]
+KERNELS = ["dropout_kernel", "fused_matmul", "layernorm_kernel", "nccl_all_reduce", "softmax_kernel"]
+COUNTERS = ["LOC", "NET_RX", "PCI-MSI-eth0", "RCU", "TIMER"]
+
+
+def build_id(label: str) -> bytes:
+    return hashlib.sha1(label.encode()).digest()
+
+
+def pack_symr(bid: bytes, starts, sizes, names) -> bytes:
+    """SYMR layout (symfile.hpp:13-18): header, sorted entries, u16-prefixed names."""
+    order = np.argsort(np.asarray(starts, np.uint64), kind="stable")
+    starts = np.asarray(starts, np.uint64)[order]
+    sizes = np.asarray(sizes, np.uint32)[order]
+    names = [names[i] for i in order]
+    enc = [n.encode() if isinstance(n, str) else n for n in names]
+    lens = np.array([len(e) for e in enc], np.int64)
+    offs = np.zeros(len(enc), np.uint32)
+    if len(enc):
+        offs[1:] = np.cumsum(lens + 2)[:-1]
+    n = len(enc)
+    ent = np.zeros(n, dtype=[("s", "<u8"), ("z", "<u4"), ("o", "<u4")])
+    ent["s"], ent["z"], ent["o"] = starts, sizes, offs
+    strtab = b"".join(struct.pack("<H", len(e)) + e for e in enc)
+    return b"SYMR" + struct.pack("<I", 1) + bid + struct.pack("<II", n, 36 + 16 * n) + ent.tobytes() + strtab
+
+
+def small_window(seed: int = 1, ranks: int = 8, samples_per_rank: int = 2000, slow_rank: int = 4,
+                 depth: int = 12, n_sym: int = 2000, pool: int = 200, unknown_frac: float = 0.01,
+                 iterations: int = 100, softirq_share: float = 0.0174, entry_delay_ns: int = 600_000,
+                 extra_bins: int = 0) -> Window:
+    """C1-shaped window; slow_rank < 0 gives a healthy window."""
+    rng = np.random.default_rng(seed)
+    # ---- one application binary: symbols at 0x1000 + 64 i, size 48 (25 % gap)
+    names = SIM_APP + SIM_KERNEL + [f"fn_{i}" for i in range(max(0, n_sym - len(SIM_APP) - len(SIM_KERNEL)))]
+    n_sym = len(names)
+    starts = 0x1000 + 64 * np.arange(n_sym, dtype=np.uint64)
+    sizes = np.full(n_sym, 48, np.uint32)
+    bid = build_id(f"app-{seed}")
+    symr = [pack_symr(bid, starts, sizes, names)]
+    bids = [bid]
+    for e in range(extra_bins):  # binaries without a symbol file: unknown labels
+        bids.append(build_id(f"jit-{seed}-{e}"))
+    idx = {n: i for i, n in enumerate(names)}
+    # ---- stack pool (leaf-first lists of (bin, pc)); root is main;train_loop
+    stacks = []
+    for p in range(pool):
+        d = int(rng.integers(max(3, depth - 4), depth + 5))
+        mid = rng.integers(len(SIM_APP) + len(SIM_KERNEL), n_sym, size=d - 2)
+        fr = [(0, int(starts[idx["main"]]) + 8), (0, int(starts[idx["train_loop"]]) + 8)]
+        for m in mid:
+            off = int(starts[m]) + (56 if rng.random() < unknown_frac else int(rng.integers(0, 48)))
+            b = 0
+            if extra_bins and rng.random() < 0.02:
+                b = int(rng.integers(1, 1 + extra_bins))
+            fr.append((b, off))
+        stacks.append(fr[::-1])
+    soft = [(0, int(starts[idx[n]]) + 4) for n in SOFTIRQ][::-1]
+    zipf_w = 1.0 / np.arange(1, pool + 1) ** 1.1
+    zipf_w /= zipf_w.sum()
+    # ---- clocks
+    period = 10_101_000 // 8  # ns between samples
+    span = samples_per_rank * period
+    iter_ns = span // iterations
+    skews = rng.integers(-10_000_000, 10_000_001, size=ranks)
+    ws = int(iter_ns * 5)  # analysis window starts after 5 iterations (true time)
+    we = int(span)
+    rank_ids = np.arange(ranks, dtype=np.int32)
+    ts_all, foff, pcs, bins_ = [], [0], [], []
+    rank_off = [0]
+    for r in range(ranks):
+        perm = rng.permutation(pool)
+        choice = perm[rng.choice(pool, size=samples_per_rank, p=zipf_w)]
+        t = np.cumsum(np.full(samples_per_rank, period) * (1 + rng.uniform(-0.02, 0.02, samples_per_rank)))
+        t = t.astype(np.int64) + int(skews[r])
+        for i in range(samples_per_rank):
+            if r == slow_rank and rng.random() < softirq_share:
+                fr = soft
+            else:
+                fr = stacks[int(choice[i])]
+            for b, o in fr:
+                bins_.append(b)
+                pcs.append(o)
+            foff.append(len(pcs))
+        ts_all.append(t)
+        rank_off.append(rank_off[-1] + samples_per_rank)
+    # ---- collectives: one AllReduce per iteration, barrier exit shared
+    c_rank, c_entry, c_exit = [], [], []
+    g_rank, g_kern, g_start, g_dur = [], [], [], []
+    for k in range(iterations):
+        t0 = k * iter_ns
+        barrier = t0 + int(iter_ns * 0.8)
+        for r in range(ranks):
+            comp = int(iter_ns * 0.7) + int(rng.normal(0, 50_000))
+            delay = entry_delay_ns if r == slow_rank else 0
+            entry = t0 + comp + delay
+            ex = max(barrier, entry + 1000) + int(rng.integers(-25_000, 25_001))
+            c_rank.append(r)
+            c_entry.append(entry + int(skews[r]))
+            c_exit.append(max(ex, entry + 1) + int(skews[r]))
+            ks = t0
+            for kk, share in ((1, 0.48), (4, 0.19), (0, 0.15), (2, 0.18)):
+                du = int(share * comp * np.exp(rng.normal(0, 0.01)))
+                g_rank.append(r)
+                g_kern.append(kk)
+                g_start.append(ks + int(skews[r]))
+                g_dur.append(du)
+                ks += du
+            g_rank.append(r)
+            g_kern.append(3)
+            g_start.append(entry + int(skews[r]))
+            g_dur.append(max(0, barrier - entry))
+    # ---- OS counters, 5 s windows on the rank clock
+    o_rank, o_ws, o_p50, o_p99, o_mig = [], [], [], [], []
+    irq_off, irq_k, irq_v, sirq_off, sirq_k, sirq_v = [0], [], [], [0], [], []
+    for r in range(ranks):
+        storm = r == slow_rank
+        for wnd in range(int(np.ceil(we / 5e9)) or 1):
+            j = lambda: rng.uniform(0.98, 1.02)
+            o_rank.append(r)
+            o_ws.append(wnd * 5_000_000_000 + int(skews[r]))
+            o_p50.append(int(50_000 * j()))
+            o_p99.append(int(400_000 * j() * (6 if storm else 1)))
+            o_mig.append(int(5 * j()))
+            irq_k += [0, 2]
+            irq_v += [int(10000 * j()), int(2000 * j() * (8 if storm else 1))]
+            irq_off.append(len(irq_k))
+            sirq_k += [4, 3, 1]
+            sirq_v += [int(8000 * j()), int(6000 * j()), int(5000 * j() * (10 if storm else 1))]
+            sirq_off.append(len(sirq_k))
+    w = Window()
+    w.window_start_ns, w.window_end_ns, w.max_skew_ns = ws, we, 50_000_000
+    w.rank_ids = rank_ids
+    w.rank_sample_off = np.asarray(rank_off, np.uint64)
+    w.bin_build_ids = np.frombuffer(b"".join(bids), np.uint8).reshape(-1, 20).copy()
+    w.sample_ts = np.concatenate(ts_all).astype(np.int64)
+    w.sample_frame_off = np.asarray(foff, np.uint64)
+    w.frame_pc = np.asarray(pcs, np.uint64)
+    w.frame_bin = np.asarray(bins_, np.uint16)
+    n = len(c_rank)
+    w.coll_rank = np.asarray(c_rank, np.int32)
+    w.coll_group = np.zeros(n, np.int32)
+    w.coll_kind = np.zeros(n, np.uint8)
+    w.coll_entry = np.asarray(c_entry, np.int64)
+    w.coll_exit = np.asarray(c_exit, np.int64)
+    w.coll_gpu_dur = w.coll_exit - w.coll_entry
+    w.group_ranks = rank_ids.copy()
+    w.gpu_rank = np.asarray(g_rank, np.int32)
+    w.gpu_kernel = np.asarray(g_kern, np.uint32)
+    w.gpu_start = np.asarray(g_start, np.int64)
+    w.gpu_dur = np.asarray(g_dur, np.int64)
+    w.kernel_names = list(KERNELS)
+    w.os_rank = np.asarray(o_rank, np.int32)
+    w.os_window_start = np.asarray(o_ws, np.int64)
+    w.os_p50 = np.asarray(o_p50, np.int64)
+    w.os_p99 = np.asarray(o_p99, np.int64)
+    w.os_migrations = np.asarray(o_mig, np.int64)
+    w.os_irq_off = np.asarray(irq_off, np.uint64)
+    w.os_irq_key = np.asarray(irq_k, np.uint32)
+    w.os_irq_val = np.asarray(irq_v, np.int64)
+    w.os_sirq_off = np.asarray(sirq_off, np.uint64)
+    w.os_sirq_key = np.asarray(sirq_k, np.uint32)
+    w.os_sirq_val = np.asarray(sirq_v, np.int64)
+    w.counter_names = list(COUNTERS)
+    w.has_baseline = True
+    w.baseline_delta = 0.005
+    w.baseline = {"main": 1.0, "train_loop": 1.0}
+    w.baseline_iteration_ms = iter_ns / 1e6
+    w.symr = symr
+    return w

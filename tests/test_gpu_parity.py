@@ -1,0 +1,97 @@
+"""GPU parity: libstg (C-ABI) vs the oracle on identical windows.
+
+Bar: folded lines, counts, totals, symbol names, lateness, GPU/OS sums, flagged
+ranks, verdicts and top paths are bit-exact; floating-point scores (fractions,
+z-scores, evidence values) agree within 1e-6 relative (north_star tolerance).
+"""
+import numpy as np
+import pytest
+
+from oracle import ref, strata_oracle as so
+from tests.compare import assert_close
+from tests.synth import small_window
+
+pytestmark = pytest.mark.gpu
+REL = 1e-6  # north_star: floating-point scores within 1e-6 relative
+
+
+def _check_window(ctx, win, against_ref=False):
+    stats = ctx.window_run(win)
+    gd = ctx.groupdata()
+    rep = ctx.report()
+    if against_ref:
+        r, _, _ = ref.window_run(win)
+        ogd, orep = r["groupdata"], r["report"]
+    else:
+        ogd, orep = so.window_pipeline(win)
+    # integer / string / order results: exact
+    assert gd["cpu_profiles"] == ogd["cpu_profiles"]
+    assert gd["gpu_profiles"] == ogd["gpu_profiles"]
+    assert gd["os_snapshots"] == ogd["os_snapshots"]
+    assert rep["verdict"] == orep["verdict"]
+    assert rep["flagged_ranks"] == orep["flagged_ranks"]
+    assert rep["top_path"] == orep["top_path"]
+    assert rep["reference_rank"] == orep["reference_rank"]
+    assert rep["notes"] == orep["notes"]
+    # lateness and iteration times are computed in the reference's FP order
+    assert gd["lateness_per_instance"] == ogd["lateness_per_instance"]
+    assert gd["iteration_times_ms"] == ogd["iteration_times_ms"]
+    assert_close(gd, ogd, REL)
+    assert_close(rep, orep, 0.0)  # the report is bit-exact (reference FP order)
+    return stats, rep
+
+
+@pytest.mark.parametrize("seed,slow", [(7, 3), (1, 4), (2, -1), (3, 0)])
+def test_synthetic_window_matches_oracle(ctx, seed, slow):
+    win = small_window(seed=seed, ranks=8, samples_per_rank=600, slow_rank=slow)
+    _check_window(ctx, win)
+
+
+def test_unknown_binaries_and_gaps(ctx):
+    win = small_window(seed=11, ranks=6, samples_per_rank=500, slow_rank=2, unknown_frac=0.2, extra_bins=2)
+    stats, _ = _check_window(ctx, win)
+    assert stats["n_unknown"] > 0
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("scenario", ["healthy", "thermal", "softirq", "dentry-lock", "logging",
+                                      "io-bottleneck"])
+@pytest.mark.parametrize("seed", [1, 2])
+def test_simulator_scenarios_match_reference(ctx, scenario, seed):
+    win = ref.simulate(scenario, seed)
+    _, rep = _check_window(ctx, win, against_ref=True)
+    lab = win.labels
+    if seed == 1:
+        assert rep["verdict"] == lab["verdict"]
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+def test_simulator_1024_ranks(ctx):
+    win = ref.simulate("softirq", 5, ranks=1024, iterations=150)
+    _check_window(ctx, win, against_ref=True)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_resolve_matches_lookup(ctx, mode):
+    rng = np.random.default_rng(5)
+    from tests.synth import build_id, pack_symr
+    n = 5000
+    starts = np.unique(rng.integers(0, 1 << 40, size=n).astype(np.uint64))
+    sizes = rng.integers(0, 4096, size=len(starts)).astype(np.uint32)
+    names = [f"s{i}_{rng.integers(0, 1 << 30)}" for i in range(len(starts))]
+    bid = build_id("resolve-test")
+    symr = pack_symr(bid, starts, sizes, names)
+    ctx.ingest(symr)
+    f = so.SymbolFile.parse(symr)
+    q = np.concatenate([starts[rng.integers(0, len(starts), 3000)] + rng.integers(0, 5000, 3000).astype(np.uint64),
+                        rng.integers(0, 1 << 41, 2000).astype(np.uint64), starts[:10], np.array([0], np.uint64)])
+    other = build_id("absent")
+    bins = (rng.random(len(q)) < 0.05).astype(np.uint16)
+    names_gpu, _ = ctx.resolve(q, bins, np.frombuffer(bid + other, np.uint8))
+    repo = so.Repo([symr])
+    exp = [repo.resolve_frame(bid if b == 0 else other, int(o), mode).decode() for o, b in zip(q, bins)]
+    if mode == 0:
+        assert names_gpu == exp
+    else:
+        names_gpu, _ = ctx.resolve(q, bins, np.frombuffer(bid + other, np.uint8), mode=1)
+        assert names_gpu == exp
