@@ -1,0 +1,380 @@
+#!/usr/bin/env python3
+"""bench.py — stack samples/s symbolized + aggregated + diffed (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], "C2"): per GPU, 128 ranks x 1M CPU stack
+samples, 64-frame stacks over three 1M-symbol tables (python, libtorch, cuda),
+50k distinct symbolized stacks per rank drawn Zipf(1.1), leaf PCs uniform
+inside their function, a straggler rank (softirq path + 0.6 ms late collective
+entry), 100 AllReduce instances, GPU kernel and OS counter streams.  One step =
+one full window through libstg: collective alignment -> fused symbolize +
+aggregate -> fold/sort -> inclusive fractions / diff -> verdict.  Inputs are
+resident in HBM (84 GB per GPU >> 126 MB L2, so no L2 flush is needed).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--ranks R] [--spr S] [--no-e2e] [--no-cpu-baseline]
+
+N > 1: launched by torchrun, one process per GPU; each GPU analyses its own
+128-rank communication group (weak scaling); timing is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "stack samples/sec symbolized+aggregated+diffed"
+UNIT = "samples/s"
+PEAKS = ROOT / "MEASURED_PEAKS.json"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def args_parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--ranks", type=int, default=128)
+    p.add_argument("--spr", type=int, default=1_000_000, help="samples per rank")
+    p.add_argument("--depth", type=int, default=64)
+    p.add_argument("--pool", type=int, default=50_000)
+    p.add_argument("--nsym", type=int, default=1_000_000)
+    p.add_argument("--seed", type=int, default=42)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-budget-s", type=float, default=20.0)
+    return p.parse_args()
+
+
+# --------------------------------------------------------------------- data
+class Workload:
+    """Symbol tables (host, SYMR) + side streams; samples generated on device."""
+
+    def __init__(self, a, group_index: int):
+        from tests.synth import c2_tables, side_streams
+        self.a = a
+        self.tables = c2_tables(a.seed, a.nsym)
+        rng = np.random.default_rng(a.seed * 1000 + group_index)
+        self.period = 10_000  # ns between samples of a rank
+        self.span = a.spr * self.period
+        self.iterations = 100
+        self.iter_ns = self.span // self.iterations
+        self.skews = rng.integers(-10_000_000, 10_000_001, size=a.ranks).astype(np.int64)
+        self.rank_base = group_index * a.ranks
+        self.slow = 4 if a.ranks > 4 else 0
+        self.side = side_streams(rng, a.ranks, self.iterations, self.iter_ns, self.span, self.slow,
+                                 self.skews, rank_base=self.rank_base)
+        w = np.arange(1, a.pool + 1, dtype=np.float64) ** -1.1
+        self.zipf_cdf = np.cumsum(w / w.sum())
+        self.zipf_cdf[-1] = 1.0
+
+    def generate(self, torch, ranks: int, spr: int, seed_off: int = 0, period: int = 0):
+        """Device tensors (ts, foff, pc, bin) for `ranks` x `spr` samples."""
+        a = self.a
+        lib = C.CDLL(str(ROOT / "paper_2603_29235_b200" / "libstg_bench.so"))
+        dev = torch.device("cuda")
+        n = ranks * spr
+        ts = torch.empty(n, dtype=torch.int64, device=dev)
+        foff = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        pc = torch.empty(n * a.depth, dtype=torch.int64, device=dev)
+        bn = torch.empty(n * a.depth, dtype=torch.int16, device=dev)
+        st = [torch.from_numpy(t[1].view(np.int64)).to(dev) for t in self.tables]
+        sz = [torch.from_numpy(t[2].view(np.int32)).to(dev) for t in self.tables]
+        cdf = torch.from_numpy(self.zipf_cdf).to(dev)
+        skew = torch.from_numpy(self.skews[:ranks].copy()).to(dev)
+        soft = self.tables[2][1][:9] + 4
+        P = C.c_void_p
+        starts = (P * 3)(*[t.data_ptr() for t in st])
+        sizes = (P * 3)(*[t.data_ptr() for t in sz])
+        nsym = (C.c_uint32 * 3)(*[a.nsym] * 3)
+        hot = (C.c_uint32 * 3)(5000, 20000, 5000)
+        softa = (C.c_uint64 * 9)(*[int(x) for x in soft])
+        lib.bench_gen_c2.argtypes = [C.c_uint64, C.c_int, C.c_uint64, C.c_int, C.c_uint32, P, P, P, P, P, P,
+                                     C.c_int, C.c_double, C.c_uint32, C.c_int64, P, P, P, P, P, P]
+        rc = lib.bench_gen_c2(a.seed + seed_off, ranks, spr, a.depth, a.pool, cdf.data_ptr(),
+                              C.cast(starts, P), C.cast(sizes, P), C.cast(nsym, P), C.cast(hot, P),
+                              C.cast(softa, P), self.slow if self.slow < ranks else -1, 0.0174, 100,
+                              period or self.period, skew.data_ptr(), ts.data_ptr(), foff.data_ptr(), pc.data_ptr(),
+                              bn.data_ptr(), P(torch.cuda.current_stream().cuda_stream))
+        assert rc == 0, f"generator failed: {rc}"
+        torch.cuda.synchronize()
+        return ts, foff, pc, bn
+
+    def window(self, ranks: int, spr: int, arrays, memory: int):
+        from paper_2603_29235_b200.abi import Window
+        from tests.synth import apply_side
+        a = self.a
+        w = Window()
+        w.memory = memory
+        w.window_start_ns = int(self.iter_ns * 5)
+        w.window_end_ns = int(self.span)
+        w.max_skew_ns = 50_000_000
+        w.rank_ids = np.arange(self.rank_base, self.rank_base + ranks, dtype=np.int32)
+        w.rank_sample_off = (np.arange(ranks + 1, dtype=np.uint64) * spr)
+        jit = bytes(20 * [0x7f])
+        w.bin_build_ids = np.frombuffer(b"".join(t[0] for t in self.tables) + jit, np.uint8).reshape(-1, 20)
+        w.sample_ts, w.sample_frame_off, w.frame_pc, w.frame_bin = arrays
+        w.n_samples_ = ranks * spr
+        w.n_frames_ = ranks * spr * a.depth
+        if ranks == a.ranks:
+            apply_side(w, self.side, ranks)
+        else:  # bounded sample: keep the side streams of the sampled ranks only
+            from tests.synth import side_streams
+            rng = np.random.default_rng(a.seed)
+            side = side_streams(rng, ranks, self.iterations, self.iter_ns, self.span, self.slow, self.skews,
+                                rank_base=self.rank_base)
+            apply_side(w, side, ranks)
+        w.has_baseline = True
+        w.baseline_delta = 0.005
+        w.baseline = {}
+        w.baseline_iteration_ms = self.iter_ns / 1e6
+        w.symr = [t[3] for t in self.tables]
+        return w
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- reference
+def reference_arm(a, wl, torch, threads: int):
+    """The reference's own CPU path (oracle/_ref: strata build_group_data +
+    diagnose, compiled from /root/reference) on a bounded sample of the same
+    workload, with its per-rank loop fanned over `threads` host threads."""
+    from oracle import ref
+    from paper_2603_29235_b200.abi import STG_MEM_HOST
+    if not ref.available():
+        return None
+    # bounded sample: `threads` ranks x k samples; the reference reloads the
+    # 1M-entry tables for every aggregated record (symrepo.cpp:99-120 via
+    # folded.cpp:24), so k is tiny.  Calibrate k on one rank.
+    def run(ranks, k):
+        # spread the k samples over the whole window span
+        ts, foff, pc, bn = wl.generate(torch, ranks, k, seed_off=17, period=max(1, wl.span // k))
+        arrays = (ts.cpu().numpy(), foff.cpu().numpy().view(np.uint64), pc.cpu().numpy().view(np.uint64),
+                  bn.cpu().numpy().view(np.uint16))
+        w = wl.window(ranks, k, arrays, STG_MEM_HOST)
+        t0 = time.perf_counter()
+        res, tb, td = ref.window_run(w, threads=min(threads, ranks), want_json=False)
+        return time.perf_counter() - t0, tb + td, ranks * k, res
+    _, t1, n1, _ = run(1, 2)
+    per_sample = max(t1 / n1, 1e-6)
+    k = max(1, int(a.cpu_budget_s * min(threads, a.ranks) / per_sample / min(threads, a.ranks)))
+    ranks = min(threads, a.ranks)
+    wall, t, n, res = run(ranks, k)
+    return {"value": n / t, "unit": UNIT, "cores": ranks, "kind": "reference",
+            "sample": f"{ranks} ranks x {k} samples of the C2 workload (64-frame stacks, 3x{a.nsym}-symbol "
+                      f"tables), build_group_data+diagnose in {t:.2f}s; the reference reloads the 1M-entry "
+                      "SYMR tables once per aggregated record (resolve_stack cache is per call)",
+            "verdict": res["report"]["verdict"]}
+
+
+def peaks():
+    try:
+        return json.loads(PEAKS.read_text())
+    except Exception:
+        return {}
+
+
+# --------------------------------------------------------------------- main
+def main():
+    a = args_parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    if a.impl == "reference":
+        if rank == 0:
+            wl = Workload(a, 0)
+            cb = reference_arm(a, wl, torch, os.cpu_count() or 1)
+            if cb is None:
+                print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libstrata_ref.so not built"}))
+            else:
+                line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
+                        "n_gpus": a.gpus, "steps": 1, "warmup": 0, "higher_is_better": True,
+                        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+                        "config": {"workload": "C2 bounded sample", "ranks_per_gpu": a.ranks,
+                                   "samples_per_rank": a.spr, "depth": a.depth},
+                        "cpu_baseline": cb,
+                        "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                                "d2h_bytes_per_step": 0}}
+                print(json.dumps(line), flush=True)
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    import paper_2603_29235_b200 as stg
+    from paper_2603_29235_b200.abi import STG_MEM_DEVICE, STG_MEM_HOST
+    wl = Workload(a, rank)
+    ctx = stg.Context(local)
+    t0 = time.time()
+    for _, _, _, symr in wl.tables:
+        ctx.ingest(symr)
+    log(f"[bench r{rank}] tables ingested in {time.time() - t0:.1f}s")
+    t0 = time.time()
+    arrays = wl.generate(torch, a.ranks, a.spr)
+    win = wl.window(a.ranks, a.spr, arrays, STG_MEM_DEVICE)
+    log(f"[bench r{rank}] generated {win.n_samples} samples / {win.n_frames} frames in {time.time() - t0:.1f}s")
+
+    def step():
+        return ctx.window_run(win, ingest=False)
+
+    for i in range(a.warmup):
+        s = step()
+        log(f"[bench r{rank}] warmup {i}: {s['ms_total']:.2f} ms (sym {s['ms_symbolize']:.2f}) "
+            f"verdict={stg.VERDICTS[s['verdict']]} lines={s['n_lines']} seqs={s['n_sequences']}")
+    rep = ctx.report()
+    sym_ms, tot_ms, launches = [], [], []
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(a.steps):
+            s = step()
+            sym_ms.append(s["ms_symbolize"])
+            tot_ms.append(s["ms_total"])
+            launches.append(s["kernel_launches"])
+        e1.record()
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / a.steps
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    n_per_gpu = s["n_samples_in_window"]
+    value = n_per_gpu * world / (ms / 1e3)
+    # ---- roofline of the dominant kernel (fused symbolize+aggregate)
+    algo_bytes = 10 * win.n_frames + 16 * win.n_samples  # pc 8 + bin 2 per frame; ts 8 + csr 8 per sample
+    k_ms = float(np.median(sym_ms))
+    pk = peaks()
+    peak = pk.get("hbm_gbs", 6650.0)
+    achieved = algo_bytes / (k_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": None, "kernel": "k_sym_agg",
+            "kernel_ms": round(k_ms, 3), "algorithmic_bytes": algo_bytes,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback 6.65 TB/s"}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": "C2: 128 ranks x 1M samples per GPU, 64-frame stacks, 3x1M-symbol tables",
+                       "ranks_per_gpu": a.ranks, "samples_per_rank": a.spr, "depth": a.depth,
+                       "distinct_stacks": a.pool, "symbols_per_table": a.nsym,
+                       "inputs": "resident in HBM, 84 GB/GPU > L2 (no flush needed)",
+                       "parallelism": f"rank-sharded groups x{world}"},
+            "verdict": rep["verdict"], "flagged_ranks": rep["flagged_ranks"],
+            "prefix_cache": {"hits": s["prefix_hits"], "misses": s["prefix_misses"]},
+            "stage_ms": {"total_device": float(np.median(tot_ms)), "symbolize_aggregate": k_ms,
+                         "collectives": s["ms_collectives"], "fold": s["ms_fold"], "diff": s["ms_diff"]},
+            "roofline": roof, "gpu_launches": int(np.median(launches)) * a.steps,
+            "clocks": clk.summary()}
+    # ---- end to end through the C-ABI with host buffers (H2D inside the timed region)
+    if not a.no_e2e:
+        host = []
+        for t in arrays:
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t)
+            host.append(h)
+        del arrays
+        win = None
+        torch.cuda.empty_cache()
+        hwin = wl.window(a.ranks, a.spr, tuple(h.numpy().view(dt) for h, dt in
+                                                zip(host, (np.int64, np.uint64, np.uint64, np.uint16))),
+                         STG_MEM_HOST)
+        ctx.window_run(hwin, ingest=False)  # warm
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        h2d = d2h = 0
+        for _ in range(a.e2e_steps):
+            st = ctx.window_run(hwin, ingest=False)
+            r = ctx.report()
+            h2d += st["h2d_bytes"]
+            d2h += st["d2h_bytes"]
+        el = (time.perf_counter() - t0) / a.e2e_steps
+        if dist:
+            t = torch.tensor([el], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        line["e2e"] = {"value": n_per_gpu * world / el, "unit": UNIT,
+                       "h2d_bytes_per_step": h2d // a.e2e_steps, "d2h_bytes_per_step": d2h // a.e2e_steps,
+                       "ms_per_step": el * 1e3, "verdict": r["verdict"]}
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = reference_arm(a, wl, torch, os.cpu_count() or 1)
+        except Exception as ex:  # the baseline must not sink the GPU line
+            line["cpu_baseline"] = {"error": str(ex)[:200]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

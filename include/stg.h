@@ -210,6 +210,9 @@ typedef struct stg_run_stats {
     uint64_t h2d_bytes;
     uint64_t d2h_bytes;
     uint32_t kernel_launches;
+    uint32_t agg_attempts;   /* >1 when a rank table had to grow           */
+    uint64_t prefix_hits;    /* symbolization memo hits (raw call chains)  */
+    uint64_t prefix_misses;
 } stg_run_stats;
 
 /* Replaces build_group_data (bundle.cpp:252-324) followed by diagnose

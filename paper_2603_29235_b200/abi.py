@@ -130,6 +130,9 @@ class StgRunStats(C.Structure):
         ("h2d_bytes", C.c_uint64),
         ("d2h_bytes", C.c_uint64),
         ("kernel_launches", C.c_uint32),
+        ("agg_attempts", C.c_uint32),
+        ("prefix_hits", C.c_uint64),
+        ("prefix_misses", C.c_uint64),
     ]
 
     def as_dict(self) -> dict:

@@ -18,6 +18,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OUT = PKG / "_build"
 LIB = PKG / "libstg.so"
+BENCH_LIB = PKG / "libstg_bench.so"
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUDA_INC = "/usr/local/cuda/include"
@@ -61,6 +62,10 @@ def build(verbose: bool = False) -> Path:
         objs.append(obj)
     if _stale(LIB, objs):
         _run([NVCC, "-shared", *ARCH, "-o", str(LIB), *map(str, objs), "-lcudart"])
+    # bench-side generator (not part of the product library)
+    if _stale(BENCH_LIB, [CSRC / "bench_gen.cu"]):
+        _run([NVCC, "-std=c++17", "-O3", *ARCH, "-Xcompiler", "-fPIC", "-shared",
+              str(CSRC / "bench_gen.cu"), "-o", str(BENCH_LIB)])
     return LIB
 
 

@@ -89,19 +89,18 @@ __device__ __forceinline__ uint32_t table_lookup(const DevTable& t, uint64_t pc,
         uint32_t lo = __ldg(t.bucket + b), hi = __ldg(t.bucket + b + 1);
         while (lo < hi) {
             uint32_t mid = (lo + hi + 1) >> 1;
-            if (__ldg(t.starts + mid) <= pc)
+            if (__ldg(&t.e[mid].x) <= pc)
                 lo = mid;
             else
                 hi = mid - 1;
         }
         i = lo;
     }
-    uint64_t e = __ldg(t.ent + i);
-    if (mode == STG_LOOKUP_NEAREST_LOWER) return uint32_t(e >> 32);
-    uint32_t size = uint32_t(e);
-    uint64_t start = __ldg(t.starts + i);
-    bool in = size == 0 ? pc == start : pc < start + uint64_t(size);
-    return in ? uint32_t(e >> 32) : kUnknownBit;
+    ulonglong2 e = __ldg(t.e + i);
+    if (mode == STG_LOOKUP_NEAREST_LOWER) return uint32_t(e.y >> 32);
+    uint32_t size = uint32_t(e.y);
+    bool in = size == 0 ? pc == e.x : pc < e.x + uint64_t(size);
+    return in ? uint32_t(e.y >> 32) : kUnknownBit;
 }
 
 // Frame key: name rank, or kUnknownBit | unknown-set slot.

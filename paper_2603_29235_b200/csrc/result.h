@@ -56,6 +56,8 @@ struct Result {
     std::vector<uint64_t> cpu_totals;
     uint64_t n_lines = 0, n_seq = 0, n_names = 0, n_unknown = 0, f_used = 0, n_gid = 0;
     uint32_t n_window_ranks = 0;
+    int agg_attempts = 0;
+    uint64_t pfx_hits = 0, pfx_misses = 0;
     // name space: final rank -> string
     std::vector<uint64_t> unk_final;       // final rank of each distinct unknown label (sorted)
     std::vector<std::string> unk_labels;   // labels in the same order

@@ -31,12 +31,12 @@ struct Error : std::runtime_error {
 
 // --------------------------------------------------------- device tables
 // One staged symbol table (the device form of a SymbolFile, symfile.hpp:20-41).
-// ent[i] = size (low 32 bits) | name rank (high 32 bits).  bucket[b] is the
+// e[i] = {start, size (low 32 bits) | name rank (high 32 bits)}, 16 bytes, so a
+// probe and the final entry fetch are single 16-byte loads.  bucket[b] is the
 // index of the last entry whose start <= base + (b << shift); the search for an
 // offset in bucket b is confined to [bucket[b], bucket[b+1]].
 struct DevTable {
-    const uint64_t* starts;
-    const uint64_t* ent;
+    const ulonglong2* e;
     const uint32_t* bucket;
     uint64_t base;
     uint64_t last_start;
@@ -67,6 +67,11 @@ struct __align__(32) SeqSlot {
     unsigned long long rep; // global sample index of the representative
 };
 
+// Prefix cache slot: raw non-leaf chain fingerprint -> Σ symbolized terms.
+struct __align__(32) PfxSlot {
+    unsigned long long hi, lo, ta, tb;
+};
+
 // Unknown-frame set slot: (bin, pc) -> slot index.
 struct __align__(16) UnkSlot {
     unsigned long long pc;
@@ -82,8 +87,7 @@ struct HostTable {
     std::vector<uint32_t> name_local;   // index into names
     std::vector<std::string> names;     // distinct names of this table
     // device
-    uint64_t* d_starts = nullptr;
-    uint64_t* d_ent = nullptr;
+    ulonglong2* d_e = nullptr;
     uint32_t* d_bucket = nullptr;
     uint32_t shift = 0, nb = 0;
     uint64_t dict_version = ~0ull;      // dictionary the ent ranks refer to
@@ -140,7 +144,7 @@ std::string hex_id(const uint8_t* id);
 std::string unknown_label(const uint8_t* id, uint64_t off);
 
 // device helpers implemented in stg_window.cu
-void launch_build_buckets(const uint64_t* starts, uint32_t n, uint64_t base, uint32_t shift,
+void launch_build_buckets(const ulonglong2* e, uint32_t n, uint64_t base, uint32_t shift,
                           uint32_t nb, uint32_t* bucket, cudaStream_t s);
 
 }  // namespace stg

@@ -24,7 +24,7 @@ void run_resolve(Ctx& c, Result& res, uint64_t n, const uint64_t* pc, const uint
         if (it == c.table_by_id.end()) continue;
         HostTable& h = *c.tables[it->second];
         if (h.starts.empty()) continue;
-        t = DevTable{h.d_starts, h.d_ent, h.d_bucket, h.starts.front(), h.starts.back(), h.shift, h.nb,
+        t = DevTable{h.d_e, h.d_bucket, h.starts.front(), h.starts.back(), h.shift, h.nb,
                      uint32_t(h.starts.size()), 1};
     }
     DevTable* d_tabs = rn.up<DevTable>("rv_tabs", tabs.data(), tabs.size());

@@ -493,6 +493,8 @@ struct Runner {
         R = w.n_ranks;
         res.n_window_ranks = uint32_t(R);
         res.n_gid = 0;
+        res.agg_attempts = 0;
+        res.pfx_hits = res.pfx_misses = 0;
         res.cpu_rank_ids.clear();
         res.cpu_rank_index.clear();
         res.cpu_totals.clear();
@@ -529,8 +531,7 @@ struct Runner {
             if (it == c.table_by_id.end()) continue;
             HostTable& h = *c.tables[it->second];
             if (h.starts.empty()) continue;
-            t.starts = h.d_starts;
-            t.ent = h.d_ent;
+            t.e = h.d_e;
             t.bucket = h.d_bucket;
             t.base = h.starts.front();
             t.last_start = h.starts.back();
@@ -570,11 +571,14 @@ struct Runner {
         unsigned* d_unk_used = dev<unsigned>("unk_used", 1);
         int* d_unk_ovf = dev<int>("unk_ovf", 1);
         std::vector<uint64_t> tab_off(R);
+        // prefix cache: ~4 slots per distinct raw chain of the previous window
+        uint32_t pfx_cap = uint32_t(std::min<uint64_t>(1u << 24, std::max<uint64_t>(1u << 16, next_pow2(4 * c_pfx_last() + 1))));
+        PfxSlot* pfx = dev<PfxSlot>("pfx", pfx_cap);
+        unsigned long long* d_stat = dev<unsigned long long>("sym_stat", 2);
         AggSlot* slots = nullptr;
         UnkSlot* unk = nullptr;
         std::vector<int> ovf(R);
         std::vector<unsigned> used(R);
-        cudaEventRecord(ev[2], st);
         for (int attempt = 0;; ++attempt) {
             uint64_t tot = 0;
             for (int r = 0; r < R; ++r) {
@@ -621,17 +625,30 @@ struct Runner {
             p.err_empty = d_eempty;
             p.err_bin = d_ebin;
             p.n_samples = n_s;
-            p.chunk = 32;
+            p.pfx = pfx;
+            p.pfx_mask = pfx_cap - 1;
+            p.stat = d_stat;
+            zero(pfx, size_t(pfx_cap) * sizeof(PfxSlot));
+            zero(d_stat, 16);
             unsigned grid = unsigned(dev_sms) * 8;
-            uint64_t chunks = (n_s + p.chunk - 1) / p.chunk;
+            uint64_t chunks = (n_s + 31) / 32;
             uint64_t need = (chunks + (kThreads / 32) - 1) / (kThreads / 32);
             if (need < grid) grid = unsigned(std::max<uint64_t>(need, 1));
+            cudaEventRecord(ev[2], st);
+            const bool smem_tabs = w.n_bins <= kMaxSmemBins;
+#define STG_SYM(GV) \
+    (smem_tabs ? (void)(k_sym_agg<GV, true><<<grid, kThreads, 0, st>>>(p)) : (void)(k_sym_agg<GV, false><<<grid, kThreads, 0, st>>>(p)))
             switch (G) {
-                case 4: LAUNCH(k_sym_agg<4>, grid, kThreads, p); break;
-                case 8: LAUNCH(k_sym_agg<8>, grid, kThreads, p); break;
-                case 16: LAUNCH(k_sym_agg<16>, grid, kThreads, p); break;
-                default: LAUNCH(k_sym_agg<32>, grid, kThreads, p); break;
+                case 4: STG_SYM(4); break;
+                case 8: STG_SYM(8); break;
+                case 16: STG_SYM(16); break;
+                default: STG_SYM(32); break;
             }
+#undef STG_SYM
+            STG_CUDA(cudaGetLastError());
+            ++launches;
+            cudaEventRecord(ev[3], st);
+            res.agg_attempts = attempt + 1;
             down(ovf.data(), d_ovf, R);
             down(used.data(), d_used, R);
             bool any = false;
@@ -645,8 +662,14 @@ struct Runner {
             if (!any && !unk_over) break;
             if (attempt > 6) fail(STG_ENOMEM, "aggregation tables kept overflowing");
         }
-        cudaEventRecord(ev[3], st);
         c_set_hints(used, get1(d_unk_used));
+        {
+            unsigned long long hm[2];
+            down(hm, d_stat, 2);
+            res.pfx_hits = hm[0];
+            res.pfx_misses = hm[1];
+            c_pfx_last() = uint32_t(std::min<unsigned long long>(hm[1], 1u << 22));
+        }
         if (get1(d_ebin)) fail(STG_EINVAL, "frame binary index out of range");
         h_n_in.resize(R);
         down(h_n_in.data(), d_nin, R);
@@ -699,6 +722,10 @@ struct Runner {
     }
     std::vector<uint32_t>& c_hints() {
         static std::map<Ctx*, std::vector<uint32_t>> m;
+        return m[&c];
+    }
+    uint32_t& c_pfx_last() {
+        static std::map<Ctx*, uint32_t> m;
         return m[&c];
     }
     uint32_t& c_unk_last() {
@@ -1308,6 +1335,9 @@ struct Runner {
         s.h2d_bytes = h2d;
         s.d2h_bytes = d2h;
         s.kernel_launches = launches;
+        s.agg_attempts = uint32_t(res.agg_attempts);
+        s.prefix_hits = res.pfx_hits;
+        s.prefix_misses = res.pfx_misses;
     }
     bool ev_unset_fold() const { return R == 0 || L == 0; }
 };

@@ -26,8 +26,7 @@ namespace stg {
 
 Ctx::~Ctx() {
     for (auto& t : tables) {
-        if (t->d_starts) cudaFree(t->d_starts);
-        if (t->d_ent) cudaFree(t->d_ent);
+        if (t->d_e) cudaFree(t->d_e);
         if (t->d_bucket) cudaFree(t->d_bucket);
     }
     bufs.clear();
@@ -57,7 +56,7 @@ inline uint64_t next_pow2(uint64_t v) {
 }
 
 // ============================================================== tables
-__global__ void k_build_buckets(const uint64_t* starts, uint32_t n, uint64_t base, uint32_t shift,
+__global__ void k_build_buckets(const ulonglong2* e, uint32_t n, uint64_t base, uint32_t shift,
                                 uint32_t nb, uint32_t* bucket) {
     for (uint64_t b = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; b <= nb;
          b += uint64_t(gridDim.x) * blockDim.x) {
@@ -70,7 +69,7 @@ __global__ void k_build_buckets(const uint64_t* starts, uint32_t n, uint64_t bas
         uint32_t lo = 0, hi = n;  // upper_bound
         while (lo < hi) {
             uint32_t mid = (lo + hi) >> 1;
-            if (starts[mid] <= key)
+            if (e[mid].x <= key)
                 lo = mid + 1;
             else
                 hi = mid;
@@ -541,13 +540,15 @@ struct AggParams {
     const uint32_t* tab_mask;    // [R]
     unsigned* tab_used;
     int* tab_overflow;
+    PfxSlot* pfx;                // prefix cache (raw non-leaf chain -> symbolized terms)
+    uint32_t pfx_mask;
     UnkSet unk;
     unsigned long long* n_in;    // [R]
     int* unsorted;               // [R]
     unsigned long long* err_empty;  // [R] min rank-relative index
     int* err_bin;
+    unsigned long long* stat;    // [0] prefix hits, [1] misses
     uint64_t n_samples;
-    uint32_t chunk;              // samples per warp chunk
 };
 
 __device__ __forceinline__ void agg_insert(AggSlot* T, uint32_t mask, uint64_t fa, uint64_t fb, uint32_t rep,
@@ -579,66 +580,132 @@ __device__ __forceinline__ void agg_insert(AggSlot* T, uint32_t mask, uint64_t f
     *overflow = 1;
 }
 
-// The fused hot kernel.  A warp owns `chunk` consecutive samples; G lanes work on
-// one sample (32/G samples per step).  Per sample: window filter on the aligned
-// clock (bundle.cpp:290-294), coalesced 8-byte pc / 2-byte bin loads with the
-// streaming cache hint, per-frame table search, a position-tagged 128-bit
-// fingerprint of the root-first name sequence (shuffle-reduced over the group),
-// and one insert into the rank's open-addressing table.
-template <int G>
+// Raw (unsymbolized) terms of a non-leaf frame: bin, pc and leaf-first position.
+__device__ __forceinline__ uint64_t raw_a(uint64_t pc, uint32_t bin, uint32_t pos) {
+    return mix_a(pc ^ (uint64_t(pos) << 40) ^ (uint64_t(bin) << 20) ^ 0x3c6ef372fe94f82bull);
+}
+__device__ __forceinline__ uint64_t raw_b(uint64_t pc, uint32_t bin, uint32_t pos) {
+    return mix_b((pc + 0x510e527fade682d1ull) * 0x9e3779b97f4a7c15ull ^ (uint64_t(bin) << 48 | pos));
+}
+
+// Prefix cache probe: 0 = miss, 1 = hit (ta/tb filled).  Stale-free within a
+// window: the cache is cleared whenever names or unknown slots can change.
+__device__ __forceinline__ bool pfx_get(const PfxSlot* T, uint32_t mask, uint64_t ha, uint64_t hb, uint64_t& ta,
+                                        uint64_t& tb) {
+    uint32_t i = uint32_t(hb >> 24) & mask;
+    for (int probe = 0; probe < 16; ++probe) {
+        unsigned long long cur = *(volatile const unsigned long long*)&T[i].hi;
+        if (cur == 0) return false;
+        if (cur == ha) {
+            unsigned long long lo = *(volatile const unsigned long long*)&T[i].lo;
+            if (lo == hb) {
+                __threadfence();
+                ta = *(volatile const unsigned long long*)&T[i].ta;
+                tb = *(volatile const unsigned long long*)&T[i].tb;
+                return true;
+            }
+            if (lo == 0) return false;  // being written: treat as a miss
+        }
+        i = (i + 1) & mask;
+    }
+    return false;
+}
+__device__ __forceinline__ void pfx_put(PfxSlot* T, uint32_t mask, uint64_t ha, uint64_t hb, uint64_t ta, uint64_t tb) {
+    uint32_t i = uint32_t(hb >> 24) & mask;
+    for (int probe = 0; probe < 16; ++probe) {
+        unsigned long long cur = atomicCAS(&T[i].hi, 0ull, (unsigned long long)ha);
+        if (cur == 0) {
+            T[i].ta = ta;
+            T[i].tb = tb;
+            __threadfence();
+            *(volatile unsigned long long*)&T[i].lo = hb;
+            return;
+        }
+        if (cur == ha) return;  // someone else stores the same chain
+        i = (i + 1) & mask;
+    }
+}
+
+// The fused hot kernel (stage a+b).  A warp takes 32 consecutive samples:
+//  phase 0  lane s loads sample s's ts and CSR bounds (coalesced), applies the
+//           window filter on the aligned clock (bundle.cpp:290-294);
+//  phase 1  G lanes per sample stream its frames (coalesced 8 B pc + 2 B bin,
+//           streaming cache hint) and fold the NON-LEAF frames into a 128-bit
+//           raw-chain fingerprint (shuffle-reduced), handed to lane s;
+//  phase 2  lane s, in parallel for all 32 samples: prefix-cache probe (the
+//           raw chain's symbolized terms — return addresses repeat, so hits
+//           dominate), leaf lookup in the staged table (symfile.cpp:54-75),
+//           fingerprint of the root-first name sequence, and one insert into
+//           the rank's open-addressing table with __match_any pre-aggregation;
+//  misses   the warp symbolizes the missing chains cooperatively and fills
+//           the cache.
+template <int G, bool SMEM_TABS>
 __global__ void __launch_bounds__(kThreads) k_sym_agg(AggParams p) {
     __shared__ DevTable s_tabs[kMaxSmemBins];
-    for (uint32_t i = threadIdx.x; i < p.n_bins && i < kMaxSmemBins; i += blockDim.x) s_tabs[i] = p.tabs[i];
-    __syncthreads();
-    const DevTable* tabs = p.n_bins <= kMaxSmemBins ? s_tabs : p.tabs;
+    if (SMEM_TABS) {
+        for (uint32_t i = threadIdx.x; i < p.n_bins; i += blockDim.x) s_tabs[i] = p.tabs[i];
+        __syncthreads();
+    }
+    const DevTable* tabs = SMEM_TABS ? s_tabs : p.tabs;
     constexpr int SPW = 32 / G;
     const int lane = threadIdx.x & 31, sub = lane / G, gl = lane % G;
     const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-    const uint64_t n_chunks = (p.n_samples + p.chunk - 1) / p.chunk;
-    for (uint64_t c = warp; c < n_chunks; c += nwarps) {
-        const uint64_t c0 = c * p.chunk;
-        const uint64_t c1 = min(p.n_samples, c0 + p.chunk);
-        // rank of the chunk's first sample (warp-uniform binary search)
-        int r;
+    const uint64_t n_batches = (p.n_samples + 31) / 32;
+    unsigned long long hits = 0, misses = 0;
+    for (uint64_t bt = warp; bt < n_batches; bt += nwarps) {
+        // ---------------- phase 0: lane s owns sample i
+        const uint64_t i = bt * 32 + lane;
+        bool valid = i < p.n_samples;
+        int r = 0;
         {
+            uint64_t q = valid ? i : p.n_samples - 1;
             int lo = 0, hi = p.R - 1;
             while (lo < hi) {
                 int mid = (lo + hi + 1) >> 1;
-                if (__ldg(p.rank_soff + mid) <= c0) lo = mid; else hi = mid - 1;
+                if (__ldg(p.rank_soff + mid) <= q) lo = mid; else hi = mid - 1;
             }
             r = lo;
         }
-        unsigned long long in_cnt = 0;
-        int cnt_rank = r;
-        for (uint64_t s0 = c0; s0 < c1; s0 += SPW) {
-            const uint64_t i = s0 + sub;
-            bool valid = i < c1;
-            int ri = r;
-            if (valid)
-                while (ri + 1 < p.R && __ldg(p.rank_soff + ri + 1) <= i) ++ri;
-            bool inwin = false;
-            uint64_t f0 = 0, f1 = 0;
-            if (valid && p.active[ri]) {
-                int64_t t = __ldcs(p.ts + i);
-                uint64_t rs = __ldg(p.rank_soff + ri);
-                if (gl == 0 && i > rs && t < __ldcs(p.ts + i - 1)) p.unsorted[ri] = 1;
-                inwin = t - p.rank_clk[ri] >= p.ws;
-                if (inwin) {
-                    f0 = __ldcs(p.foff + i);
-                    f1 = __ldcs(p.foff + i + 1);
+        uint64_t rs = __ldg(p.rank_soff + r);
+        bool inwin = false;
+        uint64_t f0 = 0, f1 = 0;
+        if (valid && p.active[r]) {
+            int64_t t = __ldcs(p.ts + i);
+            if (i > rs && t < __ldcs(p.ts + i - 1)) p.unsorted[r] = 1;
+            inwin = t - __ldg(p.rank_clk + r) >= p.ws;
+            if (inwin) {
+                f0 = __ldcs(p.foff + i);
+                f1 = __ldcs(p.foff + i + 1);
+                if (f1 == f0) {
+                    atomicMin(p.err_empty + r, (unsigned long long)(i - rs));
+                    inwin = false;
                 }
             }
+        }
+        const uint32_t depth = uint32_t(f1 - f0);
+        // ---------------- phase 1: raw non-leaf chain fingerprints
+        const unsigned need = __ballot_sync(0xffffffffu, inwin && depth > 1);
+        uint64_t my_ra = 0, my_rb = 0, leaf_pc = 0;
+        uint32_t leaf_bin = 0;
+        if (inwin) {
+            leaf_pc = __ldcs(p.pc + f0);
+            leaf_bin = __ldcs(p.bin + f0);
+        }
+        for (int s0 = 0; s0 < 32; s0 += SPW) {
+            if (!((need >> s0) & ((SPW == 32 ? 0xffffffffu : ((1u << SPW) - 1))))) continue;
+            const int src = s0 + sub;
+            const uint64_t a0 = __shfl_sync(0xffffffffu, f0, src);
+            const uint64_t a1 = __shfl_sync(0xffffffffu, f1, src);
+            const bool on = (need >> src) & 1u;
             uint64_t ha = 0, hb = 0;
-            if (inwin) {
-                const uint64_t d = f1 - f0;
-                for (uint64_t j = f0 + gl; j < f1; j += G) {
-                    uint64_t pc = __ldcs(p.pc + j);
+            if (on) {
+                for (uint64_t j = a0 + 1 + gl; j < a1; j += G) {
+                    uint64_t pcv = __ldcs(p.pc + j);
                     uint32_t bn = __ldcs(p.bin + j);
-                    uint32_t key = resolve_frame(tabs, p.n_bins, pc, bn, p.mode, p.unk, p.err_bin);
-                    uint32_t pos = uint32_t(d - 1 - (j - f0));  // root-first position
-                    ha += term_a(key, pos);
-                    hb += term_b(key, pos);
+                    uint32_t pos = uint32_t(j - a0);
+                    ha += raw_a(pcv, bn, pos);
+                    hb += raw_b(pcv, bn, pos);
                 }
             }
 #pragma unroll
@@ -646,26 +713,73 @@ __global__ void __launch_bounds__(kThreads) k_sym_agg(AggParams p) {
                 ha += __shfl_xor_sync(0xffffffffu, ha, o);
                 hb += __shfl_xor_sync(0xffffffffu, hb, o);
             }
-            if (gl == 0 && inwin) {
-                const uint64_t rs = __ldg(p.rank_soff + ri);
-                if (f1 == f0) {
-                    atomicMin(p.err_empty + ri, (unsigned long long)(i - rs));
-                } else {
-                    uint64_t fa, fb;
-                    fp_finish(ha, hb, f1 - f0, fa, fb);
-                    if (!*(volatile int*)(p.tab_overflow + ri))
-                        agg_insert(p.slots + p.tab_off[ri], p.tab_mask[ri], fa, fb, uint32_t(i - rs), 1u,
-                                   p.tab_used + ri, p.tab_overflow + ri);
+            // hand the chain fingerprint of sample src to lane src
+#pragma unroll
+            for (int g = 0; g < SPW; ++g) {
+                uint64_t xa = __shfl_sync(0xffffffffu, ha, g * G);
+                uint64_t xb = __shfl_sync(0xffffffffu, hb, g * G);
+                if (lane == s0 + g) {
+                    my_ra = mix_a(xa ^ (uint64_t(depth) * 0x8cb92ba72f3d8dd7ull));
+                    my_rb = mix_b(xb + uint64_t(depth));
+                    if (my_ra == 0) my_ra = 1;
+                    if (my_rb == 0) my_rb = 1;
                 }
-                if (ri != cnt_rank) {
-                    if (in_cnt) atomicAdd(p.n_in + cnt_rank, in_cnt);
-                    in_cnt = 0;
-                    cnt_rank = ri;
-                }
-                ++in_cnt;
             }
         }
-        if (gl == 0 && in_cnt) atomicAdd(p.n_in + cnt_rank, in_cnt);
+        // ---------------- phase 2: per-lane cache probe, leaf lookup
+        uint64_t ta = 0, tb = 0;
+        bool hit = true;
+        if (inwin && depth > 1) hit = pfx_get(p.pfx, p.pfx_mask, my_ra, my_rb, ta, tb);
+        unsigned miss = __ballot_sync(0xffffffffu, inwin && depth > 1 && !hit);
+        hits += __popc(need & ~miss) * (lane == 0);
+        misses += __popc(miss) * (lane == 0);
+        while (miss) {
+            const int src = __ffs(miss) - 1;
+            miss &= miss - 1;
+            const uint64_t a0 = __shfl_sync(0xffffffffu, f0, src);
+            const uint64_t a1 = __shfl_sync(0xffffffffu, f1, src);
+            const uint64_t d = a1 - a0;
+            uint64_t xa = 0, xb = 0;
+            for (uint64_t j = a0 + 1 + lane; j < a1; j += 32) {
+                uint32_t key = resolve_frame(tabs, p.n_bins, p.pc[j], p.bin[j], p.mode, p.unk, p.err_bin);
+                uint32_t pos = uint32_t(d - 1 - (j - a0));  // root-first position
+                xa += term_a(key, pos);
+                xb += term_b(key, pos);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                xa += __shfl_xor_sync(0xffffffffu, xa, o);
+                xb += __shfl_xor_sync(0xffffffffu, xb, o);
+            }
+            if (lane == src) {
+                ta = xa;
+                tb = xb;
+                pfx_put(p.pfx, p.pfx_mask, my_ra, my_rb, ta, tb);
+            }
+        }
+        uint64_t fa = 0, fb = 0;
+        if (inwin) {
+            uint32_t key = resolve_frame(tabs, p.n_bins, leaf_pc, leaf_bin, p.mode, p.unk, p.err_bin);
+            ta += term_a(key, depth - 1);
+            tb += term_b(key, depth - 1);
+            fp_finish(ta, tb, depth, fa, fb);
+        }
+        // ---------------- aggregate: identical (rank, stack) in the batch combine
+        const unsigned act = __ballot_sync(0xffffffffu, inwin);
+        if (act) {
+            unsigned m = __match_any_sync(0xffffffffu, inwin ? fa : 0ull) & __match_any_sync(0xffffffffu, r) & act;
+            if (inwin && (__ffs(m) - 1) == lane) {
+                if (!*(volatile int*)(p.tab_overflow + r))
+                    agg_insert(p.slots + __ldg(p.tab_off + r), __ldg(p.tab_mask + r), fa, fb, uint32_t(i - rs),
+                               __popc(m), p.tab_used + r, p.tab_overflow + r);
+            }
+            unsigned mr = __match_any_sync(0xffffffffu, r) & act;
+            if (inwin && (__ffs(mr) - 1) == lane) atomicAdd(p.n_in + r, (unsigned long long)__popc(mr));
+        }
+    }
+    if (lane == 0 && (hits | misses)) {
+        atomicAdd(p.stat, hits);
+        atomicAdd(p.stat + 1, misses);
     }
 }
 
@@ -1068,9 +1182,9 @@ __global__ void k_clk_of_cpu(int R, const int32_t* rank_ids, const int64_t* off,
 
 }  // namespace
 
-void launch_build_buckets(const uint64_t* starts, uint32_t n, uint64_t base, uint32_t shift, uint32_t nb,
+void launch_build_buckets(const ulonglong2* e, uint32_t n, uint64_t base, uint32_t shift, uint32_t nb,
                           uint32_t* bucket, cudaStream_t s) {
-    k_build_buckets<<<grid_for(uint64_t(nb) + 1), kThreads, 0, s>>>(starts, n, base, shift, nb, bucket);
+    k_build_buckets<<<grid_for(uint64_t(nb) + 1), kThreads, 0, s>>>(e, n, base, shift, nb, bucket);
     STG_CUDA(cudaGetLastError());
 }
 

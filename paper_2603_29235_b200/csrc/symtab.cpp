@@ -137,26 +137,25 @@ void symtab_refresh_dictionary(Ctx& c) {
         for (size_t i = 0; i < t.names.size(); ++i)
             rank_of[i] = uint32_t(std::lower_bound(c.dict.begin(), c.dict.end(), t.names[i]) - c.dict.begin());
         uint32_t n = uint32_t(t.starts.size());
-        std::vector<uint64_t> ent(n);
-        for (uint32_t i = 0; i < n; ++i)
-            ent[i] = uint64_t(t.sizes[i]) | uint64_t(rank_of[t.name_local[i]]) << 32;
-        if (!t.d_starts && n > 0) {
-            STG_CUDA(cudaMalloc(&t.d_starts, n * sizeof(uint64_t)));
-            STG_CUDA(cudaMalloc(&t.d_ent, n * sizeof(uint64_t)));
-            STG_CUDA(cudaMemcpyAsync(t.d_starts, t.starts.data(), n * sizeof(uint64_t),
-                                     cudaMemcpyHostToDevice, c.stream));
-            // bucket index: about one bucket per entry
+        std::vector<ulonglong2> ent(n);
+        for (uint32_t i = 0; i < n; ++i) {
+            ent[i].x = t.starts[i];
+            ent[i].y = uint64_t(t.sizes[i]) | uint64_t(rank_of[t.name_local[i]]) << 32;
+        }
+        if (!t.d_e && n > 0) {
+            STG_CUDA(cudaMalloc(&t.d_e, n * sizeof(ulonglong2)));
+            // bucket index: about four buckets per entry (short in-bucket searches)
             uint64_t span = t.starts[n - 1] - t.starts[0];
             uint32_t shift = 0;
-            while (shift < 63 && (span >> shift) > uint64_t(n) * 2) ++shift;
+            while (shift < 63 && (span >> shift) > uint64_t(n) * 4) ++shift;
             t.shift = shift;
             t.nb = uint32_t((span >> shift) + 1);
             STG_CUDA(cudaMalloc(&t.d_bucket, (size_t(t.nb) + 1) * sizeof(uint32_t)));
-            launch_build_buckets(t.d_starts, n, t.starts[0], t.shift, t.nb, t.d_bucket, c.stream);
         }
-        if (n > 0)
-            STG_CUDA(cudaMemcpyAsync(t.d_ent, ent.data(), n * sizeof(uint64_t), cudaMemcpyHostToDevice,
-                                     c.stream));
+        if (n > 0) {
+            STG_CUDA(cudaMemcpyAsync(t.d_e, ent.data(), n * sizeof(ulonglong2), cudaMemcpyHostToDevice, c.stream));
+            launch_build_buckets(t.d_e, n, t.starts[0], t.shift, t.nb, t.d_bucket, c.stream);
+        }
         t.dict_version = c.dict_version;
         STG_CUDA(cudaStreamSynchronize(c.stream));
     }

@@ -111,40 +111,62 @@ def small_window(seed: int = 1, ranks: int = 8, samples_per_rank: int = 2000, sl
             foff.append(len(pcs))
         ts_all.append(t)
         rank_off.append(rank_off[-1] + samples_per_rank)
-    # ---- collectives: one AllReduce per iteration, barrier exit shared
+    side = side_streams(rng, ranks, iterations, iter_ns, we, slow_rank, skews, entry_delay_ns)
+    w = Window()
+    w.window_start_ns, w.window_end_ns, w.max_skew_ns = ws, we, 50_000_000
+    w.rank_ids = rank_ids
+    w.rank_sample_off = np.asarray(rank_off, np.uint64)
+    w.bin_build_ids = np.frombuffer(b"".join(bids), np.uint8).reshape(-1, 20).copy()
+    w.sample_ts = np.concatenate(ts_all).astype(np.int64)
+    w.sample_frame_off = np.asarray(foff, np.uint64)
+    w.frame_pc = np.asarray(pcs, np.uint64)
+    w.frame_bin = np.asarray(bins_, np.uint16)
+    apply_side(w, side, ranks)
+    w.has_baseline = True
+    w.baseline_delta = 0.005
+    w.baseline = {"main": 1.0, "train_loop": 1.0}
+    w.baseline_iteration_ms = iter_ns / 1e6
+    w.symr = symr
+    return w
+
+
+def side_streams(rng, ranks, iterations, iter_ns, span_ns, slow_rank, skews, entry_delay_ns=600_000,
+                 rank_base=0):
+    """Collectives (one AllReduce per iteration), GPU kernel events and 5 s OS
+    counter windows for `ranks` ranks with ids rank_base + r."""
     c_rank, c_entry, c_exit = [], [], []
     g_rank, g_kern, g_start, g_dur = [], [], [], []
     for k in range(iterations):
         t0 = k * iter_ns
         barrier = t0 + int(iter_ns * 0.8)
+        comp = (int(iter_ns * 0.7) + rng.normal(0, 50_000, size=ranks)).astype(np.int64)
+        jit = rng.integers(-25_000, 25_001, size=ranks)
         for r in range(ranks):
-            comp = int(iter_ns * 0.7) + int(rng.normal(0, 50_000))
             delay = entry_delay_ns if r == slow_rank else 0
-            entry = t0 + comp + delay
-            ex = max(barrier, entry + 1000) + int(rng.integers(-25_000, 25_001))
-            c_rank.append(r)
+            entry = t0 + int(comp[r]) + delay
+            ex = max(barrier, entry + 1000) + int(jit[r])
+            c_rank.append(rank_base + r)
             c_entry.append(entry + int(skews[r]))
             c_exit.append(max(ex, entry + 1) + int(skews[r]))
             ks = t0
             for kk, share in ((1, 0.48), (4, 0.19), (0, 0.15), (2, 0.18)):
-                du = int(share * comp * np.exp(rng.normal(0, 0.01)))
-                g_rank.append(r)
+                du = int(share * int(comp[r]) * np.exp(rng.normal(0, 0.01)))
+                g_rank.append(rank_base + r)
                 g_kern.append(kk)
                 g_start.append(ks + int(skews[r]))
                 g_dur.append(du)
                 ks += du
-            g_rank.append(r)
+            g_rank.append(rank_base + r)
             g_kern.append(3)
             g_start.append(entry + int(skews[r]))
             g_dur.append(max(0, barrier - entry))
-    # ---- OS counters, 5 s windows on the rank clock
     o_rank, o_ws, o_p50, o_p99, o_mig = [], [], [], [], []
     irq_off, irq_k, irq_v, sirq_off, sirq_k, sirq_v = [0], [], [], [0], [], []
     for r in range(ranks):
         storm = r == slow_rank
-        for wnd in range(int(np.ceil(we / 5e9)) or 1):
+        for wnd in range(int(np.ceil(span_ns / 5e9)) or 1):
             j = lambda: rng.uniform(0.98, 1.02)
-            o_rank.append(r)
+            o_rank.append(rank_base + r)
             o_ws.append(wnd * 5_000_000_000 + int(skews[r]))
             o_p50.append(int(50_000 * j()))
             o_p99.append(int(400_000 * j() * (6 if storm else 1)))
@@ -155,43 +177,56 @@ def small_window(seed: int = 1, ranks: int = 8, samples_per_rank: int = 2000, sl
             sirq_k += [4, 3, 1]
             sirq_v += [int(8000 * j()), int(6000 * j()), int(5000 * j() * (10 if storm else 1))]
             sirq_off.append(len(sirq_k))
-    w = Window()
-    w.window_start_ns, w.window_end_ns, w.max_skew_ns = ws, we, 50_000_000
-    w.rank_ids = rank_ids
-    w.rank_sample_off = np.asarray(rank_off, np.uint64)
-    w.bin_build_ids = np.frombuffer(b"".join(bids), np.uint8).reshape(-1, 20).copy()
-    w.sample_ts = np.concatenate(ts_all).astype(np.int64)
-    w.sample_frame_off = np.asarray(foff, np.uint64)
-    w.frame_pc = np.asarray(pcs, np.uint64)
-    w.frame_bin = np.asarray(bins_, np.uint16)
-    n = len(c_rank)
-    w.coll_rank = np.asarray(c_rank, np.int32)
+    return dict(c_rank=c_rank, c_entry=c_entry, c_exit=c_exit, g_rank=g_rank, g_kern=g_kern,
+                g_start=g_start, g_dur=g_dur, o_rank=o_rank, o_ws=o_ws, o_p50=o_p50, o_p99=o_p99,
+                o_mig=o_mig, irq_off=irq_off, irq_k=irq_k, irq_v=irq_v, sirq_off=sirq_off,
+                sirq_k=sirq_k, sirq_v=sirq_v, rank_base=rank_base)
+
+
+def apply_side(w: Window, side: dict, ranks: int):
+    n = len(side["c_rank"])
+    w.coll_rank = np.asarray(side["c_rank"], np.int32)
     w.coll_group = np.zeros(n, np.int32)
     w.coll_kind = np.zeros(n, np.uint8)
-    w.coll_entry = np.asarray(c_entry, np.int64)
-    w.coll_exit = np.asarray(c_exit, np.int64)
+    w.coll_entry = np.asarray(side["c_entry"], np.int64)
+    w.coll_exit = np.asarray(side["c_exit"], np.int64)
     w.coll_gpu_dur = w.coll_exit - w.coll_entry
-    w.group_ranks = rank_ids.copy()
-    w.gpu_rank = np.asarray(g_rank, np.int32)
-    w.gpu_kernel = np.asarray(g_kern, np.uint32)
-    w.gpu_start = np.asarray(g_start, np.int64)
-    w.gpu_dur = np.asarray(g_dur, np.int64)
+    w.group_ranks = np.arange(side["rank_base"], side["rank_base"] + ranks, dtype=np.int32)
+    w.gpu_rank = np.asarray(side["g_rank"], np.int32)
+    w.gpu_kernel = np.asarray(side["g_kern"], np.uint32)
+    w.gpu_start = np.asarray(side["g_start"], np.int64)
+    w.gpu_dur = np.asarray(side["g_dur"], np.int64)
     w.kernel_names = list(KERNELS)
-    w.os_rank = np.asarray(o_rank, np.int32)
-    w.os_window_start = np.asarray(o_ws, np.int64)
-    w.os_p50 = np.asarray(o_p50, np.int64)
-    w.os_p99 = np.asarray(o_p99, np.int64)
-    w.os_migrations = np.asarray(o_mig, np.int64)
-    w.os_irq_off = np.asarray(irq_off, np.uint64)
-    w.os_irq_key = np.asarray(irq_k, np.uint32)
-    w.os_irq_val = np.asarray(irq_v, np.int64)
-    w.os_sirq_off = np.asarray(sirq_off, np.uint64)
-    w.os_sirq_key = np.asarray(sirq_k, np.uint32)
-    w.os_sirq_val = np.asarray(sirq_v, np.int64)
+    w.os_rank = np.asarray(side["o_rank"], np.int32)
+    w.os_window_start = np.asarray(side["o_ws"], np.int64)
+    w.os_p50 = np.asarray(side["o_p50"], np.int64)
+    w.os_p99 = np.asarray(side["o_p99"], np.int64)
+    w.os_migrations = np.asarray(side["o_mig"], np.int64)
+    w.os_irq_off = np.asarray(side["irq_off"], np.uint64)
+    w.os_irq_key = np.asarray(side["irq_k"], np.uint32)
+    w.os_irq_val = np.asarray(side["irq_v"], np.int64)
+    w.os_sirq_off = np.asarray(side["sirq_off"], np.uint64)
+    w.os_sirq_key = np.asarray(side["sirq_k"], np.uint32)
+    w.os_sirq_val = np.asarray(side["sirq_v"], np.int64)
     w.counter_names = list(COUNTERS)
-    w.has_baseline = True
-    w.baseline_delta = 0.005
-    w.baseline = {"main": 1.0, "train_loop": 1.0}
-    w.baseline_iteration_ms = iter_ns / 1e6
-    w.symr = symr
-    return w
+
+
+C2_BINARIES = (("python3.11", "py"), ("libtorch_cuda.so", "at::native"), ("libcuda.so", "cu"))
+
+
+def c2_tables(seed: int = 42, nsym: int = 1_000_000):
+    """Three 1M-symbol tables (python, libtorch, cuda): sizes log-uniform 16-4096 B,
+    ~10 % gap fraction.  The cuda table's first 9 names are the softirq path.
+    Returns [(build_id, starts, sizes, symr)]."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for b, (label, prefix) in enumerate(C2_BINARIES):
+        sizes = np.exp(rng.uniform(np.log(16), np.log(4096), nsym)).astype(np.uint32)
+        gaps = (sizes * rng.uniform(0.0, 0.22, nsym)).astype(np.uint64)
+        starts = (0x10000 + np.concatenate([[0], np.cumsum(sizes.astype(np.uint64) + gaps)[:-1]])).astype(np.uint64)
+        names = [f"{prefix}_{i:07d}" for i in range(nsym)]
+        if b == 2:
+            names[:9] = SOFTIRQ
+        bid = build_id(f"c2-{label}-{seed}")
+        out.append((bid, starts, sizes, pack_symr(bid, starts, sizes, names)))
+    return out
