@@ -512,6 +512,8 @@ struct Runner {
         const uint64_t *foff, *pc;
         const uint16_t* bin;
         if (w.memory == STG_MEM_DEVICE) {
+            if ((reinterpret_cast<uintptr_t>(w.frame_pc) | reinterpret_cast<uintptr_t>(w.frame_bin)) & 15)
+                fail(STG_EINVAL, "device frame_pc / frame_bin must be 16-byte aligned");
             ts = w.sample_ts;
             foff = w.sample_frame_off;
             pc = w.frame_pc;
@@ -555,11 +557,6 @@ struct Runner {
             caps[r] = uint32_t(std::max<uint64_t>(64, next_pow2(want)));
         }
         uint32_t unk_cap = uint32_t(std::max<uint64_t>(4096, next_pow2(c_unk_hint())));
-        int G = 32;
-        double avg = n_s ? double(n_f) / double(n_s) : 1;
-        if (avg <= 4) G = 4;
-        else if (avg <= 8) G = 8;
-        else if (avg <= 16) G = 16;
         int dev_sms = 148;
         STG_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c.device));
         unsigned long long* d_nin = dev<unsigned long long>("nin", R);
@@ -625,6 +622,7 @@ struct Runner {
             p.err_empty = d_eempty;
             p.err_bin = d_ebin;
             p.n_samples = n_s;
+            p.n_frames = n_f;
             p.pfx = pfx;
             p.pfx_mask = pfx_cap - 1;
             p.stat = d_stat;
@@ -636,15 +634,10 @@ struct Runner {
             if (need < grid) grid = unsigned(std::max<uint64_t>(need, 1));
             cudaEventRecord(ev[2], st);
             const bool smem_tabs = w.n_bins <= kMaxSmemBins;
-#define STG_SYM(GV) \
-    (smem_tabs ? (void)(k_sym_agg<GV, true><<<grid, kThreads, 0, st>>>(p)) : (void)(k_sym_agg<GV, false><<<grid, kThreads, 0, st>>>(p)))
-            switch (G) {
-                case 4: STG_SYM(4); break;
-                case 8: STG_SYM(8); break;
-                case 16: STG_SYM(16); break;
-                default: STG_SYM(32); break;
-            }
-#undef STG_SYM
+            if (smem_tabs)
+                k_sym_agg<true><<<grid, kThreads, 0, st>>>(p);
+            else
+                k_sym_agg<false><<<grid, kThreads, 0, st>>>(p);
             STG_CUDA(cudaGetLastError());
             ++launches;
             cudaEventRecord(ev[3], st);

@@ -549,16 +549,21 @@ struct AggParams {
     int* err_bin;
     unsigned long long* stat;    // [0] prefix hits, [1] misses
     uint64_t n_samples;
+    uint64_t n_frames;
 };
 
 __device__ __forceinline__ void agg_insert(AggSlot* T, uint32_t mask, uint64_t fa, uint64_t fb, uint32_t rep,
                                            uint32_t cnt, unsigned* used, int* overflow) {
     uint32_t i = uint32_t(fb >> 20) & mask;
     for (uint32_t probe = 0; probe <= mask; ++probe) {
-        unsigned long long cur = *(volatile unsigned long long*)&T[i].hi;
-        if (cur == 0) {
-            cur = atomicCAS(&T[i].hi, 0ull, (unsigned long long)fa);
-            if (cur == 0) {
+        ulonglong2 cur = __ldcg(reinterpret_cast<const ulonglong2*>(T + i));  // (hi, lo) in one L2 read
+        if (cur.x == fa && cur.y == fb) {
+            atomicAdd(&T[i].count, cnt);
+            return;
+        }
+        if (cur.x == 0) {
+            unsigned long long prev = atomicCAS(&T[i].hi, 0ull, (unsigned long long)fa);
+            if (prev == 0) {
                 T[i].rep = rep;
                 __threadfence();
                 *(volatile unsigned long long*)&T[i].lo = fb;
@@ -566,10 +571,15 @@ __device__ __forceinline__ void agg_insert(AggSlot* T, uint32_t mask, uint64_t f
                 if (atomicAdd(used, 1u) + 1 > (mask + 1) / 2) *overflow = 1;
                 return;
             }
+            cur.x = prev;
+            cur.y = 0;
         }
-        if (cur == fa) {
-            unsigned long long lo;
-            while ((lo = *(volatile unsigned long long*)&T[i].lo) == 0) __nanosleep(16);
+        if (cur.x == fa) {
+            unsigned long long lo = cur.y;
+            while (lo == 0) {
+                __nanosleep(16);
+                lo = *(volatile unsigned long long*)&T[i].lo;
+            }
             if (lo == fb) {
                 atomicAdd(&T[i].count, cnt);
                 return;
@@ -588,28 +598,10 @@ __device__ __forceinline__ uint64_t raw_b(uint64_t pc, uint32_t bin, uint32_t po
     return mix_b((pc + 0x510e527fade682d1ull) * 0x9e3779b97f4a7c15ull ^ (uint64_t(bin) << 48 | pos));
 }
 
-// Prefix cache probe: 0 = miss, 1 = hit (ta/tb filled).  Stale-free within a
-// window: the cache is cleared whenever names or unknown slots can change.
-__device__ __forceinline__ bool pfx_get(const PfxSlot* T, uint32_t mask, uint64_t ha, uint64_t hb, uint64_t& ta,
-                                        uint64_t& tb) {
-    uint32_t i = uint32_t(hb >> 24) & mask;
-    for (int probe = 0; probe < 16; ++probe) {
-        unsigned long long cur = *(volatile const unsigned long long*)&T[i].hi;
-        if (cur == 0) return false;
-        if (cur == ha) {
-            unsigned long long lo = *(volatile const unsigned long long*)&T[i].lo;
-            if (lo == hb) {
-                __threadfence();
-                ta = *(volatile const unsigned long long*)&T[i].ta;
-                tb = *(volatile const unsigned long long*)&T[i].tb;
-                return true;
-            }
-            if (lo == 0) return false;  // being written: treat as a miss
-        }
-        i = (i + 1) & mask;
-    }
-    return false;
-}
+// Prefix cache.  Entries are immutable once published: writer claims hi by CAS,
+// stores (ta, tb), fences, then stores lo.  A reader takes (hi, lo) and (ta, tb)
+// with two 16-byte L2 reads issued together; an entry seen with lo published but
+// (ta, tb) still zero (a torn read racing the writer) is treated as a miss.
 __device__ __forceinline__ void pfx_put(PfxSlot* T, uint32_t mask, uint64_t ha, uint64_t hb, uint64_t ta, uint64_t tb) {
     uint32_t i = uint32_t(hb >> 24) & mask;
     for (int probe = 0; probe < 16; ++probe) {
@@ -626,20 +618,22 @@ __device__ __forceinline__ void pfx_put(PfxSlot* T, uint32_t mask, uint64_t ha, 
     }
 }
 
-// The fused hot kernel (stage a+b).  A warp takes 32 consecutive samples:
-//  phase 0  lane s loads sample s's ts and CSR bounds (coalesced), applies the
-//           window filter on the aligned clock (bundle.cpp:290-294);
-//  phase 1  G lanes per sample stream its frames (coalesced 8 B pc + 2 B bin,
-//           streaming cache hint) and fold the NON-LEAF frames into a 128-bit
-//           raw-chain fingerprint (shuffle-reduced), handed to lane s;
-//  phase 2  lane s, in parallel for all 32 samples: prefix-cache probe (the
-//           raw chain's symbolized terms — return addresses repeat, so hits
-//           dominate), leaf lookup in the staged table (symfile.cpp:54-75),
-//           fingerprint of the root-first name sequence, and one insert into
-//           the rank's open-addressing table with __match_any pre-aggregation;
+// The fused hot kernel (stage a+b), one lane per sample.  A warp takes 32
+// consecutive samples — one contiguous block of frames in HBM:
+//  phase 0  lane s loads its ts and CSR bounds (coalesced), applies the window
+//           filter on the aligned clock (bundle.cpp:290-294);
+//  phase 1  lane s streams its own frames with 16-byte vector loads (8 frames =
+//           4 x 16 B of pc + 16 B of bin per step, streaming cache hint) and
+//           folds the NON-LEAF frames into a 128-bit raw-chain fingerprint;
+//           the warp as a whole reads its 20 KB block sector-complete;
+//  phase 2  lane s: prefix-cache probe (the raw chain's symbolized terms —
+//           return addresses repeat, so hits dominate) overlapped with the leaf
+//           lookup in the staged table (symfile.cpp:54-75), fingerprint of the
+//           root-first name sequence, and one insert into the rank's
+//           open-addressing table with __match_any pre-aggregation;
 //  misses   the warp symbolizes the missing chains cooperatively and fills
 //           the cache.
-template <int G, bool SMEM_TABS>
+template <bool SMEM_TABS>
 __global__ void __launch_bounds__(kThreads) k_sym_agg(AggParams p) {
     __shared__ DevTable s_tabs[kMaxSmemBins];
     if (SMEM_TABS) {
@@ -647,8 +641,7 @@ __global__ void __launch_bounds__(kThreads) k_sym_agg(AggParams p) {
         __syncthreads();
     }
     const DevTable* tabs = SMEM_TABS ? s_tabs : p.tabs;
-    constexpr int SPW = 32 / G;
-    const int lane = threadIdx.x & 31, sub = lane / G, gl = lane % G;
+    const int lane = threadIdx.x & 31;
     const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
     const uint64_t n_batches = (p.n_samples + 31) / 32;
@@ -684,53 +677,116 @@ __global__ void __launch_bounds__(kThreads) k_sym_agg(AggParams p) {
             }
         }
         const uint32_t depth = uint32_t(f1 - f0);
-        // ---------------- phase 1: raw non-leaf chain fingerprints
-        const unsigned need = __ballot_sync(0xffffffffu, inwin && depth > 1);
-        uint64_t my_ra = 0, my_rb = 0, leaf_pc = 0;
+        // ---------------- phase 1: this lane's frames, 8 per step
+        uint64_t leaf_pc = 0, ha = 0, hb = 0;
         uint32_t leaf_bin = 0;
         if (inwin) {
-            leaf_pc = __ldcs(p.pc + f0);
-            leaf_bin = __ldcs(p.bin + f0);
-        }
-        for (int s0 = 0; s0 < 32; s0 += SPW) {
-            if (!((need >> s0) & ((SPW == 32 ? 0xffffffffu : ((1u << SPW) - 1))))) continue;
-            const int src = s0 + sub;
-            const uint64_t a0 = __shfl_sync(0xffffffffu, f0, src);
-            const uint64_t a1 = __shfl_sync(0xffffffffu, f1, src);
-            const bool on = (need >> src) & 1u;
-            uint64_t ha = 0, hb = 0;
-            if (on) {
-                for (uint64_t j = a0 + 1 + gl; j < a1; j += G) {
-                    uint64_t pcv = __ldcs(p.pc + j);
-                    uint32_t bn = __ldcs(p.bin + j);
-                    uint32_t pos = uint32_t(j - a0);
-                    ha += raw_a(pcv, bn, pos);
-                    hb += raw_b(pcv, bn, pos);
+            for (uint64_t blk = f0 & ~7ull; blk < f1; blk += 8) {
+                if (blk + 8 <= p.n_frames) {
+                    const ulonglong2* pv = reinterpret_cast<const ulonglong2*>(p.pc + blk);
+                    const ulonglong2 q0 = __ldcs(pv), q1 = __ldcs(pv + 1), q2 = __ldcs(pv + 2), q3 = __ldcs(pv + 3);
+                    const uint4 bq = __ldcs(reinterpret_cast<const uint4*>(p.bin + blk));
+                    const uint64_t pcs[8] = {q0.x, q0.y, q1.x, q1.y, q2.x, q2.y, q3.x, q3.y};
+                    const uint32_t bns[8] = {bq.x & 0xffffu, bq.x >> 16, bq.y & 0xffffu, bq.y >> 16,
+                                             bq.z & 0xffffu, bq.z >> 16, bq.w & 0xffffu, bq.w >> 16};
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) {
+                        const uint64_t j = blk + t;
+                        if (j == f0) {
+                            leaf_pc = pcs[t];
+                            leaf_bin = bns[t];
+                        }
+                        const uint64_t m = (j > f0 && j < f1) ? ~0ull : 0ull;
+                        const uint32_t pos = uint32_t(j - f0);
+                        ha += raw_a(pcs[t], bns[t], pos) & m;
+                        hb += raw_b(pcs[t], bns[t], pos) & m;
+                    }
+                } else {  // tail of the frame array: scalar
+                    for (uint64_t j = blk > f0 ? blk : f0; j < f1 && j < blk + 8; ++j) {
+                        const uint64_t pcv = __ldcs(p.pc + j);
+                        const uint32_t bv = __ldcs(p.bin + j);
+                        if (j == f0) {
+                            leaf_pc = pcv;
+                            leaf_bin = bv;
+                        } else {
+                            const uint32_t pos = uint32_t(j - f0);
+                            ha += raw_a(pcv, bv, pos);
+                            hb += raw_b(pcv, bv, pos);
+                        }
+                    }
                 }
             }
-#pragma unroll
-            for (int o = G / 2; o > 0; o >>= 1) {
-                ha += __shfl_xor_sync(0xffffffffu, ha, o);
-                hb += __shfl_xor_sync(0xffffffffu, hb, o);
-            }
-            // hand the chain fingerprint of sample src to lane src
-#pragma unroll
-            for (int g = 0; g < SPW; ++g) {
-                uint64_t xa = __shfl_sync(0xffffffffu, ha, g * G);
-                uint64_t xb = __shfl_sync(0xffffffffu, hb, g * G);
-                if (lane == s0 + g) {
-                    my_ra = mix_a(xa ^ (uint64_t(depth) * 0x8cb92ba72f3d8dd7ull));
-                    my_rb = mix_b(xb + uint64_t(depth));
-                    if (my_ra == 0) my_ra = 1;
-                    if (my_rb == 0) my_rb = 1;
+        }
+        const unsigned need = __ballot_sync(0xffffffffu, inwin && depth > 1);
+        uint64_t my_ra = mix_a(ha ^ (uint64_t(depth) * 0x8cb92ba72f3d8dd7ull));
+        uint64_t my_rb = mix_b(hb + uint64_t(depth));
+        if (my_ra == 0) my_ra = 1;
+        if (my_rb == 0) my_rb = 1;
+        // ---------------- phase 2: per-lane cache probe overlapped with the leaf lookup
+        const bool want_pfx = inwin && depth > 1;
+        // issue the first probe of both structures before either resolves
+        const uint32_t pslot = uint32_t(my_rb >> 24) & p.pfx_mask;
+        ulonglong2 pa = make_ulonglong2(0, 0), pb = make_ulonglong2(0, 0);
+        if (want_pfx) {
+            pa = __ldcg(reinterpret_cast<const ulonglong2*>(p.pfx + pslot));
+            pb = __ldcg(reinterpret_cast<const ulonglong2*>(p.pfx + pslot) + 1);
+        }
+        uint32_t leaf_key = kUnknownBit;
+        bool leaf_search = false;
+        uint32_t blo = 0, bhi = 0;
+        const DevTable* T = nullptr;
+        if (inwin) {
+            if (leaf_bin < p.n_bins) {
+                T = tabs + leaf_bin;
+                if (T->valid && leaf_pc >= T->base) {
+                    const uint64_t bk = (leaf_pc - T->base) >> T->shift;
+                    if (bk >= T->nb) {
+                        blo = bhi = T->n - 1;
+                    } else {
+                        blo = __ldg(T->bucket + bk);
+                        bhi = __ldg(T->bucket + bk + 1);
+                    }
+                    leaf_search = true;
                 }
+            } else {
+                *p.err_bin = 1;
             }
         }
-        // ---------------- phase 2: per-lane cache probe, leaf lookup
         uint64_t ta = 0, tb = 0;
-        bool hit = true;
-        if (inwin && depth > 1) hit = pfx_get(p.pfx, p.pfx_mask, my_ra, my_rb, ta, tb);
-        unsigned miss = __ballot_sync(0xffffffffu, inwin && depth > 1 && !hit);
+        bool hit = !want_pfx;
+        if (want_pfx) {
+            uint32_t slot = pslot;
+            for (int probe = 0; probe < 16; ++probe) {
+                if (pa.x == 0) break;
+                if (pa.x == my_ra) {
+                    if (pa.y == my_rb && (pb.x | pb.y) != 0) {
+                        ta = pb.x;
+                        tb = pb.y;
+                        hit = true;
+                    }
+                    if (pa.y == my_rb || pa.y == 0) break;
+                }
+                slot = (slot + 1) & p.pfx_mask;
+                pa = __ldcg(reinterpret_cast<const ulonglong2*>(p.pfx + slot));
+                pb = __ldcg(reinterpret_cast<const ulonglong2*>(p.pfx + slot) + 1);
+            }
+        }
+        if (leaf_search) {
+            while (blo < bhi) {
+                const uint32_t mid = (blo + bhi + 1) >> 1;
+                if (__ldg(&T->e[mid].x) <= leaf_pc) blo = mid; else bhi = mid - 1;
+            }
+            const ulonglong2 e = __ldg(T->e + blo);
+            if (p.mode == STG_LOOKUP_NEAREST_LOWER) {
+                leaf_key = uint32_t(e.y >> 32);
+            } else {
+                const uint32_t size = uint32_t(e.y);
+                const bool in = size == 0 ? leaf_pc == e.x : leaf_pc < e.x + uint64_t(size);
+                if (in) leaf_key = uint32_t(e.y >> 32);
+            }
+        }
+        if (inwin && leaf_key == kUnknownBit) leaf_key = kUnknownBit | unk_get(p.unk, leaf_bin, leaf_pc);
+        unsigned miss = __ballot_sync(0xffffffffu, want_pfx && !hit);
         hits += __popc(need & ~miss) * (lane == 0);
         misses += __popc(miss) * (lane == 0);
         while (miss) {
@@ -759,21 +815,20 @@ __global__ void __launch_bounds__(kThreads) k_sym_agg(AggParams p) {
         }
         uint64_t fa = 0, fb = 0;
         if (inwin) {
-            uint32_t key = resolve_frame(tabs, p.n_bins, leaf_pc, leaf_bin, p.mode, p.unk, p.err_bin);
-            ta += term_a(key, depth - 1);
-            tb += term_b(key, depth - 1);
+            ta += term_a(leaf_key, depth - 1);
+            tb += term_b(leaf_key, depth - 1);
             fp_finish(ta, tb, depth, fa, fb);
         }
         // ---------------- aggregate: identical (rank, stack) in the batch combine
         const unsigned act = __ballot_sync(0xffffffffu, inwin);
         if (act) {
-            unsigned m = __match_any_sync(0xffffffffu, inwin ? fa : 0ull) & __match_any_sync(0xffffffffu, r) & act;
+            const unsigned mr = __match_any_sync(0xffffffffu, r) & act;
+            const unsigned m = __match_any_sync(0xffffffffu, inwin ? fa : 0ull) & mr;
             if (inwin && (__ffs(m) - 1) == lane) {
                 if (!*(volatile int*)(p.tab_overflow + r))
                     agg_insert(p.slots + __ldg(p.tab_off + r), __ldg(p.tab_mask + r), fa, fb, uint32_t(i - rs),
                                __popc(m), p.tab_used + r, p.tab_overflow + r);
             }
-            unsigned mr = __match_any_sync(0xffffffffu, r) & act;
             if (inwin && (__ffs(mr) - 1) == lane) atomicAdd(p.n_in + r, (unsigned long long)__popc(mr));
         }
     }
