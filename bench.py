@@ -45,7 +45,7 @@ def log(*a):
 def args_parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--ranks", type=int, default=128)
@@ -170,7 +170,10 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            if self.recording:
+                self.rows.append([x.strip() for x in line.split(",")])
+
+    recording = False
 
     def __exit__(self, *exc):
         if self.proc:
@@ -278,9 +281,12 @@ def main():
     win = wl.window(a.ranks, a.spr, arrays, STG_MEM_DEVICE)
     log(f"[bench r{rank}] generated {win.n_samples} samples / {win.n_frames} frames in {time.time() - t0:.1f}s")
 
-    def step():
-        return ctx.window_run(win, ingest=False)
+    cfg = {"want_waterline": 1}  # every rank scored against its peers (compute_waterline + flag_ranks)
 
+    def step():
+        return ctx.window_run(win, cfg=cfg, ingest=False)
+
+    clk = ClockSampler(local).__enter__()  # started before warm-up: NVML start-up stays untimed
     for i in range(a.warmup):
         s = step()
         log(f"[bench r{rank}] warmup {i}: {s['ms_total']:.2f} ms (sym {s['ms_symbolize']:.2f}) "
@@ -291,15 +297,17 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        e0.record()
-        for _ in range(a.steps):
-            s = step()
-            sym_ms.append(s["ms_symbolize"])
-            tot_ms.append(s["ms_total"])
-            launches.append(s["kernel_launches"])
-        e1.record()
-        torch.cuda.synchronize()
+    clk.recording = True
+    e0.record()
+    for _ in range(a.steps):
+        s = step()
+        sym_ms.append(s["ms_symbolize"])
+        tot_ms.append(s["ms_total"])
+        launches.append(s["kernel_launches"])
+    e1.record()
+    torch.cuda.synchronize()
+    clk.recording = False
+    clk.__exit__(None, None, None)
     if dist:
         dist.barrier()
     ms = e0.elapsed_time(e1) / a.steps
@@ -346,13 +354,13 @@ def main():
         hwin = wl.window(a.ranks, a.spr, tuple(h.numpy().view(dt) for h, dt in
                                                 zip(host, (np.int64, np.uint64, np.uint64, np.uint16))),
                          STG_MEM_HOST)
-        ctx.window_run(hwin, ingest=False)  # warm
+        ctx.window_run(hwin, cfg=cfg, ingest=False)  # warm
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
         h2d = d2h = 0
         for _ in range(a.e2e_steps):
-            st = ctx.window_run(hwin, ingest=False)
+            st = ctx.window_run(hwin, cfg=cfg, ingest=False)
             r = ctx.report()
             h2d += st["h2d_bytes"]
             d2h += st["d2h_bytes"]

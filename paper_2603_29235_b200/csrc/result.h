@@ -73,6 +73,7 @@ struct Result {
     Report report;
     bool waterline_done = false;
     std::string waterline_json;
+    uint64_t wl_flags = 0, wl_F = 0;
     stg_run_stats stats{};
 };
 

@@ -11,6 +11,7 @@ namespace stg {
 void window_run(Ctx& c, const stg_window& w, const stg_config& cfg);
 std::string groupdata_json(Ctx& c);
 std::string report_json(Ctx& c);
+std::string waterline_json(Ctx& c);
 void run_resolve(Ctx& c, Result& res, uint64_t n, const uint64_t* pc, const uint16_t* bin, int32_t n_bins,
                  const uint8_t* ids, int mode, uint32_t* out);
 void rank_lines(Ctx& c, uint32_t i, std::vector<uint64_t>& key_off, std::vector<uint32_t>& keys,
@@ -183,7 +184,8 @@ int stg_result_waterline_json(stg_ctx* ctx, char* buf, uint64_t cap, uint64_t* n
     int rc = guard([&] {
         stg::Result& r = need_result(ctx);
         if (!r.waterline_done) stg::fail(STG_ESTATE, "run the window with want_waterline = 1");
-        s = r.waterline_json;
+        std::lock_guard<std::mutex> lk(ctx->impl.mu);
+        s = stg::waterline_json(ctx->impl);
     });
     if (rc) return rc;
     return copy_out(s, buf, cap, needed);

@@ -305,6 +305,65 @@ std::string groupdata_json(Ctx& c) {
     return j.s;
 }
 
+// compute_waterline / flag_ranks rendering from the device-resident result.
+std::string waterline_json(Ctx& c) {
+    Result& r = *c.result;
+    if (!r.waterline_json.empty()) return r.waterline_json;
+    const uint64_t F = r.wl_F, nf = r.wl_flags;
+    std::vector<double> hm(F), hs(F);
+    std::vector<uint8_t> hp(F);
+    std::vector<uint32_t> dense(F), fr(nf), ff(nf);
+    std::vector<double> ffr(nf), fth(nf);
+    d2h(c, hm.data(), "wl_mean", F);
+    d2h(c, hs.data(), "wl_sd", F);
+    d2h(c, hp.data(), "wl_pres", F);
+    d2h(c, dense.data(), "dense_final", F);
+    d2h(c, fr.data(), "wl_or", nf);
+    d2h(c, ff.data(), "wl_of", nf);
+    d2h(c, ffr.data(), "wl_ofr", nf);
+    d2h(c, fth.data(), "wl_oth", nf);
+    std::vector<int32_t> rids(r.n_window_ranks);
+    d2h(c, rids.data(), "rids", r.n_window_ranks);
+    JsonW j;
+    j.raw("{\"functions\": [");
+    bool first = true;
+    for (uint64_t f = 0; f < F; ++f) {
+        if (!hp[f]) continue;
+        if (!first) j.raw(", ");
+        first = false;
+        j.raw("[");
+        j.str(r.name_of(dense[f]));
+        j.raw(", ");
+        j.num(hm[f]);
+        j.raw(", ");
+        j.num(hs[f]);
+        j.raw("]");
+    }
+    j.raw("], \"flags\": [");
+    // flag_ranks order: ranks ascending, names in map order
+    std::vector<size_t> order(nf);
+    std::iota(order.begin(), order.end(), 0);
+    std::sort(order.begin(), order.end(), [&](size_t a, size_t b) {
+        return fr[a] != fr[b] ? fr[a] < fr[b] : ff[a] < ff[b];
+    });
+    for (size_t i = 0; i < nf; ++i) {
+        size_t k = order[i];
+        if (i) j.raw(", ");
+        j.raw("[");
+        j.num(int64_t(rids[fr[k]]));
+        j.raw(", ");
+        j.str(r.name_of(dense[ff[k]]));
+        j.raw(", ");
+        j.num(ffr[k]);
+        j.raw(", ");
+        j.num(fth[k]);
+        j.raw("]");
+    }
+    j.raw("]}");
+    r.waterline_json = j.s;
+    return j.s;
+}
+
 void window_run(Ctx& c, const stg_window& w, const stg_config& cfg) {
     if (!c.result) c.result = std::make_unique<Result>();
     Result& r = *c.result;

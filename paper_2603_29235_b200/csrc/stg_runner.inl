@@ -924,8 +924,17 @@ struct Runner {
         uint64_t cells = uint64_t(R) * F;
         if (cells > (1ull << 31)) fail(STG_ENOMEM, "rank x name matrix too large");
         d_incl = dev<unsigned long long>("incl", cells);
-        zero(d_incl, cells * 8);
-        LAUNCH(k_incl, grid_for(L * 32), kThreads, L, d_lkey, d_lcount, d_dn_off, d_dn, F, d_incl);
+        if (F * sizeof(unsigned) <= 160 * 1024) {
+            const size_t sm = F * sizeof(unsigned);
+            if (sm > 48 * 1024)
+                STG_CUDA(cudaFuncSetAttribute(k_incl_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+            k_incl_smem<<<R, 1024, sm, st>>>(R, d_line_off, d_lkey, d_lcount, d_dn_off, d_dn, F, d_incl);
+            STG_CUDA(cudaGetLastError());
+            ++launches;
+        } else {
+            zero(d_incl, cells * 8);
+            LAUNCH(k_incl, grid_for(L * 32), kThreads, L, d_lkey, d_lcount, d_dn_off, d_dn, F, d_incl);
+        }
         cudaEventRecord(ev[6], st);
     }
 
@@ -996,17 +1005,17 @@ struct Runner {
         if (!np) return out;
         uint64_t* keys = dev<uint64_t>("xf_keys", np);
         uint64_t* keys_s = dev<uint64_t>("xf_keys_s", np);
-        uint32_t* line = dev<uint32_t>("xf_line", np);
-        uint32_t* line_s = dev<uint32_t>("xf_line_s", np);
-        LAUNCH(k_pair_emit, grid_for(n), kThreads, n, lk, d_dn_off, d_dn, po, keys, line);
-        sort_pairs(keys, keys_s, line, line_s, np);
+        double* vals = dev<double>("xf_vals", np);
+        double* vals_s = dev<double>("xf_vals_s", np);
+        LAUNCH(k_pair_emit, grid_for(n), kThreads, n, lk, cnt, total, d_dn_off, d_dn, po, keys, vals);
+        sort_pairs(keys, keys_s, vals, vals_s, np);
         uint32_t* flag = dev<uint32_t>("xf_flag", np);
         LAUNCH(k_pair_segflags, grid_for(np), kThreads, np, keys_s, flag);
         uint32_t* seg = dev<uint32_t>("xf_seg", np);
         uint64_t nseg = select_flagged(flag, seg, np);
         uint32_t* of = dev<uint32_t>("xf_of", nseg);
         double* ov = dev<double>("xf_ov", nseg);
-        LAUNCH(k_pair_segsum, grid_for(nseg, 64), 64, nseg, seg, np, keys_s, cnt, total, of, ov);
+        LAUNCH(k_pair_segsum, grid_for(nseg, 64), 64, nseg, seg, np, keys_s, vals_s, of, ov);
         std::vector<uint32_t> hf(nseg);
         std::vector<double> hv(nseg);
         down(hf.data(), of, nseg);
@@ -1229,58 +1238,24 @@ struct Runner {
         zero(n_out, 8);
         LAUNCH(k_flag, grid_for(F * nr), kThreads, F, rows, int(nr), d_incl, d_totals, cfg.k, mean, sd, o_r, o_f, o_fr,
                o_th, n_out, cap);
-        uint64_t nf = std::min<uint64_t>(get1(n_out), cap);
-        std::vector<double> hm(F), hs(F);
-        std::vector<uint8_t> hp(F);
-        down(hm.data(), mean, F);
-        down(hs.data(), sd, F);
-        down(hp.data(), pres, F);
-        std::vector<uint32_t> fr(nf), ff(nf);
-        std::vector<double> ffr(nf), fth(nf);
-        down(fr.data(), o_r, nf);
-        down(ff.data(), o_f, nf);
-        down(ffr.data(), o_fr, nf);
-        down(fth.data(), o_th, nf);
-        JsonW j;
-        j.raw("{\"functions\": [");
-        bool first = true;
-        for (uint64_t f = 0; f < F; ++f) {
-            if (!hp[f]) continue;
-            if (!first) j.raw(", ");
-            first = false;
-            j.raw("[");
-            j.str(dense_name(uint32_t(f)));
-            j.raw(", ");
-            j.num(hm[f]);
-            j.raw(", ");
-            j.num(hs[f]);
-            j.raw("]");
-        }
-        j.raw("], \"flags\": [");
-        // flag_ranks order: ranks ascending, names in map order
-        std::vector<size_t> order(nf);
-        std::iota(order.begin(), order.end(), 0);
-        std::sort(order.begin(), order.end(), [&](size_t a, size_t b) {
-            return fr[a] != fr[b] ? fr[a] < fr[b] : ff[a] < ff[b];
-        });
-        for (size_t i = 0; i < nf; ++i) {
-            size_t k = order[i];
-            if (i) j.raw(", ");
-            j.raw("[");
-            j.num(int64_t(w.rank_ids[fr[k]]));
-            j.raw(", ");
-            j.str(dense_name(ff[k]));
-            j.raw(", ");
-            j.num(ffr[k]);
-            j.raw(", ");
-            j.num(fth[k]);
-            j.raw("]");
-        }
-        j.raw("]}");
-        res.waterline_json = j.s;
+        res.wl_flags = std::min<uint64_t>(get1(n_out), cap);
+        res.wl_F = F;
+        res.waterline_json.clear();  // rendered on request (waterline_json())
+    }
+
+    // STG_TRACE=1: host wall time per stage on stderr
+    bool trace = std::getenv("STG_TRACE") != nullptr;
+    std::chrono::steady_clock::time_point t_last = std::chrono::steady_clock::now();
+    void mark(const char* what) {
+        if (!trace) return;
+        auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[stg] %-12s %8.3f ms\n", what,
+                     std::chrono::duration<double, std::milli>(now - t_last).count());
+        t_last = now;
     }
 
     void run() {
+        mark("start");
         res.group = w.group;
         res.has_baseline = w.has_baseline != 0;
         res.baseline_delta = w.baseline_delta;
@@ -1290,10 +1265,14 @@ struct Runner {
         res.baseline_iteration_ms = w.baseline_iteration_ms;
         cudaEventRecord(ev[0], st);
         rank_space();
+        mark("rank_space");
         collectives();
         cudaEventRecord(ev[1], st);
+        mark("collectives");
         gpu_os();
+        mark("gpu_os");
         samples();
+        mark("samples+fold");
         if (ev_unset_fold()) {
             cudaEventRecord(ev[2], st);
             cudaEventRecord(ev[3], st);
@@ -1302,8 +1281,10 @@ struct Runner {
             cudaEventRecord(ev[6], st);
         }
         diagnose();
+        mark("diagnose");
         res.waterline_done = false;
         if (cfg.want_waterline) waterline();
+        mark("waterline");
         cudaEventRecord(ev[7], st);
         STG_CUDA(cudaStreamSynchronize(st));
         stg_run_stats& s = res.stats;
@@ -1331,6 +1312,7 @@ struct Runner {
         s.agg_attempts = uint32_t(res.agg_attempts);
         s.prefix_hits = res.pfx_hits;
         s.prefix_misses = res.pfx_misses;
+        mark("stats");
     }
     bool ev_unset_fold() const { return R == 0 || L == 0; }
 };

@@ -15,7 +15,10 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -1200,14 +1203,17 @@ __global__ void k_pair_count(uint64_t n, const uint64_t* lkey, const uint64_t* d
         cnt[i] = dn_off[s + 1] - dn_off[s];
     }
 }
-__global__ void k_pair_emit(uint64_t n, const uint64_t* lkey, const uint64_t* dn_off, const uint32_t* dn,
-                            const uint64_t* pair_off, uint64_t* keys, uint32_t* line) {
+__global__ void k_pair_emit(uint64_t n, const uint64_t* lkey, const unsigned long long* cnt_of, uint64_t total,
+                            const uint64_t* dn_off, const uint32_t* dn, const uint64_t* pair_off, uint64_t* keys,
+                            double* vals) {
+    const double t = __ull2double_rn(total);
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
         uint32_t s = lkey ? uint32_t(lkey[i]) : uint32_t(i);
+        const double x = __ddiv_rn(__ull2double_rn(cnt_of[i]), t);  // double(l.count) / double(total)
         uint64_t o = pair_off[i];
         for (uint64_t k = dn_off[s]; k < dn_off[s + 1]; ++k, ++o) {
             keys[o] = (uint64_t(dn[k]) << 32) | uint32_t(i);
-            line[o] = uint32_t(i);
+            vals[o] = x;
         }
     }
 }
@@ -1215,16 +1221,44 @@ __global__ void k_pair_segflags(uint64_t np, const uint64_t* keys, uint32_t* fla
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < np; i += uint64_t(gridDim.x) * blockDim.x)
         flag[i] = i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32);
 }
+// One thread per name: the reference's running sum, in line order, of the
+// precomputed per-line quotients (loads batched ahead of the dependent adds).
 __global__ void k_pair_segsum(uint64_t nseg, const uint32_t* seg, uint64_t np, const uint64_t* keys,
-                              const unsigned long long* cnt_of, uint64_t total, uint32_t* out_f, double* out_v) {
+                              const double* vals, uint32_t* out_f, double* out_v) {
     for (uint64_t g = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; g < nseg; g += uint64_t(gridDim.x) * blockDim.x) {
-        uint64_t a = seg[g], b = g + 1 < nseg ? seg[g + 1] : np;
-        double acc = 0.0, t = __ull2double_rn(total);
-        for (uint64_t i = a; i < b; ++i)
-            acc = __dadd_rn(acc, __ddiv_rn(__ull2double_rn(cnt_of[uint32_t(keys[i])]), t));
+        const uint64_t a = seg[g], b = g + 1 < nseg ? seg[g + 1] : np;
+        double acc = 0.0;
+        uint64_t i = a;
+        for (; i + 8 <= b; i += 8) {
+            double v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = vals[i + k];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc = __dadd_rn(acc, v[k]);
+        }
+        for (; i < b; ++i) acc = __dadd_rn(acc, vals[i]);
         out_f[g] = uint32_t(keys[a] >> 32);
         out_v[g] = acc;
     }
+}
+
+// Inclusive counts of one rank per CTA in shared memory (u32 counters; a rank
+// has < 2^32 samples), written out as a dense row.
+__global__ void k_incl_smem(int R, const uint64_t* line_off, const uint64_t* lkey, const unsigned long long* lcount,
+                            const uint64_t* dn_off, const uint32_t* dn, uint64_t F, unsigned long long* incl) {
+    extern __shared__ unsigned int sc[];
+    const int r = blockIdx.x;
+    for (uint64_t f = threadIdx.x; f < F; f += blockDim.x) sc[f] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (uint64_t l = line_off[r] + wid; l < line_off[r + 1]; l += nw) {
+        const uint32_t s = uint32_t(lkey[l]);
+        const unsigned c = unsigned(lcount[l]);
+        for (uint64_t k = dn_off[s] + lane; k < dn_off[s + 1]; k += 32) atomicAdd(sc + dn[k], c);
+    }
+    __syncthreads();
+    unsigned long long* row = incl + uint64_t(r) * F;
+    for (uint64_t f = threadIdx.x; f < F; f += blockDim.x) row[f] = sc[f];
 }
 
 __global__ void k_u32_to_u64(uint64_t n, const uint32_t* a, unsigned long long* b) {

@@ -95,3 +95,18 @@ def test_resolve_matches_lookup(ctx, mode):
     else:
         names_gpu, _ = ctx.resolve(q, bins, np.frombuffer(bid + other, np.uint8), mode=1)
         assert names_gpu == exp
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("seed,slow", [(7, 3), (4, 1)])
+def test_waterline_matches_reference(ctx, seed, slow):
+    """compute_waterline + flag_ranks (diagnosis.cpp:35-71) over the window's
+    CPU profiles: means/stddevs within 1e-6, flagged (rank, function) exact."""
+    win = small_window(seed=seed, ranks=8, samples_per_rank=600, slow_rank=slow)
+    ctx.window_run(win, cfg={"want_waterline": 1})
+    got = ctx.waterline()
+    exp = ref.waterline(win)
+    assert [f[0] for f in got["functions"]] == [f[0] for f in exp["functions"]]
+    assert_close([f[1:] for f in got["functions"]], [f[1:] for f in exp["functions"]], REL)
+    assert [(f[0], f[1]) for f in got["flags"]] == [(f[0], f[1]) for f in exp["flags"]]
+    assert_close([f[2:] for f in got["flags"]], [f[2:] for f in exp["flags"]], REL)
