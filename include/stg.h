@@ -63,6 +63,9 @@ typedef struct stg_ctx stg_ctx;
 /* ---------------------------------------------------------------- lifecycle */
 const char* stg_last_error(void);
 int stg_abi_version(void);
+/* sizeof(stg_window), sizeof(stg_config), sizeof(stg_run_stats) as compiled —
+ * lets a foreign binding (ctypes, cgo, JNI) verify its struct mirrors. */
+void stg_abi_sizes(uint64_t* window, uint64_t* config, uint64_t* stats);
 /* stg_create: one context per GPU (device ordinal). */
 int stg_create(int device, stg_ctx** out);
 void stg_destroy(stg_ctx* ctx);

@@ -65,6 +65,12 @@ extern "C" {
 const char* stg_last_error(void) { return g_err.c_str(); }
 int stg_abi_version(void) { return STG_ABI_VERSION; }
 
+void stg_abi_sizes(uint64_t* window, uint64_t* config, uint64_t* stats) {
+    if (window) *window = sizeof(stg_window);
+    if (config) *config = sizeof(stg_config);
+    if (stats) *stats = sizeof(stg_run_stats);
+}
+
 int stg_create(int device, stg_ctx** out) {
     return guard([&] {
         int n = 0;
