@@ -19,6 +19,9 @@ CSRC = PKG / "csrc"
 OUT = PKG / "_build"
 LIB = PKG / "libstg.so"
 BENCH_LIB = PKG / "libstg_bench.so"
+SHIM_LIB = PKG / "libstg_strata.so"
+REF_INC = Path("/root/reference/proj/core/include")
+JSON_DIR = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUDA_INC = "/usr/local/cuda/include"
@@ -66,6 +69,12 @@ def build(verbose: bool = False) -> Path:
     if _stale(BENCH_LIB, [CSRC / "bench_gen.cu"]):
         _run([NVCC, "-std=c++17", "-O3", *ARCH, "-Xcompiler", "-fPIC", "-shared",
               str(CSRC / "bench_gen.cu"), "-o", str(BENCH_LIB)])
+    # C++ drop-in shim over the C-ABI: needs the reference's headers (this
+    # container only; the built .so travels to the GPU box)
+    if REF_INC.exists() and _stale(SHIM_LIB, [CSRC / "shim" / "strata_stg.cpp", ROOT / "include" / "stg.h", LIB]):
+        _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", f"-I{ROOT / 'include'}", f"-I{REF_INC}",
+              f"-I{JSON_DIR}", str(CSRC / "shim" / "strata_stg.cpp"), "-o", str(SHIM_LIB),
+              f"-L{PKG}", "-lstg", "-Wl,-rpath,$ORIGIN"])
     return LIB
 
 

@@ -1,0 +1,297 @@
+// strata_stg.cpp — the C++ drop-in: re-defines the reference's hot-path entry
+// points on top of libstg's C-ABI (include/stg.h), with the reference's own
+// declarations (proj/core/include/strata/*.hpp, included in place) so callers
+// such as tools/strata.cpp and tests/acceptance.cpp relink unchanged:
+//
+//   strata::build_group_data   bundle.hpp:51-52  (bundle.cpp:252-324)   -> stg_window_run
+//   strata::resolve_stacks     symrepo.hpp:55-57 (symrepo.cpp:122-143)  -> stg_resolve
+//   strata::resolve_stack      symrepo.hpp:51-53 (symrepo.cpp:99-120)   -> stg_resolve
+//
+// The reference TUs that define these symbols are compiled with
+// -D<name>=<name>_reference (oracle/Makefile `dropin`), everything else of the
+// reference links as is.  Errors from the library come back as strata::Error
+// with the reference's message text.
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "json.hpp"
+#include "stg.h"
+#include "strata/bundle.hpp"
+#include "strata/symrepo.hpp"
+
+namespace {
+
+stg_ctx* ctx() {
+    static std::once_flag once;
+    static stg_ctx* c = nullptr;
+    std::call_once(once, [] {
+        const char* d = std::getenv("STG_DEVICE");
+        if (stg_create(d ? std::atoi(d) : 0, &c) != STG_OK)
+            throw strata::Error(std::string("libstg: ") + stg_last_error());
+        std::atexit([] { stg_destroy(c); });
+    });
+    return c;
+}
+
+void check(int rc) {
+    if (rc != STG_OK) throw strata::Error(stg_last_error());
+}
+
+// SymbolRepository::load (symrepo.cpp:90-97): the file bytes, if present.
+bool load_symr(const strata::SymbolRepository& repo, const strata::BuildId& id, std::vector<uint8_t>& out) {
+    std::ifstream in(repo.path_for(id), std::ios::binary);
+    if (!in) return false;
+    out.assign(std::istreambuf_iterator<char>(in), std::istreambuf_iterator<char>());
+    return true;
+}
+
+// Stages every referenced binary's table (idempotent per build id).
+void ingest_ids(const strata::SymbolRepository& repo, const std::vector<strata::BuildId>& ids) {
+    std::vector<uint8_t> bytes;
+    for (const auto& id : ids)
+        if (load_symr(repo, id, bytes))
+            check(stg_symtab_ingest(ctx(), id.bytes().data(), bytes.data(), bytes.size(), nullptr));
+}
+
+struct BinIndex {
+    std::map<strata::BuildId, uint16_t> idx;
+    std::vector<strata::BuildId> ids;
+    std::vector<uint8_t> raw;
+    uint16_t of(const strata::BuildId& id) {
+        auto it = idx.find(id);
+        if (it != idx.end()) return it->second;
+        uint16_t k = uint16_t(ids.size());
+        idx.emplace(id, k);
+        ids.push_back(id);
+        raw.insert(raw.end(), id.bytes().begin(), id.bytes().end());
+        return k;
+    }
+};
+
+std::string take_json(int (*fn)(stg_ctx*, char*, uint64_t, uint64_t*)) {
+    uint64_t need = 0;
+    check(fn(ctx(), nullptr, 0, &need));
+    std::string s(need, '\0');
+    check(fn(ctx(), s.data(), need, &need));
+    s.resize(need ? need - 1 : 0);
+    return s;
+}
+
+}  // namespace
+
+namespace strata {
+
+std::vector<std::vector<std::string>> resolve_stacks(const std::vector<std::vector<FrameRef>>& stacks,
+                                                     const SymbolRepository& repo, SymbolFile::LookupMode mode) {
+    BinIndex bins;
+    std::vector<uint64_t> pc;
+    std::vector<uint16_t> bin;
+    for (const auto& s : stacks)
+        for (const auto& f : s) {
+            pc.push_back(f.offset);
+            bin.push_back(bins.of(f.build_id));
+        }
+    ingest_ids(repo, bins.ids);
+    std::vector<uint32_t> keys(pc.size());
+    check(stg_resolve(ctx(), pc.size(), pc.data(), bin.data(), int32_t(bins.ids.size()), bins.raw.data(),
+                      mode == SymbolFile::LookupMode::ExactRange ? STG_LOOKUP_EXACT_RANGE : STG_LOOKUP_NEAREST_LOWER,
+                      keys.data()));
+    std::map<uint32_t, std::string> names;
+    std::vector<std::vector<std::string>> out;
+    out.reserve(stacks.size());
+    size_t k = 0;
+    for (const auto& s : stacks) {
+        std::vector<std::string> row;
+        row.reserve(s.size());
+        for (size_t i = 0; i < s.size(); ++i, ++k) {
+            auto it = names.find(keys[k]);
+            if (it == names.end()) {
+                uint64_t need = 0;
+                check(stg_name(ctx(), keys[k], nullptr, 0, &need));
+                std::string nm(need, '\0');
+                check(stg_name(ctx(), keys[k], nm.data(), need, &need));
+                nm.resize(need - 1);
+                it = names.emplace(keys[k], std::move(nm)).first;
+            }
+            row.push_back(it->second);
+        }
+        out.push_back(std::move(row));
+    }
+    return out;
+}
+
+std::vector<std::string> resolve_stack(const std::vector<FrameRef>& stack, const SymbolRepository& repo,
+                                       SymbolFile::LookupMode mode) {
+    return resolve_stacks({stack}, repo, mode).front();
+}
+
+GroupData build_group_data(const LoadedBundle& b, const DiagnosisConfig& config) {
+    (void)config;  // unused by the reference too (bundle.cpp:322)
+    // ---- LoadedBundle -> stg_window (structure of arrays)
+    BinIndex bins;
+    std::vector<int32_t> rank_ids;
+    std::vector<uint64_t> rank_off{0}, frame_off{0}, pc;
+    std::vector<int64_t> ts;
+    std::vector<uint16_t> bin;
+    for (const auto& [rank, stream] : b.samples) {
+        rank_ids.push_back(rank);
+        for (const StackSample& s : stream) {
+            if (s.rank != stream.front().rank) throw Error("aggregate_samples: mixed ranks");
+            ts.push_back(s.timestamp_ns);
+            for (const FrameRef& f : s.frames) {
+                pc.push_back(f.offset);
+                bin.push_back(bins.of(f.build_id));
+            }
+            frame_off.push_back(pc.size());
+        }
+        rank_off.push_back(ts.size());
+    }
+    ingest_ids(SymbolRepository(b.dir), bins.ids);
+    std::vector<int32_t> c_rank, c_group;
+    std::vector<uint8_t> c_kind;
+    std::vector<int64_t> c_entry, c_exit, c_dur;
+    for (const CollectiveEvent& e : b.collectives) {
+        c_rank.push_back(e.rank);
+        c_group.push_back(e.group);
+        c_kind.push_back(uint8_t(e.kind));
+        c_entry.push_back(e.host_entry_ns);
+        c_exit.push_back(e.host_exit_ns);
+        c_dur.push_back(e.gpu_duration_ns);
+    }
+    std::map<std::string, uint32_t> kid;
+    for (const GpuEvent& e : b.gpu_events) kid.emplace(e.kernel, 0);
+    std::vector<const char*> knames;
+    for (auto& [k, v] : kid) {
+        v = uint32_t(knames.size());
+        knames.push_back(k.c_str());
+    }
+    std::vector<int32_t> g_rank;
+    std::vector<uint32_t> g_k;
+    std::vector<int64_t> g_start, g_dur;
+    for (const GpuEvent& e : b.gpu_events) {
+        g_rank.push_back(e.rank);
+        g_k.push_back(kid.at(e.kernel));
+        g_start.push_back(e.start_ns);
+        g_dur.push_back(e.duration_ns);
+    }
+    std::map<std::string, uint32_t> cid;
+    for (const OsCounterRecord& o : b.os_counters) {
+        for (const auto& [k, v] : o.snapshot.interrupts) cid.emplace(k, 0);
+        for (const auto& [k, v] : o.snapshot.softirqs) cid.emplace(k, 0);
+    }
+    std::vector<const char*> cnames;
+    for (auto& [k, v] : cid) {
+        v = uint32_t(cnames.size());
+        cnames.push_back(k.c_str());
+    }
+    std::vector<int32_t> o_rank;
+    std::vector<int64_t> o_ws, o_p50, o_p99, o_mig, irq_v, sirq_v;
+    std::vector<uint64_t> irq_off{0}, sirq_off{0};
+    std::vector<uint32_t> irq_k, sirq_k;
+    for (const OsCounterRecord& o : b.os_counters) {
+        o_rank.push_back(o.rank);
+        o_ws.push_back(o.window_start_ns);
+        o_p50.push_back(o.snapshot.sched_delay_p50_ns);
+        o_p99.push_back(o.snapshot.sched_delay_p99_ns);
+        o_mig.push_back(o.snapshot.numa_migrations);
+        for (const auto& [k, v] : o.snapshot.interrupts) {
+            irq_k.push_back(cid.at(k));
+            irq_v.push_back(v);
+        }
+        for (const auto& [k, v] : o.snapshot.softirqs) {
+            sirq_k.push_back(cid.at(k));
+            sirq_v.push_back(v);
+        }
+        irq_off.push_back(irq_k.size());
+        sirq_off.push_back(sirq_k.size());
+    }
+    stg_window w{};
+    w.memory = STG_MEM_HOST;
+    w.group = b.group;
+    w.window_start_ns = b.window_start_ns;
+    w.window_end_ns = b.window_end_ns;
+    w.max_skew_ns = b.max_skew_ns;
+    w.n_ranks = int32_t(rank_ids.size());
+    w.rank_ids = rank_ids.data();
+    w.rank_sample_off = rank_off.data();
+    w.n_bins = int32_t(bins.ids.size());
+    w.bin_build_ids = bins.raw.data();
+    w.n_samples = ts.size();
+    w.sample_ts = ts.data();
+    w.sample_frame_off = frame_off.data();
+    w.n_frames = pc.size();
+    w.frame_pc = pc.data();
+    w.frame_bin = bin.data();
+    w.n_coll = c_rank.size();
+    w.coll_rank = c_rank.data();
+    w.coll_group = c_group.data();
+    w.coll_kind = c_kind.data();
+    w.coll_entry = c_entry.data();
+    w.coll_exit = c_exit.data();
+    w.coll_gpu_dur = c_dur.data();
+    w.n_group_ranks = int32_t(b.group_ranks.size());
+    w.group_ranks = b.group_ranks.data();
+    w.n_gpu = g_rank.size();
+    w.gpu_rank = g_rank.data();
+    w.gpu_kernel = g_k.data();
+    w.gpu_start = g_start.data();
+    w.gpu_dur = g_dur.data();
+    w.n_kernel_names = uint32_t(knames.size());
+    w.kernel_names = knames.data();
+    w.n_os = o_rank.size();
+    w.os_rank = o_rank.data();
+    w.os_window_start = o_ws.data();
+    w.os_p50 = o_p50.data();
+    w.os_p99 = o_p99.data();
+    w.os_migrations = o_mig.data();
+    w.os_irq_off = irq_off.data();
+    w.os_irq_key = irq_k.data();
+    w.os_irq_val = irq_v.data();
+    w.os_sirq_off = sirq_off.data();
+    w.os_sirq_key = sirq_k.data();
+    w.os_sirq_val = sirq_v.data();
+    w.n_counter_names = uint32_t(cnames.size());
+    w.counter_names = cnames.data();
+    stg_config cfg;
+    stg_config_default(&cfg);
+    check(stg_window_run(ctx(), &w, &cfg, nullptr));
+
+    // ---- result -> GroupData (diagnosis.hpp:192-201)
+    nlohmann::json j = nlohmann::json::parse(take_json(stg_result_groupdata_json));
+    GroupData d;
+    d.group = b.group;
+    d.baseline = b.baseline;
+    d.baseline_iteration_ms = b.baseline_iteration_ms;
+    for (const auto& p : j.at("cpu_profiles")) {
+        FoldedProfile& f = d.cpu_profiles[p.at("rank").get<int>()];
+        f.total = p.at("total").get<uint64_t>();
+        for (const auto& l : p.at("lines"))
+            f.lines.push_back({l.at(0).get<std::vector<std::string>>(), l.at(1).get<uint64_t>()});
+    }
+    for (const auto& p : j.at("gpu_profiles")) {
+        GpuProfile& g = d.gpu_profiles[p.at("rank").get<int>()];
+        for (const auto& k : p.at("kernels")) g.kernel_time_ns[k.at(0).get<std::string>()] = k.at(1).get<int64_t>();
+    }
+    for (const auto& p : j.at("os_snapshots")) {
+        OsSnapshot& o = d.os_snapshots[p.at("rank").get<int>()];
+        for (const auto& k : p.at("interrupts")) o.interrupts[k.at(0).get<std::string>()] = k.at(1).get<int64_t>();
+        for (const auto& k : p.at("softirqs")) o.softirqs[k.at(0).get<std::string>()] = k.at(1).get<int64_t>();
+        o.sched_delay_p50_ns = p.at("p50").get<int64_t>();
+        o.sched_delay_p99_ns = p.at("p99").get<int64_t>();
+        o.numa_migrations = p.at("migrations").get<int64_t>();
+    }
+    for (const auto& inst : j.at("lateness_per_instance")) {
+        std::map<int, double> m;
+        for (const auto& rl : inst) m[rl.at(0).get<int>()] = rl.at(1).get<double>();
+        d.lateness_per_instance.push_back(std::move(m));
+    }
+    d.iteration_times_ms = j.at("iteration_times_ms").get<std::vector<double>>();
+    return d;
+}
+
+}  // namespace strata

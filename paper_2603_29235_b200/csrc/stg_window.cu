@@ -593,12 +593,15 @@ __device__ __forceinline__ void agg_insert(AggSlot* T, uint32_t mask, uint64_t f
     *overflow = 1;
 }
 
-// Raw (unsymbolized) terms of a non-leaf frame: bin, pc and leaf-first position.
-__device__ __forceinline__ uint64_t raw_a(uint64_t pc, uint32_t bin, uint32_t pos) {
-    return mix_a(pc ^ (uint64_t(pos) << 40) ^ (uint64_t(bin) << 20) ^ 0x3c6ef372fe94f82bull);
+// Raw (unsymbolized) term of a non-leaf frame (bin, pc, leaf-first position):
+// one strong 64-bit mix per frame; the chain fingerprint is (Σ t, Σ rotr(t, 29)),
+// two sums that no single multiset identity makes equal for distinct chains.
+__device__ __forceinline__ uint64_t raw_t(uint64_t pc, uint32_t bin, uint32_t pos) {
+    return mix_a(pc ^ (uint64_t(bin | (pos << 16)) << 32) ^ 0x3c6ef372fe94f82bull);
 }
-__device__ __forceinline__ uint64_t raw_b(uint64_t pc, uint32_t bin, uint32_t pos) {
-    return mix_b((pc + 0x510e527fade682d1ull) * 0x9e3779b97f4a7c15ull ^ (uint64_t(bin) << 48 | pos));
+__device__ __forceinline__ void raw_add(uint64_t& ha, uint64_t& hb, uint64_t t) {
+    ha += t;
+    hb += (t >> 29) | (t << 35);
 }
 
 // Prefix cache.  Entries are immutable once published: writer claims hi by CAS,
@@ -686,35 +689,39 @@ __global__ void __launch_bounds__(kThreads) k_sym_agg(AggParams p) {
         if (inwin) {
             for (uint64_t blk = f0 & ~7ull; blk < f1; blk += 8) {
                 if (blk + 8 <= p.n_frames) {
+                    // read-only path, L1-allocating: the lane's next 16 B load takes the
+                    // other half of the same 32 B sector
                     const ulonglong2* pv = reinterpret_cast<const ulonglong2*>(p.pc + blk);
-                    const ulonglong2 q0 = __ldcs(pv), q1 = __ldcs(pv + 1), q2 = __ldcs(pv + 2), q3 = __ldcs(pv + 3);
-                    const uint4 bq = __ldcs(reinterpret_cast<const uint4*>(p.bin + blk));
+                    const ulonglong2 q0 = __ldg(pv), q1 = __ldg(pv + 1), q2 = __ldg(pv + 2), q3 = __ldg(pv + 3);
+                    const uint4 bq = __ldg(reinterpret_cast<const uint4*>(p.bin + blk));
                     const uint64_t pcs[8] = {q0.x, q0.y, q1.x, q1.y, q2.x, q2.y, q3.x, q3.y};
                     const uint32_t bns[8] = {bq.x & 0xffffu, bq.x >> 16, bq.y & 0xffffu, bq.y >> 16,
                                              bq.z & 0xffffu, bq.z >> 16, bq.w & 0xffffu, bq.w >> 16};
+                    const uint32_t pos0 = uint32_t(blk - f0);
+                    if (blk > f0 && blk + 8 <= f1) {  // interior block: all 8 frames are non-leaf
 #pragma unroll
-                    for (int t = 0; t < 8; ++t) {
-                        const uint64_t j = blk + t;
-                        if (j == f0) {
-                            leaf_pc = pcs[t];
-                            leaf_bin = bns[t];
+                        for (int t = 0; t < 8; ++t) raw_add(ha, hb, raw_t(pcs[t], bns[t], pos0 + t));
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) {
+                            const uint64_t j = blk + t;
+                            if (j == f0) {
+                                leaf_pc = pcs[t];
+                                leaf_bin = bns[t];
+                            }
+                            const uint64_t m = (j > f0 && j < f1) ? ~0ull : 0ull;
+                            raw_add(ha, hb, raw_t(pcs[t], bns[t], pos0 + t) & m);
                         }
-                        const uint64_t m = (j > f0 && j < f1) ? ~0ull : 0ull;
-                        const uint32_t pos = uint32_t(j - f0);
-                        ha += raw_a(pcs[t], bns[t], pos) & m;
-                        hb += raw_b(pcs[t], bns[t], pos) & m;
                     }
                 } else {  // tail of the frame array: scalar
                     for (uint64_t j = blk > f0 ? blk : f0; j < f1 && j < blk + 8; ++j) {
-                        const uint64_t pcv = __ldcs(p.pc + j);
-                        const uint32_t bv = __ldcs(p.bin + j);
+                        const uint64_t pcv = p.pc[j];
+                        const uint32_t bv = p.bin[j];
                         if (j == f0) {
                             leaf_pc = pcv;
                             leaf_bin = bv;
                         } else {
-                            const uint32_t pos = uint32_t(j - f0);
-                            ha += raw_a(pcv, bv, pos);
-                            hb += raw_b(pcv, bv, pos);
+                            raw_add(ha, hb, raw_t(pcv, bv, uint32_t(j - f0)));
                         }
                     }
                 }

@@ -1,0 +1,26 @@
+"""The drop-in proof: the reference's own acceptance gate (proj/tests/acceptance.cpp,
+compiled unchanged) relinked so that strata::build_group_data / resolve_stacks
+come from libstg's C++ shim (paper_2603_29235_b200/csrc/shim/strata_stg.cpp) on
+the GPU.  Every criterion that exercises the path (c1 scenario classification
+over 60 simulator bundles, c7 symbolization round trip and misattribution, c9
+clock alignment, c11 temporal threshold) must still PASS.
+Built by oracle/Makefile `dropin` (needs /root/reference at build time only).
+"""
+import subprocess
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+STG = ROOT / "oracle" / "_ref" / "acceptance_stg"
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not STG.exists(), reason="oracle/_ref/acceptance_stg not built (make -C oracle dropin)")
+def test_reference_acceptance_gate_relinked_on_gpu():
+    r = subprocess.run([str(STG)], capture_output=True, text=True, timeout=900)
+    print(r.stdout)
+    lines = [l for l in r.stdout.splitlines() if "criterion" in l]
+    assert len(lines) == 11, r.stdout + r.stderr
+    assert all(l.startswith("PASS") for l in lines), r.stdout
+    assert r.returncode == 0
