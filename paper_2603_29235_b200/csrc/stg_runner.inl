@@ -634,10 +634,20 @@ struct Runner {
             if (need < grid) grid = unsigned(std::max<uint64_t>(need, 1));
             cudaEventRecord(ev[2], st);
             const bool smem_tabs = w.n_bins <= kMaxSmemBins;
-            if (smem_tabs)
-                k_sym_agg<true><<<grid, kThreads, 0, st>>>(p);
-            else
-                k_sym_agg<false><<<grid, kThreads, 0, st>>>(p);
+            // STG_SYM_MINB (experiments): resident CTAs per SM the register budget targets
+            static const int minb = std::getenv("STG_SYM_MINB") ? std::atoi(std::getenv("STG_SYM_MINB")) : 4;
+            grid = unsigned(dev_sms) * unsigned(minb) * 4;
+            if (need < grid) grid = unsigned(std::max<uint64_t>(need, 1));
+#define STG_SYM(MB) \
+    (smem_tabs ? (void)(k_sym_agg<true, MB, 1><<<grid, kThreads, 0, st>>>(p)) : (void)(k_sym_agg<false, MB, 1><<<grid, kThreads, 0, st>>>(p)))
+            switch (minb) {
+                case 3: STG_SYM(3); break;
+                case 5: STG_SYM(5); break;
+                case 6: STG_SYM(6); break;
+                case 8: STG_SYM(8); break;
+                default: STG_SYM(4); break;
+            }
+#undef STG_SYM
             STG_CUDA(cudaGetLastError());
             ++launches;
             cudaEventRecord(ev[3], st);

@@ -639,8 +639,8 @@ __device__ __forceinline__ void pfx_put(PfxSlot* T, uint32_t mask, uint64_t ha, 
 //           open-addressing table with __match_any pre-aggregation;
 //  misses   the warp symbolizes the missing chains cooperatively and fills
 //           the cache.
-template <bool SMEM_TABS>
-__global__ void __launch_bounds__(kThreads) k_sym_agg(AggParams p) {
+template <bool SMEM_TABS, int MINB, int UB>
+__global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
     __shared__ DevTable s_tabs[kMaxSmemBins];
     if (SMEM_TABS) {
         for (uint32_t i = threadIdx.x; i < p.n_bins; i += blockDim.x) s_tabs[i] = p.tabs[i];
@@ -687,34 +687,50 @@ __global__ void __launch_bounds__(kThreads) k_sym_agg(AggParams p) {
         uint64_t leaf_pc = 0, ha = 0, hb = 0;
         uint32_t leaf_bin = 0;
         if (inwin) {
-            for (uint64_t blk = f0 & ~7ull; blk < f1; blk += 8) {
-                if (blk + 8 <= p.n_frames) {
-                    // read-only path, L1-allocating: the lane's next 16 B load takes the
-                    // other half of the same 32 B sector
-                    const ulonglong2* pv = reinterpret_cast<const ulonglong2*>(p.pc + blk);
-                    const ulonglong2 q0 = __ldg(pv), q1 = __ldg(pv + 1), q2 = __ldg(pv + 2), q3 = __ldg(pv + 3);
-                    const uint4 bq = __ldg(reinterpret_cast<const uint4*>(p.bin + blk));
-                    const uint64_t pcs[8] = {q0.x, q0.y, q1.x, q1.y, q2.x, q2.y, q3.x, q3.y};
-                    const uint32_t bns[8] = {bq.x & 0xffffu, bq.x >> 16, bq.y & 0xffffu, bq.y >> 16,
-                                             bq.z & 0xffffu, bq.z >> 16, bq.w & 0xffffu, bq.w >> 16};
-                    const uint32_t pos0 = uint32_t(blk - f0);
-                    if (blk > f0 && blk + 8 <= f1) {  // interior block: all 8 frames are non-leaf
+            // UB blocks of 8 frames per step: all their loads are issued before hashing
+            for (uint64_t blk = f0 & ~7ull; blk < f1; blk += 8 * UB) {
+                if (blk + 8 * UB <= p.n_frames) {
+                    uint64_t pcs[UB][8];
+                    uint32_t bns[UB][8];
 #pragma unroll
-                        for (int t = 0; t < 8; ++t) raw_add(ha, hb, raw_t(pcs[t], bns[t], pos0 + t));
-                    } else {
+                    for (int u = 0; u < UB; ++u) {
+                        // read-only path, L1-allocating: the lane's next 16 B load takes the
+                        // other half of the same 32 B sector
+                        const uint64_t bb = blk + 8 * u;
+                        if (u == 0 || bb < f1) {
+                            const ulonglong2* pv = reinterpret_cast<const ulonglong2*>(p.pc + bb);
+                            const ulonglong2 q0 = __ldg(pv), q1 = __ldg(pv + 1), q2 = __ldg(pv + 2), q3 = __ldg(pv + 3);
+                            const uint4 bq = __ldg(reinterpret_cast<const uint4*>(p.bin + bb));
+                            pcs[u][0] = q0.x; pcs[u][1] = q0.y; pcs[u][2] = q1.x; pcs[u][3] = q1.y;
+                            pcs[u][4] = q2.x; pcs[u][5] = q2.y; pcs[u][6] = q3.x; pcs[u][7] = q3.y;
+                            bns[u][0] = bq.x & 0xffffu; bns[u][1] = bq.x >> 16; bns[u][2] = bq.y & 0xffffu;
+                            bns[u][3] = bq.y >> 16; bns[u][4] = bq.z & 0xffffu; bns[u][5] = bq.z >> 16;
+                            bns[u][6] = bq.w & 0xffffu; bns[u][7] = bq.w >> 16;
+                        }
+                    }
 #pragma unroll
-                        for (int t = 0; t < 8; ++t) {
-                            const uint64_t j = blk + t;
-                            if (j == f0) {
-                                leaf_pc = pcs[t];
-                                leaf_bin = bns[t];
+                    for (int u = 0; u < UB; ++u) {
+                        const uint64_t bb = blk + 8 * u;
+                        if (u > 0 && bb >= f1) break;
+                        const uint32_t pos0 = uint32_t(bb - f0);
+                        if (bb > f0 && bb + 8 <= f1) {  // interior block: all 8 frames are non-leaf
+#pragma unroll
+                            for (int t = 0; t < 8; ++t) raw_add(ha, hb, raw_t(pcs[u][t], bns[u][t], pos0 + t));
+                        } else {
+#pragma unroll
+                            for (int t = 0; t < 8; ++t) {
+                                const uint64_t j = bb + t;
+                                if (j == f0) {
+                                    leaf_pc = pcs[u][t];
+                                    leaf_bin = bns[u][t];
+                                }
+                                const uint64_t m = (j > f0 && j < f1) ? ~0ull : 0ull;
+                                raw_add(ha, hb, raw_t(pcs[u][t], bns[u][t], pos0 + t) & m);
                             }
-                            const uint64_t m = (j > f0 && j < f1) ? ~0ull : 0ull;
-                            raw_add(ha, hb, raw_t(pcs[t], bns[t], pos0 + t) & m);
                         }
                     }
                 } else {  // tail of the frame array: scalar
-                    for (uint64_t j = blk > f0 ? blk : f0; j < f1 && j < blk + 8; ++j) {
+                    for (uint64_t j = blk > f0 ? blk : f0; j < f1 && j < blk + 8 * UB; ++j) {
                         const uint64_t pcv = p.pc[j];
                         const uint32_t bv = p.bin[j];
                         if (j == f0) {
