@@ -1025,7 +1025,7 @@ struct Runner {
         uint64_t nseg = select_flagged(flag, seg, np);
         uint32_t* of = dev<uint32_t>("xf_of", nseg);
         double* ov = dev<double>("xf_ov", nseg);
-        LAUNCH(k_pair_segsum, grid_for(nseg, 64), 64, nseg, seg, np, keys_s, vals_s, of, ov);
+        LAUNCH(k_pair_segsum, grid_for(nseg * 32), kThreads, nseg, seg, np, keys_s, vals_s, of, ov);
         std::vector<uint32_t> hf(nseg);
         std::vector<double> hv(nseg);
         down(hf.data(), of, nseg);

@@ -1034,12 +1034,28 @@ struct SeqLess {
     const uint32_t* arena;
     const uint64_t* off;
     __device__ __forceinline__ int cmp(uint32_t a, uint32_t b) const {
-        const uint32_t* x = arena + off[a];
-        const uint32_t* y = arena + off[b];
-        uint64_t la = off[a + 1] - off[a], lb = off[b + 1] - off[b];
-        uint64_t n = la < lb ? la : lb;
-        for (uint64_t i = 0; i < n; ++i) {
-            uint32_t u = x[i], v = y[i];
+        const uint64_t oa = off[a], ob = off[b];
+        const uint32_t* x = arena + oa;
+        const uint32_t* y = arena + ob;
+        const uint64_t la = off[a + 1] - oa, lb = off[b + 1] - ob;
+        const uint64_t n = la < lb ? la : lb;
+        uint64_t i = 0;
+        if (((oa ^ ob) & 3) == 0) {  // same 16-byte phase: compare 4 names per load
+            for (; i < n && ((oa + i) & 3); ++i) {
+                const uint32_t u = x[i], v = y[i];
+                if (u != v) return u < v ? -1 : 1;
+            }
+            for (; i + 4 <= n; i += 4) {
+                const uint4 u = *reinterpret_cast<const uint4*>(x + i);
+                const uint4 v = *reinterpret_cast<const uint4*>(y + i);
+                if (u.x != v.x) return u.x < v.x ? -1 : 1;
+                if (u.y != v.y) return u.y < v.y ? -1 : 1;
+                if (u.z != v.z) return u.z < v.z ? -1 : 1;
+                if (u.w != v.w) return u.w < v.w ? -1 : 1;
+            }
+        }
+        for (; i < n; ++i) {
+            const uint32_t u = x[i], v = y[i];
             if (u != v) return u < v ? -1 : 1;
         }
         return la < lb ? -1 : (la > lb ? 1 : 0);
@@ -1244,29 +1260,40 @@ __global__ void k_pair_segflags(uint64_t np, const uint64_t* keys, uint32_t* fla
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < np; i += uint64_t(gridDim.x) * blockDim.x)
         flag[i] = i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32);
 }
-// One thread per name: the reference's running sum, in line order, of the
-// precomputed per-line quotients (loads batched ahead of the dependent adds).
+// One warp per name: the reference's running sum, in line order, of the
+// precomputed per-line quotients.  The warp loads 32 consecutive quotients per
+// step (coalesced); every lane then runs the same strictly sequential add chain
+// over them (shuffles are independent of the accumulator, so they issue ahead).
 __global__ void k_pair_segsum(uint64_t nseg, const uint32_t* seg, uint64_t np, const uint64_t* keys,
                               const double* vals, uint32_t* out_f, double* out_v) {
-    for (uint64_t g = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; g < nseg; g += uint64_t(gridDim.x) * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    for (uint64_t g = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; g < nseg;
+         g += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
         const uint64_t a = seg[g], b = g + 1 < nseg ? seg[g + 1] : np;
         double acc = 0.0;
-        uint64_t i = a;
-        for (; i + 8 <= b; i += 8) {
-            double v[8];
+        for (uint64_t c = a; c < b; c += 32) {
+            const double v = c + lane < b ? vals[c + lane] : 0.0;
+            const int n = int(b - c < 32 ? b - c : 32);
+            if (n == 32) {
 #pragma unroll
-            for (int k = 0; k < 8; ++k) v[k] = vals[i + k];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) acc = __dadd_rn(acc, v[k]);
+                for (int k = 0; k < 32; ++k) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, v, k));
+            } else {
+                for (int k = 0; k < n; ++k) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, v, k));
+            }
         }
-        for (; i < b; ++i) acc = __dadd_rn(acc, vals[i]);
-        out_f[g] = uint32_t(keys[a] >> 32);
-        out_v[g] = acc;
+        if (lane == 0) {
+            out_f[g] = uint32_t(keys[a] >> 32);
+            out_v[g] = acc;
+        }
     }
 }
 
 // Inclusive counts of one rank per CTA in shared memory (u32 counters; a rank
-// has < 2^32 samples), written out as a dense row.
+// has < 2^32 samples), written out as a dense row.  Each warp walks a contiguous
+// run of the rank's (sorted) lines, lane k owning distinct-name slot k of the
+// current line.  Consecutive lines share their root prefix, so lane k keeps a
+// pending (name, count) and only flushes it to shared memory when its name
+// changes: the hot root names cost one atomic per run instead of one per line.
 __global__ void k_incl_smem(int R, const uint64_t* line_off, const uint64_t* lkey, const unsigned long long* lcount,
                             const uint64_t* dn_off, const uint32_t* dn, uint64_t F, unsigned long long* incl) {
     extern __shared__ unsigned int sc[];
@@ -1274,11 +1301,26 @@ __global__ void k_incl_smem(int R, const uint64_t* line_off, const uint64_t* lke
     for (uint64_t f = threadIdx.x; f < F; f += blockDim.x) sc[f] = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (uint64_t l = line_off[r] + wid; l < line_off[r + 1]; l += nw) {
+    const uint64_t l0 = line_off[r], l1 = line_off[r + 1];
+    const uint64_t per = (l1 - l0 + nw - 1) / nw;
+    const uint64_t a = l0 + per * wid, b = a + per < l1 ? a + per : l1;
+    uint32_t pend_name = 0xffffffffu;
+    unsigned pend = 0;
+    for (uint64_t l = a; l < b; ++l) {
         const uint32_t s = uint32_t(lkey[l]);
         const unsigned c = unsigned(lcount[l]);
-        for (uint64_t k = dn_off[s] + lane; k < dn_off[s + 1]; k += 32) atomicAdd(sc + dn[k], c);
+        const uint64_t k0 = dn_off[s], k1 = dn_off[s + 1];
+        const uint64_t k = k0 + lane;
+        const uint32_t name = k < k1 ? dn[k] : 0xffffffffu;
+        if (name != pend_name) {
+            if (pend) atomicAdd(sc + pend_name, pend);
+            pend_name = name;
+            pend = 0;
+        }
+        if (name != 0xffffffffu) pend += c;
+        for (uint64_t kk = k + 32; kk < k1; kk += 32) atomicAdd(sc + dn[kk], c);
     }
+    if (pend) atomicAdd(sc + pend_name, pend);
     __syncthreads();
     unsigned long long* row = incl + uint64_t(r) * F;
     for (uint64_t f = threadIdx.x; f < F; f += blockDim.x) row[f] = sc[f];
