@@ -58,6 +58,9 @@ def args_parse():
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-budget-s", type=float, default=20.0)
+    p.add_argument("--config", default="c2", choices=["c2", "c4"],
+                   help="c2 = headline (samples/s); c4 = collective alignment, 1,024 ranks x 50k events")
+    p.add_argument("--events", type=int, default=50_000, help="c4: events per rank")
     return p.parse_args()
 
 
@@ -234,6 +237,57 @@ def peaks():
         return {}
 
 
+# ----------------------------------------------------------------------- c4
+def bench_c4(a, torch, stg, rank, local, world, dist):
+    """C4: NCCL collective-event alignment, 1,024 ranks x 50k AllReduce/AllGather
+    events per GPU (device-resident), NIC-softirq straggler.  Metric: events/s."""
+    from tests.synth import c4_window
+    ranks = 1024
+    win = c4_window(ranks=ranks, events_per_rank=a.events, seed=1 + rank, device=True, torch=torch)
+    ctx = stg.Context(local)
+    for _ in range(a.warmup):
+        s = ctx.window_run(win)
+        log(f"[c4 r{rank}] warmup {s['ms_total']:.2f} ms (collectives {s['ms_collectives']:.2f}) "
+            f"instances={s['n_instances']} windowed={s['n_windowed']}")
+    rep = ctx.report()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    coll = []
+    e0.record()
+    for _ in range(a.steps):
+        s = ctx.window_run(win)
+        coll.append(s["ms_collectives"])
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / a.steps
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    n_ev = ranks * a.events
+    cm = float(np.median(coll))
+    algo = 24 * n_ev  # entry+exit read, lateness written (SURVEY.md §8(d) stage d)
+    peak = peaks().get("hbm_gbs", 6650.0)
+    line = {"metric": "collective events/sec aligned (match+align+lateness+straggler+verdict)",
+            "value": n_ev * world / (ms / 1e3), "unit": "events/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": f"C4: {ranks} ranks x {a.events} events (AllReduce/AllGather), straggler rank 4",
+                       "inputs": "collective arrays resident in HBM"},
+            "verdict": rep["verdict"], "flagged_ranks": rep["flagged_ranks"],
+            "stage_ms": {"collectives": cm, "total_device": s["ms_total"]},
+            "roofline": {"bound": "hbm", "achieved": round(algo / (cm / 1e3) / 1e9, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(algo / (cm / 1e3) / 1e9 / peak, 4), "traffic": None,
+                         "kernel": "collective stage (k_coll_* + k_straggler_*)", "algorithmic_bytes": algo}}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 # --------------------------------------------------------------------- main
 def main():
     a = args_parse()
@@ -270,6 +324,8 @@ def main():
 
     import paper_2603_29235_b200 as stg
     from paper_2603_29235_b200.abi import STG_MEM_DEVICE, STG_MEM_HOST
+    if a.config == "c4":
+        return bench_c4(a, torch, stg, rank, local, world, dist)
     wl = Workload(a, rank)
     ctx = stg.Context(local)
     t0 = time.time()

@@ -161,7 +161,9 @@ typedef struct stg_window {
     uint32_t n_counter_names;
     const char* const* counter_names;
 
-    /* historical baseline (BaselineProfile, diagnosis.hpp:142-147) */
+    /* historical baseline (BaselineProfile, diagnosis.hpp:142-147).  As in a
+     * LoadedBundle it is always present: has_baseline = 0 means an empty profile
+     * with the default delta 0.005, has_baseline_iteration = 0 means 0.0 ms. */
     int32_t has_baseline;
     double baseline_delta;
     uint32_t n_baseline;
@@ -169,6 +171,9 @@ typedef struct stg_window {
     const double* baseline_fracs;
     int32_t has_baseline_iteration;
     double baseline_iteration_ms;
+
+    /* stg_memory of the coll_* arrays (group_ranks stays host) */
+    int32_t coll_memory;
 } stg_window;
 
 /* DiagnosisConfig (diagnosis.hpp:203-210) + GpuDiffConfig (:83-92) + OsDiffConfig

@@ -691,8 +691,10 @@ def build_group_data(win, mode: int = EXACT_RANGE) -> dict:
         a["p99"] = max(a["p99"], int(win.os_p99[i]))
         a["migrations"] += int(win.os_migrations[i])
     gd["os_snapshots"] = osn
-    gd["baseline"] = {"delta": win.baseline_delta, "fractions": dict(win.baseline)} if win.has_baseline else None
-    gd["baseline_iteration_ms"] = win.baseline_iteration_ms
+    # LoadedBundle always carries a baseline (bundle.hpp:37-38); build_group_data
+    # copies it (bundle.cpp:257-258), empty / 0.0 when the bundle had none
+    gd["baseline"] = {"delta": win.baseline_delta if win.has_baseline else 0.005, "fractions": dict(win.baseline)}
+    gd["baseline_iteration_ms"] = win.baseline_iteration_ms if win.baseline_iteration_ms is not None else 0.0
     return gd
 
 

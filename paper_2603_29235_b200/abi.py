@@ -86,6 +86,7 @@ class StgWindow(C.Structure):
         ("baseline_fracs", _p),
         ("has_baseline_iteration", C.c_int32),
         ("baseline_iteration_ms", C.c_double),
+        ("coll_memory", C.c_int32),
     ]
 
 
@@ -212,6 +213,8 @@ class Window:
     frame_pc: object = field(default_factory=lambda: np.zeros(0, np.uint64))
     frame_bin: object = field(default_factory=lambda: np.zeros(0, np.uint16))
     memory: int = STG_MEM_HOST
+    coll_memory: int = STG_MEM_HOST
+    n_coll_: Optional[int] = None
     n_samples_: Optional[int] = None
     n_frames_: Optional[int] = None
     # collectives
@@ -288,13 +291,19 @@ class Window:
             w.sample_frame_off = _ptr(self.sample_frame_off, keep)
             w.frame_pc = _ptr(self.frame_pc, keep)
             w.frame_bin = _ptr(self.frame_bin, keep)
-        w.n_coll = len(self.coll_rank)
-        w.coll_rank = _ptr(np.asarray(self.coll_rank, np.int32), keep)
-        w.coll_group = _ptr(np.asarray(self.coll_group, np.int32), keep)
-        w.coll_kind = _ptr(np.asarray(self.coll_kind, np.uint8), keep)
-        w.coll_entry = _ptr(np.asarray(self.coll_entry, np.int64), keep)
-        w.coll_exit = _ptr(np.asarray(self.coll_exit, np.int64), keep)
-        w.coll_gpu_dur = _ptr(np.asarray(self.coll_gpu_dur, np.int64), keep)
+        w.coll_memory = self.coll_memory
+        if self.coll_memory == STG_MEM_HOST:
+            w.n_coll = len(self.coll_rank)
+            w.coll_rank = _ptr(np.asarray(self.coll_rank, np.int32), keep)
+            w.coll_group = _ptr(np.asarray(self.coll_group, np.int32), keep)
+            w.coll_kind = _ptr(np.asarray(self.coll_kind, np.uint8), keep)
+            w.coll_entry = _ptr(np.asarray(self.coll_entry, np.int64), keep)
+            w.coll_exit = _ptr(np.asarray(self.coll_exit, np.int64), keep)
+            w.coll_gpu_dur = _ptr(np.asarray(self.coll_gpu_dur, np.int64), keep)
+        else:
+            w.n_coll = self.n_coll_ if self.n_coll_ is not None else int(self.coll_rank.numel())
+            for f in ("coll_rank", "coll_group", "coll_kind", "coll_entry", "coll_exit", "coll_gpu_dur"):
+                setattr(w, f, _ptr(getattr(self, f), keep))
         w.n_group_ranks = len(self.group_ranks)
         w.group_ranks = _ptr(np.asarray(self.group_ranks, np.int32), keep)
         w.n_gpu = len(self.gpu_rank)

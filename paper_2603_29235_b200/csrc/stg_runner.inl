@@ -187,7 +187,11 @@ struct Runner {
             const int32_t* d = up<int32_t>(nm, host, n);
             LAUNCH(k_max_rank, grid_for(n), kThreads, n, d, d_mm, d_mm + 1);
         };
-        scan(w.coll_rank, w.n_coll, "coll_rank");
+        if (w.coll_memory == STG_MEM_DEVICE) {
+            if (w.n_coll) LAUNCH(k_max_rank, grid_for(w.n_coll), kThreads, w.n_coll, w.coll_rank, d_mm, d_mm + 1);
+        } else {
+            scan(w.coll_rank, w.n_coll, "coll_rank");
+        }
         scan(w.gpu_rank, w.n_gpu, "gpu_rank");
         scan(w.os_rank, w.n_os, "os_rank");
         int out[2];
@@ -218,11 +222,12 @@ struct Runner {
         const uint64_t n = w.n_coll;
         if (n == 0) return;
         if (n >= 0xffffffffull) fail(STG_EINVAL, "too many collective events");
-        const int32_t* d_rank = static_cast<const int32_t*>(c.buf("coll_rank").p);  // uploaded in rank_space
-        const int32_t* d_group = up<int32_t>("coll_group", w.coll_group, n);
-        const uint8_t* d_kind = up<uint8_t>("coll_kind", w.coll_kind, n);
-        const int64_t* d_entry = up<int64_t>("coll_entry", w.coll_entry, n);
-        const int64_t* d_exit = up<int64_t>("coll_exit", w.coll_exit, n);
+        const bool cdev = w.coll_memory == STG_MEM_DEVICE;
+        const int32_t* d_rank = cdev ? w.coll_rank : static_cast<const int32_t*>(c.buf("coll_rank").p);
+        const int32_t* d_group = cdev ? w.coll_group : up<int32_t>("coll_group", w.coll_group, n);
+        const uint8_t* d_kind = cdev ? w.coll_kind : up<uint8_t>("coll_kind", w.coll_kind, n);
+        const int64_t* d_entry = cdev ? w.coll_entry : up<int64_t>("coll_entry", w.coll_entry, n);
+        const int64_t* d_exit = cdev ? w.coll_exit : up<int64_t>("coll_exit", w.coll_exit, n);
         uint64_t* key = dev<uint64_t>("c_key", n);
         uint64_t* key_s = dev<uint64_t>("c_key_s", n);
         uint32_t* idx = dev<uint32_t>("c_idx", n);
@@ -1267,12 +1272,14 @@ struct Runner {
     void run() {
         mark("start");
         res.group = w.group;
-        res.has_baseline = w.has_baseline != 0;
-        res.baseline_delta = w.baseline_delta;
+        // a LoadedBundle always carries a baseline (bundle.hpp:37-38), which
+        // build_group_data copies (bundle.cpp:257-258): empty / 0.0 if absent
+        res.has_baseline = true;
+        res.baseline_delta = w.has_baseline ? w.baseline_delta : 0.005;
         res.baseline.clear();
         for (uint32_t i = 0; i < w.n_baseline; ++i) res.baseline[w.baseline_names[i]] = w.baseline_fracs[i];
-        res.has_baseline_iteration = w.has_baseline_iteration != 0;
-        res.baseline_iteration_ms = w.baseline_iteration_ms;
+        res.has_baseline_iteration = true;
+        res.baseline_iteration_ms = w.has_baseline_iteration ? w.baseline_iteration_ms : 0.0;
         cudaEventRecord(ev[0], st);
         rank_space();
         mark("rank_space");

@@ -230,3 +230,59 @@ def c2_tables(seed: int = 42, nsym: int = 1_000_000):
         bid = build_id(f"c2-{label}-{seed}")
         out.append((bid, starts, sizes, pack_symr(bid, starts, sizes, names)))
     return out
+
+
+def c4_window(ranks: int = 1024, events_per_rank: int = 2000, seed: int = 1, slow: int = 4,
+              device: bool = False, torch=None) -> Window:
+    """per rank, events alternating AllReduce/AllGather every
+    2 ms, exit = t + 1.2 ms +- 25 us, entry +- 25 us, per-rank clock skew
+    U[-10, +10] ms, the slow rank enters 0.6 ms late, NET_RX storm on its NIC.
+    device=True builds the collective arrays with torch on the GPU."""
+    rng = np.random.default_rng(seed)
+    skews = rng.integers(-10_000_000, 10_000_001, size=ranks).astype(np.int64)
+    E = events_per_rank
+    w = Window()
+    if device:
+        g = torch.Generator(device="cuda").manual_seed(seed)
+        dev = torch.device("cuda")
+        r = torch.arange(ranks, device=dev, dtype=torch.int64).repeat_interleave(E)
+        e = torch.arange(E, device=dev, dtype=torch.int64).repeat(ranks)
+        t = e * 2_000_000
+        sk = torch.from_numpy(skews).to(dev)[r]
+        je = torch.randint(-25_000, 25_001, (ranks * E,), device=dev, generator=g)
+        jx = torch.randint(-25_000, 25_001, (ranks * E,), device=dev, generator=g)
+        entry = t + je + sk + (r == slow).to(torch.int64) * 600_000
+        exit_ = t + 1_200_000 + jx + sk
+        w.coll_memory = 1
+        w.n_coll_ = ranks * E
+        w.coll_rank = r.to(torch.int32)
+        w.coll_group = torch.zeros(ranks * E, dtype=torch.int32, device=dev)
+        w.coll_kind = ((e % 2) * 2).to(torch.uint8)
+        w.coll_entry, w.coll_exit = entry, exit_
+        w.coll_gpu_dur = exit_ - entry
+    else:
+        r = np.repeat(np.arange(ranks, dtype=np.int64), E)
+        e = np.tile(np.arange(E, dtype=np.int64), ranks)
+        t = e * 2_000_000
+        entry = t + rng.integers(-25_000, 25_001, ranks * E) + skews[r] + (r == slow) * 600_000
+        exit_ = t + 1_200_000 + rng.integers(-25_000, 25_001, ranks * E) + skews[r]
+        w.coll_rank = r.astype(np.int32)
+        w.coll_group = np.zeros(ranks * E, np.int32)
+        w.coll_kind = ((e % 2) * 2).astype(np.uint8)
+        w.coll_entry, w.coll_exit = entry.astype(np.int64), exit_.astype(np.int64)
+        w.coll_gpu_dur = w.coll_exit - w.coll_entry
+    w.group_ranks = np.arange(ranks, dtype=np.int32)
+    span = E * 2_000_000
+    w.window_start_ns = 20_000_000
+    w.window_end_ns = span
+    w.max_skew_ns = 50_000_000
+    side = side_streams(rng, ranks, 1, span, span, slow, skews)
+    for k in ("c_rank", "c_entry", "c_exit", "g_rank", "g_kern", "g_start", "g_dur"):
+        side[k] = []
+    coll = {k: getattr(w, k) for k in ("coll_rank", "coll_group", "coll_kind", "coll_entry", "coll_exit",
+                                       "coll_gpu_dur", "group_ranks")}
+    apply_side(w, side, ranks)
+    for k, v in coll.items():
+        setattr(w, k, v)
+    w.symr = []
+    return w

@@ -110,3 +110,27 @@ def test_waterline_matches_reference(ctx, seed, slow):
     assert_close([f[1:] for f in got["functions"]], [f[1:] for f in exp["functions"]], REL)
     assert [(f[0], f[1]) for f in got["flags"]] == [(f[0], f[1]) for f in exp["flags"]]
     assert_close([f[2:] for f in got["flags"]], [f[2:] for f in exp["flags"]], REL)
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+def test_c4_collectives_1024_ranks_match_reference(ctx):
+    """C4 shape (1,024 ranks, alternating AllReduce/AllGather, NIC-softirq
+    straggler) at 2,000 events per rank: instances, offsets, lateness, the
+    straggler and the os-interference verdict exactly as the reference."""
+    from tests.synth import c4_window
+    win = c4_window(ranks=1024, events_per_rank=2000, seed=3)
+    stats, rep = _check_window(ctx, win, against_ref=True)
+    assert rep["verdict"] == "os-interference" and rep["flagged_ranks"] == [4]
+    assert stats["n_windowed"] > 0
+
+
+def test_collectives_irregular_streams_match_oracle(ctx):
+    """Missing events and late joiners force the sequential greedy fallback."""
+    from tests.synth import c4_window
+    win = c4_window(ranks=16, events_per_rank=300, seed=5)
+    keep = np.ones(len(win.coll_rank), bool)
+    rng = np.random.default_rng(1)
+    keep[rng.choice(len(keep), 40, replace=False)] = False  # drop events: partial instances
+    for f in ("coll_rank", "coll_group", "coll_kind", "coll_entry", "coll_exit", "coll_gpu_dur"):
+        setattr(win, f, getattr(win, f)[keep])
+    _check_window(ctx, win)
