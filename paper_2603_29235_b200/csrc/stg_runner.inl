@@ -234,15 +234,28 @@ struct Runner {
         uint32_t* idx_s = dev<uint32_t>("c_idx_s", n);
         int* d_err = dev<int>("c_err", 1);
         zero(d_err, sizeof(int));
-        LAUNCH(k_coll_keys, grid_for(n), kThreads, n, d_rank, d_group, d_kind, key, idx, d_err);
-        sort_pairs(key, key_s, idx, idx_s, n);
+        int* d_rg = dev<int>("c_ranges", 3);
+        {
+            int init[3] = {INT_MAX, INT_MIN, 0};
+            STG_CUDA(cudaMemcpyAsync(d_rg, init, sizeof init, cudaMemcpyHostToDevice, st));
+        }
+        LAUNCH(k_coll_ranges, grid_for(n), kThreads, n, d_group, d_kind, d_rg, d_rg + 1, d_rg + 2);
+        int rg[3];
+        down(rg, d_rg, 3);
+        auto bits_for = [](uint64_t v) { int b = 0; while (b < 64 && (v >> b)) ++b; return b; };
+        const int rbits = std::max(1, bits_for(uint64_t(span - 1)));
+        const int kbits = std::max(1, bits_for(uint64_t(rg[2])));
+        const int gbits = bits_for(uint64_t(int64_t(rg[1]) - rg[0]));
+        const uint64_t rmask = (1ull << rbits) - 1;
+        LAUNCH(k_coll_keys, grid_for(n), kThreads, n, d_rank, d_group, d_kind, rg[0], kbits, rbits, key, idx, d_err);
+        sort_pairs(key, key_s, idx, idx_s, n, gbits + kbits + rbits);
         int64_t* s_entry = dev<int64_t>("c_sentry", n);
         int64_t* s_exit = dev<int64_t>("c_sexit", n);
         unsigned long long* errs = dev<unsigned long long>("c_errs", 2);
         STG_CUDA(cudaMemsetAsync(errs, 0xff, 2 * sizeof(unsigned long long), st));
         uint32_t* seg_flag = dev<uint32_t>("c_segflag", n);
         uint32_t* stream_flag = dev<uint32_t>("c_stflag", n);
-        LAUNCH(k_coll_gather, grid_for(n), kThreads, n, key_s, idx_s, d_entry, d_exit, s_entry, s_exit, errs,
+        LAUNCH(k_coll_gather, grid_for(n), kThreads, n, key_s, idx_s, d_entry, d_exit, rbits, s_entry, s_exit, errs,
                errs + 1, seg_flag, stream_flag);
         unsigned long long he[2];
         down(he, errs, 2);
@@ -336,24 +349,37 @@ struct Runner {
         zero(isize, I * sizeof(unsigned));
         zero(iing, I * sizeof(unsigned));
         LAUNCH(k_coll_inst, grid_for(n), kThreads, n, key_s, nullptr, stream_of_pos, d_ibase, inst_local, s_exit,
-               d_member, inst_of, imax, isize, iing);
-        // align_clocks
+               d_member, inst_of, imax, isize, iing, rmask);
+        // align_clocks: deltas of complete-instance events, compacted, sorted per rank
+        int64_t* dval = dev<int64_t>("c_dval", n);
+        uint32_t* dflag = dev<uint32_t>("c_dflag", n);
+        long long* d_dmin = dev<long long>("c_dmin", 1);
+        zero(d_dmin, 8);
+        LAUNCH(k_coll_deltas, grid_for(n), kThreads, n, inst_of, s_exit, imax, iing, n_group, dval, dflag, d_dmin);
+        const long long dmin = get1(d_dmin);
+        const int dbits = std::max(1, bits_for(uint64_t(-dmin)));
+        if (rbits + dbits > 64) fail(STG_EINVAL, "barrier-exit spread too large for the median key");
+        uint64_t* dkey_all = dev<uint64_t>("c_dkey_all", n);
+        LAUNCH(k_coll_dkeys, grid_for(n), kThreads, n, key_s, rmask, dval, dmin, dbits, dkey_all);
         uint64_t* dkey = dev<uint64_t>("c_dkey", n);
+        uint64_t n_d;
+        {
+            unsigned long long* nsel = dev<unsigned long long>("c_nsel", 1);
+            size_t tb = 0;
+            STG_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, dkey_all, dflag, dkey, nsel, n, st));
+            STG_CUDA(cub::DeviceSelect::Flagged(temp(tb), tb, dkey_all, dflag, dkey, nsel, n, st));
+            ++launches;
+            n_d = get1(nsel);
+        }
         uint64_t* dkey_s = dev<uint64_t>("c_dkey_s", n);
-        unsigned long long* nd = dev<unsigned long long>("c_nd", 1);
-        int* rerr = dev<int>("c_rerr", 1);
-        zero(nd, 8);
-        zero(rerr, 4);
-        LAUNCH(k_coll_deltas, grid_for(n), kThreads, n, key_s, inst_of, s_exit, imax, iing, n_group, dkey, nd, rerr);
-        uint64_t n_d = get1(nd);
-        if (get1(rerr)) fail(STG_EINVAL, "barrier-exit spread beyond 2^39 ns is not supported");
-        sort_keys(dkey, dkey_s, n_d);
-        LAUNCH(k_coll_median, grid_for(span), kThreads, span, dkey_s, n_d, d_off, d_has_off);
+        sort_keys(dkey, dkey_s, n_d, rbits + dbits);
+        LAUNCH(k_coll_median, grid_for(span), kThreads, span, dkey_s, n_d, dbits, dmin, d_off, d_has_off);
         res.have_offsets = n_d > 0;
         // windowed complete instances ordered by max aligned exit
         unsigned long long* aexit = dev<unsigned long long>("c_aexit", I);
         zero(aexit, I * 8);  // int64 0: build_group_data initialises max_exit to 0
-        LAUNCH(k_coll_aligned_exit, grid_for(n), kThreads, n, key_s, inst_of, s_exit, iing, n_group, d_off, aexit);
+        LAUNCH(k_coll_aligned_exit, grid_for(n), kThreads, n, key_s, inst_of, s_exit, iing, n_group, d_off, aexit,
+               rmask);
         uint64_t* wkey = dev<uint64_t>("c_wkey", I);
         uint64_t* wkey_s = dev<uint64_t>("c_wkey_s", I);
         uint32_t* winst = dev<uint32_t>("c_winst", I);
@@ -370,10 +396,11 @@ struct Runner {
         LAUNCH(k_coll_winv, grid_for(n_w), kThreads, n_w, winst_s, inst_w);
         long long* wmin = dev<long long>("c_wmin", n_w);
         LAUNCH(k_fill_i64, grid_for(n_w), kThreads, wmin, n_w, LLONG_MAX);
-        LAUNCH(k_coll_minadj, grid_for(n), kThreads, n, key_s, inst_of, inst_w, s_entry, d_off, wmin);
+        LAUNCH(k_coll_minadj, grid_for(n), kThreads, n, key_s, inst_of, inst_w, s_entry, d_off, wmin, rmask);
         d_lat = dev<double>("lat", uint64_t(span) * n_w);
         LAUNCH(k_fill_f64, grid_for(uint64_t(span) * n_w), kThreads, d_lat, uint64_t(span) * n_w, nan(""));
-        LAUNCH(k_coll_lateness, grid_for(n), kThreads, n, key_s, inst_of, inst_w, s_entry, d_off, wmin, n_w, d_lat);
+        LAUNCH(k_coll_lateness, grid_for(n), kThreads, n, key_s, inst_of, inst_w, s_entry, d_off, wmin, n_w, d_lat,
+               rmask);
         if (n_w > 1) {
             double* it = dev<double>("c_it", n_w);
             LAUNCH(k_coll_itertimes, grid_for(n_w), kThreads, n_w, wkey_s, it);
@@ -392,8 +419,8 @@ struct Runner {
             double* zm = dev<double>("s_zm", span);
             uint64_t* fl = dev<uint64_t>("s_fl", span);
             uint8_t* hz = dev<uint8_t>("s_hz", span);
-            LAUNCH(k_straggler_rank, grid_for(span, 64), 64, n_w, span, d_lat, cfg.k, mu, sg, m, pres, ma, ml, zm, fl,
-                   hz);
+            LAUNCH(k_straggler_rank, grid_for(uint64_t(span) * 32), kThreads, n_w, span, d_lat, cfg.k, mu, sg, m, pres,
+                   ma, ml, zm, fl, hz);
             down(res.lat_present.data(), pres, span);
             down(res.mean_lat_all.data(), ma, span);
             down(res.mean_lat_alert.data(), ml, span);

@@ -82,21 +82,43 @@ __global__ void k_build_buckets(const ulonglong2* e, uint32_t n, uint64_t base, 
 }
 
 // ========================================================= collectives
-// key = (group ^ signbit) << 32 | kind << 24 | rank   (stable sort => per-rank order kept)
-__global__ void k_coll_keys(uint64_t n, const int32_t* rank, const int32_t* group, const uint8_t* kind,
-                            uint64_t* key, uint32_t* idx, int* err_rank) {
+// Group/kind ranges, so the stream key uses only the bits it needs.
+__global__ void k_coll_ranges(uint64_t n, const int32_t* group, const uint8_t* kind, int* gmin, int* gmax, int* kmax) {
+    int lo = INT_MAX, hi = INT_MIN, km = 0;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        lo = min(lo, group[i]);
+        hi = max(hi, group[i]);
+        km = max(km, int(kind[i]));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        km = max(km, __shfl_xor_sync(0xffffffffu, km, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(gmin, lo);
+        atomicMax(gmax, hi);
+        atomicMax(kmax, km);
+    }
+}
+
+// key = (group - gmin) << (kbits + rbits) | kind << rbits | rank: a stable sort
+// on it splits events into (group, kind) streams and per-rank runs while keeping
+// each rank's input order (collective.cpp:33-43).
+__global__ void k_coll_keys(uint64_t n, const int32_t* rank, const int32_t* group, const uint8_t* kind, int gmin,
+                            int kbits, int rbits, uint64_t* key, uint32_t* idx, int* err_rank) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x) {
         int32_t r = rank[i];
         if (r < 0 || r >= (1 << 24)) *err_rank = 1;
-        key[i] = (uint64_t(uint32_t(group[i]) ^ 0x80000000u) << 32) | (uint64_t(kind[i]) << 24) |
+        key[i] = (uint64_t(uint32_t(group[i] - gmin)) << (kbits + rbits)) | (uint64_t(kind[i]) << rbits) |
                  uint64_t(uint32_t(r) & 0xffffffu);
         idx[i] = uint32_t(i);
     }
 }
 
 __global__ void k_coll_gather(uint64_t n, const uint64_t* key, const uint32_t* idx, const int64_t* entry,
-                              const int64_t* exit_, int64_t* s_entry, int64_t* s_exit,
+                              const int64_t* exit_, int rbits, int64_t* s_entry, int64_t* s_exit,
                               unsigned long long* err_ee, unsigned long long* err_ord,
                               uint32_t* seg_flag, uint32_t* stream_flag) {
     for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < n;
@@ -107,7 +129,7 @@ __global__ void k_coll_gather(uint64_t n, const uint64_t* key, const uint32_t* i
         s_exit[p] = ex;
         if (en >= ex) atomicMin(err_ee, (unsigned long long)e);
         bool new_seg = p == 0 || key[p] != key[p - 1];
-        bool new_stream = p == 0 || (key[p] >> 24) != (key[p - 1] >> 24);
+        bool new_stream = p == 0 || (key[p] >> rbits) != (key[p - 1] >> rbits);
         if (!new_seg && en < entry[idx[p - 1]]) atomicMin(err_ord, (unsigned long long)e);
         seg_flag[p] = new_seg;
         stream_flag[p] = new_stream;
@@ -264,42 +286,50 @@ __global__ void k_coll_inst(uint64_t n, const uint64_t* key, const uint32_t* seg
                             const uint32_t* stream_of_pos, const uint64_t* inst_base,
                             const uint32_t* inst_local, const int64_t* s_exit, const uint8_t* group_member,
                             uint32_t* inst_of, unsigned long long* inst_max_exit, unsigned* inst_size,
-                            unsigned* inst_ingroup) {
+                            unsigned* inst_ingroup, uint64_t rmask) {
     for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < n;
          p += uint64_t(gridDim.x) * blockDim.x) {
         uint32_t s = stream_of_pos[p];
         uint32_t g = uint32_t(inst_base[s] + inst_local[p]);
         inst_of[p] = g;
-        uint32_t r = uint32_t(key[p] & 0xffffff);
+        uint32_t r = uint32_t(key[p] & rmask);
         atomicMax((long long*)&inst_max_exit[g], (long long)s_exit[p]);
         atomicAdd(&inst_size[g], 1u);
         if (group_member[r]) atomicAdd(&inst_ingroup[g], 1u);
     }
 }
 
-// align_clocks (collective.cpp:105-125) inputs: (rank, exit - max exit) over
-// complete instances, as a composite sort key rank<<40 | (delta + 2^39).
-__global__ void k_coll_deltas(uint64_t n, const uint64_t* key, const uint32_t* inst_of,
-                              const int64_t* s_exit, const unsigned long long* inst_max_exit,
-                              const unsigned* inst_ingroup, unsigned n_group, uint64_t* dkey,
-                              unsigned long long* n_out, int* range_err) {
+// align_clocks (collective.cpp:105-125) inputs: delta = exit - max exit for
+// events of complete instances (flag = 1), min delta for the key width.
+__global__ void k_coll_deltas(uint64_t n, const uint32_t* inst_of, const int64_t* s_exit,
+                              const unsigned long long* inst_max_exit, const unsigned* inst_ingroup, unsigned n_group,
+                              int64_t* dval, uint32_t* dflag, long long* dmin) {
+    long long lo = 0;
     for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < n;
          p += uint64_t(gridDim.x) * blockDim.x) {
-        uint32_t g = inst_of[p];
-        if (inst_ingroup[g] < n_group) continue;  // partial
-        int64_t d = s_exit[p] - (long long)inst_max_exit[g];
-        if (d < -(1ll << 39)) *range_err = 1;
-        uint64_t r = key[p] & 0xffffff;
-        unsigned long long o = atomicAdd(n_out, 1ull);
-        dkey[o] = (r << 40) | uint64_t(d + (1ll << 39));
+        const uint32_t g = inst_of[p];
+        const bool ok = inst_ingroup[g] >= n_group;
+        const int64_t d = ok ? s_exit[p] - (long long)inst_max_exit[g] : 0;
+        dval[p] = d;
+        dflag[p] = ok;
+        lo = min(lo, (long long)d);
     }
+    for (int o = 16; o > 0; o >>= 1) lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    if ((threadIdx.x & 31) == 0) atomicMin(dmin, lo);
+}
+// composite sort key rank << dbits | (delta - dmin)
+__global__ void k_coll_dkeys(uint64_t n, const uint64_t* key, uint64_t rmask, const int64_t* dval, long long dmin,
+                             int dbits, uint64_t* dkey) {
+    for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < n;
+         p += uint64_t(gridDim.x) * blockDim.x)
+        dkey[p] = ((key[p] & rmask) << dbits) | uint64_t(dval[p] - dmin);
 }
 
 // Per rank: median of its sorted deltas (even n: truncating int64 mean, :122).
-__global__ void k_coll_median(int rank_span, const uint64_t* dkey, uint64_t n, int64_t* off,
+__global__ void k_coll_median(int rank_span, const uint64_t* dkey, uint64_t n, int dbits, long long dmin, int64_t* off,
                               uint8_t* has_off) {
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rank_span; r += gridDim.x * blockDim.x) {
-        uint64_t lo_key = uint64_t(r) << 40, hi_key = uint64_t(r + 1) << 40;
+        uint64_t lo_key = uint64_t(r) << dbits, hi_key = uint64_t(r + 1) << dbits;
         uint64_t a = 0, b = n;
         while (a < b) {
             uint64_t m = (a + b) >> 1;
@@ -317,7 +347,8 @@ __global__ void k_coll_median(int rank_span, const uint64_t* dkey, uint64_t n, i
             off[r] = 0;
             continue;
         }
-        auto val = [&](uint64_t i) { return int64_t(dkey[lo + i] & ((1ull << 40) - 1)) - (1ll << 39); };
+        const uint64_t dm = dbits >= 64 ? ~0ull : ((1ull << dbits) - 1);
+        auto val = [&](uint64_t i) { return int64_t(dkey[lo + i] & dm) + dmin; };
         has_off[r] = 1;
         off[r] = cnt % 2 ? val(cnt / 2) : (val(cnt / 2 - 1) + val(cnt / 2)) / 2;
     }
@@ -326,12 +357,12 @@ __global__ void k_coll_median(int rank_span, const uint64_t* dkey, uint64_t n, i
 // Windowing (bundle.cpp:270-279): max aligned exit per complete instance, init 0.
 __global__ void k_coll_aligned_exit(uint64_t n, const uint64_t* key, const uint32_t* inst_of,
                                     const int64_t* s_exit, const unsigned* inst_ingroup, unsigned n_group,
-                                    const int64_t* off, unsigned long long* inst_aexit) {
+                                    const int64_t* off, unsigned long long* inst_aexit, uint64_t rmask) {
     for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < n;
          p += uint64_t(gridDim.x) * blockDim.x) {
         uint32_t g = inst_of[p];
         if (inst_ingroup[g] < n_group) continue;
-        uint32_t r = uint32_t(key[p] & 0xffffff);
+        uint32_t r = uint32_t(key[p] & rmask);
         atomicMax((long long*)&inst_aexit[g], (long long)(s_exit[p] - off[r]));
     }
 }
@@ -358,24 +389,24 @@ __global__ void k_coll_winv(uint64_t n_w, const uint32_t* winst_sorted, uint32_t
 
 // entry_lateness (collective.cpp:127-142): adj = entry - off, min, (adj-min)/1e6.
 __global__ void k_coll_minadj(uint64_t n, const uint64_t* key, const uint32_t* inst_of, const uint32_t* inst_w,
-                              const int64_t* s_entry, const int64_t* off, long long* wmin) {
+                              const int64_t* s_entry, const int64_t* off, long long* wmin, uint64_t rmask) {
     for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < n;
          p += uint64_t(gridDim.x) * blockDim.x) {
         uint32_t w = inst_w[inst_of[p]];
         if (w == 0xffffffffu) continue;
-        uint32_t r = uint32_t(key[p] & 0xffffff);
+        uint32_t r = uint32_t(key[p] & rmask);
         atomicMin(&wmin[w], (long long)(s_entry[p] - off[r]));
     }
 }
 
 __global__ void k_coll_lateness(uint64_t n, const uint64_t* key, const uint32_t* inst_of,
                                 const uint32_t* inst_w, const int64_t* s_entry, const int64_t* off,
-                                const long long* wmin, uint64_t n_w, double* lat /* [rank_span][n_w] */) {
+                                const long long* wmin, uint64_t n_w, double* lat /* [rank_span][n_w] */, uint64_t rmask) {
     for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < n;
          p += uint64_t(gridDim.x) * blockDim.x) {
         uint32_t w = inst_w[inst_of[p]];
         if (w == 0xffffffffu) continue;
-        uint32_t r = uint32_t(key[p] & 0xffffff);
+        uint32_t r = uint32_t(key[p] & rmask);
         int64_t adj = s_entry[p] - off[r];
         lat[uint64_t(r) * n_w + w] = __ddiv_rn(__ll2double_rn(adj - wmin[w]), 1e6);
     }
@@ -423,34 +454,56 @@ __global__ void k_straggler_inst(uint64_t n_w, int rank_span, const double* lat,
 
 // Per rank: flags, mean lateness (alert: over >=2-rank instances; median
 // reference: over all), mean z over flagged — each summed in instance order.
+// One warp per rank: lanes load 32 consecutive instances (coalesced row of the
+// rank-major matrix) and every lane runs the same in-order add chains.
 __global__ void k_straggler_rank(uint64_t n_w, int rank_span, const double* lat, double k, const double* mu_w,
                                  const double* sigma_w, const uint32_t* m_w, uint8_t* present,
                                  double* mean_all, double* mean_alert, double* z_mean, uint64_t* flags,
                                  uint8_t* has_z) {
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rank_span; r += gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    for (int r = int((blockIdx.x * blockDim.x + threadIdx.x) >> 5); r < rank_span;
+         r += int((gridDim.x * blockDim.x) >> 5)) {
         double s_all = 0.0, s2 = 0.0, sz = 0.0;
         uint64_t n_all = 0, n2 = 0, nz = 0;
         const double* row = lat + uint64_t(r) * n_w;
-        for (uint64_t w = 0; w < n_w; ++w) {
-            double l = row[w];
-            if (!(l == l)) continue;
-            s_all = __dadd_rn(s_all, l);
-            ++n_all;
-            if (m_w[w] < 2) continue;
-            s2 = __dadd_rn(s2, l);
-            ++n2;
-            double mu = mu_w[w], sg = sigma_w[w];
-            if (sg > 0.0 && l > __dadd_rn(mu, __dmul_rn(k, sg))) {
-                sz = __dadd_rn(sz, __ddiv_rn(__dsub_rn(l, mu), sg));
-                ++nz;
+        for (uint64_t c = 0; c < n_w; c += 32) {
+            const uint64_t w = c + lane;
+            double l = nan(""), z = 0.0;
+            bool two = false, fl = false;
+            if (w < n_w) {
+                l = row[w];
+                two = m_w[w] >= 2;
+                if (l == l && two) {
+                    const double mu = mu_w[w], sg = sigma_w[w];
+                    fl = sg > 0.0 && l > __dadd_rn(mu, __dmul_rn(k, sg));
+                    if (fl) z = __ddiv_rn(__dsub_rn(l, mu), sg);
+                }
+            }
+            const bool pres = l == l;
+            const unsigned mp = __ballot_sync(0xffffffffu, pres);
+            const unsigned m2 = __ballot_sync(0xffffffffu, pres && two);
+            const unsigned mf = __ballot_sync(0xffffffffu, fl);
+            n_all += __popc(mp);
+            n2 += __popc(m2);
+            nz += __popc(mf);
+            unsigned bits = mp;
+            while (bits) {  // in instance order
+                const int t = __ffs(bits) - 1;
+                bits &= bits - 1;
+                const double v = __shfl_sync(0xffffffffu, l, t);
+                s_all = __dadd_rn(s_all, v);
+                if ((m2 >> t) & 1u) s2 = __dadd_rn(s2, v);
+                if ((mf >> t) & 1u) sz = __dadd_rn(sz, __shfl_sync(0xffffffffu, z, t));
             }
         }
-        present[r] = n_all > 0;
-        mean_all[r] = n_all ? __ddiv_rn(s_all, double(n_all)) : 0.0;
-        mean_alert[r] = n2 ? __ddiv_rn(s2, double(n2)) : 0.0;
-        z_mean[r] = nz ? __ddiv_rn(sz, double(nz)) : 0.0;
-        flags[r] = nz;
-        has_z[r] = nz > 0;
+        if (lane == 0) {
+            present[r] = n_all > 0;
+            mean_all[r] = n_all ? __ddiv_rn(s_all, double(n_all)) : 0.0;
+            mean_alert[r] = n2 ? __ddiv_rn(s2, double(n2)) : 0.0;
+            z_mean[r] = nz ? __ddiv_rn(sz, double(nz)) : 0.0;
+            flags[r] = nz;
+            has_z[r] = nz > 0;
+        }
     }
 }
 
