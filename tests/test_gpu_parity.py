@@ -134,3 +134,15 @@ def test_collectives_irregular_streams_match_oracle(ctx):
     for f in ("coll_rank", "coll_group", "coll_kind", "coll_entry", "coll_exit", "coll_gpu_dur"):
         setattr(win, f, getattr(win, f)[keep])
     _check_window(ctx, win)
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("scenario,verdict", [("logging", "temporal-degradation"), ("thermal", None)])
+def test_c5_4096_ranks_against_baseline(ctx, scenario, verdict):
+    """C5: 4,096 ranks compared against the historical
+    baseline.  All-rank thermal injection: target_ranks = all; the reference
+    concludes `inconclusive` (temporal route is CPU-only) — parity, not the label."""
+    win = ref.simulate(scenario, 7, ranks=4096)
+    _, rep = _check_window(ctx, win, against_ref=True)
+    if verdict:
+        assert rep["verdict"] == verdict and len(rep["flagged_ranks"]) == 4096
