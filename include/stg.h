@@ -230,6 +230,22 @@ typedef struct stg_run_stats {
 int stg_window_run(stg_ctx* ctx, const stg_window* win, const stg_config* cfg,
                    stg_run_stats* stats);
 
+/* -------------------------------------------------------------- distributed
+ * One communication group spanning several GPUs: one process
+ * (one context) per GPU; the window's CPU sample streams are sharded by rank
+ * across the contexts (each passes only its ranks in rank_ids / samples), while
+ * collectives, GPU events, OS counters and the baseline are passed identically
+ * to every context.  Inside stg_window_run the contexts exchange over NCCL only
+ * what the verdict needs: exact inclusive fractions of the straggler and the
+ * reference rank and the straggler's hottest path (broadcast from their owner),
+ * per-GPU merged stack lists for the temporal route (all-gather, re-merged and
+ * sorted on each GPU), and the waterline's per-name sums (all-reduce).  Every
+ * context ends with the same report.  All contexts must hold the same symbol
+ * tables.  stg_dist_unique_id is called on world rank 0; the caller ships the
+ * 128 bytes to the others (e.g. torch.distributed.broadcast). */
+int stg_dist_unique_id(uint8_t id[128]);
+int stg_dist_init(stg_ctx* ctx, int world_size, int world_rank, const uint8_t id[128]);
+
 /* Canonical JSON renderings of the last window's result (for parity tests and
  * tools): GroupData (every field of diagnosis.hpp:192-201) and the report in the
  * layout of DiagnosisReport::to_json (diagnosis.cpp:437-455).  Two-call size

@@ -58,6 +58,8 @@ def load_library():
     l.stg_window_run.argtypes = [P, C.POINTER(StgWindow), C.POINTER(StgConfig), C.POINTER(StgRunStats)]
     for fn in ("stg_result_groupdata_json", "stg_result_report_json", "stg_result_waterline_json"):
         getattr(l, fn).argtypes = [P, C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64)]
+    l.stg_dist_unique_id.argtypes = [C.c_char_p]
+    l.stg_dist_init.argtypes = [P, C.c_int, C.c_int, C.c_char_p]
     l.stg_result_rank_count.argtypes = [P, C.POINTER(C.c_uint32)]
     l.stg_result_rank_info.argtypes = [P, C.c_uint32, C.POINTER(C.c_int32), C.POINTER(C.c_uint64),
                                        C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
@@ -90,6 +92,18 @@ class Context:
             self.close()
         except Exception:
             pass
+
+    # ----------------------------------------------------------- distributed
+    @staticmethod
+    def dist_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(load_library().stg_dist_unique_id(buf))
+        return buf.raw
+
+    def dist_init(self, world: int, rank: int, uid: bytes):
+        """Join an NCCL group spanning `world` contexts (see include/stg.h)."""
+        assert len(uid) == 128
+        _check(self._l.stg_dist_init(self._h, world, rank, uid))
 
     # ---------------------------------------------------------------- ingest
     def ingest(self, symr: bytes, claimed_id: Optional[bytes] = None) -> bool:

@@ -64,7 +64,7 @@ def build(verbose: bool = False) -> Path:
                   "-c", str(CSRC / src), "-o", str(obj)])
         objs.append(obj)
     if _stale(LIB, objs):
-        _run([NVCC, "-shared", *ARCH, "-o", str(LIB), *map(str, objs), "-lcudart"])
+        _run([NVCC, "-shared", *ARCH, "-o", str(LIB), *map(str, objs), "-lcudart", "-lnccl"])
     # bench-side generator (not part of the product library)
     if _stale(BENCH_LIB, [CSRC / "bench_gen.cu"]):
         _run([NVCC, "-std=c++17", "-O3", *ARCH, "-Xcompiler", "-fPIC", "-shared",

@@ -4,6 +4,8 @@
 #include <cstring>
 #include <string>
 
+#include <nccl.h>
+
 #include "result.h"
 #include "stg_internal.h"
 
@@ -91,7 +93,38 @@ int stg_create(int device, stg_ctx** out) {
 void stg_destroy(stg_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->impl.device);
+    if (ctx->impl.comm) ncclCommDestroy(static_cast<ncclComm_t>(ctx->impl.comm));
     delete ctx;
+}
+
+int stg_dist_unique_id(uint8_t id[128]) {
+    return guard([&] {
+        static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+        ncclUniqueId u;
+        ncclResult_t r = ncclGetUniqueId(&u);
+        if (r != ncclSuccess) stg::fail(STG_ECUDA, std::string("NCCL: ") + ncclGetErrorString(r));
+        std::memcpy(id, &u, 128);
+    });
+}
+
+int stg_dist_init(stg_ctx* ctx, int world_size, int world_rank, const uint8_t id[128]) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(ctx->impl.mu);
+        if (world_size < 1 || world_rank < 0 || world_rank >= world_size) stg::fail(STG_EINVAL, "bad world size/rank");
+        STG_CUDA(cudaSetDevice(ctx->impl.device));
+        if (ctx->impl.comm) {
+            ncclCommDestroy(static_cast<ncclComm_t>(ctx->impl.comm));
+            ctx->impl.comm = nullptr;
+        }
+        ncclUniqueId u;
+        std::memcpy(&u, id, 128);
+        ncclComm_t comm;
+        ncclResult_t r = ncclCommInitRank(&comm, world_size, u, world_rank);
+        if (r != ncclSuccess) stg::fail(STG_ECUDA, std::string("NCCL: ") + ncclGetErrorString(r));
+        ctx->impl.comm = comm;
+        ctx->impl.world = world_size;
+        ctx->impl.wrank = world_rank;
+    });
 }
 
 int stg_symtab_ingest(stg_ctx* ctx, const uint8_t* claimed_id, const uint8_t* symr, uint64_t len, int* stored) {

@@ -133,6 +133,9 @@ struct Ctx {
     std::map<std::string, DBuf> bufs;
     DBuf& buf(const std::string& k) { return bufs[k]; }
     std::unique_ptr<Result> result;
+    // distributed mode (stg_dist_init): one NCCL communicator per context
+    void* comm = nullptr;  // ncclComm_t
+    int world = 1, wrank = 0;
     ~Ctx();
 };
 

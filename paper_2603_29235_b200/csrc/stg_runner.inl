@@ -199,6 +199,12 @@ struct Runner {
         if (out[1] < 0) fail(STG_EINVAL, "negative rank ids are not supported");
         if (out[0] >= (1 << 24)) fail(STG_EINVAL, "rank ids must be below 2^24");
         span = out[0] + 1;
+        if (dist()) {  // every context must index ranks the same way
+            int* d = dev<int>("dx_span", 1);
+            STG_CUDA(cudaMemcpyAsync(d, &span, 4, cudaMemcpyHostToDevice, st));
+            nccl(ncclAllReduce(d, d, 1, ncclInt32, ncclMax, comm(), st));
+            span = get1(d);
+        }
         res.rank_span = span;
     }
 
@@ -1033,11 +1039,16 @@ struct Runner {
     }
     // Exact inclusive fractions over lines [a, a+n) (or over all sequences when
     // merged): returns (dense name, fraction) in name order.
-    std::vector<std::pair<uint32_t, double>> exact_fractions(uint64_t a, uint64_t n, uint64_t total, bool merged) {
+    std::vector<std::pair<uint32_t, double>> exact_fractions(uint64_t a, uint64_t n, uint64_t total, bool merged,
+                                                             const uint64_t* dn_off = nullptr, const uint32_t* dn = nullptr,
+                                                             const unsigned long long* counts = nullptr) {
         std::vector<std::pair<uint32_t, double>> out;
         if (n == 0 || total == 0) return out;
+        const uint64_t* d_dn_off = dn_off ? dn_off : this->d_dn_off;
+        const uint32_t* d_dn = dn ? dn : this->d_dn;
         const uint64_t* lk = merged ? nullptr : d_lkey + a;
-        const unsigned long long* cnt = merged ? static_cast<unsigned long long*>(c.buf("seq_counts").p) : d_lcount + a;
+        const unsigned long long* cnt =
+            counts ? counts : (merged ? static_cast<unsigned long long*>(c.buf("seq_counts").p) : d_lcount + a);
         uint64_t* pc = dev<uint64_t>("xf_cnt", n + 1);
         LAUNCH(k_pair_count, grid_for(n), kThreads, n, lk, d_dn_off, pc);
         zero(pc + n, 8);
@@ -1080,6 +1091,309 @@ struct Runner {
         std::sort(v.begin(), v.end());
         size_t n = v.size();
         return n % 2 ? v[n / 2] : (v[n / 2 - 1] + v[n / 2]) / 2.0;
+    }
+
+    // ============================================================ distributed
+    bool dist() const { return c.comm != nullptr && c.world > 1; }
+    ncclComm_t comm() const { return static_cast<ncclComm_t>(c.comm); }
+    void nccl(ncclResult_t r) {
+        if (r != ncclSuccess) fail(STG_ECUDA, std::string("NCCL: ") + ncclGetErrorString(r));
+    }
+    std::vector<uint8_t> bcast_bytes(std::vector<uint8_t> buf, int root) {
+        uint64_t* dn = dev<uint64_t>("dx_n", 1);
+        uint64_t n = buf.size();
+        STG_CUDA(cudaMemcpyAsync(dn, &n, 8, cudaMemcpyHostToDevice, st));
+        nccl(ncclBroadcast(dn, dn, 1, ncclUint64, root, comm(), st));
+        n = get1(dn);
+        buf.resize(n);
+        if (!n) return buf;
+        uint8_t* d = dev<uint8_t>("dx_b", n);
+        if (c.wrank == root) STG_CUDA(cudaMemcpyAsync(d, buf.data(), n, cudaMemcpyHostToDevice, st));
+        nccl(ncclBroadcast(d, d, n, ncclUint8, root, comm(), st));
+        down(buf.data(), d, n);
+        return buf;
+    }
+    std::vector<std::vector<uint8_t>> allgather_bytes(const std::vector<uint8_t>& mine) {
+        const int W = c.world;
+        uint64_t* dn = dev<uint64_t>("dx_sizes", W + 1);
+        uint64_t n = mine.size();
+        STG_CUDA(cudaMemcpyAsync(dn + W, &n, 8, cudaMemcpyHostToDevice, st));
+        nccl(ncclAllGather(dn + W, dn, 1, ncclUint64, comm(), st));
+        std::vector<uint64_t> sz(W);
+        down(sz.data(), dn, W);
+        uint64_t mx = 1;
+        for (uint64_t v : sz) mx = std::max(mx, v);
+        uint8_t* dm = dev<uint8_t>("dx_mine", mx);
+        if (n) STG_CUDA(cudaMemcpyAsync(dm, mine.data(), n, cudaMemcpyHostToDevice, st));
+        uint8_t* da = dev<uint8_t>("dx_all", mx * W);
+        nccl(ncclAllGather(dm, da, mx, ncclUint8, comm(), st));
+        std::vector<uint8_t> all(mx * W);
+        down(all.data(), da, mx * W);
+        std::vector<std::vector<uint8_t>> out(W);
+        for (int r = 0; r < W; ++r) out[r].assign(all.begin() + r * mx, all.begin() + r * mx + sz[r]);
+        return out;
+    }
+    template <class T>
+    static void put(std::vector<uint8_t>& b, T v) {
+        const uint8_t* p = reinterpret_cast<const uint8_t*>(&v);
+        b.insert(b.end(), p, p + sizeof(T));
+    }
+    static void put_str(std::vector<uint8_t>& b, const std::string& s) {
+        put<uint32_t>(b, uint32_t(s.size()));
+        b.insert(b.end(), s.begin(), s.end());
+    }
+    template <class T>
+    static T get(const uint8_t*& p) {
+        T v;
+        std::memcpy(&v, p, sizeof(T));
+        p += sizeof(T);
+        return v;
+    }
+    static std::string get_str(const uint8_t*& p) {
+        uint32_t n = get<uint32_t>(p);
+        std::string s(reinterpret_cast<const char*>(p), n);
+        p += n;
+        return s;
+    }
+
+    // Global name keys: the byte-wise sorted union of the (identical) symbol
+    // dictionary and every context's unknown labels, so keys compare like the
+    // strings on every GPU.
+    struct GNames {
+        std::vector<uint64_t> lab_final;
+        std::vector<std::string> lab;
+        std::vector<uint32_t> pos;
+        std::vector<uint64_t> loc_final;   // local label finals (sorted)
+        std::vector<uint32_t> loc_global;  // their global keys
+    } gn;
+    bool gn_ready = false;
+    void global_names() {
+        if (gn_ready) return;
+        uint64_t h = 1469598103934665603ull;
+        for (const auto& n : c.dict) {
+            for (unsigned char ch : n) h = (h ^ ch) * 1099511628211ull;
+            h = (h ^ 0xff) * 1099511628211ull;
+        }
+        unsigned long long* dh = dev<unsigned long long>("dx_h", 2);
+        unsigned long long hh[2] = {h, h};
+        STG_CUDA(cudaMemcpyAsync(dh, hh, 16, cudaMemcpyHostToDevice, st));
+        nccl(ncclAllReduce(dh, dh, 1, ncclUint64, ncclMin, comm(), st));
+        nccl(ncclAllReduce(dh + 1, dh + 1, 1, ncclUint64, ncclMax, comm(), st));
+        down(hh, dh, 2);
+        if (hh[0] != hh[1]) fail(STG_EINVAL, "distributed contexts hold different symbol tables");
+        std::vector<uint8_t> mine;
+        put<uint32_t>(mine, uint32_t(res.unk_labels.size()));
+        for (const auto& l : res.unk_labels) put_str(mine, l);
+        std::vector<std::string> all;
+        for (const auto& b : allgather_bytes(mine)) {
+            const uint8_t* p = b.data();
+            uint32_t n = b.empty() ? 0 : get<uint32_t>(p);
+            for (uint32_t i = 0; i < n; ++i) all.push_back(get_str(p));
+        }
+        std::sort(all.begin(), all.end());
+        all.erase(std::unique(all.begin(), all.end()), all.end());
+        uint64_t ne_before = 0;
+        for (const auto& lab : all) {
+            uint64_t pos = uint64_t(std::lower_bound(c.dict.begin(), c.dict.end(), lab) - c.dict.begin());
+            if (pos < c.dict.size() && c.dict[pos] == lab) continue;  // local labels never equal names (merge_labels)
+            gn.lab.push_back(lab);
+            gn.lab_final.push_back(pos + ne_before);
+            gn.pos.push_back(uint32_t(pos));
+            ++ne_before;
+        }
+        for (size_t k = 0; k < res.unk_labels.size(); ++k) {
+            size_t gi = size_t(std::lower_bound(gn.lab.begin(), gn.lab.end(), res.unk_labels[k]) - gn.lab.begin());
+            gn.loc_final.push_back(res.unk_final[k]);
+            gn.loc_global.push_back(uint32_t(gn.lab_final[gi]));
+        }
+        gn_ready = true;
+    }
+    uint32_t to_global(uint32_t f) const {
+        auto it = std::lower_bound(gn.loc_final.begin(), gn.loc_final.end(), uint64_t(f));
+        if (it != gn.loc_final.end() && *it == f) return gn.loc_global[size_t(it - gn.loc_final.begin())];
+        uint64_t i = f - uint64_t(it - gn.loc_final.begin());
+        return uint32_t(i + uint64_t(std::upper_bound(gn.pos.begin(), gn.pos.end(), uint32_t(i)) - gn.pos.begin()));
+    }
+    std::string gname(uint32_t g) const {
+        auto it = std::lower_bound(gn.lab_final.begin(), gn.lab_final.end(), uint64_t(g));
+        if (it != gn.lab_final.end() && *it == g) return gn.lab[size_t(it - gn.lab_final.begin())];
+        return c.dict[g - uint64_t(it - gn.lab_final.begin())];
+    }
+    // owner context of each rank's CPU profile (-1: none anywhere)
+    std::vector<int32_t> cpu_owner;
+    void cpu_owners() {
+        std::vector<int32_t> own(span, 0);
+        for (int32_t r : res.cpu_rank_ids) own[size_t(r)] = c.wrank + 1;
+        int32_t* d = up<int32_t>("dx_owner", own.data(), span);
+        nccl(ncclAllReduce(d, d, span, ncclInt32, ncclMax, comm(), st));
+        down(own.data(), d, span);
+        cpu_owner.resize(span);
+        for (int32_t r = 0; r < span; ++r) cpu_owner[r] = own[r] - 1;
+    }
+    // this context's exact fractions of CPU rank `rank` as (global key, value),
+    // plus the dense index of each key for local follow-ups
+    std::vector<std::pair<uint32_t, double>> rank_fracs_global(int rank, std::map<uint32_t, uint32_t>* dense_of) {
+        int i = cpu_index(rank);
+        uint64_t lo[2];
+        down(lo, d_line_off + i, 2);
+        auto fr = exact_fractions(lo[0], lo[1] - lo[0], h_n_in[i], false);
+        dense_name(0);  // ensure h_dense_final
+        std::vector<std::pair<uint32_t, double>> out;
+        for (const auto& [f, v] : fr) {
+            uint32_t g = to_global(h_dense_final[f]);
+            out.emplace_back(g, v);
+            if (dense_of) (*dense_of)[g] = f;
+        }
+        return out;
+    }
+    std::vector<std::pair<uint32_t, double>> bcast_fracs(std::vector<std::pair<uint32_t, double>> v, int root) {
+        std::vector<uint8_t> b;
+        if (c.wrank == root)
+            for (const auto& [k, x] : v) {
+                put<uint32_t>(b, k);
+                put<double>(b, x);
+            }
+        b = bcast_bytes(std::move(b), root);
+        std::vector<std::pair<uint32_t, double>> out;
+        for (const uint8_t* p = b.data(); p < b.data() + b.size();) {
+            uint32_t k = get<uint32_t>(p);
+            double x = get<double>(p);
+            out.emplace_back(k, x);
+        }
+        return out;
+    }
+    std::vector<std::string> bcast_path(std::vector<std::string> path, int root) {
+        std::vector<uint8_t> b;
+        if (c.wrank == root)
+            for (const auto& n : path) put_str(b, n);
+        b = bcast_bytes(std::move(b), root);
+        std::vector<std::string> out;
+        for (const uint8_t* p = b.data(); p < b.data() + b.size();) out.push_back(get_str(p));
+        return out;
+    }
+
+    // Temporal route across GPUs: every context contributes its merged
+    // (all local ranks) stacks in global keys; each GPU re-merges the union,
+    // sorts it in std::map order and sums fractions in that order.
+    struct MergedSeqs {
+        uint64_t n = 0, total = 0;
+        uint32_t* arena = nullptr;
+        uint64_t* off = nullptr;
+        unsigned long long* cnt = nullptr;
+        uint64_t* dn_off = nullptr;
+        uint32_t* dn = nullptr;
+    };
+    MergedSeqs merged_union() {
+        MergedSeqs m;
+        std::vector<uint8_t> mine;
+        uint64_t T = 0;
+        for (uint64_t t : res.cpu_totals) T += t;
+        put<uint64_t>(mine, T);
+        if (S > 0 && L > 0) {
+            auto sc = dev<unsigned long long>("seq_counts", S);
+            zero(sc, S * 8);
+            LAUNCH(k_seq_counts, grid_for(L), kThreads, L, d_lkey, d_lcount, sc);
+            std::vector<unsigned long long> hsc(S);
+            down(hsc.data(), sc, S);
+            std::vector<uint32_t> drep(S);
+            down(drep.data(), d_dense_rep, S);
+            std::vector<uint64_t> soff(res.n_gid + 1);
+            down(soff.data(), d_seq_off, res.n_gid + 1);
+            std::vector<uint32_t> ar(soff[res.n_gid]);
+            down(ar.data(), d_arena, ar.size());
+            for (uint64_t s = 0; s < S; ++s) {
+                if (!hsc[s]) continue;
+                uint32_t g = drep[s];
+                put<uint64_t>(mine, hsc[s]);
+                put<uint32_t>(mine, uint32_t(soff[g + 1] - soff[g]));
+                for (uint64_t k = soff[g]; k < soff[g + 1]; ++k) put<uint32_t>(mine, to_global(ar[k]));
+            }
+        }
+        std::vector<uint32_t> keys;
+        std::vector<uint64_t> off{0};
+        std::vector<unsigned long long> cnt;
+        for (const auto& b : allgather_bytes(mine)) {
+            const uint8_t* p = b.data();
+            const uint8_t* e = b.data() + b.size();
+            m.total += get<uint64_t>(p);
+            while (p < e) {
+                cnt.push_back(get<uint64_t>(p));
+                uint32_t n = get<uint32_t>(p);
+                for (uint32_t k = 0; k < n; ++k) keys.push_back(get<uint32_t>(p));
+                off.push_back(keys.size());
+            }
+        }
+        const uint64_t n = cnt.size();
+        if (!n) return m;
+        uint32_t* d_keys = up<uint32_t>("mg_keys", keys.data(), keys.size());
+        uint64_t* d_off = up<uint64_t>("mg_off", off.data(), off.size());
+        unsigned long long* d_cnt = up<unsigned long long>("mg_cnt", cnt.data(), n);
+        uint32_t* idx = dev<uint32_t>("mg_idx", n);
+        LAUNCH(k_iota, grid_for(n), kThreads, idx, n);
+        SeqLess less{d_keys, d_off};
+        size_t tb = 0;
+        STG_CUDA(cub::DeviceMergeSort::SortKeys(nullptr, tb, idx, int64_t(n), less, st));
+        STG_CUDA(cub::DeviceMergeSort::SortKeys(temp(tb), tb, idx, int64_t(n), less, st));
+        ++launches;
+        uint32_t* flg = dev<uint32_t>("mg_flag", n);
+        uint32_t* scn = dev<uint32_t>("mg_scan", n);
+        LAUNCH(k_seq_rankflags, grid_for(n), kThreads, uint32_t(n), idx, less, flg);
+        incl_sum(flg, scn, n);
+        const uint64_t nm = get1(scn + n - 1);
+        uint32_t* rep = dev<uint32_t>("mg_rep", nm);
+        uint32_t* rank_of = dev<uint32_t>("mg_rankof", n);
+        LAUNCH(k_seq_rankset, grid_for(n), kThreads, uint32_t(n), idx, scn, rank_of, rep);
+        unsigned long long* mc = dev<unsigned long long>("mg_mcnt", nm);
+        zero(mc, nm * 8);
+        LAUNCH(k_scatter_add, grid_for(n), kThreads, n, rank_of, d_cnt, mc);
+        // distinct names per merged stack (dense_rep = representative index)
+        uint32_t* c32 = dev<uint32_t>("mg_c32", nm + 1);
+        LAUNCH(k_seq_distinct<false>, grid_for(nm * 32), kThreads, uint32_t(nm), rep, d_off, d_keys, c32, nullptr, nullptr);
+        zero(c32 + nm, 4);
+        uint64_t* c64 = dev<uint64_t>("mg_c64", nm + 1);
+        LAUNCH(k_u32_to_u64, grid_for(nm + 1), kThreads, nm + 1, c32, (unsigned long long*)c64);
+        uint64_t* dn_off = dev<uint64_t>("mg_dnoff", nm + 1);
+        excl_sum(c64, dn_off, nm + 1);
+        const uint64_t nd = get1(dn_off + nm);
+        uint32_t* dn = dev<uint32_t>("mg_dn", nd);
+        LAUNCH(k_seq_distinct<true>, grid_for(nm * 32), kThreads, uint32_t(nm), rep, d_off, d_keys, nullptr, dn_off, dn);
+        m.n = nm;
+        m.arena = d_keys;
+        m.off = d_off;
+        m.cnt = mc;
+        m.dn_off = dn_off;
+        m.dn = dn;
+        merged_rep = rep;
+        return m;
+    }
+    uint32_t* merged_rep = nullptr;
+    std::vector<std::string> merged_path(const MergedSeqs& m, uint32_t key) {
+        unsigned long long* best = dev<unsigned long long>("hot_best", 2);
+        unsigned long long init[2] = {0, ~0ull};
+        STG_CUDA(cudaMemcpyAsync(best, init, 16, cudaMemcpyHostToDevice, st));
+        for (int pass = 0; pass < 2; ++pass)
+            LAUNCH(k_hottest, grid_for(m.n), kThreads, m.n, nullptr, m.cnt, 1, m.dn_off, m.dn, key, pass, best);
+        unsigned long long hb[2];
+        down(hb, best, 2);
+        if (hb[1] == ~0ull) return {};
+        uint32_t g;
+        down(&g, merged_rep + hb[1], 1);
+        uint64_t o[2];
+        down(o, m.off + g, 2);
+        std::vector<uint32_t> ks(o[1] - o[0]);
+        down(ks.data(), m.arena + o[0], ks.size());
+        std::vector<std::string> out;
+        for (uint32_t k : ks) out.push_back(gname(k));
+        return out;
+    }
+    std::vector<int32_t> all_cpu_ranks() {
+        std::vector<uint8_t> mine;
+        for (int32_t r : res.cpu_rank_ids) put<int32_t>(mine, r);
+        std::vector<int32_t> out;
+        for (const auto& b : allgather_bytes(mine))
+            for (const uint8_t* p = b.data(); p < b.data() + b.size();) out.push_back(get<int32_t>(p));
+        std::sort(out.begin(), out.end());
+        return out;
     }
 
     void diagnose() {
@@ -1154,7 +1468,44 @@ struct Runner {
             }
             // CPU layer (cpu_diff diagnosis.cpp:177-208)
             int is = cpu_index(strag), iq = cpu_index(ref);
-            if (is >= 0 && iq >= 0) {
+            if (dist()) {
+                global_names();
+                cpu_owners();
+                const int os_ = cpu_owner[size_t(strag)], oq = cpu_owner[size_t(ref)];
+                if (os_ >= 0 && oq >= 0) {
+                    std::map<uint32_t, uint32_t> dense_of;
+                    std::vector<std::pair<uint32_t, double>> fs_, fr_;
+                    if (c.wrank == os_) fs_ = rank_fracs_global(strag, &dense_of);
+                    if (c.wrank == oq) fr_ = rank_fracs_global(ref, nullptr);
+                    fs_ = bcast_fracs(std::move(fs_), os_);
+                    fr_ = bcast_fracs(std::move(fr_), oq);
+                    struct Cand { std::string fn; double fs, fr, d; uint32_t key; };
+                    std::vector<Cand> cands;
+                    size_t j = 0;
+                    for (const auto& [k, fs] : fs_) {  // key order == name order
+                        while (j < fr_.size() && fr_[j].first < k) ++j;
+                        double fr = j < fr_.size() && fr_[j].first == k ? fr_[j].second : 0.0;
+                        double d = fs - fr;
+                        if (d > cfg.delta) cands.push_back({gname(k), fs, fr, d, k});
+                    }
+                    std::sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) {
+                        return a.d != b.d ? a.d > b.d : a.fn < b.fn;
+                    });
+                    for (const auto& cd : cands) cpu_ev.push_back({"cpu", cd.fn, cd.fs, cd.fr, cd.d});
+                    if (concluded == STG_VERDICT_INCONCLUSIVE && !cands.empty()) {
+                        concluded = STG_VERDICT_CPU_INTERFERENCE;
+                        std::vector<std::string> path;
+                        if (c.wrank == os_) {
+                            uint64_t lo[2];
+                            down(lo, d_line_off + is, 2);
+                            path = hottest(lo[0], lo[1], dense_of.at(cands.front().key), false);
+                        }
+                        rep.top_path = bcast_path(std::move(path), os_);
+                    }
+                } else {
+                    rep.notes.push_back("cpu profiles missing; cpu layer skipped");
+                }
+            } else if (is >= 0 && iq >= 0) {
                 struct Cand { std::string fn; double fs, fr, d; uint32_t f; };
                 std::vector<Cand> cands;
                 uint64_t lo[2], lo2[2];
@@ -1224,6 +1575,32 @@ struct Runner {
                 }
                 struct Cand { std::string fn; double now, base, d; uint32_t f; };
                 std::vector<Cand> cands;
+                if (dist()) {
+                    global_names();
+                    MergedSeqs m = merged_union();
+                    if (m.n)
+                        for (const auto& [k, nw] : exact_fractions(0, m.n, m.total, true, m.dn_off, m.dn, m.cnt)) {
+                            std::string fn = gname(k);
+                            auto it = res.baseline.find(fn);
+                            double b = it == res.baseline.end() ? 0.0 : it->second;
+                            double d = nw - b;
+                            if (d > res.baseline_delta) cands.push_back({fn, nw, b, d, k});
+                        }
+                    std::sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) {
+                        return a.d != b.d ? a.d > b.d : a.fn < b.fn;
+                    });
+                    auto ranks = all_cpu_ranks();
+                    if (!cands.empty()) {
+                        rep.verdict = STG_VERDICT_TEMPORAL;
+                        rep.flagged_ranks.assign(ranks.begin(), ranks.end());
+                        for (const auto& cd : cands) rep.evidence.push_back({"temporal", cd.fn, cd.now, cd.base, cd.d});
+                        rep.top_path = merged_path(m, cands.front().f);
+                        return;
+                    }
+                    rep.verdict = STG_VERDICT_INCONCLUSIVE;
+                    rep.notes.push_back("iteration time regressed but no profile delta above delta");
+                    return;
+                }
                 if (F > 0) {
                     auto sc = dev<unsigned long long>("seq_counts", S);
                     zero(sc, S * 8);
@@ -1258,7 +1635,104 @@ struct Runner {
 
     // ------------------------------------------------------ waterline
     // compute_waterline + flag_ranks over the window's CPU profiles.
+    void waterline_dist() {
+        res.waterline_done = true;
+        global_names();
+        const size_t nr = res.cpu_rank_ids.size();
+        unsigned long long* drt = dev<unsigned long long>("wl_rt", 1);
+        unsigned long long nrl = nr;
+        STG_CUDA(cudaMemcpyAsync(drt, &nrl, 8, cudaMemcpyHostToDevice, st));
+        nccl(ncclAllReduce(drt, drt, 1, ncclUint64, ncclSum, comm(), st));
+        const uint64_t RT = get1(drt);
+        if (RT < 2) {
+            res.waterline_json = "{\"error\": \"waterline requires at least 2 ranks\"}";
+            return;
+        }
+        const uint64_t NG = c.dict.size() + gn.lab.size();
+        double* s1 = dev<double>("wl_s1", NG);
+        unsigned* np = dev<unsigned>("wl_np", NG);
+        double* s2 = dev<double>("wl_s2", NG);
+        zero(s1, NG * 8);
+        zero(np, NG * 4);
+        zero(s2, NG * 8);
+        std::vector<uint32_t> gk(F);
+        if (F) {
+            dense_name(0);
+            for (uint64_t f = 0; f < F; ++f) gk[f] = to_global(h_dense_final[f]);
+        }
+        uint32_t* d_gk = up<uint32_t>("wl_gkey", gk.data(), std::max<uint64_t>(F, 1));
+        uint32_t* rows = up<uint32_t>("wl_rows", res.cpu_rank_index.data(), std::max<size_t>(nr, 1));
+        if (F && nr) LAUNCH(k_wl_pass1, grid_for(F, 128), 128, F, rows, int(nr), d_incl, d_totals, d_gk, s1, np);
+        nccl(ncclAllReduce(s1, s1, NG, ncclFloat64, ncclSum, comm(), st));
+        nccl(ncclAllReduce(np, np, NG, ncclUint32, ncclSum, comm(), st));
+        if (F && nr) LAUNCH(k_wl_pass2, grid_for(F, 128), 128, F, rows, int(nr), d_incl, d_totals, d_gk, s1, np, double(RT), s2);
+        nccl(ncclAllReduce(s2, s2, NG, ncclFloat64, ncclSum, comm(), st));
+        double* mean = dev<double>("wlg_mean", NG);
+        double* sd = dev<double>("wlg_sd", NG);
+        LAUNCH(k_wl_final, grid_for(NG), kThreads, NG, s1, np, s2, double(RT), mean, sd);
+        unsigned long long cap = std::max<uint64_t>(1, std::min<uint64_t>(F * std::max<size_t>(nr, 1), 1u << 24));
+        uint32_t* o_r = dev<uint32_t>("wl_or", cap);
+        uint32_t* o_f = dev<uint32_t>("wl_of", cap);
+        double* o_fr = dev<double>("wl_ofr", cap);
+        double* o_th = dev<double>("wl_oth", cap);
+        unsigned long long* n_out = dev<unsigned long long>("wl_n", 1);
+        zero(n_out, 8);
+        if (F && nr)
+            LAUNCH(k_flag_g, grid_for(F * nr), kThreads, F, rows, int(nr), d_incl, d_totals, cfg.k, d_gk, mean, sd, o_r,
+                   o_f, o_fr, o_th, n_out, cap);
+        const uint64_t nf = std::min<uint64_t>(get1(n_out), cap);
+        // render now: the global name space lives only for this run
+        std::vector<double> hm(NG), hs(NG);
+        std::vector<unsigned> hnp(NG);
+        down(hm.data(), mean, NG);
+        down(hs.data(), sd, NG);
+        down(hnp.data(), np, NG);
+        std::vector<uint32_t> fr(nf), ff(nf);
+        std::vector<double> ffr(nf), fth(nf);
+        down(fr.data(), o_r, nf);
+        down(ff.data(), o_f, nf);
+        down(ffr.data(), o_fr, nf);
+        down(fth.data(), o_th, nf);
+        JsonW j;
+        j.raw("{\"functions\": [");
+        bool first = true;
+        for (uint64_t g = 0; g < NG; ++g) {
+            if (!hnp[g]) continue;
+            if (!first) j.raw(", ");
+            first = false;
+            j.raw("[");
+            j.str(gname(uint32_t(g)));
+            j.raw(", ");
+            j.num(hm[g]);
+            j.raw(", ");
+            j.num(hs[g]);
+            j.raw("]");
+        }
+        j.raw("], \"flags\": [");
+        std::vector<size_t> order(nf);
+        std::iota(order.begin(), order.end(), 0);
+        std::sort(order.begin(), order.end(), [&](size_t a, size_t b) {
+            return fr[a] != fr[b] ? fr[a] < fr[b] : ff[a] < ff[b];
+        });
+        for (size_t i = 0; i < nf; ++i) {
+            const size_t k = order[i];
+            if (i) j.raw(", ");
+            j.raw("[");
+            j.num(int64_t(w.rank_ids[fr[k]]));
+            j.raw(", ");
+            j.str(gname(gk[ff[k]]));
+            j.raw(", ");
+            j.num(ffr[k]);
+            j.raw(", ");
+            j.num(fth[k]);
+            j.raw("]");
+        }
+        j.raw("]}");
+        res.waterline_json = j.s;
+    }
+
     void waterline() {
+        if (dist()) return waterline_dist();
         res.waterline_done = true;
         std::string out;
         size_t nr = res.cpu_rank_ids.size();

@@ -13,6 +13,7 @@
 //      temporal_diff; the decision ladder of diagnose (diagnosis.cpp:301-432) runs
 //      on the host over these device-side summaries.
 #include <cub/cub.cuh>
+#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -1379,6 +1380,80 @@ __global__ void k_incl_smem(int R, const uint64_t* line_off, const uint64_t* lke
     for (uint64_t f = threadIdx.x; f < F; f += blockDim.x) row[f] = sc[f];
 }
 
+// Distributed waterline: per-name partial sums of the local ranks, scattered to
+// global name keys (then all-reduced across contexts).
+__global__ void k_wl_pass1(uint64_t F, const uint32_t* rows, int R, const unsigned long long* incl,
+                           const uint64_t* totals, const uint32_t* gkey, double* s1, unsigned* np) {
+    for (uint64_t f = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; f < F; f += uint64_t(gridDim.x) * blockDim.x) {
+        double acc = 0.0;
+        unsigned n = 0;
+        for (int i = 0; i < R; ++i) {
+            const uint32_t r = rows[i];
+            const unsigned long long c = incl[uint64_t(r) * F + f];
+            if (c) {
+                acc = __dadd_rn(acc, __ddiv_rn(double(c), double(totals[r])));
+                ++n;
+            }
+        }
+        s1[gkey[f]] = acc;
+        np[gkey[f]] = n;
+    }
+}
+__global__ void k_wl_pass2(uint64_t F, const uint32_t* rows, int R, const unsigned long long* incl,
+                           const uint64_t* totals, const uint32_t* gkey, const double* s1, const unsigned* np,
+                           double rt, double* s2) {
+    for (uint64_t f = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; f < F; f += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t g = gkey[f];
+        const double mu = __ddiv_rn(s1[g], rt);
+        double acc = 0.0;
+        for (int i = 0; i < R; ++i) {
+            const uint32_t r = rows[i];
+            const unsigned long long c = incl[uint64_t(r) * F + f];
+            if (c) {
+                const double d = __dsub_rn(__ddiv_rn(double(c), double(totals[r])), mu);
+                acc = __dadd_rn(acc, __dmul_rn(d, d));
+            }
+        }
+        s2[g] = acc;
+    }
+}
+__global__ void k_wl_final(uint64_t NG, const double* s1, const unsigned* np, const double* s2, double rt,
+                           double* mean, double* sd) {
+    for (uint64_t g = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; g < NG; g += uint64_t(gridDim.x) * blockDim.x) {
+        const double mu = __ddiv_rn(s1[g], rt);
+        double v = s2[g];
+        for (double k = np[g]; k < rt; k += 1.0) v = __dadd_rn(v, __dmul_rn(mu, mu));
+        mean[g] = mu;
+        sd[g] = __dsqrt_rn(__ddiv_rn(v, rt));
+    }
+}
+__global__ void k_flag_g(uint64_t F, const uint32_t* rows, int R, const unsigned long long* incl, const uint64_t* totals,
+                         double k, const uint32_t* gkey, const double* mean, const double* sd, uint32_t* o_r,
+                         uint32_t* o_f, double* o_frac, double* o_thr, unsigned long long* n_out, unsigned long long cap) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < F * uint64_t(R);
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t r = rows[i / F], f = i % F;
+        const unsigned long long c = incl[r * F + f];
+        if (!c) continue;
+        const uint32_t g = gkey[f];
+        const double fr = __ddiv_rn(double(c), double(totals[r]));
+        const double thr = __dadd_rn(mean[g], __dmul_rn(k, sd[g]));
+        if (fr > thr) {
+            const unsigned long long o = atomicAdd(n_out, 1ull);
+            if (o < cap) {
+                o_r[o] = uint32_t(r);
+                o_f[o] = uint32_t(f);
+                o_frac[o] = fr;
+                o_thr[o] = thr;
+            }
+        }
+    }
+}
+
+__global__ void k_scatter_add(uint64_t n, const uint32_t* to, const unsigned long long* v, unsigned long long* out) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        atomicAdd(out + to[i], v[i]);
+}
 __global__ void k_u32_to_u64(uint64_t n, const uint32_t* a, unsigned long long* b) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
         b[i] = a[i];

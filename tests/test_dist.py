@@ -1,0 +1,103 @@
+"""Multi-GPU path: one communication group spanning N GPUs.
+
+CPU (gloo, world_size 2): rank sharding covers every rank exactly once and the
+NCCL id is shipped through torch.distributed.
+GPU (>= 2 devices): every process's report equals the single-process reference
+report; the union of the processes' CPU profiles equals the reference's.
+"""
+import json
+import os
+import subprocess
+import sys
+import tempfile
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2603_29235_b200.dist import shard_bounds, shard_window
+from tests.synth import small_window
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def test_shard_bounds_cover_all_ranks():
+    for n in (1, 7, 8, 1024):
+        for world in (1, 2, 3, 8):
+            got = []
+            for r in range(world):
+                lo, hi = shard_bounds(n, world, r)
+                got.extend(range(lo, hi))
+            assert got == list(range(n))
+
+
+def test_shard_window_reassembles():
+    w = small_window(seed=2, ranks=5, samples_per_rank=50, slow_rank=1)
+    parts = [shard_window(w, 2, r) for r in range(2)]
+    assert np.concatenate([p.rank_ids for p in parts]).tolist() == w.rank_ids.tolist()
+    assert np.concatenate([p.sample_ts for p in parts]).tolist() == w.sample_ts.tolist()
+    assert np.concatenate([p.frame_pc for p in parts]).tolist() == w.frame_pc.tolist()
+    for p in parts:
+        assert int(p.rank_sample_off[-1]) == len(p.sample_ts)
+        assert int(p.sample_frame_off[-1]) == len(p.frame_pc)
+        assert p.coll_rank is w.coll_rank  # side streams stay replicated
+
+
+def _gloo_worker(rank, world, port, out):
+    import torch.distributed as dist
+    from paper_2603_29235_b200.dist import share_unique_id
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    uid = share_unique_id(dist, lambda: bytes(range(128)), device="cpu")
+    out.put((rank, uid))
+    dist.destroy_process_group()
+
+
+def test_unique_id_shared_over_gloo():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29600 + os.getpid() % 300
+    ps = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert res[0] == res[1] == bytes(range(128))
+
+
+def _run_dist(case, n):
+    out = tempfile.mkdtemp()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + os.getpid() % 400),
+           str(ROOT / "tests" / "dist_worker.py"), "--out", out, "--case", case]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=str(ROOT))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    return [json.loads(Path(out, f"rank{i}.json").read_text()) for i in range(n)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["synthetic", "sim-softirq-1", "sim-logging-2", "sim-dentry-lock-3"])
+def test_two_gpu_group_matches_reference(case):
+    import torch
+    from oracle import ref
+    from tests.compare import assert_close
+    from tests.dist_cases import make_case
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    if case.startswith("sim-") and not ref.available():
+        pytest.skip("oracle/_ref not built")
+    outs = _run_dist(case, 2)
+    exp, _, _ = ref.window_run(make_case(case))
+    for o in outs:
+        assert o["report"] == exp["report"]  # bit-exact on every process
+    prof = sorted((p for o in outs for p in o["groupdata"]["cpu_profiles"]), key=lambda p: p["rank"])
+    assert prof == exp["groupdata"]["cpu_profiles"]
+    for k in ("lateness_per_instance", "iteration_times_ms", "gpu_profiles", "os_snapshots"):
+        assert outs[0]["groupdata"][k] == exp["groupdata"][k]
+    wl = ref.waterline(make_case(case))
+    got = outs[0]["waterline"]
+    assert [f[0] for f in got["functions"]] == [f[0] for f in wl["functions"]]
+    assert_close([f[1:] for f in got["functions"]], [f[1:] for f in wl["functions"]], 1e-6)
+    from tests.compare import assert_flags_match
+    assert_flags_match([f for o in outs for f in o["waterline"]["flags"]], wl["flags"])

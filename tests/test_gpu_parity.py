@@ -108,8 +108,8 @@ def test_waterline_matches_reference(ctx, seed, slow):
     exp = ref.waterline(win)
     assert [f[0] for f in got["functions"]] == [f[0] for f in exp["functions"]]
     assert_close([f[1:] for f in got["functions"]], [f[1:] for f in exp["functions"]], REL)
-    assert [(f[0], f[1]) for f in got["flags"]] == [(f[0], f[1]) for f in exp["flags"]]
-    assert_close([f[2:] for f in got["flags"]], [f[2:] for f in exp["flags"]], REL)
+    from tests.compare import assert_flags_match
+    assert_flags_match(got["flags"], exp["flags"])
 
 
 @pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
