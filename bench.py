@@ -68,20 +68,26 @@ def args_parse():
 class Workload:
     """Symbol tables (host, SYMR) + side streams; samples generated on device."""
 
-    def __init__(self, a, group_index: int):
+    def __init__(self, a, shard: int = 0, world: int = 1):
+        """One communication group of world x a.ranks ranks; this process owns the
+        samples of ranks [shard * a.ranks, (shard + 1) * a.ranks).  Collectives,
+        GPU and OS streams cover the whole group (identical on every process)."""
         from tests.synth import c2_tables, side_streams
         self.a = a
         self.tables = c2_tables(a.seed, a.nsym)
-        rng = np.random.default_rng(a.seed * 1000 + group_index)
+        rng = np.random.default_rng(a.seed * 1000)
         self.period = 10_000  # ns between samples of a rank
         self.span = a.spr * self.period
         self.iterations = 100
         self.iter_ns = self.span // self.iterations
-        self.skews = rng.integers(-10_000_000, 10_000_001, size=a.ranks).astype(np.int64)
-        self.rank_base = group_index * a.ranks
-        self.slow = 4 if a.ranks > 4 else 0
-        self.side = side_streams(rng, a.ranks, self.iterations, self.iter_ns, self.span, self.slow,
-                                 self.skews, rank_base=self.rank_base)
+        self.group_size = world * a.ranks
+        self.skews_all = rng.integers(-10_000_000, 10_000_001, size=self.group_size).astype(np.int64)
+        self.rank_base = shard * a.ranks
+        self.skews = self.skews_all[self.rank_base:self.rank_base + a.ranks]
+        self.slow_global = 4 if self.group_size > 4 else 0
+        self.slow = self.slow_global - self.rank_base  # local index (may be out of range)
+        self.side = side_streams(rng, self.group_size, self.iterations, self.iter_ns, self.span,
+                                 self.slow_global, self.skews_all)
         w = np.arange(1, a.pool + 1, dtype=np.float64) ** -1.1
         self.zipf_cdf = np.cumsum(w / w.sum())
         self.zipf_cdf[-1] = 1.0
@@ -111,7 +117,7 @@ class Workload:
                                      C.c_int, C.c_double, C.c_uint32, C.c_int64, P, P, P, P, P, P]
         rc = lib.bench_gen_c2(a.seed + seed_off, ranks, spr, a.depth, a.pool, cdf.data_ptr(),
                               C.cast(starts, P), C.cast(sizes, P), C.cast(nsym, P), C.cast(hot, P),
-                              C.cast(softa, P), self.slow if self.slow < ranks else -1, 0.0174, 100,
+                              C.cast(softa, P), self.slow if 0 <= self.slow < ranks else -1, 0.0174, 100,
                               period or self.period, skew.data_ptr(), ts.data_ptr(), foff.data_ptr(), pc.data_ptr(),
                               bn.data_ptr(), P(torch.cuda.current_stream().cuda_stream))
         assert rc == 0, f"generator failed: {rc}"
@@ -135,12 +141,12 @@ class Workload:
         w.n_samples_ = ranks * spr
         w.n_frames_ = ranks * spr * a.depth
         if ranks == a.ranks:
-            apply_side(w, self.side, ranks)
+            apply_side(w, self.side, self.group_size)
         else:  # bounded sample: keep the side streams of the sampled ranks only
             from tests.synth import side_streams
             rng = np.random.default_rng(a.seed)
-            side = side_streams(rng, ranks, self.iterations, self.iter_ns, self.span, self.slow, self.skews,
-                                rank_base=self.rank_base)
+            side = side_streams(rng, ranks, self.iterations, self.iter_ns, self.span, self.slow_global,
+                                self.skews_all, rank_base=self.rank_base)
             apply_side(w, side, ranks)
         w.has_baseline = True
         w.baseline_delta = 0.005
@@ -326,8 +332,11 @@ def main():
     from paper_2603_29235_b200.abi import STG_MEM_DEVICE, STG_MEM_HOST
     if a.config == "c4":
         return bench_c4(a, torch, stg, rank, local, world, dist)
-    wl = Workload(a, rank)
+    wl = Workload(a, rank, world)
     ctx = stg.Context(local)
+    if world > 1:  # one communication group spanning the GPUs: libstg's own NCCL group
+        from paper_2603_29235_b200.dist import share_unique_id
+        ctx.dist_init(world, rank, share_unique_id(dist, stg.Context.dist_unique_id, device="cuda"))
     t0 = time.time()
     for _, _, _, symr in wl.tables:
         ctx.ingest(symr)
@@ -390,7 +399,9 @@ def main():
                        "ranks_per_gpu": a.ranks, "samples_per_rank": a.spr, "depth": a.depth,
                        "distinct_stacks": a.pool, "symbols_per_table": a.nsym,
                        "inputs": "resident in HBM, 84 GB/GPU > L2 (no flush needed)",
-                       "parallelism": f"rank-sharded groups x{world}"},
+                       "group_ranks": wl.group_size,
+                       "parallelism": f"one {wl.group_size}-rank group sharded by rank over {world} GPU(s), "
+                                      "NCCL exchange of straggler/reference fractions + waterline all-reduce"},
             "verdict": rep["verdict"], "flagged_ranks": rep["flagged_ranks"],
             "prefix_cache": {"hits": s["prefix_hits"], "misses": s["prefix_misses"]},
             "stage_ms": {"total_device": float(np.median(tot_ms)), "symbolize_aggregate": k_ms,
@@ -398,7 +409,25 @@ def main():
             "roofline": roof, "gpu_launches": int(np.median(launches)) * a.steps,
             "clocks": clk.summary()}
     # ---- end to end through the C-ABI with host buffers (H2D inside the timed region)
-    if not a.no_e2e:
+    e2e_ok = not a.no_e2e
+    if e2e_ok and world > 1:
+        try:
+            import psutil
+            need = world * (win.n_frames * 10 + win.n_samples * 16) * 1.25
+            if psutil.virtual_memory().available < need:
+                e2e_ok = False
+                line["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
+                               "reason": f"host RAM {psutil.virtual_memory().available / 1e9:.0f} GB < "
+                                         f"{need / 1e9:.0f} GB of pinned inputs for {world} processes"}
+        except ImportError:
+            pass
+        t = torch.tensor([1 if e2e_ok else 0], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)  # every process takes the same branch
+        if not t.item() and e2e_ok:
+            e2e_ok = False
+            line["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
+                           "reason": "another process lacks host RAM for pinned inputs"}
+    if e2e_ok:
         host = []
         for t in arrays:
             h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)

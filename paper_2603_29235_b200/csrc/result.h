@@ -1,6 +1,7 @@
 // result.h — host-side view of one window's result (GroupData + report).
 #pragma once
 
+#include <algorithm>
 #include <map>
 #include <optional>
 #include <string>
@@ -74,6 +75,17 @@ struct Result {
     bool waterline_done = false;
     std::string waterline_json;
     uint64_t wl_flags = 0, wl_F = 0;
+    // distributed waterline: global name space kept for lazy rendering
+    bool wl_dist = false;
+    uint64_t wl_NG = 0;
+    std::vector<uint64_t> g_lab_final;
+    std::vector<std::string> g_lab;
+    std::vector<uint32_t> wl_gkey;  // dense name -> global key
+    std::string gname(uint32_t g) const {
+        auto it = std::lower_bound(g_lab_final.begin(), g_lab_final.end(), uint64_t(g));
+        if (it != g_lab_final.end() && *it == g) return g_lab[size_t(it - g_lab_final.begin())];
+        return (*dict)[g - uint64_t(it - g_lab_final.begin())];
+    }
     stg_run_stats stats{};
 };
 

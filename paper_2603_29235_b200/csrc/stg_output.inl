@@ -306,9 +306,65 @@ std::string groupdata_json(Ctx& c) {
 }
 
 // compute_waterline / flag_ranks rendering from the device-resident result.
+static std::string waterline_json_dist(Ctx& c) {
+    Result& r = *c.result;
+    const uint64_t NG = r.wl_NG, nf = r.wl_flags;
+    std::vector<double> hm(NG), hs(NG);
+    std::vector<unsigned> hnp(NG);
+    d2h(c, hm.data(), "wlg_mean", NG);
+    d2h(c, hs.data(), "wlg_sd", NG);
+    d2h(c, hnp.data(), "wl_np", NG);
+    std::vector<uint32_t> fr(nf), ff(nf);
+    std::vector<double> ffr(nf), fth(nf);
+    d2h(c, fr.data(), "wl_or", nf);
+    d2h(c, ff.data(), "wl_of", nf);
+    d2h(c, ffr.data(), "wl_ofr", nf);
+    d2h(c, fth.data(), "wl_oth", nf);
+    std::vector<int32_t> rids(r.n_window_ranks);
+    d2h(c, rids.data(), "rids", r.n_window_ranks);
+    JsonW j;
+    j.raw("{\"functions\": [");
+    bool first = true;
+    for (uint64_t g = 0; g < NG; ++g) {
+        if (!hnp[g]) continue;
+        if (!first) j.raw(", ");
+        first = false;
+        j.raw("[");
+        j.str(r.gname(uint32_t(g)));
+        j.raw(", ");
+        j.num(hm[g]);
+        j.raw(", ");
+        j.num(hs[g]);
+        j.raw("]");
+    }
+    j.raw("], \"flags\": [");
+    std::vector<size_t> order(nf);
+    std::iota(order.begin(), order.end(), 0);
+    std::sort(order.begin(), order.end(), [&](size_t a, size_t b) {
+        return fr[a] != fr[b] ? fr[a] < fr[b] : ff[a] < ff[b];
+    });
+    for (size_t i = 0; i < nf; ++i) {
+        const size_t k = order[i];
+        if (i) j.raw(", ");
+        j.raw("[");
+        j.num(int64_t(rids[fr[k]]));
+        j.raw(", ");
+        j.str(r.gname(r.wl_gkey[ff[k]]));
+        j.raw(", ");
+        j.num(ffr[k]);
+        j.raw(", ");
+        j.num(fth[k]);
+        j.raw("]");
+    }
+    j.raw("]}");
+    r.waterline_json = j.s;
+    return j.s;
+}
+
 std::string waterline_json(Ctx& c) {
     Result& r = *c.result;
     if (!r.waterline_json.empty()) return r.waterline_json;
+    if (r.wl_dist) return waterline_json_dist(c);
     const uint64_t F = r.wl_F, nf = r.wl_flags;
     std::vector<double> hm(F), hs(F);
     std::vector<uint8_t> hp(F);

@@ -1169,11 +1169,16 @@ struct Runner {
     bool gn_ready = false;
     void global_names() {
         if (gn_ready) return;
-        uint64_t h = 1469598103934665603ull;
-        for (const auto& n : c.dict) {
-            for (unsigned char ch : n) h = (h ^ ch) * 1099511628211ull;
-            h = (h ^ 0xff) * 1099511628211ull;
+        if (c.dict_hash_version != c.dict_version) {  // once per dictionary
+            uint64_t hv = 1469598103934665603ull;
+            for (const auto& n : c.dict) {
+                for (unsigned char ch : n) hv = (hv ^ ch) * 1099511628211ull;
+                hv = (hv ^ 0xff) * 1099511628211ull;
+            }
+            c.dict_hash = hv;
+            c.dict_hash_version = c.dict_version;
         }
+        const uint64_t h = c.dict_hash;
         unsigned long long* dh = dev<unsigned long long>("dx_h", 2);
         unsigned long long hh[2] = {h, h};
         STG_CUDA(cudaMemcpyAsync(dh, hh, 16, cudaMemcpyHostToDevice, st));
@@ -1469,16 +1474,21 @@ struct Runner {
             // CPU layer (cpu_diff diagnosis.cpp:177-208)
             int is = cpu_index(strag), iq = cpu_index(ref);
             if (dist()) {
+                mark("d:enter");
                 global_names();
+                mark("d:names");
                 cpu_owners();
+                mark("d:owners");
                 const int os_ = cpu_owner[size_t(strag)], oq = cpu_owner[size_t(ref)];
                 if (os_ >= 0 && oq >= 0) {
                     std::map<uint32_t, uint32_t> dense_of;
                     std::vector<std::pair<uint32_t, double>> fs_, fr_;
                     if (c.wrank == os_) fs_ = rank_fracs_global(strag, &dense_of);
                     if (c.wrank == oq) fr_ = rank_fracs_global(ref, nullptr);
+                    mark("d:fracs");
                     fs_ = bcast_fracs(std::move(fs_), os_);
                     fr_ = bcast_fracs(std::move(fr_), oq);
+                    mark("d:bcast");
                     struct Cand { std::string fn; double fs, fr, d; uint32_t key; };
                     std::vector<Cand> cands;
                     size_t j = 0;
@@ -1501,6 +1511,7 @@ struct Runner {
                             path = hottest(lo[0], lo[1], dense_of.at(cands.front().key), false);
                         }
                         rep.top_path = bcast_path(std::move(path), os_);
+                        mark("d:path");
                     }
                 } else {
                     rep.notes.push_back("cpu profiles missing; cpu layer skipped");
@@ -1680,58 +1691,18 @@ struct Runner {
         if (F && nr)
             LAUNCH(k_flag_g, grid_for(F * nr), kThreads, F, rows, int(nr), d_incl, d_totals, cfg.k, d_gk, mean, sd, o_r,
                    o_f, o_fr, o_th, n_out, cap);
-        const uint64_t nf = std::min<uint64_t>(get1(n_out), cap);
-        // render now: the global name space lives only for this run
-        std::vector<double> hm(NG), hs(NG);
-        std::vector<unsigned> hnp(NG);
-        down(hm.data(), mean, NG);
-        down(hs.data(), sd, NG);
-        down(hnp.data(), np, NG);
-        std::vector<uint32_t> fr(nf), ff(nf);
-        std::vector<double> ffr(nf), fth(nf);
-        down(fr.data(), o_r, nf);
-        down(ff.data(), o_f, nf);
-        down(ffr.data(), o_fr, nf);
-        down(fth.data(), o_th, nf);
-        JsonW j;
-        j.raw("{\"functions\": [");
-        bool first = true;
-        for (uint64_t g = 0; g < NG; ++g) {
-            if (!hnp[g]) continue;
-            if (!first) j.raw(", ");
-            first = false;
-            j.raw("[");
-            j.str(gname(uint32_t(g)));
-            j.raw(", ");
-            j.num(hm[g]);
-            j.raw(", ");
-            j.num(hs[g]);
-            j.raw("]");
-        }
-        j.raw("], \"flags\": [");
-        std::vector<size_t> order(nf);
-        std::iota(order.begin(), order.end(), 0);
-        std::sort(order.begin(), order.end(), [&](size_t a, size_t b) {
-            return fr[a] != fr[b] ? fr[a] < fr[b] : ff[a] < ff[b];
-        });
-        for (size_t i = 0; i < nf; ++i) {
-            const size_t k = order[i];
-            if (i) j.raw(", ");
-            j.raw("[");
-            j.num(int64_t(w.rank_ids[fr[k]]));
-            j.raw(", ");
-            j.str(gname(gk[ff[k]]));
-            j.raw(", ");
-            j.num(ffr[k]);
-            j.raw(", ");
-            j.num(fth[k]);
-            j.raw("]");
-        }
-        j.raw("]}");
-        res.waterline_json = j.s;
+        res.wl_flags = std::min<uint64_t>(get1(n_out), cap);
+        res.wl_F = F;
+        res.wl_dist = true;
+        res.wl_NG = NG;
+        res.g_lab_final = gn.lab_final;
+        res.g_lab = gn.lab;
+        res.wl_gkey = gk;
+        res.waterline_json.clear();  // rendered on request
     }
 
     void waterline() {
+        res.wl_dist = false;
         if (dist()) return waterline_dist();
         res.waterline_done = true;
         std::string out;

@@ -1420,6 +1420,11 @@ __global__ void k_wl_pass2(uint64_t F, const uint32_t* rows, int R, const unsign
 __global__ void k_wl_final(uint64_t NG, const double* s1, const unsigned* np, const double* s2, double rt,
                            double* mean, double* sd) {
     for (uint64_t g = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; g < NG; g += uint64_t(gridDim.x) * blockDim.x) {
+        if (!np[g]) {  // name absent everywhere: no waterline entry
+            mean[g] = 0.0;
+            sd[g] = 0.0;
+            continue;
+        }
         const double mu = __ddiv_rn(s1[g], rt);
         double v = s2[g];
         for (double k = np[g]; k < rt; k += 1.0) v = __dadd_rn(v, __dmul_rn(mu, mu));
