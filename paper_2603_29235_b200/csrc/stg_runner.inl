@@ -1179,6 +1179,7 @@ struct Runner {
             c.dict_hash_version = c.dict_version;
         }
         const uint64_t h = c.dict_hash;
+        if (c.dict_agreed_version != c.dict_version) {
         unsigned long long* dh = dev<unsigned long long>("dx_h", 2);
         unsigned long long hh[2] = {h, h};
         STG_CUDA(cudaMemcpyAsync(dh, hh, 16, cudaMemcpyHostToDevice, st));
@@ -1186,24 +1187,38 @@ struct Runner {
         nccl(ncclAllReduce(dh + 1, dh + 1, 1, ncclUint64, ncclMax, comm(), st));
         down(hh, dh, 2);
         if (hh[0] != hh[1]) fail(STG_EINVAL, "distributed contexts hold different symbol tables");
+        c.dict_agreed_version = c.dict_version;
+        }
+        mark("g:agree");
+        // each label travels with its dictionary position (known from
+        // merge_labels: final = pos + index among labels), so the merge needs
+        // no search in the dictionary
         std::vector<uint8_t> mine;
         put<uint32_t>(mine, uint32_t(res.unk_labels.size()));
-        for (const auto& l : res.unk_labels) put_str(mine, l);
-        std::vector<std::string> all;
-        for (const auto& b : allgather_bytes(mine)) {
+        for (size_t k = 0; k < res.unk_labels.size(); ++k) {
+            put<uint32_t>(mine, uint32_t(res.unk_final[k] - k));
+            put_str(mine, res.unk_labels[k]);
+        }
+        std::vector<std::pair<std::string, uint32_t>> all;
+        auto gathered = allgather_bytes(mine);
+        mark("g:allgather");
+        for (const auto& b : gathered) {
             const uint8_t* p = b.data();
             uint32_t n = b.empty() ? 0 : get<uint32_t>(p);
-            for (uint32_t i = 0; i < n; ++i) all.push_back(get_str(p));
+            for (uint32_t i = 0; i < n; ++i) {
+                uint32_t pos = get<uint32_t>(p);
+                all.emplace_back(get_str(p), pos);
+            }
         }
         std::sort(all.begin(), all.end());
-        all.erase(std::unique(all.begin(), all.end()), all.end());
+        all.erase(std::unique(all.begin(), all.end(),
+                              [](const auto& a, const auto& b) { return a.first == b.first; }),
+                  all.end());
         uint64_t ne_before = 0;
-        for (const auto& lab : all) {
-            uint64_t pos = uint64_t(std::lower_bound(c.dict.begin(), c.dict.end(), lab) - c.dict.begin());
-            if (pos < c.dict.size() && c.dict[pos] == lab) continue;  // local labels never equal names (merge_labels)
+        for (const auto& [lab, pos] : all) {
             gn.lab.push_back(lab);
-            gn.lab_final.push_back(pos + ne_before);
-            gn.pos.push_back(uint32_t(pos));
+            gn.lab_final.push_back(uint64_t(pos) + ne_before);
+            gn.pos.push_back(pos);
             ++ne_before;
         }
         for (size_t k = 0; k < res.unk_labels.size(); ++k) {
@@ -1212,6 +1227,7 @@ struct Runner {
             gn.loc_global.push_back(uint32_t(gn.lab_final[gi]));
         }
         gn_ready = true;
+        mark("g:merge");
     }
     uint32_t to_global(uint32_t f) const {
         auto it = std::lower_bound(gn.loc_final.begin(), gn.loc_final.end(), uint64_t(f));
@@ -1237,7 +1253,7 @@ struct Runner {
     }
     // this context's exact fractions of CPU rank `rank` as (global key, value),
     // plus the dense index of each key for local follow-ups
-    std::vector<std::pair<uint32_t, double>> rank_fracs_global(int rank, std::map<uint32_t, uint32_t>* dense_of) {
+    std::vector<std::pair<uint32_t, double>> rank_fracs_global(int rank, std::vector<uint32_t>* dense_of) {
         int i = cpu_index(rank);
         uint64_t lo[2];
         down(lo, d_line_off + i, 2);
@@ -1247,7 +1263,7 @@ struct Runner {
         for (const auto& [f, v] : fr) {
             uint32_t g = to_global(h_dense_final[f]);
             out.emplace_back(g, v);
-            if (dense_of) (*dense_of)[g] = f;
+            if (dense_of) dense_of->push_back(f);  // parallel to out (keys ascending)
         }
         return out;
     }
@@ -1481,13 +1497,40 @@ struct Runner {
                 mark("d:owners");
                 const int os_ = cpu_owner[size_t(strag)], oq = cpu_owner[size_t(ref)];
                 if (os_ >= 0 && oq >= 0) {
-                    std::map<uint32_t, uint32_t> dense_of;
+                    std::vector<uint32_t> dense_of;
                     std::vector<std::pair<uint32_t, double>> fs_, fr_;
                     if (c.wrank == os_) fs_ = rank_fracs_global(strag, &dense_of);
                     if (c.wrank == oq) fr_ = rank_fracs_global(ref, nullptr);
                     mark("d:fracs");
-                    fs_ = bcast_fracs(std::move(fs_), os_);
-                    fr_ = bcast_fracs(std::move(fr_), oq);
+                    {  // one all-gather carries both lists from their owners
+                        std::vector<uint8_t> mine;
+                        auto pack = [&](const std::vector<std::pair<uint32_t, double>>& v) {
+                            put<uint64_t>(mine, v.size());
+                            for (const auto& [k, x] : v) {
+                                put<uint32_t>(mine, k);
+                                put<double>(mine, x);
+                            }
+                        };
+                        pack(fs_);
+                        pack(fr_);
+                        auto all = allgather_bytes(mine);
+                        auto unpack = [&](const std::vector<uint8_t>& b, int which) {
+                            const uint8_t* p = b.data();
+                            std::vector<std::pair<uint32_t, double>> v;
+                            for (int w = 0; w <= which; ++w) {
+                                uint64_t n = get<uint64_t>(p);
+                                v.clear();
+                                for (uint64_t i = 0; i < n; ++i) {
+                                    uint32_t k = get<uint32_t>(p);
+                                    double x = get<double>(p);
+                                    v.emplace_back(k, x);
+                                }
+                            }
+                            return v;
+                        };
+                        fs_ = unpack(all[size_t(os_)], 0);
+                        fr_ = unpack(all[size_t(oq)], 1);
+                    }
                     mark("d:bcast");
                     struct Cand { std::string fn; double fs, fr, d; uint32_t key; };
                     std::vector<Cand> cands;
@@ -1508,7 +1551,8 @@ struct Runner {
                         if (c.wrank == os_) {
                             uint64_t lo[2];
                             down(lo, d_line_off + is, 2);
-                            path = hottest(lo[0], lo[1], dense_of.at(cands.front().key), false);
+                            auto it = std::lower_bound(fs_.begin(), fs_.end(), std::make_pair(cands.front().key, -1e300));
+                            path = hottest(lo[0], lo[1], dense_of[size_t(it - fs_.begin())], false);
                         }
                         rep.top_path = bcast_path(std::move(path), os_);
                         mark("d:path");
@@ -1736,8 +1780,9 @@ struct Runner {
     void mark(const char* what) {
         if (!trace) return;
         auto now = std::chrono::steady_clock::now();
-        std::fprintf(stderr, "[stg] %-12s %8.3f ms\n", what,
-                     std::chrono::duration<double, std::milli>(now - t_last).count());
+        std::fprintf(stderr, "[stg] r%d %-12s %8.3f ms  @%.3f\n", c.wrank, what,
+                     std::chrono::duration<double, std::milli>(now - t_last).count(),
+                     std::fmod(std::chrono::duration<double, std::milli>(now.time_since_epoch()).count(), 1e5));
         t_last = now;
     }
 
