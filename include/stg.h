@@ -17,7 +17,7 @@
  *  - Plain pointers and sizes only; no torch or C++ types.  Bulk sample arrays may
  *    live in host memory (copied in by the call) or already in device memory
  *    (stg_window.memory = STG_MEM_DEVICE, pointers valid on the context's GPU;
- *    frame_pc and frame_bin 16-byte aligned, as cudaMalloc returns them).
+ *    frame_pc 32-byte and frame_bin 16-byte aligned, as cudaMalloc returns them).
  *  - A context owns device memory, streams and the loaded symbol tables; calls on
  *    one context are serialised by an internal mutex.
  */

@@ -550,8 +550,8 @@ struct Runner {
         const uint64_t *foff, *pc;
         const uint16_t* bin;
         if (w.memory == STG_MEM_DEVICE) {
-            if ((reinterpret_cast<uintptr_t>(w.frame_pc) | reinterpret_cast<uintptr_t>(w.frame_bin)) & 15)
-                fail(STG_EINVAL, "device frame_pc / frame_bin must be 16-byte aligned");
+            if ((reinterpret_cast<uintptr_t>(w.frame_pc) & 31) || (reinterpret_cast<uintptr_t>(w.frame_bin) & 15))
+                fail(STG_EINVAL, "device frame_pc must be 32-byte and frame_bin 16-byte aligned");
             ts = w.sample_ts;
             foff = w.sample_frame_off;
             pc = w.frame_pc;
@@ -673,7 +673,7 @@ struct Runner {
             cudaEventRecord(ev[2], st);
             const bool smem_tabs = w.n_bins <= kMaxSmemBins;
             // STG_SYM_MINB (experiments): resident CTAs per SM the register budget targets
-            static const int minb = std::getenv("STG_SYM_MINB") ? std::atoi(std::getenv("STG_SYM_MINB")) : 4;
+            static const int minb = std::getenv("STG_SYM_MINB") ? std::atoi(std::getenv("STG_SYM_MINB")) : 5;
             grid = unsigned(dev_sms) * unsigned(minb) * 4;
             if (need < grid) grid = unsigned(std::max<uint64_t>(need, 1));
 #define STG_SYM(MB) \

@@ -658,6 +658,13 @@ __device__ __forceinline__ void raw_add(uint64_t& ha, uint64_t& hb, uint64_t t) 
     hb += (t >> 29) | (t << 35);
 }
 
+// 256-bit read-only global load (sm_100: LDG.E.ENL2.256), 32-byte aligned.
+__device__ __forceinline__ void ld256(const uint64_t* p, uint64_t& a, uint64_t& b, uint64_t& c, uint64_t& d) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0, %1, %2, %3}, [%4];"
+                 : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
+                 : "l"(p));
+}
+
 // Prefix cache.  Entries are immutable once published: writer claims hi by CAS,
 // stores (ta, tb), fences, then stores lo.  A reader takes (hi, lo) and (ta, tb)
 // with two 16-byte L2 reads issued together; an entry seen with lo published but
@@ -752,11 +759,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
                         // other half of the same 32 B sector
                         const uint64_t bb = blk + 8 * u;
                         if (u == 0 || bb < f1) {
-                            const ulonglong2* pv = reinterpret_cast<const ulonglong2*>(p.pc + bb);
-                            const ulonglong2 q0 = __ldg(pv), q1 = __ldg(pv + 1), q2 = __ldg(pv + 2), q3 = __ldg(pv + 3);
+                            // two 256-bit loads: each lane takes a whole 32 B sector per
+                            // instruction (half the L1 wavefronts of 16 B loads)
+                            ld256(p.pc + bb, pcs[u][0], pcs[u][1], pcs[u][2], pcs[u][3]);
+                            ld256(p.pc + bb + 4, pcs[u][4], pcs[u][5], pcs[u][6], pcs[u][7]);
                             const uint4 bq = __ldg(reinterpret_cast<const uint4*>(p.bin + bb));
-                            pcs[u][0] = q0.x; pcs[u][1] = q0.y; pcs[u][2] = q1.x; pcs[u][3] = q1.y;
-                            pcs[u][4] = q2.x; pcs[u][5] = q2.y; pcs[u][6] = q3.x; pcs[u][7] = q3.y;
                             bns[u][0] = bq.x & 0xffffu; bns[u][1] = bq.x >> 16; bns[u][2] = bq.y & 0xffffu;
                             bns[u][3] = bq.y >> 16; bns[u][4] = bq.z & 0xffffu; bns[u][5] = bq.z >> 16;
                             bns[u][6] = bq.w & 0xffffu; bns[u][7] = bq.w >> 16;
