@@ -265,6 +265,21 @@ int stg_result_rank_info(stg_ctx* ctx, uint32_t i, int32_t* rank, uint64_t* n_li
 int stg_result_rank_lines(stg_ctx* ctx, uint32_t i, uint64_t* line_key_off /* n_lines+1 */,
                           uint32_t* keys, uint64_t* counts);
 
+/* Folded-text artifacts of the last window, rendered on the device (two-call
+ * size query like the JSON getters; *needed counts the trailing NUL).
+ *   stg_result_folded_text  FoldedProfile::to_string (folded.cpp:33-43) of the
+ *                           rank's CPU profile — what `strata flamegraph` writes
+ *                           to <out>.folded (tools/strata.cpp:119-131).
+ *   stg_result_diff_folded  diff_folded(profile(a), profile(b)) (folded.cpp:83-96)
+ *                           — what `strata diagnose` writes per flagged rank
+ *                           against the reference rank (tools/strata.cpp:97-109).
+ * A rank without a CPU profile fails with "unknown rank id: <rank>" (rank_profile,
+ * tools/strata.cpp:111-116).  In a distributed group both ranks must be held by
+ * this context. */
+int stg_result_folded_text(stg_ctx* ctx, int32_t rank, char* buf, uint64_t cap, uint64_t* needed);
+int stg_result_diff_folded(stg_ctx* ctx, int32_t rank_a, int32_t rank_b, char* buf, uint64_t cap,
+                           uint64_t* needed);
+
 #ifdef __cplusplus
 }
 #endif

@@ -103,8 +103,11 @@ def simulate(scenario: str, seed: int, ranks: int = 0, iterations: int = 0,
 
 
 def window_run(win: Window, threads: int = 1, want_json: bool = True,
-               tmpdir: Optional[str] = None):
-    """Reference build_group_data + diagnose.  Returns (result_json, t_build_s, t_diag_s)."""
+               tmpdir: Optional[str] = None, artifacts: bool = False):
+    """Reference build_group_data + diagnose.  Returns (result_json, t_build_s, t_diag_s).
+
+    artifacts=True adds result_json["artifacts"]: FoldedProfile::to_string of every
+    rank and diff_folded texts (see ref_harness.cpp)."""
     cw, keep = win.to_c()
     n = len(win.symr)
     bufs = [C.create_string_buffer(s, len(s)) for s in win.symr]
@@ -115,7 +118,7 @@ def window_run(win: Window, threads: int = 1, want_json: bool = True,
     err = C.create_string_buffer(1024)
     tmp = tmpdir or tempfile.gettempdir()
     rc = lib().ref_window_run(C.byref(cw), n, ptrs, lens, tmp.encode(), threads,
-                              int(want_json), C.byref(out), C.byref(tb), C.byref(td), err, 1024)
+                              2 if artifacts else int(want_json), C.byref(out), C.byref(tb), C.byref(td), err, 1024)
     if rc != 0:
         raise RefError(err.value.decode())
     return _take_json(out), tb.value, td.value

@@ -482,6 +482,31 @@ int ref_window_run(const stg_window* w, int n_symr, const uint8_t* const* symr,
             json j;
             if (want_json) j["groupdata"] = groupdata_json(data);
             j["report"] = json::parse(rep.to_json());
+            if (want_json == 2) {
+                // the text artifacts of `strata diagnose` / `strata flamegraph`
+                // (tools/strata.cpp:97-131): every rank's folded text, each
+                // flagged rank's diff against the reference rank, and the diff
+                // of the first two profiled ranks both ways
+                json folded = json::array(), diffs = json::array();
+                std::vector<int> ranks;
+                for (const auto& [rank, prof] : data.cpu_profiles) {
+                    folded.push_back(json::array({rank, prof.to_string()}));
+                    ranks.push_back(rank);
+                }
+                auto add_diff = [&](int a, int b) {
+                    diffs.push_back(json::array(
+                        {a, b, diff_folded(data.cpu_profiles.at(a), data.cpu_profiles.at(b))}));
+                };
+                if (rep.reference_rank && data.cpu_profiles.count(*rep.reference_rank))
+                    for (int r : rep.flagged_ranks)
+                        if (data.cpu_profiles.count(r)) add_diff(r, *rep.reference_rank);
+                if (ranks.size() >= 2) {
+                    add_diff(ranks[0], ranks[1]);
+                    add_diff(ranks[1], ranks[0]);
+                }
+                if (!ranks.empty()) add_diff(ranks[0], ranks[0]);
+                j["artifacts"] = {{"folded", folded}, {"diffs", diffs}};
+            }
             *out_json = dup_string(j.dump());
         }
         fs::remove_all(dir);

@@ -60,6 +60,9 @@ def load_library():
         getattr(l, fn).argtypes = [P, C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64)]
     l.stg_dist_unique_id.argtypes = [C.c_char_p]
     l.stg_dist_init.argtypes = [P, C.c_int, C.c_int, C.c_char_p]
+    l.stg_result_folded_text.argtypes = [P, C.c_int32, C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64)]
+    l.stg_result_diff_folded.argtypes = [P, C.c_int32, C.c_int32, C.c_char_p, C.c_uint64,
+                                         C.POINTER(C.c_uint64)]
     l.stg_result_rank_count.argtypes = [P, C.POINTER(C.c_uint32)]
     l.stg_result_rank_info.argtypes = [P, C.c_uint32, C.POINTER(C.c_int32), C.POINTER(C.c_uint64),
                                        C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
@@ -161,6 +164,21 @@ class Context:
 
     def waterline(self) -> dict:
         return self._json(self._l.stg_result_waterline_json)
+
+    def _text(self, fn, *args) -> str:
+        need = C.c_uint64()
+        _check(fn(self._h, *args, None, 0, C.byref(need)))
+        buf = C.create_string_buffer(need.value)
+        _check(fn(self._h, *args, buf, need.value, C.byref(need)))
+        return buf.raw[:need.value - 1].decode("utf-8", "surrogateescape")
+
+    def folded_text(self, rank: int) -> str:
+        """FoldedProfile::to_string of `rank`'s CPU profile (folded.cpp:33-43), rendered on the GPU."""
+        return self._text(self._l.stg_result_folded_text, rank)
+
+    def diff_folded(self, rank_a: int, rank_b: int) -> str:
+        """diff_folded(profile(a), profile(b)) (folded.cpp:83-96), rendered on the GPU."""
+        return self._text(self._l.stg_result_diff_folded, rank_a, rank_b)
 
     def folded(self):
         """{rank: (total, [(names root-first, count), ...])} via the structured getters."""

@@ -26,7 +26,27 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUDA_INC = "/usr/local/cuda/include"
 
-CU_SOURCES = ["stg_window.cu"]
+
+
+def _nccl_dir():
+    """The NCCL torch ships with (nvidia/nccl wheel), so libstg and torch.distributed
+    share one libnccl.so.2 in a process whichever is loaded first; the system
+    NCCL only when the wheel is absent."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    if spec and spec.submodule_search_locations:
+        d = Path(list(spec.submodule_search_locations)[0])
+        if (d / "lib" / "libnccl.so.2").exists() and (d / "include" / "nccl.h").exists():
+            return d
+    return None
+
+
+NCCL_DIR = _nccl_dir()
+NCCL_INC = [f"-I{NCCL_DIR / 'include'}"] if NCCL_DIR else []
+NCCL_LINK = ([f"-L{NCCL_DIR / 'lib'}", "-l:libnccl.so.2", "-Xlinker", f"-rpath={NCCL_DIR / 'lib'}"]
+             if NCCL_DIR else ["-lnccl"])
+
+CU_SOURCES = ["stg_window.cu", "stg_render.cu"]
 CPP_SOURCES = ["symtab.cpp", "stg_api.cpp"]
 HEADERS = ["stg_internal.h", "kernels.cuh", "result.h", "stg_runner.inl", "stg_output.inl"]
 
@@ -55,16 +75,16 @@ def build(verbose: bool = False) -> Path:
         if _stale(obj, [CSRC / src] + hdrs):
             _run([NVCC, "-std=c++17", "-O3", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC",
                   "-Xptxas", "-v" if verbose else "-O3", "-diag-suppress", "177",
-                  f"-I{ROOT / 'include'}", "-c", str(CSRC / src), "-o", str(obj)])
+                  *NCCL_INC, f"-I{ROOT / 'include'}", "-c", str(CSRC / src), "-o", str(obj)])
         objs.append(obj)
     for src in CPP_SOURCES:
         obj = OUT / (Path(src).stem + ".o")
         if _stale(obj, [CSRC / src] + hdrs):
-            _run(["g++", "-std=c++17", "-O2", "-fPIC", f"-I{ROOT / 'include'}", f"-I{CUDA_INC}",
+            _run(["g++", "-std=c++17", "-O2", "-fPIC", *NCCL_INC, f"-I{ROOT / 'include'}", f"-I{CUDA_INC}",
                   "-c", str(CSRC / src), "-o", str(obj)])
         objs.append(obj)
     if _stale(LIB, objs):
-        _run([NVCC, "-shared", *ARCH, "-o", str(LIB), *map(str, objs), "-lcudart", "-lnccl"])
+        _run([NVCC, "-shared", *ARCH, "-o", str(LIB), *map(str, objs), "-lcudart", *NCCL_LINK])
     # bench-side generator (not part of the product library)
     if _stale(BENCH_LIB, [CSRC / "bench_gen.cu"]):
         _run([NVCC, "-std=c++17", "-O3", *ARCH, "-Xcompiler", "-fPIC", "-shared",

@@ -87,6 +87,11 @@ struct Result {
         return (*dict)[g - uint64_t(it - g_lab_final.begin())];
     }
     stg_run_stats stats{};
+    // folded-text artifacts (stg_render.cu): last rendering kept on the device
+    bool render_valid = false, render_unk_ready = false;
+    int render_kind = -1;
+    int32_t render_a = 0, render_b = 0;
+    uint64_t render_len = 0;
 };
 
 }  // namespace stg

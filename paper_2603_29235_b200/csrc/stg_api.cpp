@@ -18,6 +18,8 @@ void run_resolve(Ctx& c, Result& res, uint64_t n, const uint64_t* pc, const uint
                  const uint8_t* ids, int mode, uint32_t* out);
 void rank_lines(Ctx& c, uint32_t i, std::vector<uint64_t>& key_off, std::vector<uint32_t>& keys,
                 std::vector<uint64_t>& counts);
+uint64_t render_folded(Ctx& c, int kind, int32_t rank_a, int32_t rank_b);
+void render_copy(Ctx& c, char* buf, uint64_t len);
 }  // namespace stg
 
 struct stg_ctx {
@@ -262,6 +264,28 @@ int stg_result_rank_lines(stg_ctx* ctx, uint32_t i, uint64_t* line_key_off, uint
         std::memcpy(keys_out, keys.data(), keys.size() * sizeof(uint32_t));
         std::memcpy(counts, cnt.data(), cnt.size() * sizeof(uint64_t));
     });
+}
+
+static int folded_text(stg_ctx* ctx, int kind, int32_t a, int32_t b, char* buf, uint64_t cap, uint64_t* needed) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(ctx->impl.mu);
+        need_result(ctx);
+        STG_CUDA(cudaSetDevice(ctx->impl.device));
+        const uint64_t len = stg::render_folded(ctx->impl, kind, a, b);
+        if (needed) *needed = len + 1;
+        if (!buf) return;
+        if (cap < len + 1) stg::fail(STG_EINVAL, "buffer too small");
+        stg::render_copy(ctx->impl, buf, len);
+    });
+}
+
+int stg_result_folded_text(stg_ctx* ctx, int32_t rank, char* buf, uint64_t cap, uint64_t* needed) {
+    return folded_text(ctx, 0, rank, 0, buf, cap, needed);
+}
+
+int stg_result_diff_folded(stg_ctx* ctx, int32_t rank_a, int32_t rank_b, char* buf, uint64_t cap,
+                           uint64_t* needed) {
+    return folded_text(ctx, 1, rank_a, rank_b, buf, cap, needed);
 }
 
 }  // extern "C"

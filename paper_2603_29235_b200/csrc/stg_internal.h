@@ -131,6 +131,7 @@ struct Ctx {
     uint64_t dict_version = 0;
     bool dict_dirty = true;
     uint64_t dict_hash = 0, dict_hash_version = ~0ull, dict_agreed_version = ~0ull;
+    uint64_t dict_blob_version = ~0ull;  // dictionary staged for text rendering
     std::map<std::string, DBuf> bufs;
     DBuf& buf(const std::string& k) { return bufs[k]; }
     std::unique_ptr<Result> result;

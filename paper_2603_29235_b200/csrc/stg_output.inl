@@ -423,6 +423,7 @@ std::string waterline_json(Ctx& c) {
 void window_run(Ctx& c, const stg_window& w, const stg_config& cfg) {
     if (!c.result) c.result = std::make_unique<Result>();
     Result& r = *c.result;
+    r.render_valid = r.render_unk_ready = false;
     Runner rn(c, w, cfg, r);
     rn.run();
 }

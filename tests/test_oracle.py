@@ -406,6 +406,25 @@ def test_oracle_equals_reference_on_synthetic():
         assert gd == r["groupdata"] and rep == r["report"]
 
 
+@pytest.mark.parametrize("scenario", ["softirq", "dentry-lock"])
+def test_oracle_text_artifacts_equal_reference(scenario):
+    """FoldedProfile::to_string and diff_folded texts (folded.cpp:33-43, 83-96)."""
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    w = ref.simulate(scenario, 3)
+    r, _, _ = ref.window_run(w, artifacts=True)
+    gd = so.build_group_data(w)
+    prof = gd["cpu_profiles"]
+    art = r["artifacts"]
+    assert [x[0] for x in art["folded"]] == sorted(prof)
+    for rank, text in art["folded"]:
+        assert prof[rank].to_string() == text
+    assert art["diffs"]
+    for a, b, text in art["diffs"]:
+        assert so.diff_folded(prof[a], prof[b]) == text
+
+
 def test_lookup_matches_reference_probes():
     from oracle import ref
     if not ref.available():
