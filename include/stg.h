@@ -265,6 +265,37 @@ int stg_result_rank_info(stg_ctx* ctx, uint32_t i, int32_t* rank, uint64_t* n_li
 int stg_result_rank_lines(stg_ctx* ctx, uint32_t i, uint64_t* line_key_off /* n_lines+1 */,
                           uint32_t* keys, uint64_t* counts);
 
+/* ---- raw-address ProfileWindow API (aggregate_samples, samples.hpp:38-44) ----
+ * One rank's time-ordered sample stream, structure of arrays.  Frames are raw
+ * (bin, offset) pairs, leaf first; a bin stands for one build id (callers intern
+ * build ids to bins, so equal FrameRefs (vprocess.hpp:48-53) have equal pairs).
+ * rank may be NULL (then the mixed-rank check is skipped). */
+typedef struct stg_stream {
+    int32_t memory;            /* STG_MEM_HOST or STG_MEM_DEVICE */
+    uint64_t n_samples;
+    const int64_t* ts;         /* [n_samples] StackSample.timestamp_ns */
+    const int32_t* rank;       /* [n_samples] StackSample.rank, or NULL */
+    const uint64_t* frame_off; /* [n_samples + 1] CSR into the frame arrays */
+    const uint64_t* frame_pc;  /* FrameRef.offset */
+    const uint16_t* frame_bin; /* FrameRef.build_id as a bin index */
+} stg_stream;
+
+enum stg_agg_flags { STG_AGG_FORCE_EXACT = 1 /* tests: skip the fingerprint table */ };
+
+/* aggregate_samples (samples.cpp:31-85) on the GPU: windows on the drain grid,
+ * per window the distinct stacks in first-seen order with their counts (counts
+ * sum to n_samples).  A record is reported as the index of its first sample (its
+ * frames are that sample's frames) and its count.  Errors carry the reference's
+ * messages: "drain interval must be positive", "empty sample stack",
+ * "aggregate_samples: mixed ranks", "aggregate_samples: timestamps regressed"
+ * (first offending sample in stream order). */
+int stg_aggregate_samples(stg_ctx* ctx, const stg_stream* stream, int64_t drain_interval_ns, int flags,
+                          uint64_t* n_windows, uint64_t* n_records);
+/* Window bounds [start, end) and record offsets (n_windows + 1) of the last call. */
+int stg_aggregate_windows(stg_ctx* ctx, int64_t* start_ns, int64_t* end_ns, uint64_t* record_off);
+/* Records of the last call: first sample index and count (n_records each). */
+int stg_aggregate_records(stg_ctx* ctx, uint64_t* first_sample, uint64_t* count);
+
 /* Folded-text artifacts of the last window, rendered on the device (two-call
  * size query like the JSON getters; *needed counts the trailing NUL).
  *   stg_result_folded_text  FoldedProfile::to_string (folded.cpp:33-43) of the

@@ -212,3 +212,28 @@ def detect_straggler(lat: np.ndarray, ranks, k: float = 2.0):
     if rc != 0:
         raise RefError(err.value.decode())
     return _take_json(out)
+
+
+def aggregate_samples(ts, frame_off, frame_pc, frame_bin, bin_ids: bytes, rank=None,
+                      drain: int = 5_000_000_000):
+    """Reference aggregate_samples (samples.cpp:31-85) on a raw SoA stream.
+    Returns [(rank, start, end, [(first_sample, count), ...])]."""
+    ts = np.ascontiguousarray(ts, np.int64)
+    foff = np.ascontiguousarray(frame_off, np.uint64)
+    pc = np.ascontiguousarray(frame_pc, np.uint64)
+    bn = np.ascontiguousarray(frame_bin, np.uint16)
+    rk = None if rank is None else np.ascontiguousarray(rank, np.int32)
+    ids = np.frombuffer(bin_ids, np.uint8).copy()
+    out = C.c_void_p()
+    err = C.create_string_buffer(1024)
+    L = lib()
+    L.ref_aggregate_samples.argtypes = [C.c_uint64] + [C.c_void_p] * 5 + [C.c_int, C.c_void_p, C.c_int64,
+                                                                         C.POINTER(C.c_void_p), C.c_char_p,
+                                                                         C.c_int]
+    rc = L.ref_aggregate_samples(len(ts), ts.ctypes.data, None if rk is None else rk.ctypes.data,
+                                 foff.ctypes.data, pc.ctypes.data, bn.ctypes.data, len(ids) // 20,
+                                 ids.ctypes.data, int(drain), C.byref(out), err, 1024)
+    if rc != 0:
+        raise RefError(err.value.decode())
+    j = _take_json(out)
+    return [(w[0], w[1], w[2], [tuple(r) for r in w[3]]) for w in j["windows"]]

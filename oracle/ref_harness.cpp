@@ -581,6 +581,48 @@ int ref_pack_symbols(const uint8_t* build_id, uint64_t n, const uint64_t* starts
     }
 }
 
+// aggregate_samples (samples.cpp:31-85) on a raw SoA stream.  Output JSON:
+// {"windows": [[rank, start, end, [[first_sample, count], ...]], ...]} where
+// first_sample is the stream index of the first sample whose frames equal the
+// record's (found by scanning the window's samples in order).
+int ref_aggregate_samples(uint64_t n, const int64_t* ts, const int32_t* rank, const uint64_t* foff,
+                          const uint64_t* pc, const uint16_t* bin, int n_bins, const uint8_t* bin_ids,
+                          int64_t drain, char** out_json, char* err, int errcap) {
+    try {
+        std::vector<BuildId> ids;
+        for (int i = 0; i < n_bins; ++i) ids.push_back(id_at(bin_ids + 20 * i));
+        std::vector<StackSample> stream(n);
+        for (uint64_t i = 0; i < n; ++i) {
+            stream[i].timestamp_ns = ts[i];
+            stream[i].rank = rank ? rank[i] : 0;
+            for (uint64_t f = foff[i]; f < foff[i + 1]; ++f) stream[i].frames.push_back({ids.at(bin[f]), pc[f]});
+        }
+        std::vector<ProfileWindow> wins = aggregate_samples(stream, drain);
+        json out = json::array();
+        uint64_t cur = 0;
+        for (const ProfileWindow& w : wins) {
+            while (cur < n && stream[cur].timestamp_ns < w.window_start_ns) ++cur;
+            std::vector<std::pair<const std::vector<FrameRef>*, uint64_t>> first;
+            uint64_t e = cur;
+            while (e < n && stream[e].timestamp_ns < w.window_end_ns) ++e;
+            json recs = json::array();
+            for (const auto& r : w.records) {
+                uint64_t f = e;
+                for (uint64_t i = cur; i < e; ++i)
+                    if (stream[i].frames == r.frames) { f = i; break; }
+                recs.push_back(json::array({f, r.count}));
+            }
+            out.push_back(json::array({w.rank, w.window_start_ns, w.window_end_ns, recs}));
+            cur = e;
+        }
+        *out_json = dup_string(json{{"windows", out}}.dump());
+        return 0;
+    } catch (const std::exception& e) {
+        set_err(err, errcap, e.what());
+        return 1;
+    }
+}
+
 // unknown_frame_label (symfile.cpp:159-163)
 int ref_unknown_label(const uint8_t* build_id, uint64_t off, char* buf, int cap) {
     std::string s = unknown_frame_label(id_at(build_id), off);

@@ -21,8 +21,8 @@ from typing import Optional
 
 import numpy as np
 
-from .abi import (STG_MEM_DEVICE, STG_MEM_HOST, VERDICTS, StgConfig, StgRunStats, StgWindow,
-                  Window, config_struct, default_config)
+from .abi import (STG_AGG_FORCE_EXACT, STG_MEM_DEVICE, STG_MEM_HOST, VERDICTS, StgConfig, StgRunStats,
+                  StgStream, StgWindow, Window, _ptr, config_struct, default_config)
 
 __all__ = ["Context", "StgError", "Window", "load_library", "LIB_PATH", "VERDICTS",
            "default_config"]
@@ -63,6 +63,10 @@ def load_library():
     l.stg_result_folded_text.argtypes = [P, C.c_int32, C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64)]
     l.stg_result_diff_folded.argtypes = [P, C.c_int32, C.c_int32, C.c_char_p, C.c_uint64,
                                          C.POINTER(C.c_uint64)]
+    l.stg_aggregate_samples.argtypes = [P, C.POINTER(StgStream), C.c_int64, C.c_int, C.POINTER(C.c_uint64),
+                                        C.POINTER(C.c_uint64)]
+    l.stg_aggregate_windows.argtypes = [P, P, P, P]
+    l.stg_aggregate_records.argtypes = [P, P, P]
     l.stg_result_rank_count.argtypes = [P, C.POINTER(C.c_uint32)]
     l.stg_result_rank_info.argtypes = [P, C.c_uint32, C.POINTER(C.c_int32), C.POINTER(C.c_uint64),
                                        C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
@@ -136,6 +140,42 @@ class Context:
         buf = C.create_string_buffer(need.value)
         _check(self._l.stg_name(self._h, key, buf, need.value, C.byref(need)))
         return buf.value.decode()
+
+    # ------------------------------------------------------ raw aggregation
+    def aggregate_samples(self, ts, frame_off, frame_pc, frame_bin, rank=None,
+                          drain_interval_ns: int = 5_000_000_000, exact: bool = False):
+        """aggregate_samples (samples.cpp:31-85) on the GPU for one rank's stream.
+
+        Arrays are numpy (host) or torch CUDA tensors (device).  Returns a list of
+        windows (start_ns, end_ns, first_sample[np.uint64], count[np.uint64]) —
+        each record is the first-seen sample of its stack and its count."""
+        keep: list = []
+        dev = hasattr(ts, "data_ptr")
+        st = StgStream()
+        st.memory = STG_MEM_DEVICE if dev else STG_MEM_HOST
+        st.n_samples = int(ts.shape[0] if dev else len(ts))
+        if dev:
+            st.ts, st.rank = _ptr(ts, keep), _ptr(rank, keep)
+            st.frame_off, st.frame_pc, st.frame_bin = (_ptr(frame_off, keep), _ptr(frame_pc, keep),
+                                                       _ptr(frame_bin, keep))
+        else:
+            st.ts = _ptr(np.asarray(ts, np.int64), keep)
+            st.rank = None if rank is None else _ptr(np.asarray(rank, np.int32), keep)
+            st.frame_off = _ptr(np.asarray(frame_off, np.uint64), keep)
+            st.frame_pc = _ptr(np.asarray(frame_pc, np.uint64), keep)
+            st.frame_bin = _ptr(np.asarray(frame_bin, np.uint16), keep)
+        nw, nr = C.c_uint64(), C.c_uint64()
+        _check(self._l.stg_aggregate_samples(self._h, C.byref(st), int(drain_interval_ns),
+                                             STG_AGG_FORCE_EXACT if exact else 0, C.byref(nw), C.byref(nr)))
+        ws = np.zeros(nw.value, np.int64)
+        we = np.zeros(nw.value, np.int64)
+        ro = np.zeros(nw.value + 1, np.uint64)
+        first = np.zeros(nr.value, np.uint64)
+        cnt = np.zeros(nr.value, np.uint64)
+        _check(self._l.stg_aggregate_windows(self._h, ws.ctypes.data, we.ctypes.data, ro.ctypes.data))
+        _check(self._l.stg_aggregate_records(self._h, first.ctypes.data, cnt.ctypes.data))
+        return [(int(ws[w]), int(we[w]), first[ro[w]:ro[w + 1]], cnt[ro[w]:ro[w + 1]])
+                for w in range(nw.value)]
 
     # ---------------------------------------------------------------- window
     def window_run(self, win: Window, cfg: Optional[dict] = None, ingest: bool = True) -> dict:

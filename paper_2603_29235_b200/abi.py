@@ -175,6 +175,22 @@ def config_struct(cfg: Optional[dict] = None) -> StgConfig:
     return c
 
 
+class StgStream(C.Structure):
+    """stg_stream (include/stg.h): one rank's raw sample stream for aggregate_samples."""
+    _fields_ = [
+        ("memory", C.c_int32),
+        ("n_samples", C.c_uint64),
+        ("ts", _p),
+        ("rank", _p),
+        ("frame_off", _p),
+        ("frame_pc", _p),
+        ("frame_bin", _p),
+    ]
+
+
+STG_AGG_FORCE_EXACT = 1
+
+
 def _ptr(a, keep: list):
     """Pointer to a numpy array (host) or torch tensor (device); None -> NULL."""
     if a is None:

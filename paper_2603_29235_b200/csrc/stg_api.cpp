@@ -19,6 +19,10 @@ void run_resolve(Ctx& c, Result& res, uint64_t n, const uint64_t* pc, const uint
 void rank_lines(Ctx& c, uint32_t i, std::vector<uint64_t>& key_off, std::vector<uint32_t>& keys,
                 std::vector<uint64_t>& counts);
 uint64_t render_folded(Ctx& c, int kind, int32_t rank_a, int32_t rank_b);
+void aggregate_samples(Ctx& c, const stg_stream& in, int64_t drain, int flags, uint64_t* n_windows,
+                       uint64_t* n_records);
+void aggregate_windows(Ctx& c, int64_t* start, int64_t* end, uint64_t* rec_off);
+void aggregate_records(Ctx& c, uint64_t* first_sample, uint64_t* count);
 void render_copy(Ctx& c, char* buf, uint64_t len);
 }  // namespace stg
 
@@ -276,6 +280,35 @@ static int folded_text(stg_ctx* ctx, int kind, int32_t a, int32_t b, char* buf, 
         if (!buf) return;
         if (cap < len + 1) stg::fail(STG_EINVAL, "buffer too small");
         stg::render_copy(ctx->impl, buf, len);
+    });
+}
+
+int stg_aggregate_samples(stg_ctx* ctx, const stg_stream* stream, int64_t drain_interval_ns, int flags,
+                          uint64_t* n_windows, uint64_t* n_records) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(ctx->impl.mu);
+        if (!stream) stg::fail(STG_EINVAL, "null stream");
+        STG_CUDA(cudaSetDevice(ctx->impl.device));
+        uint64_t w = 0, r = 0;
+        stg::aggregate_samples(ctx->impl, *stream, drain_interval_ns, flags, &w, &r);
+        if (n_windows) *n_windows = w;
+        if (n_records) *n_records = r;
+    });
+}
+
+int stg_aggregate_windows(stg_ctx* ctx, int64_t* start_ns, int64_t* end_ns, uint64_t* record_off) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(ctx->impl.mu);
+        STG_CUDA(cudaSetDevice(ctx->impl.device));
+        stg::aggregate_windows(ctx->impl, start_ns, end_ns, record_off);
+    });
+}
+
+int stg_aggregate_records(stg_ctx* ctx, uint64_t* first_sample, uint64_t* count) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(ctx->impl.mu);
+        STG_CUDA(cudaSetDevice(ctx->impl.device));
+        stg::aggregate_records(ctx->impl, first_sample, count);
     });
 }
 

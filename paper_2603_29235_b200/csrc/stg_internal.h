@@ -135,6 +135,9 @@ struct Ctx {
     std::map<std::string, DBuf> bufs;
     DBuf& buf(const std::string& k) { return bufs[k]; }
     std::unique_ptr<Result> result;
+    // last aggregate_samples result (stg_samples.cu), device-resident
+    bool ag_valid = false, ag_exact = false;
+    uint64_t ag_windows = 0, ag_records = 0;
     // distributed mode (stg_dist_init): one NCCL communicator per context
     void* comm = nullptr;  // ncclComm_t
     int world = 1, wrank = 0;

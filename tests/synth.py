@@ -286,3 +286,46 @@ def c4_window(ranks: int = 1024, events_per_rank: int = 2000, seed: int = 1, slo
         setattr(w, k, v)
     w.symr = []
     return w
+
+
+def raw_stream(seed: int = 1, n: int = 2000, n_stacks: int = 40, max_depth: int = 12, n_bins: int = 2,
+               span_ns: int = 17_000_000_000, t0: int = 3_000_000_000, rank: int = 3):
+    """One rank's raw sample stream for aggregate_samples (samples.cpp:31-85):
+    stacks drawn from a small population (so records merge), shared prefixes and
+    near-duplicates (same frames, different bin; one frame more/less) so that the
+    merge is by full stack, timestamps non-decreasing with repeats and gaps wider
+    than the drain interval.  Returns (ts, rank[], frame_off, pc, bin, bin_ids)."""
+    rng = np.random.default_rng(seed)
+    pop = []
+    for k in range(n_stacks):
+        d = int(rng.integers(1, max_depth + 1))
+        pcs = rng.integers(0x1000, 0x1000 + 64 * 40, size=d).astype(np.uint64) & ~np.uint64(3)
+        bins = rng.integers(0, n_bins, size=d).astype(np.uint16)
+        pop.append((pcs, bins))
+        if k % 7 == 3:  # near-duplicates
+            b2 = bins.copy()
+            b2[-1] = (b2[-1] + 1) % n_bins
+            pop.append((pcs.copy(), b2))
+            pop.append((pcs[:-1].copy() if d > 1 else pcs.copy(), bins[:-1].copy() if d > 1 else bins.copy()))
+    w = rng.zipf(1.4, size=n) % len(pop)
+    steps = rng.integers(0, 2 * span_ns // max(n, 1) + 1, size=n)
+    steps[rng.random(n) < 0.1] = 0
+    jumps = rng.random(n) < 0.002
+    steps[jumps] += 11_000_000_000
+    ts = (t0 + np.cumsum(steps)).astype(np.int64)
+    off = np.zeros(n + 1, np.uint64)
+    off[1:] = np.cumsum([len(pop[i][0]) for i in w])
+    pc = np.concatenate([pop[i][0] for i in w]) if n else np.zeros(0, np.uint64)
+    bn = np.concatenate([pop[i][1] for i in w]) if n else np.zeros(0, np.uint16)
+    ids = b"".join(build_id(f"raw{b}") for b in range(n_bins))
+    return ts, np.full(n, rank, np.int32), off, pc, bn, ids
+
+
+def oracle_stream(ts, rank, off, pc, bn, ids: bytes):
+    """The same stream in strata_oracle.aggregate_samples' form."""
+    bids = [ids[20 * b:20 * b + 20] for b in range(len(ids) // 20)]
+    out = []
+    for i in range(len(ts)):
+        fr = tuple((bids[int(bn[f])], int(pc[f])) for f in range(int(off[i]), int(off[i + 1])))
+        out.append((int(ts[i]), int(rank[i]) if rank is not None else 0, fr))
+    return out

@@ -425,6 +425,23 @@ def test_oracle_text_artifacts_equal_reference(scenario):
         assert so.diff_folded(prof[a], prof[b]) == text
 
 
+@pytest.mark.parametrize("seed,drain", [(1, 5_000_000_000), (2, 1_000_000_000), (3, 7), (4, 10**15)])
+def test_oracle_aggregate_samples_equals_reference(seed, drain):
+    """aggregate_samples (samples.cpp:31-85): windows, first-seen record order, counts."""
+    from oracle import ref
+    from tests.synth import oracle_stream, raw_stream
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    ts, rk, off, pc, bn, ids = raw_stream(seed=seed, n=1500, t0=-4_000_000_123 if seed == 2 else 3_000_000_000)
+    got = ref.aggregate_samples(ts, off, pc, bn, ids, rank=rk, drain=drain)
+    stream = oracle_stream(ts, rk, off, pc, bn, ids)
+    exp = so.aggregate_samples(stream, drain)
+    assert [(g[1], g[2]) for g in got] == [(e[0], e[1]) for e in exp]
+    for g, e in zip(got, exp):
+        assert [c for _, c in g[3]] == [c for _, c in e[2]]
+        assert [stream[f][2] for f, _ in g[3]] == [fr for fr, _ in e[2]]
+
+
 def test_lookup_matches_reference_probes():
     from oracle import ref
     if not ref.available():
