@@ -58,8 +58,10 @@ def args_parse():
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-budget-s", type=float, default=20.0)
-    p.add_argument("--config", default="c2", choices=["c2", "c4"],
-                   help="c2 = headline (samples/s); c4 = collective alignment, 1,024 ranks x 50k events")
+    p.add_argument("--config", default="c2", choices=["c2", "c4", "agg"],
+                   help="c2 = headline (samples/s); c4 = collective alignment, 1,024 ranks x 50k events; "
+                        "agg = raw aggregate_samples on the BM_Aggregation stream shape")
+    p.add_argument("--agg-samples", type=int, default=64_000_000, help="agg: samples in the stream")
     p.add_argument("--events", type=int, default=50_000, help="c4: events per rank")
     return p.parse_args()
 
@@ -294,6 +296,88 @@ def bench_c4(a, torch, stg, rank, local, world, dist):
         dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------------- agg
+def agg_stream(torch, n: int, seed: int, device: str):
+    """The stream of the reference's BM_Aggregation (benchmarks/bench.cpp:79-95):
+    16 stacks x 12 frames of one binary (offsets 0x1000 + s*64 + d*8), a sample
+    every 10 us, stacks drawn uniformly — here n samples long."""
+    g = torch.Generator(device=device).manual_seed(seed)
+    pick = torch.randint(0, 16, (n,), generator=g, device=device, dtype=torch.int64)
+    d = torch.arange(12, device=device, dtype=torch.int64)
+    pc = (0x1000 + pick[:, None] * 64 + d[None, :] * 8).reshape(-1)
+    ts = torch.arange(n, device=device, dtype=torch.int64) * 10_000
+    off = torch.arange(n + 1, device=device, dtype=torch.int64) * 12
+    bn = torch.zeros(n * 12, device=device, dtype=torch.int16)
+    return ts, off, pc, bn
+
+
+def bench_agg(a, torch, stg, rank, local, world, dist):
+    """Raw-address aggregate_samples (samples.cpp:31-85, §8(f) row 4): one rank's
+    stream per GPU, device-resident, drained every 5 s.  Metric: samples/s."""
+    n = a.agg_samples
+    ts, off, pc, bn = agg_stream(torch, n, 7 + rank, "cuda")
+    ctx = stg.Context(local)
+    for _ in range(a.warmup):
+        wins = ctx.aggregate_samples(ts, off, pc, bn)
+    nrec = sum(len(w[2]) for w in wins)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(a.steps):
+        ctx.aggregate_samples(ts, off, pc, bn)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / a.steps
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    # end to end: the stream in pinned host memory, copied in by the call, records copied out
+    h = [x.cpu().pin_memory() for x in (ts, off, pc, bn)]
+    ctx.aggregate_samples(*h)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(2):
+        ctx.aggregate_samples(*h)
+    e2e_s = (time.perf_counter() - t0) / 2
+    algo = n * (8 + 8 + 12 * 10)  # ts + frame offset + 12 frames x (8 B pc + 2 B bin), read once
+    peak = peaks().get("hbm_gbs", 6650.0)
+    cb = None
+    if rank == 0 and not a.no_cpu_baseline:
+        from oracle import ref
+        if ref.available():
+            k = 2_000_000
+            hs = [x[:k].cpu().numpy() for x in (ts,)] + [off[:k + 1].cpu().numpy().view(np.uint64),
+                                                        pc[:12 * k].cpu().numpy().view(np.uint64),
+                                                        bn[:12 * k].cpu().numpy().view(np.uint16)]
+            from tests.synth import build_id
+            t = ref.aggregate_samples(hs[0], hs[1], hs[2], hs[3], build_id("a"), time_only=True)
+            cb = {"value": k / t, "unit": "samples/s", "cores": 1, "kind": "reference",
+                  "sample": f"first {k} samples of the stream, strata::aggregate_samples alone "
+                            "(single-threaded, as the reference runs it)"}
+    line = {"metric": "raw samples/sec aggregated (aggregate_samples, 5 s drain)",
+            "value": n * world / (ms / 1e3), "unit": "samples/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": f"BM_Aggregation stream shape (bench.cpp:79-95) x {n} samples per GPU",
+                       "inputs": "stream resident in HBM (> L2)", "windows": len(wins), "records": nrec},
+            "e2e": {"value": n * world / e2e_s, "unit": "samples/s",
+                    "h2d_bytes_per_step": int(sum(x.numel() * x.element_size() for x in h)),
+                    "d2h_bytes_per_step": int(nrec * 16 + len(wins) * 24)},
+            "roofline": {"bound": "hbm", "achieved": round(algo / (ms / 1e3) / 1e9, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(algo / (ms / 1e3) / 1e9 / peak, 4), "traffic": None,
+                         "kernel": "whole call (k_agg_hash + k_agg_verify + compaction)",
+                         "algorithmic_bytes": algo},
+            "cpu_baseline": cb}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 # --------------------------------------------------------------------- main
 def main():
     a = args_parse()
@@ -332,6 +416,8 @@ def main():
     from paper_2603_29235_b200.abi import STG_MEM_DEVICE, STG_MEM_HOST
     if a.config == "c4":
         return bench_c4(a, torch, stg, rank, local, world, dist)
+    if a.config == "agg":
+        return bench_agg(a, torch, stg, rank, local, world, dist)
     wl = Workload(a, rank, world)
     ctx = stg.Context(local)
     if world > 1:  # one communication group spanning the GPUs: libstg's own NCCL group

@@ -215,9 +215,10 @@ def detect_straggler(lat: np.ndarray, ranks, k: float = 2.0):
 
 
 def aggregate_samples(ts, frame_off, frame_pc, frame_bin, bin_ids: bytes, rank=None,
-                      drain: int = 5_000_000_000):
+                      drain: int = 5_000_000_000, time_only: bool = False):
     """Reference aggregate_samples (samples.cpp:31-85) on a raw SoA stream.
-    Returns [(rank, start, end, [(first_sample, count), ...])]."""
+    Returns [(rank, start, end, [(first_sample, count), ...])], or with
+    time_only=True the seconds spent inside aggregate_samples alone."""
     ts = np.ascontiguousarray(ts, np.int64)
     foff = np.ascontiguousarray(frame_off, np.uint64)
     pc = np.ascontiguousarray(frame_pc, np.uint64)
@@ -228,12 +229,16 @@ def aggregate_samples(ts, frame_off, frame_pc, frame_bin, bin_ids: bytes, rank=N
     err = C.create_string_buffer(1024)
     L = lib()
     L.ref_aggregate_samples.argtypes = [C.c_uint64] + [C.c_void_p] * 5 + [C.c_int, C.c_void_p, C.c_int64,
-                                                                         C.POINTER(C.c_void_p), C.c_char_p,
-                                                                         C.c_int]
+                                                                         C.c_void_p, C.POINTER(C.c_double),
+                                                                         C.c_char_p, C.c_int]
+    t = C.c_double()
     rc = L.ref_aggregate_samples(len(ts), ts.ctypes.data, None if rk is None else rk.ctypes.data,
                                  foff.ctypes.data, pc.ctypes.data, bn.ctypes.data, len(ids) // 20,
-                                 ids.ctypes.data, int(drain), C.byref(out), err, 1024)
+                                 ids.ctypes.data, int(drain), None if time_only else C.addressof(out),
+                                 C.byref(t), err, 1024)
     if rc != 0:
         raise RefError(err.value.decode())
+    if time_only:
+        return t.value
     j = _take_json(out)
     return [(w[0], w[1], w[2], [tuple(r) for r in w[3]]) for w in j["windows"]]

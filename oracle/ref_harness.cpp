@@ -587,7 +587,7 @@ int ref_pack_symbols(const uint8_t* build_id, uint64_t n, const uint64_t* starts
 // record's (found by scanning the window's samples in order).
 int ref_aggregate_samples(uint64_t n, const int64_t* ts, const int32_t* rank, const uint64_t* foff,
                           const uint64_t* pc, const uint16_t* bin, int n_bins, const uint8_t* bin_ids,
-                          int64_t drain, char** out_json, char* err, int errcap) {
+                          int64_t drain, char** out_json, double* t_agg, char* err, int errcap) {
     try {
         std::vector<BuildId> ids;
         for (int i = 0; i < n_bins; ++i) ids.push_back(id_at(bin_ids + 20 * i));
@@ -597,7 +597,10 @@ int ref_aggregate_samples(uint64_t n, const int64_t* ts, const int32_t* rank, co
             stream[i].rank = rank ? rank[i] : 0;
             for (uint64_t f = foff[i]; f < foff[i + 1]; ++f) stream[i].frames.push_back({ids.at(bin[f]), pc[f]});
         }
+        auto t0 = std::chrono::steady_clock::now();
         std::vector<ProfileWindow> wins = aggregate_samples(stream, drain);
+        if (t_agg) *t_agg = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (!out_json) return 0;
         json out = json::array();
         uint64_t cur = 0;
         for (const ProfileWindow& w : wins) {

@@ -150,11 +150,11 @@ class Context:
         windows (start_ns, end_ns, first_sample[np.uint64], count[np.uint64]) —
         each record is the first-seen sample of its stack and its count."""
         keep: list = []
-        dev = hasattr(ts, "data_ptr")
+        dev = bool(getattr(ts, "is_cuda", False))
         st = StgStream()
         st.memory = STG_MEM_DEVICE if dev else STG_MEM_HOST
         st.n_samples = int(ts.shape[0] if dev else len(ts))
-        if dev:
+        if hasattr(ts, "data_ptr"):  # torch tensors (CUDA, or pinned host for end-to-end use)
             st.ts, st.rank = _ptr(ts, keep), _ptr(rank, keep)
             st.frame_off, st.frame_pc, st.frame_bin = (_ptr(frame_off, keep), _ptr(frame_pc, keep),
                                                        _ptr(frame_bin, keep))

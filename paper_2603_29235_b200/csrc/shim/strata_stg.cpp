@@ -6,6 +6,7 @@
 //   strata::build_group_data   bundle.hpp:51-52  (bundle.cpp:252-324)   -> stg_window_run
 //   strata::resolve_stacks     symrepo.hpp:55-57 (symrepo.cpp:122-143)  -> stg_resolve
 //   strata::resolve_stack      symrepo.hpp:51-53 (symrepo.cpp:99-120)   -> stg_resolve
+//   strata::aggregate_samples  samples.hpp:38-44 (samples.cpp:31-85)    -> stg_aggregate_samples
 //
 // The reference TUs that define these symbols are compiled with
 // -D<name>=<name>_reference (oracle/Makefile `dropin`), everything else of the
@@ -21,7 +22,10 @@
 
 #include "json.hpp"
 #include "stg.h"
+#include <unordered_map>
+
 #include "strata/bundle.hpp"
+#include "strata/samples.hpp"
 #include "strata/symrepo.hpp"
 
 namespace {
@@ -292,6 +296,64 @@ GroupData build_group_data(const LoadedBundle& b, const DiagnosisConfig& config)
     }
     d.iteration_times_ms = j.at("iteration_times_ms").get<std::vector<double>>();
     return d;
+}
+
+// Raw samples -> SoA (build ids interned to bins), aggregated on the GPU; each
+// record's frames are its first-seen sample's frames.
+std::vector<ProfileWindow> aggregate_samples(const std::vector<StackSample>& stream, int64_t drain_interval_ns) {
+    const uint64_t n = stream.size();
+    std::vector<int64_t> ts(n);
+    std::vector<int32_t> rank(n);
+    std::vector<uint64_t> off(n + 1, 0);
+    for (uint64_t i = 0; i < n; ++i) off[i + 1] = off[i] + stream[i].frames.size();
+    std::vector<uint64_t> pc(off[n]);
+    std::vector<uint16_t> bin(off[n]);
+    std::unordered_map<BuildId, uint16_t, BuildIdHash> bins;
+    const BuildId* last = nullptr;  // consecutive frames mostly share a binary
+    uint16_t last_bin = 0;
+    uint64_t k = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const StackSample& s = stream[i];
+        ts[i] = s.timestamp_ns;
+        rank[i] = s.rank;
+        for (const FrameRef& f : s.frames) {
+            if (!last || !(f.build_id == *last)) {
+                auto it = bins.find(f.build_id);
+                if (it == bins.end()) {
+                    if (bins.size() > 0xffff) throw Error("libstg: more than 65536 build ids in one stream");
+                    it = bins.emplace(f.build_id, uint16_t(bins.size())).first;
+                }
+                last = &it->first;
+                last_bin = it->second;
+            }
+            pc[k] = f.offset;
+            bin[k++] = last_bin;
+        }
+    }
+    stg_stream st{};
+    st.memory = STG_MEM_HOST;
+    st.n_samples = n;
+    st.ts = ts.data();
+    st.rank = rank.data();
+    st.frame_off = off.data();
+    st.frame_pc = pc.data();
+    st.frame_bin = bin.data();
+    uint64_t nw = 0, nr = 0;
+    check(stg_aggregate_samples(ctx(), &st, drain_interval_ns, 0, &nw, &nr));
+    std::vector<int64_t> ws(nw), we(nw);
+    std::vector<uint64_t> ro(nw + 1), first(nr), count(nr);
+    check(stg_aggregate_windows(ctx(), ws.data(), we.data(), ro.data()));
+    check(stg_aggregate_records(ctx(), first.data(), count.data()));
+    std::vector<ProfileWindow> out(nw);
+    for (uint64_t w = 0; w < nw; ++w) {
+        ProfileWindow& pw = out[w];
+        pw.rank = stream.front().rank;
+        pw.window_start_ns = ws[w];
+        pw.window_end_ns = we[w];
+        pw.records.reserve(ro[w + 1] - ro[w]);
+        for (uint64_t r = ro[w]; r < ro[w + 1]; ++r) pw.records.push_back({stream[first[r]].frames, count[r]});
+    }
+    return out;
 }
 
 }  // namespace strata

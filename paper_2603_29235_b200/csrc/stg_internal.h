@@ -138,6 +138,7 @@ struct Ctx {
     // last aggregate_samples result (stg_samples.cu), device-resident
     bool ag_valid = false, ag_exact = false;
     uint64_t ag_windows = 0, ag_records = 0;
+    uint64_t ag_cap_hint = 1u << 16;  // table slots the last call needed
     // distributed mode (stg_dist_init): one NCCL communicator per context
     void* comm = nullptr;  // ncclComm_t
     int world = 1, wrank = 0;

@@ -24,3 +24,17 @@ def test_reference_acceptance_gate_relinked_on_gpu():
     assert len(lines) == 11, r.stdout + r.stderr
     assert all(l.startswith("PASS") for l in lines), r.stdout
     assert r.returncode == 0
+
+
+DS = ROOT / "oracle" / "_ref" / "dropin_samples"
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not DS.exists(), reason="oracle/_ref/dropin_samples not built (make -C oracle dropin)")
+def test_aggregate_samples_relinked_on_gpu():
+    """strata::aggregate_samples from the shim (GPU) equals the reference's own
+    (samples.cpp compiled in place, renamed) on the BM_Aggregation stream of
+    benchmarks/bench.cpp:79-100 and on random streams; errors carry the same text."""
+    r = subprocess.run([str(DS)], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0 and "ALL PASS" in r.stdout, r.stdout + r.stderr

@@ -139,3 +139,34 @@ def test_large_stream_properties(ctx):
     exp = so.aggregate_samples(stream)
     assert [c for _, c in exp[0][2]] == [c for _, c in r0]
     assert [stream[f][2] for f, _ in r0] == [fr for fr, _ in exp[0][2]]
+
+
+@need_ref
+def test_aggregate_unaligned_device_input(ctx):
+    """frame arrays not 32/16-byte aligned take the scalar-load kernel variant."""
+    import torch
+    ts, rk, off, pc, bn, ids = raw_stream(seed=13, n=4000)
+    exp = ref.aggregate_samples(ts, off, pc, bn, ids, rank=rk)
+    pc_u = torch.from_numpy(np.concatenate([[0], pc]).astype(np.uint64).view(np.int64)).cuda()[1:]
+    bn_u = torch.from_numpy(np.concatenate([[0], bn]).astype(np.uint16).view(np.int16)).cuda()[1:]
+    assert pc_u.data_ptr() % 32 and bn_u.data_ptr() % 16
+    t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a).view(dt)).cuda()
+    got = ctx.aggregate_samples(t(ts, np.int64), t(off, np.int64), pc_u, bn_u, rank=t(rk, np.int32))
+    got = [(s, e, [(int(f), int(c)) for f, c in zip(fs, cs)]) for s, e, fs, cs in got]
+    assert got == [(s, e, r) for _, s, e, r in exp]
+
+
+def test_aggregate_table_growth_all_distinct(ctx):
+    """A stream of 1.5 M distinct stacks overflows the initial table several
+    times (grow-and-retry); the result equals the exact path and every sample is
+    its own record."""
+    n = 1_500_000
+    rng = np.random.default_rng(3)
+    ts = np.sort(rng.integers(0, 20_000_000_000, size=n)).astype(np.int64)
+    off = (np.arange(n + 1) * 3).astype(np.uint64)
+    pc = np.stack([np.arange(n), rng.integers(0, 1 << 40, size=n), np.full(n, 7)], 1).reshape(-1).astype(np.uint64)
+    bn = np.zeros(3 * n, np.uint16)
+    fast = _gpu(ctx, ts, None, off, pc, bn, 5_000_000_000)
+    assert sum(len(r) for _, _, r in fast) == n
+    assert [f for _, _, r in fast for f, _ in r] == list(range(n))
+    assert fast == _gpu(ctx, ts, None, off, pc, bn, 5_000_000_000, exact=True)
