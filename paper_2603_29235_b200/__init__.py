@@ -139,7 +139,8 @@ class Context:
         _check(self._l.stg_name(self._h, key, None, 0, C.byref(need)))
         buf = C.create_string_buffer(need.value)
         _check(self._l.stg_name(self._h, key, buf, need.value, C.byref(need)))
-        return buf.value.decode()
+        # names are arbitrary bytes (NUL and non-UTF-8 included): keep them all
+        return buf.raw[:need.value - 1].decode("utf-8", "surrogateescape")
 
     # ------------------------------------------------------ raw aggregation
     def aggregate_samples(self, ts, frame_off, frame_pc, frame_bin, rank=None,

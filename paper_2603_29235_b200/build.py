@@ -46,8 +46,8 @@ NCCL_INC = [f"-I{NCCL_DIR / 'include'}"] if NCCL_DIR else []
 NCCL_LINK = ([f"-L{NCCL_DIR / 'lib'}", "-l:libnccl.so.2", "-Xlinker", f"-rpath={NCCL_DIR / 'lib'}"]
              if NCCL_DIR else ["-lnccl"])
 
-CU_SOURCES = ["stg_window.cu", "stg_render.cu", "stg_samples.cu"]
-CPP_SOURCES = ["symtab.cpp", "stg_api.cpp"]
+CU_SOURCES = ["stg_window.cu", "stg_render.cu", "stg_samples.cu", "symtab.cu"]
+CPP_SOURCES = ["stg_api.cpp"]
 HEADERS = ["stg_internal.h", "kernels.cuh", "result.h", "stg_runner.inl", "stg_output.inl"]
 
 

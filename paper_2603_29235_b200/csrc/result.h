@@ -62,7 +62,7 @@ struct Result {
     // name space: final rank -> string
     std::vector<uint64_t> unk_final;       // final rank of each distinct unknown label (sorted)
     std::vector<std::string> unk_labels;   // labels in the same order
-    const std::vector<std::string>* dict = nullptr;
+    const Dict* dict = nullptr;
     std::string name_of(uint32_t final_rank) const;
     // ---- baseline
     bool has_baseline = false;
@@ -84,7 +84,7 @@ struct Result {
     std::string gname(uint32_t g) const {
         auto it = std::lower_bound(g_lab_final.begin(), g_lab_final.end(), uint64_t(g));
         if (it != g_lab_final.end() && *it == g) return g_lab[size_t(it - g_lab_final.begin())];
-        return (*dict)[g - uint64_t(it - g_lab_final.begin())];
+        return std::string((*dict)[g - uint64_t(it - g_lab_final.begin())]);
     }
     stg_run_stats stats{};
     // folded-text artifacts (stg_render.cu): last rendering kept on the device

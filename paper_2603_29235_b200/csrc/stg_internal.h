@@ -9,6 +9,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <string_view>
 #include <unordered_map>
 #include <vector>
 
@@ -80,17 +81,36 @@ struct __align__(16) UnkSlot {
 };
 
 // ------------------------------------------------------------ host-side
+// One ingested SYMR table (symtab.cu).  Entries, names and the search index
+// live on the device; the host keeps the identity and the search bounds.
 struct HostTable {
     uint8_t id[20];
-    std::vector<uint64_t> starts;
-    std::vector<uint32_t> sizes;
-    std::vector<uint32_t> name_local;   // index into names
-    std::vector<std::string> names;     // distinct names of this table
-    // device
-    ulonglong2* d_e = nullptr;
+    uint32_t n = 0;
+    uint64_t first_start = 0, last_start = 0;
+    uint64_t strtab_off = 0;
+    uint8_t* d_payload = nullptr;     // the SYMR bytes (name strings are read from here)
+    uint32_t* d_name_off = nullptr;   // first name byte of entry i, relative to the string table
+    uint32_t* d_name_len = nullptr;
+    ulonglong2* d_e = nullptr;        // {start, size | name_rank << 32}
     uint32_t* d_bucket = nullptr;
     uint32_t shift = 0, nb = 0;
-    uint64_t dict_version = ~0ull;      // dictionary the ent ranks refer to
+    uint64_t dict_version = ~0ull;    // dictionary the ranks in d_e refer to
+    HostTable() = default;
+    HostTable(const HostTable&) = delete;
+    HostTable& operator=(const HostTable&) = delete;
+    ~HostTable();
+};
+
+// The sorted name dictionary: every loaded table's distinct names in byte-wise
+// order (std::string operator<), concatenated; name i = blob[off[i], off[i+1]).
+struct Dict {
+    std::string blob;
+    std::vector<uint64_t> off{0};
+    size_t size() const { return off.size() - 1; }
+    std::string_view operator[](size_t i) const {
+        return std::string_view(blob.data() + off[i], size_t(off[i + 1] - off[i]));
+    }
+    size_t lower_bound(std::string_view s) const;
 };
 
 // Grow-only device buffer.
@@ -126,12 +146,12 @@ struct Ctx {
     std::mutex mu;
     std::vector<std::unique_ptr<HostTable>> tables;
     std::map<std::string, size_t> table_by_id;  // raw 20-byte id -> index
-    // sorted name dictionary over all loaded tables
-    std::vector<std::string> dict;
+    // sorted name dictionary over all loaded tables (device copy: bufs
+    // "dict_blob" / "dict_off", valid for dict_version)
+    Dict dict;
     uint64_t dict_version = 0;
     bool dict_dirty = true;
     uint64_t dict_hash = 0, dict_hash_version = ~0ull, dict_agreed_version = ~0ull;
-    uint64_t dict_blob_version = ~0ull;  // dictionary staged for text rendering
     std::map<std::string, DBuf> bufs;
     DBuf& buf(const std::string& k) { return bufs[k]; }
     std::unique_ptr<Result> result;

@@ -23,9 +23,8 @@ void run_resolve(Ctx& c, Result& res, uint64_t n, const uint64_t* pc, const uint
         auto it = c.table_by_id.find(std::string(reinterpret_cast<const char*>(ids + 20 * b), 20));
         if (it == c.table_by_id.end()) continue;
         HostTable& h = *c.tables[it->second];
-        if (h.starts.empty()) continue;
-        t = DevTable{h.d_e, h.d_bucket, h.starts.front(), h.starts.back(), h.shift, h.nb,
-                     uint32_t(h.starts.size()), 1};
+        if (h.n == 0) continue;
+        t = DevTable{h.d_e, h.d_bucket, h.first_start, h.last_start, h.shift, h.nb, h.n, 1};
     }
     DevTable* d_tabs = rn.up<DevTable>("rv_tabs", tabs.data(), tabs.size());
     const uint64_t* d_pc = rn.up<uint64_t>("rv_pc", pc, n);

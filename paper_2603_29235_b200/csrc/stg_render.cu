@@ -19,8 +19,8 @@
 //      exclusive scan into text offsets;
 //   3. one warp per line writes its bytes: a warp scan places the names, each
 //      lane copies one name, lane 0 writes the counts.
-// The names come from the dictionary blob (cached on the device per dictionary
-// version) and the window's unknown labels "[<build-id hex>+0x<off>]".
+// The names come from the dictionary blob the symbol tables' refresh left on the
+// device (symtab.cu) and the window's unknown labels "[<build-id hex>+0x<off>]".
 #include <cub/cub.cuh>
 
 #include <cstring>
@@ -205,19 +205,7 @@ T get1(Ctx& c, const T* d) {
 
 // Upload the name blobs the arena's final ranks refer to.
 Names stage_names(Ctx& c, Result& r) {
-    if (c.dict_blob_version != c.dict_version || !c.buf("rd_dict_off").p) {
-        std::vector<uint64_t> off(c.dict.size() + 1, 0);
-        for (size_t i = 0; i < c.dict.size(); ++i) off[i + 1] = off[i] + c.dict[i].size();
-        std::string blob;
-        blob.reserve(off.back());
-        for (const auto& s : c.dict) blob += s;
-        uint64_t* d_off = dbuf<uint64_t>(c, "rd_dict_off", off.size());
-        char* d_blob = dbuf<char>(c, "rd_dict", blob.size() + 1);
-        STG_CUDA(cudaMemcpyAsync(d_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice, c.stream));
-        STG_CUDA(cudaMemcpyAsync(d_blob, blob.data(), blob.size(), cudaMemcpyHostToDevice, c.stream));
-        STG_CUDA(cudaStreamSynchronize(c.stream));
-        c.dict_blob_version = c.dict_version;
-    }
+    // the dictionary blob is already on the device (symtab.cu, bufs dict_blob / dict_off)
     if (!r.render_unk_ready) {
         const size_t nu = r.unk_labels.size();
         std::vector<uint64_t> off(nu + 1, 0);
@@ -234,7 +222,7 @@ Names stage_names(Ctx& c, Result& r) {
         STG_CUDA(cudaStreamSynchronize(c.stream));
         r.render_unk_ready = true;
     }
-    return Names{static_cast<const uint64_t*>(c.buf("rd_dict_off").p), static_cast<const char*>(c.buf("rd_dict").p),
+    return Names{static_cast<const uint64_t*>(c.buf("dict_off").p), static_cast<const char*>(c.buf("dict_blob").p),
                  static_cast<const uint64_t*>(c.buf("rd_unk_final").p),
                  static_cast<const uint64_t*>(c.buf("rd_unk_off").p), static_cast<const char*>(c.buf("rd_unk").p),
                  uint32_t(r.unk_labels.size())};

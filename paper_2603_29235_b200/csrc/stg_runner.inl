@@ -570,14 +570,14 @@ struct Runner {
             auto it = c.table_by_id.find(std::string(reinterpret_cast<const char*>(w.bin_build_ids + 20 * b), 20));
             if (it == c.table_by_id.end()) continue;
             HostTable& h = *c.tables[it->second];
-            if (h.starts.empty()) continue;
+            if (h.n == 0) continue;
             t.e = h.d_e;
             t.bucket = h.d_bucket;
-            t.base = h.starts.front();
-            t.last_start = h.starts.back();
+            t.base = h.first_start;
+            t.last_start = h.last_start;
             t.shift = h.shift;
             t.nb = h.nb;
-            t.n = uint32_t(h.starts.size());
+            t.n = h.n;
             t.valid = 1;
         }
         DevTable* d_tabs = up<DevTable>("tabs", tabs.data(), tabs.size());
@@ -801,7 +801,7 @@ struct Runner {
                 unk_final_by_slot[labels[i].second] = uint32_t(last_final);
                 continue;
             }
-            uint64_t pos = uint64_t(std::lower_bound(dict.begin(), dict.end(), lab) - dict.begin());
+            uint64_t pos = uint64_t(dict.lower_bound(lab));
             bool eq = pos < dict.size() && dict[pos] == lab;
             uint64_t fr = pos + ne_before;
             unk_final_by_slot[labels[i].second] = uint32_t(fr);
@@ -1171,8 +1171,8 @@ struct Runner {
         if (gn_ready) return;
         if (c.dict_hash_version != c.dict_version) {  // once per dictionary
             uint64_t hv = 1469598103934665603ull;
-            for (const auto& n : c.dict) {
-                for (unsigned char ch : n) hv = (hv ^ ch) * 1099511628211ull;
+            for (size_t i = 0; i < c.dict.size(); ++i) {
+                for (unsigned char ch : c.dict[i]) hv = (hv ^ ch) * 1099511628211ull;
                 hv = (hv ^ 0xff) * 1099511628211ull;
             }
             c.dict_hash = hv;
@@ -1238,7 +1238,7 @@ struct Runner {
     std::string gname(uint32_t g) const {
         auto it = std::lower_bound(gn.lab_final.begin(), gn.lab_final.end(), uint64_t(g));
         if (it != gn.lab_final.end() && *it == g) return gn.lab[size_t(it - gn.lab_final.begin())];
-        return c.dict[g - uint64_t(it - gn.lab_final.begin())];
+        return std::string(c.dict[g - uint64_t(it - gn.lab_final.begin())]);
     }
     // owner context of each rank's CPU profile (-1: none anywhere)
     std::vector<int32_t> cpu_owner;

@@ -29,10 +29,7 @@
 namespace stg {
 
 Ctx::~Ctx() {
-    for (auto& t : tables) {
-        if (t->d_e) cudaFree(t->d_e);
-        if (t->d_bucket) cudaFree(t->d_bucket);
-    }
+    tables.clear();  // HostTable frees its device arrays
     bufs.clear();
     if (stream) cudaStreamDestroy(stream);
 }
@@ -42,7 +39,7 @@ std::string Result::name_of(uint32_t f) const {
     auto it = std::lower_bound(unk_final.begin(), unk_final.end(), uint64_t(f));
     if (it != unk_final.end() && *it == f) return unk_labels[size_t(it - unk_final.begin())];
     uint64_t before = uint64_t(it - unk_final.begin());
-    return (*dict)[f - before];
+    return std::string((*dict)[f - before]);
 }
 
 namespace {
