@@ -265,6 +265,29 @@ int stg_result_rank_info(stg_ctx* ctx, uint32_t i, int32_t* rank, uint64_t* n_li
 int stg_result_rank_lines(stg_ctx* ctx, uint32_t i, uint64_t* line_key_off /* n_lines+1 */,
                           uint32_t* keys, uint64_t* counts);
 
+/* ---- bundle ingest (load_bundle, bundle.cpp:181-233) ----
+ * Loads a bundle directory as written by write_bundle (bundle.cpp:83-164):
+ * meta.json, gpu_events.jsonl and os_counters.jsonl on the host (nlohmann::json,
+ * as the reference), samples.jsonl and collectives.jsonl decoded on the GPU into
+ * a device-resident window, and the binaries' SYMR tables ingested from
+ * <dir>/symbols/.  The window stays owned by the context until the next load;
+ * stg_bundle_window returns it (memory = coll_memory = STG_MEM_DEVICE) for
+ * stg_window_run.  Errors: the reference's messages for missing files
+ * ("missing bundle file: <path>"), build ids and collective kinds; nlohmann's own
+ * text for the host-parsed files; "<file> line N: <what>" for malformed bulk lines. */
+typedef struct stg_bundle_info {
+    uint32_t n_ranks, n_bins, n_tables_ingested, pad;
+    uint64_t n_samples, n_frames, n_coll, n_gpu, n_os;
+    uint64_t bulk_bytes;        /* samples.jsonl + collectives.jsonl */
+    double read_s, decode_s;    /* file reads; GPU decode of the bulk files */
+    double total_s;
+} stg_bundle_info;
+
+int stg_bundle_load(stg_ctx* ctx, const char* dir, stg_bundle_info* info);
+int stg_bundle_window(stg_ctx* ctx, stg_window* out);
+/* Copy bytes from the context's device memory (e.g. a bundle window's arrays). */
+int stg_device_to_host(stg_ctx* ctx, void* dst, const void* src, uint64_t bytes);
+
 /* ---- raw-address ProfileWindow API (aggregate_samples, samples.hpp:38-44) ----
  * One rank's time-ordered sample stream, structure of arrays.  Frames are raw
  * (bin, offset) pairs, leaf first; a bin stands for one build id (callers intern

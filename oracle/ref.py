@@ -242,3 +242,34 @@ def aggregate_samples(ts, frame_off, frame_pc, frame_bin, bin_ids: bytes, rank=N
         return t.value
     j = _take_json(out)
     return [(w[0], w[1], w[2], [tuple(r) for r in w[3]]) for w in j["windows"]]
+
+
+def write_bundle(scenario: str, seed: int, dirpath: str, ranks: int = 0, iterations: int = 0,
+                 sample_rate_hz: float = 0.0):
+    """Simulate a scenario and write_bundle (bundle.cpp:83-164) it to dirpath."""
+    err = C.create_string_buffer(1024)
+    h = lib().ref_sim_create(scenario.encode(), seed, ranks, iterations, sample_rate_hz, 0.0, -1, 0, err, 1024)
+    if not h:
+        raise RefError(err.value.decode())
+    try:
+        L = lib()
+        L.ref_sim_write_bundle.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_int]
+        if L.ref_sim_write_bundle(h, str(dirpath).encode(), err, 1024) != 0:
+            raise RefError(err.value.decode())
+    finally:
+        lib().ref_sim_free(h)
+
+
+def bundle_run(dirpath: str, want_json: bool = True):
+    """Reference load_bundle + build_group_data + diagnose.
+    Returns (result_json, t_load_s, t_build_s, t_diag_s)."""
+    L = lib()
+    L.ref_bundle_run.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_double),
+                                 C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_char_p, C.c_int]
+    out = C.c_void_p()
+    tl, tb, td = C.c_double(), C.c_double(), C.c_double()
+    err = C.create_string_buffer(1024)
+    if L.ref_bundle_run(str(dirpath).encode(), int(want_json), C.byref(out), C.byref(tl), C.byref(tb),
+                        C.byref(td), err, 1024) != 0:
+        raise RefError(err.value.decode())
+    return _take_json(out), tl.value, tb.value, td.value

@@ -460,6 +460,44 @@ int ref_sim_symr(void* h, int i, const uint8_t** p, uint64_t* n) {
 const char* ref_sim_labels_json(void* h) { return static_cast<SimHandle*>(h)->labels.c_str(); }
 void ref_sim_free(void* h) { delete static_cast<SimHandle*>(h); }
 
+// write_bundle (bundle.cpp:83-164) of a simulation into dir.
+int ref_sim_write_bundle(void* h, const char* dir, char* err, int errcap) {
+    try {
+        write_bundle(static_cast<SimHandle*>(h)->res, dir);
+        return 0;
+    } catch (const std::exception& e) {
+        set_err(err, errcap, e.what());
+        return 1;
+    }
+}
+
+// load_bundle + build_group_data + diagnose on a bundle directory, timed per stage.
+int ref_bundle_run(const char* dir, int want_json, char** out_json, double* t_load, double* t_build,
+                   double* t_diag, char* err, int errcap) {
+    try {
+        auto t0 = std::chrono::steady_clock::now();
+        LoadedBundle b = load_bundle(dir);
+        auto t1 = std::chrono::steady_clock::now();
+        GroupData data = build_group_data(b);
+        auto t2 = std::chrono::steady_clock::now();
+        DiagnosisReport rep = diagnose(data);
+        auto t3 = std::chrono::steady_clock::now();
+        if (t_load) *t_load = std::chrono::duration<double>(t1 - t0).count();
+        if (t_build) *t_build = std::chrono::duration<double>(t2 - t1).count();
+        if (t_diag) *t_diag = std::chrono::duration<double>(t3 - t2).count();
+        if (out_json) {
+            json j;
+            if (want_json) j["groupdata"] = groupdata_json(data);
+            j["report"] = json::parse(rep.to_json());
+            *out_json = dup_string(j.dump());
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        set_err(err, errcap, e.what());
+        return 1;
+    }
+}
+
 // build_group_data + diagnose on the reference.  threads <= 1 runs the
 // reference build_group_data as-is (single-threaded, the reference's only
 // mode); threads > 1 uses the rank-parallel harness above.

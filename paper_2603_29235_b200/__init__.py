@@ -21,8 +21,8 @@ from typing import Optional
 
 import numpy as np
 
-from .abi import (STG_AGG_FORCE_EXACT, STG_MEM_DEVICE, STG_MEM_HOST, VERDICTS, StgConfig, StgRunStats,
-                  StgStream, StgWindow, Window, _ptr, config_struct, default_config)
+from .abi import (STG_AGG_FORCE_EXACT, STG_MEM_DEVICE, STG_MEM_HOST, VERDICTS, StgBundleInfo, StgConfig,
+                  StgRunStats, StgStream, StgWindow, Window, _ptr, config_struct, default_config)
 
 __all__ = ["Context", "StgError", "Window", "load_library", "LIB_PATH", "VERDICTS",
            "default_config"]
@@ -63,6 +63,9 @@ def load_library():
     l.stg_result_folded_text.argtypes = [P, C.c_int32, C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64)]
     l.stg_result_diff_folded.argtypes = [P, C.c_int32, C.c_int32, C.c_char_p, C.c_uint64,
                                          C.POINTER(C.c_uint64)]
+    l.stg_bundle_load.argtypes = [P, C.c_char_p, C.POINTER(StgBundleInfo)]
+    l.stg_bundle_window.argtypes = [P, C.POINTER(StgWindow)]
+    l.stg_device_to_host.argtypes = [P, P, P, C.c_uint64]
     l.stg_aggregate_samples.argtypes = [P, C.POINTER(StgStream), C.c_int64, C.c_int, C.POINTER(C.c_uint64),
                                         C.POINTER(C.c_uint64)]
     l.stg_aggregate_windows.argtypes = [P, P, P, P]
@@ -141,6 +144,53 @@ class Context:
         _check(self._l.stg_name(self._h, key, buf, need.value, C.byref(need)))
         # names are arbitrary bytes (NUL and non-UTF-8 included): keep them all
         return buf.raw[:need.value - 1].decode("utf-8", "surrogateescape")
+
+    # ---------------------------------------------------------------- bundle
+    def load_bundle(self, path) -> dict:
+        """load_bundle (bundle.cpp:181-233) with the bulk files decoded on the GPU;
+        the bundle's symbol tables are ingested.  Returns stg_bundle_info."""
+        info = StgBundleInfo()
+        _check(self._l.stg_bundle_load(self._h, str(path).encode(), C.byref(info)))
+        return info.as_dict()
+
+    def bundle_window(self) -> StgWindow:
+        w = StgWindow()
+        _check(self._l.stg_bundle_window(self._h, C.byref(w)))
+        return w
+
+    def bundle_run(self, cfg: Optional[dict] = None) -> dict:
+        """build_group_data + diagnose on the loaded bundle (device-resident window)."""
+        w = self.bundle_window()
+        cc = config_struct(cfg)
+        st = StgRunStats()
+        _check(self._l.stg_window_run(self._h, C.byref(w), C.byref(cc), C.byref(st)))
+        self.last_stats = st.as_dict()
+        return self.last_stats
+
+    def bundle_arrays(self) -> dict:
+        """The loaded bundle's window with its device arrays copied to numpy (tests)."""
+        w = self.bundle_window()
+
+        def dev(ptr, n, dt):
+            a = np.zeros(n, dt)
+            if n:
+                _check(self._l.stg_device_to_host(self._h, a.ctypes.data, ptr, a.nbytes))
+            return a
+        ns, nf, nc = w.n_samples, w.n_frames, w.n_coll
+        return {
+            "rank_ids": np.ctypeslib.as_array(C.cast(w.rank_ids, C.POINTER(C.c_int32)), (w.n_ranks,)).copy()
+            if w.n_ranks else np.zeros(0, np.int32),
+            "rank_sample_off": np.ctypeslib.as_array(C.cast(w.rank_sample_off, C.POINTER(C.c_uint64)),
+                                                     (w.n_ranks + 1,)).copy(),
+            "bin_build_ids": C.string_at(w.bin_build_ids, 20 * w.n_bins) if w.n_bins else b"",
+            "sample_ts": dev(w.sample_ts, ns, np.int64),
+            "sample_frame_off": dev(w.sample_frame_off, ns + 1 if ns else 0, np.uint64),
+            "frame_pc": dev(w.frame_pc, nf, np.uint64),
+            "frame_bin": dev(w.frame_bin, nf, np.uint16),
+            "coll_rank": dev(w.coll_rank, nc, np.int32), "coll_group": dev(w.coll_group, nc, np.int32),
+            "coll_kind": dev(w.coll_kind, nc, np.uint8), "coll_entry": dev(w.coll_entry, nc, np.int64),
+            "coll_exit": dev(w.coll_exit, nc, np.int64), "coll_gpu_dur": dev(w.coll_gpu_dur, nc, np.int64),
+        }
 
     # ------------------------------------------------------ raw aggregation
     def aggregate_samples(self, ts, frame_off, frame_pc, frame_bin, rank=None,

@@ -191,6 +191,19 @@ class StgStream(C.Structure):
 STG_AGG_FORCE_EXACT = 1
 
 
+class StgBundleInfo(C.Structure):
+    """stg_bundle_info (include/stg.h)."""
+    _fields_ = [
+        ("n_ranks", C.c_uint32), ("n_bins", C.c_uint32), ("n_tables_ingested", C.c_uint32), ("pad", C.c_uint32),
+        ("n_samples", C.c_uint64), ("n_frames", C.c_uint64), ("n_coll", C.c_uint64), ("n_gpu", C.c_uint64),
+        ("n_os", C.c_uint64), ("bulk_bytes", C.c_uint64), ("read_s", C.c_double), ("decode_s", C.c_double),
+        ("total_s", C.c_double),
+    ]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad"}
+
+
 def _ptr(a, keep: list):
     """Pointer to a numpy array (host) or torch tensor (device); None -> NULL."""
     if a is None:

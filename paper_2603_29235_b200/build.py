@@ -46,9 +46,9 @@ NCCL_INC = [f"-I{NCCL_DIR / 'include'}"] if NCCL_DIR else []
 NCCL_LINK = ([f"-L{NCCL_DIR / 'lib'}", "-l:libnccl.so.2", "-Xlinker", f"-rpath={NCCL_DIR / 'lib'}"]
              if NCCL_DIR else ["-lnccl"])
 
-CU_SOURCES = ["stg_window.cu", "stg_render.cu", "stg_samples.cu", "symtab.cu"]
-CPP_SOURCES = ["stg_api.cpp"]
-HEADERS = ["stg_internal.h", "kernels.cuh", "result.h", "stg_runner.inl", "stg_output.inl"]
+CU_SOURCES = ["stg_window.cu", "stg_render.cu", "stg_samples.cu", "symtab.cu", "stg_bundle.cu"]
+CPP_SOURCES = ["stg_api.cpp", "stg_bundle_host.cpp"]
+HEADERS = ["stg_internal.h", "kernels.cuh", "result.h", "stg_runner.inl", "stg_output.inl", "bundle.h"]
 
 
 def _run(cmd):
@@ -80,7 +80,7 @@ def build(verbose: bool = False) -> Path:
     for src in CPP_SOURCES:
         obj = OUT / (Path(src).stem + ".o")
         if _stale(obj, [CSRC / src] + hdrs):
-            _run(["g++", "-std=c++17", "-O2", "-fPIC", *NCCL_INC, f"-I{ROOT / 'include'}", f"-I{CUDA_INC}",
+            _run(["g++", "-std=c++17", "-O2", "-fPIC", *NCCL_INC, f"-I{ROOT / 'include'}", f"-I{JSON_DIR}", f"-I{CUDA_INC}",
                   "-c", str(CSRC / src), "-o", str(obj)])
         objs.append(obj)
     if _stale(LIB, objs):

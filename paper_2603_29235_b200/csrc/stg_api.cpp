@@ -6,6 +6,7 @@
 
 #include <nccl.h>
 
+#include "bundle.h"
 #include "result.h"
 #include "stg_internal.h"
 
@@ -280,6 +281,34 @@ static int folded_text(stg_ctx* ctx, int kind, int32_t a, int32_t b, char* buf, 
         if (!buf) return;
         if (cap < len + 1) stg::fail(STG_EINVAL, "buffer too small");
         stg::render_copy(ctx->impl, buf, len);
+    });
+}
+
+int stg_bundle_load(stg_ctx* ctx, const char* dir, stg_bundle_info* info) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(ctx->impl.mu);
+        if (!dir) stg::fail(STG_EINVAL, "null bundle directory");
+        STG_CUDA(cudaSetDevice(ctx->impl.device));
+        ctx->impl.bundle.reset();
+        stg::bundle_load(ctx->impl, dir, info);
+    });
+}
+
+int stg_bundle_window(stg_ctx* ctx, stg_window* out) {
+    return guard([&] {
+        if (!ctx->impl.bundle) stg::fail(STG_ESTATE, "no bundle loaded on this context");
+        *out = ctx->impl.bundle->w;
+    });
+}
+
+int stg_device_to_host(stg_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(ctx->impl.mu);
+        STG_CUDA(cudaSetDevice(ctx->impl.device));
+        if (bytes) {
+            STG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->impl.stream));
+            STG_CUDA(cudaStreamSynchronize(ctx->impl.stream));
+        }
     });
 }
 

@@ -139,6 +139,7 @@ struct DBuf {
 };
 
 struct Result;  // defined in stg_window.cu
+struct Bundle;  // bundle.h
 
 struct Ctx {
     int device = 0;
@@ -155,6 +156,8 @@ struct Ctx {
     std::map<std::string, DBuf> bufs;
     DBuf& buf(const std::string& k) { return bufs[k]; }
     std::unique_ptr<Result> result;
+    // last loaded bundle (stg_bundle_load); its bulk arrays live in bufs "bd_*"
+    std::shared_ptr<Bundle> bundle;
     // last aggregate_samples result (stg_samples.cu), device-resident
     bool ag_valid = false, ag_exact = false;
     uint64_t ag_windows = 0, ag_records = 0;
