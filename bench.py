@@ -58,10 +58,12 @@ def args_parse():
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-budget-s", type=float, default=20.0)
-    p.add_argument("--config", default="c2", choices=["c2", "c4", "agg"],
+    p.add_argument("--config", default="c2", choices=["c2", "c4", "agg", "bundle"],
                    help="c2 = headline (samples/s); c4 = collective alignment, 1,024 ranks x 50k events; "
-                        "agg = raw aggregate_samples on the BM_Aggregation stream shape")
+                        "agg = raw aggregate_samples on the BM_Aggregation stream shape; "
+                        "bundle = load_bundle (JSONL) + analysis of a C1-scale bundle directory")
     p.add_argument("--agg-samples", type=int, default=64_000_000, help="agg: samples in the stream")
+    p.add_argument("--bundle-spr", type=int, default=100_000, help="bundle: samples per rank (C1: 100k)")
     p.add_argument("--events", type=int, default=50_000, help="c4: events per rank")
     return p.parse_args()
 
@@ -378,6 +380,129 @@ def bench_agg(a, torch, stg, rank, local, world, dist):
         dist.destroy_process_group()
 
 
+# ------------------------------------------------------------------- bundle
+def write_bench_bundle(torch, wl, b, d: Path):
+    """A write_bundle-format directory (bundle.cpp:83-164) for the workload."""
+    from paper_2603_29235_b200.abi import STG_MEM_HOST
+    ts, foff, pc, bn = wl.generate(torch, b.ranks, b.spr)
+    host = (ts.cpu().numpy(), foff.cpu().numpy().view(np.uint64), pc.cpu().numpy().view(np.uint64),
+            bn.cpu().numpy().view(np.uint16))
+    w = wl.window(b.ranks, b.spr, host, STG_MEM_HOST)
+    d.mkdir(parents=True, exist_ok=True)
+    dump = lambda o: json.dumps(o, sort_keys=True, separators=(",", ":"))
+    meta = {"scenario": "bench-c1", "seed": b.seed, "ranks": b.ranks, "iterations": wl.iterations,
+            "sample_rate_hz": 1e9 / wl.period, "group": 0, "max_skew_ns": int(w.max_skew_ns),
+            "window_start_ns": int(w.window_start_ns), "window_end_ns": int(w.window_end_ns),
+            "baseline": {"epoch": "bench", "delta": 0.005, "iteration_ms": float(w.baseline_iteration_ms),
+                         "fractions": {}},
+            "group_ranks": [int(x) for x in w.group_ranks]}
+    (d / "meta.json").write_text(json.dumps(meta, indent=2, sort_keys=True) + "\n")
+    with open(d / "gpu_events.jsonl", "w") as f:
+        for i in range(len(w.gpu_rank)):
+            f.write(dump({"rank": int(w.gpu_rank[i]), "iter": 0, "kernel": w.kernel_names[int(w.gpu_kernel[i])],
+                          "start": int(w.gpu_start[i]), "dur": int(w.gpu_dur[i])}) + "\n")
+    with open(d / "os_counters.jsonl", "w") as f:
+        for i in range(len(w.os_rank)):
+            irq = {w.counter_names[int(w.os_irq_key[k])]: int(w.os_irq_val[k])
+                   for k in range(int(w.os_irq_off[i]), int(w.os_irq_off[i + 1]))}
+            sirq = {w.counter_names[int(w.os_sirq_key[k])]: int(w.os_sirq_val[k])
+                    for k in range(int(w.os_sirq_off[i]), int(w.os_sirq_off[i + 1]))}
+            f.write(dump({"rank": int(w.os_rank[i]), "window_start": int(w.os_window_start[i]), "interrupts": irq,
+                          "softirqs": sirq, "sched_delay_p50_ns": int(w.os_p50[i]),
+                          "sched_delay_p99_ns": int(w.os_p99[i]), "numa_migrations": int(w.os_migrations[i])})
+                    + "\n")
+    for bid, _, _, symr in wl.tables:
+        h = bid.hex()
+        (d / "symbols" / h[:2]).mkdir(parents=True, exist_ok=True)
+        (d / "symbols" / h[:2] / (h + ".symr")).write_bytes(symr)
+    lib = C.CDLL(str(ROOT / "paper_2603_29235_b200" / "libstg_bench.so"))
+    P = C.c_void_p
+    lib.bench_write_jsonl.argtypes = [C.c_char_p, C.c_char_p, C.c_int, P, P, P, P, P, P, C.c_int, P, C.c_uint64,
+                                      P, P, P, P, P, P]
+    arr = lambda x, dt: np.ascontiguousarray(np.asarray(x).astype(dt))
+    keep = [arr(w.rank_ids, np.int32), arr(w.rank_sample_off, np.uint64), host[0], host[1], host[2], host[3],
+            arr(w.bin_build_ids, np.uint8), arr(w.coll_rank, np.int32), arr(w.coll_group, np.int32),
+            arr(w.coll_kind, np.uint8), arr(w.coll_entry, np.int64), arr(w.coll_exit, np.int64),
+            arr(w.coll_gpu_dur, np.int64)]
+    rc = lib.bench_write_jsonl(str(d / "samples.jsonl").encode(), str(d / "collectives.jsonl").encode(),
+                               len(keep[0]), *[k.ctypes.data for k in keep[:6]], len(keep[6]),
+                               keep[6].ctypes.data, len(keep[7]), *[k.ctypes.data for k in keep[7:]])
+    assert rc == 0
+    return b.ranks * b.spr
+
+
+def bench_bundle(a, torch, stg, rank, local, world, dist):
+    """load_bundle (bundle.cpp:181-233) + build_group_data + diagnose of a C1-scale
+    bundle directory (8 ranks x 100k samples, 12-frame stacks, 10k-symbol tables):
+    JSONL bulk decoded on the GPU.  Metric: bundle samples/s, files to verdict."""
+    import copy
+    import shutil
+    import tempfile
+    b = copy.copy(a)
+    b.ranks, b.spr, b.depth, b.nsym, b.pool = 8, a.bundle_spr, 12, 10_000, 2_000
+    wl = Workload(b, rank, world)
+    d = Path(tempfile.mkdtemp(prefix=f"stg_bundle_r{rank}_"))
+    t0 = time.perf_counter()
+    n = write_bench_bundle(torch, wl, b, d)
+    log(f"[bundle r{rank}] wrote {d} in {time.perf_counter() - t0:.1f}s")
+    ctx = stg.Context(local)
+    for _ in range(a.warmup):
+        info = ctx.load_bundle(d)
+        log(f"[bundle r{rank}] warmup load: {info}")
+        st = ctx.bundle_run()
+    rep = ctx.report()
+    log(f"[bundle r{rank}] verdict {rep['verdict']}")
+    if dist:
+        dist.barrier()
+    times, infos = [], []
+    for _ in range(a.steps):
+        t0 = time.perf_counter()
+        infos.append(ctx.load_bundle(d))
+        st = ctx.bundle_run()
+        times.append(time.perf_counter() - t0)
+    sec = float(np.mean(times))
+    if dist:
+        t = torch.tensor([sec], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sec = float(t.item())
+    dec = float(np.mean([i["decode_s"] for i in infos]))
+    rd = float(np.mean([i["read_s"] for i in infos]))
+    bulk = infos[-1]["bulk_bytes"]
+    cb = None
+    if rank == 0 and not a.no_cpu_baseline:
+        from oracle import ref
+        if ref.available():
+            tl, nref = ref.bundle_load_time(str(d))
+            assert nref == n
+            cb = {"value": n / tl, "unit": "samples/s", "cores": 1, "kind": "reference",
+                  "sample": f"the same bundle directory through strata::load_bundle alone ({tl:.2f}s, "
+                            "single-threaded); its build_group_data on this bundle is not timed: it reloads the "
+                            "SYMR tables once per aggregated record (resolve_stack, symrepo.cpp:99-120) and "
+                            "nearly every sample is its own record here (hours)",
+                  "load_bundle_s": tl}
+    line = {"metric": "bundle samples/sec (load_bundle JSONL + build_group_data + diagnose)",
+            "value": n * world / sec, "unit": "samples/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u8", "data": "synthetic",
+            "config": {"workload": "C1-scale bundle directory: 8 ranks x 100k samples, 12-frame stacks, "
+                                   "3 x 10k-symbol tables", "bulk_bytes": bulk},
+            "verdict": rep["verdict"], "flagged_ranks": rep["flagged_ranks"],
+            "stage_s": {"file_read": rd, "gpu_decode": dec, "analysis_device_ms": st["ms_total"]},
+            "roofline": {"bound": "hbm", "achieved": round(bulk / dec / 1e9, 1), "peak": peaks().get("hbm_gbs", 6650.0),
+                         "unit": "GB/s", "frac": round(bulk / dec / 1e9 / peaks().get("hbm_gbs", 6650.0), 4),
+                         "traffic": None, "kernel": "JSONL decode incl. H2D of the file bytes (host-timed)",
+                         "algorithmic_bytes": bulk},
+            "e2e": {"value": n * world / sec, "unit": "samples/s", "h2d_bytes_per_step": bulk,
+                    "d2h_bytes_per_step": 0},
+            "cpu_baseline": cb}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    shutil.rmtree(d, ignore_errors=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 # --------------------------------------------------------------------- main
 def main():
     a = args_parse()
@@ -418,6 +543,8 @@ def main():
         return bench_c4(a, torch, stg, rank, local, world, dist)
     if a.config == "agg":
         return bench_agg(a, torch, stg, rank, local, world, dist)
+    if a.config == "bundle":
+        return bench_bundle(a, torch, stg, rank, local, world, dist)
     wl = Workload(a, rank, world)
     ctx = stg.Context(local)
     if world > 1:  # one communication group spanning the GPUs: libstg's own NCCL group

@@ -273,3 +273,15 @@ def bundle_run(dirpath: str, want_json: bool = True):
                         C.byref(td), err, 1024) != 0:
         raise RefError(err.value.decode())
     return _take_json(out), tl.value, tb.value, td.value
+
+
+def bundle_load_time(dirpath: str):
+    """Reference load_bundle alone: (seconds, samples)."""
+    L = lib()
+    L.ref_bundle_load_time.argtypes = [C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.c_char_p,
+                                       C.c_int]
+    t, n = C.c_double(), C.c_uint64()
+    err = C.create_string_buffer(1024)
+    if L.ref_bundle_load_time(str(dirpath).encode(), C.byref(t), C.byref(n), err, 1024) != 0:
+        raise RefError(err.value.decode())
+    return t.value, n.value

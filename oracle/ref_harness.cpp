@@ -471,6 +471,22 @@ int ref_sim_write_bundle(void* h, const char* dir, char* err, int errcap) {
     }
 }
 
+// load_bundle alone (bundle.cpp:181-233), timed; returns the sample count.
+int ref_bundle_load_time(const char* dir, double* t_load, uint64_t* n_samples, char* err, int errcap) {
+    try {
+        auto t0 = std::chrono::steady_clock::now();
+        LoadedBundle b = load_bundle(dir);
+        *t_load = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        uint64_t n = 0;
+        for (const auto& [r, s] : b.samples) n += s.size();
+        *n_samples = n;
+        return 0;
+    } catch (const std::exception& e) {
+        set_err(err, errcap, e.what());
+        return 1;
+    }
+}
+
 // load_bundle + build_group_data + diagnose on a bundle directory, timed per stage.
 int ref_bundle_run(const char* dir, int want_json, char** out_json, double* t_load, double* t_build,
                    double* t_diag, char* err, int errcap) {

@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 namespace {
 
 __device__ __forceinline__ uint64_t h64(uint64_t z) {
@@ -138,4 +140,67 @@ extern "C" int bench_gen_c2(uint64_t seed, int ranks, uint64_t spr, int depth, u
     g.bin = bin;
     k_gen<<<148 * 16, 256, 0, (cudaStream_t)stream>>>(g);
     return int(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// Bundle writer for `bench.py --config bundle`: samples.jsonl and
+// collectives.jsonl exactly as write_bundle emits them (nlohmann dump of
+// sample_to_json / the collective record, keys in sorted order, bundle.cpp:31-42,
+// 128-139) from host SoA arrays.
+#include <cstdio>
+#include <string>
+#include <vector>
+
+extern "C" int bench_write_jsonl(const char* samples_path, const char* coll_path, int n_ranks, const int32_t* rank_ids,
+                                 const uint64_t* rank_off, const int64_t* ts, const uint64_t* foff, const uint64_t* pc,
+                                 const uint16_t* bin, int n_bins, const uint8_t* bin_ids, uint64_t n_coll,
+                                 const int32_t* c_rank, const int32_t* c_group, const uint8_t* c_kind,
+                                 const int64_t* c_entry, const int64_t* c_exit, const int64_t* c_dur) {
+    static const char* kinds[] = {"AllReduce", "ReduceScatter", "AllGather", "Broadcast", "P2P"};
+    static const char* hexd = "0123456789abcdef";
+    std::vector<std::string> hx(static_cast<size_t>(n_bins));
+    for (int b = 0; b < n_bins; ++b)
+        for (int j = 0; j < 20; ++j) {
+            hx[size_t(b)] += hexd[bin_ids[20 * b + j] >> 4];
+            hx[size_t(b)] += hexd[bin_ids[20 * b + j] & 15];
+        }
+    FILE* f = std::fopen(samples_path, "wb");
+    if (!f) return 1;
+    std::string line;
+    char num[32];
+    for (int r = 0; r < n_ranks; ++r)
+        for (uint64_t s = rank_off[r]; s < rank_off[r + 1]; ++s) {
+            line.assign("{\"frames\":[");
+            for (uint64_t k = foff[s]; k < foff[s + 1]; ++k) {
+                if (k > foff[s]) line += ',';
+                line += "[\"";
+                line += hx[bin[k]];
+                line += "\",";
+                std::snprintf(num, sizeof num, "%llu", (unsigned long long)pc[k]);
+                line += num;
+                line += ']';
+            }
+            std::snprintf(num, sizeof num, "%d", rank_ids[r]);
+            line += "],\"rank\":";
+            line += num;
+            line += ",\"spaces\":\"";
+            line.append(size_t(foff[s + 1] - foff[s]), 'u');
+            std::snprintf(num, sizeof num, "%d", 1000 + rank_ids[r]);
+            line += "\",\"thread\":";
+            line += num;
+            std::snprintf(num, sizeof num, "%lld", (long long)ts[s]);
+            line += ",\"ts\":";
+            line += num;
+            line += "}\n";
+            std::fwrite(line.data(), 1, line.size(), f);
+        }
+    std::fclose(f);
+    f = std::fopen(coll_path, "wb");
+    if (!f) return 1;
+    for (uint64_t i = 0; i < n_coll; ++i)
+        std::fprintf(f, "{\"entry\":%lld,\"exit\":%lld,\"gpu_duration\":%lld,\"group\":%d,\"kind\":\"%s\",\"rank\":%d}\n",
+                     (long long)c_entry[i], (long long)c_exit[i], (long long)c_dur[i], c_group[i], kinds[c_kind[i]],
+                     c_rank[i]);
+    std::fclose(f);
+    return 0;
 }

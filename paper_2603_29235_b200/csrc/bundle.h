@@ -43,8 +43,9 @@ struct Bundle {
     stg_bundle_info info{};
 };
 
-void bundle_decode_samples(Ctx& c, const std::string& bytes, BundleBulk& b);
-void bundle_decode_collectives(Ctx& c, const std::string& bytes, BundleBulk& b);
+const uint8_t* upload_file(Ctx& c, const std::string& path, const std::string& tag, uint64_t& size);
+void bundle_decode_samples(Ctx& c, const uint8_t* d, uint64_t size, BundleBulk& b);
+void bundle_decode_collectives(Ctx& c, const uint8_t* d, uint64_t size, BundleBulk& b);
 void bundle_load(Ctx& c, const std::string& dir, stg_bundle_info* info);
 
 }  // namespace stg

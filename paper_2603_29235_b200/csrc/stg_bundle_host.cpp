@@ -76,23 +76,21 @@ void bundle_load(Ctx& c, const std::string& dir_s, stg_bundle_info* info) {
     } catch (const json::exception& e) {
         fail(STG_EINVAL, e.what());
     }
+    // bulk files: pipelined read -> device, then decoded on the GPU
     double t_read = 0, t_dec = 0;
+    uint64_t bytes_s = 0, bytes_c = 0;
     auto tr = std::chrono::steady_clock::now();
-    std::string samples = read_file(dir / "samples.jsonl");
+    const uint8_t* ds = upload_file(c, (dir / "samples.jsonl").string(), "bs", bytes_s);
     t_read += secs(tr);
     auto td = std::chrono::steady_clock::now();
-    bundle_decode_samples(c, samples, b.bulk);
+    bundle_decode_samples(c, ds, bytes_s, b.bulk);
     t_dec += secs(td);
-    const uint64_t bytes_s = samples.size();
-    samples = std::string();
     tr = std::chrono::steady_clock::now();
-    std::string colls = read_file(dir / "collectives.jsonl");
+    const uint8_t* dc = upload_file(c, (dir / "collectives.jsonl").string(), "bc", bytes_c);
     t_read += secs(tr);
     td = std::chrono::steady_clock::now();
-    bundle_decode_collectives(c, colls, b.bulk);
+    bundle_decode_collectives(c, dc, bytes_c, b.bulk);
     t_dec += secs(td);
-    const uint64_t bytes_c = colls.size();
-    colls = std::string();
     try {
         // gpu_events.jsonl (bundle.cpp:216-225): kernels interned in name order
         std::vector<std::string> kern;

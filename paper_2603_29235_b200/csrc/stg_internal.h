@@ -158,6 +158,13 @@ struct Ctx {
     std::unique_ptr<Result> result;
     // last loaded bundle (stg_bundle_load); its bulk arrays live in bufs "bd_*"
     std::shared_ptr<Bundle> bundle;
+    // bundle file upload threads: pinned double buffers + a stream each
+    struct Uploader {
+        cudaStream_t stream = nullptr;
+        void* pin[2] = {nullptr, nullptr};
+        cudaEvent_t ev[2] = {nullptr, nullptr};
+    };
+    std::vector<Uploader> up;
     // last aggregate_samples result (stg_samples.cu), device-resident
     bool ag_valid = false, ag_exact = false;
     uint64_t ag_windows = 0, ag_records = 0;

@@ -31,6 +31,13 @@ namespace stg {
 Ctx::~Ctx() {
     tables.clear();  // HostTable frees its device arrays
     bufs.clear();
+    for (auto& u : up) {
+        for (int k = 0; k < 2; ++k) {
+            if (u.pin[k]) cudaFreeHost(u.pin[k]);
+            if (u.ev[k]) cudaEventDestroy(u.ev[k]);
+        }
+        if (u.stream) cudaStreamDestroy(u.stream);
+    }
     if (stream) cudaStreamDestroy(stream);
 }
 
