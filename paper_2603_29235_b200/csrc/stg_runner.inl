@@ -1039,18 +1039,32 @@ struct Runner {
     }
     // Exact inclusive fractions over lines [a, a+n) (or over all sequences when
     // merged): returns (dense name, fraction) in name order.
-    std::vector<std::pair<uint32_t, double>> exact_fractions(uint64_t a, uint64_t n, uint64_t total, bool merged,
-                                                             const uint64_t* dn_off = nullptr, const uint32_t* dn = nullptr,
-                                                             const unsigned long long* counts = nullptr) {
-        std::vector<std::pair<uint32_t, double>> out;
-        if (n == 0 || total == 0) return out;
+    using Fracs = std::vector<std::pair<uint32_t, double>>;
+    Fracs exact_fractions(uint64_t a, uint64_t n, uint64_t total, bool merged, const uint64_t* dn_off = nullptr,
+                          const uint32_t* dn = nullptr, const unsigned long long* counts = nullptr) {
+        return std::move(exact_fractions2(a, n, total, 0, 0, 0, merged, dn_off, dn, counts)[0]);
+    }
+    // Two line ranges in one pass (the straggler and the reference rank): one
+    // pair sort with the side in the key, all the running sums in one launch.
+    std::array<Fracs, 2> exact_fractions2(uint64_t a0, uint64_t n0, uint64_t t0, uint64_t a1, uint64_t n1, uint64_t t1,
+                                          bool merged, const uint64_t* dn_off = nullptr, const uint32_t* dn = nullptr,
+                                          const unsigned long long* counts = nullptr) {
+        std::array<Fracs, 2> out;
+        if (t0 == 0) n0 = 0;
+        if (t1 == 0) n1 = 0;
+        const uint64_t n = n0 + n1;
+        if (n == 0) return out;
         const uint64_t* d_dn_off = dn_off ? dn_off : this->d_dn_off;
         const uint32_t* d_dn = dn ? dn : this->d_dn;
-        const uint64_t* lk = merged ? nullptr : d_lkey + a;
-        const unsigned long long* cnt =
-            counts ? counts : (merged ? static_cast<unsigned long long*>(c.buf("seq_counts").p) : d_lcount + a);
+        const uint64_t* lk0 = merged ? nullptr : d_lkey + a0;
+        const uint64_t* lk1 = merged ? nullptr : d_lkey + a1;
+        const unsigned long long* cnt0 =
+            counts ? counts : (merged ? static_cast<unsigned long long*>(c.buf("seq_counts").p) : d_lcount + a0);
+        const unsigned long long* cnt1 = merged ? cnt0 : d_lcount + a1;
+        int LB = 1;
+        while ((uint64_t(1) << LB) < std::max(n0, n1)) ++LB;
         uint64_t* pc = dev<uint64_t>("xf_cnt", n + 1);
-        LAUNCH(k_pair_count, grid_for(n), kThreads, n, lk, d_dn_off, pc);
+        LAUNCH(k_pair_count, grid_for(n), kThreads, n, n0, lk0, lk1, d_dn_off, pc);
         zero(pc + n, 8);
         uint64_t* po = dev<uint64_t>("xf_off", n + 1);
         excl_sum(pc, po, n + 1);
@@ -1060,21 +1074,22 @@ struct Runner {
         uint64_t* keys_s = dev<uint64_t>("xf_keys_s", np);
         double* vals = dev<double>("xf_vals", np);
         double* vals_s = dev<double>("xf_vals_s", np);
-        LAUNCH(k_pair_emit, grid_for(n), kThreads, n, lk, cnt, total, d_dn_off, d_dn, po, keys, vals);
-        sort_pairs(keys, keys_s, vals, vals_s, np);
+        LAUNCH(k_pair_emit, grid_for(n), kThreads, n, n0, lk0, lk1, cnt0, cnt1, t0, t1, d_dn_off, d_dn, po, LB, keys,
+               vals);
+        sort_pairs(keys, keys_s, vals, vals_s, np, LB + 32);
         uint32_t* flag = dev<uint32_t>("xf_flag", np);
-        LAUNCH(k_pair_segflags, grid_for(np), kThreads, np, keys_s, flag);
+        LAUNCH(k_pair_segflags, grid_for(np), kThreads, np, keys_s, LB, flag);
         uint32_t* seg = dev<uint32_t>("xf_seg", np);
         uint64_t nseg = select_flagged(flag, seg, np);
         uint32_t* of = dev<uint32_t>("xf_of", nseg);
         double* ov = dev<double>("xf_ov", nseg);
-        LAUNCH(k_pair_segsum, grid_for(nseg * 32), kThreads, nseg, seg, np, keys_s, vals_s, of, ov);
+        LAUNCH(k_pair_segsum, grid_for(nseg * 32, kSegWarps * 32), kSegWarps * 32, nseg, seg, np, keys_s, LB, vals_s,
+               of, ov);
         std::vector<uint32_t> hf(nseg);
         std::vector<double> hv(nseg);
         down(hf.data(), of, nseg);
         down(hv.data(), ov, nseg);
-        out.resize(nseg);
-        for (uint64_t i = 0; i < nseg; ++i) out[i] = {hf[i], hv[i]};
+        for (uint64_t i = 0; i < nseg; ++i) out[hf[i] >> 31].push_back({hf[i] & 0x7fffffffu, hv[i]});
         return out;
     }
     static double mean_of(const std::vector<double>& v) {
@@ -1566,8 +1581,10 @@ struct Runner {
                 uint64_t lo[2], lo2[2];
                 down(lo, d_line_off + is, 2);
                 down(lo2, d_line_off + iq, 2);
-                auto fs_ = exact_fractions(lo[0], lo[1] - lo[0], h_n_in[is], false);
-                auto fr_ = exact_fractions(lo2[0], lo2[1] - lo2[0], h_n_in[iq], false);
+                auto both = exact_fractions2(lo[0], lo[1] - lo[0], h_n_in[is], lo2[0], lo2[1] - lo2[0], h_n_in[iq],
+                                             false);
+                const auto& fs_ = both[0];
+                const auto& fr_ = both[1];
                 size_t j = 0;
                 for (const auto& [f, fs] : fs_) {  // name order (dense index order)
                     while (j < fr_.size() && fr_[j].first < f) ++j;

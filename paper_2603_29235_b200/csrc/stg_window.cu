@@ -16,6 +16,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -1301,53 +1302,103 @@ __global__ void k_hottest(uint64_t n, const uint64_t* seq_of, const unsigned lon
 // Exact inclusive fractions in the reference's summation order
 // (folded.cpp:45-54): (name, line) pairs sorted, then one sequential sum of
 // double(count)/double(total) per name in line order.
-__global__ void k_pair_count(uint64_t n, const uint64_t* lkey, const uint64_t* dn_off, uint64_t* cnt) {
+__global__ void k_pair_count(uint64_t n, uint64_t n0, const uint64_t* lkey0, const uint64_t* lkey1,
+                             const uint64_t* dn_off, uint64_t* cnt) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
-        uint32_t s = lkey ? uint32_t(lkey[i]) : uint32_t(i);
+        const bool side = i >= n0;
+        const uint64_t j = side ? i - n0 : i;
+        const uint64_t* lk = side ? lkey1 : lkey0;
+        const uint32_t s = lk ? uint32_t(lk[j]) : uint32_t(j);
         cnt[i] = dn_off[s + 1] - dn_off[s];
     }
 }
-__global__ void k_pair_emit(uint64_t n, const uint64_t* lkey, const unsigned long long* cnt_of, uint64_t total,
-                            const uint64_t* dn_off, const uint32_t* dn, const uint64_t* pair_off, uint64_t* keys,
-                            double* vals) {
-    const double t = __ull2double_rn(total);
+// Pairs (name, line) of up to two line ranges (side 0: lines [0, n0), side 1:
+// [n0, n)); key = (side << 31 | name) << LB | line within its side (LB bits hold
+// a line index, so the radix sort only runs LB + 32 bits), value =
+// double(count) / double(total of its side).
+__global__ void k_pair_emit(uint64_t n, uint64_t n0, const uint64_t* lkey0, const uint64_t* lkey1,
+                            const unsigned long long* cnt0, const unsigned long long* cnt1, uint64_t total0,
+                            uint64_t total1, const uint64_t* dn_off, const uint32_t* dn, const uint64_t* pair_off,
+                            int LB, uint64_t* keys, double* vals) {
+    const double t0 = __ull2double_rn(total0), t1 = __ull2double_rn(total1);
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
-        uint32_t s = lkey ? uint32_t(lkey[i]) : uint32_t(i);
-        const double x = __ddiv_rn(__ull2double_rn(cnt_of[i]), t);  // double(l.count) / double(total)
+        const bool side = i >= n0;
+        const uint64_t j = side ? i - n0 : i;
+        const uint64_t* lk = side ? lkey1 : lkey0;
+        const uint32_t s = lk ? uint32_t(lk[j]) : uint32_t(j);
+        const double x = __ddiv_rn(__ull2double_rn((side ? cnt1 : cnt0)[j]), side ? t1 : t0);  // count / total
         uint64_t o = pair_off[i];
+        const uint64_t sb = side ? 1ull << 31 : 0ull;
         for (uint64_t k = dn_off[s]; k < dn_off[s + 1]; ++k, ++o) {
-            keys[o] = (uint64_t(dn[k]) << 32) | uint32_t(i);
+            keys[o] = ((sb | dn[k]) << LB) | j;
             vals[o] = x;
         }
     }
 }
-__global__ void k_pair_segflags(uint64_t np, const uint64_t* keys, uint32_t* flag) {
+__global__ void k_pair_segflags(uint64_t np, const uint64_t* keys, int LB, uint32_t* flag) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < np; i += uint64_t(gridDim.x) * blockDim.x)
-        flag[i] = i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32);
+        flag[i] = i == 0 || (keys[i] >> LB) != (keys[i - 1] >> LB);
 }
-// One warp per name: the reference's running sum, in line order, of the
-// precomputed per-line quotients.  The warp loads 32 consecutive quotients per
-// step (coalesced); every lane then runs the same strictly sequential add chain
-// over them (shuffles are independent of the accumulator, so they issue ahead).
-__global__ void k_pair_segsum(uint64_t nseg, const uint32_t* seg, uint64_t np, const uint64_t* keys,
-                              const double* vals, uint32_t* out_f, double* out_v) {
-    const int lane = threadIdx.x & 31;
-    for (uint64_t g = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; g < nseg;
-         g += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+// One warp per (side, name): the reference's running sum, in line order, of
+// the precomputed per-line quotients (folded.cpp:48-52).  Lane 0 runs the
+// strictly sequential add chain over a 256-value chunk in shared memory while
+// all lanes' loads of the next chunk are in flight (issued before the chain,
+// stored after it), so the chain never waits on L2.
+constexpr int kSegChunk = 256;
+constexpr int kSegWarps = 8;
+__global__ void __launch_bounds__(kSegWarps * 32) k_pair_segsum(uint64_t nseg, const uint32_t* seg, uint64_t np,
+                                                                const uint64_t* keys, int LB, const double* vals,
+                                                                uint32_t* out_side_f, double* out_v) {
+    __shared__ double buf[kSegWarps][2][kSegChunk];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t g = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; g < nseg; g += nw) {
         const uint64_t a = seg[g], b = g + 1 < nseg ? seg[g + 1] : np;
         double acc = 0.0;
-        for (uint64_t c = a; c < b; c += 32) {
-            const double v = c + lane < b ? vals[c + lane] : 0.0;
-            const int n = int(b - c < 32 ? b - c : 32);
-            if (n == 32) {
+        if (b - a <= 32) {  // short: lane 0 adds the (already loaded) values of the warp
+            const double v = a + lane < b ? __ldg(vals + a + lane) : 0.0;
+            double vv[32];
 #pragma unroll
-                for (int k = 0; k < 32; ++k) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, v, k));
-            } else {
-                for (int k = 0; k < n; ++k) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, v, k));
+            for (int k = 0; k < 32; ++k) vv[k] = __shfl_sync(0xffffffffu, v, k);
+            const int n = int(b - a);
+            for (int k = 0; k < n; ++k) acc = __dadd_rn(acc, vv[k]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < kSegChunk / 32; ++j) {
+                const uint64_t x = a + lane + 32 * j;
+                buf[w][0][lane + 32 * j] = x < b ? __ldg(vals + x) : 0.0;
+            }
+            __syncwarp();
+            int cur = 0;
+            for (uint64_t c = a; c < b; c += kSegChunk) {
+                double r[kSegChunk / 32];
+#pragma unroll
+                for (int j = 0; j < kSegChunk / 32; ++j) {
+                    const uint64_t x = c + kSegChunk + lane + 32 * j;
+                    r[j] = x < b ? __ldg(vals + x) : 0.0;
+                }
+                if (lane == 0) {
+                    const int n = int(b - c < kSegChunk ? b - c : kSegChunk);
+                    const double* q = buf[w][cur];
+                    int t = 0;
+                    for (; t + 8 <= n; t += 8) {
+                        double y[8];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) y[k] = q[t + k];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) acc = __dadd_rn(acc, y[k]);
+                    }
+                    for (; t < n; ++t) acc = __dadd_rn(acc, q[t]);
+                }
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < kSegChunk / 32; ++j) buf[w][cur ^ 1][lane + 32 * j] = r[j];
+                __syncwarp();
+                cur ^= 1;
             }
         }
         if (lane == 0) {
-            out_f[g] = uint32_t(keys[a] >> 32);
+            out_side_f[g] = uint32_t(keys[a] >> LB);  // side << 31 | name
             out_v[g] = acc;
         }
     }
