@@ -672,18 +672,21 @@ struct Runner {
             if (need < grid) grid = unsigned(std::max<uint64_t>(need, 1));
             cudaEventRecord(ev[2], st);
             const bool smem_tabs = w.n_bins <= kMaxSmemBins;
-            // STG_SYM_MINB (experiments): resident CTAs per SM the register budget targets
-            static const int minb = std::getenv("STG_SYM_MINB") ? std::atoi(std::getenv("STG_SYM_MINB")) : 5;
+            // STG_SYM_MINB / STG_SYM_PF (experiments): resident CTAs per SM the register
+            // budget targets, and the frame-load variant (0 plain, 1 L2::256B hint,
+            // 2 register double buffer, 3 L2 prefetch of the next block)
+            static const int minb = std::getenv("STG_SYM_MINB") ? std::atoi(std::getenv("STG_SYM_MINB")) : 4;
+            static const int pfv = std::getenv("STG_SYM_PF") ? std::atoi(std::getenv("STG_SYM_PF")) : 0;
             grid = unsigned(dev_sms) * unsigned(minb) * 4;
             if (need < grid) grid = unsigned(std::max<uint64_t>(need, 1));
-#define STG_SYM(MB) \
-    (smem_tabs ? (void)(k_sym_agg<true, MB, 1><<<grid, kThreads, 0, st>>>(p)) : (void)(k_sym_agg<false, MB, 1><<<grid, kThreads, 0, st>>>(p)))
-            switch (minb) {
-                case 3: STG_SYM(3); break;
-                case 5: STG_SYM(5); break;
-                case 6: STG_SYM(6); break;
-                case 8: STG_SYM(8); break;
-                default: STG_SYM(4); break;
+#define STG_SYM(MB, PF) k_sym_agg<true, MB, PF><<<grid, kThreads, 0, st>>>(p)
+            if (!smem_tabs) {
+                k_sym_agg<false, 4, 0><<<grid, kThreads, 0, st>>>(p);
+            } else if (minb == 3) {
+                if (pfv == 2) STG_SYM(3, 2); else if (pfv == 1) STG_SYM(3, 1); else STG_SYM(3, 0);
+            } else {
+                if (pfv == 2) STG_SYM(4, 2); else if (pfv == 1) STG_SYM(4, 1); else if (pfv == 3) STG_SYM(4, 3);
+                else STG_SYM(4, 0);
             }
 #undef STG_SYM
             STG_CUDA(cudaGetLastError());

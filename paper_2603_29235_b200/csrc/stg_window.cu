@@ -614,38 +614,43 @@ struct AggParams {
     uint64_t n_frames;
 };
 
+// atom.global.cas.b128 against an empty (0, 0) key: returns the previous key.
+__device__ __forceinline__ void cas128(unsigned long long* addr, unsigned long long va, unsigned long long vb,
+                                       unsigned long long& oa, unsigned long long& ob) {
+    asm volatile("{\n\t.reg .b128 c, v, d;\n\t"
+                 "mov.b128 c, {%2, %2};\n\t"
+                 "mov.b128 v, {%3, %4};\n\t"
+                 "atom.global.cas.b128 d, [%5], c, v;\n\t"
+                 "mov.b128 {%0, %1}, d;\n\t}"
+                 : "=l"(oa), "=l"(ob)
+                 : "l"(0ull), "l"(va), "l"(vb), "l"(addr)
+                 : "memory");
+}
+
+// Open addressing on the 128-bit key (hi, lo): one 16 B L2 read per probe; an
+// empty slot is claimed with a single 128-bit CAS (both halves at once, so no
+// reader ever sees a half-written key and no fence is needed); counts are
+// fire-and-forget reductions.  rep is read only after the kernel.
 __device__ __forceinline__ void agg_insert(AggSlot* T, uint32_t mask, uint64_t fa, uint64_t fb, uint32_t rep,
                                            uint32_t cnt, unsigned* used, int* overflow) {
     uint32_t i = uint32_t(fb >> 20) & mask;
     for (uint32_t probe = 0; probe <= mask; ++probe) {
         ulonglong2 cur = __ldcg(reinterpret_cast<const ulonglong2*>(T + i));  // (hi, lo) in one L2 read
-        if (cur.x == fa && cur.y == fb) {
-            atomicAdd(&T[i].count, cnt);
-            return;
-        }
-        if (cur.x == 0) {
-            unsigned long long prev = atomicCAS(&T[i].hi, 0ull, (unsigned long long)fa);
-            if (prev == 0) {
+        if ((cur.x | cur.y) == 0) {
+            unsigned long long oa, ob;
+            cas128(&T[i].hi, fa, fb, oa, ob);
+            if ((oa | ob) == 0) {
                 T[i].rep = rep;
-                __threadfence();
-                *(volatile unsigned long long*)&T[i].lo = fb;
                 atomicAdd(&T[i].count, cnt);
                 if (atomicAdd(used, 1u) + 1 > (mask + 1) / 2) *overflow = 1;
                 return;
             }
-            cur.x = prev;
-            cur.y = 0;
+            cur.x = oa;
+            cur.y = ob;
         }
-        if (cur.x == fa) {
-            unsigned long long lo = cur.y;
-            while (lo == 0) {
-                __nanosleep(16);
-                lo = *(volatile unsigned long long*)&T[i].lo;
-            }
-            if (lo == fb) {
-                atomicAdd(&T[i].count, cnt);
-                return;
-            }
+        if (cur.x == fa && cur.y == fb) {
+            atomicAdd(&T[i].count, cnt);
+            return;
         }
         i = (i + 1) & mask;
     }
@@ -663,6 +668,29 @@ __device__ __forceinline__ void raw_add(uint64_t& ha, uint64_t& hb, uint64_t t) 
     hb += (t >> 29) | (t << 35);
 }
 
+// Raw-chain fingerprint, block form.  Frames are taken in aligned blocks of 8
+// (the vector loads' granularity); a block contributes five 64x64->128-bit
+// products — four over pc pairs, one over the packed bins — each operand
+// xor-keyed by its slot and the block's position q, and the sum of the low
+// and high halves is the 128-bit fingerprint (ha, hb).  A single changed frame
+// always changes the exact product, so (ha, hb) with the sample's alignment
+// and depth mixed in at the end is a cache key; frames outside the sample's
+// non-leaf range are zeroed, so the key depends on the chain, its depth and
+// f0 mod 8 only.  ~9 instructions per frame instead of one 64-bit mix each.
+__device__ __forceinline__ void mum_acc(uint64_t x, uint64_t y, uint64_t& ha, uint64_t& hb) {
+    ha += x * y;
+    hb += __umul64hi(x, y);
+}
+__device__ __forceinline__ void raw_block(const uint64_t (&pc)[8], uint64_t b01, uint64_t b23, uint64_t q,
+                                          uint64_t& ha, uint64_t& hb) {
+    const uint64_t B = (q + 1) * 0x9e3779b97f4a7c15ull;
+    mum_acc(pc[0] ^ B ^ 0x243f6a8885a308d3ull, pc[1] ^ B ^ 0x13198a2e03707344ull, ha, hb);
+    mum_acc(pc[2] ^ B ^ 0xa4093822299f31d0ull, pc[3] ^ B ^ 0x082efa98ec4e6c89ull, ha, hb);
+    mum_acc(pc[4] ^ B ^ 0x452821e638d01377ull, pc[5] ^ B ^ 0xbe5466cf34e90c6cull, ha, hb);
+    mum_acc(pc[6] ^ B ^ 0xc0ac29b7c97c50ddull, pc[7] ^ B ^ 0x3f84d5b5b5470917ull, ha, hb);
+    mum_acc(b01 ^ B ^ 0x9216d5d98979fb1bull, b23 ^ B ^ 0xd1310ba698dfb5acull, ha, hb);
+}
+
 // 256-bit read-only global load (sm_100: LDG.E.ENL2.256), 32-byte aligned.
 __device__ __forceinline__ void ld256(const uint64_t* p, uint64_t& a, uint64_t& b, uint64_t& c, uint64_t& d) {
     asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0, %1, %2, %3}, [%4];"
@@ -670,34 +698,66 @@ __device__ __forceinline__ void ld256(const uint64_t* p, uint64_t& a, uint64_t& 
                  : "l"(p));
 }
 
-// Prefix cache.  Entries are immutable once published: writer claims hi by CAS,
-// stores (ta, tb), fences, then stores lo.  A reader takes (hi, lo) and (ta, tb)
-// with two 16-byte L2 reads issued together; an entry seen with lo published but
-// (ta, tb) still zero (a torn read racing the writer) is treated as a miss.
+// One aligned block of 8 frames for this lane: pcs by two 256-bit loads (each
+// lane takes a whole 32 B sector per instruction, read-only path, no L1
+// allocation), bins by one 16 B load; scalar and zero-filled past the end of
+// the frame array.  PF == 1 adds the L2::256B prefetch-size hint.
+template <int PF>
+__device__ __forceinline__ void load_block(const uint64_t* pc, const uint16_t* bin, uint64_t n_frames, uint64_t bb,
+                                           uint64_t (&pcs)[8], uint4& bq) {
+    if (bb + 8 <= n_frames) {
+        if (PF == 1) {
+            asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u64 {%0, %1, %2, %3}, [%4];"
+                         : "=l"(pcs[0]), "=l"(pcs[1]), "=l"(pcs[2]), "=l"(pcs[3]) : "l"(pc + bb));
+            asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u64 {%0, %1, %2, %3}, [%4];"
+                         : "=l"(pcs[4]), "=l"(pcs[5]), "=l"(pcs[6]), "=l"(pcs[7]) : "l"(pc + bb + 4));
+            asm volatile("ld.global.nc.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(bq.x), "=r"(bq.y), "=r"(bq.z), "=r"(bq.w) : "l"(bin + bb));
+        } else {
+            ld256(pc + bb, pcs[0], pcs[1], pcs[2], pcs[3]);
+            ld256(pc + bb + 4, pcs[4], pcs[5], pcs[6], pcs[7]);
+            bq = __ldg(reinterpret_cast<const uint4*>(bin + bb));
+        }
+    } else {
+        uint32_t bw[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            const bool ok = bb + t < n_frames;
+            pcs[t] = ok ? pc[bb + t] : 0;
+            bw[t >> 1] |= (ok ? uint32_t(bin[bb + t]) : 0u) << (16 * (t & 1));
+        }
+        bq = make_uint4(bw[0], bw[1], bw[2], bw[3]);
+    }
+}
+
+// Prefix cache.  Entries are immutable once published: the writer claims the
+// 128-bit key (hi, lo) with one CAS, then stores (ta, tb) as one 16 B store.  A
+// reader takes (hi, lo) and (ta, tb) with two 16-byte L2 reads issued together;
+// a key seen with (ta, tb) still zero (racing the writer) is treated as a miss.
 __device__ __forceinline__ void pfx_put(PfxSlot* T, uint32_t mask, uint64_t ha, uint64_t hb, uint64_t ta, uint64_t tb) {
     uint32_t i = uint32_t(hb >> 24) & mask;
     for (int probe = 0; probe < 16; ++probe) {
-        unsigned long long cur = atomicCAS(&T[i].hi, 0ull, (unsigned long long)ha);
-        if (cur == 0) {
-            T[i].ta = ta;
-            T[i].tb = tb;
-            __threadfence();
-            *(volatile unsigned long long*)&T[i].lo = hb;
+        unsigned long long oa, ob;
+        cas128(&T[i].hi, ha, hb, oa, ob);
+        if ((oa | ob) == 0) {
+            __stcg(reinterpret_cast<ulonglong2*>(&T[i].ta), make_ulonglong2(ta, tb));
             return;
         }
-        if (cur == ha) return;  // someone else stores the same chain
+        if (oa == ha && ob == hb) return;  // someone else stores the same chain
         i = (i + 1) & mask;
     }
 }
 
 // The fused hot kernel (stage a+b), one lane per sample.  A warp takes 32
-// consecutive samples — one contiguous block of frames in HBM:
-//  phase 0  lane s loads its ts and CSR bounds (coalesced), applies the window
-//           filter on the aligned clock (bundle.cpp:290-294);
-//  phase 1  lane s streams its own frames with 16-byte vector loads (8 frames =
-//           4 x 16 B of pc + 16 B of bin per step, streaming cache hint) and
-//           folds the NON-LEAF frames into a 128-bit raw-chain fingerprint;
-//           the warp as a whole reads its 20 KB block sector-complete;
+// consecutive samples — one contiguous block of frames in HBM — and owns a
+// contiguous range of such batches, so its rank only moves forward:
+//  phase 0  lane s loads its ts and CSR bound (coalesced; the neighbours' by
+//           shuffle), applies the window filter on the aligned clock
+//           (bundle.cpp:290-294);
+//  phase 1  lane s streams its own frames in aligned blocks of 8 (two 256-bit
+//           pc loads + 16 B of bins) and folds the NON-LEAF frames into a
+//           128-bit raw-chain fingerprint (raw_block); the warp as a whole
+//           reads its 20 KB block sector-complete;
 //  phase 2  lane s: prefix-cache probe (the raw chain's symbolized terms —
 //           return addresses repeat, so hits dominate) overlapped with the leaf
 //           lookup in the staged table (symfile.cpp:54-75), fingerprint of the
@@ -705,7 +765,7 @@ __device__ __forceinline__ void pfx_put(PfxSlot* T, uint32_t mask, uint64_t ha, 
 //           open-addressing table with __match_any pre-aggregation;
 //  misses   the warp symbolizes the missing chains cooperatively and fills
 //           the cache.
-template <bool SMEM_TABS, int MINB, int UB>
+template <bool SMEM_TABS, int MINB, int PF>
 __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
     __shared__ DevTable s_tabs[kMaxSmemBins];
     if (SMEM_TABS) {
@@ -718,100 +778,84 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
     const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
     const uint64_t n_batches = (p.n_samples + 31) / 32;
     unsigned long long hits = 0, misses = 0;
-    for (uint64_t bt = warp; bt < n_batches; bt += nwarps) {
-        // ---------------- phase 0: lane s owns sample i
+    // each warp owns a contiguous range of batches, so its rank advances
+    // monotonically (one cached boundary compare per batch, no search)
+    const uint64_t per = (n_batches + nwarps - 1) / nwarps;
+    const uint64_t b_begin = warp * per;
+    const uint64_t b_end = b_begin + per < n_batches ? b_begin + per : n_batches;
+    int r_cur = 0;
+    if (b_begin < b_end) {
+        const uint64_t q = b_begin * 32;
+        int lo = 0, hi = p.R - 1;
+        while (lo < hi) {
+            int mid = (lo + hi + 1) >> 1;
+            if (__ldg(p.rank_soff + mid) <= q) lo = mid; else hi = mid - 1;
+        }
+        r_cur = lo;
+    }
+    for (uint64_t bt = b_begin; bt < b_end; ++bt) {
+        // ---------------- phase 0: lane s owns sample i; its stream loads are
+        // issued before the rank-dependent ones resolve
         const uint64_t i = bt * 32 + lane;
-        bool valid = i < p.n_samples;
-        int r = 0;
+        const bool valid = i < p.n_samples;
+        const uint64_t q = valid ? i : p.n_samples - 1;
+        const int64_t t = __ldcs(p.ts + q);
+        uint64_t f0 = __ldcs(p.foff + q);
+        const bool own_next = lane == 31 || i + 1 >= p.n_samples;
+        uint64_t f1 = own_next ? __ldcs(p.foff + q + 1) : 0;
+        const int64_t t_prev = lane == 0 && q > 0 ? __ldcs(p.ts + q - 1) : 0;
+        int r = r_cur;
+        while (q >= __ldg(p.rank_soff + r + 1)) ++r;
+        r_cur = __shfl_sync(0xffffffffu, r, 31);
+        const uint64_t rs = __ldg(p.rank_soff + r);
         {
-            uint64_t q = valid ? i : p.n_samples - 1;
-            int lo = 0, hi = p.R - 1;
-            while (lo < hi) {
-                int mid = (lo + hi + 1) >> 1;
-                if (__ldg(p.rank_soff + mid) <= q) lo = mid; else hi = mid - 1;
-            }
-            r = lo;
+            const uint64_t up = __shfl_down_sync(0xffffffffu, f0, 1);
+            if (!own_next) f1 = up;
+            int64_t tp = __shfl_up_sync(0xffffffffu, t, 1);
+            if (lane == 0) tp = t_prev;
+            if (valid && q > rs && t < tp && p.active[r]) p.unsorted[r] = 1;
         }
-        uint64_t rs = __ldg(p.rank_soff + r);
-        bool inwin = false;
-        uint64_t f0 = 0, f1 = 0;
-        if (valid && p.active[r]) {
-            int64_t t = __ldcs(p.ts + i);
-            if (i > rs && t < __ldcs(p.ts + i - 1)) p.unsorted[r] = 1;
-            inwin = t - __ldg(p.rank_clk + r) >= p.ws;
-            if (inwin) {
-                f0 = __ldcs(p.foff + i);
-                f1 = __ldcs(p.foff + i + 1);
-                if (f1 == f0) {
-                    atomicMin(p.err_empty + r, (unsigned long long)(i - rs));
-                    inwin = false;
-                }
-            }
+        bool inwin = valid && p.active[r] && t - __ldg(p.rank_clk + r) >= p.ws;
+        if (inwin && f1 == f0) {
+            atomicMin(p.err_empty + r, (unsigned long long)(i - rs));
+            inwin = false;
         }
+        if (!inwin) f0 = f1 = 0;
         const uint32_t depth = uint32_t(f1 - f0);
         // ---------------- phase 1: this lane's frames, 8 per step
         uint64_t leaf_pc = 0, ha = 0, hb = 0;
         uint32_t leaf_bin = 0;
         if (inwin) {
-            // UB blocks of 8 frames per step: all their loads are issued before hashing
-            for (uint64_t blk = f0 & ~7ull; blk < f1; blk += 8 * UB) {
-                if (blk + 8 * UB <= p.n_frames) {
-                    uint64_t pcs[UB][8];
-                    uint32_t bns[UB][8];
+            const uint64_t a0 = f0 & ~7ull;
+            for (uint64_t bb = a0; bb < f1; bb += 8) {
+                uint64_t pcs[8];
+                uint4 bq;
+                load_block<PF>(p.pc, p.bin, p.n_frames, bb, pcs, bq);
+                if (!(bb > f0 && bb + 8 <= f1)) {  // boundary block: take the leaf, zero the rest
+                    uint32_t bw[4] = {bq.x, bq.y, bq.z, bq.w};
 #pragma unroll
-                    for (int u = 0; u < UB; ++u) {
-                        // read-only path, L1-allocating: the lane's next 16 B load takes the
-                        // other half of the same 32 B sector
-                        const uint64_t bb = blk + 8 * u;
-                        if (u == 0 || bb < f1) {
-                            // two 256-bit loads: each lane takes a whole 32 B sector per
-                            // instruction (half the L1 wavefronts of 16 B loads)
-                            ld256(p.pc + bb, pcs[u][0], pcs[u][1], pcs[u][2], pcs[u][3]);
-                            ld256(p.pc + bb + 4, pcs[u][4], pcs[u][5], pcs[u][6], pcs[u][7]);
-                            const uint4 bq = __ldg(reinterpret_cast<const uint4*>(p.bin + bb));
-                            bns[u][0] = bq.x & 0xffffu; bns[u][1] = bq.x >> 16; bns[u][2] = bq.y & 0xffffu;
-                            bns[u][3] = bq.y >> 16; bns[u][4] = bq.z & 0xffffu; bns[u][5] = bq.z >> 16;
-                            bns[u][6] = bq.w & 0xffffu; bns[u][7] = bq.w >> 16;
-                        }
-                    }
-#pragma unroll
-                    for (int u = 0; u < UB; ++u) {
-                        const uint64_t bb = blk + 8 * u;
-                        if (u > 0 && bb >= f1) break;
-                        const uint32_t pos0 = uint32_t(bb - f0);
-                        if (bb > f0 && bb + 8 <= f1) {  // interior block: all 8 frames are non-leaf
-#pragma unroll
-                            for (int t = 0; t < 8; ++t) raw_add(ha, hb, raw_t(pcs[u][t], bns[u][t], pos0 + t));
-                        } else {
-#pragma unroll
-                            for (int t = 0; t < 8; ++t) {
-                                const uint64_t j = bb + t;
-                                if (j == f0) {
-                                    leaf_pc = pcs[u][t];
-                                    leaf_bin = bns[u][t];
-                                }
-                                const uint64_t m = (j > f0 && j < f1) ? ~0ull : 0ull;
-                                raw_add(ha, hb, raw_t(pcs[u][t], bns[u][t], pos0 + t) & m);
-                            }
-                        }
-                    }
-                } else {  // tail of the frame array: scalar
-                    for (uint64_t j = blk > f0 ? blk : f0; j < f1 && j < blk + 8 * UB; ++j) {
-                        const uint64_t pcv = p.pc[j];
-                        const uint32_t bv = p.bin[j];
+                    for (int t = 0; t < 8; ++t) {
+                        const uint64_t j = bb + t;
+                        const uint32_t bv = (bw[t >> 1] >> (16 * (t & 1))) & 0xffffu;
                         if (j == f0) {
-                            leaf_pc = pcv;
+                            leaf_pc = pcs[t];
                             leaf_bin = bv;
-                        } else {
-                            raw_add(ha, hb, raw_t(pcv, bv, uint32_t(j - f0)));
+                        }
+                        if (!(j > f0 && j < f1)) {
+                            pcs[t] = 0;
+                            bw[t >> 1] &= ~(0xffffu << (16 * (t & 1)));
                         }
                     }
+                    bq = make_uint4(bw[0], bw[1], bw[2], bw[3]);
                 }
+                raw_block(pcs, uint64_t(bq.x) | (uint64_t(bq.y) << 32), uint64_t(bq.z) | (uint64_t(bq.w) << 32),
+                          (bb - a0) >> 3, ha, hb);
             }
         }
         const unsigned need = __ballot_sync(0xffffffffu, inwin && depth > 1);
-        uint64_t my_ra = mix_a(ha ^ (uint64_t(depth) * 0x8cb92ba72f3d8dd7ull));
-        uint64_t my_rb = mix_b(hb + uint64_t(depth));
+        const uint64_t shape = uint64_t(depth) | (uint64_t(f0 & 7) << 32);
+        uint64_t my_ra = mix_a(ha ^ (shape * 0x8cb92ba72f3d8dd7ull));
+        uint64_t my_rb = mix_b(hb + shape);
         if (my_ra == 0) my_ra = 1;
         if (my_rb == 0) my_rb = 1;
         // ---------------- phase 2: per-lane cache probe overlapped with the leaf lookup
