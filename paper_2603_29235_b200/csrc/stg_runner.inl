@@ -664,6 +664,8 @@ struct Runner {
             p.pfx = pfx;
             p.pfx_mask = pfx_cap - 1;
             p.stat = d_stat;
+            static const int order = std::getenv("STG_SYM_ORDER") ? std::atoi(std::getenv("STG_SYM_ORDER")) : 0;
+            p.order = order;
             zero(pfx, size_t(pfx_cap) * sizeof(PfxSlot));
             zero(d_stat, 16);
             unsigned grid = unsigned(dev_sms) * 8;
@@ -672,22 +674,24 @@ struct Runner {
             if (need < grid) grid = unsigned(std::max<uint64_t>(need, 1));
             cudaEventRecord(ev[2], st);
             const bool smem_tabs = w.n_bins <= kMaxSmemBins;
-            // STG_SYM_MINB / STG_SYM_PF (experiments): resident CTAs per SM the register
-            // budget targets, and the frame-load variant (0 plain, 1 L2::256B hint,
-            // 2 register double buffer, 3 L2 prefetch of the next block)
+            // STG_SYM_MINB / STG_SYM_UB (experiments): resident CTAs per SM the register
+            // budget targets, and the frame blocks each lane has in flight per step
             static const int minb = std::getenv("STG_SYM_MINB") ? std::atoi(std::getenv("STG_SYM_MINB")) : 4;
-            static const int pfv = std::getenv("STG_SYM_PF") ? std::atoi(std::getenv("STG_SYM_PF")) : 0;
+            static const int ubv = std::getenv("STG_SYM_UB") ? std::atoi(std::getenv("STG_SYM_UB")) : 1;
             grid = unsigned(dev_sms) * unsigned(minb) * 4;
             if (need < grid) grid = unsigned(std::max<uint64_t>(need, 1));
-#define STG_SYM(MB, PF) k_sym_agg<true, MB, PF><<<grid, kThreads, 0, st>>>(p)
-            if (!smem_tabs) {
-                k_sym_agg<false, 4, 0><<<grid, kThreads, 0, st>>>(p);
-            } else if (minb == 3) {
-                if (pfv == 2) STG_SYM(3, 2); else if (pfv == 1) STG_SYM(3, 1); else STG_SYM(3, 0);
-            } else {
-                if (pfv == 2) STG_SYM(4, 2); else if (pfv == 1) STG_SYM(4, 1); else if (pfv == 3) STG_SYM(4, 3);
-                else STG_SYM(4, 0);
-            }
+#define STG_SYM(MB, UB) k_sym_agg<true, MB, UB><<<grid, kThreads, 0, st>>>(p)
+            if (!smem_tabs) k_sym_agg<false, 4, 1><<<grid, kThreads, 0, st>>>(p);
+            else if (minb == 3 && ubv == 2) STG_SYM(3, 2);
+            else if (minb == 2 && ubv == 4) STG_SYM(2, 4);
+            else if (minb == 2 && ubv == 2) STG_SYM(2, 2);
+            else if (minb == 1 && ubv == 8) STG_SYM(1, 8);
+            else if (minb == 3) STG_SYM(3, 1);
+            else if (minb == 5 && ubv == 0) STG_SYM(5, 0);
+            else if (minb == 6 && ubv == 0) STG_SYM(6, 0);
+            else if (minb == 4 && ubv == 0) STG_SYM(4, 0);
+            else if (minb == 5) STG_SYM(5, 1);
+            else STG_SYM(4, 1);
 #undef STG_SYM
             STG_CUDA(cudaGetLastError());
             ++launches;
@@ -697,7 +701,7 @@ struct Runner {
             down(used.data(), d_used, R);
             bool any = false;
             for (int r = 0; r < R; ++r)
-                if (ovf[r]) {
+                if (ovf[r] || used[r] > (caps[r] >> 1)) {  // probe cap hit, or past the 50 % load limit
                     caps[r] = caps[r] >= (1u << 30) ? caps[r] : caps[r] * 4;
                     any = true;
                 }

@@ -612,6 +612,7 @@ struct AggParams {
     unsigned long long* stat;    // [0] prefix hits, [1] misses
     uint64_t n_samples;
     uint64_t n_frames;
+    int order;                   // 0: contiguous batch ranges per warp, 1: grid-stride
 };
 
 // atom.global.cas.b128 against an empty (0, 0) key: returns the previous key.
@@ -629,12 +630,16 @@ __device__ __forceinline__ void cas128(unsigned long long* addr, unsigned long l
 
 // Open addressing on the 128-bit key (hi, lo): one 16 B L2 read per probe; an
 // empty slot is claimed with a single 128-bit CAS (both halves at once, so no
-// reader ever sees a half-written key and no fence is needed); counts are
-// fire-and-forget reductions.  rep is read only after the kernel.
+// reader ever sees a half-written key and no fence is needed); counts and the
+// per-rank occupancy are fire-and-forget reductions (the host compares the
+// occupancy with the 50 % load limit after the kernel and retries larger); a
+// probe run longer than kMaxProbe also marks the table for a retry.  rep is
+// read only after the kernel.
+constexpr uint32_t kMaxProbe = 512;
 __device__ __forceinline__ void agg_insert(AggSlot* T, uint32_t mask, uint64_t fa, uint64_t fb, uint32_t rep,
                                            uint32_t cnt, unsigned* used, int* overflow) {
     uint32_t i = uint32_t(fb >> 20) & mask;
-    for (uint32_t probe = 0; probe <= mask; ++probe) {
+    for (uint32_t probe = 0; probe <= mask && probe < kMaxProbe; ++probe) {
         ulonglong2 cur = __ldcg(reinterpret_cast<const ulonglong2*>(T + i));  // (hi, lo) in one L2 read
         if ((cur.x | cur.y) == 0) {
             unsigned long long oa, ob;
@@ -642,7 +647,7 @@ __device__ __forceinline__ void agg_insert(AggSlot* T, uint32_t mask, uint64_t f
             if ((oa | ob) == 0) {
                 T[i].rep = rep;
                 atomicAdd(&T[i].count, cnt);
-                if (atomicAdd(used, 1u) + 1 > (mask + 1) / 2) *overflow = 1;
+                atomicAdd(used, 1u);
                 return;
             }
             cur.x = oa;
@@ -689,6 +694,16 @@ __device__ __forceinline__ void raw_block(const uint64_t (&pc)[8], uint64_t b01,
     mum_acc(pc[4] ^ B ^ 0x452821e638d01377ull, pc[5] ^ B ^ 0xbe5466cf34e90c6cull, ha, hb);
     mum_acc(pc[6] ^ B ^ 0xc0ac29b7c97c50ddull, pc[7] ^ B ^ 0x3f84d5b5b5470917ull, ha, hb);
     mum_acc(b01 ^ B ^ 0x9216d5d98979fb1bull, b23 ^ B ^ 0xd1310ba698dfb5acull, ha, hb);
+}
+
+// Half-block form (4 frames: one 256-bit pc load + 8 B of bins): two pc-pair
+// products and one bins product against an odd per-position key.
+__device__ __forceinline__ void raw_half(uint64_t p0, uint64_t p1, uint64_t p2, uint64_t p3, uint64_t bins,
+                                         uint64_t q, uint64_t& ha, uint64_t& hb) {
+    const uint64_t B = (q + 1) * 0x9e3779b97f4a7c15ull;
+    mum_acc(p0 ^ B ^ 0x243f6a8885a308d3ull, p1 ^ B ^ 0x13198a2e03707344ull, ha, hb);
+    mum_acc(p2 ^ B ^ 0xa4093822299f31d0ull, p3 ^ B ^ 0x082efa98ec4e6c89ull, ha, hb);
+    mum_acc(bins ^ B ^ 0x9216d5d98979fb1bull, (B ^ 0xd1310ba698dfb5acull) | 1ull, ha, hb);
 }
 
 // 256-bit read-only global load (sm_100: LDG.E.ENL2.256), 32-byte aligned.
@@ -765,7 +780,7 @@ __device__ __forceinline__ void pfx_put(PfxSlot* T, uint32_t mask, uint64_t ha, 
 //           open-addressing table with __match_any pre-aggregation;
 //  misses   the warp symbolizes the missing chains cooperatively and fills
 //           the cache.
-template <bool SMEM_TABS, int MINB, int PF>
+template <bool SMEM_TABS, int MINB, int UB>
 __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
     __shared__ DevTable s_tabs[kMaxSmemBins];
     if (SMEM_TABS) {
@@ -777,12 +792,15 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
     const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
     const uint64_t n_batches = (p.n_samples + 31) / 32;
-    unsigned long long hits = 0, misses = 0;
-    // each warp owns a contiguous range of batches, so its rank advances
-    // monotonically (one cached boundary compare per batch, no search)
+    unsigned hits = 0, misses = 0;  // lane 0's per-warp tallies (< 2^32 per warp)
+    // batch order: contiguous ranges per warp, or grid-stride (p.order = 1: at
+    // any moment the grid works on ~one rank, whose aggregation table stays in
+    // L2).  Either way a warp's rank only moves forward, so it advances by
+    // compares instead of a search per batch.
     const uint64_t per = (n_batches + nwarps - 1) / nwarps;
-    const uint64_t b_begin = warp * per;
-    const uint64_t b_end = b_begin + per < n_batches ? b_begin + per : n_batches;
+    const uint64_t b_begin = p.order ? warp : warp * per;
+    const uint64_t b_end = p.order ? n_batches : (b_begin + per < n_batches ? b_begin + per : n_batches);
+    const uint64_t b_step = p.order ? nwarps : 1;
     int r_cur = 0;
     if (b_begin < b_end) {
         const uint64_t q = b_begin * 32;
@@ -793,7 +811,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
         }
         r_cur = lo;
     }
-    for (uint64_t bt = b_begin; bt < b_end; ++bt) {
+    for (uint64_t bt = b_begin; bt < b_end; bt += b_step) {
         // ---------------- phase 0: lane s owns sample i; its stream loads are
         // issued before the rank-dependent ones resolve
         const uint64_t i = bt * 32 + lane;
@@ -825,35 +843,78 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
         // ---------------- phase 1: this lane's frames, 8 per step
         uint64_t leaf_pc = 0, ha = 0, hb = 0;
         uint32_t leaf_bin = 0;
-        if (inwin) {
-            const uint64_t a0 = f0 & ~7ull;
-            for (uint64_t bb = a0; bb < f1; bb += 8) {
-                uint64_t pcs[8];
-                uint4 bq;
-                load_block<PF>(p.pc, p.bin, p.n_frames, bb, pcs, bq);
-                if (!(bb > f0 && bb + 8 <= f1)) {  // boundary block: take the leaf, zero the rest
-                    uint32_t bw[4] = {bq.x, bq.y, bq.z, bq.w};
+        if (UB == 0 && inwin) {
+            // half blocks: 4 frames per step, fewest registers per lane
+            const uint64_t a0 = f0 & ~3ull;
+            for (uint64_t bb = a0; bb < f1; bb += 4) {
+                uint64_t x0, x1, x2, x3, bins;
+                if (bb + 4 <= p.n_frames) {
+                    ld256(p.pc + bb, x0, x1, x2, x3);
+                    bins = __ldg(reinterpret_cast<const unsigned long long*>(p.bin + bb));
+                } else {
+                    x0 = p.pc[bb];
+                    x1 = bb + 1 < p.n_frames ? p.pc[bb + 1] : 0;
+                    x2 = bb + 2 < p.n_frames ? p.pc[bb + 2] : 0;
+                    x3 = 0;
+                    bins = uint64_t(p.bin[bb]) | (bb + 1 < p.n_frames ? uint64_t(p.bin[bb + 1]) << 16 : 0) |
+                           (bb + 2 < p.n_frames ? uint64_t(p.bin[bb + 2]) << 32 : 0);
+                }
+                if (!(bb > f0 && bb + 4 <= f1)) {  // boundary: take the leaf, zero the rest
+                    uint64_t* xs[4] = {&x0, &x1, &x2, &x3};
 #pragma unroll
-                    for (int t = 0; t < 8; ++t) {
+                    for (int t = 0; t < 4; ++t) {
                         const uint64_t j = bb + t;
-                        const uint32_t bv = (bw[t >> 1] >> (16 * (t & 1))) & 0xffffu;
                         if (j == f0) {
-                            leaf_pc = pcs[t];
-                            leaf_bin = bv;
+                            leaf_pc = *xs[t];
+                            leaf_bin = uint32_t(bins >> (16 * t)) & 0xffffu;
                         }
                         if (!(j > f0 && j < f1)) {
-                            pcs[t] = 0;
-                            bw[t >> 1] &= ~(0xffffu << (16 * (t & 1)));
+                            *xs[t] = 0;
+                            bins &= ~(0xffffull << (16 * t));
                         }
                     }
-                    bq = make_uint4(bw[0], bw[1], bw[2], bw[3]);
                 }
-                raw_block(pcs, uint64_t(bq.x) | (uint64_t(bq.y) << 32), uint64_t(bq.z) | (uint64_t(bq.w) << 32),
-                          (bb - a0) >> 3, ha, hb);
+                raw_half(x0, x1, x2, x3, bins, (bb - a0) >> 2, ha, hb);
+            }
+        }
+        if (UB > 0 && inwin) {
+            const uint64_t a0 = f0 & ~7ull;
+            for (uint64_t bs = a0; bs < f1; bs += 8 * (UB > 0 ? UB : 1)) {
+                // UB blocks per step: all their loads are issued before any hashing
+                constexpr int NB = UB > 0 ? UB : 1;
+                uint64_t pcs[NB][8];
+                uint4 bq[NB];
+#pragma unroll
+                for (int u = 0; u < NB; ++u)
+                    if (u == 0 || bs + 8 * u < f1) load_block<0>(p.pc, p.bin, p.n_frames, bs + 8 * u, pcs[u], bq[u]);
+#pragma unroll
+                for (int u = 0; u < NB; ++u) {
+                    const uint64_t bb = bs + 8 * u;
+                    if (u > 0 && bb >= f1) break;
+                    if (!(bb > f0 && bb + 8 <= f1)) {  // boundary block: take the leaf, zero the rest
+                        uint32_t bw[4] = {bq[u].x, bq[u].y, bq[u].z, bq[u].w};
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) {
+                            const uint64_t j = bb + t;
+                            const uint32_t bv = (bw[t >> 1] >> (16 * (t & 1))) & 0xffffu;
+                            if (j == f0) {
+                                leaf_pc = pcs[u][t];
+                                leaf_bin = bv;
+                            }
+                            if (!(j > f0 && j < f1)) {
+                                pcs[u][t] = 0;
+                                bw[t >> 1] &= ~(0xffffu << (16 * (t & 1)));
+                            }
+                        }
+                        bq[u] = make_uint4(bw[0], bw[1], bw[2], bw[3]);
+                    }
+                    raw_block(pcs[u], uint64_t(bq[u].x) | (uint64_t(bq[u].y) << 32),
+                              uint64_t(bq[u].z) | (uint64_t(bq[u].w) << 32), (bb - a0) >> 3, ha, hb);
+                }
             }
         }
         const unsigned need = __ballot_sync(0xffffffffu, inwin && depth > 1);
-        const uint64_t shape = uint64_t(depth) | (uint64_t(f0 & 7) << 32);
+        const uint64_t shape = uint64_t(depth) | (uint64_t(f0 & (UB == 0 ? 3 : 7)) << 32);
         uint64_t my_ra = mix_a(ha ^ (shape * 0x8cb92ba72f3d8dd7ull));
         uint64_t my_rb = mix_b(hb + shape);
         if (my_ra == 0) my_ra = 1;
@@ -961,16 +1022,15 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
             const unsigned mr = __match_any_sync(0xffffffffu, r) & act;
             const unsigned m = __match_any_sync(0xffffffffu, inwin ? fa : 0ull) & mr;
             if (inwin && (__ffs(m) - 1) == lane) {
-                if (!*(volatile int*)(p.tab_overflow + r))
-                    agg_insert(p.slots + __ldg(p.tab_off + r), __ldg(p.tab_mask + r), fa, fb, uint32_t(i - rs),
+                agg_insert(p.slots + __ldg(p.tab_off + r), __ldg(p.tab_mask + r), fa, fb, uint32_t(i - rs),
                                __popc(m), p.tab_used + r, p.tab_overflow + r);
             }
             if (inwin && (__ffs(mr) - 1) == lane) atomicAdd(p.n_in + r, (unsigned long long)__popc(mr));
         }
     }
     if (lane == 0 && (hits | misses)) {
-        atomicAdd(p.stat, hits);
-        atomicAdd(p.stat + 1, misses);
+        atomicAdd(p.stat, (unsigned long long)hits);
+        atomicAdd(p.stat + 1, (unsigned long long)misses);
     }
 }
 
