@@ -247,6 +247,20 @@ def peaks():
         return {}
 
 
+def ncu_traffic(kernel, algo_bytes):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed
+    `ncu --set full` capture of this same workload (profiles/ncu_traffic.json,
+    written by tools/ncu_summary.py --traffic-json); None when the capture was
+    taken on a different workload size."""
+    try:
+        rec = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())[kernel]
+    except Exception:
+        return None
+    if int(rec.get("algorithmic_bytes", -1)) != int(algo_bytes):
+        return None
+    return rec["dram_bytes"]
+
+
 # ----------------------------------------------------------------------- c4
 def bench_c4(a, torch, stg, rank, local, world, dist):
     """C4: NCCL collective-event alignment, 1,024 ranks x 50k AllReduce/AllGather
@@ -610,7 +624,7 @@ def main():
     peak = pk.get("hbm_gbs", 6650.0)
     achieved = algo_bytes / (k_ms / 1e3) / 1e9
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": None, "kernel": "k_sym_agg",
+            "frac": round(achieved / peak, 4), "traffic": ncu_traffic("k_sym_agg", algo_bytes), "kernel": "k_sym_agg",
             "kernel_ms": round(k_ms, 3), "algorithmic_bytes": algo_bytes,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback 6.65 TB/s"}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,

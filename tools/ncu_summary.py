@@ -42,6 +42,9 @@ def main():
     ap.add_argument("--peak", type=float, default=6552.3)
     ap.add_argument("--title", default="")
     ap.add_argument("--command", default="")
+    ap.add_argument("--traffic-json", default="", help="record DRAM bytes/launch under this kernel key "
+                    "in profiles/ncu_traffic.json (read by bench.py's roofline.traffic)")
+    ap.add_argument("--source", default="", help="the profiles/ summary the traffic number comes from")
     a = ap.parse_args()
     print(f"# {a.title}\n")
     if a.command:
@@ -70,6 +73,14 @@ def main():
                     scale = {"GB": 1e9, "MB": 1e6, "KB": 1e3, "byte": 1, "Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3}
                     tr = float(rd.replace(",", "")) * scale.get(ru.strip(), 1) + float(wr.replace(",", "")) * scale.get(wu.strip(), 1)
                     print(f"DRAM traffic {tr / 1e9:.2f} GB = {tr / a.algo_bytes:.2f}x the algorithmic bytes.")
+                    if a.traffic_json:
+                        import json
+                        from pathlib import Path
+                        tj = Path(__file__).resolve().parent.parent / "profiles" / "ncu_traffic.json"
+                        d = json.loads(tj.read_text()) if tj.exists() else {}
+                        d[a.traffic_json] = {"dram_bytes": int(tr), "algorithmic_bytes": int(a.algo_bytes),
+                                             "ncu_ms": round(t * 1e3, 3), "source": a.source}
+                        tj.write_text(json.dumps(d, indent=1) + "\n")
             print()
     if a.launches:
         rows = list(csv.reader(open(a.launches)))
