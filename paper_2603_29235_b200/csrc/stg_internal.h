@@ -144,6 +144,7 @@ struct Bundle;  // bundle.h
 struct Ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;  // independent side stages overlapped with k_sym_agg
     std::mutex mu;
     std::vector<std::unique_ptr<HostTable>> tables;
     std::map<std::string, size_t> table_by_id;  // raw 20-byte id -> index

@@ -83,13 +83,36 @@ struct Runner {
     std::vector<uint64_t> h_n_in;
     std::vector<uint32_t> h_dense_final;
     cudaEvent_t ev[8];
+    cudaEvent_t ev_pre = nullptr;  // the main stream just before k_sym_agg
+    bool gpu_os_done = false;
 
     Runner(Ctx& c_, const stg_window& w_, const stg_config& cfg_, Result& r_)
         : c(c_), w(w_), cfg(cfg_), res(r_), st(c_.stream) {
         for (auto& e : ev) STG_CUDA(cudaEventCreate(&e));
+        STG_CUDA(cudaEventCreateWithFlags(&ev_pre, cudaEventDisableTiming));
     }
     ~Runner() {
         for (auto& e : ev) cudaEventDestroy(e);
+        cudaEventDestroy(ev_pre);
+    }
+    // The GPU/OS layer sums (build_group_data bundle.cpp:302-320) do not depend on
+    // the sample stream: they run on a side stream (ordered after everything the
+    // main stream did before k_sym_agg) while k_sym_agg streams, and their host
+    // downloads synchronise only the side stream.
+    void side_gpu_os() {
+        if (gpu_os_done) return;
+        if (!c.side) STG_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+        STG_CUDA(cudaStreamWaitEvent(c.side, ev_pre, 0));
+        cudaStream_t keep = st;
+        st = c.side;
+        try {
+            gpu_os();
+        } catch (...) {
+            st = keep;
+            throw;
+        }
+        st = keep;
+        gpu_os_done = true;
     }
 
     template <class T>
@@ -674,30 +697,21 @@ struct Runner {
             if (need < grid) grid = unsigned(std::max<uint64_t>(need, 1));
             cudaEventRecord(ev[2], st);
             const bool smem_tabs = w.n_bins <= kMaxSmemBins;
-            // STG_SYM_MINB / STG_SYM_UB (experiments): resident CTAs per SM the register
-            // budget targets, and the frame blocks each lane has in flight per step
+            // STG_SYM_MINB (experiments): 3 resident CTAs per SM (80 registers) instead of 4
             static const int minb = std::getenv("STG_SYM_MINB") ? std::atoi(std::getenv("STG_SYM_MINB")) : 4;
-            static const int ubv = std::getenv("STG_SYM_UB") ? std::atoi(std::getenv("STG_SYM_UB")) : 1;
             grid = unsigned(dev_sms) * unsigned(minb) * 4;
             if (need < grid) grid = unsigned(std::max<uint64_t>(need, 1));
-#define STG_SYM(MB, UB) k_sym_agg<true, MB, UB><<<grid, kThreads, 0, st>>>(p)
+            if (attempt == 0) cudaEventRecord(ev_pre, st);
             if (!smem_tabs) k_sym_agg<false, 4, 1><<<grid, kThreads, 0, st>>>(p);
-            else if (minb == 3 && ubv == 2) STG_SYM(3, 2);
-            else if (minb == 2 && ubv == 4) STG_SYM(2, 4);
-            else if (minb == 2 && ubv == 2) STG_SYM(2, 2);
-            else if (minb == 1 && ubv == 8) STG_SYM(1, 8);
-            else if (minb == 3) STG_SYM(3, 1);
-            else if (minb == 5 && ubv == 0) STG_SYM(5, 0);
-            else if (minb == 6 && ubv == 0) STG_SYM(6, 0);
-            else if (minb == 4 && ubv == 0) STG_SYM(4, 0);
-            else if (minb == 5) STG_SYM(5, 1);
-            else STG_SYM(4, 1);
-#undef STG_SYM
+            else if (minb == 3) k_sym_agg<true, 3, 1><<<grid, kThreads, 0, st>>>(p);
+            else k_sym_agg<true, 4, 1><<<grid, kThreads, 0, st>>>(p);
             STG_CUDA(cudaGetLastError());
             ++launches;
             cudaEventRecord(ev[3], st);
+            if (attempt == 0) side_gpu_os();  // host + side-stream work while the kernel streams
             res.agg_attempts = attempt + 1;
             down(ovf.data(), d_ovf, R);
+            mark("s:k_sym_agg");
             down(used.data(), d_used, R);
             bool any = false;
             for (int r = 0; r < R; ++r)
@@ -754,6 +768,7 @@ struct Runner {
                 res.cpu_totals.push_back(h_n_in[r]);
             }
         d_totals = up<uint64_t>("totals", h_n_in.data(), R);
+        mark("s:validate");
         fold(slots, tab_off, caps, unk, unk_cap, d_rsoff, foff, pc, bin, d_tabs);
     }
 
@@ -777,6 +792,10 @@ struct Runner {
         return m[&c];
     }
     uint32_t& c_unk_last() {
+        static std::map<Ctx*, uint32_t> m;
+        return m[&c];
+    }
+    uint32_t& c_gid_last() {
         static std::map<Ctx*, uint32_t> m;
         return m[&c];
     }
@@ -856,28 +875,33 @@ struct Runner {
         ++launches;
         L = get1(nl);
         res.n_lines = L;
+        mark("f:compact");
         if (L == 0) return;
-        // global dedupe -> sequence ids
-        uint64_t scap = next_pow2(2 * L);
-        SeqSlot* sslots = dev<SeqSlot>("sslots", scap);
-        zero(sslots, scap * sizeof(SeqSlot));
-        STG_CUDA(cudaMemsetAsync(sslots, 0, scap * sizeof(SeqSlot), st));
-        // gid field must start at 0xffffffff
-        {
-            std::vector<SeqSlot> tmp;  // set gid via a memset pattern pass
-        }
-        LAUNCH(k_fill_gid, grid_for(scap), kThreads, sslots, scap);
+        // global dedupe -> sequence ids.  The table is sized from the previous
+        // window's distinct count (lines repeat the same stacks across ranks), with a
+        // retry at 2 slots per line if it fills up.
         unsigned* nseq = dev<unsigned>("nseq", 1);
         int* sovf = dev<int>("sovf", 1);
-        zero(nseq, 4);
-        zero(sovf, 4);
         uint32_t* l_gid = dev<uint32_t>("l_gid", L);
         uint64_t* seq_rep = dev<uint64_t>("seq_rep", L);
-        LAUNCH(k_seq_dedupe, grid_for(L), kThreads, L, l_hi, l_lo, l_rep, sslots, scap - 1, nseq, l_gid, seq_rep,
-               sovf);
-        uint32_t G = get1(nseq);
+        const uint64_t scap_full = next_pow2(2 * L);
+        uint64_t scap = std::min<uint64_t>(scap_full, next_pow2(std::max<uint64_t>(4 * uint64_t(c_gid_last()) + 1024, 1u << 16)));
+        uint32_t G = 0;
+        for (;;) {
+            SeqSlot* sslots = dev<SeqSlot>("sslots", scap);
+            LAUNCH(k_fill_gid, grid_for(scap), kThreads, sslots, scap);  // clears the slots, gid = unpublished
+            zero(nseq, 4);
+            zero(sovf, 4);
+            LAUNCH(k_seq_dedupe, grid_for(L), kThreads, L, l_hi, l_lo, l_rep, sslots, scap - 1, nseq, l_gid, seq_rep,
+                   sovf);
+            G = get1(nseq);
+            if (!get1(sovf)) break;
+            if (scap >= scap_full) fail(STG_ENOMEM, "sequence table overflow");
+            scap = scap_full;
+        }
+        c_gid_last() = G;
         res.n_gid = G;
-        if (get1(sovf)) fail(STG_ENOMEM, "sequence table overflow");
+        mark("f:dedupe");
         // materialize
         uint64_t* seq_len = dev<uint64_t>("seq_len", G + 1);
         LAUNCH(k_seq_len64, grid_for(G), kThreads, G, seq_rep, foff, seq_len);
@@ -907,6 +931,7 @@ struct Runner {
         down(hb.data(), u_bin, NU);
         down(hp.data(), u_pc, NU);
         merge_labels(NU, hs, hb, hp, unk_cap);
+        mark("f:labels");
         LAUNCH(k_remap, grid_for(A), kThreads, A, d_arena, static_cast<const uint32_t*>(c.buf("u_final").p),
                static_cast<const uint32_t*>(c.buf("u_pos").p), uint32_t(n_pos));
         uint64_t NF = c.dict.size() + res.unk_labels.size();
@@ -926,6 +951,7 @@ struct Runner {
             incl_sum(flg, scn, G);
             S = get1(scn + G - 1);
             res.n_seq = S;
+            mark("f:seqsort");
             uint32_t* seq_rank = dev<uint32_t>("seq_rank", G);
             d_dense_rep = dev<uint32_t>("dense_rep", S);
             LAUNCH(k_seq_rankset, grid_for(G), kThreads, G, gids, scn, seq_rank, d_dense_rep);
@@ -952,6 +978,7 @@ struct Runner {
         }
         d_line_off = dev<uint64_t>("line_off", R + 1);
         LAUNCH(k_line_bounds, grid_for(R + 1), kThreads, R, d_lkey, L, d_line_off);
+        mark("f:linesort");
         cudaEventRecord(ev[5], st);
         // ---- stage c: distinct names per sequence, used-name space, inclusive counts
         uint64_t* dcnt = dev<uint64_t>("dn_cnt", S + 1);
@@ -973,6 +1000,7 @@ struct Runner {
         excl_sum(used, used_scan, NF + 1);
         F = get1(used_scan + NF);
         res.f_used = F;
+        mark("f:names");
         d_dense_final = dev<uint32_t>("dense_final", F);
         LAUNCH(k_dense_final, grid_for(NF), kThreads, NF, used, used_scan, d_dense_final);
         LAUNCH(k_dense_names, grid_for(ND), kThreads, ND, d_dn, used_scan);
@@ -1590,6 +1618,7 @@ struct Runner {
                 down(lo2, d_line_off + iq, 2);
                 auto both = exact_fractions2(lo[0], lo[1] - lo[0], h_n_in[is], lo2[0], lo2[1] - lo2[0], h_n_in[iq],
                                              false);
+                mark("d:fracs2");
                 const auto& fs_ = both[0];
                 const auto& fr_ = both[1];
                 size_t j = 0;
@@ -1606,6 +1635,7 @@ struct Runner {
                 if (concluded == STG_VERDICT_INCONCLUSIVE && !cands.empty()) {
                     concluded = STG_VERDICT_CPU_INTERFERENCE;
                     rep.top_path = hottest(lo[0], lo[1], cands.front().f, false);
+                    mark("d:hottest");
                 }
             } else {
                 rep.notes.push_back("cpu profiles missing; cpu layer skipped");
@@ -1827,9 +1857,8 @@ struct Runner {
         collectives();
         cudaEventRecord(ev[1], st);
         mark("collectives");
-        gpu_os();
-        mark("gpu_os");
-        samples();
+        samples();  // runs gpu_os() on the side stream while k_sym_agg streams
+        if (!gpu_os_done) gpu_os();
         mark("samples+fold");
         if (ev_unset_fold()) {
             cudaEventRecord(ev[2], st);

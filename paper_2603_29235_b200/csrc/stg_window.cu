@@ -39,6 +39,7 @@ Ctx::~Ctx() {
         }
         if (u.stream) cudaStreamDestroy(u.stream);
     }
+    if (side) cudaStreamDestroy(side);
     if (stream) cudaStreamDestroy(stream);
 }
 
@@ -696,16 +697,6 @@ __device__ __forceinline__ void raw_block(const uint64_t (&pc)[8], uint64_t b01,
     mum_acc(b01 ^ B ^ 0x9216d5d98979fb1bull, b23 ^ B ^ 0xd1310ba698dfb5acull, ha, hb);
 }
 
-// Half-block form (4 frames: one 256-bit pc load + 8 B of bins): two pc-pair
-// products and one bins product against an odd per-position key.
-__device__ __forceinline__ void raw_half(uint64_t p0, uint64_t p1, uint64_t p2, uint64_t p3, uint64_t bins,
-                                         uint64_t q, uint64_t& ha, uint64_t& hb) {
-    const uint64_t B = (q + 1) * 0x9e3779b97f4a7c15ull;
-    mum_acc(p0 ^ B ^ 0x243f6a8885a308d3ull, p1 ^ B ^ 0x13198a2e03707344ull, ha, hb);
-    mum_acc(p2 ^ B ^ 0xa4093822299f31d0ull, p3 ^ B ^ 0x082efa98ec4e6c89ull, ha, hb);
-    mum_acc(bins ^ B ^ 0x9216d5d98979fb1bull, (B ^ 0xd1310ba698dfb5acull) | 1ull, ha, hb);
-}
-
 // 256-bit read-only global load (sm_100: LDG.E.ENL2.256), 32-byte aligned.
 __device__ __forceinline__ void ld256(const uint64_t* p, uint64_t& a, uint64_t& b, uint64_t& c, uint64_t& d) {
     asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0, %1, %2, %3}, [%4];"
@@ -843,45 +834,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
         // ---------------- phase 1: this lane's frames, 8 per step
         uint64_t leaf_pc = 0, ha = 0, hb = 0;
         uint32_t leaf_bin = 0;
-        if (UB == 0 && inwin) {
-            // half blocks: 4 frames per step, fewest registers per lane
-            const uint64_t a0 = f0 & ~3ull;
-            for (uint64_t bb = a0; bb < f1; bb += 4) {
-                uint64_t x0, x1, x2, x3, bins;
-                if (bb + 4 <= p.n_frames) {
-                    ld256(p.pc + bb, x0, x1, x2, x3);
-                    bins = __ldg(reinterpret_cast<const unsigned long long*>(p.bin + bb));
-                } else {
-                    x0 = p.pc[bb];
-                    x1 = bb + 1 < p.n_frames ? p.pc[bb + 1] : 0;
-                    x2 = bb + 2 < p.n_frames ? p.pc[bb + 2] : 0;
-                    x3 = 0;
-                    bins = uint64_t(p.bin[bb]) | (bb + 1 < p.n_frames ? uint64_t(p.bin[bb + 1]) << 16 : 0) |
-                           (bb + 2 < p.n_frames ? uint64_t(p.bin[bb + 2]) << 32 : 0);
-                }
-                if (!(bb > f0 && bb + 4 <= f1)) {  // boundary: take the leaf, zero the rest
-                    uint64_t* xs[4] = {&x0, &x1, &x2, &x3};
-#pragma unroll
-                    for (int t = 0; t < 4; ++t) {
-                        const uint64_t j = bb + t;
-                        if (j == f0) {
-                            leaf_pc = *xs[t];
-                            leaf_bin = uint32_t(bins >> (16 * t)) & 0xffffu;
-                        }
-                        if (!(j > f0 && j < f1)) {
-                            *xs[t] = 0;
-                            bins &= ~(0xffffull << (16 * t));
-                        }
-                    }
-                }
-                raw_half(x0, x1, x2, x3, bins, (bb - a0) >> 2, ha, hb);
-            }
-        }
-        if (UB > 0 && inwin) {
+        if (inwin) {
             const uint64_t a0 = f0 & ~7ull;
-            for (uint64_t bs = a0; bs < f1; bs += 8 * (UB > 0 ? UB : 1)) {
+            for (uint64_t bs = a0; bs < f1; bs += 8 * UB) {
                 // UB blocks per step: all their loads are issued before any hashing
-                constexpr int NB = UB > 0 ? UB : 1;
+                constexpr int NB = UB;
                 uint64_t pcs[NB][8];
                 uint4 bq[NB];
 #pragma unroll
@@ -914,7 +871,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
             }
         }
         const unsigned need = __ballot_sync(0xffffffffu, inwin && depth > 1);
-        const uint64_t shape = uint64_t(depth) | (uint64_t(f0 & (UB == 0 ? 3 : 7)) << 32);
+        const uint64_t shape = uint64_t(depth) | (uint64_t(f0 & 7) << 32);
         uint64_t my_ra = mix_a(ha ^ (shape * 0x8cb92ba72f3d8dd7ull));
         uint64_t my_rb = mix_b(hb + shape);
         if (my_ra == 0) my_ra = 1;
@@ -1173,9 +1130,10 @@ __global__ void k_remap(uint64_t n, uint32_t* arena, const uint32_t* unk_final, 
         arena[i] = remap_key(arena[i], unk_final, pos_sorted, n_pos);
 }
 
-__global__ void k_fill_gid(SeqSlot* s, uint64_t n) {
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
-        s[i].gid = 0xffffffffu;
+__global__ void k_fill_gid(SeqSlot* s, uint64_t n) {  // empty slot: key 0, gid unpublished
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        reinterpret_cast<ulonglong4*>(s)[i] = make_ulonglong4(0ull, 0ull, 0xffffffffull, 0ull);
+    }
 }
 __global__ void k_seq_len64(uint32_t G, const uint64_t* seq_rep, const uint64_t* foff, uint64_t* len) {
     for (uint64_t g = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; g < G; g += uint64_t(gridDim.x) * blockDim.x) {
