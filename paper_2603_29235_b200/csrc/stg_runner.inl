@@ -83,17 +83,26 @@ struct Runner {
     std::vector<uint64_t> h_n_in;
     std::vector<uint32_t> h_dense_final;
     cudaEvent_t ev[8];
-    cudaEvent_t ev_pre = nullptr;  // the main stream just before k_sym_agg
+    cudaEvent_t ev_pre = nullptr;   // main-stream point a side-stream stage starts after
+    cudaEvent_t ev_incl = nullptr;  // inclusive counts done (side stream)
     bool gpu_os_done = false;
+    bool incl_pending = false;
+    void wait_incl() {
+        if (!incl_pending) return;
+        STG_CUDA(cudaStreamWaitEvent(st, ev_incl, 0));
+        incl_pending = false;
+    }
 
     Runner(Ctx& c_, const stg_window& w_, const stg_config& cfg_, Result& r_)
         : c(c_), w(w_), cfg(cfg_), res(r_), st(c_.stream) {
         for (auto& e : ev) STG_CUDA(cudaEventCreate(&e));
         STG_CUDA(cudaEventCreateWithFlags(&ev_pre, cudaEventDisableTiming));
+        STG_CUDA(cudaEventCreateWithFlags(&ev_incl, cudaEventDisableTiming));
     }
     ~Runner() {
         for (auto& e : ev) cudaEventDestroy(e);
         cudaEventDestroy(ev_pre);
+        cudaEventDestroy(ev_incl);
     }
     // The GPU/OS layer sums (build_group_data bundle.cpp:302-320) do not depend on
     // the sample stream: they run on a side stream (ordered after everything the
@@ -1007,16 +1016,29 @@ struct Runner {
         uint64_t cells = uint64_t(R) * F;
         if (cells > (1ull << 31)) fail(STG_ENOMEM, "rank x name matrix too large");
         d_incl = dev<unsigned long long>("incl", cells);
-        if (F * sizeof(unsigned) <= 160 * 1024) {
-            const size_t sm = F * sizeof(unsigned);
-            if (sm > 48 * 1024)
-                STG_CUDA(cudaFuncSetAttribute(k_incl_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-            k_incl_smem<<<R, 1024, sm, st>>>(R, d_line_off, d_lkey, d_lcount, d_dn_off, d_dn, F, d_incl);
+        // The rank x name inclusive counts feed only the waterline: they run on the
+        // side stream, overlapped with the straggler/reference fractions and the
+        // decision ladder; waterline() (and the end of the run) wait for them.
+        if (!c.side) STG_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+        cudaEventRecord(ev_pre, st);
+        STG_CUDA(cudaStreamWaitEvent(c.side, ev_pre, 0));
+        {
+            cudaStream_t keep = st;
+            st = c.side;
+            if (F * sizeof(unsigned) <= 160 * 1024) {
+                const size_t sm = F * sizeof(unsigned);
+                if (sm > 48 * 1024)
+                    STG_CUDA(cudaFuncSetAttribute(k_incl_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+                k_incl_smem<<<R, 1024, sm, st>>>(R, d_line_off, d_lkey, d_lcount, d_dn_off, d_dn, F, d_incl);
+                ++launches;
+            } else {
+                zero(d_incl, cells * 8);
+                LAUNCH(k_incl, grid_for(L * 32), kThreads, L, d_lkey, d_lcount, d_dn_off, d_dn, F, d_incl);
+            }
+            st = keep;
             STG_CUDA(cudaGetLastError());
-            ++launches;
-        } else {
-            zero(d_incl, cells * 8);
-            LAUNCH(k_incl, grid_for(L * 32), kThreads, L, d_lkey, d_lcount, d_dn_off, d_dn, F, d_incl);
+            STG_CUDA(cudaEventRecord(ev_incl, c.side));
+            incl_pending = true;
         }
         cudaEventRecord(ev[6], st);
     }
@@ -1800,6 +1822,7 @@ struct Runner {
     }
 
     void waterline() {
+        wait_incl();
         res.wl_dist = false;
         if (dist()) return waterline_dist();
         res.waterline_done = true;
@@ -1872,6 +1895,7 @@ struct Runner {
         res.waterline_done = false;
         if (cfg.want_waterline) waterline();
         mark("waterline");
+        wait_incl();
         cudaEventRecord(ev[7], st);
         STG_CUDA(cudaStreamSynchronize(st));
         stg_run_stats& s = res.stats;

@@ -1019,18 +1019,41 @@ __global__ void k_regress_exact(int n, const int* ranks, const uint64_t* rank_so
 __global__ void k_compact_lines(int R, const uint64_t* tab_off, const uint32_t* tab_mask, const AggSlot* slots,
                                 const uint64_t* rank_soff, uint32_t* l_rank, uint64_t* l_hi, uint64_t* l_lo,
                                 uint32_t* l_count, uint64_t* l_rep, unsigned long long* n_out) {
-    int r = blockIdx.y;
-    uint32_t cap = tab_mask[r] + 1;
+    // one output reservation per block (block-wide ballot counts), not per line
+    __shared__ unsigned warp_n[kThreads / 32];
+    __shared__ unsigned long long base;
+    const int r = blockIdx.y;
+    const uint32_t cap = tab_mask[r] + 1;
     const AggSlot* T = slots + tab_off[r];
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += gridDim.x * blockDim.x) {
-        AggSlot s = T[i];
-        if (s.hi == 0) continue;
-        unsigned long long o = atomicAdd(n_out, 1ull);
-        l_rank[o] = uint32_t(r);
-        l_hi[o] = s.hi;
-        l_lo[o] = s.lo;
-        l_count[o] = s.count;
-        l_rep[o] = rank_soff[r] + s.rep;
+    const uint64_t soff = rank_soff[r];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (uint32_t i0 = blockIdx.x * blockDim.x; i0 < cap; i0 += gridDim.x * blockDim.x) {
+        const uint32_t i = i0 + threadIdx.x;
+        AggSlot s{};
+        if (i < cap) s = T[i];
+        const bool live = s.hi != 0;
+        const unsigned m = __ballot_sync(0xffffffffu, live);
+        if (lane == 0) warp_n[wid] = __popc(m);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned tot = 0;
+            for (int w = 0; w < kThreads / 32; ++w) {
+                const unsigned c = warp_n[w];
+                warp_n[w] = tot;
+                tot += c;
+            }
+            base = tot ? atomicAdd(n_out, (unsigned long long)tot) : 0;
+        }
+        __syncthreads();
+        if (live) {
+            const unsigned long long o = base + warp_n[wid] + __popc(m & ((1u << lane) - 1));
+            l_rank[o] = uint32_t(r);
+            l_hi[o] = s.hi;
+            l_lo[o] = s.lo;
+            l_count[o] = s.count;
+            l_rep[o] = soff + s.rep;
+        }
+        __syncthreads();
     }
 }
 
