@@ -146,3 +146,31 @@ def test_c5_4096_ranks_against_baseline(ctx, scenario, verdict):
     _, rep = _check_window(ctx, win, against_ref=True)
     if verdict:
         assert rep["verdict"] == verdict and len(rep["flagged_ranks"]) == 4096
+
+
+def test_table_hints_grow_across_windows():
+    """Tables sized from the previous window's counts (rank aggregation tables,
+    sequence dedupe, prefix cache, unknown labels) must grow by retry when a later
+    window needs more: a small window first, then one with 40x the distinct stacks,
+    on a fresh context.  Both stay bit-exact against the oracle."""
+    import paper_2603_29235_b200 as stg
+    c = stg.Context(0)
+    try:
+        small = small_window(seed=21, ranks=4, samples_per_rank=300, slow_rank=1, pool=10)
+        _check_window(c, small)
+        big = small_window(seed=22, ranks=12, samples_per_rank=3000, slow_rank=5, pool=400, unknown_frac=0.05)
+        stats, _ = _check_window(c, big)
+        assert stats["agg_attempts"] > 1, "the aggregation tables should have grown by retry"
+        # and shrinking back is exact too (tables larger than needed)
+        _check_window(c, small_window(seed=23, ranks=4, samples_per_rank=300, slow_rank=2, pool=10))
+    finally:
+        c.close()
+
+
+@pytest.mark.parametrize("depth", [3, 40, 70])
+def test_stack_depths_and_alignments(ctx, depth):
+    """Frame blocks of 8 are read at absolute alignment: stacks shorter than a block,
+    spanning several blocks, and every f0 mod 8 (depths vary per sample) must all
+    fold exactly."""
+    win = small_window(seed=30 + depth, ranks=6, samples_per_rank=700, slow_rank=2, depth=depth, pool=150)
+    _check_window(ctx, win)
