@@ -945,25 +945,66 @@ struct Runner {
                static_cast<const uint32_t*>(c.buf("u_pos").p), uint32_t(n_pos));
         uint64_t NF = c.dict.size() + res.unk_labels.size();
         res.n_names = NF;
-        // lexicographic sort of the sequences
-        uint32_t* gids = dev<uint32_t>("gids", G);
-        LAUNCH(k_iota, grid_for(G), kThreads, gids, G);
+        // lexicographic order of the sequences
+        uint32_t* seq_rank = dev<uint32_t>("seq_rank", G);
         {
-            SeqLess less{d_arena, d_seq_off};
-            size_t tb = 0;
-            STG_CUDA(cub::DeviceMergeSort::SortKeys(nullptr, tb, gids, int64_t(G), less, st));
-            STG_CUDA(cub::DeviceMergeSort::SortKeys(temp(tb), tb, gids, int64_t(G), less, st));
-            ++launches;
-            uint32_t* flg = dev<uint32_t>("sq_flag", G);
-            uint32_t* scn = dev<uint32_t>("sq_scan", G);
-            LAUNCH(k_seq_rankflags, grid_for(G), kThreads, G, gids, less, flg);
-            incl_sum(flg, scn, G);
-            S = get1(scn + G - 1);
-            res.n_seq = S;
+            uint64_t maxlen = 0;
+            {
+                uint64_t* mx = dev<uint64_t>("pd_max", 1);
+                size_t tb = 0;
+                STG_CUDA(cub::DeviceReduce::Max(nullptr, tb, seq_len, mx, int64_t(G), st));
+                STG_CUDA(cub::DeviceReduce::Max(temp(tb), tb, seq_len, mx, int64_t(G), st));
+                ++launches;
+                maxlen = get1(mx);
+            }
+            int p_log = 1;
+            while ((uint64_t(1) << p_log) < maxlen) ++p_log;
+            const uint64_t n0 = uint64_t(G) << p_log;
+            if (n0 <= (1ull << 27)) {
+                // prefix doubling (k_pd_*): log2(P) radix sorts of shrinking pair-key arrays
+                uint32_t* cur = dev<uint32_t>("pd_cur", n0);
+                LAUNCH(k_pd_init, grid_for(n0), kThreads, n0, uint32_t(p_log), d_seq_off, d_arena, cur);
+                uint64_t* key = dev<uint64_t>("pd_key", n0 / 2);
+                uint64_t* key_s = dev<uint64_t>("pd_key_s", n0 / 2);
+                uint32_t* idx = dev<uint32_t>("pd_idx", n0 / 2);
+                uint32_t* idx_s = dev<uint32_t>("pd_idx_s", n0 / 2);
+                uint32_t* flg = dev<uint32_t>("pd_flag", n0 / 2);
+                uint32_t* rnk = dev<uint32_t>("pd_rank", n0 / 2);
+                uint64_t n = n0;
+                uint64_t vmax = NF + 1;  // level-0 values: name + 1, sentinel 0
+                for (int lvl = 1; lvl <= p_log; ++lvl) {
+                    n /= 2;
+                    int vb = 1;
+                    while ((uint64_t(1) << vb) <= vmax) ++vb;
+                    LAUNCH(k_pd_pairs, grid_for(n), kThreads, n, cur, key, idx);
+                    sort_pairs(key, key_s, idx, idx_s, n, 32 + vb);
+                    LAUNCH(k_pd_flags, grid_for(n), kThreads, n, key_s, flg);
+                    incl_sum(flg, rnk, n);
+                    LAUNCH(k_pd_scatter, grid_for(n), kThreads, n, idx_s, rnk, cur);
+                    vmax = n;  // dense ranks 1..(distinct blocks) <= n
+                }
+                S = get1(rnk + (G - 1));
+                res.n_seq = S;
+                d_dense_rep = dev<uint32_t>("dense_rep", S);
+                LAUNCH(k_pd_final, grid_for(G), kThreads, G, cur, seq_rank, d_dense_rep);
+            } else {  // very deep stacks: comparator merge sort
+                uint32_t* gids = dev<uint32_t>("gids", G);
+                LAUNCH(k_iota, grid_for(G), kThreads, gids, G);
+                SeqLess less{d_arena, d_seq_off};
+                size_t tb = 0;
+                STG_CUDA(cub::DeviceMergeSort::SortKeys(nullptr, tb, gids, int64_t(G), less, st));
+                STG_CUDA(cub::DeviceMergeSort::SortKeys(temp(tb), tb, gids, int64_t(G), less, st));
+                ++launches;
+                uint32_t* fl = dev<uint32_t>("sq_flag", G);
+                uint32_t* scn = dev<uint32_t>("sq_scan", G);
+                LAUNCH(k_seq_rankflags, grid_for(G), kThreads, G, gids, less, fl);
+                incl_sum(fl, scn, G);
+                S = get1(scn + G - 1);
+                res.n_seq = S;
+                d_dense_rep = dev<uint32_t>("dense_rep", S);
+                LAUNCH(k_seq_rankset, grid_for(G), kThreads, G, gids, scn, seq_rank, d_dense_rep);
+            }
             mark("f:seqsort");
-            uint32_t* seq_rank = dev<uint32_t>("seq_rank", G);
-            d_dense_rep = dev<uint32_t>("dense_rep", S);
-            LAUNCH(k_seq_rankset, grid_for(G), kThreads, G, gids, scn, seq_rank, d_dense_rep);
             uint64_t* lkey = dev<uint64_t>("lkey", L);
             LAUNCH(k_line_keys, grid_for(L), kThreads, L, l_rank, l_gid, seq_rank, lkey);
             d_lkey = dev<uint64_t>("lkey_s", L);

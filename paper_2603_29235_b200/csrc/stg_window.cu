@@ -1227,6 +1227,43 @@ __global__ void k_seq_rankset(uint32_t G, const uint32_t* sorted, const uint32_t
     }
 }
 
+// Sequence order by prefix doubling over aligned blocks: every sequence is
+// padded to P = 2^m names with a sentinel (0) below every name (name + 1), so
+// comparing padded sequences is exactly the std::map<std::vector<std::string>>
+// order (shorter prefix first, folded.cpp:18).  Level k ranks each aligned block
+// of 2^k names among all such blocks by the pair of its halves' level-(k-1)
+// ranks (a radix sort of 64-bit pair keys); at level m a block is a whole
+// sequence, so its rank is the sequence's dense position.
+__global__ void k_pd_init(uint64_t n, uint32_t p_log, const uint64_t* off, const uint32_t* arena, uint32_t* cur) {
+    for (uint64_t x = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; x < n; x += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t g = x >> p_log, j = x & ((1ull << p_log) - 1);
+        const uint64_t o = off[g], len = off[g + 1] - o;
+        cur[x] = j < len ? arena[o + j] + 1u : 0u;
+    }
+}
+__global__ void k_pd_pairs(uint64_t n, const uint32_t* cur, uint64_t* key, uint32_t* idx) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint2 v = reinterpret_cast<const uint2*>(cur)[i];
+        key[i] = (uint64_t(v.x) << 32) | v.y;
+        idx[i] = uint32_t(i);
+    }
+}
+__global__ void k_pd_flags(uint64_t n, const uint64_t* ks, uint32_t* flag) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        flag[i] = (i == 0 || ks[i] != ks[i - 1]) ? 1u : 0u;
+}
+__global__ void k_pd_scatter(uint64_t n, const uint32_t* idx_s, const uint32_t* rank, uint32_t* cur) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        cur[idx_s[i]] = rank[i];
+}
+__global__ void k_pd_final(uint32_t G, const uint32_t* cur, uint32_t* seq_rank, uint32_t* dense_rep) {
+    for (uint64_t g = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; g < G; g += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t d = cur[g] - 1;  // ranks are 1-based
+        seq_rank[g] = d;
+        dense_rep[d] = uint32_t(g);     // any member: equal ranks are equal name sequences
+    }
+}
+
 __global__ void k_line_keys(uint64_t L, const uint32_t* l_rank, const uint32_t* l_gid, const uint32_t* seq_rank,
                             uint64_t* lkey) {
     for (uint64_t l = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; l < L; l += uint64_t(gridDim.x) * blockDim.x)
