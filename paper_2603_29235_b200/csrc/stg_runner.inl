@@ -457,7 +457,7 @@ struct Runner {
             double* zm = dev<double>("s_zm", span);
             uint64_t* fl = dev<uint64_t>("s_fl", span);
             uint8_t* hz = dev<uint8_t>("s_hz", span);
-            LAUNCH(k_straggler_rank, grid_for(uint64_t(span) * 32), kThreads, n_w, span, d_lat, cfg.k, mu, sg, m, pres,
+            LAUNCH(k_straggler_rank, grid_for(uint64_t(span) * 32, kStragWarps * 32), kStragWarps * 32, n_w, span, d_lat, cfg.k, mu, sg, m, pres,
                    ma, ml, zm, fl, hz);
             down(res.lat_present.data(), pres, span);
             down(res.mean_lat_all.data(), ma, span);

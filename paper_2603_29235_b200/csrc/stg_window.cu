@@ -460,49 +460,66 @@ __global__ void k_straggler_inst(uint64_t n_w, int rank_span, const double* lat,
 }
 
 // Per rank: flags, mean lateness (alert: over >=2-rank instances; median
-// reference: over all), mean z over flagged — each summed in instance order.
-// One warp per rank: lanes load 32 consecutive instances (coalesced row of the
-// rank-major matrix) and every lane runs the same in-order add chains.
-__global__ void k_straggler_rank(uint64_t n_w, int rank_span, const double* lat, double k, const double* mu_w,
-                                 const double* sigma_w, const uint32_t* m_w, uint8_t* present,
-                                 double* mean_all, double* mean_alert, double* z_mean, uint64_t* flags,
-                                 uint8_t* has_z) {
-    const int lane = threadIdx.x & 31;
+// reference: over all), mean z over flagged — each summed in instance order
+// (diagnosis.cpp:97-110, bit-exact: the same sequence of double roundings).
+// One warp per rank, in chunks of kStragChunk instances: all lanes load the
+// chunk (coalesced row of the rank-major matrix), decide presence / alert /
+// flag and z, and stage (value, z, bits) in shared memory; then lanes 0, 1, 2
+// run the three in-order add chains side by side over the chunk (lane 0: all
+// present, lane 1: present in >= 2-rank instances, lane 2: z of flagged), one
+// dependent add per element per chain and no shuffles.
+constexpr int kStragChunk = 256;
+constexpr int kStragWarps = 8;
+__global__ void __launch_bounds__(kStragWarps * 32) k_straggler_rank(
+    uint64_t n_w, int rank_span, const double* lat, double k, const double* mu_w, const double* sigma_w,
+    const uint32_t* m_w, uint8_t* present, double* mean_all, double* mean_alert, double* z_mean, uint64_t* flags,
+    uint8_t* has_z) {
+    __shared__ double s_val[kStragWarps][kStragChunk];
+    __shared__ double s_z[kStragWarps][kStragChunk];
+    __shared__ uint8_t s_bits[kStragWarps][kStragChunk];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int r = int((blockIdx.x * blockDim.x + threadIdx.x) >> 5); r < rank_span;
          r += int((gridDim.x * blockDim.x) >> 5)) {
-        double s_all = 0.0, s2 = 0.0, sz = 0.0;
+        double acc = 0.0;  // lane 0: Σ all present, lane 1: Σ alert, lane 2: Σ z of flagged
         uint64_t n_all = 0, n2 = 0, nz = 0;
         const double* row = lat + uint64_t(r) * n_w;
-        for (uint64_t c = 0; c < n_w; c += 32) {
-            const uint64_t w = c + lane;
-            double l = nan(""), z = 0.0;
-            bool two = false, fl = false;
-            if (w < n_w) {
-                l = row[w];
-                two = m_w[w] >= 2;
-                if (l == l && two) {
-                    const double mu = mu_w[w], sg = sigma_w[w];
-                    fl = sg > 0.0 && l > __dadd_rn(mu, __dmul_rn(k, sg));
-                    if (fl) z = __ddiv_rn(__dsub_rn(l, mu), sg);
+        for (uint64_t c0 = 0; c0 < n_w; c0 += kStragChunk) {
+            const uint32_t cn = uint32_t(n_w - c0 < kStragChunk ? n_w - c0 : kStragChunk);
+            for (uint32_t j = lane; j < kStragChunk; j += 32) {
+                const uint64_t w = c0 + j;
+                double l = nan(""), z = 0.0;
+                bool two = false, fl = false;
+                if (j < cn) {
+                    l = row[w];
+                    two = m_w[w] >= 2;
+                    if (l == l && two) {
+                        const double mu = mu_w[w], sg = sigma_w[w];
+                        fl = sg > 0.0 && l > __dadd_rn(mu, __dmul_rn(k, sg));
+                        if (fl) z = __ddiv_rn(__dsub_rn(l, mu), sg);
+                    }
+                }
+                const bool pres = l == l;
+                n_all += __popc(__ballot_sync(0xffffffffu, pres));
+                n2 += __popc(__ballot_sync(0xffffffffu, pres && two));
+                nz += __popc(__ballot_sync(0xffffffffu, fl));
+                s_val[wid][j] = l;
+                s_z[wid][j] = z;
+                s_bits[wid][j] = uint8_t((pres ? 1 : 0) | (pres && two ? 2 : 0) | (fl ? 4 : 0));
+            }
+            __syncwarp();
+            if (lane < 3) {
+                const double* src = lane == 2 ? s_z[wid] : s_val[wid];
+#pragma unroll 8
+                for (uint32_t j = 0; j < cn; ++j) {
+                    const double v = src[j];
+                    if ((s_bits[wid][j] >> lane) & 1) acc = __dadd_rn(acc, v);
                 }
             }
-            const bool pres = l == l;
-            const unsigned mp = __ballot_sync(0xffffffffu, pres);
-            const unsigned m2 = __ballot_sync(0xffffffffu, pres && two);
-            const unsigned mf = __ballot_sync(0xffffffffu, fl);
-            n_all += __popc(mp);
-            n2 += __popc(m2);
-            nz += __popc(mf);
-            unsigned bits = mp;
-            while (bits) {  // in instance order
-                const int t = __ffs(bits) - 1;
-                bits &= bits - 1;
-                const double v = __shfl_sync(0xffffffffu, l, t);
-                s_all = __dadd_rn(s_all, v);
-                if ((m2 >> t) & 1u) s2 = __dadd_rn(s2, v);
-                if ((mf >> t) & 1u) sz = __dadd_rn(sz, __shfl_sync(0xffffffffu, z, t));
-            }
+            __syncwarp();
         }
+        const double s_all = __shfl_sync(0xffffffffu, acc, 0);
+        const double s2 = __shfl_sync(0xffffffffu, acc, 1);
+        const double sz = __shfl_sync(0xffffffffu, acc, 2);
         if (lane == 0) {
             present[r] = n_all > 0;
             mean_all[r] = n_all ? __ddiv_rn(s_all, double(n_all)) : 0.0;
