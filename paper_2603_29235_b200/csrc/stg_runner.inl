@@ -396,22 +396,28 @@ struct Runner {
         LAUNCH(k_coll_deltas, grid_for(n), kThreads, n, inst_of, s_exit, imax, iing, n_group, dval, dflag, d_dmin);
         const long long dmin = get1(d_dmin);
         const int dbits = std::max(1, bits_for(uint64_t(-dmin)));
-        if (rbits + dbits > 64) fail(STG_EINVAL, "barrier-exit spread too large for the median key");
-        uint64_t* dkey_all = dev<uint64_t>("c_dkey_all", n);
-        LAUNCH(k_coll_dkeys, grid_for(n), kThreads, n, key_s, rmask, dval, dmin, dbits, dkey_all);
-        uint64_t* dkey = dev<uint64_t>("c_dkey", n);
-        uint64_t n_d;
+        uint64_t n_d = 0;
         {
-            unsigned long long* nsel = dev<unsigned long long>("c_nsel", 1);
-            size_t tb = 0;
-            STG_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, dkey_all, dflag, dkey, nsel, n, st));
-            STG_CUDA(cub::DeviceSelect::Flagged(temp(tb), tb, dkey_all, dflag, dkey, nsel, n, st));
-            ++launches;
-            n_d = get1(nsel);
+            // the rank of every (stream, rank) segment -> per-rank segment lists (host CSR)
+            uint32_t* d_segrank = dev<uint32_t>("c_segrank", n_seg);
+            LAUNCH(k_seg_rank, grid_for(n_seg), kThreads, n_seg, seg_pos, key_s, rmask, d_segrank);
+            std::vector<uint32_t> h_sr(n_seg);
+            down(h_sr.data(), d_segrank, n_seg);
+            std::vector<uint32_t> rso(size_t(span) + 1, 0), rsegs(n_seg);
+            for (uint64_t j = 0; j < n_seg; ++j) ++rso[size_t(h_sr[j]) + 1];
+            for (int32_t r = 0; r < span; ++r) rso[size_t(r) + 1] += rso[size_t(r)];
+            {
+                std::vector<uint32_t> fill(rso.begin(), rso.end() - 1);
+                for (uint64_t j = 0; j < n_seg; ++j) rsegs[fill[h_sr[j]]++] = uint32_t(j);
+            }
+            uint32_t* d_rso = up<uint32_t>("c_rso", rso.data(), size_t(span) + 1);
+            uint32_t* d_rsegs = up<uint32_t>("c_rsegs", rsegs.data(), std::max<uint64_t>(n_seg, 1));
+            unsigned long long* d_nd = dev<unsigned long long>("c_nd", 1);
+            zero(d_nd, 8);
+            LAUNCH(k_coll_median_sel, unsigned(std::min<int64_t>(span, 148 * 16)), 256, int(span), d_rso, d_rsegs,
+                   seg_pos, dval, dflag, dmin, dbits, d_off, d_has_off, d_nd);
+            n_d = get1(d_nd);
         }
-        uint64_t* dkey_s = dev<uint64_t>("c_dkey_s", n);
-        sort_keys(dkey, dkey_s, n_d, rbits + dbits);
-        LAUNCH(k_coll_median, grid_for(span), kThreads, span, dkey_s, n_d, dbits, dmin, d_off, d_has_off);
         res.have_offsets = n_d > 0;
         // windowed complete instances ordered by max aligned exit
         unsigned long long* aexit = dev<unsigned long long>("c_aexit", I);

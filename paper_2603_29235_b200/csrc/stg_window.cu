@@ -324,42 +324,96 @@ __global__ void k_coll_deltas(uint64_t n, const uint32_t* inst_of, const int64_t
     for (int o = 16; o > 0; o >>= 1) lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
     if ((threadIdx.x & 31) == 0) atomicMin(dmin, lo);
 }
-// composite sort key rank << dbits | (delta - dmin)
-__global__ void k_coll_dkeys(uint64_t n, const uint64_t* key, uint64_t rmask, const int64_t* dval, long long dmin,
-                             int dbits, uint64_t* dkey) {
-    for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < n;
-         p += uint64_t(gridDim.x) * blockDim.x)
-        dkey[p] = ((key[p] & rmask) << dbits) | uint64_t(dval[p] - dmin);
+// align_clocks (collective.cpp:105-125) without sorting the deltas: one CTA per
+// rank walks the rank's (stream, rank) segments and finds the two middle order
+// statistics of its barrier-exit deltas by radix select (8-bit digits from the
+// top, shared-memory histograms, warp-aggregated increments), then takes the
+// median exactly like the reference (even count: truncating int64 mean, :122).
+__global__ void k_seg_rank(uint64_t n_seg, const uint32_t* seg_pos, const uint64_t* key, uint64_t rmask,
+                           uint32_t* seg_rank) {
+    for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < n_seg; j += uint64_t(gridDim.x) * blockDim.x)
+        seg_rank[j] = uint32_t(key[seg_pos[j]] & rmask);
 }
-
-// Per rank: median of its sorted deltas (even n: truncating int64 mean, :122).
-__global__ void k_coll_median(int rank_span, const uint64_t* dkey, uint64_t n, int dbits, long long dmin, int64_t* off,
-                              uint8_t* has_off) {
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rank_span; r += gridDim.x * blockDim.x) {
-        uint64_t lo_key = uint64_t(r) << dbits, hi_key = uint64_t(r + 1) << dbits;
-        uint64_t a = 0, b = n;
-        while (a < b) {
-            uint64_t m = (a + b) >> 1;
-            if (dkey[m] < lo_key) a = m + 1; else b = m;
-        }
-        uint64_t lo = a;
-        b = n;
-        while (a < b) {
-            uint64_t m = (a + b) >> 1;
-            if (dkey[m] < hi_key) a = m + 1; else b = m;
-        }
-        uint64_t cnt = a - lo;
+__global__ void __launch_bounds__(256) k_coll_median_sel(int rank_span, const uint32_t* rso, const uint32_t* rsegs,
+                                                        const uint32_t* seg_pos, const int64_t* dval,
+                                                        const uint32_t* dflag, long long dmin, int dbits,
+                                                        int64_t* off, uint8_t* has_off, unsigned long long* n_total) {
+    __shared__ unsigned hist[2][256];
+    __shared__ unsigned long long s_pref[2], s_k[2], s_cnt;
+    const int lane = threadIdx.x & 31;
+    for (int r = blockIdx.x; r < rank_span; r += gridDim.x) {
+        const uint32_t j0 = rso[r], j1 = rso[r + 1];
+        // pass 0: count the rank's flagged deltas
+        unsigned long long c = 0;
+        for (uint32_t j = j0; j < j1; ++j)
+            for (uint32_t q = seg_pos[rsegs[j]] + threadIdx.x; q < seg_pos[rsegs[j] + 1]; q += blockDim.x) c += dflag[q];
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (threadIdx.x == 0) s_cnt = 0;
+        __syncthreads();
+        if (lane == 0 && c) atomicAdd(&s_cnt, c);
+        __syncthreads();
+        const unsigned long long cnt = s_cnt;
         if (cnt == 0) {
-            has_off[r] = 0;
-            off[r] = 0;
+            if (threadIdx.x == 0) {
+                has_off[r] = 0;
+                off[r] = 0;
+            }
+            __syncthreads();
             continue;
         }
-        const uint64_t dm = dbits >= 64 ? ~0ull : ((1ull << dbits) - 1);
-        auto val = [&](uint64_t i) { return int64_t(dkey[lo + i] & dm) + dmin; };
-        has_off[r] = 1;
-        off[r] = cnt % 2 ? val(cnt / 2) : (val(cnt / 2 - 1) + val(cnt / 2)) / 2;
+        if (threadIdx.x == 0) {
+            s_pref[0] = s_pref[1] = 0;
+            s_k[0] = (cnt - 1) / 2;
+            s_k[1] = cnt / 2;
+            atomicAdd(n_total, cnt);
+        }
+        for (int sh = ((dbits + 7) / 8 - 1) * 8; sh >= 0; sh -= 8) {
+            for (int t = threadIdx.x; t < 512; t += blockDim.x) (&hist[0][0])[t] = 0;
+            __syncthreads();
+            const unsigned long long p0 = s_pref[0] >> sh >> 8, p1 = s_pref[1] >> sh >> 8;
+            for (uint32_t j = j0; j < j1; ++j) {
+                const uint32_t a = seg_pos[rsegs[j]], b = seg_pos[rsegs[j] + 1];
+                for (uint32_t q0 = a; q0 < b; q0 += blockDim.x) {  // warp-uniform trip count
+                    const uint32_t q = q0 + threadIdx.x;
+                    unsigned d0 = 0xffffffffu, d1 = 0xffffffffu;
+                    if (q < b && dflag[q]) {
+                        const unsigned long long v = (unsigned long long)(dval[q] - dmin);
+                        const unsigned long long hi = v >> sh >> 8;
+                        const unsigned dg = unsigned(v >> sh) & 255u;
+                        if (hi == p0) d0 = dg;
+                        if (hi == p1) d1 = dg;
+                    }
+                    const unsigned m0 = __match_any_sync(0xffffffffu, d0);
+                    if (d0 != 0xffffffffu && (__ffs(m0) - 1) == lane) atomicAdd(&hist[0][d0], __popc(m0));
+                    const unsigned m1 = __match_any_sync(0xffffffffu, d1);
+                    if (d1 != 0xffffffffu && (__ffs(m1) - 1) == lane) atomicAdd(&hist[1][d1], __popc(m1));
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x < 2) {
+                const int T = threadIdx.x;
+                unsigned long long k = s_k[T], cum = 0;
+                for (int bn = 0; bn < 256; ++bn) {
+                    const unsigned h = hist[T][bn];
+                    if (cum + h > k) {
+                        s_pref[T] |= (unsigned long long)bn << sh;
+                        s_k[T] = k - cum;
+                        break;
+                    }
+                    cum += h;
+                }
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            const int64_t lo = int64_t(s_pref[0]) + dmin, hi = int64_t(s_pref[1]) + dmin;
+            has_off[r] = 1;
+            off[r] = cnt % 2 ? hi : (lo + hi) / 2;
+        }
+        __syncthreads();
     }
 }
+
 
 // Windowing (bundle.cpp:270-279): max aligned exit per complete instance, init 0.
 __global__ void k_coll_aligned_exit(uint64_t n, const uint64_t* key, const uint32_t* inst_of,
