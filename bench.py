@@ -208,17 +208,20 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- reference
-def reference_arm(a, wl, torch, threads: int):
+def reference_arm(a, wl, torch, threads: int, steps: int = 1, warmup: int = 0):
     """The reference's own CPU path (oracle/_ref: strata build_group_data +
     diagnose, compiled from /root/reference) on a bounded sample of the same
-    workload, with its per-rank loop fanned over `threads` host threads."""
+    workload, with its per-rank loop fanned over `threads` host threads.
+    `warmup` untimed and `steps` timed runs, each a bounded sample sized so the
+    whole leg stays within a few minutes (the reference's own timers: the
+    build_group_data + diagnose calls, input marshalling excluded)."""
     from oracle import ref
     from paper_2603_29235_b200.abi import STG_MEM_HOST
     if not ref.available():
         return None
-    # bounded sample: `threads` ranks x k samples; the reference reloads the
-    # 1M-entry tables for every aggregated record (symrepo.cpp:99-120 via
-    # folded.cpp:24), so k is tiny.  Calibrate k on one rank.
+    # the reference reloads the 1M-entry tables for every aggregated record
+    # (symrepo.cpp:99-120 via folded.cpp:24), so a step holds few samples per
+    # rank.  Calibrate with every thread busy (table reloads contend for memory).
     def run(ranks, k):
         # spread the k samples over the whole window span
         ts, foff, pc, bn = wl.generate(torch, ranks, k, seed_off=17, period=max(1, wl.span // k))
@@ -228,15 +231,22 @@ def reference_arm(a, wl, torch, threads: int):
         t0 = time.perf_counter()
         res, tb, td = ref.window_run(w, threads=min(threads, ranks), want_json=False)
         return time.perf_counter() - t0, tb + td, ranks * k, res
-    _, t1, n1, _ = run(1, 2)
-    per_sample = max(t1 / n1, 1e-6)
-    k = max(1, int(a.cpu_budget_s * min(threads, a.ranks) / per_sample / min(threads, a.ranks)))
     ranks = min(threads, a.ranks)
-    wall, t, n, res = run(ranks, k)
-    return {"value": n / t, "unit": UNIT, "cores": ranks, "kind": "reference",
-            "sample": f"{ranks} ranks x {k} samples of the C2 workload (64-frame stacks, 3x{a.nsym}-symbol "
-                      f"tables), build_group_data+diagnose in {t:.2f}s; the reference reloads the 1M-entry "
-                      "SYMR tables once per aggregated record (resolve_stack cache is per call)",
+    _, t1, _, _ = run(ranks, 1)
+    budget = max(2.0, min(a.cpu_budget_s, 150.0 / max(1, steps + warmup)))
+    k = max(1, int(budget / max(t1, 1e-6)))
+    for _ in range(warmup):
+        run(ranks, k)
+    tot_t = tot_n = 0.0
+    res = None
+    for _ in range(max(1, steps)):
+        _, t, n, res = run(ranks, k)
+        tot_t += t
+        tot_n += n
+    return {"value": tot_n / tot_t, "unit": UNIT, "cores": ranks, "kind": "reference",
+            "sample": f"{max(1, steps)} x ({ranks} ranks x {k} samples) of the C2 workload (64-frame stacks, "
+                      f"3x{a.nsym}-symbol tables), build_group_data+diagnose in {tot_t:.2f}s; the reference reloads "
+                      "the 1M-entry SYMR tables once per aggregated record (resolve_stack cache is per call)",
             "verdict": res["report"]["verdict"]}
 
 
@@ -533,15 +543,17 @@ def main():
     if a.impl == "reference":
         if rank == 0:
             wl = Workload(a, 0)
-            cb = reference_arm(a, wl, torch, os.cpu_count() or 1)
+            cb = reference_arm(a, wl, torch, os.cpu_count() or 1, steps=a.steps, warmup=a.warmup)
             if cb is None:
                 print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libstrata_ref.so not built"}))
             else:
                 line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
-                        "n_gpus": a.gpus, "steps": 1, "warmup": 0, "higher_is_better": True,
+                        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "higher_is_better": True,
                         "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-                        "config": {"workload": "C2 bounded sample", "ranks_per_gpu": a.ranks,
-                                   "samples_per_rank": a.spr, "depth": a.depth},
+                        "config": {"workload": "C2: 128 ranks x 1M samples per GPU, 64-frame stacks, 3x1M-symbol tables",
+                                   "ranks_per_gpu": a.ranks, "samples_per_rank": a.spr, "depth": a.depth,
+                                   "distinct_stacks": a.pool, "symbols_per_table": a.nsym,
+                                   "inputs": "host memory, bounded sample per step (see cpu_baseline.sample)"},
                         "cpu_baseline": cb,
                         "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                                 "d2h_bytes_per_step": 0}}
