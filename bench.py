@@ -232,17 +232,20 @@ def reference_arm(a, wl, torch, threads: int, steps: int = 1, warmup: int = 0):
         res, tb, td = ref.window_run(w, threads=min(threads, ranks), want_json=False)
         return time.perf_counter() - t0, tb + td, ranks * k, res
     ranks = min(threads, a.ranks)
-    _, t1, _, _ = run(ranks, 1)
+    w1, t1, _, _ = run(ranks, 2)
     budget = max(2.0, min(a.cpu_budget_s, 150.0 / max(1, steps + warmup)))
-    k = max(1, int(budget / max(t1, 1e-6)))
+    k = max(1, int(2 * budget / max(w1, t1, 1e-6)))
+    print(f"[bench ref] calibration: {ranks} ranks x 2 samples in {w1:.2f}s wall ({t1:.2f}s in the reference); "
+          f"{k} samples per rank per step", file=sys.stderr, flush=True)
     for _ in range(warmup):
         run(ranks, k)
     tot_t = tot_n = 0.0
     res = None
-    for _ in range(max(1, steps)):
-        _, t, n, res = run(ranks, k)
+    for i in range(max(1, steps)):
+        w, t, n, res = run(ranks, k)
         tot_t += t
         tot_n += n
+        print(f"[bench ref] step {i}: {n} samples in {t:.2f}s ({w:.2f}s wall)", file=sys.stderr, flush=True)
     return {"value": tot_n / tot_t, "unit": UNIT, "cores": ranks, "kind": "reference",
             "sample": f"{max(1, steps)} x ({ranks} ranks x {k} samples) of the C2 workload (64-frame stacks, "
                       f"3x{a.nsym}-symbol tables), build_group_data+diagnose in {tot_t:.2f}s; the reference reloads "
