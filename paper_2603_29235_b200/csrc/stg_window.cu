@@ -1136,12 +1136,15 @@ __global__ void k_seq_dedupe(uint64_t L, const uint64_t* l_hi, const uint64_t* l
         uint64_t fa = l_hi[l], fb = l_lo[l];
         uint64_t i = mix_a(fa ^ fb) & mask;
         uint32_t gid = 0xffffffffu;
-        for (uint64_t probe = 0; probe <= mask; ++probe) {
+        // a table sized from the previous window may be too small: past half
+        // load, or after a long probe run, the call retries at 2 slots per line
+        for (uint64_t probe = 0; probe <= mask && probe < 1024; ++probe) {
             unsigned long long cur = *(volatile unsigned long long*)&T[i].hi;
             if (cur == 0) {
                 cur = atomicCAS(&T[i].hi, 0ull, (unsigned long long)fa);
                 if (cur == 0) {
                     gid = atomicAdd(n_seq, 1u);
+                    if (uint64_t(gid) + 1 > (mask + 1) / 2) *overflow = 1;
                     T[i].lo = fb;
                     T[i].rep = l_rep[l];
                     seq_rep[gid] = l_rep[l];
