@@ -1017,7 +1017,9 @@ struct Runner {
             unsigned long long* lc64 = dev<unsigned long long>("lc64", L);
             LAUNCH(k_u32_to_u64, grid_for(L), kThreads, L, l_cnt32, lc64);
             d_lcount = dev<unsigned long long>("lcount_s", L);
-            sort_pairs(lkey, d_lkey, lc64, d_lcount, L);
+            int rb = 1;  // line key = rank << 32 | sequence rank: sort only the bits in use
+            while ((uint64_t(1) << rb) < uint64_t(R)) ++rb;
+            sort_pairs(lkey, d_lkey, lc64, d_lcount, L, 32 + rb);
             if (S < G) {  // identical name sequences from distinct keys: merge lines
                 uint64_t* uk = dev<uint64_t>("rbk_k", L);
                 unsigned long long* uv = dev<unsigned long long>("rbk_v", L);
