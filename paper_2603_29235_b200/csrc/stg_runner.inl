@@ -87,6 +87,7 @@ struct Runner {
     cudaEvent_t ev_incl = nullptr;  // inclusive counts done (side stream)
     bool gpu_os_done = false;
     bool incl_pending = false;
+    uint64_t max_seq_len = 0;
     void wait_incl() {
         if (!incl_pending) return;
         STG_CUDA(cudaStreamWaitEvent(st, ev_incl, 0));
@@ -954,7 +955,7 @@ struct Runner {
         // lexicographic order of the sequences
         uint32_t* seq_rank = dev<uint32_t>("seq_rank", G);
         {
-            uint64_t maxlen = 0;
+            uint64_t maxlen = 0;  // kept in max_seq_len for the hottest-path download
             {
                 uint64_t* mx = dev<uint64_t>("pd_max", 1);
                 size_t tb = 0;
@@ -962,6 +963,7 @@ struct Runner {
                 STG_CUDA(cub::DeviceReduce::Max(temp(tb), tb, seq_len, mx, int64_t(G), st));
                 ++launches;
                 maxlen = get1(mx);
+                max_seq_len = maxlen;
             }
             int p_log = 1;
             while ((uint64_t(1) << p_log) < maxlen) ++p_log;
@@ -1124,24 +1126,37 @@ struct Runner {
         if (merged) {
             auto sc = static_cast<unsigned long long*>(c.buf("seq_counts").p);
             for (int pass = 0; pass < 2; ++pass)
-                LAUNCH(k_hottest, grid_for(S), kThreads, S, nullptr, sc, 1, d_dn_off, d_dn, f, pass, best);
+                LAUNCH(k_hottest, grid_for(uint64_t(S) * 32), kThreads, S, nullptr, sc, 1, d_dn_off, d_dn, f, pass, best);
         } else {
             for (int pass = 0; pass < 2; ++pass)
-                LAUNCH(k_hottest, grid_for(b - a), kThreads, b - a, d_lkey + a, d_lcount + a, 0, d_dn_off, d_dn, f, pass,
+                LAUNCH(k_hottest, grid_for((b - a) * 32), kThreads, b - a, d_lkey + a, d_lcount + a, 0, d_dn_off, d_dn, f, pass,
                        best);
         }
-        unsigned long long hb[2];
-        down(hb, best, 2);
-        if (hb[1] == ~0ull) return {};
-        uint32_t s;
-        if (merged)
-            s = uint32_t(hb[1]);
-        else {
-            uint64_t k;
-            down(&k, d_lkey + a + hb[1], 1);
-            s = uint32_t(k);
+        // one download for the winner's whole name sequence
+        const uint32_t cap = uint32_t(std::max<uint64_t>(max_seq_len, 1));
+        uint32_t* pk = dev<uint32_t>("hot_pack", size_t(cap) + 2);
+        LAUNCH(k_hot_pack, 1, 256, best, merged ? nullptr : d_lkey + a, merged ? 1 : 0, d_dense_rep, d_seq_off, d_arena,
+               cap, pk);
+        std::vector<uint32_t> hp(size_t(cap) + 2);
+        down(hp.data(), pk, hp.size());
+        if (!hp[0]) return {};
+        if (hp[1] > cap) {  // longer than any sequence seen at the sort: fall back
+            unsigned long long hb[2];
+            down(hb, best, 2);
+            uint32_t s;
+            if (merged)
+                s = uint32_t(hb[1]);
+            else {
+                uint64_t k;
+                down(&k, d_lkey + a + hb[1], 1);
+                s = uint32_t(k);
+            }
+            return seq_names(s);
         }
-        return seq_names(s);
+        std::vector<std::string> out;
+        out.reserve(hp[1]);
+        for (uint32_t k = 0; k < hp[1]; ++k) out.push_back(res.name_of(hp[2 + k]));
+        return out;
     }
     // Exact inclusive fractions over lines [a, a+n) (or over all sequences when
     // merged): returns (dense name, fraction) in name order.
@@ -1514,7 +1529,7 @@ struct Runner {
         unsigned long long init[2] = {0, ~0ull};
         STG_CUDA(cudaMemcpyAsync(best, init, 16, cudaMemcpyHostToDevice, st));
         for (int pass = 0; pass < 2; ++pass)
-            LAUNCH(k_hottest, grid_for(m.n), kThreads, m.n, nullptr, m.cnt, 1, m.dn_off, m.dn, key, pass, best);
+            LAUNCH(k_hottest, grid_for(m.n * 32), kThreads, m.n, nullptr, m.cnt, 1, m.dn_off, m.dn, key, pass, best);
         unsigned long long hb[2];
         down(hb, best, 2);
         if (hb[1] == ~0ull) return {};

@@ -1479,20 +1479,48 @@ __global__ void k_seq_counts(uint64_t L, const uint64_t* lkey, const unsigned lo
 __global__ void k_hottest(uint64_t n, const uint64_t* seq_of, const unsigned long long* cnt_of, int seq_is_index,
                           const uint64_t* dn_off, const uint32_t* dn, uint32_t f, int pass,
                           unsigned long long* best) {
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
-        unsigned long long c = cnt_of[i];
+    // one warp per line: the lanes test 32 of the line's distinct names at once
+    const int lane = threadIdx.x & 31;
+    const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t i = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; i < n; i += nw) {
+        const unsigned long long c = cnt_of[i];
         if (c == 0) continue;
         if (pass == 1 && c != best[0]) continue;
-        uint32_t s = seq_is_index ? uint32_t(i) : uint32_t(seq_of[i]);
+        const uint32_t s = seq_is_index ? uint32_t(i) : uint32_t(seq_of[i]);
+        const uint64_t k0 = dn_off[s], k1 = dn_off[s + 1];
         bool has = false;
-        for (uint64_t k = dn_off[s]; k < dn_off[s + 1]; ++k)
-            if (dn[k] == f) { has = true; break; }
-        if (!has) continue;
+        for (uint64_t k = k0; k < k1; k += 32) {
+            const bool hit = k + lane < k1 && dn[k + lane] == f;
+            if (__any_sync(0xffffffffu, hit)) {
+                has = true;
+                break;
+            }
+        }
+        if (!has || lane != 0) continue;
         if (pass == 0)
             atomicMax(best, c);
         else
             atomicMin(best + 1, (unsigned long long)i);
     }
+}
+
+// The hottest line's name sequence, packed for one download: out[0] = found,
+// out[1] = length, out[2..] = the names (cap entries at most).
+__global__ void k_hot_pack(const unsigned long long* best, const uint64_t* lkey, int merged, const uint32_t* dense_rep,
+                           const uint64_t* seq_off, const uint32_t* arena, uint32_t cap, uint32_t* out) {
+    const unsigned long long bi = best[1];
+    if (bi == ~0ull) {
+        if (threadIdx.x == 0) out[0] = out[1] = 0;
+        return;
+    }
+    const uint32_t s = merged ? uint32_t(bi) : uint32_t(lkey[bi]);
+    const uint32_t g = dense_rep[s];
+    const uint64_t o0 = seq_off[g], len = seq_off[g + 1] - o0;
+    if (threadIdx.x == 0) {
+        out[0] = 1;
+        out[1] = uint32_t(len);
+    }
+    for (uint64_t k = threadIdx.x; k < len && k < cap; k += blockDim.x) out[2 + k] = arena[o0 + k];
 }
 
 // Exact inclusive fractions in the reference's summation order
