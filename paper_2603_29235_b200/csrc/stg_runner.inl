@@ -157,11 +157,12 @@ struct Runner {
 
     // ---------------------------------------------------------------- cub
     template <class K, class V>
-    void sort_pairs(const K* kin, K* kout, const V* vin, V* vout, uint64_t n, int end_bit = sizeof(K) * 8) {
+    void sort_pairs(const K* kin, K* kout, const V* vin, V* vout, uint64_t n, int end_bit = sizeof(K) * 8,
+                    int begin_bit = 0) {
         if (!n) return;
         size_t tb = 0;
-        STG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, vin, vout, n, 0, end_bit, st));
-        STG_CUDA(cub::DeviceRadixSort::SortPairs(temp(tb), tb, kin, kout, vin, vout, n, 0, end_bit, st));
+        STG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, vin, vout, n, begin_bit, end_bit, st));
+        STG_CUDA(cub::DeviceRadixSort::SortPairs(temp(tb), tb, kin, kout, vin, vout, n, begin_bit, end_bit, st));
         ++launches;
     }
     template <class K>
@@ -1195,16 +1196,25 @@ struct Runner {
         uint64_t* keys_s = dev<uint64_t>("xf_keys_s", np);
         double* vals = dev<double>("xf_vals", np);
         double* vals_s = dev<double>("xf_vals_s", np);
-        LAUNCH(k_pair_emit, grid_for(n), kThreads, n, n0, lk0, lk1, cnt0, cnt1, t0, t1, d_dn_off, d_dn, po, LB, keys,
+        // names of the window's own dictionary are dense (< F); caller-given
+        // global keys may use all 31 bits
+        int NB = 31;
+        if (!dn) {
+            NB = 1;
+            while (NB < 31 && (uint64_t(1) << NB) < F) ++NB;
+        }
+        LAUNCH(k_pair_emit, grid_for(n), kThreads, n, n0, lk0, lk1, cnt0, cnt1, t0, t1, d_dn_off, d_dn, po, LB, NB, keys,
                vals);
-        sort_pairs(keys, keys_s, vals, vals_s, np, LB + 32);
+        // pairs are emitted in line order and the radix sort is stable, so
+        // sorting the (side, name) bits alone keeps each name's lines in order
+        sort_pairs(keys, keys_s, vals, vals_s, np, LB + NB + 1, LB);
         uint32_t* flag = dev<uint32_t>("xf_flag", np);
         LAUNCH(k_pair_segflags, grid_for(np), kThreads, np, keys_s, LB, flag);
         uint32_t* seg = dev<uint32_t>("xf_seg", np);
         uint64_t nseg = select_flagged(flag, seg, np);
         uint32_t* of = dev<uint32_t>("xf_of", nseg);
         double* ov = dev<double>("xf_ov", nseg);
-        LAUNCH(k_pair_segsum, grid_for(nseg * 32, kSegWarps * 32), kSegWarps * 32, nseg, seg, np, keys_s, LB, vals_s,
+        LAUNCH(k_pair_segsum, grid_for(nseg * 32, kSegWarps * 32), kSegWarps * 32, nseg, seg, np, keys_s, LB, NB, vals_s,
                of, ov);
         std::vector<uint32_t> hf(nseg);
         std::vector<double> hv(nseg);

@@ -1537,13 +1537,13 @@ __global__ void k_pair_count(uint64_t n, uint64_t n0, const uint64_t* lkey0, con
     }
 }
 // Pairs (name, line) of up to two line ranges (side 0: lines [0, n0), side 1:
-// [n0, n)); key = (side << 31 | name) << LB | line within its side (LB bits hold
-// a line index, so the radix sort only runs LB + 32 bits), value =
+// [n0, n)); key = (side << NB | name) << LB | line within its side (the stable
+// radix sort only runs the NB + 1 side/name bits above LB), value =
 // double(count) / double(total of its side).
 __global__ void k_pair_emit(uint64_t n, uint64_t n0, const uint64_t* lkey0, const uint64_t* lkey1,
                             const unsigned long long* cnt0, const unsigned long long* cnt1, uint64_t total0,
                             uint64_t total1, const uint64_t* dn_off, const uint32_t* dn, const uint64_t* pair_off,
-                            int LB, uint64_t* keys, double* vals) {
+                            int LB, int NB, uint64_t* keys, double* vals) {
     const double t0 = __ull2double_rn(total0), t1 = __ull2double_rn(total1);
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
         const bool side = i >= n0;
@@ -1552,7 +1552,7 @@ __global__ void k_pair_emit(uint64_t n, uint64_t n0, const uint64_t* lkey0, cons
         const uint32_t s = lk ? uint32_t(lk[j]) : uint32_t(j);
         const double x = __ddiv_rn(__ull2double_rn((side ? cnt1 : cnt0)[j]), side ? t1 : t0);  // count / total
         uint64_t o = pair_off[i];
-        const uint64_t sb = side ? 1ull << 31 : 0ull;
+        const uint64_t sb = side ? 1ull << NB : 0ull;
         for (uint64_t k = dn_off[s]; k < dn_off[s + 1]; ++k, ++o) {
             keys[o] = ((sb | dn[k]) << LB) | j;
             vals[o] = x;
@@ -1571,7 +1571,8 @@ __global__ void k_pair_segflags(uint64_t np, const uint64_t* keys, int LB, uint3
 constexpr int kSegChunk = 256;
 constexpr int kSegWarps = 8;
 __global__ void __launch_bounds__(kSegWarps * 32) k_pair_segsum(uint64_t nseg, const uint32_t* seg, uint64_t np,
-                                                                const uint64_t* keys, int LB, const double* vals,
+                                                                const uint64_t* keys, int LB, int NB,
+                                                                const double* vals,
                                                                 uint32_t* out_side_f, double* out_v) {
     __shared__ double buf[kSegWarps][2][kSegChunk];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1622,7 +1623,8 @@ __global__ void __launch_bounds__(kSegWarps * 32) k_pair_segsum(uint64_t nseg, c
             }
         }
         if (lane == 0) {
-            out_side_f[g] = uint32_t(keys[a] >> LB);  // side << 31 | name
+            const uint64_t k = keys[a] >> LB;  // side << NB | name
+            out_side_f[g] = uint32_t((k >> NB) << 31 | (k & ((1ull << NB) - 1)));
             out_v[g] = acc;
         }
     }
