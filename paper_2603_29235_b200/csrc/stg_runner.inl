@@ -985,8 +985,8 @@ struct Runner {
                     n /= 2;
                     int vb = 1;
                     while ((uint64_t(1) << vb) <= vmax) ++vb;
-                    LAUNCH(k_pd_pairs, grid_for(n), kThreads, n, cur, key, idx);
-                    sort_pairs(key, key_s, idx, idx_s, n, 32 + vb);
+                    LAUNCH(k_pd_pairs, grid_for(n), kThreads, n, cur, vb, key, idx);
+                    sort_pairs(key, key_s, idx, idx_s, n, 2 * vb);
                     LAUNCH(k_pd_flags, grid_for(n), kThreads, n, key_s, flg);
                     incl_sum(flg, rnk, n);
                     LAUNCH(k_pd_scatter, grid_for(n), kThreads, n, idx_s, rnk, cur);

@@ -1315,10 +1315,11 @@ __global__ void k_pd_init(uint64_t n, uint32_t p_log, const uint64_t* off, const
         cur[x] = j < len ? arena[o + j] + 1u : 0u;
     }
 }
-__global__ void k_pd_pairs(uint64_t n, const uint32_t* cur, uint64_t* key, uint32_t* idx) {
+// key = (left << vb) | right: both values are < 2^vb, so the radix sort runs 2·vb bits
+__global__ void k_pd_pairs(uint64_t n, const uint32_t* cur, int vb, uint64_t* key, uint32_t* idx) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
         const uint2 v = reinterpret_cast<const uint2*>(cur)[i];
-        key[i] = (uint64_t(v.x) << 32) | v.y;
+        key[i] = (uint64_t(v.x) << vb) | v.y;
         idx[i] = uint32_t(i);
     }
 }
