@@ -1103,6 +1103,24 @@ struct Runner {
         }
         return res.name_of(h_dense_final[f]);
     }
+    // names of a few dense indices: gathered on the device unless the whole
+    // dense -> name map is already on the host (or most of it is wanted)
+    std::vector<std::string> dense_names(const std::vector<uint32_t>& fs) {
+        std::vector<std::string> out;
+        out.reserve(fs.size());
+        if (h_dense_final.size() == F || fs.size() * 64 >= F) {
+            for (uint32_t f : fs) out.push_back(dense_name(f));
+            return out;
+        }
+        if (fs.empty()) return out;
+        const uint32_t* q = up<uint32_t>("dn_q", fs.data(), fs.size());
+        uint32_t* g = dev<uint32_t>("dn_g", fs.size());
+        LAUNCH(k_gather_u32, grid_for(fs.size()), kThreads, uint64_t(fs.size()), q, d_dense_final, g);
+        std::vector<uint32_t> h(fs.size());
+        down(h.data(), g, h.size());
+        for (uint32_t k : h) out.push_back(res.name_of(k));
+        return out;
+    }
     int cpu_index(int rank) const {
         auto it = std::lower_bound(res.cpu_rank_ids.begin(), res.cpu_rank_ids.end(), rank);
         if (it == res.cpu_rank_ids.end() || *it != rank) return -1;
@@ -1722,7 +1740,14 @@ struct Runner {
                     while (j < fr_.size() && fr_[j].first < f) ++j;
                     double fr = j < fr_.size() && fr_[j].first == f ? fr_[j].second : 0.0;
                     double d = fs - fr;
-                    if (d > cfg.delta) cands.push_back({dense_name(f), fs, fr, d, f});
+                    if (d > cfg.delta) cands.push_back({std::string(), fs, fr, d, f});
+                }
+                {
+                    std::vector<uint32_t> want;
+                    want.reserve(cands.size());
+                    for (const auto& cd : cands) want.push_back(cd.f);
+                    auto nm = dense_names(want);
+                    for (size_t k = 0; k < cands.size(); ++k) cands[k].fn = std::move(nm[k]);
                 }
                 std::sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) {
                     return a.d != b.d ? a.d > b.d : a.fn < b.fn;

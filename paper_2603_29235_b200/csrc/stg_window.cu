@@ -1748,6 +1748,10 @@ __global__ void k_scatter_add(uint64_t n, const uint32_t* to, const unsigned lon
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
         atomicAdd(out + to[i], v[i]);
 }
+__global__ void k_gather_u32(uint64_t n, const uint32_t* idx, const uint32_t* src, uint32_t* out) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        out[i] = src[idx[i]];
+}
 __global__ void k_u32_to_u64(uint64_t n, const uint32_t* a, unsigned long long* b) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
         b[i] = a[i];
