@@ -1076,7 +1076,9 @@ struct Runner {
         STG_CUDA(cudaStreamWaitEvent(c.side, ev_pre, 0));
         {
             cudaStream_t keep = st;
-            st = c.side;
+            // STG_INCL_MAIN=1 (experiments): keep the counts on the main stream
+            static const bool incl_main = std::getenv("STG_INCL_MAIN") != nullptr;
+            if (!incl_main) st = c.side;
             if (F * sizeof(unsigned) <= 160 * 1024) {
                 const size_t sm = F * sizeof(unsigned);
                 if (sm > 48 * 1024)
