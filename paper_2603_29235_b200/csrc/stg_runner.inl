@@ -1050,13 +1050,14 @@ struct Runner {
         LAUNCH(k_u32_to_u64, grid_for(S + 1), kThreads, S + 1, dcnt32, (unsigned long long*)dcnt);
         d_dn_off = dev<uint64_t>("dn_off", S + 1);
         excl_sum(dcnt, d_dn_off, S + 1);
-        uint64_t ND = get1(d_dn_off + S);
-        d_dn = dev<uint32_t>("dn", ND);
+        // distinct names per sequence <= its length: size by the arena, count stays on the device
+        const uint64_t ND = A;
+        d_dn = dev<uint32_t>("dn", std::max<uint64_t>(ND, 1));
         LAUNCH(k_seq_distinct<true>, grid_for(S * 32), kThreads, uint32_t(S), d_dense_rep, d_seq_off, d_arena, nullptr,
                d_dn_off, d_dn);
         uint32_t* used = dev<uint32_t>("used", NF + 1);
         zero(used, (NF + 1) * 4);
-        LAUNCH(k_mark_used, grid_for(ND), kThreads, ND, d_dn, used);
+        LAUNCH(k_mark_used, grid_for(ND), kThreads, d_dn_off + S, d_dn, used);
         uint32_t* used_scan = dev<uint32_t>("used_scan", NF + 1);
         excl_sum(used, used_scan, NF + 1);
         F = get1(used_scan + NF);
@@ -1064,7 +1065,7 @@ struct Runner {
         mark("f:names");
         d_dense_final = dev<uint32_t>("dense_final", F);
         LAUNCH(k_dense_final, grid_for(NF), kThreads, NF, used, used_scan, d_dense_final);
-        LAUNCH(k_dense_names, grid_for(ND), kThreads, ND, d_dn, used_scan);
+        LAUNCH(k_dense_names, grid_for(ND), kThreads, d_dn_off + S, d_dn, used_scan);
         uint64_t cells = uint64_t(R) * F;
         if (cells > (1ull << 31)) fail(STG_ENOMEM, "rank x name matrix too large");
         d_incl = dev<unsigned long long>("incl", cells);

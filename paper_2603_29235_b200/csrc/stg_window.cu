@@ -1388,11 +1388,14 @@ __global__ void k_seq_distinct(uint32_t S, const uint32_t* dense_rep, const uint
     }
 }
 
-__global__ void k_mark_used(uint64_t n, const uint32_t* dn, uint32_t* used) {
+// n read on the device (the exclusive sum's last entry): no host round trip
+__global__ void k_mark_used(const uint64_t* n_ptr, const uint32_t* dn, uint32_t* used) {
+    const uint64_t n = *n_ptr;
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
         used[dn[i]] = 1;
 }
-__global__ void k_dense_names(uint64_t n, uint32_t* dn, const uint32_t* used_scan) {
+__global__ void k_dense_names(const uint64_t* n_ptr, uint32_t* dn, const uint32_t* used_scan) {
+    const uint64_t n = *n_ptr;
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
         dn[i] = used_scan[dn[i]];  // exclusive scan -> dense index
 }
