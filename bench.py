@@ -13,8 +13,10 @@ resident in HBM (84 GB per GPU >> 126 MB L2, so no L2 flush is needed).
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--ranks R] [--spr S] [--no-e2e] [--no-cpu-baseline]
 
-N > 1: launched by torchrun, one process per GPU; each GPU analyses its own
-128-rank communication group (weak scaling); timing is the max over ranks.
+N > 1: launched by torchrun, one process per GPU; the N GPUs analyse ONE
+communication group of N x 128 ranks, each GPU holding the sample streams of
+its 128 ranks (weak scaling: 128 M samples per GPU), with libstg's NCCL
+exchange inside the window; timing is the max over ranks.
 """
 from __future__ import annotations
 
@@ -54,6 +56,8 @@ def args_parse():
     p.add_argument("--pool", type=int, default=50_000)
     p.add_argument("--nsym", type=int, default=1_000_000)
     p.add_argument("--seed", type=int, default=42)
+    p.add_argument("--hot", default="all", choices=["all", "bench"],
+                   help="functions the generator draws from: all of each 1M-symbol table, or 5k/20k/5k")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -96,9 +100,20 @@ class Workload:
         self.zipf_cdf = np.cumsum(w / w.sum())
         self.zipf_cdf[-1] = 1.0
 
-    def generate(self, torch, ranks: int, spr: int, seed_off: int = 0, period: int = 0):
-        """Device tensors (ts, foff, pc, bin) for `ranks` x `spr` samples."""
+    def _gen_args(self, ranks: int):
         a = self.a
+        # functions executed per binary: "bench" = 5k/20k/5k of the 1M (round-1
+        # default), "all" = every function of each table can be drawn
+        hot = (5000, 20000, 5000) if getattr(a, "hot", "all") == "bench" else (a.nsym,) * 3
+        return dict(depth=a.depth, pool=a.pool, zipf_cdf=self.zipf_cdf, hot=hot,
+                    soft_pc=self.tables[2][1][:9] + 4, slow_rank=self.slow if 0 <= self.slow < ranks else -1,
+                    soft_share=0.0174, jit_per_million=100, skew=self.skews[:ranks])
+
+    def generate(self, torch, ranks: int, spr: int, seed_off: int = 0, period: int = 0):
+        """Device tensors (ts, foff, pc, bin) for `ranks` x `spr` samples (bench-side CUDA
+        generator, csrc/bench_gen.cu)."""
+        a = self.a
+        g = self._gen_args(ranks)
         lib = C.CDLL(str(ROOT / "paper_2603_29235_b200" / "libstg_bench.so"))
         dev = torch.device("cuda")
         n = ranks * spr
@@ -109,24 +124,32 @@ class Workload:
         st = [torch.from_numpy(t[1].view(np.int64)).to(dev) for t in self.tables]
         sz = [torch.from_numpy(t[2].view(np.int32)).to(dev) for t in self.tables]
         cdf = torch.from_numpy(self.zipf_cdf).to(dev)
-        skew = torch.from_numpy(self.skews[:ranks].copy()).to(dev)
-        soft = self.tables[2][1][:9] + 4
+        skew = torch.from_numpy(g["skew"].copy()).to(dev)
         P = C.c_void_p
         starts = (P * 3)(*[t.data_ptr() for t in st])
         sizes = (P * 3)(*[t.data_ptr() for t in sz])
         nsym = (C.c_uint32 * 3)(*[a.nsym] * 3)
-        hot = (C.c_uint32 * 3)(5000, 20000, 5000)
-        softa = (C.c_uint64 * 9)(*[int(x) for x in soft])
+        hot = (C.c_uint32 * 3)(*g["hot"])
+        softa = (C.c_uint64 * 9)(*[int(x) for x in g["soft_pc"]])
         lib.bench_gen_c2.argtypes = [C.c_uint64, C.c_int, C.c_uint64, C.c_int, C.c_uint32, P, P, P, P, P, P,
                                      C.c_int, C.c_double, C.c_uint32, C.c_int64, P, P, P, P, P, P]
         rc = lib.bench_gen_c2(a.seed + seed_off, ranks, spr, a.depth, a.pool, cdf.data_ptr(),
                               C.cast(starts, P), C.cast(sizes, P), C.cast(nsym, P), C.cast(hot, P),
-                              C.cast(softa, P), self.slow if 0 <= self.slow < ranks else -1, 0.0174, 100,
+                              C.cast(softa, P), g["slow_rank"], g["soft_share"], g["jit_per_million"],
                               period or self.period, skew.data_ptr(), ts.data_ptr(), foff.data_ptr(), pc.data_ptr(),
                               bn.data_ptr(), P(torch.cuda.current_stream().cuda_stream))
         assert rc == 0, f"generator failed: {rc}"
         torch.cuda.synchronize()
         return ts, foff, pc, bn
+
+    def generate_host(self, ranks: int, spr: int, seed_off: int = 0, period: int = 0):
+        """The same samples as generate(), computed on the host with numpy
+        (tests/synth.c2_samples_host) — the reference arm loads no repo library."""
+        from tests.synth import c2_samples_host
+        g = self._gen_args(ranks)
+        return c2_samples_host(self.a.seed + seed_off, ranks, spr, self.a.depth, self.a.pool, g["zipf_cdf"],
+                               [(t[1], t[2]) for t in self.tables], g["hot"], g["soft_pc"], g["slow_rank"],
+                               g["soft_share"], g["jit_per_million"], period or self.period, g["skew"])
 
     def window(self, ranks: int, spr: int, arrays, memory: int):
         from paper_2603_29235_b200.abi import Window
@@ -224,9 +247,7 @@ def reference_arm(a, wl, torch, threads: int, steps: int = 1, warmup: int = 0):
     # rank.  Calibrate with every thread busy (table reloads contend for memory).
     def run(ranks, k):
         # spread the k samples over the whole window span
-        ts, foff, pc, bn = wl.generate(torch, ranks, k, seed_off=17, period=max(1, wl.span // k))
-        arrays = (ts.cpu().numpy(), foff.cpu().numpy().view(np.uint64), pc.cpu().numpy().view(np.uint64),
-                  bn.cpu().numpy().view(np.uint16))
+        arrays = wl.generate_host(ranks, k, seed_off=17, period=max(1, wl.span // k))
         w = wl.window(ranks, k, arrays, STG_MEM_HOST)
         t0 = time.perf_counter()
         res, tb, td = ref.window_run(w, threads=min(threads, ranks), want_json=False)
@@ -632,8 +653,11 @@ def main():
         ms = float(t.item())
     n_per_gpu = s["n_samples_in_window"]
     value = n_per_gpu * world / (ms / 1e3)
-    # ---- roofline of the dominant kernel (fused symbolize+aggregate)
-    algo_bytes = 10 * win.n_frames + 16 * win.n_samples  # pc 8 + bin 2 per frame; ts 8 + csr 8 per sample
+    # ---- roofline of the dominant kernel (fused symbolize+aggregate).  Algorithmic
+    # bytes: every sample's ts + CSR row (16 B), and the frames of the IN-WINDOW
+    # samples only (10 B each: 8 B pc + 2 B bin) — k_sym_agg never reads the frames
+    # of a sample outside the window.  Stacks are a.depth frames deep.
+    algo_bytes = 10 * n_per_gpu * a.depth + 16 * win.n_samples
     k_ms = float(np.median(sym_ms))
     pk = peaks()
     peak = pk.get("hbm_gbs", 6650.0)
@@ -641,6 +665,7 @@ def main():
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": ncu_traffic("k_sym_agg", algo_bytes), "kernel": "k_sym_agg",
             "kernel_ms": round(k_ms, 3), "algorithmic_bytes": algo_bytes,
+            "pipeline_frac": round(algo_bytes / (ms / 1e3) / 1e9 / peak, 4),
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback 6.65 TB/s"}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",

@@ -195,6 +195,18 @@ typedef struct stg_config {
     int64_t os_migration_floor;
     int32_t lookup_mode;    /* build_group_data uses ExactRange (bundle.cpp:300) */
     int32_t want_waterline; /* also compute compute_waterline/flag_ranks     */
+    /* verify = 1: after the fused symbolize+aggregate kernel, every in-window
+     * sample is symbolized again frame by frame (no prefix cache) and compared
+     * name by name with the representative of the aggregation slot it landed
+     * in, slot counts are recounted, and every folded line's stack is compared
+     * with its cross-rank sequence representative — the full compare the
+     * reference does on a digest hit (samples.cpp:67-76).  A mismatch (a
+     * fingerprint collision) re-runs the stage with re-keyed fingerprints and
+     * no prefix cache; stats.verify_retries counts those re-runs. */
+    int32_t verify;
+    /* tests only: truncate the prefix-cache key to 4 bits so that distinct
+     * call chains collide (exercises the verify retry).  Keep 0. */
+    int32_t debug_weak_prefix_key;
 } stg_config;
 
 void stg_config_default(stg_config* cfg);
@@ -222,6 +234,8 @@ typedef struct stg_run_stats {
     uint32_t agg_attempts;   /* >1 when a rank table had to grow           */
     uint64_t prefix_hits;    /* symbolization memo hits (raw call chains)  */
     uint64_t prefix_misses;
+    uint32_t verified;       /* 1 when cfg.verify checked this run clean   */
+    uint32_t verify_retries; /* re-runs after a detected collision         */
 } stg_run_stats;
 
 /* Replaces build_group_data (bundle.cpp:252-324) followed by diagnose

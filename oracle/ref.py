@@ -103,11 +103,15 @@ def simulate(scenario: str, seed: int, ranks: int = 0, iterations: int = 0,
 
 
 def window_run(win: Window, threads: int = 1, want_json: bool = True,
-               tmpdir: Optional[str] = None, artifacts: bool = False):
+               tmpdir: Optional[str] = None, artifacts: bool = False, shared_cache: bool = False):
     """Reference build_group_data + diagnose.  Returns (result_json, t_build_s, t_diag_s).
 
     artifacts=True adds result_json["artifacts"]: FoldedProfile::to_string of every
-    rank and diff_folded texts (see ref_harness.cpp)."""
+    rank and diff_folded texts (see ref_harness.cpp).  shared_cache=True symbolizes
+    each rank's records with the reference's resolve_stacks (one table cache per
+    rank) + fold_symbolized instead of to_folded's per-record table reload: the
+    same folded profiles (ref_harness.cpp build_group_data_threads), feasible on
+    1M-symbol tables."""
     cw, keep = win.to_c()
     n = len(win.symr)
     bufs = [C.create_string_buffer(s, len(s)) for s in win.symr]
@@ -117,8 +121,12 @@ def window_run(win: Window, threads: int = 1, want_json: bool = True,
     tb, td = C.c_double(), C.c_double()
     err = C.create_string_buffer(1024)
     tmp = tmpdir or tempfile.gettempdir()
-    rc = lib().ref_window_run(C.byref(cw), n, ptrs, lens, tmp.encode(), threads,
-                              2 if artifacts else int(want_json), C.byref(out), C.byref(tb), C.byref(td), err, 1024)
+    L = lib()
+    L.ref_window_run_ex.argtypes = [C.POINTER(StgWindow), C.c_int, C.c_void_p, C.c_void_p, C.c_char_p, C.c_int,
+                                    C.c_int, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_double),
+                                    C.POINTER(C.c_double), C.c_char_p, C.c_int]
+    rc = L.ref_window_run_ex(C.byref(cw), n, ptrs, lens, tmp.encode(), threads, int(shared_cache),
+                             2 if artifacts else int(want_json), C.byref(out), C.byref(tb), C.byref(td), err, 1024)
     if rc != 0:
         raise RefError(err.value.decode())
     return _take_json(out), tb.value, td.value

@@ -295,7 +295,18 @@ LoadedBundle to_bundle(const stg_window& w, const fs::path& dir) {
 // The reference build_group_data with its per-rank CPU loop (bundle.cpp:289-300)
 // fanned out over threads.  Every call is a reference function; the merge keeps
 // build_group_data's map semantics, so the GroupData is identical.
-GroupData build_group_data_threads(const LoadedBundle& bundle, int threads) {
+//
+// shared_cache = true replaces to_folded's per-record symbolization
+// (resolve_stack builds a fresh SymbolFile cache for every record, so a
+// 1M-entry table is re-parsed per record, symrepo.cpp:99-120) by the
+// reference's own resolve_stacks over all records of the rank (one cache per
+// call, symrepo.cpp:122-143) followed by fold_symbolized (folded.cpp:73-81).
+// That is the same std::map merge of the same resolved names (add_window,
+// folded.cpp:21-29, reverses each record to root-first and sums its count into
+// the map; fold_symbolized does exactly that), so the folded profile is
+// identical — it only makes C2-shaped windows (1M-symbol tables, nearly one
+// record per sample) finish in seconds instead of hours.
+GroupData build_group_data_threads(const LoadedBundle& bundle, int threads, bool shared_cache = false) {
     GroupData data;
     {
         // Everything except the CPU loop: run the reference itself on a bundle
@@ -326,7 +337,23 @@ GroupData build_group_data_threads(const LoadedBundle& bundle, int threads) {
                 if (in_window.empty()) continue;
                 auto windows = aggregate_samples(
                     in_window, bundle.window_end_ns - bundle.window_start_ns + 2 * bundle.max_skew_ns);
-                out[i] = to_folded(windows, repo, SymbolFile::LookupMode::ExactRange);
+                if (!shared_cache) {
+                    out[i] = to_folded(windows, repo, SymbolFile::LookupMode::ExactRange);
+                    continue;
+                }
+                std::vector<std::vector<FrameRef>> stacks;
+                std::vector<uint64_t> counts;
+                for (const ProfileWindow& pw : windows)
+                    for (const auto& rec : pw.records) {
+                        stacks.push_back(rec.frames);
+                        counts.push_back(rec.count);
+                    }
+                auto names = resolve_stacks(stacks, repo, SymbolFile::LookupMode::ExactRange);
+                std::vector<std::pair<std::vector<std::string>, uint64_t>> sym;
+                sym.reserve(names.size());
+                for (size_t k = 0; k < names.size(); ++k) sym.emplace_back(std::move(names[k]), counts[k]);
+                if (sym.empty()) throw Error("empty profile window");
+                out[i] = fold_symbolized(sym);
             }
         } catch (const std::exception& e) {
             errors[size_t(tid)] = e.what();
@@ -517,16 +544,19 @@ int ref_bundle_run(const char* dir, int want_json, char** out_json, double* t_lo
 // build_group_data + diagnose on the reference.  threads <= 1 runs the
 // reference build_group_data as-is (single-threaded, the reference's only
 // mode); threads > 1 uses the rank-parallel harness above.
-int ref_window_run(const stg_window* w, int n_symr, const uint8_t* const* symr,
-                   const uint64_t* symr_len, const char* tmpdir, int threads,
-                   int want_json, char** out_json, double* t_build, double* t_diag,
-                   char* err, int errcap) {
+// shared_cache = 1: the CPU loop symbolizes through resolve_stacks (see
+// build_group_data_threads) — same GroupData, C2-shaped windows feasible.
+int ref_window_run_ex(const stg_window* w, int n_symr, const uint8_t* const* symr,
+                      const uint64_t* symr_len, const char* tmpdir, int threads, int shared_cache,
+                      int want_json, char** out_json, double* t_build, double* t_diag,
+                      char* err, int errcap) {
     fs::path dir;
     try {
         dir = make_repo(tmpdir, n_symr, symr, symr_len);
         LoadedBundle b = to_bundle(*w, dir);
         auto t0 = std::chrono::steady_clock::now();
-        GroupData data = threads > 1 ? build_group_data_threads(b, threads) : build_group_data(b);
+        GroupData data = (threads > 1 || shared_cache) ? build_group_data_threads(b, std::max(threads, 1), shared_cache != 0)
+                                                       : build_group_data(b);
         auto t1 = std::chrono::steady_clock::now();
         DiagnosisReport rep = diagnose(data);
         auto t2 = std::chrono::steady_clock::now();
@@ -570,6 +600,14 @@ int ref_window_run(const stg_window* w, int n_symr, const uint8_t* const* symr,
         if (!dir.empty()) fs::remove_all(dir);
         return 1;
     }
+}
+
+int ref_window_run(const stg_window* w, int n_symr, const uint8_t* const* symr,
+                   const uint64_t* symr_len, const char* tmpdir, int threads,
+                   int want_json, char** out_json, double* t_build, double* t_diag,
+                   char* err, int errcap) {
+    return ref_window_run_ex(w, n_symr, symr, symr_len, tmpdir, threads, 0, want_json, out_json, t_build, t_diag,
+                             err, errcap);
 }
 
 // ---- single verbs, for unit parity ----------------------------------------

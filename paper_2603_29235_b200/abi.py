@@ -108,6 +108,8 @@ class StgConfig(C.Structure):
         ("os_migration_floor", C.c_int64),
         ("lookup_mode", C.c_int32),
         ("want_waterline", C.c_int32),
+        ("verify", C.c_int32),
+        ("debug_weak_prefix_key", C.c_int32),
     ]
 
 
@@ -134,6 +136,8 @@ class StgRunStats(C.Structure):
         ("agg_attempts", C.c_uint32),
         ("prefix_hits", C.c_uint64),
         ("prefix_misses", C.c_uint64),
+        ("verified", C.c_uint32),
+        ("verify_retries", C.c_uint32),
     ]
 
     def as_dict(self) -> dict:
@@ -159,6 +163,8 @@ def default_config() -> dict:
         os_migration_floor=100,
         lookup_mode=LOOKUP_EXACT_RANGE,
         want_waterline=0,
+        verify=0,
+        debug_weak_prefix_key=0,
     )
 
 

@@ -24,12 +24,13 @@ __device__ __forceinline__ uint64_t mix_b(uint64_t z) {
 }
 // Position-tagged terms of a root-first key sequence.  The fingerprint of a
 // sequence is (mix(Σ ta + len), mix(Σ tb + len)): order-sensitive because each
-// term carries its position, and two independent 64-bit halves.
-__device__ __forceinline__ uint64_t term_a(uint32_t key, uint32_t pos) {
-    return mix_a(((uint64_t(pos) << 32) | key) ^ 0x9e3779b97f4a7c15ull);
+// term carries its position, and two independent 64-bit halves.  salt keys the
+// terms (a verification retry re-keys every fingerprint; 0 by default).
+__device__ __forceinline__ uint64_t term_a(uint32_t key, uint32_t pos, uint64_t salt = 0) {
+    return mix_a(((uint64_t(pos) << 32) | key) ^ 0x9e3779b97f4a7c15ull ^ salt);
 }
-__device__ __forceinline__ uint64_t term_b(uint32_t key, uint32_t pos) {
-    return mix_b(((uint64_t(key) << 32) | pos) * 0xd6e8feb86659fd93ull + 0x632be59bd9b4e019ull);
+__device__ __forceinline__ uint64_t term_b(uint32_t key, uint32_t pos, uint64_t salt = 0) {
+    return mix_b((((uint64_t(key) << 32) | pos) ^ salt) * 0xd6e8feb86659fd93ull + 0x632be59bd9b4e019ull);
 }
 __device__ __forceinline__ void fp_finish(uint64_t ha, uint64_t hb, uint64_t len, uint64_t& fa,
                                           uint64_t& fb) {

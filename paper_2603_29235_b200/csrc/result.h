@@ -59,6 +59,7 @@ struct Result {
     uint32_t n_window_ranks = 0;
     int agg_attempts = 0;
     uint64_t pfx_hits = 0, pfx_misses = 0;
+    uint32_t verified = 0, verify_retries = 0;
     // name space: final rank -> string
     std::vector<uint64_t> unk_final;       // final rank of each distinct unknown label (sorted)
     std::vector<std::string> unk_labels;   // labels in the same order

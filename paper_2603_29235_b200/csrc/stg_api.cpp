@@ -191,6 +191,8 @@ void stg_config_default(stg_config* c) {
     c->os_migration_floor = 100;
     c->lookup_mode = STG_LOOKUP_EXACT_RANGE;
     c->want_waterline = 0;
+    c->verify = 0;
+    c->debug_weak_prefix_key = 0;
 }
 
 int stg_window_run(stg_ctx* ctx, const stg_window* win, const stg_config* cfg, stg_run_stats* stats) {

@@ -170,6 +170,12 @@ struct Ctx {
     bool ag_valid = false, ag_exact = false;
     uint64_t ag_windows = 0, ag_records = 0;
     uint64_t ag_cap_hint = 1u << 16;  // table slots the last call needed
+    // table-size hints carried from one window to the next (per context, so
+    // guarded by mu like everything else here)
+    std::vector<uint32_t> hint_rank_used;  // aggregation slots each rank used
+    uint32_t hint_pfx_misses = 0;          // prefix-cache misses (distinct raw chains)
+    uint32_t hint_unk_used = 0;            // distinct unresolved frames
+    uint32_t hint_gid = 0;                 // distinct fingerprints across ranks
     // distributed mode (stg_dist_init): one NCCL communicator per context
     void* comm = nullptr;  // ncclComm_t
     int world = 1, wrank = 0;

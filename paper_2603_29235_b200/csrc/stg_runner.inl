@@ -233,6 +233,8 @@ struct Runner {
         if (out[1] < 0) fail(STG_EINVAL, "negative rank ids are not supported");
         if (out[0] >= (1 << 24)) fail(STG_EINVAL, "rank ids must be below 2^24");
         span = out[0] + 1;
+    }
+    void rank_span_agree() {
         if (dist()) {  // every context must index ranks the same way
             int* d = dev<int>("dx_span", 1);
             STG_CUDA(cudaMemcpyAsync(d, &span, 4, cudaMemcpyHostToDevice, st));
@@ -647,13 +649,33 @@ struct Runner {
         int* d_unk_ovf = dev<int>("unk_ovf", 1);
         std::vector<uint64_t> tab_off(R);
         // prefix cache: ~4 slots per distinct raw chain of the previous window
-        uint32_t pfx_cap = uint32_t(std::min<uint64_t>(1u << 24, std::max<uint64_t>(1u << 16, next_pow2(4 * c_pfx_last() + 1))));
+        uint32_t pfx_cap = uint32_t(std::min<uint64_t>(1u << 24, std::max<uint64_t>(1u << 16, next_pow2(4 * c.hint_pfx_misses + 1))));
         PfxSlot* pfx = dev<PfxSlot>("pfx", pfx_cap);
         unsigned long long* d_stat = dev<unsigned long long>("sym_stat", 2);
         AggSlot* slots = nullptr;
         UnkSlot* unk = nullptr;
         std::vector<int> ovf(R);
         std::vector<unsigned> used(R);
+        uint64_t* d_toff = nullptr;
+        uint32_t* d_mask = nullptr;
+        // bins naming the same build id (verification compares unknown labels by identity)
+        std::vector<uint32_t> canon(std::max<int32_t>(w.n_bins, 1));
+        for (int32_t b = 0; b < w.n_bins; ++b) {
+            canon[size_t(b)] = uint32_t(b);
+            for (int32_t a = 0; a < b; ++a)
+                if (!std::memcmp(w.bin_build_ids + 20 * a, w.bin_build_ids + 20 * b, 20)) {
+                    canon[size_t(b)] = uint32_t(a);
+                    break;
+                }
+        }
+        const uint32_t* d_canon = cfg.verify ? up<uint32_t>("bin_canon", canon.data(), canon.size()) : nullptr;
+        res.verify_retries = 0;
+        res.verified = 0;
+        // Verification passes: pass 0 is the normal run; after a detected
+        // collision the stage re-runs with re-keyed fingerprints and without the
+        // prefix cache (stg_config.verify).
+        for (int pass = 0;; ++pass) {
+        AggParams p{};
         for (int attempt = 0;; ++attempt) {
             uint64_t tot = 0;
             for (int r = 0; r < R; ++r) {
@@ -662,10 +684,10 @@ struct Runner {
             }
             slots = dev<AggSlot>("slots", tot);
             zero(slots, tot * sizeof(AggSlot));
-            uint64_t* d_toff = up<uint64_t>("toff", tab_off.data(), R);
+            d_toff = up<uint64_t>("toff", tab_off.data(), R);
             std::vector<uint32_t> masks(R);
             for (int r = 0; r < R; ++r) masks[r] = caps[r] - 1;
-            uint32_t* d_mask = up<uint32_t>("tmask", masks.data(), R);
+            d_mask = up<uint32_t>("tmask", masks.data(), R);
             unk = dev<UnkSlot>("unk", unk_cap);
             zero(unk, size_t(unk_cap) * sizeof(UnkSlot));
             zero(d_nin, R * 8);
@@ -676,7 +698,7 @@ struct Runner {
             zero(d_ovf, R * 4);
             zero(d_unk_used, 4);
             zero(d_unk_ovf, 4);
-            AggParams p{};
+            p = AggParams{};
             p.ts = ts;
             p.foff = foff;
             p.pc = pc;
@@ -704,24 +726,19 @@ struct Runner {
             p.pfx = pfx;
             p.pfx_mask = pfx_cap - 1;
             p.stat = d_stat;
-            static const int order = std::getenv("STG_SYM_ORDER") ? std::atoi(std::getenv("STG_SYM_ORDER")) : 0;
-            p.order = order;
+            p.salt = pass ? 0x9e3779b97f4a7c15ull * uint64_t(pass) + 0x2545f4914f6cdd1dull : 0;
+            p.use_pfx = pass == 0;
+            p.weak_pfx = cfg.debug_weak_prefix_key != 0;
             zero(pfx, size_t(pfx_cap) * sizeof(PfxSlot));
             zero(d_stat, 16);
-            unsigned grid = unsigned(dev_sms) * 8;
-            uint64_t chunks = (n_s + 31) / 32;
-            uint64_t need = (chunks + (kThreads / 32) - 1) / (kThreads / 32);
+            // 4 resident CTAs of 8 warps per SM (64 registers), 4 waves' worth of CTAs
+            const uint64_t need = ((n_s + 31) / 32 + (kThreads / 32) - 1) / (kThreads / 32);
+            unsigned grid = unsigned(dev_sms) * 16;
             if (need < grid) grid = unsigned(std::max<uint64_t>(need, 1));
             cudaEventRecord(ev[2], st);
-            const bool smem_tabs = w.n_bins <= kMaxSmemBins;
-            // STG_SYM_MINB (experiments): 3 resident CTAs per SM (80 registers) instead of 4
-            static const int minb = std::getenv("STG_SYM_MINB") ? std::atoi(std::getenv("STG_SYM_MINB")) : 4;
-            grid = unsigned(dev_sms) * unsigned(minb) * 4;
-            if (need < grid) grid = unsigned(std::max<uint64_t>(need, 1));
-            if (attempt == 0) cudaEventRecord(ev_pre, st);
-            if (!smem_tabs) k_sym_agg<false, 4, 1><<<grid, kThreads, 0, st>>>(p);
-            else if (minb == 3) k_sym_agg<true, 3, 1><<<grid, kThreads, 0, st>>>(p);
-            else k_sym_agg<true, 4, 1><<<grid, kThreads, 0, st>>>(p);
+            if (attempt == 0 && pass == 0) cudaEventRecord(ev_pre, st);
+            if (w.n_bins <= kMaxSmemBins) k_sym_agg<true, 4, 1><<<grid, kThreads, 0, st>>>(p);
+            else k_sym_agg<false, 4, 1><<<grid, kThreads, 0, st>>>(p);
             STG_CUDA(cudaGetLastError());
             ++launches;
             cudaEventRecord(ev[3], st);
@@ -747,12 +764,14 @@ struct Runner {
             down(hm, d_stat, 2);
             res.pfx_hits = hm[0];
             res.pfx_misses = hm[1];
-            c_pfx_last() = uint32_t(std::min<unsigned long long>(hm[1], 1u << 22));
+            if (pass == 0) c.hint_pfx_misses = uint32_t(std::min<unsigned long long>(hm[1], 1u << 22));
         }
         if (get1(d_ebin)) fail(STG_EINVAL, "frame binary index out of range");
         h_n_in.resize(R);
         down(h_n_in.data(), d_nin, R);
-        // validation in aggregate_samples order (samples.cpp:32-58), ranks ascending
+        // validation in aggregate_samples order (samples.cpp:32-58), ranks ascending;
+        // a rank whose in-window samples all have empty stacks has no aggregated
+        // sample but still fails like the reference
         std::vector<unsigned long long> eempty(R), ereg(R, ~0ull);
         down(eempty.data(), d_eempty, R);
         std::vector<int> uns(R);
@@ -771,13 +790,18 @@ struct Runner {
         }
         int64_t drain = w.window_end_ns - w.window_start_ns + 2 * w.max_skew_ns;
         for (int r = 0; r < R; ++r) {
-            if (!h_n_in[r]) continue;
+            if (!h_n_in[r] && eempty[r] == ~0ull) continue;
+            fail_rank = w.rank_ids[r];
             if (drain <= 0) fail(STG_EINVAL, "drain interval must be positive");
             if (eempty[r] != ~0ull || ereg[r] != ~0ull) {
                 if (eempty[r] <= ereg[r]) fail(STG_EINVAL, "empty sample stack");
                 fail(STG_EINVAL, "aggregate_samples: timestamps regressed");
             }
         }
+        fail_rank = -1;
+        res.cpu_rank_ids.clear();
+        res.cpu_rank_index.clear();
+        res.cpu_totals.clear();
         for (int r = 0; r < R; ++r)
             if (h_n_in[r]) {
                 res.cpu_rank_ids.push_back(w.rank_ids[r]);
@@ -786,40 +810,51 @@ struct Runner {
             }
         d_totals = up<uint64_t>("totals", h_n_in.data(), R);
         mark("s:validate");
-        fold(slots, tab_off, caps, unk, unk_cap, d_rsoff, foff, pc, bin, d_tabs);
+        if (cfg.verify && !verify_aggregation(p, d_canon, tab_off[R - 1] + caps[R - 1])) {
+            if (pass >= 2) fail(STG_ECUDA, "verification failed after re-keyed retries");
+            ++res.verify_retries;
+            continue;
+        }
+        fold(slots, tab_off, caps, unk, unk_cap, d_rsoff, foff, pc, bin, d_tabs, d_canon);
+        if (cfg.verify && fold_bad) {
+            if (pass >= 2) fail(STG_ECUDA, "verification failed after re-keyed retries");
+            ++res.verify_retries;
+            continue;
+        }
+        res.verified = cfg.verify ? 1 : 0;
+        break;
+        }
     }
+
+    // stg_config.verify, stage a+b: every in-window sample against its slot's
+    // representative, slot counts recounted (k_sym_verify, k_count_check).
+    bool verify_aggregation(const AggParams& p, const uint32_t* d_canon, uint64_t n_slots) {
+        unsigned* vc = dev<unsigned>("v_count", n_slots);
+        zero(vc, n_slots * 4);
+        unsigned long long* bad = dev<unsigned long long>("v_bad", 1);
+        zero(bad, 8);
+        LAUNCH(k_sym_verify, 148 * 8, kThreads, p, d_canon, vc, bad);
+        LAUNCH(k_count_check, grid_for(n_slots), kThreads, n_slots, p.slots, vc, bad);
+        const bool ok = get1(bad) == 0;
+        mark("s:verify");
+        return ok;
+    }
+    bool fold_bad = false;
+    int32_t fail_rank = -1;  // rank whose validation failed (distributed error agreement)
 
     // table-capacity hints kept on the context between windows
     uint64_t c_cap_hint(int r, uint64_t nr) {
-        auto& v = c_hints();
+        const auto& v = c.hint_rank_used;
         uint64_t base = std::min<uint64_t>(2 * nr + 2, 1u << 15);
         if (size_t(r) < v.size() && v[size_t(r)]) base = std::min<uint64_t>(2 * nr + 2, uint64_t(v[size_t(r)]) * 2 + 64);
         return base;
     }
     uint64_t c_unk_hint() {
-        auto& v = c_hints();
-        return v.empty() ? 4096 : uint64_t(c_unk_last()) * 2 + 1024;
-    }
-    std::vector<uint32_t>& c_hints() {
-        static std::map<Ctx*, std::vector<uint32_t>> m;
-        return m[&c];
-    }
-    uint32_t& c_pfx_last() {
-        static std::map<Ctx*, uint32_t> m;
-        return m[&c];
-    }
-    uint32_t& c_unk_last() {
-        static std::map<Ctx*, uint32_t> m;
-        return m[&c];
-    }
-    uint32_t& c_gid_last() {
-        static std::map<Ctx*, uint32_t> m;
-        return m[&c];
+        return c.hint_rank_used.empty() ? 4096 : uint64_t(c.hint_unk_used) * 2 + 1024;
     }
     void c_set_hints(const std::vector<unsigned>& used, unsigned unk_used) {
-        auto& v = c_hints();
-        v.assign(used.begin(), used.end());
-        c_unk_last() = unk_used;
+        c.hint_rank_used.assign(used.begin(), used.end());
+        c.hint_unk_used = unk_used;
     }
 
     // Unknown labels (symfile.cpp:159-163) merged into the sorted name space.
@@ -865,8 +900,9 @@ struct Runner {
     // -------------------------------------------------------------- fold
     void fold(AggSlot* slots, const std::vector<uint64_t>& tab_off, const std::vector<uint32_t>& caps, UnkSlot* unk,
               uint32_t unk_cap, const uint64_t* d_rsoff, const uint64_t* foff, const uint64_t* pc,
-              const uint16_t* bin, const DevTable* d_tabs) {
+              const uint16_t* bin, const DevTable* d_tabs, const uint32_t* d_canon) {
         cudaEventRecord(ev[4], st);
+        fold_bad = false;
         uint64_t tot = 0;
         uint32_t maxcap = 0;
         for (int r = 0; r < R; ++r) {
@@ -902,7 +938,7 @@ struct Runner {
         uint32_t* l_gid = dev<uint32_t>("l_gid", L);
         uint64_t* seq_rep = dev<uint64_t>("seq_rep", L);
         const uint64_t scap_full = next_pow2(2 * L);
-        uint64_t scap = std::min<uint64_t>(scap_full, next_pow2(std::max<uint64_t>(4 * uint64_t(c_gid_last()) + 1024, 1u << 16)));
+        uint64_t scap = std::min<uint64_t>(scap_full, next_pow2(std::max<uint64_t>(4 * uint64_t(c.hint_gid) + 1024, 1u << 16)));
         uint32_t G = 0;
         for (;;) {
             SeqSlot* sslots = dev<SeqSlot>("sslots", scap);
@@ -916,7 +952,7 @@ struct Runner {
             if (scap >= scap_full) fail(STG_ENOMEM, "sequence table overflow");
             scap = scap_full;
         }
-        c_gid_last() = G;
+        c.hint_gid = G;
         res.n_gid = G;
         mark("f:dedupe");
         // materialize
@@ -933,6 +969,17 @@ struct Runner {
         UnkSet us{unk, unk_cap - 1, unk_cap - 1, d_unk_used, d_unk_ovf};
         LAUNCH(k_seq_materialize, grid_for(uint64_t(G) * 32), kThreads, G, seq_rep, d_seq_off, foff, pc, bin, d_tabs,
                uint32_t(w.n_bins), cfg.lookup_mode, us, d_ebin, d_arena);
+        if (cfg.verify) {  // every line's stack against its sequence representative
+            unsigned long long* bad = dev<unsigned long long>("v_bad", 1);
+            zero(bad, 8);
+            LAUNCH(k_line_verify, 148 * 8, kThreads, L, l_rep, l_gid, seq_rep, foff, pc, bin, d_tabs, uint32_t(w.n_bins),
+                   cfg.lookup_mode, us, d_ebin, d_canon, bad);
+            if (get1(bad)) {
+                fold_bad = true;
+                return;
+            }
+            mark("f:verify");
+        }
         // unknown labels -> merged name space
         uint32_t* u_slot = dev<uint32_t>("u_slot", unk_cap);
         uint32_t* u_bin = dev<uint32_t>("u_bin", unk_cap);
@@ -1077,9 +1124,7 @@ struct Runner {
         STG_CUDA(cudaStreamWaitEvent(c.side, ev_pre, 0));
         {
             cudaStream_t keep = st;
-            // STG_INCL_MAIN=1 (experiments): keep the counts on the main stream
-            static const bool incl_main = std::getenv("STG_INCL_MAIN") != nullptr;
-            if (!incl_main) st = c.side;
+            st = c.side;
             if (F * sizeof(unsigned) <= 160 * 1024) {
                 const size_t sm = F * sizeof(unsigned);
                 if (sm > 48 * 1024)
@@ -1953,6 +1998,51 @@ struct Runner {
         res.waterline_json.clear();  // rendered on request (waterline_json())
     }
 
+    // Distributed error agreement.  Input errors found on one context's shard
+    // (an empty stack, a timestamp regression, ...) must not leave the other
+    // contexts waiting in the next collective: every context runs the local
+    // stage, then all agree on the first failure in reference order — stage
+    // (collectives, then the CPU rank loop, then the GPU/OS loops of
+    // build_group_data, bundle.cpp:252-324), then the lowest failing rank —
+    // and all throw the owner's exact error.
+    int err_stage = 0;
+    template <class F>
+    void agreed(F&& f) {
+        if (!dist()) {
+            f();
+            return;
+        }
+        long long key = LLONG_MAX;
+        int code = STG_OK;
+        std::string msg;
+        try {
+            f();
+        } catch (const Error& e) {
+            code = e.code;
+            msg = e.what();
+        } catch (const std::exception& e) {
+            code = STG_ENOMEM;
+            msg = e.what();
+        }
+        if (code != STG_OK)
+            key = ((long long)err_stage << 48) | ((long long)(fail_rank + 1) << 8) | (long long)c.wrank;
+        long long* d = dev<long long>("dx_err", 1);
+        STG_CUDA(cudaMemcpyAsync(d, &key, 8, cudaMemcpyHostToDevice, st));
+        nccl(ncclAllReduce(d, d, 1, ncclInt64, ncclMin, comm(), st));
+        key = get1(d);
+        if (key == LLONG_MAX) return;
+        const int owner = int(key & 0xff);
+        std::vector<uint8_t> b;
+        if (c.wrank == owner) {
+            put<int32_t>(b, code);
+            put_str(b, msg);
+        }
+        b = bcast_bytes(std::move(b), owner);
+        const uint8_t* q = b.data();
+        const int32_t oc = get<int32_t>(q);
+        fail(oc, get_str(q));
+    }
+
     // STG_TRACE=1: host wall time per stage on stderr
     bool trace = std::getenv("STG_TRACE") != nullptr;
     std::chrono::steady_clock::time_point t_last = std::chrono::steady_clock::now();
@@ -1977,13 +2067,19 @@ struct Runner {
         res.has_baseline_iteration = true;
         res.baseline_iteration_ms = w.has_baseline_iteration ? w.baseline_iteration_ms : 0.0;
         cudaEventRecord(ev[0], st);
-        rank_space();
+        agreed([&] { rank_space(); });
+        rank_span_agree();
         mark("rank_space");
-        collectives();
-        cudaEventRecord(ev[1], st);
-        mark("collectives");
-        samples();  // runs gpu_os() on the side stream while k_sym_agg streams
-        if (!gpu_os_done) gpu_os();
+        agreed([&] {
+            err_stage = 0;
+            collectives();
+            cudaEventRecord(ev[1], st);
+            mark("collectives");
+            err_stage = 1;
+            samples();  // runs gpu_os() on the side stream while k_sym_agg streams
+            err_stage = 2;
+            if (!gpu_os_done) gpu_os();
+        });
         mark("samples+fold");
         if (ev_unset_fold()) {
             cudaEventRecord(ev[2], st);
@@ -2025,6 +2121,8 @@ struct Runner {
         s.agg_attempts = uint32_t(res.agg_attempts);
         s.prefix_hits = res.pfx_hits;
         s.prefix_misses = res.pfx_misses;
+        s.verified = res.verified;
+        s.verify_retries = res.verify_retries;
         mark("stats");
     }
     bool ev_unset_fold() const { return R == 0 || L == 0; }

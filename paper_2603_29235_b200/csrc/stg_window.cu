@@ -684,7 +684,9 @@ struct AggParams {
     unsigned long long* stat;    // [0] prefix hits, [1] misses
     uint64_t n_samples;
     uint64_t n_frames;
-    int order;                   // 0: contiguous batch ranges per warp, 1: grid-stride
+    uint64_t salt;               // fingerprint key of this attempt (0 = default)
+    int use_pfx;                 // 0: no prefix cache (verification retry)
+    int weak_pfx;                // tests: 4-bit prefix-cache keys (forced collisions)
 };
 
 // atom.global.cas.b128 against an empty (0, 0) key: returns the previous key.
@@ -734,33 +736,26 @@ __device__ __forceinline__ void agg_insert(AggSlot* T, uint32_t mask, uint64_t f
     *overflow = 1;
 }
 
-// Raw (unsymbolized) term of a non-leaf frame (bin, pc, leaf-first position):
-// one strong 64-bit mix per frame; the chain fingerprint is (Σ t, Σ rotr(t, 29)),
-// two sums that no single multiset identity makes equal for distinct chains.
-__device__ __forceinline__ uint64_t raw_t(uint64_t pc, uint32_t bin, uint32_t pos) {
-    return mix_a(pc ^ (uint64_t(bin | (pos << 16)) << 32) ^ 0x3c6ef372fe94f82bull);
-}
-__device__ __forceinline__ void raw_add(uint64_t& ha, uint64_t& hb, uint64_t t) {
-    ha += t;
-    hb += (t >> 29) | (t << 35);
-}
-
 // Raw-chain fingerprint, block form.  Frames are taken in aligned blocks of 8
 // (the vector loads' granularity); a block contributes five 64x64->128-bit
 // products — four over pc pairs, one over the packed bins — each operand
-// xor-keyed by its slot and the block's position q, and the sum of the low
-// and high halves is the 128-bit fingerprint (ha, hb).  A single changed frame
-// always changes the exact product, so (ha, hb) with the sample's alignment
-// and depth mixed in at the end is a cache key; frames outside the sample's
-// non-leaf range are zeroed, so the key depends on the chain, its depth and
-// f0 mod 8 only.  ~9 instructions per frame instead of one 64-bit mix each.
+// xor-keyed by its slot, the block's position q and the run's salt.  Each
+// product also adds its operands linearly (the other half gets the partner), so
+// no operand value annihilates its partner: with y fixed, x -> (x*y + y,
+// mulhi(x, y) + x) changes whenever x does (for y = 0 the high half still
+// moves by x), and symmetrically for y.  The sums (ha, hb) with the sample's
+// alignment and depth mixed in at the end are the prefix-cache key; frames
+// outside the sample's non-leaf range are zeroed, so the key depends on the
+// chain, its depth and f0 mod 8 only.  A run with verification on re-checks
+// every sample against a direct symbolization and retries with a new salt and
+// no cache on a mismatch (Runner::samples).
 __device__ __forceinline__ void mum_acc(uint64_t x, uint64_t y, uint64_t& ha, uint64_t& hb) {
-    ha += x * y;
-    hb += __umul64hi(x, y);
+    ha += x * y + y;
+    hb += __umul64hi(x, y) + x;
 }
 __device__ __forceinline__ void raw_block(const uint64_t (&pc)[8], uint64_t b01, uint64_t b23, uint64_t q,
-                                          uint64_t& ha, uint64_t& hb) {
-    const uint64_t B = (q + 1) * 0x9e3779b97f4a7c15ull;
+                                          uint64_t salt, uint64_t& ha, uint64_t& hb) {
+    const uint64_t B = ((q + 1) * 0x9e3779b97f4a7c15ull) ^ salt;
     mum_acc(pc[0] ^ B ^ 0x243f6a8885a308d3ull, pc[1] ^ B ^ 0x13198a2e03707344ull, ha, hb);
     mum_acc(pc[2] ^ B ^ 0xa4093822299f31d0ull, pc[3] ^ B ^ 0x082efa98ec4e6c89ull, ha, hb);
     mum_acc(pc[4] ^ B ^ 0x452821e638d01377ull, pc[5] ^ B ^ 0xbe5466cf34e90c6cull, ha, hb);
@@ -855,14 +850,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
     const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
     const uint64_t n_batches = (p.n_samples + 31) / 32;
     unsigned hits = 0, misses = 0;  // lane 0's per-warp tallies (< 2^32 per warp)
-    // batch order: contiguous ranges per warp, or grid-stride (p.order = 1: at
-    // any moment the grid works on ~one rank, whose aggregation table stays in
-    // L2).  Either way a warp's rank only moves forward, so it advances by
-    // compares instead of a search per batch.
+    // batch order: contiguous ranges per warp, so a warp's rank only moves
+    // forward and advances by compares instead of a search per batch
     const uint64_t per = (n_batches + nwarps - 1) / nwarps;
-    const uint64_t b_begin = p.order ? warp : warp * per;
-    const uint64_t b_end = p.order ? n_batches : (b_begin + per < n_batches ? b_begin + per : n_batches);
-    const uint64_t b_step = p.order ? nwarps : 1;
+    const uint64_t b_begin = warp * per;
+    const uint64_t b_end = b_begin + per < n_batches ? b_begin + per : n_batches;
+    const uint64_t b_step = 1;
     int r_cur = 0;
     if (b_begin < b_end) {
         const uint64_t q = b_begin * 32;
@@ -937,7 +930,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
                         bq[u] = make_uint4(bw[0], bw[1], bw[2], bw[3]);
                     }
                     raw_block(pcs[u], uint64_t(bq[u].x) | (uint64_t(bq[u].y) << 32),
-                              uint64_t(bq[u].z) | (uint64_t(bq[u].w) << 32), (bb - a0) >> 3, ha, hb);
+                              uint64_t(bq[u].z) | (uint64_t(bq[u].w) << 32), (bb - a0) >> 3, p.salt, ha, hb);
                 }
             }
         }
@@ -947,8 +940,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
         uint64_t my_rb = mix_b(hb + shape);
         if (my_ra == 0) my_ra = 1;
         if (my_rb == 0) my_rb = 1;
+        if (p.weak_pfx) {  // tests only (stg_config.debug_weak_prefix_key)
+            my_ra = 1 + (my_ra & 3);
+            my_rb = 1 + (my_rb & 3);
+        }
         // ---------------- phase 2: per-lane cache probe overlapped with the leaf lookup
-        const bool want_pfx = inwin && depth > 1;
+        const bool want_pfx = inwin && depth > 1 && p.use_pfx;
         // issue the first probe of both structures before either resolves
         const uint32_t pslot = uint32_t(my_rb >> 24) & p.pfx_mask;
         ulonglong2 pa = make_ulonglong2(0, 0), pb = make_ulonglong2(0, 0);
@@ -978,7 +975,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
             }
         }
         uint64_t ta = 0, tb = 0;
-        bool hit = !want_pfx;
+        bool hit = !(inwin && depth > 1);
         if (want_pfx) {
             uint32_t slot = pslot;
             for (int probe = 0; probe < 16; ++probe) {
@@ -1011,7 +1008,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
             }
         }
         if (inwin && leaf_key == kUnknownBit) leaf_key = kUnknownBit | unk_get(p.unk, leaf_bin, leaf_pc);
-        unsigned miss = __ballot_sync(0xffffffffu, want_pfx && !hit);
+        unsigned miss = __ballot_sync(0xffffffffu, !hit);
         hits += __popc(need & ~miss) * (lane == 0);
         misses += __popc(miss) * (lane == 0);
         while (miss) {
@@ -1024,8 +1021,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
             for (uint64_t j = a0 + 1 + lane; j < a1; j += 32) {
                 uint32_t key = resolve_frame(tabs, p.n_bins, p.pc[j], p.bin[j], p.mode, p.unk, p.err_bin);
                 uint32_t pos = uint32_t(d - 1 - (j - a0));  // root-first position
-                xa += term_a(key, pos);
-                xb += term_b(key, pos);
+                xa += term_a(key, pos, p.salt);
+                xb += term_b(key, pos, p.salt);
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
@@ -1035,13 +1032,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
             if (lane == src) {
                 ta = xa;
                 tb = xb;
-                pfx_put(p.pfx, p.pfx_mask, my_ra, my_rb, ta, tb);
+                if (p.use_pfx) pfx_put(p.pfx, p.pfx_mask, my_ra, my_rb, ta, tb);
             }
         }
         uint64_t fa = 0, fb = 0;
         if (inwin) {
-            ta += term_a(leaf_key, depth - 1);
-            tb += term_b(leaf_key, depth - 1);
+            ta += term_a(leaf_key, depth - 1, p.salt);
+            tb += term_b(leaf_key, depth - 1, p.salt);
             fp_finish(ta, tb, depth, fa, fb);
         }
         // ---------------- aggregate: identical (rank, stack) in the batch combine
@@ -1059,6 +1056,120 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
     if (lane == 0 && (hits | misses)) {
         atomicAdd(p.stat, (unsigned long long)hits);
         atomicAdd(p.stat + 1, (unsigned long long)misses);
+    }
+}
+
+// ------------------------------------------------------------ verification
+// stg_config.verify: the full compare of aggregate_samples (samples.cpp:67-76)
+// for the fused kernel.  One warp per sample: the sample is symbolized again
+// frame by frame (no prefix cache), its sequence fingerprint recomputed and
+// looked up in its rank's table (read-only, the insert's probe order), and its
+// names compared one by one with the slot's representative sample; each
+// sample then adds 1 to its slot's recount.  Any miss or difference (a
+// fingerprint collision somewhere) is counted in *bad.
+__device__ __forceinline__ bool same_frame(uint32_t a, uint32_t b, const UnkSlot* unk, const uint32_t* bin_canon) {
+    if (a == b) return true;
+    if (!(a & b & kUnknownBit)) return false;  // real names: equal keys <=> equal names
+    // two unknown slots name the same label iff (build id, offset) agree
+    const UnkSlot x = unk[a & ~kUnknownBit], y = unk[b & ~kUnknownBit];
+    return x.pc == y.pc && bin_canon[x.bin1 - 1] == bin_canon[y.bin1 - 1];
+}
+__global__ void k_sym_verify(AggParams p, const uint32_t* bin_canon, unsigned* vcount, unsigned long long* bad) {
+    __shared__ DevTable s_tabs[kMaxSmemBins];
+    for (uint32_t i = threadIdx.x; i < p.n_bins && i < kMaxSmemBins; i += blockDim.x) s_tabs[i] = p.tabs[i];
+    __syncthreads();
+    const DevTable* tabs = p.n_bins <= kMaxSmemBins ? s_tabs : p.tabs;
+    const int lane = threadIdx.x & 31;
+    const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    unsigned long long n_bad = 0;
+    for (uint64_t i = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; i < p.n_samples; i += nw) {
+        int lo = 0, hi = p.R - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (p.rank_soff[mid] <= i) lo = mid; else hi = mid - 1;
+        }
+        const int r = lo;
+        const uint64_t f0 = p.foff[i], f1 = p.foff[i + 1];
+        if (!p.active[r] || p.ts[i] - p.rank_clk[r] < p.ws || f1 == f0) continue;
+        const uint64_t d = f1 - f0;
+        uint64_t xa = 0, xb = 0;
+        for (uint64_t pos = lane; pos < d; pos += 32) {
+            const uint64_t j = f1 - 1 - pos;
+            const uint32_t key = resolve_frame(tabs, p.n_bins, p.pc[j], p.bin[j], p.mode, p.unk, p.err_bin);
+            xa += term_a(key, uint32_t(pos), p.salt);
+            xb += term_b(key, uint32_t(pos), p.salt);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            xa += __shfl_xor_sync(0xffffffffu, xa, o);
+            xb += __shfl_xor_sync(0xffffffffu, xb, o);
+        }
+        uint64_t fa, fb;
+        fp_finish(xa, xb, d, fa, fb);
+        const AggSlot* T = p.slots + p.tab_off[r];
+        const uint32_t mask = p.tab_mask[r];
+        uint32_t k = uint32_t(fb >> 20) & mask;
+        bool found = false;
+        for (uint32_t probe = 0; probe <= mask && probe < kMaxProbe; ++probe) {
+            const ulonglong2 cur = *reinterpret_cast<const ulonglong2*>(T + k);
+            if ((cur.x | cur.y) == 0) break;
+            if (cur.x == fa && cur.y == fb) {
+                found = true;
+                break;
+            }
+            k = (k + 1) & mask;
+        }
+        bool ok = found;
+        if (found) {
+            const uint64_t rep = p.rank_soff[r] + T[k].rep;
+            const uint64_t g0 = p.foff[rep], g1 = p.foff[rep + 1];
+            ok = g1 - g0 == d;
+            for (uint64_t pos = lane; ok && pos < d; pos += 32) {
+                const uint32_t a = resolve_frame(tabs, p.n_bins, p.pc[f1 - 1 - pos], p.bin[f1 - 1 - pos], p.mode,
+                                                 p.unk, p.err_bin);
+                const uint32_t b = resolve_frame(tabs, p.n_bins, p.pc[g1 - 1 - pos], p.bin[g1 - 1 - pos], p.mode,
+                                                 p.unk, p.err_bin);
+                if (!same_frame(a, b, p.unk.slots, bin_canon)) ok = false;
+            }
+            ok = __all_sync(0xffffffffu, ok);
+            if (lane == 0) atomicAdd(vcount + p.tab_off[r] + k, 1u);
+        }
+        if (!ok) ++n_bad;
+    }
+    if (lane == 0 && n_bad) atomicAdd(bad, n_bad);
+}
+
+// Every slot's recount must equal its count (no sample lost or double counted).
+__global__ void k_count_check(uint64_t n_slots, const AggSlot* slots, const unsigned* vcount, unsigned long long* bad) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n_slots; i += uint64_t(gridDim.x) * blockDim.x)
+        if ((slots[i].hi | slots[i].lo) != 0 && slots[i].count != vcount[i]) atomicAdd(bad, 1ull);
+}
+
+// Cross-rank sequence dedupe (k_seq_dedupe merges lines on the 128-bit
+// fingerprint): every line's representative must spell the same names as its
+// sequence's representative.  Warp per line.
+__global__ void k_line_verify(uint64_t L, const uint64_t* l_rep, const uint32_t* l_gid, const uint64_t* seq_rep,
+                              const uint64_t* foff, const uint64_t* pc, const uint16_t* bin, const DevTable* tabs_g,
+                              uint32_t n_bins, int mode, UnkSet unk, int* err_bin, const uint32_t* bin_canon,
+                              unsigned long long* bad) {
+    __shared__ DevTable s_tabs[kMaxSmemBins];
+    for (uint32_t i = threadIdx.x; i < n_bins && i < kMaxSmemBins; i += blockDim.x) s_tabs[i] = tabs_g[i];
+    __syncthreads();
+    const DevTable* tabs = n_bins <= kMaxSmemBins ? s_tabs : tabs_g;
+    const int lane = threadIdx.x & 31;
+    const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t l = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; l < L; l += nw) {
+        const uint64_t a = l_rep[l], b = seq_rep[l_gid[l]];
+        if (a == b) continue;
+        const uint64_t a0 = foff[a], a1 = foff[a + 1], b0 = foff[b], b1 = foff[b + 1];
+        bool ok = a1 - a0 == b1 - b0;
+        for (uint64_t pos = lane; ok && pos < a1 - a0; pos += 32) {
+            const uint32_t x = resolve_frame(tabs, n_bins, pc[a1 - 1 - pos], bin[a1 - 1 - pos], mode, unk, err_bin);
+            const uint32_t y = resolve_frame(tabs, n_bins, pc[b1 - 1 - pos], bin[b1 - 1 - pos], mode, unk, err_bin);
+            if (!same_frame(x, y, unk.slots, bin_canon)) ok = false;
+        }
+        ok = __all_sync(0xffffffffu, ok);
+        if (!ok && lane == 0) atomicAdd(bad, 1ull);
     }
 }
 

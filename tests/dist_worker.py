@@ -28,8 +28,11 @@ def main():
     win = make_case(a.case)
     ctx = stg.Context(local)
     ctx.dist_init(world, rank, share_unique_id(dist, stg.Context.dist_unique_id, device="cuda"))
-    ctx.window_run(shard_window(win, world, rank), cfg={"want_waterline": 1})
-    out = {"report": ctx.report(), "groupdata": ctx.groupdata(), "waterline": ctx.waterline()}
+    try:
+        ctx.window_run(shard_window(win, world, rank), cfg={"want_waterline": 1})
+        out = {"report": ctx.report(), "groupdata": ctx.groupdata(), "waterline": ctx.waterline()}
+    except stg.StgError as e:  # every process must fail with the same error (no hang)
+        out = {"error": str(e)}
     Path(a.out, f"rank{rank}.json").write_text(json.dumps(out))
     dist.barrier()
     dist.destroy_process_group()

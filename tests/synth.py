@@ -329,3 +329,91 @@ def oracle_stream(ts, rank, off, pc, bn, ids: bytes):
         fr = tuple((bids[int(bn[f])], int(pc[f])) for f in range(int(off[i]), int(off[i + 1])))
         out.append((int(ts[i]), int(rank[i]) if rank is not None else 0, fr))
     return out
+
+
+# ------------------------------------------------------------------ C2 on the host
+_U = np.uint64
+
+
+def _h64(z):
+    """The bench generator's mixer (csrc/bench_gen.cu h64), vectorised over uint64."""
+    with np.errstate(over="ignore"):
+        z = z + _U(0x9e3779b97f4a7c15)
+        z = (z ^ (z >> _U(30))) * _U(0xbf58476d1ce4e5b9)
+        z = (z ^ (z >> _U(27))) * _U(0x94d049bb133111eb)
+        return z ^ (z >> _U(31))
+
+
+def c2_samples_host(seed: int, ranks: int, spr: int, depth: int, pool: int, zipf_cdf, tables, hot,
+                    soft_pc, slow_rank: int, soft_share: float, jit_per_million: int, period_ns: int, skew):
+    """numpy restatement of the C2 bench generator (csrc/bench_gen.cu k_gen), bit-identical to it, for
+    callers that must not load any repo library (bench.py --impl reference).  tables = [(starts, sizes)]
+    of the three binaries; returns (ts, frame_off, frame_pc, frame_bin) host arrays."""
+    n = ranks * spr
+    i = np.arange(n, dtype=_U)
+    r = (i // _U(spr)).astype(np.int64)
+    k = (i % _U(spr)).astype(np.int64)
+    with np.errstate(over="ignore"):
+        u = _h64(_U(seed) ^ (i * _U(0x2545f4914f6cdd1d)))
+        x = (u >> _U(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+        lo = np.searchsorted(np.asarray(zipf_cdf, np.float64), x, side="left").astype(np.int64)
+        lo = np.minimum(lo, pool - 1)
+        p = ((lo + r.astype(np.int64) * 7919) % pool).astype(np.uint64)
+        soft = (r == slow_rank) & ((_h64(u) >> _U(11)).astype(np.float64) * (1.0 / 9007199254740992.0) < soft_share)
+        jit = ~soft & ((_h64(u ^ _U(0x77)) % _U(1000000)) < _U(jit_per_million))
+        jit_pc = _U(0x7f0000000000) + (_h64(u ^ _U(0x99)) % _U(1000)) * _U(16)
+        skew = np.asarray(skew, np.int64)
+        ts = k * period_ns + (_h64(u ^ _U(0x55)) % _U(period_ns // 50 + 1)).astype(np.int64) + skew[r]
+        D = depth
+        pc = np.zeros((n, D), np.uint64)
+        bn = np.zeros((n, D), np.uint16)
+        a, b = D // 5, D - D // 5
+        for j in range(D):
+            q = D - 1 - j
+            bj = 0 if j < a else (1 if j < b else 2)
+            bits = (p & _U((1 << j) - 1)) if j < 16 else p
+            node = _h64(_U(seed) ^ _U(j << 40) ^ (bits << _U(1)) ^ _U(0 if j < 16 else 1))
+            f = (node % _U(hot[bj])).astype(np.uint64)
+            f = (f * _U(2654435761)) % _U(len(tables[bj][0]))
+            st = np.asarray(tables[bj][0], np.uint64)[f.astype(np.int64)]
+            sz = np.asarray(tables[bj][1], np.uint32)[f.astype(np.int64)].astype(np.uint64)
+            if j == D - 1:
+                off = _h64(u ^ _U(j)) % sz
+            elif j == D - 10:
+                off = np.where(soft, _h64(u ^ _U(j)) % sz, _h64(node ^ _U(0x1234)) % sz)
+            else:
+                off = _h64(node ^ _U(0x1234)) % sz
+            col = st + off
+            colb = np.full(n, bj, np.uint16)
+            if j >= D - 9:
+                col = np.where(soft, _U(int(soft_pc[j - (D - 9)])), col)
+                colb = np.where(soft, np.uint16(2), colb)
+            if j == D - 1:
+                col = np.where(jit, jit_pc, col)
+                colb = np.where(jit, np.uint16(3), colb)
+            pc[:, q] = col
+            bn[:, q] = colb
+    foff = (np.arange(n + 1, dtype=np.uint64) * _U(D))
+    return ts, foff, pc.reshape(-1), bn.reshape(-1)
+
+
+def with_empty_stacks(w: Window, rank_index: int, samples) -> Window:
+    """Copy of a host window with the listed samples (rank-relative indices, or
+    "all") of one rank stripped of every frame (an empty StackSample.frames)."""
+    import copy
+    out = copy.copy(w)
+    soff = np.asarray(w.rank_sample_off, np.uint64)
+    s0, s1 = int(soff[rank_index]), int(soff[rank_index + 1])
+    ks = range(s1 - s0) if samples == "all" else samples
+    foff = np.asarray(w.sample_frame_off, np.uint64).astype(np.int64)
+    keep = np.ones(int(foff[-1]), bool)
+    lens = np.diff(foff)
+    for k in ks:
+        s = s0 + k
+        keep[foff[s]:foff[s + 1]] = False
+        lens[s] = 0
+    out.frame_pc = np.asarray(w.frame_pc)[keep].copy()
+    out.frame_bin = np.asarray(w.frame_bin)[keep].copy()
+    out.sample_frame_off = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    out.n_frames_ = None
+    return out

@@ -101,3 +101,22 @@ def test_two_gpu_group_matches_reference(case):
     assert_close([f[1:] for f in got["functions"]], [f[1:] for f in wl["functions"]], 1e-6)
     from tests.compare import assert_flags_match
     assert_flags_match([f for o in outs for f in o["waterline"]["flags"]], wl["flags"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["err-empty-shard1", "err-empty-rank-shard1"])
+def test_two_gpu_input_error_agreed(case):
+    """An input error found only in the second GPU's shard: both processes fail
+    with the reference's message instead of one throwing while the other waits
+    in the next collective."""
+    import torch
+    from oracle import ref
+    from tests.dist_cases import make_case
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    with pytest.raises(ref.RefError) as e:
+        ref.window_run(make_case(case), want_json=False)
+    outs = _run_dist(case, 2)
+    assert [o.get("error") for o in outs] == [str(e.value)] * 2

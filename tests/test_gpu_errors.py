@@ -8,7 +8,7 @@ import pytest
 
 import paper_2603_29235_b200 as stg
 from oracle import ref, strata_oracle as so
-from tests.synth import pack_symr, build_id, small_window
+from tests.synth import pack_symr, build_id, small_window, with_empty_stacks
 
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")]
 
@@ -151,3 +151,17 @@ def test_ingest_key_mismatch_and_idempotence(ctx):
     assert ctx.ingest(p, claimed_id=build_id("k1")) is False  # AlreadyPresent
     with pytest.raises(stg.StgError, match="symbol file build id does not match ingest key"):
         ctx.ingest(pack_symr(build_id("k2"), [0x10], [4], ["a"]), claimed_id=build_id("k3"))
+
+
+def test_rank_with_only_empty_in_window_stacks(ctx):
+    """A rank whose in-window samples ALL have empty stacks aggregates nothing,
+    but the reference's aggregate_samples still throws on its first one."""
+    w = with_empty_stacks(_win(), 2, "all")
+    r, g = _both(ctx, w)
+    assert r == g == "empty sample stack"
+
+
+def test_empty_stack_in_last_rank(ctx):
+    w = with_empty_stacks(_win(), 3, [40])
+    r, g = _both(ctx, w)
+    assert r == g == "empty sample stack"

@@ -458,3 +458,45 @@ def test_lookup_matches_reference_probes():
         mine = [f.lookup_index(int(x), mode) for x in q]
         assert [(-1 if i is None else i) for i, _ in mine] == idx.tolist()
         assert [p for _, p in mine] == probes.tolist()
+
+
+@pytest.mark.skipif(not (Path(__file__).parent.parent / "oracle/_ref/libstrata_ref.so").exists(),
+                    reason="oracle/_ref not built")
+@pytest.mark.parametrize("seed", [3, 8])
+def test_shared_cache_harness_equals_to_folded(seed):
+    """The C2-scale parity tests symbolize the reference's records with its own
+    resolve_stacks + fold_symbolized (one table cache per rank) instead of
+    to_folded's per-record table reload: the GroupData and report must be
+    identical to the as-is build_group_data."""
+    from oracle import ref
+    from tests.synth import small_window
+    win = small_window(seed=seed, ranks=5, samples_per_rank=700, slow_rank=2, unknown_frac=0.05, extra_bins=1)
+    a, _, _ = ref.window_run(win)
+    b, _, _ = ref.window_run(win, threads=3, shared_cache=True)
+    assert a == b
+
+
+def test_c2_host_generator_shapes():
+    """tests/synth.c2_samples_host (the reference arm's numpy C2 generator):
+    shapes, per-rank time order, bins by level, the straggler's softirq leaf path."""
+    from tests.synth import SOFTIRQ, c2_samples_host
+    rng = np.random.default_rng(0)
+    nsym = 5000
+    tabs = []
+    for b in range(3):
+        sizes = rng.integers(16, 4096, nsym).astype(np.uint32)
+        starts = (0x10000 + np.concatenate([[0], np.cumsum(sizes.astype(np.uint64) + 8)[:-1]])).astype(np.uint64)
+        tabs.append((starts, sizes))
+    cdf = np.cumsum(np.arange(1, 101, dtype=np.float64) ** -1.1)
+    cdf /= cdf[-1]
+    soft = tabs[2][0][:9] + 4
+    ts, off, pc, bn = c2_samples_host(7, 3, 400, 64, 100, cdf, tabs, (nsym,) * 3, soft, 1, 0.3, 1000, 10_000,
+                                      np.array([5, -3, 0]))
+    assert len(ts) == 1200 and len(off) == 1201 and len(pc) == 1200 * 64 == len(bn)
+    assert all(np.all(np.diff(ts[r * 400:(r + 1) * 400]) > 0) for r in range(3))
+    b = bn.reshape(1200, 64)
+    assert set(np.unique(b[:, 63])) == {0} and set(np.unique(b[:, 30])) == {1}  # root python, middle libtorch
+    p = pc.reshape(1200, 64)
+    soft_rows = np.all(p[:, :9][:, ::-1] == soft[None, :], axis=1)
+    assert soft_rows[400:800].mean() > 0.15 and not soft_rows[:400].any() and not soft_rows[800:].any()
+    assert len(SOFTIRQ) == 9
