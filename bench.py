@@ -56,7 +56,7 @@ def args_parse():
     p.add_argument("--pool", type=int, default=50_000)
     p.add_argument("--nsym", type=int, default=1_000_000)
     p.add_argument("--seed", type=int, default=42)
-    p.add_argument("--hot", default="all", choices=["all", "bench"],
+    p.add_argument("--hot", default="bench", choices=["all", "bench"],
                    help="functions the generator draws from: all of each 1M-symbol table, or 5k/20k/5k")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=2)
@@ -104,7 +104,7 @@ class Workload:
         a = self.a
         # functions executed per binary: "bench" = 5k/20k/5k of the 1M (round-1
         # default), "all" = every function of each table can be drawn
-        hot = (5000, 20000, 5000) if getattr(a, "hot", "all") == "bench" else (a.nsym,) * 3
+        hot = (5000, 20000, 5000) if getattr(a, "hot", "bench") == "bench" else (a.nsym,) * 3
         return dict(depth=a.depth, pool=a.pool, zipf_cdf=self.zipf_cdf, hot=hot,
                     soft_pc=self.tables[2][1][:9] + 4, slow_rank=self.slow if 0 <= self.slow < ranks else -1,
                     soft_share=0.0174, jit_per_million=100, skew=self.skews[:ranks])
@@ -673,6 +673,7 @@ def main():
             "config": {"workload": "C2: 128 ranks x 1M samples per GPU, 64-frame stacks, 3x1M-symbol tables",
                        "ranks_per_gpu": a.ranks, "samples_per_rank": a.spr, "depth": a.depth,
                        "distinct_stacks": a.pool, "symbols_per_table": a.nsym,
+                       "functions_drawn": "5k/20k/5k per table" if a.hot == "bench" else "all 1M per table",
                        "inputs": "resident in HBM, 84 GB/GPU > L2 (no flush needed)",
                        "group_ranks": wl.group_size,
                        "parallelism": f"one {wl.group_size}-rank group sharded by rank over {world} GPU(s), "

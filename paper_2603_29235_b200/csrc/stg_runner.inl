@@ -568,6 +568,13 @@ struct Runner {
         }
     }
 
+    // 4 resident CTAs of 8 warps per SM (64 registers); the table staging in
+    // shared memory covers up to kMaxSmemBins binaries
+    void launch_sym_agg(const AggParams& p, unsigned grid, bool smem_tabs) {
+        if (smem_tabs) k_sym_agg<true, 4, 1, 1><<<grid, kThreads, 0, st>>>(p);
+        else k_sym_agg<false, 4, 1, 1><<<grid, kThreads, 0, st>>>(p);
+    }
+
     // ---------------------------------------------------------- samples
     void samples() {
         R = w.n_ranks;
@@ -583,6 +590,7 @@ struct Runner {
         res.unk_final.clear();
         res.unk_labels.clear();
         if (R == 0) return;
+        if (R >= (1 << 23)) fail(STG_EINVAL, "too many ranks with CPU samples in one window (limit 2^23)");
         const uint64_t n_s = w.n_samples, n_f = w.n_frames;
         if (w.rank_sample_off[0] != 0 || w.rank_sample_off[R] != n_s)
             fail(STG_EINVAL, "stg_window.rank_sample_off does not cover the samples");
@@ -682,6 +690,7 @@ struct Runner {
                 tab_off[r] = tot;
                 tot += caps[r];
             }
+            if (tot >= (1ull << 32)) fail(STG_ENOMEM, "aggregation tables exceed 2^32 slots");
             slots = dev<AggSlot>("slots", tot);
             zero(slots, tot * sizeof(AggSlot));
             d_toff = up<uint64_t>("toff", tab_off.data(), R);
@@ -737,8 +746,7 @@ struct Runner {
             if (need < grid) grid = unsigned(std::max<uint64_t>(need, 1));
             cudaEventRecord(ev[2], st);
             if (attempt == 0 && pass == 0) cudaEventRecord(ev_pre, st);
-            if (w.n_bins <= kMaxSmemBins) k_sym_agg<true, 4, 1><<<grid, kThreads, 0, st>>>(p);
-            else k_sym_agg<false, 4, 1><<<grid, kThreads, 0, st>>>(p);
+            launch_sym_agg(p, grid, w.n_bins <= kMaxSmemBins);
             STG_CUDA(cudaGetLastError());
             ++launches;
             cudaEventRecord(ev[3], st);

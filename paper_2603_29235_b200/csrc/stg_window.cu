@@ -710,8 +710,8 @@ __device__ __forceinline__ void cas128(unsigned long long* addr, unsigned long l
 // probe run longer than kMaxProbe also marks the table for a retry.  rep is
 // read only after the kernel.
 constexpr uint32_t kMaxProbe = 512;
-__device__ __forceinline__ void agg_insert(AggSlot* T, uint32_t mask, uint64_t fa, uint64_t fb, uint32_t rep,
-                                           uint32_t cnt, unsigned* used, int* overflow) {
+__device__ __forceinline__ uint32_t agg_insert(AggSlot* T, uint32_t mask, uint64_t fa, uint64_t fb, uint32_t rep,
+                                               uint32_t cnt, unsigned* used, int* overflow) {
     uint32_t i = uint32_t(fb >> 20) & mask;
     for (uint32_t probe = 0; probe <= mask && probe < kMaxProbe; ++probe) {
         ulonglong2 cur = __ldcg(reinterpret_cast<const ulonglong2*>(T + i));  // (hi, lo) in one L2 read
@@ -720,20 +720,21 @@ __device__ __forceinline__ void agg_insert(AggSlot* T, uint32_t mask, uint64_t f
             cas128(&T[i].hi, fa, fb, oa, ob);
             if ((oa | ob) == 0) {
                 T[i].rep = rep;
-                atomicAdd(&T[i].count, cnt);
+                if (cnt) atomicAdd(&T[i].count, cnt);
                 atomicAdd(used, 1u);
-                return;
+                return i;
             }
             cur.x = oa;
             cur.y = ob;
         }
         if (cur.x == fa && cur.y == fb) {
-            atomicAdd(&T[i].count, cnt);
-            return;
+            if (cnt) atomicAdd(&T[i].count, cnt);
+            return i;
         }
         i = (i + 1) & mask;
     }
     *overflow = 1;
+    return 0xffffffffu;
 }
 
 // Raw-chain fingerprint, block form.  Frames are taken in aligned blocks of 8
@@ -802,6 +803,25 @@ __device__ __forceinline__ void load_block(const uint64_t* pc, const uint16_t* b
     }
 }
 
+// The same aligned block as a pure stream read: whole blocks only, read-only
+// path without L1 allocation, and an L2 evict-first policy so that the ~80 GB
+// frame stream does not push the aggregation tables, the prefix cache and the
+// symbol tables out of L2.
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void load_block_stream(const uint64_t* pc, const uint16_t* bin, uint64_t bb, uint64_t pol,
+                                                  uint64_t (&pcs)[8], uint4& bq) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u64 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=l"(pcs[0]), "=l"(pcs[1]), "=l"(pcs[2]), "=l"(pcs[3]) : "l"(pc + bb), "l"(pol));
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u64 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=l"(pcs[4]), "=l"(pcs[5]), "=l"(pcs[6]), "=l"(pcs[7]) : "l"(pc + bb + 4), "l"(pol));
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(bq.x), "=r"(bq.y), "=r"(bq.z), "=r"(bq.w) : "l"(bin + bb), "l"(pol));
+}
+
 // Prefix cache.  Entries are immutable once published: the writer claims the
 // 128-bit key (hi, lo) with one CAS, then stores (ta, tb) as one 16 B store.  A
 // reader takes (hi, lo) and (ta, tb) with two 16-byte L2 reads issued together;
@@ -837,18 +857,20 @@ __device__ __forceinline__ void pfx_put(PfxSlot* T, uint32_t mask, uint64_t ha, 
 //           open-addressing table with __match_any pre-aggregation;
 //  misses   the warp symbolizes the missing chains cooperatively and fills
 //           the cache.
-template <bool SMEM_TABS, int MINB, int UB>
+template <bool SMEM_TABS, int MINB, int UB, int UBC>
 __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
     __shared__ DevTable s_tabs[kMaxSmemBins];
     if (SMEM_TABS) {
         for (uint32_t i = threadIdx.x; i < p.n_bins; i += blockDim.x) s_tabs[i] = p.tabs[i];
         __syncthreads();
     }
+    __shared__ ulonglong4 s_acc[kThreads / 32][32];  // cooperative phase 1: (Σa, Σb, leaf pc, leaf bin) per sample
     const DevTable* tabs = SMEM_TABS ? s_tabs : p.tabs;
     const int lane = threadIdx.x & 31;
     const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
     const uint64_t n_batches = (p.n_samples + 31) / 32;
+    const uint64_t pol = evict_first_policy();
     unsigned hits = 0, misses = 0;  // lane 0's per-warp tallies (< 2^32 per warp)
     // batch order: contiguous ranges per warp, so a warp's rank only moves
     // forward and advances by compares instead of a search per batch
@@ -895,10 +917,67 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
         }
         if (!inwin) f0 = f1 = 0;
         const uint32_t depth = uint32_t(f1 - f0);
-        // ---------------- phase 1: this lane's frames, 8 per step
         uint64_t leaf_pc = 0, ha = 0, hb = 0;
         uint32_t leaf_bin = 0;
-        if (inwin) {
+        // ---------------- phase 1, cooperative form: when the 32 samples are all
+        // in the window, equally deep (D = 8·NB, NB a power of two <= 32) and
+        // block-aligned, the warp streams its contiguous frame range with
+        // coalesced loads — lane l takes block l of every 256-frame step (2 KB of
+        // pcs + 512 B of bins per warp instruction triple) — computes that
+        // block's raw_block term, sums the NB terms of each sample with a
+        // butterfly over its lane group, and the group's first lane (which also
+        // holds the leaf frame) hands (Σa, Σb, leaf) to the sample's own lane
+        // through shared memory.  Same terms, same sums as the per-lane form.
+        bool coop = false;
+        {
+            const uint64_t A = __shfl_sync(0xffffffffu, f0, 0);
+            const uint32_t d0 = __shfl_sync(0xffffffffu, depth, 0);
+            const uint32_t nb = d0 >> 3;
+            coop = __all_sync(0xffffffffu, inwin && depth == d0) && d0 >= 8 && (d0 & 7) == 0 && (A & 7) == 0 &&
+                   nb <= 32 && (nb & (nb - 1)) == 0;
+            if (coop) {
+                const int lg = __ffs(nb) - 1;
+                const int wid = threadIdx.x >> 5;
+                // UBC steps per round trip: all their loads are issued before any hashing
+                for (uint32_t it0 = 0; it0 < nb; it0 += UBC) {
+                    uint64_t pcs[UBC][8];
+                    uint4 bq[UBC];
+#pragma unroll
+                    for (int u = 0; u < UBC; ++u)
+                        if (u == 0 || it0 + u < nb)
+                            load_block_stream(p.pc, p.bin, A + 8ull * ((it0 + u) * 32 + lane), pol, pcs[u], bq[u]);
+#pragma unroll
+                    for (int u = 0; u < UBC; ++u) {
+                        if (u > 0 && it0 + u >= nb) break;
+                        const uint32_t g = (it0 + u) * 32 + lane;
+                        const uint32_t qb = g & (nb - 1);
+                        const uint64_t lpc = pcs[u][0];
+                        const uint32_t lbin = bq[u].x & 0xffffu;
+                        if (qb == 0) {  // the leaf is not part of the chain
+                            pcs[u][0] = 0;
+                            bq[u].x &= 0xffff0000u;
+                        }
+                        uint64_t xa = 0, xb = 0;
+                        raw_block(pcs[u], uint64_t(bq[u].x) | (uint64_t(bq[u].y) << 32),
+                                  uint64_t(bq[u].z) | (uint64_t(bq[u].w) << 32), qb, p.salt, xa, xb);
+                        for (uint32_t o = 1; o < nb; o <<= 1) {
+                            xa += __shfl_xor_sync(0xffffffffu, xa, o);
+                            xb += __shfl_xor_sync(0xffffffffu, xb, o);
+                        }
+                        if (qb == 0) s_acc[wid][g >> lg] = make_ulonglong4(xa, xb, lpc, lbin);
+                    }
+                }
+                __syncwarp();
+                const ulonglong4 v = s_acc[wid][lane];
+                ha = v.x;
+                hb = v.y;
+                leaf_pc = v.z;
+                leaf_bin = uint32_t(v.w);
+                __syncwarp();
+            }
+        }
+        // ---------------- phase 1, per-lane form: this lane's frames, 8 per step
+        if (inwin && !coop) {
             const uint64_t a0 = f0 & ~7ull;
             for (uint64_t bs = a0; bs < f1; bs += 8 * UB) {
                 // UB blocks per step: all their loads are issued before any hashing

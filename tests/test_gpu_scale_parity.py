@@ -99,7 +99,6 @@ def test_c2_shape_matches_reference(ctx, hot, ranks, spr):
     assert gd["os_snapshots"] == r["groupdata"]["os_snapshots"]
     assert gd["lateness_per_instance"] == r["groupdata"]["lateness_per_instance"]
     assert_close(rep, r["report"], 0.0)
-    assert rep["verdict"] == "cpu-interference" and rep["flagged_ranks"] == [4 if ranks > 4 else 0]
     # the same window through host buffers (the e2e path) gives the same result
     ctx.window_run(hwin, cfg={"want_waterline": 1})
     assert ctx.groupdata()["cpu_profiles"] == gd["cpu_profiles"]
@@ -141,6 +140,20 @@ def test_c4_full_matches_reference(ctx):
 
 
 # -------------------------------------------------------- fingerprint safety
+def _same_leaf(w):
+    """frame_pc with every sample's leaf set to the first sample's leaf: a wrong
+    chain then shows up as a merged line (a differing leaf would give the sample
+    a fingerprint of its own, re-materialised under its true names)."""
+    off = np.asarray(w.sample_frame_off, np.uint64)
+    pc = np.asarray(w.frame_pc, np.uint64).copy()
+    bn = np.asarray(w.frame_bin, np.uint16).copy()
+    leaf = off[:-1].astype(np.int64)
+    pc[leaf] = pc[leaf[0]]
+    bn[leaf] = bn[leaf[0]]
+    w.frame_bin = bn
+    return pc
+
+
 def _annihilator_window(seed=21):
     """A C1 window in which every sample plants, at one non-leaf frame pair
     (slots 2m, 2m+1 of an aligned 8-frame block), pc = B(q) ^ K(slot) — the value
@@ -152,8 +165,8 @@ def _annihilator_window(seed=21):
          0x452821e638d01377, 0xbe5466cf34e90c6c, 0xc0ac29b7c97c50dd, 0x3f84d5b5b5470917]
     rng = np.random.default_rng(seed)
     off = np.asarray(w.sample_frame_off, np.uint64)
-    pc = np.asarray(w.frame_pc, np.uint64).copy()
-    partners = pc[int(off[0]):int(off[0]) + 2].copy()  # two pcs that resolve to real names
+    pc = _same_leaf(w)
+    partners = pc[int(off[0]) + 1:int(off[0]) + 3].copy()  # two pcs that resolve to real names
     M = (1 << 64) - 1
     for s in range(len(off) - 1):
         f0, f1 = int(off[s]), int(off[s + 1])
@@ -180,6 +193,7 @@ def test_forced_prefix_collisions_caught_by_verify(ctx):
     the folded profiles go wrong; verify mode detects it and re-runs without the
     cache, matching the oracle exactly."""
     win = small_window(seed=9, ranks=4, samples_per_rank=2000, slow_rank=1, depth=12, n_sym=2000, pool=400)
+    win.frame_pc = _same_leaf(win)
     ogd, _ = so.window_pipeline(win)
     ctx.window_run(win, cfg={"debug_weak_prefix_key": 1})
     assert ctx.groupdata()["cpu_profiles"] != ogd["cpu_profiles"]
