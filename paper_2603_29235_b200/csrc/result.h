@@ -60,6 +60,7 @@ struct Result {
     int agg_attempts = 0;
     uint64_t pfx_hits = 0, pfx_misses = 0;
     uint32_t verified = 0, verify_retries = 0;
+    uint64_t f_nd_bound = 1;  // bound on the (sequence, distinct name) pairs of the fold
     // name space: final rank -> string
     std::vector<uint64_t> unk_final;       // final rank of each distinct unknown label (sorted)
     std::vector<std::string> unk_labels;   // labels in the same order

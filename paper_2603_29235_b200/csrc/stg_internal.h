@@ -176,6 +176,9 @@ struct Ctx {
     uint32_t hint_pfx_misses = 0;          // prefix-cache misses (distinct raw chains)
     uint32_t hint_unk_used = 0;            // distinct unresolved frames
     uint32_t hint_gid = 0;                 // distinct fingerprints across ranks
+    // unknown label -> (position in the dictionary, equals a real name), for dict_version
+    std::unordered_map<std::string, std::pair<uint64_t, bool>> label_pos;
+    uint64_t label_pos_version = ~0ull;
     // distributed mode (stg_dist_init): one NCCL communicator per context
     void* comm = nullptr;  // ncclComm_t
     int world = 1, wrank = 0;

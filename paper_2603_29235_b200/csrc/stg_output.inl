@@ -45,18 +45,20 @@ void run_resolve(Ctx& c, Result& res, uint64_t n, const uint64_t* pc, const uint
                   UnkSet{unk, cap - 1, cap, used, ovf}, ebin, d_out);
     if (rn.get1(ebin)) fail(STG_EINVAL, "frame binary index out of range");
     if (rn.get1(ovf)) fail(STG_ENOMEM, "unknown-frame set overflow");
-    uint32_t* u_slot = rn.dev<uint32_t>("rv_uslot", cap);
-    uint32_t* u_bin = rn.dev<uint32_t>("rv_ubin", cap);
-    uint64_t* u_pc = rn.dev<uint64_t>("rv_upc", cap);
+    ulonglong2* u_rec = rn.dev<ulonglong2>("rv_urec", cap);
     unsigned* nu = rn.dev<unsigned>("rv_nu", 1);
     rn.zero(nu, 4);
-    LAUNCH(k_unk_compact, grid_for(cap), kThreads, cap, unk, u_slot, u_bin, u_pc, nu);
+    LAUNCH(k_unk_compact, grid_for(cap), kThreads, cap, unk, u_rec, nu);
     uint32_t NU = rn.get1(nu);
+    std::vector<ulonglong2> ur(NU);
+    rn.down(ur.data(), u_rec, NU);
     std::vector<uint32_t> hs(NU), hb(NU);
     std::vector<uint64_t> hp(NU);
-    rn.down(hs.data(), u_slot, NU);
-    rn.down(hb.data(), u_bin, NU);
-    rn.down(hp.data(), u_pc, NU);
+    for (uint32_t k = 0; k < NU; ++k) {
+        hp[k] = ur[k].x;
+        hs[k] = uint32_t(ur[k].y);
+        hb[k] = uint32_t(ur[k].y >> 32);
+    }
     rn.merge_labels(NU, hs, hb, hp, cap);
     if (n) {
         LAUNCH(k_remap, grid_for(n), kThreads, n, d_out, static_cast<const uint32_t*>(c.buf("u_final").p),

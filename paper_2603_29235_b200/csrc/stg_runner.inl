@@ -57,7 +57,7 @@ struct Runner {
     const stg_config& cfg;
     Result& res;
     cudaStream_t st;
-    uint32_t launches = 0;
+    uint32_t launches = 0, syncs = 0;
     uint64_t h2d = 0, d2h = 0;
     int32_t span = 0;
     // device state shared between stages
@@ -84,26 +84,17 @@ struct Runner {
     std::vector<uint32_t> h_dense_final;
     cudaEvent_t ev[8];
     cudaEvent_t ev_pre = nullptr;   // main-stream point a side-stream stage starts after
-    cudaEvent_t ev_incl = nullptr;  // inclusive counts done (side stream)
     bool gpu_os_done = false;
-    bool incl_pending = false;
     uint64_t max_seq_len = 0;
-    void wait_incl() {
-        if (!incl_pending) return;
-        STG_CUDA(cudaStreamWaitEvent(st, ev_incl, 0));
-        incl_pending = false;
-    }
 
     Runner(Ctx& c_, const stg_window& w_, const stg_config& cfg_, Result& r_)
         : c(c_), w(w_), cfg(cfg_), res(r_), st(c_.stream) {
         for (auto& e : ev) STG_CUDA(cudaEventCreate(&e));
         STG_CUDA(cudaEventCreateWithFlags(&ev_pre, cudaEventDisableTiming));
-        STG_CUDA(cudaEventCreateWithFlags(&ev_incl, cudaEventDisableTiming));
     }
     ~Runner() {
         for (auto& e : ev) cudaEventDestroy(e);
         cudaEventDestroy(ev_pre);
-        cudaEventDestroy(ev_incl);
     }
     // The GPU/OS layer sums (build_group_data bundle.cpp:302-320) do not depend on
     // the sample stream: they run on a side stream (ordered after everything the
@@ -143,6 +134,7 @@ struct Runner {
         STG_CUDA(cudaMemcpyAsync(host, d, n * sizeof(T), cudaMemcpyDeviceToHost, st));
         STG_CUDA(cudaStreamSynchronize(st));
         d2h += n * sizeof(T);
+        ++syncs;
     }
     template <class T>
     T get1(const T* d) {
@@ -874,6 +866,10 @@ struct Runner {
         const auto& dict = c.dict;
         res.dict = &c.dict;
         res.unk_final.clear();
+        if (c.label_pos_version != c.dict_version || c.label_pos.size() > (1u << 20)) {  // per dictionary, bounded
+            c.label_pos.clear();
+            c.label_pos_version = c.dict_version;
+        }
         res.unk_labels.clear();
         std::vector<std::pair<std::string, uint32_t>> labels(NU);
         for (uint32_t i = 0; i < NU; ++i) labels[i] = {unknown_label(w.bin_build_ids + 20 * hb[i], hp[i]), hs[i]};
@@ -887,8 +883,17 @@ struct Runner {
                 unk_final_by_slot[labels[i].second] = uint32_t(last_final);
                 continue;
             }
-            uint64_t pos = uint64_t(dict.lower_bound(lab));
-            bool eq = pos < dict.size() && dict[pos] == lab;
+            uint64_t pos;
+            bool eq;
+            auto ci = c.label_pos.find(lab);
+            if (ci != c.label_pos.end()) {
+                pos = ci->second.first;
+                eq = ci->second.second;
+            } else {
+                pos = uint64_t(dict.lower_bound(lab));
+                eq = pos < dict.size() && dict[pos] == lab;
+                c.label_pos.emplace(lab, std::make_pair(pos, eq));
+            }
             uint64_t fr = pos + ne_before;
             unk_final_by_slot[labels[i].second] = uint32_t(fr);
             last_final = fr;
@@ -941,22 +946,25 @@ struct Runner {
         // global dedupe -> sequence ids.  The table is sized from the previous
         // window's distinct count (lines repeat the same stacks across ranks), with a
         // retry at 2 slots per line if it fills up.
-        unsigned* nseq = dev<unsigned>("nseq", 1);
-        int* sovf = dev<int>("sovf", 1);
+        unsigned long long* dstat = dev<unsigned long long>("seq_stat", 3);
         uint32_t* l_gid = dev<uint32_t>("l_gid", L);
         uint64_t* seq_rep = dev<uint64_t>("seq_rep", L);
         const uint64_t scap_full = next_pow2(2 * L);
         uint64_t scap = std::min<uint64_t>(scap_full, next_pow2(std::max<uint64_t>(4 * uint64_t(c.hint_gid) + 1024, 1u << 16)));
         uint32_t G = 0;
+        uint64_t A = 0;
         for (;;) {
             SeqSlot* sslots = dev<SeqSlot>("sslots", scap);
             LAUNCH(k_fill_gid, grid_for(scap), kThreads, sslots, scap);  // clears the slots, gid = unpublished
-            zero(nseq, 4);
-            zero(sovf, 4);
-            LAUNCH(k_seq_dedupe, grid_for(L), kThreads, L, l_hi, l_lo, l_rep, sslots, scap - 1, nseq, l_gid, seq_rep,
-                   sovf);
-            G = get1(nseq);
-            if (!get1(sovf)) break;
+            zero(dstat, 24);
+            LAUNCH(k_seq_dedupe, grid_for(L), kThreads, L, l_hi, l_lo, l_rep, sslots, scap - 1, dstat, l_gid, seq_rep,
+                   foff);
+            unsigned long long hs3[3];
+            down(hs3, dstat, 3);
+            G = uint32_t(hs3[0]);
+            A = hs3[1];
+            max_seq_len = hs3[2];
+            if (!(hs3[0] >> 32)) break;
             if (scap >= scap_full) fail(STG_ENOMEM, "sequence table overflow");
             scap = scap_full;
         }
@@ -969,8 +977,7 @@ struct Runner {
         zero(seq_len + G, 8);
         d_seq_off = dev<uint64_t>("seq_off", G + 1);
         excl_sum(seq_len, d_seq_off, uint64_t(G) + 1);
-        uint64_t A = get1(d_seq_off + G);
-        d_arena = dev<uint32_t>("arena", A);
+        d_arena = dev<uint32_t>("arena", std::max<uint64_t>(A, 1));
         unsigned* d_unk_used = static_cast<unsigned*>(c.buf("unk_used").p);
         int* d_unk_ovf = static_cast<int*>(c.buf("unk_ovf").p);
         int* d_ebin = static_cast<int*>(c.buf("ebin").p);
@@ -989,19 +996,21 @@ struct Runner {
             mark("f:verify");
         }
         // unknown labels -> merged name space
-        uint32_t* u_slot = dev<uint32_t>("u_slot", unk_cap);
-        uint32_t* u_bin = dev<uint32_t>("u_bin", unk_cap);
-        uint64_t* u_pc = dev<uint64_t>("u_pc", unk_cap);
+        ulonglong2* u_rec = dev<ulonglong2>("u_rec", unk_cap);
         unsigned* nu = dev<unsigned>("nu", 1);
         zero(nu, 4);
-        LAUNCH(k_unk_compact, grid_for(unk_cap), kThreads, unk_cap, unk, u_slot, u_bin, u_pc, nu);
+        LAUNCH(k_unk_compact, grid_for(unk_cap), kThreads, unk_cap, unk, u_rec, nu);
         uint32_t NU = get1(nu);
         res.n_unknown = NU;
+        std::vector<ulonglong2> ur(NU);
+        down(ur.data(), u_rec, NU);
         std::vector<uint32_t> hs(NU), hb(NU);
         std::vector<uint64_t> hp(NU);
-        down(hs.data(), u_slot, NU);
-        down(hb.data(), u_bin, NU);
-        down(hp.data(), u_pc, NU);
+        for (uint32_t k = 0; k < NU; ++k) {
+            hp[k] = ur[k].x;
+            hs[k] = uint32_t(ur[k].y);
+            hb[k] = uint32_t(ur[k].y >> 32);
+        }
         merge_labels(NU, hs, hb, hp, unk_cap);
         mark("f:labels");
         LAUNCH(k_remap, grid_for(A), kThreads, A, d_arena, static_cast<const uint32_t*>(c.buf("u_final").p),
@@ -1011,16 +1020,7 @@ struct Runner {
         // lexicographic order of the sequences
         uint32_t* seq_rank = dev<uint32_t>("seq_rank", G);
         {
-            uint64_t maxlen = 0;  // kept in max_seq_len for the hottest-path download
-            {
-                uint64_t* mx = dev<uint64_t>("pd_max", 1);
-                size_t tb = 0;
-                STG_CUDA(cub::DeviceReduce::Max(nullptr, tb, seq_len, mx, int64_t(G), st));
-                STG_CUDA(cub::DeviceReduce::Max(temp(tb), tb, seq_len, mx, int64_t(G), st));
-                ++launches;
-                maxlen = get1(mx);
-                max_seq_len = maxlen;
-            }
+            const uint64_t maxlen = max_seq_len;  // from the dedupe stats
             int p_log = 1;
             while ((uint64_t(1) << p_log) < maxlen) ++p_log;
             const uint64_t n0 = uint64_t(G) << p_log;
@@ -1107,6 +1107,7 @@ struct Runner {
         excl_sum(dcnt, d_dn_off, S + 1);
         // distinct names per sequence <= its length: size by the arena, count stays on the device
         const uint64_t ND = A;
+        res.f_nd_bound = std::max<uint64_t>(ND, 1);
         d_dn = dev<uint32_t>("dn", std::max<uint64_t>(ND, 1));
         LAUNCH(k_seq_distinct<true>, grid_for(S * 32), kThreads, uint32_t(S), d_dense_rep, d_seq_off, d_arena, nullptr,
                d_dn_off, d_dn);
@@ -1121,34 +1122,42 @@ struct Runner {
         d_dense_final = dev<uint32_t>("dense_final", F);
         LAUNCH(k_dense_final, grid_for(NF), kThreads, NF, used, used_scan, d_dense_final);
         LAUNCH(k_dense_names, grid_for(ND), kThreads, d_dn_off + S, d_dn, used_scan);
-        uint64_t cells = uint64_t(R) * F;
-        if (cells > (1ull << 31)) fail(STG_ENOMEM, "rank x name matrix too large");
-        d_incl = dev<unsigned long long>("incl", cells);
-        // The rank x name inclusive counts feed only the waterline: they run on the
-        // side stream, overlapped with the straggler/reference fractions and the
-        // decision ladder; waterline() (and the end of the run) wait for them.
-        if (!c.side) STG_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
-        cudaEventRecord(ev_pre, st);
-        STG_CUDA(cudaStreamWaitEvent(c.side, ev_pre, 0));
-        {
-            cudaStream_t keep = st;
-            st = c.side;
-            if (F * sizeof(unsigned) <= 160 * 1024) {
-                const size_t sm = F * sizeof(unsigned);
-                if (sm > 48 * 1024)
-                    STG_CUDA(cudaFuncSetAttribute(k_incl_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-                k_incl_smem<<<R, 1024, sm, st>>>(R, d_line_off, d_lkey, d_lcount, d_dn_off, d_dn, F, d_incl);
-                ++launches;
-            } else {
-                zero(d_incl, cells * 8);
-                LAUNCH(k_incl, grid_for(L * 32), kThreads, L, d_lkey, d_lcount, d_dn_off, d_dn, F, d_incl);
-            }
-            st = keep;
-            STG_CUDA(cudaGetLastError());
-            STG_CUDA(cudaEventRecord(ev_incl, c.side));
-            incl_pending = true;
-        }
         cudaEventRecord(ev[6], st);
+    }
+
+    // Inclusive counts per (name, window rank), F-major (incl[f * R + r]); only
+    // the waterline needs them, so they are computed on request.
+    bool incl_done = false;
+    void inclusive_counts() {
+        if (incl_done) return;
+        incl_done = true;
+        const uint64_t cells = uint64_t(R) * F;
+        if (cells > (1ull << 33)) fail(STG_ENOMEM, "rank x name matrix too large");
+        d_incl = dev<unsigned long long>("incl", std::max<uint64_t>(cells, 1));
+        zero(d_incl, cells * 8);
+        if (!F || !L) return;
+        const uint32_t Rp = uint32_t((R + 3) & ~3);
+        const uint64_t cm = uint64_t(S) * Rp;
+        const uint64_t* nd_ptr = d_dn_off + S;
+        if (cm * 4 <= (4ull << 30)) {
+            uint32_t* C = dev<uint32_t>("incl_c", cm);
+            zero(C, cm * 4);
+            LAUNCH(k_lines_to_mat, grid_for(L), kThreads, L, d_lkey, d_lcount, Rp, C);
+            const uint64_t nd = get1(nd_ptr);
+            uint32_t* pf = dev<uint32_t>("incl_pf", std::max<uint64_t>(nd, 1));
+            uint32_t* ps = dev<uint32_t>("incl_ps", std::max<uint64_t>(nd, 1));
+            uint32_t* col_f = dev<uint32_t>("incl_colf", std::max<uint64_t>(nd, 1));
+            uint32_t* col_s = dev<uint32_t>("incl_cols", std::max<uint64_t>(nd, 1));
+            LAUNCH(k_name_pairs, grid_for(uint64_t(S) * 32), kThreads, uint32_t(S), d_dn_off, d_dn, pf, ps);
+            int fb = 1;
+            while (fb < 32 && (uint64_t(1) << fb) < F) ++fb;
+            sort_pairs(pf, col_f, ps, col_s, nd, fb);
+            LAUNCH(k_incl_spmm, grid_for((nd + kSpmmSeg - 1) / kSpmmSeg * 32), kThreads, nd_ptr, col_f, col_s, C,
+                   uint32_t(R), Rp, d_incl);
+        } else {
+            LAUNCH(k_incl_lines, grid_for(L * 32), kThreads, L, d_lkey, d_lcount, d_dn_off, d_dn, uint32_t(R), d_incl);
+        }
+        mark("w:incl");
     }
 
     // ------------------------------------------------------- diagnose
@@ -1238,13 +1247,13 @@ struct Runner {
     using Fracs = std::vector<std::pair<uint32_t, double>>;
     Fracs exact_fractions(uint64_t a, uint64_t n, uint64_t total, bool merged, const uint64_t* dn_off = nullptr,
                           const uint32_t* dn = nullptr, const unsigned long long* counts = nullptr) {
-        return std::move(exact_fractions2(a, n, total, 0, 0, 0, merged, dn_off, dn, counts)[0]);
+        return std::move(exact_fractions2(a, n, total, 0, 0, 0, merged, dn_off, dn, counts, nullptr)[0]);
     }
     // Two line ranges in one pass (the straggler and the reference rank): one
     // pair sort with the side in the key, all the running sums in one launch.
     std::array<Fracs, 2> exact_fractions2(uint64_t a0, uint64_t n0, uint64_t t0, uint64_t a1, uint64_t n1, uint64_t t1,
                                           bool merged, const uint64_t* dn_off = nullptr, const uint32_t* dn = nullptr,
-                                          const unsigned long long* counts = nullptr) {
+                                          const unsigned long long* counts = nullptr, const uint8_t* want = nullptr) {
         std::array<Fracs, 2> out;
         if (t0 == 0) n0 = 0;
         if (t1 == 0) n1 = 0;
@@ -1260,7 +1269,7 @@ struct Runner {
         int LB = 1;
         while ((uint64_t(1) << LB) < std::max(n0, n1)) ++LB;
         uint64_t* pc = dev<uint64_t>("xf_cnt", n + 1);
-        LAUNCH(k_pair_count, grid_for(n), kThreads, n, n0, lk0, lk1, d_dn_off, pc);
+        LAUNCH(k_pair_count, grid_for(n * 32), kThreads, n, n0, lk0, lk1, d_dn_off, d_dn, want, pc);
         zero(pc + n, 8);
         uint64_t* po = dev<uint64_t>("xf_off", n + 1);
         excl_sum(pc, po, n + 1);
@@ -1277,8 +1286,8 @@ struct Runner {
             NB = 1;
             while (NB < 31 && (uint64_t(1) << NB) < F) ++NB;
         }
-        LAUNCH(k_pair_emit, grid_for(n), kThreads, n, n0, lk0, lk1, cnt0, cnt1, t0, t1, d_dn_off, d_dn, po, LB, NB, keys,
-               vals);
+        LAUNCH(k_pair_emit, grid_for(n * 32), kThreads, n, n0, lk0, lk1, cnt0, cnt1, t0, t1, d_dn_off, d_dn, want, po, LB,
+               NB, keys, vals);
         // pairs are emitted in line order and the radix sort is stable, so
         // sorting the (side, name) bits alone keeps each name's lines in order
         sort_pairs(keys, keys_s, vals, vals_s, np, LB + NB + 1, LB);
@@ -1783,11 +1792,23 @@ struct Runner {
             } else if (is >= 0 && iq >= 0) {
                 struct Cand { std::string fn; double fs, fr, d; uint32_t f; };
                 std::vector<Cand> cands;
-                uint64_t lo[2], lo2[2];
-                down(lo, d_line_off + is, 2);
-                down(lo2, d_line_off + iq, 2);
+                std::vector<uint64_t> loff(size_t(R) + 1);
+                down(loff.data(), d_line_off, loff.size());
+                const uint64_t lo[2] = {loff[size_t(is)], loff[size_t(is) + 1]};
+                const uint64_t lo2[2] = {loff[size_t(iq)], loff[size_t(iq) + 1]};
+                // Candidates first: fs and fr are sequential double sums of
+                // count/total over <= n lines each (folded.cpp:45-54), so each is
+                // within (n + 2) * 2^-52 of its exact-integer estimate inc/total.
+                // Names whose estimated d stays below delta by more than the sum
+                // of both bounds cannot pass d > delta; the rest get the exact
+                // line-order sums (the values the report carries).
+                inclusive_counts();
+                uint8_t* want = dev<uint8_t>("xf_want", std::max<uint64_t>(F, 1));
+                const double margin = double((lo[1] - lo[0]) + (lo2[1] - lo2[0]) + 8) * std::ldexp(1.0, -50);
+                LAUNCH(k_diff_cands, grid_for(F), kThreads, F, d_incl, uint32_t(R), uint32_t(is), uint32_t(iq),
+                       double(h_n_in[is]), double(h_n_in[iq]), cfg.delta - margin, want);
                 auto both = exact_fractions2(lo[0], lo[1] - lo[0], h_n_in[is], lo2[0], lo2[1] - lo2[0], h_n_in[iq],
-                                             false);
+                                             false, nullptr, nullptr, nullptr, want);
                 mark("d:fracs2");
                 const auto& fs_ = both[0];
                 const auto& fr_ = both[1];
@@ -1923,6 +1944,7 @@ struct Runner {
     // compute_waterline + flag_ranks over the window's CPU profiles.
     void waterline_dist() {
         res.waterline_done = true;
+        inclusive_counts();
         global_names();
         const size_t nr = res.cpu_rank_ids.size();
         unsigned long long* drt = dev<unsigned long long>("wl_rt", 1);
@@ -1948,10 +1970,10 @@ struct Runner {
         }
         uint32_t* d_gk = up<uint32_t>("wl_gkey", gk.data(), std::max<uint64_t>(F, 1));
         uint32_t* rows = up<uint32_t>("wl_rows", res.cpu_rank_index.data(), std::max<size_t>(nr, 1));
-        if (F && nr) LAUNCH(k_wl_pass1, grid_for(F, 128), 128, F, rows, int(nr), d_incl, d_totals, d_gk, s1, np);
+        if (F && nr) LAUNCH(k_wl_pass1, grid_for(F, 128), 128, F, rows, int(nr), uint32_t(R), d_incl, d_totals, d_gk, s1, np);
         nccl(ncclAllReduce(s1, s1, NG, ncclFloat64, ncclSum, comm(), st));
         nccl(ncclAllReduce(np, np, NG, ncclUint32, ncclSum, comm(), st));
-        if (F && nr) LAUNCH(k_wl_pass2, grid_for(F, 128), 128, F, rows, int(nr), d_incl, d_totals, d_gk, s1, np, double(RT), s2);
+        if (F && nr) LAUNCH(k_wl_pass2, grid_for(F, 128), 128, F, rows, int(nr), uint32_t(R), d_incl, d_totals, d_gk, s1, np, double(RT), s2);
         nccl(ncclAllReduce(s2, s2, NG, ncclFloat64, ncclSum, comm(), st));
         double* mean = dev<double>("wlg_mean", NG);
         double* sd = dev<double>("wlg_sd", NG);
@@ -1964,7 +1986,7 @@ struct Runner {
         unsigned long long* n_out = dev<unsigned long long>("wl_n", 1);
         zero(n_out, 8);
         if (F && nr)
-            LAUNCH(k_flag_g, grid_for(F * nr), kThreads, F, rows, int(nr), d_incl, d_totals, cfg.k, d_gk, mean, sd, o_r,
+            LAUNCH(k_flag_g, grid_for(F * nr), kThreads, F, rows, int(nr), uint32_t(R), d_incl, d_totals, cfg.k, d_gk, mean, sd, o_r,
                    o_f, o_fr, o_th, n_out, cap);
         res.wl_flags = std::min<uint64_t>(get1(n_out), cap);
         res.wl_F = F;
@@ -1977,7 +1999,6 @@ struct Runner {
     }
 
     void waterline() {
-        wait_incl();
         res.wl_dist = false;
         if (dist()) return waterline_dist();
         res.waterline_done = true;
@@ -1987,11 +2008,12 @@ struct Runner {
             res.waterline_json = "{\"error\": \"waterline requires at least 2 ranks\"}";
             return;
         }
+        inclusive_counts();
         uint32_t* rows = up<uint32_t>("wl_rows", res.cpu_rank_index.data(), nr);
         double* mean = dev<double>("wl_mean", F);
         double* sd = dev<double>("wl_sd", F);
         uint8_t* pres = dev<uint8_t>("wl_pres", F);
-        LAUNCH(k_waterline, grid_for(F, 128), 128, F, rows, int(nr), d_incl, d_totals, mean, sd, pres);
+        LAUNCH(k_waterline, grid_for(F, 128), 128, F, rows, int(nr), uint32_t(R), d_incl, d_totals, mean, sd, pres);
         unsigned long long cap = std::max<uint64_t>(1, std::min<uint64_t>(F * nr, 1u << 24));
         uint32_t* o_r = dev<uint32_t>("wl_or", cap);
         uint32_t* o_f = dev<uint32_t>("wl_of", cap);
@@ -1999,7 +2021,7 @@ struct Runner {
         double* o_th = dev<double>("wl_oth", cap);
         unsigned long long* n_out = dev<unsigned long long>("wl_n", 1);
         zero(n_out, 8);
-        LAUNCH(k_flag, grid_for(F * nr), kThreads, F, rows, int(nr), d_incl, d_totals, cfg.k, mean, sd, o_r, o_f, o_fr,
+        LAUNCH(k_flag, grid_for(F * nr), kThreads, F, rows, int(nr), uint32_t(R), d_incl, d_totals, cfg.k, mean, sd, o_r, o_f, o_fr,
                o_th, n_out, cap);
         res.wl_flags = std::min<uint64_t>(get1(n_out), cap);
         res.wl_F = F;
@@ -2057,8 +2079,8 @@ struct Runner {
     void mark(const char* what) {
         if (!trace) return;
         auto now = std::chrono::steady_clock::now();
-        std::fprintf(stderr, "[stg] r%d %-12s %8.3f ms  @%.3f\n", c.wrank, what,
-                     std::chrono::duration<double, std::milli>(now - t_last).count(),
+        std::fprintf(stderr, "[stg] r%d %-12s %8.3f ms  syncs %3u launches %3u  @%.3f\n", c.wrank, what,
+                     std::chrono::duration<double, std::milli>(now - t_last).count(), syncs, launches,
                      std::fmod(std::chrono::duration<double, std::milli>(now.time_since_epoch()).count(), 1e5));
         t_last = now;
     }
@@ -2101,7 +2123,6 @@ struct Runner {
         res.waterline_done = false;
         if (cfg.want_waterline) waterline();
         mark("waterline");
-        wait_incl();
         cudaEventRecord(ev[7], st);
         STG_CUDA(cudaStreamSynchronize(st));
         stg_run_stats& s = res.stats;

@@ -1319,9 +1319,13 @@ __global__ void k_compact_lines(int R, const uint64_t* tab_off, const uint32_t* 
 }
 
 // Global dedupe of symbolized stacks across ranks: fingerprint -> sequence id.
+// stat = {distinct count (u32) | overflow (u32) << 32, Σ lengths, max length}: the
+// host reads all three with one download.
 __global__ void k_seq_dedupe(uint64_t L, const uint64_t* l_hi, const uint64_t* l_lo, const uint64_t* l_rep,
-                             SeqSlot* T, uint64_t mask, unsigned* n_seq, uint32_t* l_gid, uint64_t* seq_rep,
-                             int* overflow) {
+                             SeqSlot* T, uint64_t mask, unsigned long long* stat, uint32_t* l_gid, uint64_t* seq_rep,
+                             const uint64_t* foff) {
+    unsigned* n_seq = reinterpret_cast<unsigned*>(stat);
+    int* overflow = reinterpret_cast<int*>(stat) + 1;
     for (uint64_t l = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; l < L; l += uint64_t(gridDim.x) * blockDim.x) {
         uint64_t fa = l_hi[l], fb = l_lo[l];
         uint64_t i = mix_a(fa ^ fb) & mask;
@@ -1336,8 +1340,12 @@ __global__ void k_seq_dedupe(uint64_t L, const uint64_t* l_hi, const uint64_t* l
                     gid = atomicAdd(n_seq, 1u);
                     if (uint64_t(gid) + 1 > (mask + 1) / 2) *overflow = 1;
                     T[i].lo = fb;
-                    T[i].rep = l_rep[l];
-                    seq_rep[gid] = l_rep[l];
+                    const uint64_t rep = l_rep[l];
+                    T[i].rep = rep;
+                    seq_rep[gid] = rep;
+                    const unsigned long long len = foff[rep + 1] - foff[rep];
+                    atomicAdd(stat + 1, len);
+                    atomicMax(stat + 2, len);
                     __threadfence();
                     atomicExch(&T[i].gid, gid);
                     break;
@@ -1383,15 +1391,13 @@ __global__ void k_seq_materialize(uint32_t G, const uint64_t* seq_rep, const uin
     }
 }
 
-__global__ void k_unk_compact(uint32_t cap, const UnkSlot* slots, uint32_t* o_slot, uint32_t* o_bin, uint64_t* o_pc,
-                              unsigned* n_out) {
+// Distinct unresolved frames as packed {pc, slot | bin << 32} records (one download).
+__global__ void k_unk_compact(uint32_t cap, const UnkSlot* slots, ulonglong2* out, unsigned* n_out) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += gridDim.x * blockDim.x) {
         uint32_t b = slots[i].bin1;
         if (b == 0 || b == 0xffffffffu) continue;
         unsigned o = atomicAdd(n_out, 1u);
-        o_slot[o] = i;
-        o_bin[o] = b - 1;
-        o_pc[o] = slots[i].pc;
+        out[o] = make_ulonglong2(slots[i].pc, uint64_t(i) | (uint64_t(b - 1) << 32));
     }
 }
 
@@ -1590,32 +1596,96 @@ __global__ void k_dense_names(const uint64_t* n_ptr, uint32_t* dn, const uint32_
         dn[i] = used_scan[dn[i]];  // exclusive scan -> dense index
 }
 
-// Inclusive counts per (rank, name): warp per folded line adds its count to each
-// distinct name of its sequence (exact integers; fraction = count / total).
-__global__ void k_incl(uint64_t L, const uint64_t* lkey, const unsigned long long* lcount, const uint64_t* dn_off,
-                       const uint32_t* dn, uint64_t F, unsigned long long* incl) {
+// Inclusive counts per (name, rank), F-major: incl[f * R + r] = Σ of the
+// counts of rank r's lines whose sequence contains name f (folded.cpp:45-54
+// counts a repeated name once per line).  As a sparse product: C[s][r] = the
+// count of rank r's line with sequence s (dense S x R, L2-resident), and the
+// name -> sequences incidence in column form; a warp walks a slice of the
+// column entries, each lane summing 4 ranks of C's row s with one 16-byte load,
+// and flushes its per-name partials with one atomic per (name, rank) run.
+__global__ void k_lines_to_mat(uint64_t L, const uint64_t* lkey, const unsigned long long* lcount, uint32_t Rp,
+                               uint32_t* C) {
+    for (uint64_t l = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; l < L; l += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t key = lkey[l];
+        C[uint64_t(uint32_t(key)) * Rp + (key >> 32)] = uint32_t(lcount[l]);
+    }
+}
+// (name, sequence) incidence pairs in dn order; sorted by name they form the
+// columns of the name x sequence matrix (no atomics on hot names' cursors)
+__global__ void k_name_pairs(uint32_t S, const uint64_t* dn_off, const uint32_t* dn, uint32_t* col_f, uint32_t* col_s) {
+    const int lane = threadIdx.x & 31;
+    for (uint64_t s = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; s < S;
+         s += (uint64_t(gridDim.x) * blockDim.x) >> 5)
+        for (uint64_t k = dn_off[s] + lane; k < dn_off[s + 1]; k += 32) {
+            col_f[k] = dn[k];
+            col_s[k] = uint32_t(s);
+        }
+}
+constexpr uint32_t kSpmmSeg = 512;  // column entries per warp
+__global__ void k_incl_spmm(const uint64_t* nd_ptr, const uint32_t* col_f, const uint32_t* col_s, const uint32_t* C,
+                            uint32_t R, uint32_t Rp, unsigned long long* incl) {
+    const uint64_t nd = *nd_ptr;
+    const int lane = threadIdx.x & 31;
+    const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t w = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; w * kSpmmSeg < nd; w += nw) {
+        const uint64_t e0 = w * kSpmmSeg, e1 = e0 + kSpmmSeg < nd ? e0 + kSpmmSeg : nd;
+        for (uint32_t c0 = 0; c0 < R; c0 += 128) {
+            const uint32_t r0 = c0 + 4 * lane;
+            const bool mine = r0 < Rp;
+            unsigned long long a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+            uint32_t cur = col_f[e0];
+            auto flush = [&](uint32_t f) {
+                if (!mine) return;
+                unsigned long long* row = incl + uint64_t(f) * R;
+                if (a0 && r0 < R) atomicAdd(row + r0, a0);
+                if (a1 && r0 + 1 < R) atomicAdd(row + r0 + 1, a1);
+                if (a2 && r0 + 2 < R) atomicAdd(row + r0 + 2, a2);
+                if (a3 && r0 + 3 < R) atomicAdd(row + r0 + 3, a3);
+                a0 = a1 = a2 = a3 = 0;
+            };
+            for (uint64_t e = e0; e < e1; ++e) {
+                const uint32_t f = col_f[e];
+                if (f != cur) {
+                    flush(cur);
+                    cur = f;
+                }
+                if (mine) {
+                    const uint4 v = __ldg(reinterpret_cast<const uint4*>(C + uint64_t(col_s[e]) * Rp + r0));
+                    a0 += v.x;
+                    a1 += v.y;
+                    a2 += v.z;
+                    a3 += v.w;
+                }
+            }
+            flush(cur);
+        }
+    }
+}
+// Fallback when the dense S x R count matrix would not fit: warp per line.
+__global__ void k_incl_lines(uint64_t L, const uint64_t* lkey, const unsigned long long* lcount, const uint64_t* dn_off,
+                             const uint32_t* dn, uint32_t R, unsigned long long* incl) {
     const int lane = threadIdx.x & 31;
     for (uint64_t l = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; l < L;
          l += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
-        uint64_t key = lkey[l];
-        uint32_t r = uint32_t(key >> 32), s = uint32_t(key);
-        unsigned long long c = lcount[l];
-        unsigned long long* row = incl + uint64_t(r) * F;
-        for (uint64_t k = dn_off[s] + lane; k < dn_off[s + 1]; k += 32) atomicAdd(row + dn[k], c);
+        const uint64_t key = lkey[l];
+        const uint32_t r = uint32_t(key >> 32), s = uint32_t(key);
+        const unsigned long long c = lcount[l];
+        for (uint64_t k = dn_off[s] + lane; k < dn_off[s + 1]; k += 32) atomicAdd(incl + uint64_t(dn[k]) * R + r, c);
     }
 }
 
 // compute_waterline (diagnosis.cpp:35-55) per name over the CPU ranks: present
 // fractions in rank order then zeros appended, population sigma; flag_ranks
 // (:57-71) strictly above mean + k sigma.
-__global__ void k_waterline(uint64_t F, const uint32_t* rows, int R, const unsigned long long* incl,
+__global__ void k_waterline(uint64_t F, const uint32_t* rows, int R, uint32_t RW, const unsigned long long* incl,
                             const uint64_t* totals, double* mean, double* sd, uint8_t* present_any) {
     for (uint64_t f = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; f < F; f += uint64_t(gridDim.x) * blockDim.x) {
         double acc = 0.0;
         int np = 0;
+        const unsigned long long* row = incl + f * RW;
         for (int i = 0; i < R; ++i) {
             uint32_t r = rows[i];
-            unsigned long long c = incl[uint64_t(r) * F + f];
+            unsigned long long c = row[r];
             if (c) {
                 acc = __dadd_rn(acc, __ddiv_rn(double(c), double(totals[r])));
                 ++np;
@@ -1626,7 +1696,7 @@ __global__ void k_waterline(uint64_t F, const uint32_t* rows, int R, const unsig
         double s2 = 0.0;
         for (int i = 0; i < R; ++i) {
             uint32_t r = rows[i];
-            unsigned long long c = incl[uint64_t(r) * F + f];
+            unsigned long long c = row[r];
             if (c) {
                 double d = __dsub_rn(__ddiv_rn(double(c), double(totals[r])), mu);
                 s2 = __dadd_rn(s2, __dmul_rn(d, d));
@@ -1638,14 +1708,14 @@ __global__ void k_waterline(uint64_t F, const uint32_t* rows, int R, const unsig
     }
 }
 
-__global__ void k_flag(uint64_t F, const uint32_t* rows, int R, const unsigned long long* incl,
+__global__ void k_flag(uint64_t F, const uint32_t* rows, int R, uint32_t RW, const unsigned long long* incl,
                        const uint64_t* totals, double k, const double* mean, const double* sd, uint32_t* o_r,
                        uint32_t* o_f, double* o_frac, double* o_thr, unsigned long long* n_out,
                        unsigned long long cap) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < F * uint64_t(R);
          i += uint64_t(gridDim.x) * blockDim.x) {
-        uint64_t r = rows[i / F], f = i % F;
-        unsigned long long c = incl[r * F + f];
+        uint64_t r = rows[i % R], f = i / R;
+        unsigned long long c = incl[f * RW + r];
         if (!c) continue;
         double fr = __ddiv_rn(double(c), double(totals[r]));
         double thr = __dadd_rn(mean[f], __dmul_rn(k, sd[f]));
@@ -1720,26 +1790,40 @@ __global__ void k_hot_pack(const unsigned long long* best, const uint64_t* lkey,
 // Exact inclusive fractions in the reference's summation order
 // (folded.cpp:45-54): (name, line) pairs sorted, then one sequential sum of
 // double(count)/double(total) per name in line order.
+// want (optional): only names f with want[f] != 0 take part (the diff's
+// candidates, see Runner::diagnose); warp per line, lanes over its names.
 __global__ void k_pair_count(uint64_t n, uint64_t n0, const uint64_t* lkey0, const uint64_t* lkey1,
-                             const uint64_t* dn_off, uint64_t* cnt) {
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+                             const uint64_t* dn_off, const uint32_t* dn, const uint8_t* want, uint64_t* cnt) {
+    const int lane = threadIdx.x & 31;
+    for (uint64_t i = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; i < n;
+         i += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
         const bool side = i >= n0;
         const uint64_t j = side ? i - n0 : i;
         const uint64_t* lk = side ? lkey1 : lkey0;
         const uint32_t s = lk ? uint32_t(lk[j]) : uint32_t(j);
-        cnt[i] = dn_off[s + 1] - dn_off[s];
+        const uint64_t k0 = dn_off[s], k1 = dn_off[s + 1];
+        uint64_t c = 0;
+        if (!want) {
+            c = k1 - k0;
+        } else {
+            for (uint64_t k = k0; k < k1; k += 32)
+                c += __popc(__ballot_sync(0xffffffffu, k + lane < k1 && want[dn[k + lane]]));
+        }
+        if (lane == 0) cnt[i] = c;
     }
 }
 // Pairs (name, line) of up to two line ranges (side 0: lines [0, n0), side 1:
 // [n0, n)); key = (side << NB | name) << LB | line within its side (the stable
 // radix sort only runs the NB + 1 side/name bits above LB), value =
-// double(count) / double(total of its side).
+// double(count) / double(total of its side).  Warp per line, coalesced.
 __global__ void k_pair_emit(uint64_t n, uint64_t n0, const uint64_t* lkey0, const uint64_t* lkey1,
                             const unsigned long long* cnt0, const unsigned long long* cnt1, uint64_t total0,
-                            uint64_t total1, const uint64_t* dn_off, const uint32_t* dn, const uint64_t* pair_off,
-                            int LB, int NB, uint64_t* keys, double* vals) {
+                            uint64_t total1, const uint64_t* dn_off, const uint32_t* dn, const uint8_t* want,
+                            const uint64_t* pair_off, int LB, int NB, uint64_t* keys, double* vals) {
     const double t0 = __ull2double_rn(total0), t1 = __ull2double_rn(total1);
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    for (uint64_t i = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; i < n;
+         i += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
         const bool side = i >= n0;
         const uint64_t j = side ? i - n0 : i;
         const uint64_t* lk = side ? lkey1 : lkey0;
@@ -1747,10 +1831,40 @@ __global__ void k_pair_emit(uint64_t n, uint64_t n0, const uint64_t* lkey0, cons
         const double x = __ddiv_rn(__ull2double_rn((side ? cnt1 : cnt0)[j]), side ? t1 : t0);  // count / total
         uint64_t o = pair_off[i];
         const uint64_t sb = side ? 1ull << NB : 0ull;
-        for (uint64_t k = dn_off[s]; k < dn_off[s + 1]; ++k, ++o) {
-            keys[o] = ((sb | dn[k]) << LB) | j;
-            vals[o] = x;
+        const uint64_t k0 = dn_off[s], k1 = dn_off[s + 1];
+        for (uint64_t kb = k0; kb < k1; kb += 32) {
+            const uint64_t k = kb + lane;
+            uint32_t f = 0;
+            bool ok = k < k1;
+            if (ok) {
+                f = dn[k];
+                if (want) ok = want[f] != 0;
+            }
+            const unsigned b = __ballot_sync(0xffffffffu, ok);
+            if (ok) {
+                const uint64_t q = o + __popc(b & ((1u << lane) - 1));
+                keys[q] = ((sb | f) << LB) | j;
+                vals[q] = x;
+            }
+            o += __popc(b);
         }
+    }
+}
+// cpu_diff pre-filter (diagnosis.cpp:177-208): a straggler name can pass
+// d = fs - fr > delta only if its exact-integer estimate passes delta - margin,
+// margin bounding the rounding of the reference's sequential sums (see
+// Runner::diagnose); those names alone get the exact line-order sums.
+__global__ void k_diff_cands(uint64_t F, const unsigned long long* incl, uint32_t R, uint32_t is, uint32_t iq,
+                             double ts, double tr, double lim, uint8_t* want) {
+    for (uint64_t f = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; f < F; f += uint64_t(gridDim.x) * blockDim.x) {
+        const unsigned long long cs = incl[f * R + is];
+        bool w = false;
+        if (cs) {
+            const double d = __dsub_rn(__ddiv_rn(__ull2double_rn(cs), ts),
+                                       __ddiv_rn(__ull2double_rn(incl[f * R + iq]), tr));
+            w = d > lim;
+        }
+        want[f] = w;
     }
 }
 __global__ void k_pair_segflags(uint64_t np, const uint64_t* keys, int LB, uint32_t* flag) {
@@ -1824,54 +1938,16 @@ __global__ void __launch_bounds__(kSegWarps * 32) k_pair_segsum(uint64_t nseg, c
     }
 }
 
-// Inclusive counts of one rank per CTA in shared memory (u32 counters; a rank
-// has < 2^32 samples), written out as a dense row.  Each warp walks a contiguous
-// run of the rank's (sorted) lines, lane k owning distinct-name slot k of the
-// current line.  Consecutive lines share their root prefix, so lane k keeps a
-// pending (name, count) and only flushes it to shared memory when its name
-// changes: the hot root names cost one atomic per run instead of one per line.
-__global__ void k_incl_smem(int R, const uint64_t* line_off, const uint64_t* lkey, const unsigned long long* lcount,
-                            const uint64_t* dn_off, const uint32_t* dn, uint64_t F, unsigned long long* incl) {
-    extern __shared__ unsigned int sc[];
-    const int r = blockIdx.x;
-    for (uint64_t f = threadIdx.x; f < F; f += blockDim.x) sc[f] = 0;
-    __syncthreads();
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const uint64_t l0 = line_off[r], l1 = line_off[r + 1];
-    const uint64_t per = (l1 - l0 + nw - 1) / nw;
-    const uint64_t a = l0 + per * wid, b = a + per < l1 ? a + per : l1;
-    uint32_t pend_name = 0xffffffffu;
-    unsigned pend = 0;
-    for (uint64_t l = a; l < b; ++l) {
-        const uint32_t s = uint32_t(lkey[l]);
-        const unsigned c = unsigned(lcount[l]);
-        const uint64_t k0 = dn_off[s], k1 = dn_off[s + 1];
-        const uint64_t k = k0 + lane;
-        const uint32_t name = k < k1 ? dn[k] : 0xffffffffu;
-        if (name != pend_name) {
-            if (pend) atomicAdd(sc + pend_name, pend);
-            pend_name = name;
-            pend = 0;
-        }
-        if (name != 0xffffffffu) pend += c;
-        for (uint64_t kk = k + 32; kk < k1; kk += 32) atomicAdd(sc + dn[kk], c);
-    }
-    if (pend) atomicAdd(sc + pend_name, pend);
-    __syncthreads();
-    unsigned long long* row = incl + uint64_t(r) * F;
-    for (uint64_t f = threadIdx.x; f < F; f += blockDim.x) row[f] = sc[f];
-}
-
 // Distributed waterline: per-name partial sums of the local ranks, scattered to
 // global name keys (then all-reduced across contexts).
-__global__ void k_wl_pass1(uint64_t F, const uint32_t* rows, int R, const unsigned long long* incl,
+__global__ void k_wl_pass1(uint64_t F, const uint32_t* rows, int R, uint32_t RW, const unsigned long long* incl,
                            const uint64_t* totals, const uint32_t* gkey, double* s1, unsigned* np) {
     for (uint64_t f = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; f < F; f += uint64_t(gridDim.x) * blockDim.x) {
         double acc = 0.0;
         unsigned n = 0;
         for (int i = 0; i < R; ++i) {
             const uint32_t r = rows[i];
-            const unsigned long long c = incl[uint64_t(r) * F + f];
+            const unsigned long long c = incl[f * RW + r];
             if (c) {
                 acc = __dadd_rn(acc, __ddiv_rn(double(c), double(totals[r])));
                 ++n;
@@ -1881,7 +1957,7 @@ __global__ void k_wl_pass1(uint64_t F, const uint32_t* rows, int R, const unsign
         np[gkey[f]] = n;
     }
 }
-__global__ void k_wl_pass2(uint64_t F, const uint32_t* rows, int R, const unsigned long long* incl,
+__global__ void k_wl_pass2(uint64_t F, const uint32_t* rows, int R, uint32_t RW, const unsigned long long* incl,
                            const uint64_t* totals, const uint32_t* gkey, const double* s1, const unsigned* np,
                            double rt, double* s2) {
     for (uint64_t f = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; f < F; f += uint64_t(gridDim.x) * blockDim.x) {
@@ -1890,7 +1966,7 @@ __global__ void k_wl_pass2(uint64_t F, const uint32_t* rows, int R, const unsign
         double acc = 0.0;
         for (int i = 0; i < R; ++i) {
             const uint32_t r = rows[i];
-            const unsigned long long c = incl[uint64_t(r) * F + f];
+            const unsigned long long c = incl[f * RW + r];
             if (c) {
                 const double d = __dsub_rn(__ddiv_rn(double(c), double(totals[r])), mu);
                 acc = __dadd_rn(acc, __dmul_rn(d, d));
@@ -1914,13 +1990,14 @@ __global__ void k_wl_final(uint64_t NG, const double* s1, const unsigned* np, co
         sd[g] = __dsqrt_rn(__ddiv_rn(v, rt));
     }
 }
-__global__ void k_flag_g(uint64_t F, const uint32_t* rows, int R, const unsigned long long* incl, const uint64_t* totals,
-                         double k, const uint32_t* gkey, const double* mean, const double* sd, uint32_t* o_r,
-                         uint32_t* o_f, double* o_frac, double* o_thr, unsigned long long* n_out, unsigned long long cap) {
+__global__ void k_flag_g(uint64_t F, const uint32_t* rows, int R, uint32_t RW, const unsigned long long* incl,
+                         const uint64_t* totals, double k, const uint32_t* gkey, const double* mean, const double* sd,
+                         uint32_t* o_r, uint32_t* o_f, double* o_frac, double* o_thr, unsigned long long* n_out,
+                         unsigned long long cap) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < F * uint64_t(R);
          i += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t r = rows[i / F], f = i % F;
-        const unsigned long long c = incl[r * F + f];
+        const uint64_t r = rows[i % R], f = i / R;
+        const unsigned long long c = incl[f * RW + r];
         if (!c) continue;
         const uint32_t g = gkey[f];
         const double fr = __ddiv_rn(double(c), double(totals[r]));

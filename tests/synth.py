@@ -63,7 +63,9 @@ def small_window(seed: int = 1, ranks: int = 8, samples_per_rank: int = 2000, sl
     n_sym = len(names)
     starts = 0x1000 + 64 * np.arange(n_sym, dtype=np.uint64)
     sizes = np.full(n_sym, 48, np.uint32)
-    bid = build_id(f"app-{seed}")
+    # distinct tables must carry distinct build ids (a context keeps the first
+    # table ingested under an id, like SymbolRepository::ingest)
+    bid = build_id(f"app-{seed}" if n_sym == 2000 else f"app-{seed}-n{n_sym}")
     symr = [pack_symr(bid, starts, sizes, names)]
     bids = [bid]
     for e in range(extra_bins):  # binaries without a symbol file: unknown labels
