@@ -62,13 +62,16 @@ def args_parse():
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-budget-s", type=float, default=20.0)
-    p.add_argument("--config", default="c2", choices=["c2", "c4", "agg", "bundle"],
-                   help="c2 = headline (samples/s); c4 = collective alignment, 1,024 ranks x 50k events; "
+    p.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "agg", "bundle"],
+                   help="c2 = headline (samples/s); c3 = the north-star 1,024-rank window (C1-style CPU "
+                        "stacks + GPU kernels + OS counters, sharded over the GPUs); "
+                        "c4 = collective alignment, 1,024 ranks x 50k events; "
                         "agg = raw aggregate_samples on the BM_Aggregation stream shape; "
                         "bundle = load_bundle (JSONL) + analysis of a C1-scale bundle directory")
     p.add_argument("--agg-samples", type=int, default=64_000_000, help="agg: samples in the stream")
     p.add_argument("--bundle-spr", type=int, default=100_000, help="bundle: samples per rank (C1: 100k)")
     p.add_argument("--events", type=int, default=50_000, help="c4: events per rank")
+    p.add_argument("--iterations", type=int, default=100, help="training iterations in the window (c3: 300)")
     return p.parse_args()
 
 
@@ -86,7 +89,7 @@ class Workload:
         rng = np.random.default_rng(a.seed * 1000)
         self.period = 10_000  # ns between samples of a rank
         self.span = a.spr * self.period
-        self.iterations = 100
+        self.iterations = getattr(a, "iterations", 100)
         self.iter_ns = self.span // self.iterations
         self.group_size = world * a.ranks
         self.skews_all = rng.integers(-10_000_000, 10_000_001, size=self.group_size).astype(np.int64)
@@ -180,7 +183,65 @@ class Workload:
         w.baseline = {}
         w.baseline_iteration_ms = self.iter_ns / 1e6
         w.symr = [t[3] for t in self.tables]
+        if memory == 1:  # STG_MEM_DEVICE: the side streams live in HBM too
+            side_to_device(w)
         return w
+
+
+def side_to_device(w):
+    """Collectives, GPU kernel events and OS counter records as device tensors
+    (stg_window.coll_memory / side_memory = STG_MEM_DEVICE): every input of the
+    timed window is HBM-resident."""
+    import torch
+    cols = {"coll_rank": np.int32, "coll_group": np.int32, "coll_kind": np.uint8, "coll_entry": np.int64,
+            "coll_exit": np.int64, "coll_gpu_dur": np.int64}
+    side = {"gpu_rank": np.int32, "gpu_kernel": np.int32, "gpu_start": np.int64, "gpu_dur": np.int64,
+            "os_rank": np.int32, "os_window_start": np.int64, "os_p50": np.int64, "os_p99": np.int64,
+            "os_migrations": np.int64, "os_irq_off": np.int64, "os_irq_key": np.int32, "os_irq_val": np.int64,
+            "os_sirq_off": np.int64, "os_sirq_key": np.int32, "os_sirq_val": np.int64}
+    w.n_coll_ = len(w.coll_rank)
+    w.n_gpu_ = len(w.gpu_rank)
+    w.n_os_ = len(w.os_rank)
+    for f, dt in {**cols, **side}.items():
+        a = np.ascontiguousarray(np.asarray(getattr(w, f)).astype(dt))
+        setattr(w, f, torch.from_numpy(a).cuda() if len(a) else torch.zeros(1, dtype=torch.int64).cuda())
+    w.coll_memory = 1
+    w.side_memory = 1
+
+
+def c3_parity_sample(a, wl, ctx, arrays, k_ranks: int = 8):
+    """Parity inside the c3 run: the folded texts (FoldedProfile::to_string) of
+    the first k ranks (the straggler among them) from the GPU run just timed,
+    against the reference's build_group_data on the same samples of those ranks
+    with the whole group's collectives / GPU / OS streams (so the clock offsets
+    and hence the window filter are the same).  The reference symbolizes with
+    its resolve_stacks + fold_symbolized (one table cache per rank), see
+    oracle/ref_harness.cpp."""
+    from oracle import ref
+    from paper_2603_29235_b200.abi import STG_MEM_HOST
+    if not ref.available():
+        return None
+    spr, D = a.spr, a.depth
+    n = k_ranks * spr
+    host = (arrays[0][:n].cpu().numpy(), arrays[1][:n + 1].cpu().numpy().view(np.uint64),
+            arrays[2][:n * D].cpu().numpy().view(np.uint64), arrays[3][:n * D].cpu().numpy().view(np.uint16))
+    w = wl.window(a.ranks, spr, host, STG_MEM_HOST)
+    w.rank_ids = w.rank_ids[:k_ranks].copy()
+    w.rank_sample_off = w.rank_sample_off[:k_ranks + 1].copy()
+    w.n_samples_, w.n_frames_ = n, n * D
+    t0 = time.perf_counter()
+    r, _, _ = ref.window_run(w, threads=k_ranks, want_json=False, artifacts=True, shared_cache=True)
+    ref_s = time.perf_counter() - t0
+    exp = {int(rk): txt for rk, txt in r["artifacts"]["folded"]}
+    same = [ctx.folded_text(int(rk)) == exp.get(int(rk)) for rk in w.rank_ids]
+    return {"ranks_checked": [int(x) for x in w.rank_ids], "folded_text_equal": all(same), "ref_seconds": round(ref_s, 1)}
+
+
+def workload_name(a):
+    if a.config == "c3":
+        return ("C3 (north-star): one 1,024-rank window, 100k CPU samples/rank (12-frame stacks, 200 distinct "
+                "stacks/rank, 3x10k-symbol tables), GPU kernel + OS counter streams, 300 iterations")
+    return "C2: 128 ranks x 1M samples per GPU, 64-frame stacks, 3x1M-symbol tables"
 
 
 # ------------------------------------------------------------------ clocks
@@ -565,6 +626,9 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     if a.impl == "reference":
+        if a.config == "c3":
+            a.ranks = 1024
+            a.spr, a.depth, a.pool, a.nsym, a.hot, a.iterations = 100_000, 12, 200, 10_000, "all", 300
         if rank == 0:
             wl = Workload(a, 0)
             cb = reference_arm(a, wl, torch, os.cpu_count() or 1, steps=a.steps, warmup=a.warmup)
@@ -573,8 +637,9 @@ def main():
             else:
                 line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
                         "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "higher_is_better": True,
-                        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-                        "config": {"workload": "C2: 128 ranks x 1M samples per GPU, 64-frame stacks, 3x1M-symbol tables",
+                        "scaling": "strong" if a.config == "c3" else "weak", "vs_baseline": None, "dtype": "u64",
+                        "data": "synthetic",
+                        "config": {"workload": workload_name(a),
                                    "ranks_per_gpu": a.ranks, "samples_per_rank": a.spr, "depth": a.depth,
                                    "distinct_stacks": a.pool, "symbols_per_table": a.nsym,
                                    "inputs": "host memory, bounded sample per step (see cpu_baseline.sample)"},
@@ -587,6 +652,14 @@ def main():
             dist.destroy_process_group()
         return
 
+    if a.config == "c3":
+        # north-star window (richer variant): 1,024 ranks in
+        # one group, C1-style CPU profiles (100k samples/rank, 12-frame stacks,
+        # 200 distinct stacks/rank, 10k-symbol tables), GPU kernel events and OS
+        # counters of 300 iterations; the 1,024 ranks are sharded over the GPUs
+        # (strong scaling: the window is fixed)
+        a.ranks = 1024 // world
+        a.spr, a.depth, a.pool, a.nsym, a.hot, a.iterations = 100_000, 12, 200, 10_000, "all", 300
     import paper_2603_29235_b200 as stg
     from paper_2603_29235_b200.abi import STG_MEM_DEVICE, STG_MEM_HOST
     if a.config == "c4":
@@ -652,7 +725,12 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     n_per_gpu = s["n_samples_in_window"]
-    value = n_per_gpu * world / (ms / 1e3)
+    n_total = n_per_gpu
+    if dist:  # in-window samples of the whole group (the shards differ slightly)
+        t = torch.tensor([n_per_gpu], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t)
+        n_total = int(t.item())
+    value = n_total / (ms / 1e3)
     # ---- roofline of the dominant kernel (fused symbolize+aggregate).  Algorithmic
     # bytes: every sample's ts + CSR row (16 B), and the frames of the IN-WINDOW
     # samples only (10 B each: 8 B pc + 2 B bin) — k_sym_agg never reads the frames
@@ -668,13 +746,15 @@ def main():
             "pipeline_frac": round(algo_bytes / (ms / 1e3) / 1e9 / peak, 4),
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback 6.65 TB/s"}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if a.config == "c3" else "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": "C2: 128 ranks x 1M samples per GPU, 64-frame stacks, 3x1M-symbol tables",
+            "config": {"workload": workload_name(a),
                        "ranks_per_gpu": a.ranks, "samples_per_rank": a.spr, "depth": a.depth,
                        "distinct_stacks": a.pool, "symbols_per_table": a.nsym,
                        "functions_drawn": "5k/20k/5k per table" if a.hot == "bench" else "all 1M per table",
-                       "inputs": "resident in HBM, 84 GB/GPU > L2 (no flush needed)",
+                       "inputs": f"resident in HBM, {(10 * win.n_frames + 16 * win.n_samples) / 1e9:.1f} GB/GPU "
+                                 "> L2 (no flush needed)",
                        "group_ranks": wl.group_size,
                        "parallelism": f"one {wl.group_size}-rank group sharded by rank over {world} GPU(s), "
                                       "NCCL exchange of straggler/reference fractions + waterline all-reduce"},
@@ -684,6 +764,14 @@ def main():
                          "collectives": s["ms_collectives"], "fold": s["ms_fold"], "diff": s["ms_diff"]},
             "roofline": roof, "ingest": ingest, "gpu_launches": int(np.median(launches)) * a.steps,
             "clocks": clk.summary()}
+    if a.config == "c3":
+        line["north_star"] = {"target": "full pipeline >= 0.40 of the HBM roofline on a 1,024-rank window",
+                              "pipeline_frac": roof["pipeline_frac"], "met": roof["pipeline_frac"] >= 0.40}
+        if rank == 0 and world == 1 and not a.no_cpu_baseline:
+            try:
+                line["parity_sample"] = c3_parity_sample(a, wl, ctx, arrays)
+            except Exception as ex:
+                line["parity_sample"] = {"error": str(ex)[:200]}
     # ---- end to end through the C-ABI with host buffers (H2D inside the timed region)
     e2e_ok = not a.no_e2e
     if e2e_ok and world > 1:
@@ -730,7 +818,7 @@ def main():
             t = torch.tensor([el], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
-        line["e2e"] = {"value": n_per_gpu * world / el, "unit": UNIT,
+        line["e2e"] = {"value": n_total / el, "unit": UNIT,
                        "h2d_bytes_per_step": h2d // a.e2e_steps, "d2h_bytes_per_step": d2h // a.e2e_steps,
                        "ms_per_step": el * 1e3, "verdict": r["verdict"]}
     if rank == 0 and world == 1 and not a.no_cpu_baseline:

@@ -174,6 +174,8 @@ typedef struct stg_window {
 
     /* stg_memory of the coll_* arrays (group_ranks stays host) */
     int32_t coll_memory;
+    /* stg_memory of the gpu_* and os_* arrays (kernel/counter names stay host) */
+    int32_t side_memory;
 } stg_window;
 
 /* DiagnosisConfig (diagnosis.hpp:203-210) + GpuDiffConfig (:83-92) + OsDiffConfig

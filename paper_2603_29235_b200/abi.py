@@ -87,6 +87,7 @@ class StgWindow(C.Structure):
         ("has_baseline_iteration", C.c_int32),
         ("baseline_iteration_ms", C.c_double),
         ("coll_memory", C.c_int32),
+        ("side_memory", C.c_int32),
     ]
 
 
@@ -249,6 +250,9 @@ class Window:
     frame_bin: object = field(default_factory=lambda: np.zeros(0, np.uint16))
     memory: int = STG_MEM_HOST
     coll_memory: int = STG_MEM_HOST
+    side_memory: int = STG_MEM_HOST
+    n_gpu_: Optional[int] = None
+    n_os_: Optional[int] = None
     n_coll_: Optional[int] = None
     n_samples_: Optional[int] = None
     n_frames_: Optional[int] = None
@@ -341,25 +345,24 @@ class Window:
                 setattr(w, f, _ptr(getattr(self, f), keep))
         w.n_group_ranks = len(self.group_ranks)
         w.group_ranks = _ptr(np.asarray(self.group_ranks, np.int32), keep)
-        w.n_gpu = len(self.gpu_rank)
-        w.gpu_rank = _ptr(np.asarray(self.gpu_rank, np.int32), keep)
-        w.gpu_kernel = _ptr(np.asarray(self.gpu_kernel, np.uint32), keep)
-        w.gpu_start = _ptr(np.asarray(self.gpu_start, np.int64), keep)
-        w.gpu_dur = _ptr(np.asarray(self.gpu_dur, np.int64), keep)
+        w.side_memory = self.side_memory
+        gpu_f = (("gpu_rank", np.int32), ("gpu_kernel", np.uint32), ("gpu_start", np.int64), ("gpu_dur", np.int64))
+        os_f = (("os_rank", np.int32), ("os_window_start", np.int64), ("os_p50", np.int64), ("os_p99", np.int64),
+                ("os_migrations", np.int64), ("os_irq_off", np.uint64), ("os_irq_key", np.uint32),
+                ("os_irq_val", np.int64), ("os_sirq_off", np.uint64), ("os_sirq_key", np.uint32),
+                ("os_sirq_val", np.int64))
+        if self.side_memory == STG_MEM_HOST:
+            w.n_gpu = len(self.gpu_rank)
+            w.n_os = len(self.os_rank)
+            for f, dt in gpu_f + os_f:
+                setattr(w, f, _ptr(np.asarray(getattr(self, f), dt), keep))
+        else:  # device tensors (data_ptr)
+            w.n_gpu = self.n_gpu_ if self.n_gpu_ is not None else int(self.gpu_rank.numel())
+            w.n_os = self.n_os_ if self.n_os_ is not None else int(self.os_rank.numel())
+            for f, _ in gpu_f + os_f:
+                setattr(w, f, _ptr(getattr(self, f), keep))
         w.n_kernel_names = len(self.kernel_names)
         w.kernel_names = _strings(self.kernel_names, keep)
-        w.n_os = len(self.os_rank)
-        w.os_rank = _ptr(np.asarray(self.os_rank, np.int32), keep)
-        w.os_window_start = _ptr(np.asarray(self.os_window_start, np.int64), keep)
-        w.os_p50 = _ptr(np.asarray(self.os_p50, np.int64), keep)
-        w.os_p99 = _ptr(np.asarray(self.os_p99, np.int64), keep)
-        w.os_migrations = _ptr(np.asarray(self.os_migrations, np.int64), keep)
-        w.os_irq_off = _ptr(np.asarray(self.os_irq_off, np.uint64), keep)
-        w.os_irq_key = _ptr(np.asarray(self.os_irq_key, np.uint32), keep)
-        w.os_irq_val = _ptr(np.asarray(self.os_irq_val, np.int64), keep)
-        w.os_sirq_off = _ptr(np.asarray(self.os_sirq_off, np.uint64), keep)
-        w.os_sirq_key = _ptr(np.asarray(self.os_sirq_key, np.uint32), keep)
-        w.os_sirq_val = _ptr(np.asarray(self.os_sirq_val, np.int64), keep)
         w.n_counter_names = len(self.counter_names)
         w.counter_names = _strings(self.counter_names, keep)
         w.has_baseline = int(bool(self.has_baseline))

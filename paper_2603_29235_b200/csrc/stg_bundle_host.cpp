@@ -176,6 +176,7 @@ void bundle_load(Ctx& c, const std::string& dir_s, stg_bundle_info* info) {
     w.frame_pc = k.pc;
     w.frame_bin = k.bin;
     w.coll_memory = STG_MEM_DEVICE;
+    w.side_memory = STG_MEM_HOST;  // gpu/os records are decoded on the host
     w.n_coll = k.n_coll;
     w.coll_rank = k.c_rank;
     w.coll_group = k.c_group;

@@ -218,8 +218,13 @@ struct Runner {
         } else {
             scan(w.coll_rank, w.n_coll, "coll_rank");
         }
-        scan(w.gpu_rank, w.n_gpu, "gpu_rank");
-        scan(w.os_rank, w.n_os, "os_rank");
+        if (w.side_memory == STG_MEM_DEVICE) {
+            if (w.n_gpu) LAUNCH(k_max_rank, grid_for(w.n_gpu), kThreads, w.n_gpu, w.gpu_rank, d_mm, d_mm + 1);
+            if (w.n_os) LAUNCH(k_max_rank, grid_for(w.n_os), kThreads, w.n_os, w.os_rank, d_mm, d_mm + 1);
+        } else {
+            scan(w.gpu_rank, w.n_gpu, "gpu_rank");
+            scan(w.os_rank, w.n_os, "os_rank");
+        }
         int out[2];
         down(out, d_mm, 2);
         if (out[1] < 0) fail(STG_EINVAL, "negative rank ids are not supported");
@@ -332,7 +337,7 @@ struct Runner {
         uint64_t* d_kbase = up<uint64_t>("c_kbase", k_base.data(), n_st + 1);
         uint32_t* first_fail = up<uint32_t>("c_ffail", h_kmin.data(), n_st);
         if (k_base[n_st])
-            LAUNCH(k_coll_regular, grid_for(k_base[n_st]), kThreads, int(n_st), d_st_seg, seg_pos, coarse, s_entry,
+            LAUNCH(k_coll_regular, grid_for(k_base[n_st] * 32), kThreads, int(n_st), d_st_seg, seg_pos, coarse, s_entry,
                    s_exit, kmin, d_kbase, k_base[n_st], w.max_skew_ns, first_fail);
         std::vector<uint32_t> k0(n_st);
         down(k0.data(), first_fail, n_st);
@@ -452,7 +457,7 @@ struct Runner {
             double* mu = dev<double>("s_mu", n_w);
             double* sg = dev<double>("s_sg", n_w);
             uint32_t* m = dev<uint32_t>("s_m", n_w);
-            LAUNCH(k_straggler_inst, grid_for(n_w, 128), 128, n_w, span, d_lat, cfg.k, mu, sg, m);
+            LAUNCH(k_straggler_inst, grid_for(n_w * 32), kThreads, n_w, span, d_lat, cfg.k, mu, sg, m);
             uint8_t* pres = dev<uint8_t>("s_pres", span);
             double* ma = dev<double>("s_ma", span);
             double* ml = dev<double>("s_ml", span);
@@ -478,10 +483,11 @@ struct Runner {
         res.os.clear();
         if (w.n_gpu) {
             const uint64_t n = w.n_gpu, K = w.n_kernel_names;
-            const int32_t* d_rank = static_cast<const int32_t*>(c.buf("gpu_rank").p);
-            const uint32_t* d_k = up<uint32_t>("gpu_k", w.gpu_kernel, n);
-            const int64_t* d_s = up<int64_t>("gpu_s", w.gpu_start, n);
-            const int64_t* d_d = up<int64_t>("gpu_d", w.gpu_dur, n);
+            const bool sdev = w.side_memory == STG_MEM_DEVICE;
+            const int32_t* d_rank = sdev ? w.gpu_rank : static_cast<const int32_t*>(c.buf("gpu_rank").p);
+            const uint32_t* d_k = sdev ? w.gpu_kernel : up<uint32_t>("gpu_k", w.gpu_kernel, n);
+            const int64_t* d_s = sdev ? w.gpu_start : up<int64_t>("gpu_s", w.gpu_start, n);
+            const int64_t* d_d = sdev ? w.gpu_dur : up<int64_t>("gpu_d", w.gpu_dur, n);
             unsigned long long* sums = dev<unsigned long long>("gpu_sums", span * K);
             uint8_t* pres = dev<uint8_t>("gpu_pres", span * K);
             int* err = dev<int>("gpu_err", 1);
@@ -501,18 +507,35 @@ struct Runner {
         }
         if (w.n_os) {
             const uint64_t n = w.n_os, C = std::max<uint32_t>(w.n_counter_names, 1);
-            const int32_t* d_rank = static_cast<const int32_t*>(c.buf("os_rank").p);
-            auto ws = up<int64_t>("os_ws", w.os_window_start, n);
-            auto p50 = up<int64_t>("os_p50", w.os_p50, n);
-            auto p99 = up<int64_t>("os_p99", w.os_p99, n);
-            auto mig = up<int64_t>("os_mig", w.os_migrations, n);
-            auto ioff = up<uint64_t>("os_ioff", w.os_irq_off, n + 1);
-            uint64_t ni = w.os_irq_off[n], ns = w.os_sirq_off[n];
-            auto ikey = up<uint32_t>("os_ikey", w.os_irq_key, ni);
-            auto ival = up<int64_t>("os_ival", w.os_irq_val, ni);
-            auto soff = up<uint64_t>("os_soff", w.os_sirq_off, n + 1);
-            auto skey = up<uint32_t>("os_skey", w.os_sirq_key, ns);
-            auto sval = up<int64_t>("os_sval", w.os_sirq_val, ns);
+            const bool sdev = w.side_memory == STG_MEM_DEVICE;
+            const int32_t* d_rank = sdev ? w.os_rank : static_cast<const int32_t*>(c.buf("os_rank").p);
+            const int64_t *ws, *p50, *p99, *mig, *ival, *sval;
+            const uint64_t *ioff, *soff;
+            const uint32_t *ikey, *skey;
+            if (sdev) {
+                ws = w.os_window_start;
+                p50 = w.os_p50;
+                p99 = w.os_p99;
+                mig = w.os_migrations;
+                ioff = w.os_irq_off;
+                ikey = w.os_irq_key;
+                ival = w.os_irq_val;
+                soff = w.os_sirq_off;
+                skey = w.os_sirq_key;
+                sval = w.os_sirq_val;
+            } else {
+                ws = up<int64_t>("os_ws", w.os_window_start, n);
+                p50 = up<int64_t>("os_p50", w.os_p50, n);
+                p99 = up<int64_t>("os_p99", w.os_p99, n);
+                mig = up<int64_t>("os_mig", w.os_migrations, n);
+                ioff = up<uint64_t>("os_ioff", w.os_irq_off, n + 1);
+                const uint64_t ni = w.os_irq_off[n], ns = w.os_sirq_off[n];
+                ikey = up<uint32_t>("os_ikey", w.os_irq_key, ni);
+                ival = up<int64_t>("os_ival", w.os_irq_val, ni);
+                soff = up<uint64_t>("os_soff", w.os_sirq_off, n + 1);
+                skey = up<uint32_t>("os_skey", w.os_sirq_key, ns);
+                sval = up<int64_t>("os_sval", w.os_sirq_val, ns);
+            }
             auto irq = dev<unsigned long long>("os_irq", span * C);
             auto irqp = dev<uint8_t>("os_irqp", span * C);
             auto sirq = dev<unsigned long long>("os_sirq", span * C);
@@ -1125,7 +1148,7 @@ struct Runner {
         cudaEventRecord(ev[6], st);
     }
 
-    // Inclusive counts per (name, window rank), F-major (incl[f * R + r]); only
+    // Inclusive counts per (window rank, name), incl[r * F + f]; only
     // the waterline needs them, so they are computed on request.
     bool incl_done = false;
     void inclusive_counts() {
@@ -1152,10 +1175,12 @@ struct Runner {
             int fb = 1;
             while (fb < 32 && (uint64_t(1) << fb) < F) ++fb;
             sort_pairs(pf, col_f, ps, col_s, nd, fb);
-            LAUNCH(k_incl_spmm, grid_for((nd + kSpmmSeg - 1) / kSpmmSeg * 32), kThreads, nd_ptr, col_f, col_s, C,
-                   uint32_t(R), Rp, d_incl);
+            // column slices per warp: enough warps to fill the GPU, <= 512 entries each
+            const uint32_t seg = uint32_t(std::max<uint64_t>(8, std::min<uint64_t>(512, nd / (148ull * 32) + 1)));
+            LAUNCH(k_incl_spmm, grid_for((nd + seg - 1) / seg * 32), kThreads, nd_ptr, col_f, col_s, C, uint32_t(R), Rp,
+                   F, seg, d_incl);
         } else {
-            LAUNCH(k_incl_lines, grid_for(L * 32), kThreads, L, d_lkey, d_lcount, d_dn_off, d_dn, uint32_t(R), d_incl);
+            LAUNCH(k_incl_lines, grid_for(L * 32), kThreads, L, d_lkey, d_lcount, d_dn_off, d_dn, F, d_incl);
         }
         mark("w:incl");
     }
@@ -1970,10 +1995,10 @@ struct Runner {
         }
         uint32_t* d_gk = up<uint32_t>("wl_gkey", gk.data(), std::max<uint64_t>(F, 1));
         uint32_t* rows = up<uint32_t>("wl_rows", res.cpu_rank_index.data(), std::max<size_t>(nr, 1));
-        if (F && nr) LAUNCH(k_wl_pass1, grid_for(F, 128), 128, F, rows, int(nr), uint32_t(R), d_incl, d_totals, d_gk, s1, np);
+        if (F && nr) LAUNCH(k_wl_pass1, grid_for(F * 32), kThreads, F, rows, int(nr), d_incl, d_totals, d_gk, s1, np);
         nccl(ncclAllReduce(s1, s1, NG, ncclFloat64, ncclSum, comm(), st));
         nccl(ncclAllReduce(np, np, NG, ncclUint32, ncclSum, comm(), st));
-        if (F && nr) LAUNCH(k_wl_pass2, grid_for(F, 128), 128, F, rows, int(nr), uint32_t(R), d_incl, d_totals, d_gk, s1, np, double(RT), s2);
+        if (F && nr) LAUNCH(k_wl_pass2, grid_for(F * 32), kThreads, F, rows, int(nr), d_incl, d_totals, d_gk, s1, np, double(RT), s2);
         nccl(ncclAllReduce(s2, s2, NG, ncclFloat64, ncclSum, comm(), st));
         double* mean = dev<double>("wlg_mean", NG);
         double* sd = dev<double>("wlg_sd", NG);
@@ -1986,7 +2011,7 @@ struct Runner {
         unsigned long long* n_out = dev<unsigned long long>("wl_n", 1);
         zero(n_out, 8);
         if (F && nr)
-            LAUNCH(k_flag_g, grid_for(F * nr), kThreads, F, rows, int(nr), uint32_t(R), d_incl, d_totals, cfg.k, d_gk, mean, sd, o_r,
+            LAUNCH(k_flag_g, grid_for(F * nr), kThreads, F, rows, int(nr), d_incl, d_totals, cfg.k, d_gk, mean, sd, o_r,
                    o_f, o_fr, o_th, n_out, cap);
         res.wl_flags = std::min<uint64_t>(get1(n_out), cap);
         res.wl_F = F;
@@ -2013,7 +2038,7 @@ struct Runner {
         double* mean = dev<double>("wl_mean", F);
         double* sd = dev<double>("wl_sd", F);
         uint8_t* pres = dev<uint8_t>("wl_pres", F);
-        LAUNCH(k_waterline, grid_for(F, 128), 128, F, rows, int(nr), uint32_t(R), d_incl, d_totals, mean, sd, pres);
+        LAUNCH(k_waterline, grid_for(F * 32), kThreads, F, rows, int(nr), d_incl, d_totals, mean, sd, pres);
         unsigned long long cap = std::max<uint64_t>(1, std::min<uint64_t>(F * nr, 1u << 24));
         uint32_t* o_r = dev<uint32_t>("wl_or", cap);
         uint32_t* o_f = dev<uint32_t>("wl_of", cap);
@@ -2021,7 +2046,7 @@ struct Runner {
         double* o_th = dev<double>("wl_oth", cap);
         unsigned long long* n_out = dev<unsigned long long>("wl_n", 1);
         zero(n_out, 8);
-        LAUNCH(k_flag, grid_for(F * nr), kThreads, F, rows, int(nr), uint32_t(R), d_incl, d_totals, cfg.k, mean, sd, o_r, o_f, o_fr,
+        LAUNCH(k_flag, grid_for(F * nr), kThreads, F, rows, int(nr), d_incl, d_totals, cfg.k, mean, sd, o_r, o_f, o_fr,
                o_th, n_out, cap);
         res.wl_flags = std::min<uint64_t>(get1(n_out), cap);
         res.wl_F = F;

@@ -173,35 +173,52 @@ __global__ void k_coll_streams(int n_streams, const uint32_t* st_seg, const uint
 
 // Regular-case proof: instance k of a stream is {every rank's k-th event} iff the
 // greedy sweep (collective.cpp:64-89) starting from all heads at k pulls them all.
-// One thread per (stream, k): seed = min pre-aligned entry, ties to the lowest
+// One warp per (stream, k): seed = min pre-aligned entry, ties to the lowest
 // rank (strict <, rank order); then every head must overlap the seed interval.
 __global__ void k_coll_regular(int n_streams, const uint32_t* st_seg, const uint32_t* seg_pos,
                                const int64_t* coarse, const int64_t* s_entry, const int64_t* s_exit,
                                const uint32_t* kmin, const uint64_t* k_base, uint64_t n_k,
                                int64_t skew, uint32_t* first_fail) {
-    for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < n_k;
-         t += uint64_t(gridDim.x) * blockDim.x) {
-        // stream of t
-        int s = 0;
-        while (s + 1 < n_streams && k_base[s + 1] <= t) ++s;
-        uint32_t k = uint32_t(t - k_base[s]);
-        uint32_t a = st_seg[s], b = st_seg[s + 1];
-        int64_t best = LLONG_MAX, best_exit = 0;
-        for (uint32_t j = a; j < b; ++j) {
-            uint64_t p = seg_pos[j] + k;
-            int64_t e = s_entry[p] - coarse[j];
-            if (e < best) {
+    // one warp per (stream, k): lanes stride over the stream's rank segments
+    const int lane = threadIdx.x & 31;
+    for (uint64_t t = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; t < n_k;
+         t += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+        int lo = 0, hi = n_streams - 1;  // stream of t: last s with k_base[s] <= t
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (k_base[mid] <= t) lo = mid; else hi = mid - 1;
+        }
+        const int s = lo;
+        const uint32_t k = uint32_t(t - k_base[s]);
+        const uint32_t a = st_seg[s], b = st_seg[s + 1];
+        // seed: min pre-aligned entry, ties to the lowest segment (rank order)
+        long long best = LLONG_MAX;
+        uint32_t bj = 0xffffffffu;
+        for (uint32_t j = a + lane; j < b; j += 32) {
+            const long long e = s_entry[seg_pos[j] + k] - coarse[j];
+            if (e < best) {  // j ascends per lane: strict < keeps the lowest
                 best = e;
-                best_exit = s_exit[p] - coarse[j];
+                bj = j;
             }
         }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const long long ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const uint32_t oj = __shfl_xor_sync(0xffffffffu, bj, o);
+            if (ob < best || (ob == best && oj < bj)) {
+                best = ob;
+                bj = oj;
+            }
+        }
+        const long long best_exit = s_exit[seg_pos[bj] + k] - coarse[bj];
         bool ok = true;
-        for (uint32_t j = a; j < b && ok; ++j) {
-            uint64_t p = seg_pos[j] + k;
-            int64_t e = s_entry[p] - coarse[j], x = s_exit[p] - coarse[j];
+        for (uint32_t j = a + lane; j < b && ok; j += 32) {
+            const uint64_t p = seg_pos[j] + k;
+            const long long e = s_entry[p] - coarse[j], x = s_exit[p] - coarse[j];
             ok = e <= best_exit + skew && x + skew >= best;
         }
-        if (!ok) atomicMin(first_fail + s, k);
+        ok = __all_sync(0xffffffffu, ok);
+        if (!ok && lane == 0) atomicMin(first_fail + s, k);
     }
 }
 
@@ -486,30 +503,39 @@ __global__ void k_coll_itertimes(uint64_t n_w, const uint64_t* wkey_sorted, doub
 // floating-point order: Σ over ranks ascending, then /n; Σ (l-μ)² ascending.
 __global__ void k_straggler_inst(uint64_t n_w, int rank_span, const double* lat, double k,
                                  double* mu_w, double* sigma_w, uint32_t* m_w) {
-    for (uint64_t w = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; w < n_w;
-         w += uint64_t(gridDim.x) * blockDim.x) {
+    // one warp per instance: lanes load 32 ranks at a time, lane 0 adds them in
+    // rank order (the reference's sequence of roundings)
+    const int lane = threadIdx.x & 31;
+    for (uint64_t w = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; w < n_w;
+         w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
         double acc = 0.0;
         uint32_t m = 0;
-        for (int r = 0; r < rank_span; ++r) {
-            double l = lat[uint64_t(r) * n_w + w];
-            if (l == l) {
-                acc = __dadd_rn(acc, l);
-                ++m;
+        for (int r0 = 0; r0 < rank_span; r0 += 32) {
+            const int r = r0 + lane;
+            const double l = r < rank_span ? lat[uint64_t(r) * n_w + w] : nan("");
+            const unsigned pres = __ballot_sync(0xffffffffu, l == l);
+            m += __popc(pres);
+            for (unsigned q = pres; q; q &= q - 1) {
+                const double v = __shfl_sync(0xffffffffu, l, __ffs(q) - 1);
+                acc = __dadd_rn(acc, v);
             }
         }
-        m_w[w] = m;
+        if (lane == 0) m_w[w] = m;
         if (m < 2) continue;
-        double mu = __ddiv_rn(acc, double(m));
+        const double mu = __ddiv_rn(acc, double(m));
         double s2 = 0.0;
-        for (int r = 0; r < rank_span; ++r) {
-            double l = lat[uint64_t(r) * n_w + w];
-            if (l == l) {
-                double d = __dsub_rn(l, mu);
-                s2 = __dadd_rn(s2, __dmul_rn(d, d));
-            }
+        for (int r0 = 0; r0 < rank_span; r0 += 32) {
+            const int r = r0 + lane;
+            const double l = r < rank_span ? lat[uint64_t(r) * n_w + w] : nan("");
+            const double d = __dsub_rn(l, mu);
+            const double dd = __dmul_rn(d, d);
+            for (unsigned q = __ballot_sync(0xffffffffu, l == l); q; q &= q - 1)
+                s2 = __dadd_rn(s2, __shfl_sync(0xffffffffu, dd, __ffs(q) - 1));
         }
-        mu_w[w] = mu;
-        sigma_w[w] = __dsqrt_rn(__ddiv_rn(s2, double(m)));
+        if (lane == 0) {
+            mu_w[w] = mu;
+            sigma_w[w] = __dsqrt_rn(__ddiv_rn(s2, double(m)));
+        }
     }
 }
 
@@ -1596,7 +1622,7 @@ __global__ void k_dense_names(const uint64_t* n_ptr, uint32_t* dn, const uint32_
         dn[i] = used_scan[dn[i]];  // exclusive scan -> dense index
 }
 
-// Inclusive counts per (name, rank), F-major: incl[f * R + r] = Σ of the
+// Inclusive counts per (rank, name), incl[r * F + f] = Σ of the
 // counts of rank r's lines whose sequence contains name f (folded.cpp:45-54
 // counts a repeated name once per line).  As a sparse product: C[s][r] = the
 // count of rank r's line with sequence s (dense S x R, L2-resident), and the
@@ -1621,14 +1647,13 @@ __global__ void k_name_pairs(uint32_t S, const uint64_t* dn_off, const uint32_t*
             col_s[k] = uint32_t(s);
         }
 }
-constexpr uint32_t kSpmmSeg = 512;  // column entries per warp
 __global__ void k_incl_spmm(const uint64_t* nd_ptr, const uint32_t* col_f, const uint32_t* col_s, const uint32_t* C,
-                            uint32_t R, uint32_t Rp, unsigned long long* incl) {
+                            uint32_t R, uint32_t Rp, uint64_t F, uint32_t seg, unsigned long long* incl) {
     const uint64_t nd = *nd_ptr;
     const int lane = threadIdx.x & 31;
     const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-    for (uint64_t w = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; w * kSpmmSeg < nd; w += nw) {
-        const uint64_t e0 = w * kSpmmSeg, e1 = e0 + kSpmmSeg < nd ? e0 + kSpmmSeg : nd;
+    for (uint64_t w = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; w * seg < nd; w += nw) {
+        const uint64_t e0 = w * seg, e1 = e0 + seg < nd ? e0 + seg : nd;
         for (uint32_t c0 = 0; c0 < R; c0 += 128) {
             const uint32_t r0 = c0 + 4 * lane;
             const bool mine = r0 < Rp;
@@ -1636,11 +1661,11 @@ __global__ void k_incl_spmm(const uint64_t* nd_ptr, const uint32_t* col_f, const
             uint32_t cur = col_f[e0];
             auto flush = [&](uint32_t f) {
                 if (!mine) return;
-                unsigned long long* row = incl + uint64_t(f) * R;
-                if (a0 && r0 < R) atomicAdd(row + r0, a0);
-                if (a1 && r0 + 1 < R) atomicAdd(row + r0 + 1, a1);
-                if (a2 && r0 + 2 < R) atomicAdd(row + r0 + 2, a2);
-                if (a3 && r0 + 3 < R) atomicAdd(row + r0 + 3, a3);
+                unsigned long long* col = incl + f;
+                if (a0 && r0 < R) atomicAdd(col + uint64_t(r0) * F, a0);
+                if (a1 && r0 + 1 < R) atomicAdd(col + uint64_t(r0 + 1) * F, a1);
+                if (a2 && r0 + 2 < R) atomicAdd(col + uint64_t(r0 + 2) * F, a2);
+                if (a3 && r0 + 3 < R) atomicAdd(col + uint64_t(r0 + 3) * F, a3);
                 a0 = a1 = a2 = a3 = 0;
             };
             for (uint64_t e = e0; e < e1; ++e) {
@@ -1663,59 +1688,81 @@ __global__ void k_incl_spmm(const uint64_t* nd_ptr, const uint32_t* col_f, const
 }
 // Fallback when the dense S x R count matrix would not fit: warp per line.
 __global__ void k_incl_lines(uint64_t L, const uint64_t* lkey, const unsigned long long* lcount, const uint64_t* dn_off,
-                             const uint32_t* dn, uint32_t R, unsigned long long* incl) {
+                             const uint32_t* dn, uint64_t F, unsigned long long* incl) {
     const int lane = threadIdx.x & 31;
     for (uint64_t l = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; l < L;
          l += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
         const uint64_t key = lkey[l];
         const uint32_t r = uint32_t(key >> 32), s = uint32_t(key);
         const unsigned long long c = lcount[l];
-        for (uint64_t k = dn_off[s] + lane; k < dn_off[s + 1]; k += 32) atomicAdd(incl + uint64_t(dn[k]) * R + r, c);
+        for (uint64_t k = dn_off[s] + lane; k < dn_off[s + 1]; k += 32) atomicAdd(incl + uint64_t(r) * F + dn[k], c);
     }
 }
 
 // compute_waterline (diagnosis.cpp:35-55) per name over the CPU ranks: present
 // fractions in rank order then zeros appended, population sigma; flag_ranks
 // (:57-71) strictly above mean + k sigma.
-__global__ void k_waterline(uint64_t F, const uint32_t* rows, int R, uint32_t RW, const unsigned long long* incl,
+// Warp per name: the lanes load 32 ranks' counts and divide in parallel, lane 0
+// adds the fractions in rank order (the reference's order), zeros after them.
+__device__ __forceinline__ double warp_ordered_sum(double acc, double v, unsigned take) {
+    for (unsigned q = take; q; q &= q - 1) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, v, __ffs(q) - 1));
+    return acc;
+}
+__global__ void k_waterline(uint64_t F, const uint32_t* rows, int R, const unsigned long long* incl,
                             const uint64_t* totals, double* mean, double* sd, uint8_t* present_any) {
-    for (uint64_t f = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; f < F; f += uint64_t(gridDim.x) * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    for (uint64_t f = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; f < F;
+         f += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
         double acc = 0.0;
         int np = 0;
-        const unsigned long long* row = incl + f * RW;
-        for (int i = 0; i < R; ++i) {
-            uint32_t r = rows[i];
-            unsigned long long c = row[r];
-            if (c) {
-                acc = __dadd_rn(acc, __ddiv_rn(double(c), double(totals[r])));
-                ++np;
+        for (int i0 = 0; i0 < R; i0 += 32) {
+            const int i = i0 + lane;
+            double x = 0.0;
+            bool pres = false;
+            if (i < R) {
+                const uint32_t r = rows[i];
+                const unsigned long long c = incl[uint64_t(r) * F + f];
+                pres = c != 0;
+                if (pres) x = __ddiv_rn(double(c), double(totals[r]));
             }
+            const unsigned m = __ballot_sync(0xffffffffu, pres);
+            np += __popc(m);
+            acc = warp_ordered_sum(acc, x, m);
         }
-        present_any[f] = np > 0;
-        double mu = __ddiv_rn(acc, double(R));
+        const double mu = __ddiv_rn(acc, double(R));
         double s2 = 0.0;
-        for (int i = 0; i < R; ++i) {
-            uint32_t r = rows[i];
-            unsigned long long c = row[r];
-            if (c) {
-                double d = __dsub_rn(__ddiv_rn(double(c), double(totals[r])), mu);
-                s2 = __dadd_rn(s2, __dmul_rn(d, d));
+        for (int i0 = 0; i0 < R; i0 += 32) {
+            const int i = i0 + lane;
+            double dd = 0.0;
+            bool pres = false;
+            if (i < R) {
+                const uint32_t r = rows[i];
+                const unsigned long long c = incl[uint64_t(r) * F + f];
+                pres = c != 0;
+                if (pres) {
+                    const double d = __dsub_rn(__ddiv_rn(double(c), double(totals[r])), mu);
+                    dd = __dmul_rn(d, d);
+                }
             }
+            s2 = warp_ordered_sum(s2, dd, __ballot_sync(0xffffffffu, pres));
         }
-        for (int i = np; i < R; ++i) s2 = __dadd_rn(s2, __dmul_rn(mu, mu));
-        mean[f] = mu;
-        sd[f] = __dsqrt_rn(__ddiv_rn(s2, double(R)));
+        if (lane == 0) {
+            for (int i = np; i < R; ++i) s2 = __dadd_rn(s2, __dmul_rn(mu, mu));
+            present_any[f] = np > 0;
+            mean[f] = mu;
+            sd[f] = __dsqrt_rn(__ddiv_rn(s2, double(R)));
+        }
     }
 }
 
-__global__ void k_flag(uint64_t F, const uint32_t* rows, int R, uint32_t RW, const unsigned long long* incl,
+__global__ void k_flag(uint64_t F, const uint32_t* rows, int R, const unsigned long long* incl,
                        const uint64_t* totals, double k, const double* mean, const double* sd, uint32_t* o_r,
                        uint32_t* o_f, double* o_frac, double* o_thr, unsigned long long* n_out,
                        unsigned long long cap) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < F * uint64_t(R);
          i += uint64_t(gridDim.x) * blockDim.x) {
-        uint64_t r = rows[i % R], f = i / R;
-        unsigned long long c = incl[f * RW + r];
+        uint64_t r = rows[i / F], f = i % F;
+        unsigned long long c = incl[r * F + f];
         if (!c) continue;
         double fr = __ddiv_rn(double(c), double(totals[r]));
         double thr = __dadd_rn(mean[f], __dmul_rn(k, sd[f]));
@@ -1857,11 +1904,11 @@ __global__ void k_pair_emit(uint64_t n, uint64_t n0, const uint64_t* lkey0, cons
 __global__ void k_diff_cands(uint64_t F, const unsigned long long* incl, uint32_t R, uint32_t is, uint32_t iq,
                              double ts, double tr, double lim, uint8_t* want) {
     for (uint64_t f = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; f < F; f += uint64_t(gridDim.x) * blockDim.x) {
-        const unsigned long long cs = incl[f * R + is];
+        const unsigned long long cs = incl[uint64_t(is) * F + f];
         bool w = false;
         if (cs) {
             const double d = __dsub_rn(__ddiv_rn(__ull2double_rn(cs), ts),
-                                       __ddiv_rn(__ull2double_rn(incl[f * R + iq]), tr));
+                                       __ddiv_rn(__ull2double_rn(incl[uint64_t(iq) * F + f]), tr));
             w = d > lim;
         }
         want[f] = w;
@@ -1940,39 +1987,58 @@ __global__ void __launch_bounds__(kSegWarps * 32) k_pair_segsum(uint64_t nseg, c
 
 // Distributed waterline: per-name partial sums of the local ranks, scattered to
 // global name keys (then all-reduced across contexts).
-__global__ void k_wl_pass1(uint64_t F, const uint32_t* rows, int R, uint32_t RW, const unsigned long long* incl,
+__global__ void k_wl_pass1(uint64_t F, const uint32_t* rows, int R, const unsigned long long* incl,
                            const uint64_t* totals, const uint32_t* gkey, double* s1, unsigned* np) {
-    for (uint64_t f = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; f < F; f += uint64_t(gridDim.x) * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    for (uint64_t f = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; f < F;
+         f += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
         double acc = 0.0;
         unsigned n = 0;
-        for (int i = 0; i < R; ++i) {
-            const uint32_t r = rows[i];
-            const unsigned long long c = incl[f * RW + r];
-            if (c) {
-                acc = __dadd_rn(acc, __ddiv_rn(double(c), double(totals[r])));
-                ++n;
+        for (int i0 = 0; i0 < R; i0 += 32) {
+            const int i = i0 + lane;
+            double x = 0.0;
+            bool pres = false;
+            if (i < R) {
+                const uint32_t r = rows[i];
+                const unsigned long long c = incl[uint64_t(r) * F + f];
+                pres = c != 0;
+                if (pres) x = __ddiv_rn(double(c), double(totals[r]));
             }
+            const unsigned m = __ballot_sync(0xffffffffu, pres);
+            n += __popc(m);
+            acc = warp_ordered_sum(acc, x, m);
         }
-        s1[gkey[f]] = acc;
-        np[gkey[f]] = n;
+        if (lane == 0) {
+            s1[gkey[f]] = acc;
+            np[gkey[f]] = n;
+        }
     }
 }
-__global__ void k_wl_pass2(uint64_t F, const uint32_t* rows, int R, uint32_t RW, const unsigned long long* incl,
+__global__ void k_wl_pass2(uint64_t F, const uint32_t* rows, int R, const unsigned long long* incl,
                            const uint64_t* totals, const uint32_t* gkey, const double* s1, const unsigned* np,
                            double rt, double* s2) {
-    for (uint64_t f = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; f < F; f += uint64_t(gridDim.x) * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    for (uint64_t f = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; f < F;
+         f += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
         const uint32_t g = gkey[f];
         const double mu = __ddiv_rn(s1[g], rt);
         double acc = 0.0;
-        for (int i = 0; i < R; ++i) {
-            const uint32_t r = rows[i];
-            const unsigned long long c = incl[f * RW + r];
-            if (c) {
-                const double d = __dsub_rn(__ddiv_rn(double(c), double(totals[r])), mu);
-                acc = __dadd_rn(acc, __dmul_rn(d, d));
+        for (int i0 = 0; i0 < R; i0 += 32) {
+            const int i = i0 + lane;
+            double dd = 0.0;
+            bool pres = false;
+            if (i < R) {
+                const uint32_t r = rows[i];
+                const unsigned long long c = incl[uint64_t(r) * F + f];
+                pres = c != 0;
+                if (pres) {
+                    const double d = __dsub_rn(__ddiv_rn(double(c), double(totals[r])), mu);
+                    dd = __dmul_rn(d, d);
+                }
             }
+            acc = warp_ordered_sum(acc, dd, __ballot_sync(0xffffffffu, pres));
         }
-        s2[g] = acc;
+        if (lane == 0) s2[g] = acc;
     }
 }
 __global__ void k_wl_final(uint64_t NG, const double* s1, const unsigned* np, const double* s2, double rt,
@@ -1990,14 +2056,14 @@ __global__ void k_wl_final(uint64_t NG, const double* s1, const unsigned* np, co
         sd[g] = __dsqrt_rn(__ddiv_rn(v, rt));
     }
 }
-__global__ void k_flag_g(uint64_t F, const uint32_t* rows, int R, uint32_t RW, const unsigned long long* incl,
+__global__ void k_flag_g(uint64_t F, const uint32_t* rows, int R, const unsigned long long* incl,
                          const uint64_t* totals, double k, const uint32_t* gkey, const double* mean, const double* sd,
                          uint32_t* o_r, uint32_t* o_f, double* o_frac, double* o_thr, unsigned long long* n_out,
                          unsigned long long cap) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < F * uint64_t(R);
          i += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t r = rows[i % R], f = i / R;
-        const unsigned long long c = incl[f * RW + r];
+        const uint64_t r = rows[i / F], f = i % F;
+        const unsigned long long c = incl[r * F + f];
         if (!c) continue;
         const uint32_t g = gkey[f];
         const double fr = __ddiv_rn(double(c), double(totals[r]));

@@ -160,7 +160,7 @@ def _annihilator_window(seed=21):
     that zeroed the round-1 block product — and draws the partner frame from two
     different functions.  Chains differing only in the partner must still fold
     under their own names (the reference full-compares, samples.cpp:67-76)."""
-    w = small_window(seed=seed, ranks=4, samples_per_rank=3000, slow_rank=-1, depth=12, n_sym=2000, pool=30)
+    w = small_window(seed=seed, ranks=4, samples_per_rank=60_000, slow_rank=-1, depth=12, n_sym=2000, pool=30)
     K = [0x243f6a8885a308d3, 0x13198a2e03707344, 0xa4093822299f31d0, 0x082efa98ec4e6c89,
          0x452821e638d01377, 0xbe5466cf34e90c6c, 0xc0ac29b7c97c50dd, 0x3f84d5b5b5470917]
     rng = np.random.default_rng(seed)
@@ -184,18 +184,32 @@ def _annihilator_window(seed=21):
 
 def test_planted_annihilator_frames_fold_exactly(ctx):
     win = _annihilator_window()
-    stats, _ = _compare(ctx, win, cfg={"verify": 1}, oracle=True)
-    assert stats["verified"] == 1 and stats["verify_retries"] == 0
+    stats, _ = _compare(ctx, win, cfg={"verify": 1}, ref_threads=4)
+    assert stats["verified"] == 1 and stats["verify_retries"] == 0 and stats["prefix_hits"] > 0
 
 
 def test_forced_prefix_collisions_caught_by_verify(ctx):
     """4-bit prefix-cache keys make distinct call chains collide: without verify
     the folded profiles go wrong; verify mode detects it and re-runs without the
     cache, matching the oracle exactly."""
-    win = small_window(seed=9, ranks=4, samples_per_rank=2000, slow_rank=1, depth=12, n_sym=2000, pool=400)
+    # long enough that later batches find chains cached by earlier ones
+    win = small_window(seed=9, ranks=4, samples_per_rank=100_000, slow_rank=1, depth=12, n_sym=2000, pool=400)
     win.frame_pc = _same_leaf(win)
-    ogd, _ = so.window_pipeline(win)
-    ctx.window_run(win, cfg={"debug_weak_prefix_key": 1})
-    assert ctx.groupdata()["cpu_profiles"] != ogd["cpu_profiles"]
-    stats, _ = _compare(ctx, win, cfg={"debug_weak_prefix_key": 1, "verify": 1}, oracle=True)
+    r, _, _ = ref.window_run(win, threads=4)
+    st = ctx.window_run(win, cfg={"debug_weak_prefix_key": 1})
+    assert st["prefix_hits"] > 0
+    assert ctx.groupdata()["cpu_profiles"] != r["groupdata"]["cpu_profiles"]
+    stats, _ = _compare(ctx, win, cfg={"debug_weak_prefix_key": 1, "verify": 1}, ref_threads=4)
     assert stats["verify_retries"] >= 1 and stats["verified"] == 1
+
+
+def test_device_resident_side_streams(ctx):
+    """coll_memory / side_memory = device: collectives, GPU kernel events and OS
+    counters read from HBM give the same GroupData and report as host inputs."""
+    import bench
+    win = small_window(seed=4, ranks=6, samples_per_rank=3000, slow_rank=2, depth=12, n_sym=2000, pool=100)
+    ctx.window_run(win)
+    gd, rep = ctx.groupdata(), ctx.report()
+    bench.side_to_device(win)
+    ctx.window_run(win)
+    assert ctx.groupdata() == gd and ctx.report() == rep
