@@ -193,6 +193,10 @@ struct Runner {
     }
 
     // ------------------------------------------------------------ ranks
+    const int32_t *cd_rank = nullptr, *cd_group = nullptr;
+    const uint8_t* cd_kind = nullptr;
+    const int64_t *cd_entry = nullptr, *cd_exit = nullptr;
+    int coll_rg[3] = {0, 0, 0};  // min group, max group, max kind
     void rank_space() {
         int mx = -1, mn = 0;
         for (int32_t i = 0; i < w.n_ranks; ++i) {
@@ -205,18 +209,26 @@ struct Runner {
             mx = std::max(mx, w.group_ranks[i]);
             mn = std::min(mn, w.group_ranks[i]);
         }
-        int* d_mm = dev<int>("mm", 2);
-        int init[2] = {mx, mn};
+        int* d_mm = dev<int>("mm", 5);  // max rank, min rank, min group, max group, max kind
+        int init[5] = {mx, mn, INT_MAX, INT_MIN, 0};
         STG_CUDA(cudaMemcpyAsync(d_mm, init, sizeof init, cudaMemcpyHostToDevice, st));
         auto scan = [&](const int32_t* host, uint64_t n, const char* nm) {
             if (!n) return;
             const int32_t* d = up<int32_t>(nm, host, n);
             LAUNCH(k_max_rank, grid_for(n), kThreads, n, d, d_mm, d_mm + 1);
         };
-        if (w.coll_memory == STG_MEM_DEVICE) {
-            if (w.n_coll) LAUNCH(k_max_rank, grid_for(w.n_coll), kThreads, w.n_coll, w.coll_rank, d_mm, d_mm + 1);
-        } else {
-            scan(w.coll_rank, w.n_coll, "coll_rank");
+        // collective arrays on the device (uploaded once here when host-resident);
+        // their group / kind ranges come back with the rank range
+        const uint64_t nc = w.n_coll;
+        const bool cdev = w.coll_memory == STG_MEM_DEVICE;
+        cd_rank = cdev ? w.coll_rank : (nc ? up<int32_t>("coll_rank", w.coll_rank, nc) : nullptr);
+        cd_group = cdev ? w.coll_group : (nc ? up<int32_t>("coll_group", w.coll_group, nc) : nullptr);
+        cd_kind = cdev ? w.coll_kind : (nc ? up<uint8_t>("coll_kind", w.coll_kind, nc) : nullptr);
+        cd_entry = cdev ? w.coll_entry : (nc ? up<int64_t>("coll_entry", w.coll_entry, nc) : nullptr);
+        cd_exit = cdev ? w.coll_exit : (nc ? up<int64_t>("coll_exit", w.coll_exit, nc) : nullptr);
+        if (nc) {
+            LAUNCH(k_max_rank, grid_for(nc), kThreads, nc, cd_rank, d_mm, d_mm + 1);
+            LAUNCH(k_coll_ranges, grid_for(nc), kThreads, nc, cd_group, cd_kind, d_mm + 2, d_mm + 3, d_mm + 4);
         }
         if (w.side_memory == STG_MEM_DEVICE) {
             if (w.n_gpu) LAUNCH(k_max_rank, grid_for(w.n_gpu), kThreads, w.n_gpu, w.gpu_rank, d_mm, d_mm + 1);
@@ -225,8 +237,11 @@ struct Runner {
             scan(w.gpu_rank, w.n_gpu, "gpu_rank");
             scan(w.os_rank, w.n_os, "os_rank");
         }
-        int out[2];
-        down(out, d_mm, 2);
+        int out[5];
+        down(out, d_mm, 5);
+        coll_rg[0] = out[2];
+        coll_rg[1] = out[3];
+        coll_rg[2] = out[4];
         if (out[1] < 0) fail(STG_EINVAL, "negative rank ids are not supported");
         if (out[0] >= (1 << 24)) fail(STG_EINVAL, "rank ids must be below 2^24");
         span = out[0] + 1;
@@ -243,10 +258,19 @@ struct Runner {
 
     // ------------------------------------------------------ collectives
     void collectives() {
-        d_off = dev<int64_t>("off", span);
-        d_has_off = dev<uint8_t>("has_off", span);
-        zero(d_off, span * sizeof(int64_t));
-        zero(d_has_off, span);
+        // one device block for everything the host reads back at the end (one
+        // download): offsets, straggler statistics, error and count words
+        const uint64_t sp = uint64_t(span);
+        const size_t o_ma = 8 * sp, o_ml = 16 * sp, o_zm = 24 * sp, o_fl = 32 * sp, o_err = 40 * sp,
+                     o_cnt = 40 * sp + 16, o_has = 40 * sp + 48, o_pres = 41 * sp + 48, o_hz = 42 * sp + 48,
+                     o_end = 43 * sp + 48;
+        uint8_t* cb = dev<uint8_t>("c_out", o_end);
+        zero(cb, o_end);
+        STG_CUDA(cudaMemsetAsync(cb + o_err, 0xff, 16, st));
+        d_off = reinterpret_cast<int64_t*>(cb);
+        d_has_off = cb + o_has;
+        unsigned long long* errs = reinterpret_cast<unsigned long long*>(cb + o_err);
+        unsigned long long* cnts = reinterpret_cast<unsigned long long*>(cb + o_cnt);  // n_seg, n_st, n_d, n_w
         res.n_instances = res.n_windowed = 0;
         res.iteration_times_ms.clear();
         res.offsets.assign(span, 0);
@@ -261,88 +285,83 @@ struct Runner {
         const uint64_t n = w.n_coll;
         if (n == 0) return;
         if (n >= 0xffffffffull) fail(STG_EINVAL, "too many collective events");
-        const bool cdev = w.coll_memory == STG_MEM_DEVICE;
-        const int32_t* d_rank = cdev ? w.coll_rank : static_cast<const int32_t*>(c.buf("coll_rank").p);
-        const int32_t* d_group = cdev ? w.coll_group : up<int32_t>("coll_group", w.coll_group, n);
-        const uint8_t* d_kind = cdev ? w.coll_kind : up<uint8_t>("coll_kind", w.coll_kind, n);
-        const int64_t* d_entry = cdev ? w.coll_entry : up<int64_t>("coll_entry", w.coll_entry, n);
-        const int64_t* d_exit = cdev ? w.coll_exit : up<int64_t>("coll_exit", w.coll_exit, n);
         uint64_t* key = dev<uint64_t>("c_key", n);
         uint64_t* key_s = dev<uint64_t>("c_key_s", n);
         uint32_t* idx = dev<uint32_t>("c_idx", n);
         uint32_t* idx_s = dev<uint32_t>("c_idx_s", n);
         int* d_err = dev<int>("c_err", 1);
         zero(d_err, sizeof(int));
-        int* d_rg = dev<int>("c_ranges", 3);
-        {
-            int init[3] = {INT_MAX, INT_MIN, 0};
-            STG_CUDA(cudaMemcpyAsync(d_rg, init, sizeof init, cudaMemcpyHostToDevice, st));
-        }
-        LAUNCH(k_coll_ranges, grid_for(n), kThreads, n, d_group, d_kind, d_rg, d_rg + 1, d_rg + 2);
-        int rg[3];
-        down(rg, d_rg, 3);
         auto bits_for = [](uint64_t v) { int b = 0; while (b < 64 && (v >> b)) ++b; return b; };
         const int rbits = std::max(1, bits_for(uint64_t(span - 1)));
-        const int kbits = std::max(1, bits_for(uint64_t(rg[2])));
-        const int gbits = bits_for(uint64_t(int64_t(rg[1]) - rg[0]));
+        const int kbits = std::max(1, bits_for(uint64_t(coll_rg[2])));
+        const int gbits = bits_for(uint64_t(int64_t(coll_rg[1]) - coll_rg[0]));
         const uint64_t rmask = (1ull << rbits) - 1;
-        LAUNCH(k_coll_keys, grid_for(n), kThreads, n, d_rank, d_group, d_kind, rg[0], kbits, rbits, key, idx, d_err);
+        LAUNCH(k_coll_keys, grid_for(n), kThreads, n, cd_rank, cd_group, cd_kind, coll_rg[0], kbits, rbits, key, idx,
+               d_err);
         sort_pairs(key, key_s, idx, idx_s, n, gbits + kbits + rbits);
         int64_t* s_entry = dev<int64_t>("c_sentry", n);
         int64_t* s_exit = dev<int64_t>("c_sexit", n);
-        unsigned long long* errs = dev<unsigned long long>("c_errs", 2);
-        STG_CUDA(cudaMemsetAsync(errs, 0xff, 2 * sizeof(unsigned long long), st));
         uint32_t* seg_flag = dev<uint32_t>("c_segflag", n);
         uint32_t* stream_flag = dev<uint32_t>("c_stflag", n);
-        LAUNCH(k_coll_gather, grid_for(n), kThreads, n, key_s, idx_s, d_entry, d_exit, rbits, s_entry, s_exit, errs,
+        LAUNCH(k_coll_gather, grid_for(n), kThreads, n, key_s, idx_s, cd_entry, cd_exit, rbits, s_entry, s_exit, errs,
                errs + 1, seg_flag, stream_flag);
-        unsigned long long he[2];
-        down(he, errs, 2);
-        if (he[0] != ~0ull || he[1] != ~0ull) {
-            if (he[0] <= he[1]) fail(STG_EINVAL, "collective event with entry >= exit");
+        // segments (stream, rank) and streams (group, kind), counts on the device
+        uint32_t* seg_pos = dev<uint32_t>("c_segpos", n + 1);
+        uint32_t* st_pos = dev<uint32_t>("c_stpos", n + 1);
+        {
+            uint32_t* iota = dev<uint32_t>("sel_iota", n);
+            LAUNCH(k_iota, grid_for(n), kThreads, iota, n);
+            size_t tb = 0;
+            STG_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, iota, seg_flag, seg_pos, cnts, n, st));
+            STG_CUDA(cub::DeviceSelect::Flagged(temp(tb), tb, iota, seg_flag, seg_pos, cnts, n, st));
+            STG_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, iota, stream_flag, st_pos, cnts + 1, n, st));
+            STG_CUDA(cub::DeviceSelect::Flagged(temp(tb), tb, iota, stream_flag, st_pos, cnts + 1, n, st));
+            launches += 2;
+        }
+        unsigned long long hc[4];  // entry >= exit, order, n_seg, n_st
+        {
+            std::vector<unsigned long long> h(4);
+            STG_CUDA(cudaMemcpyAsync(h.data(), errs, 16, cudaMemcpyDeviceToHost, st));
+            STG_CUDA(cudaMemcpyAsync(h.data() + 2, cnts, 16, cudaMemcpyDeviceToHost, st));
+            STG_CUDA(cudaStreamSynchronize(st));
+            ++syncs;
+            for (int q = 0; q < 4; ++q) hc[q] = h[size_t(q)];
+        }
+        if (hc[0] != ~0ull || hc[1] != ~0ull) {
+            if (hc[0] <= hc[1]) fail(STG_EINVAL, "collective event with entry >= exit");
             fail(STG_EINVAL, "collective events not time-ordered within rank");
         }
-        // segments (stream, rank) and streams (group, kind)
-        uint32_t* seg_pos = dev<uint32_t>("c_segpos", n + 1);
-        uint64_t n_seg = select_flagged(seg_flag, seg_pos, n);
-        uint32_t* st_pos = dev<uint32_t>("c_stpos", n + 1);
-        uint64_t n_st = select_flagged(stream_flag, st_pos, n);
-        std::vector<uint32_t> h_seg(n_seg + 1), h_st(n_st);
-        down(h_seg.data(), seg_pos, n_seg);
-        down(h_st.data(), st_pos, n_st);
-        h_seg[n_seg] = uint32_t(n);
-        std::vector<uint32_t> st_seg(n_st + 1), seg_stream(n_seg);
-        for (uint64_t s = 0, j = 0; s < n_st; ++s) {
-            while (h_seg[j] != h_st[s]) ++j;
-            st_seg[s] = uint32_t(j);
+        const uint64_t n_seg = hc[2], n_st = hc[3];
+        {
+            const uint32_t nn = uint32_t(n);
+            STG_CUDA(cudaMemcpyAsync(seg_pos + n_seg, &nn, 4, cudaMemcpyHostToDevice, st));
         }
-        st_seg[n_st] = uint32_t(n_seg);
-        for (uint64_t s = 0; s < n_st; ++s)
-            for (uint32_t j = st_seg[s]; j < st_seg[s + 1]; ++j) seg_stream[j] = uint32_t(s);
-        seg_pos = up<uint32_t>("c_segpos2", h_seg.data(), n_seg + 1);
-        uint32_t* d_st_seg = up<uint32_t>("c_stseg", st_seg.data(), n_st + 1);
-        uint32_t* d_seg_stream = up<uint32_t>("c_segstream", seg_stream.data(), n_seg);
+        uint32_t* d_st_seg = dev<uint32_t>("c_stseg", n_st + 1);
+        uint32_t* d_seg_stream = dev<uint32_t>("c_segstream", n_seg);
+        LAUNCH(k_stream_tables, grid_for(n_seg + n_st + 1), kThreads, cnts, seg_pos, st_pos, d_st_seg, d_seg_stream);
         uint32_t* stream_of_pos = dev<uint32_t>("c_streamofpos", n);
         incl_sum(stream_flag, stream_of_pos, n);  // 1-based
         // coarse offsets + counts
         int64_t* coarse = dev<int64_t>("c_coarse", n_seg);
-        uint32_t* kmin = dev<uint32_t>("c_kmin", n_st);
-        uint32_t* kmax = dev<uint32_t>("c_kmax", n_st);
+        uint32_t* kmm = dev<uint32_t>("c_kminmax", 2 * n_st);
+        uint32_t* kmin = kmm;
+        uint32_t* kmax = kmm + n_st;
         LAUNCH(k_coll_streams, unsigned(n_st), kThreads, int(n_st), d_st_seg, seg_pos, s_entry, coarse, kmin, kmax);
-        std::vector<uint32_t> h_kmin(n_st), h_kmax(n_st);
-        down(h_kmin.data(), kmin, n_st);
-        down(h_kmax.data(), kmax, n_st);
+        std::vector<uint32_t> h_kmm(2 * n_st);
+        down(h_kmm.data(), kmm, 2 * n_st);
+        const uint32_t* h_kmin = h_kmm.data();
+        const uint32_t* h_kmax = h_kmm.data() + n_st;
         std::vector<uint64_t> k_base(n_st + 1, 0);
         for (uint64_t s = 0; s < n_st; ++s) k_base[s + 1] = k_base[s] + h_kmin[s];
         uint64_t* d_kbase = up<uint64_t>("c_kbase", k_base.data(), n_st + 1);
-        uint32_t* first_fail = up<uint32_t>("c_ffail", h_kmin.data(), n_st);
+        uint32_t* first_fail = up<uint32_t>("c_ffail", h_kmin, n_st);
         if (k_base[n_st])
             LAUNCH(k_coll_regular, grid_for(k_base[n_st] * 32), kThreads, int(n_st), d_st_seg, seg_pos, coarse, s_entry,
                    s_exit, kmin, d_kbase, k_base[n_st], w.max_skew_ns, first_fail);
         std::vector<uint32_t> k0(n_st);
         down(k0.data(), first_fail, n_st);
         uint32_t* inst_local = dev<uint32_t>("c_instlocal", n);
-        uint32_t* d_k0 = up<uint32_t>("c_k0", k0.data(), n_st);
+        uint32_t* d_k0 = first_fail;  // = k0 on the device
         LAUNCH(k_coll_assign_regular, unsigned(std::min<uint64_t>(n_seg, 65535)), 128, int(n_st), d_st_seg, seg_pos,
                d_seg_stream, uint32_t(n_seg), d_k0, inst_local);
         std::vector<int> irregular;
@@ -364,11 +383,12 @@ struct Runner {
             for (int s : irregular) n_inst[size_t(s)] = tmp[size_t(s)];
         }
         // stream_of_pos is 1-based (inclusive scan): shift the base table
-        std::vector<uint64_t> inst_base(n_st + 1, 0);
-        for (uint64_t s = 0; s < n_st; ++s) inst_base[s + 1] = inst_base[s] + n_inst[s];
         std::vector<uint64_t> base1(n_st + 1, 0);
-        for (uint64_t s = 0; s < n_st; ++s) base1[s + 1] = inst_base[s];
-        uint64_t I = inst_base[n_st];
+        uint64_t I = 0;
+        for (uint64_t s = 0; s < n_st; ++s) {
+            base1[s + 1] = I;
+            I += n_inst[s];
+        }
         res.n_instances = I;
         uint64_t* d_ibase = up<uint64_t>("c_ibase", base1.data(), n_st + 1);
         // group membership
@@ -389,37 +409,26 @@ struct Runner {
         zero(iing, I * sizeof(unsigned));
         LAUNCH(k_coll_inst, grid_for(n), kThreads, n, key_s, nullptr, stream_of_pos, d_ibase, inst_local, s_exit,
                d_member, inst_of, imax, isize, iing, rmask);
-        // align_clocks: deltas of complete-instance events, compacted, sorted per rank
+        // align_clocks: deltas of complete-instance events, per-rank radix select
         int64_t* dval = dev<int64_t>("c_dval", n);
         uint32_t* dflag = dev<uint32_t>("c_dflag", n);
         long long* d_dmin = dev<long long>("c_dmin", 1);
         zero(d_dmin, 8);
         LAUNCH(k_coll_deltas, grid_for(n), kThreads, n, inst_of, s_exit, imax, iing, n_group, dval, dflag, d_dmin);
+        // per-rank segment lists on the device: segments sorted by their rank
+        uint32_t* d_segrank = dev<uint32_t>("c_segrank", n_seg);
+        uint32_t* d_segrank_s = dev<uint32_t>("c_segrank_s", n_seg);
+        uint32_t* d_segid = dev<uint32_t>("c_segid", n_seg);
+        uint32_t* d_rsegs = dev<uint32_t>("c_rsegs", std::max<uint64_t>(n_seg, 1));
+        uint32_t* d_rso = dev<uint32_t>("c_rso", sp + 1);
+        LAUNCH(k_seg_rank, grid_for(n_seg), kThreads, n_seg, seg_pos, key_s, rmask, d_segrank);
+        LAUNCH(k_iota, grid_for(n_seg), kThreads, d_segid, n_seg);
+        sort_pairs(d_segrank, d_segrank_s, d_segid, d_rsegs, n_seg, rbits);
+        LAUNCH(k_rank_offsets, grid_for(sp + 1), kThreads, span, d_segrank_s, n_seg, d_rso);
         const long long dmin = get1(d_dmin);
         const int dbits = std::max(1, bits_for(uint64_t(-dmin)));
-        uint64_t n_d = 0;
-        {
-            // the rank of every (stream, rank) segment -> per-rank segment lists (host CSR)
-            uint32_t* d_segrank = dev<uint32_t>("c_segrank", n_seg);
-            LAUNCH(k_seg_rank, grid_for(n_seg), kThreads, n_seg, seg_pos, key_s, rmask, d_segrank);
-            std::vector<uint32_t> h_sr(n_seg);
-            down(h_sr.data(), d_segrank, n_seg);
-            std::vector<uint32_t> rso(size_t(span) + 1, 0), rsegs(n_seg);
-            for (uint64_t j = 0; j < n_seg; ++j) ++rso[size_t(h_sr[j]) + 1];
-            for (int32_t r = 0; r < span; ++r) rso[size_t(r) + 1] += rso[size_t(r)];
-            {
-                std::vector<uint32_t> fill(rso.begin(), rso.end() - 1);
-                for (uint64_t j = 0; j < n_seg; ++j) rsegs[fill[h_sr[j]]++] = uint32_t(j);
-            }
-            uint32_t* d_rso = up<uint32_t>("c_rso", rso.data(), size_t(span) + 1);
-            uint32_t* d_rsegs = up<uint32_t>("c_rsegs", rsegs.data(), std::max<uint64_t>(n_seg, 1));
-            unsigned long long* d_nd = dev<unsigned long long>("c_nd", 1);
-            zero(d_nd, 8);
-            LAUNCH(k_coll_median_sel, unsigned(std::min<int64_t>(span, 148 * 16)), 256, int(span), d_rso, d_rsegs,
-                   seg_pos, dval, dflag, dmin, dbits, d_off, d_has_off, d_nd);
-            n_d = get1(d_nd);
-        }
-        res.have_offsets = n_d > 0;
+        LAUNCH(k_coll_median_sel, unsigned(std::min<int64_t>(span, 148 * 16)), 256, int(span), d_rso, d_rsegs, seg_pos,
+               dval, dflag, dmin, dbits, d_off, d_has_off, cnts + 2);
         // windowed complete instances ordered by max aligned exit
         unsigned long long* aexit = dev<unsigned long long>("c_aexit", I);
         zero(aexit, I * 8);  // int64 0: build_group_data initialises max_exit to 0
@@ -429,11 +438,10 @@ struct Runner {
         uint64_t* wkey_s = dev<uint64_t>("c_wkey_s", I);
         uint32_t* winst = dev<uint32_t>("c_winst", I);
         uint32_t* winst_s = dev<uint32_t>("c_winst_s", I);
-        unsigned long long* nw = dev<unsigned long long>("c_nw", 1);
-        zero(nw, 8);
+        unsigned long long* nw = cnts + 3;
         LAUNCH(k_coll_window_select, grid_for(I), kThreads, I, iing, n_group, aexit, w.window_start_ns, wkey, winst,
                nw);
-        uint64_t n_w = get1(nw);
+        const uint64_t n_w = get1(nw);
         res.n_windowed = n_w;
         sort_pairs(wkey, wkey_s, winst, winst_s, n_w);
         uint32_t* inst_w = dev<uint32_t>("c_instw", I);
@@ -442,39 +450,41 @@ struct Runner {
         long long* wmin = dev<long long>("c_wmin", n_w);
         LAUNCH(k_fill_i64, grid_for(n_w), kThreads, wmin, n_w, LLONG_MAX);
         LAUNCH(k_coll_minadj, grid_for(n), kThreads, n, key_s, inst_of, inst_w, s_entry, d_off, wmin, rmask);
-        d_lat = dev<double>("lat", uint64_t(span) * n_w);
-        LAUNCH(k_fill_f64, grid_for(uint64_t(span) * n_w), kThreads, d_lat, uint64_t(span) * n_w, nan(""));
+        d_lat = dev<double>("lat", sp * n_w);
+        LAUNCH(k_fill_f64, grid_for(sp * n_w), kThreads, d_lat, sp * n_w, nan(""));
         LAUNCH(k_coll_lateness, grid_for(n), kThreads, n, key_s, inst_of, inst_w, s_entry, d_off, wmin, n_w, d_lat,
                rmask);
-        if (n_w > 1) {
-            double* it = dev<double>("c_it", n_w);
-            LAUNCH(k_coll_itertimes, grid_for(n_w), kThreads, n_w, wkey_s, it);
-            res.iteration_times_ms.resize(n_w - 1);
-            down(res.iteration_times_ms.data(), it, n_w - 1);
-        }
+        double* it = dev<double>("c_it", std::max<uint64_t>(n_w, 1));
+        if (n_w > 1) LAUNCH(k_coll_itertimes, grid_for(n_w), kThreads, n_w, wkey_s, it);
         // detect_straggler statistics
         if (n_w) {
             double* mu = dev<double>("s_mu", n_w);
             double* sg = dev<double>("s_sg", n_w);
             uint32_t* m = dev<uint32_t>("s_m", n_w);
             LAUNCH(k_straggler_inst, grid_for(n_w * 32), kThreads, n_w, span, d_lat, cfg.k, mu, sg, m);
-            uint8_t* pres = dev<uint8_t>("s_pres", span);
-            double* ma = dev<double>("s_ma", span);
-            double* ml = dev<double>("s_ml", span);
-            double* zm = dev<double>("s_zm", span);
-            uint64_t* fl = dev<uint64_t>("s_fl", span);
-            uint8_t* hz = dev<uint8_t>("s_hz", span);
-            LAUNCH(k_straggler_rank, grid_for(uint64_t(span) * 32, kStragWarps * 32), kStragWarps * 32, n_w, span, d_lat, cfg.k, mu, sg, m, pres,
-                   ma, ml, zm, fl, hz);
-            down(res.lat_present.data(), pres, span);
-            down(res.mean_lat_all.data(), ma, span);
-            down(res.mean_lat_alert.data(), ml, span);
-            down(res.z_mean.data(), zm, span);
-            down(res.flag_count.data(), fl, span);
-            down(res.has_z.data(), hz, span);
+            LAUNCH(k_straggler_rank, grid_for(sp * 32, kStragWarps * 32), kStragWarps * 32, n_w, span, d_lat, cfg.k, mu,
+                   sg, m, cb + o_pres, reinterpret_cast<double*>(cb + o_ma), reinterpret_cast<double*>(cb + o_ml),
+                   reinterpret_cast<double*>(cb + o_zm), reinterpret_cast<uint64_t*>(cb + o_fl), cb + o_hz);
         }
-        down(res.offsets.data(), d_off, span);
-        down(res.has_offset.data(), d_has_off, span);
+        // one download for offsets, straggler statistics and counts; one for the iteration times
+        std::vector<uint8_t> h(o_end);
+        if (n_w > 1) {
+            res.iteration_times_ms.resize(n_w - 1);
+            STG_CUDA(cudaMemcpyAsync(res.iteration_times_ms.data(), it, (n_w - 1) * 8, cudaMemcpyDeviceToHost, st));
+            d2h += (n_w - 1) * 8;
+        }
+        down(h.data(), cb, o_end);
+        std::memcpy(res.offsets.data(), h.data(), 8 * sp);
+        std::memcpy(res.mean_lat_all.data(), h.data() + o_ma, 8 * sp);
+        std::memcpy(res.mean_lat_alert.data(), h.data() + o_ml, 8 * sp);
+        std::memcpy(res.z_mean.data(), h.data() + o_zm, 8 * sp);
+        std::memcpy(res.flag_count.data(), h.data() + o_fl, 8 * sp);
+        std::memcpy(res.has_offset.data(), h.data() + o_has, sp);
+        std::memcpy(res.lat_present.data(), h.data() + o_pres, sp);
+        std::memcpy(res.has_z.data(), h.data() + o_hz, sp);
+        unsigned long long nd;
+        std::memcpy(&nd, h.data() + o_cnt + 16, 8);
+        res.have_offsets = nd > 0;
     }
 
     // ------------------------------------------------------------ gpu/os

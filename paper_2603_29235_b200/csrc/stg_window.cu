@@ -143,6 +143,49 @@ __global__ void k_coll_gather(uint64_t n, const uint64_t* key, const uint32_t* i
     }
 }
 
+// Stream and segment tables on the device (no host round trip): st_seg[s] =
+// index of the first segment of stream s (seg_pos is sorted, st_pos a subset of
+// it), seg_stream[j] = stream containing segment j.
+__global__ void k_stream_tables(const unsigned long long* counts, const uint32_t* seg_pos, const uint32_t* st_pos,
+                                uint32_t* st_seg, uint32_t* seg_stream) {
+    const uint64_t n_seg = counts[0], n_st = counts[1];
+    for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < n_seg + n_st + 1;
+         t += uint64_t(gridDim.x) * blockDim.x) {
+        if (t < n_st) {
+            const uint32_t v = st_pos[t];
+            uint64_t lo = 0, hi = n_seg;
+            while (lo < hi) {
+                const uint64_t mid = (lo + hi) >> 1;
+                if (seg_pos[mid] < v) lo = mid + 1; else hi = mid;
+            }
+            st_seg[t] = uint32_t(lo);
+        } else if (t == n_st) {
+            st_seg[n_st] = uint32_t(n_seg);
+        } else {
+            const uint64_t j = t - n_st - 1;
+            const uint32_t v = seg_pos[j];
+            uint64_t lo = 0, hi = n_st;  // upper_bound(st_pos, v) - 1
+            while (lo < hi) {
+                const uint64_t mid = (lo + hi) >> 1;
+                if (st_pos[mid] <= v) lo = mid + 1; else hi = mid;
+            }
+            seg_stream[j] = uint32_t(lo - 1);
+        }
+    }
+}
+// per-rank segment lists from the segments sorted by rank: rso[r] = first
+// position of rank r in the sorted rank list
+__global__ void k_rank_offsets(int span, const uint32_t* ranks_sorted, uint64_t n_seg, uint32_t* rso) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r <= span; r += gridDim.x * blockDim.x) {
+        uint64_t lo = 0, hi = n_seg;
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (ranks_sorted[mid] < uint32_t(r)) lo = mid + 1; else hi = mid;
+        }
+        rso[r] = uint32_t(lo);
+    }
+}
+
 // One block per stream: coarse offsets (collective.cpp:49-54), counts.
 __global__ void k_coll_streams(int n_streams, const uint32_t* st_seg, const uint32_t* seg_pos,
                                const int64_t* s_entry, int64_t* coarse, uint32_t* kmin, uint32_t* kmax) {
