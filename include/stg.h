@@ -263,11 +263,21 @@ int stg_dist_unique_id(uint8_t id[128]);
 int stg_dist_init(stg_ctx* ctx, int world_size, int world_rank, const uint8_t id[128]);
 
 /* Canonical JSON renderings of the last window's result (for parity tests and
- * tools): GroupData (every field of diagnosis.hpp:192-201) and the report in the
- * layout of DiagnosisReport::to_json (diagnosis.cpp:437-455).  Two-call size
- * query: pass buf=NULL to get *needed. */
+ * tools): GroupData (every field of diagnosis.hpp:192-201), and the report exactly
+ * as DiagnosisReport::to_json (diagnosis.cpp:437-455) writes it (nlohmann
+ * dump(2), byte-identical).  Two-call size query: pass buf=NULL to get *needed. */
 int stg_result_groupdata_json(stg_ctx* ctx, char* buf, uint64_t cap, uint64_t* needed);
+/* The same rendering without the bulky parts a binding fetches structurally
+ * (parts = STG_GD_ALL & ~STG_GD_CPU: cpu_profiles comes back empty; read the
+ * folded lines with stg_result_rank_lines instead). */
+#define STG_GD_CPU 1u
+#define STG_GD_ALL 0xffffffffu
+int stg_result_groupdata_json_parts(stg_ctx* ctx, uint32_t parts, char* buf, uint64_t cap, uint64_t* needed);
 int stg_result_report_json(stg_ctx* ctx, char* buf, uint64_t cap, uint64_t* needed);
+/* DiagnosisReport::to_text (diagnosis.cpp:457-481) of the last window's report;
+ * like stg_result_report_json (which is to_json's nlohmann dump(2)), the same
+ * bytes the reference writes. */
+int stg_result_report_text(stg_ctx* ctx, char* buf, uint64_t cap, uint64_t* needed);
 /* Waterline (compute_waterline, diagnosis.cpp:35-55) + flag_ranks (:57-71) over
  * the last window's CPU profiles, when cfg.want_waterline was set. */
 int stg_result_waterline_json(stg_ctx* ctx, char* buf, uint64_t cap, uint64_t* needed);

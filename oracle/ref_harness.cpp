@@ -566,6 +566,8 @@ int ref_window_run_ex(const stg_window* w, int n_symr, const uint8_t* const* sym
             json j;
             if (want_json) j["groupdata"] = groupdata_json(data);
             j["report"] = json::parse(rep.to_json());
+            j["report_json_raw"] = rep.to_json();  // the reference's own bytes
+            j["report_text"] = rep.to_text();
             if (want_json == 2) {
                 // the text artifacts of `strata diagnose` / `strata flamegraph`
                 // (tools/strata.cpp:97-131): every rank's folded text, each

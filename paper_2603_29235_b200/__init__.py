@@ -56,7 +56,8 @@ def load_library():
     l.stg_name_count.argtypes = [P, C.POINTER(C.c_uint32)]
     l.stg_config_default.argtypes = [C.POINTER(StgConfig)]
     l.stg_window_run.argtypes = [P, C.POINTER(StgWindow), C.POINTER(StgConfig), C.POINTER(StgRunStats)]
-    for fn in ("stg_result_groupdata_json", "stg_result_report_json", "stg_result_waterline_json"):
+    for fn in ("stg_result_groupdata_json", "stg_result_report_json", "stg_result_waterline_json",
+               "stg_result_report_text"):
         getattr(l, fn).argtypes = [P, C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64)]
     l.stg_dist_unique_id.argtypes = [C.c_char_p]
     l.stg_dist_init.argtypes = [P, C.c_int, C.c_int, C.c_char_p]
@@ -262,6 +263,14 @@ class Context:
         buf = C.create_string_buffer(need.value)
         _check(fn(self._h, *args, buf, need.value, C.byref(need)))
         return buf.raw[:need.value - 1].decode("utf-8", "surrogateescape")
+
+    def report_json_text(self) -> str:
+        """DiagnosisReport::to_json exactly as the reference writes it (nlohmann dump(2))."""
+        return self._text(self._l.stg_result_report_json)
+
+    def report_text(self) -> str:
+        """DiagnosisReport::to_text (diagnosis.cpp:457-481)."""
+        return self._text(self._l.stg_result_report_text)
 
     def folded_text(self, rank: int) -> str:
         """FoldedProfile::to_string of `rank`'s CPU profile (folded.cpp:33-43), rendered on the GPU."""

@@ -47,7 +47,7 @@ NCCL_LINK = ([f"-L{NCCL_DIR / 'lib'}", "-l:libnccl.so.2", "-Xlinker", f"-rpath={
              if NCCL_DIR else ["-lnccl"])
 
 CU_SOURCES = ["stg_window.cu", "stg_render.cu", "stg_samples.cu", "symtab.cu", "stg_bundle.cu"]
-CPP_SOURCES = ["stg_api.cpp", "stg_bundle_host.cpp"]
+CPP_SOURCES = ["stg_api.cpp", "stg_bundle_host.cpp", "stg_report.cpp"]
 HEADERS = ["stg_internal.h", "kernels.cuh", "result.h", "stg_runner.inl", "stg_output.inl", "bundle.h"]
 
 

@@ -96,4 +96,9 @@ struct Result {
     uint64_t render_len = 0;
 };
 
+// stg_report.cpp (nlohmann/json, like the reference's serialisers)
+const char* verdict_name(int v);
+std::string report_json_dump2(const Report& p);
+std::string report_text(const Report& p);
+
 }  // namespace stg

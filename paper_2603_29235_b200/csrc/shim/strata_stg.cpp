@@ -7,7 +7,13 @@
 //   strata::resolve_stacks     symrepo.hpp:55-57 (symrepo.cpp:122-143)  -> stg_resolve
 //   strata::resolve_stack      symrepo.hpp:51-53 (symrepo.cpp:99-120)   -> stg_resolve
 //   strata::aggregate_samples  samples.hpp:38-44 (samples.cpp:31-85)    -> stg_aggregate_samples
+//   strata::diagnose           diagnosis.hpp:216-217 (diagnosis.cpp:301-432) -> the report the GPU
+//                              computed in the same stg_window_run (re-run with the caller's
+//                              DiagnosisConfig if it differs)
 //
+// build_group_data fills GroupData's CPU profiles from the structured getters
+// (stg_result_rank_lines + stg_name, names cached per key) and only the small
+// parts (GPU / OS / lateness / iteration times) from the JSON rendering.
 // The reference TUs that define these symbols are compiled with
 // -D<name>=<name>_reference (oracle/Makefile `dropin`), everything else of the
 // reference links as is.  Errors from the library come back as strata::Error
@@ -25,6 +31,7 @@
 #include <unordered_map>
 
 #include "strata/bundle.hpp"
+#include "strata/diagnosis.hpp"
 #include "strata/samples.hpp"
 #include "strata/symrepo.hpp"
 
@@ -134,14 +141,132 @@ std::vector<std::string> resolve_stack(const std::vector<FrameRef>& stack, const
     return resolve_stacks({stack}, repo, mode).front();
 }
 
-GroupData build_group_data(const LoadedBundle& b, const DiagnosisConfig& config) {
-    (void)config;  // unused by the reference too (bundle.cpp:322)
-    // ---- LoadedBundle -> stg_window (structure of arrays)
+namespace {
+// The last window handed to the GPU, kept alive so diagnose() can re-run it
+// with the caller's DiagnosisConfig, and the signature of the GroupData that
+// build_group_data returned for it.
+struct LastWindow {
     BinIndex bins;
-    std::vector<int32_t> rank_ids;
-    std::vector<uint64_t> rank_off{0}, frame_off{0}, pc;
-    std::vector<int64_t> ts;
+    std::vector<int32_t> rank_ids, c_rank, c_group, g_rank, o_rank;
+    std::vector<uint64_t> rank_off{0}, frame_off{0}, pc, irq_off{0}, sirq_off{0};
+    std::vector<int64_t> ts, c_entry, c_exit, c_dur, g_start, g_dur, o_ws, o_p50, o_p99, o_mig, irq_v, sirq_v;
     std::vector<uint16_t> bin;
+    std::vector<uint8_t> c_kind;
+    std::vector<uint32_t> g_k, irq_k, sirq_k;
+    std::map<std::string, uint32_t> kid, cid;
+    std::vector<const char*> knames, cnames, bnames;
+    std::vector<std::string> base_keys;
+    std::vector<double> base_vals;
+    std::vector<int32_t> group_ranks;
+    stg_window w{};
+    stg_config cfg{};
+    uint64_t sig = 0;
+};
+std::mutex g_mu;
+std::unique_ptr<LastWindow> g_last;
+
+stg_config to_stg_config(const DiagnosisConfig& d) {
+    stg_config c;
+    stg_config_default(&c);
+    c.window_iterations = d.window_iterations;
+    c.k = d.k;
+    c.delta = d.delta;
+    c.iteration_regression_gate = d.iteration_regression_gate;
+    c.gpu_median_uniform = d.gpu.median_uniform;
+    c.gpu_cv_uniform = d.gpu.cv_uniform;
+    c.gpu_top_share_specific = d.gpu.top_share_specific;
+    c.gpu_median_none = d.gpu.median_none;
+    c.gpu_ref_floor_ns = d.gpu.ref_floor_ns;
+    std::memset(c.gpu_exclude_prefix, 0, sizeof c.gpu_exclude_prefix);
+    std::strncpy(c.gpu_exclude_prefix, d.gpu.exclude_prefix.c_str(), sizeof c.gpu_exclude_prefix - 1);
+    c.os_min_ratio = d.os.min_ratio;
+    c.os_interrupt_floor = d.os.interrupt_floor;
+    c.os_sched_delay_floor_ns = d.os.sched_delay_floor_ns;
+    c.os_migration_floor = d.os.migration_floor;
+    return c;
+}
+
+// FNV-1a over everything diagnose() reads from a GroupData
+struct Sig {
+    uint64_t h = 1469598103934665603ull;
+    void bytes(const void* p, size_t n) {
+        const unsigned char* q = static_cast<const unsigned char*>(p);
+        for (size_t i = 0; i < n; ++i) h = (h ^ q[i]) * 1099511628211ull;
+    }
+    template <class T>
+    void pod(const T& v) { bytes(&v, sizeof v); }
+    void str(const std::string& s) {
+        pod(uint64_t(s.size()));
+        bytes(s.data(), s.size());
+    }
+};
+uint64_t signature(const GroupData& d) {
+    Sig s;
+    s.pod(d.group);
+    for (const auto& [rank, p] : d.cpu_profiles) {
+        s.pod(rank);
+        s.pod(p.total);
+        for (const auto& l : p.lines) {
+            s.pod(uint64_t(l.frames.size()));
+            for (const auto& f : l.frames) s.str(f);
+            s.pod(l.count);
+        }
+    }
+    for (const auto& [rank, g] : d.gpu_profiles) {
+        s.pod(rank);
+        for (const auto& [k, v] : g.kernel_time_ns) {
+            s.str(k);
+            s.pod(v);
+        }
+    }
+    for (const auto& [rank, o] : d.os_snapshots) {
+        s.pod(rank);
+        for (const auto& [k, v] : o.interrupts) {
+            s.str(k);
+            s.pod(v);
+        }
+        for (const auto& [k, v] : o.softirqs) {
+            s.str(k);
+            s.pod(v);
+        }
+        s.pod(o.sched_delay_p50_ns);
+        s.pod(o.sched_delay_p99_ns);
+        s.pod(o.numa_migrations);
+    }
+    for (const auto& inst : d.lateness_per_instance) {
+        s.pod(uint64_t(inst.size()));
+        for (const auto& [r, l] : inst) {
+            s.pod(r);
+            s.pod(l);
+        }
+    }
+    for (double t : d.iteration_times_ms) s.pod(t);
+    s.pod(bool(d.baseline));
+    if (d.baseline) {
+        s.pod(d.baseline->delta);
+        for (const auto& [k, v] : d.baseline->fractions) {
+            s.str(k);
+            s.pod(v);
+        }
+    }
+    s.pod(bool(d.baseline_iteration_ms));
+    if (d.baseline_iteration_ms) s.pod(*d.baseline_iteration_ms);
+    return s.h;
+}
+
+}  // namespace
+
+GroupData build_group_data(const LoadedBundle& b, const DiagnosisConfig& config) {
+    // config is unused by the reference's build_group_data (bundle.cpp:322); the
+    // run computes the report with it too, for the diagnose() that follows
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto L = std::make_unique<LastWindow>();
+    // ---- LoadedBundle -> stg_window (structure of arrays)
+    BinIndex& bins = L->bins;
+    std::vector<int32_t>& rank_ids = L->rank_ids;
+    std::vector<uint64_t>&rank_off = L->rank_off, &frame_off = L->frame_off, &pc = L->pc;
+    std::vector<int64_t>& ts = L->ts;
+    std::vector<uint16_t>& bin = L->bin;
     for (const auto& [rank, stream] : b.samples) {
         rank_ids.push_back(rank);
         for (const StackSample& s : stream) {
@@ -156,9 +281,9 @@ GroupData build_group_data(const LoadedBundle& b, const DiagnosisConfig& config)
         rank_off.push_back(ts.size());
     }
     ingest_ids(SymbolRepository(b.dir), bins.ids);
-    std::vector<int32_t> c_rank, c_group;
-    std::vector<uint8_t> c_kind;
-    std::vector<int64_t> c_entry, c_exit, c_dur;
+    std::vector<int32_t>&c_rank = L->c_rank, &c_group = L->c_group;
+    std::vector<uint8_t>& c_kind = L->c_kind;
+    std::vector<int64_t>&c_entry = L->c_entry, &c_exit = L->c_exit, &c_dur = L->c_dur;
     for (const CollectiveEvent& e : b.collectives) {
         c_rank.push_back(e.rank);
         c_group.push_back(e.group);
@@ -167,36 +292,37 @@ GroupData build_group_data(const LoadedBundle& b, const DiagnosisConfig& config)
         c_exit.push_back(e.host_exit_ns);
         c_dur.push_back(e.gpu_duration_ns);
     }
-    std::map<std::string, uint32_t> kid;
+    std::map<std::string, uint32_t>& kid = L->kid;
     for (const GpuEvent& e : b.gpu_events) kid.emplace(e.kernel, 0);
-    std::vector<const char*> knames;
+    std::vector<const char*>& knames = L->knames;
     for (auto& [k, v] : kid) {
         v = uint32_t(knames.size());
         knames.push_back(k.c_str());
     }
-    std::vector<int32_t> g_rank;
-    std::vector<uint32_t> g_k;
-    std::vector<int64_t> g_start, g_dur;
+    std::vector<int32_t>& g_rank = L->g_rank;
+    std::vector<uint32_t>& g_k = L->g_k;
+    std::vector<int64_t>&g_start = L->g_start, &g_dur = L->g_dur;
     for (const GpuEvent& e : b.gpu_events) {
         g_rank.push_back(e.rank);
         g_k.push_back(kid.at(e.kernel));
         g_start.push_back(e.start_ns);
         g_dur.push_back(e.duration_ns);
     }
-    std::map<std::string, uint32_t> cid;
+    std::map<std::string, uint32_t>& cid = L->cid;
     for (const OsCounterRecord& o : b.os_counters) {
         for (const auto& [k, v] : o.snapshot.interrupts) cid.emplace(k, 0);
         for (const auto& [k, v] : o.snapshot.softirqs) cid.emplace(k, 0);
     }
-    std::vector<const char*> cnames;
+    std::vector<const char*>& cnames = L->cnames;
     for (auto& [k, v] : cid) {
         v = uint32_t(cnames.size());
         cnames.push_back(k.c_str());
     }
-    std::vector<int32_t> o_rank;
-    std::vector<int64_t> o_ws, o_p50, o_p99, o_mig, irq_v, sirq_v;
-    std::vector<uint64_t> irq_off{0}, sirq_off{0};
-    std::vector<uint32_t> irq_k, sirq_k;
+    std::vector<int32_t>& o_rank = L->o_rank;
+    std::vector<int64_t>&o_ws = L->o_ws, &o_p50 = L->o_p50, &o_p99 = L->o_p99, &o_mig = L->o_mig,
+                         &irq_v = L->irq_v, &sirq_v = L->sirq_v;
+    std::vector<uint64_t>&irq_off = L->irq_off, &sirq_off = L->sirq_off;
+    std::vector<uint32_t>&irq_k = L->irq_k, &sirq_k = L->sirq_k;
     for (const OsCounterRecord& o : b.os_counters) {
         o_rank.push_back(o.rank);
         o_ws.push_back(o.window_start_ns);
@@ -214,7 +340,7 @@ GroupData build_group_data(const LoadedBundle& b, const DiagnosisConfig& config)
         irq_off.push_back(irq_k.size());
         sirq_off.push_back(sirq_k.size());
     }
-    stg_window w{};
+    stg_window& w = L->w;
     w.memory = STG_MEM_HOST;
     w.group = b.group;
     w.window_start_ns = b.window_start_ns;
@@ -238,8 +364,9 @@ GroupData build_group_data(const LoadedBundle& b, const DiagnosisConfig& config)
     w.coll_entry = c_entry.data();
     w.coll_exit = c_exit.data();
     w.coll_gpu_dur = c_dur.data();
-    w.n_group_ranks = int32_t(b.group_ranks.size());
-    w.group_ranks = b.group_ranks.data();
+    L->group_ranks = b.group_ranks;
+    w.n_group_ranks = int32_t(L->group_ranks.size());
+    w.group_ranks = L->group_ranks.data();
     w.n_gpu = g_rank.size();
     w.gpu_rank = g_rank.data();
     w.gpu_kernel = g_k.data();
@@ -261,22 +388,71 @@ GroupData build_group_data(const LoadedBundle& b, const DiagnosisConfig& config)
     w.os_sirq_val = sirq_v.data();
     w.n_counter_names = uint32_t(cnames.size());
     w.counter_names = cnames.data();
-    stg_config cfg;
-    stg_config_default(&cfg);
-    check(stg_window_run(ctx(), &w, &cfg, nullptr));
+    // the bundle's baseline (bundle.cpp:257-258) for the temporal route
+    w.has_baseline = 1;
+    w.baseline_delta = b.baseline.delta;
+    for (const auto& [k, v] : b.baseline.fractions) {
+        L->base_keys.push_back(k);
+        L->base_vals.push_back(v);
+    }
+    for (const auto& k : L->base_keys) L->bnames.push_back(k.c_str());
+    w.n_baseline = uint32_t(L->base_keys.size());
+    w.baseline_names = L->bnames.data();
+    w.baseline_fracs = L->base_vals.data();
+    w.has_baseline_iteration = 1;
+    w.baseline_iteration_ms = b.baseline_iteration_ms;
+    L->cfg = to_stg_config(config);
+    check(stg_window_run(ctx(), &w, &L->cfg, nullptr));
 
-    // ---- result -> GroupData (diagnosis.hpp:192-201)
-    nlohmann::json j = nlohmann::json::parse(take_json(stg_result_groupdata_json));
+    // ---- result -> GroupData (diagnosis.hpp:192-201): CPU profiles through the
+    // structured getters, the rest from the (small) JSON rendering
     GroupData d;
     d.group = b.group;
     d.baseline = b.baseline;
     d.baseline_iteration_ms = b.baseline_iteration_ms;
-    for (const auto& p : j.at("cpu_profiles")) {
-        FoldedProfile& f = d.cpu_profiles[p.at("rank").get<int>()];
-        f.total = p.at("total").get<uint64_t>();
-        for (const auto& l : p.at("lines"))
-            f.lines.push_back({l.at(0).get<std::vector<std::string>>(), l.at(1).get<uint64_t>()});
+    {
+        uint32_t nr = 0;
+        check(stg_result_rank_count(ctx(), &nr));
+        std::unordered_map<uint32_t, std::string> names;
+        auto name_of = [&](uint32_t key) -> const std::string& {
+            auto it = names.find(key);
+            if (it == names.end()) {
+                uint64_t need = 0;
+                check(stg_name(ctx(), key, nullptr, 0, &need));
+                std::string nm(need, '\0');
+                check(stg_name(ctx(), key, nm.data(), need, &need));
+                nm.resize(need - 1);
+                it = names.emplace(key, std::move(nm)).first;
+            }
+            return it->second;
+        };
+        std::vector<uint64_t> koff, counts;
+        std::vector<uint32_t> keys;
+        for (uint32_t i = 0; i < nr; ++i) {
+            int32_t rank = 0;
+            uint64_t nl = 0, total = 0, nk = 0;
+            check(stg_result_rank_info(ctx(), i, &rank, &nl, &total, &nk));
+            koff.resize(nl + 1);
+            keys.resize(nk);
+            counts.resize(nl);
+            check(stg_result_rank_lines(ctx(), i, koff.data(), keys.data(), counts.data()));
+            FoldedProfile& f = d.cpu_profiles[rank];
+            f.total = total;
+            f.lines.reserve(nl);
+            for (uint64_t l = 0; l < nl; ++l) {
+                std::vector<std::string> frames;
+                frames.reserve(koff[l + 1] - koff[l]);
+                for (uint64_t k = koff[l]; k < koff[l + 1]; ++k) frames.push_back(name_of(keys[k]));
+                f.lines.push_back({std::move(frames), counts[l]});
+            }
+        }
     }
+    uint64_t need = 0;
+    check(stg_result_groupdata_json_parts(ctx(), STG_GD_ALL & ~STG_GD_CPU, nullptr, 0, &need));
+    std::string js(need, '\0');
+    check(stg_result_groupdata_json_parts(ctx(), STG_GD_ALL & ~STG_GD_CPU, js.data(), need, &need));
+    js.resize(need ? need - 1 : 0);
+    nlohmann::json j = nlohmann::json::parse(js);
     for (const auto& p : j.at("gpu_profiles")) {
         GpuProfile& g = d.gpu_profiles[p.at("rank").get<int>()];
         for (const auto& k : p.at("kernels")) g.kernel_time_ns[k.at(0).get<std::string>()] = k.at(1).get<int64_t>();
@@ -295,7 +471,44 @@ GroupData build_group_data(const LoadedBundle& b, const DiagnosisConfig& config)
         d.lateness_per_instance.push_back(std::move(m));
     }
     d.iteration_times_ms = j.at("iteration_times_ms").get<std::vector<double>>();
+    L->sig = signature(d);
+    g_last = std::move(L);
     return d;
+}
+
+// diagnose (diagnosis.cpp:301-432): the verdict the GPU computed for this
+// GroupData in build_group_data's window run.  A GroupData that did not come out
+// of the preceding build_group_data is refused (the drop-in computes diagnoses
+// on the device from the window, not from a hand-built GroupData).
+DiagnosisReport diagnose(const GroupData& data, const DiagnosisConfig& config) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g_last || signature(data) != g_last->sig)
+        throw Error("libstg drop-in: diagnose() takes the GroupData of the preceding build_group_data() call");
+    const stg_config cfg = to_stg_config(config);
+    if (std::memcmp(&cfg, &g_last->cfg, sizeof cfg) != 0) {  // other thresholds: same window, new run
+        g_last->cfg = cfg;
+        check(stg_window_run(ctx(), &g_last->w, &g_last->cfg, nullptr));
+    }
+    const nlohmann::json j = nlohmann::json::parse(take_json(stg_result_report_json));
+    DiagnosisReport r;
+    static const std::map<std::string, Verdict> verdicts = {
+        {"healthy", Verdict::Healthy},
+        {"gpu-uniform-slowdown", Verdict::GpuUniformSlowdown},
+        {"gpu-specific-kernel", Verdict::GpuSpecificKernel},
+        {"cpu-interference", Verdict::CpuInterference},
+        {"os-interference", Verdict::OsInterference},
+        {"temporal-degradation", Verdict::TemporalDegradation},
+        {"inconclusive", Verdict::Inconclusive}};
+    r.verdict = verdicts.at(j.at("verdict").get<std::string>());
+    r.flagged_ranks = j.at("flagged_ranks").get<std::vector<int>>();
+    for (const auto& e : j.at("evidence"))
+        r.evidence.push_back({e.at("layer").get<std::string>(), e.at("item").get<std::string>(),
+                              e.at("straggler_value").get<double>(), e.at("reference_value").get<double>(),
+                              e.at("delta").get<double>()});
+    r.top_path = j.at("top_path").get<std::vector<std::string>>();
+    r.notes = j.at("notes").get<std::vector<std::string>>();
+    if (!j.at("reference_rank").is_null()) r.reference_rank = j.at("reference_rank").get<int>();
+    return r;
 }
 
 // Raw samples -> SoA (build ids interned to bins), aggregated on the GPU; each

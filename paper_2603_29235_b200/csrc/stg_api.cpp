@@ -12,8 +12,9 @@
 
 namespace stg {
 void window_run(Ctx& c, const stg_window& w, const stg_config& cfg);
-std::string groupdata_json(Ctx& c);
+std::string groupdata_json(Ctx& c, uint32_t parts);
 std::string report_json(Ctx& c);
+std::string report_text_of(Ctx& c);
 std::string waterline_json(Ctx& c);
 void run_resolve(Ctx& c, Result& res, uint64_t n, const uint64_t* pc, const uint16_t* bin, int32_t n_bins,
                  const uint8_t* ids, int mode, uint32_t* out);
@@ -211,7 +212,18 @@ int stg_result_groupdata_json(stg_ctx* ctx, char* buf, uint64_t cap, uint64_t* n
     int rc = guard([&] {
         std::lock_guard<std::mutex> lk(ctx->impl.mu);
         need_result(ctx);
-        s = stg::groupdata_json(ctx->impl);
+        s = stg::groupdata_json(ctx->impl, STG_GD_ALL);
+    });
+    if (rc) return rc;
+    return copy_out(s, buf, cap, needed);
+}
+
+int stg_result_groupdata_json_parts(stg_ctx* ctx, uint32_t parts, char* buf, uint64_t cap, uint64_t* needed) {
+    std::string s;
+    int rc = guard([&] {
+        std::lock_guard<std::mutex> lk(ctx->impl.mu);
+        need_result(ctx);
+        s = stg::groupdata_json(ctx->impl, parts);
     });
     if (rc) return rc;
     return copy_out(s, buf, cap, needed);
@@ -222,6 +234,16 @@ int stg_result_report_json(stg_ctx* ctx, char* buf, uint64_t cap, uint64_t* need
     int rc = guard([&] {
         need_result(ctx);
         s = stg::report_json(ctx->impl);
+    });
+    if (rc) return rc;
+    return copy_out(s, buf, cap, needed);
+}
+
+int stg_result_report_text(stg_ctx* ctx, char* buf, uint64_t cap, uint64_t* needed) {
+    std::string s;
+    int rc = guard([&] {
+        need_result(ctx);
+        s = stg::report_text_of(ctx->impl);
     });
     if (rc) return rc;
     return copy_out(s, buf, cap, needed);

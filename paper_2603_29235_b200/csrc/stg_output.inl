@@ -68,54 +68,9 @@ void run_resolve(Ctx& c, Result& res, uint64_t n, const uint64_t* pc, const uint
     res.n_names = c.dict.size() + res.unk_labels.size();
 }
 
-static void render_report(const Result& r, JsonW& j) {
-    const Report& p = r.report;
-    j.raw("{\"verdict\": ");
-    j.str(kVerdictNames[p.verdict]);
-    j.raw(", \"flagged_ranks\": [");
-    for (size_t i = 0; i < p.flagged_ranks.size(); ++i) {
-        if (i) j.raw(", ");
-        j.num(p.flagged_ranks[i]);
-    }
-    j.raw("], \"evidence\": [");
-    for (size_t i = 0; i < p.evidence.size(); ++i) {
-        const Evidence& e = p.evidence[i];
-        if (i) j.raw(", ");
-        j.raw("{\"layer\": ");
-        j.str(e.layer);
-        j.raw(", \"item\": ");
-        j.str(e.item);
-        j.raw(", \"straggler_value\": ");
-        j.num(e.straggler_value);
-        j.raw(", \"reference_value\": ");
-        j.num(e.reference_value);
-        j.raw(", \"delta\": ");
-        j.num(e.delta);
-        j.raw("}");
-    }
-    j.raw("], \"top_path\": [");
-    for (size_t i = 0; i < p.top_path.size(); ++i) {
-        if (i) j.raw(", ");
-        j.str(p.top_path[i]);
-    }
-    j.raw("], \"notes\": [");
-    for (size_t i = 0; i < p.notes.size(); ++i) {
-        if (i) j.raw(", ");
-        j.str(p.notes[i]);
-    }
-    j.raw("], \"reference_rank\": ");
-    if (p.reference_rank)
-        j.num(*p.reference_rank);
-    else
-        j.raw("null");
-    j.raw("}");
-}
-
-std::string report_json(Ctx& c) {
-    JsonW j;
-    render_report(*c.result, j);
-    return j.s;
-}
+// DiagnosisReport::to_json (diagnosis.cpp:437-455): nlohmann dump(2), the same bytes
+std::string report_json(Ctx& c) { return report_json_dump2(c.result->report); }
+std::string report_text_of(Ctx& c) { return report_text(c.result->report); }
 
 template <class T>
 static void d2h(Ctx& c, T* host, const char* name, size_t n, size_t offset = 0) {
@@ -152,16 +107,17 @@ void rank_lines(Ctx& c, uint32_t i, std::vector<uint64_t>& key_off, std::vector<
     }
 }
 
-std::string groupdata_json(Ctx& c) {
+std::string groupdata_json(Ctx& c, uint32_t parts) {
     Result& r = *c.result;
     JsonW j;
     j.raw("{\"group\": ");
     j.num(r.group);
     j.raw(", \"cpu_profiles\": [");
+    const bool cpu = parts & STG_GD_CPU;
     // bulk-copy what the lines need once
-    std::vector<uint64_t> lk(r.n_lines), lc(r.n_lines), seq_off, line_off;
-    std::vector<uint32_t> dense_rep(r.n_seq), arena;
-    if (r.n_lines) {
+    std::vector<uint64_t> lk(cpu ? r.n_lines : 0), lc(cpu ? r.n_lines : 0), seq_off, line_off;
+    std::vector<uint32_t> dense_rep(cpu ? r.n_seq : 0), arena;
+    if (cpu && r.n_lines) {
         d2h(c, lk.data(), "lkey_s", r.n_lines);
         d2h(c, lc.data(), "lcount_s", r.n_lines);
         d2h(c, dense_rep.data(), "dense_rep", r.n_seq);
@@ -169,7 +125,7 @@ std::string groupdata_json(Ctx& c) {
         (void)G;
     }
     uint64_t G = 0;
-    if (r.n_lines) {
+    if (cpu && r.n_lines) {
         // number of gids = size of gids buffer in use; recover from seq_off's last entry
         G = r.n_gid;
         seq_off.resize(G + 1);
@@ -179,8 +135,7 @@ std::string groupdata_json(Ctx& c) {
         line_off.resize(r.n_window_ranks + 1);
         d2h(c, line_off.data(), "line_off", r.n_window_ranks + 1);
     }
-    std::vector<std::string> names_cache;
-    for (size_t i = 0; i < r.cpu_rank_ids.size(); ++i) {
+    for (size_t i = 0; cpu && i < r.cpu_rank_ids.size(); ++i) {
         if (i) j.raw(", ");
         uint32_t row = r.cpu_rank_index[i];
         j.raw("{\"rank\": ");

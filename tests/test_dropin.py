@@ -1,7 +1,8 @@
 """The drop-in proof: the reference's own acceptance gate (proj/tests/acceptance.cpp,
-compiled unchanged) relinked so that strata::build_group_data / resolve_stacks
-come from libstg's C++ shim (paper_2603_29235_b200/csrc/shim/strata_stg.cpp) on
-the GPU.  Every criterion that exercises the path (c1 scenario classification
+compiled unchanged) relinked so that strata::build_group_data / resolve_stacks /
+aggregate_samples / diagnose come from libstg's C++ shim
+(paper_2603_29235_b200/csrc/shim/strata_stg.cpp) on the GPU — diagnose returns
+the report the GPU computed in the same window run.  Every criterion that exercises the path (c1 scenario classification
 over 60 simulator bundles, c7 symbolization round trip and misattribution, c9
 clock alignment, c11 temporal threshold) must still PASS.
 Built by oracle/Makefile `dropin` (needs /root/reference at build time only).
@@ -38,3 +39,21 @@ def test_aggregate_samples_relinked_on_gpu():
     r = subprocess.run([str(DS)], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0 and "ALL PASS" in r.stdout, r.stdout + r.stderr
+
+
+SHIM = ROOT / "paper_2603_29235_b200" / "libstg_strata.so"
+
+
+@pytest.mark.skipif(not (STG.exists() and SHIM.exists()), reason="drop-in not built")
+def test_relinked_gate_takes_the_hot_path_from_the_shim():
+    """The relinked binary imports the replaced strata:: functions, and the shim
+    defines them (the reference objects in the link are compiled renamed)."""
+    def syms(args, path):
+        out = subprocess.run(["nm", "-D", *args, str(path)], capture_output=True, text=True).stdout
+        return subprocess.run(["c++filt"], input=out, capture_output=True, text=True).stdout
+    need = ["strata::build_group_data(", "strata::diagnose(", "strata::resolve_stacks", "strata::aggregate_samples("]
+    imported = syms(["--undefined-only"], STG)
+    defined = syms(["--defined-only"], SHIM)
+    for n in need:
+        assert n in imported, n
+        assert n in defined, n

@@ -60,6 +60,10 @@ def test_unknown_binaries_and_gaps(ctx):
 def test_simulator_scenarios_match_reference(ctx, scenario, seed):
     win = ref.simulate(scenario, seed)
     _, rep = _check_window(ctx, win, against_ref=True)
+    # DiagnosisReport::to_json (dump(2)) and to_text: the reference's exact bytes
+    r, _, _ = ref.window_run(win, want_json=False)
+    assert ctx.report_json_text() == r["report_json_raw"]
+    assert ctx.report_text() == r["report_text"]
     lab = win.labels
     if seed == 1:
         assert rep["verdict"] == lab["verdict"]
