@@ -360,6 +360,23 @@ int stg_result_folded_text(stg_ctx* ctx, int32_t rank, char* buf, uint64_t cap, 
 int stg_result_diff_folded(stg_ctx* ctx, int32_t rank_a, int32_t rank_b, char* buf, uint64_t cap,
                            uint64_t* needed);
 
+/* Flame graphs of the last window (render_flamegraph / render_diff_flamegraph,
+ * svg.cpp:157-172, options as SvgOptions svg.hpp): the same SVG bytes the
+ * reference writes for FoldedProfile(rank) — or for the diff of rank_before's
+ * profile against rank_after's — from the device-resident folded lines.  opts
+ * NULL = the reference defaults (1200, 16, 0.001, "flame graph").  Two-call size
+ * query; "unknown rank id: <rank>" for a rank without a CPU profile. */
+typedef struct stg_svg_options {
+    int32_t width;
+    int32_t row_height;
+    double min_fraction;
+    const char* title;
+} stg_svg_options;
+int stg_result_flamegraph_svg(stg_ctx* ctx, int32_t rank, const stg_svg_options* opts, char* buf, uint64_t cap,
+                              uint64_t* needed);
+int stg_result_diff_flamegraph_svg(stg_ctx* ctx, int32_t rank_before, int32_t rank_after,
+                                   const stg_svg_options* opts, char* buf, uint64_t cap, uint64_t* needed);
+
 #ifdef __cplusplus
 }
 #endif

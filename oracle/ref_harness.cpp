@@ -32,6 +32,7 @@
 #include "json.hpp"
 #include "stg.h"
 #include "strata/bundle.hpp"
+#include "strata/svg.hpp"
 #include "strata/collective.hpp"
 #include "strata/diagnosis.hpp"
 #include "strata/folded.hpp"
@@ -591,7 +592,24 @@ int ref_window_run_ex(const stg_window* w, int n_symr, const uint8_t* const* sym
                     add_diff(ranks[1], ranks[0]);
                 }
                 if (!ranks.empty()) add_diff(ranks[0], ranks[0]);
-                j["artifacts"] = {{"folded", folded}, {"diffs", diffs}};
+                // flame graphs (svg.cpp:157-172) with the CLI's titles (tools/strata.cpp:119-148)
+                json svgs = json::array(), svg_diffs = json::array();
+                for (size_t q = 0; q < ranks.size() && q < 6; ++q) {
+                    SvgOptions o;
+                    o.title = "rank " + std::to_string(ranks[q]);
+                    svgs.push_back(json::array({ranks[q], render_flamegraph(data.cpu_profiles.at(ranks[q]), o)}));
+                }
+                auto add_svg_diff = [&](int a, int b) {
+                    SvgOptions o;
+                    o.title = "rank " + std::to_string(a) + " vs rank " + std::to_string(b);
+                    svg_diffs.push_back(json::array(
+                        {a, b, render_diff_flamegraph(data.cpu_profiles.at(a), data.cpu_profiles.at(b), o)}));
+                };
+                if (rep.reference_rank && data.cpu_profiles.count(*rep.reference_rank))
+                    for (int r : rep.flagged_ranks)
+                        if (data.cpu_profiles.count(r)) add_svg_diff(r, *rep.reference_rank);
+                if (ranks.size() >= 2) add_svg_diff(ranks[0], ranks[1]);
+                j["artifacts"] = {{"folded", folded}, {"diffs", diffs}, {"svg", svgs}, {"svg_diffs", svg_diffs}};
             }
             *out_json = dup_string(j.dump());
         }

@@ -22,7 +22,7 @@ from typing import Optional
 import numpy as np
 
 from .abi import (STG_AGG_FORCE_EXACT, STG_MEM_DEVICE, STG_MEM_HOST, VERDICTS, StgBundleInfo, StgConfig,
-                  StgRunStats, StgStream, StgWindow, Window, _ptr, config_struct, default_config)
+                  StgRunStats, StgStream, StgSvgOptions, StgWindow, Window, _ptr, config_struct, default_config)
 
 __all__ = ["Context", "StgError", "Window", "load_library", "LIB_PATH", "VERDICTS",
            "default_config"]
@@ -62,6 +62,10 @@ def load_library():
     l.stg_dist_unique_id.argtypes = [C.c_char_p]
     l.stg_dist_init.argtypes = [P, C.c_int, C.c_int, C.c_char_p]
     l.stg_result_folded_text.argtypes = [P, C.c_int32, C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64)]
+    l.stg_result_flamegraph_svg.argtypes = [P, C.c_int32, C.POINTER(StgSvgOptions), C.c_char_p, C.c_uint64,
+                                            C.POINTER(C.c_uint64)]
+    l.stg_result_diff_flamegraph_svg.argtypes = [P, C.c_int32, C.c_int32, C.POINTER(StgSvgOptions), C.c_char_p,
+                                                 C.c_uint64, C.POINTER(C.c_uint64)]
     l.stg_result_diff_folded.argtypes = [P, C.c_int32, C.c_int32, C.c_char_p, C.c_uint64,
                                          C.POINTER(C.c_uint64)]
     l.stg_bundle_load.argtypes = [P, C.c_char_p, C.POINTER(StgBundleInfo)]
@@ -279,6 +283,18 @@ class Context:
     def diff_folded(self, rank_a: int, rank_b: int) -> str:
         """diff_folded(profile(a), profile(b)) (folded.cpp:83-96), rendered on the GPU."""
         return self._text(self._l.stg_result_diff_folded, rank_a, rank_b)
+
+    def flamegraph_svg(self, rank: int, title: str = "flame graph", width: int = 1200, row_height: int = 16,
+                       min_fraction: float = 0.001) -> str:
+        """render_flamegraph (svg.cpp:157-163) of `rank`'s CPU profile."""
+        o = StgSvgOptions(width, row_height, min_fraction, title.encode())
+        return self._text(self._l.stg_result_flamegraph_svg, rank, C.byref(o))
+
+    def diff_flamegraph_svg(self, rank_before: int, rank_after: int, title: str = "flame graph", width: int = 1200,
+                            row_height: int = 16, min_fraction: float = 0.001) -> str:
+        """render_diff_flamegraph (svg.cpp:165-172) of two ranks' CPU profiles."""
+        o = StgSvgOptions(width, row_height, min_fraction, title.encode())
+        return self._text(self._l.stg_result_diff_flamegraph_svg, rank_before, rank_after, C.byref(o))
 
     def folded(self):
         """{rank: (total, [(names root-first, count), ...])} via the structured getters."""

@@ -114,6 +114,12 @@ class StgConfig(C.Structure):
     ]
 
 
+class StgSvgOptions(C.Structure):
+    """stg_svg_options (SvgOptions, svg.hpp)."""
+    _fields_ = [("width", C.c_int32), ("row_height", C.c_int32), ("min_fraction", C.c_double),
+                ("title", C.c_char_p)]
+
+
 class StgRunStats(C.Structure):
     _fields_ = [
         ("n_samples_in_window", C.c_uint64),

@@ -61,6 +61,14 @@ struct Result {
     uint64_t pfx_hits = 0, pfx_misses = 0;
     uint32_t verified = 0, verify_retries = 0;
     uint64_t f_nd_bound = 1;  // bound on the (sequence, distinct name) pairs of the fold
+    // host mirror of the folded lines, downloaded once on first use (getters)
+    struct HostFold {
+        bool ok = false;
+        std::vector<uint64_t> lkey, lcount, seq_off, line_off;
+        std::vector<uint32_t> dense_rep, arena;
+    } hf;
+    std::string svg_text;  // last rendered flame graph (two-call size query)
+    uint64_t svg_key = ~0ull;
     // name space: final rank -> string
     std::vector<uint64_t> unk_final;       // final rank of each distinct unknown label (sorted)
     std::vector<std::string> unk_labels;   // labels in the same order

@@ -15,6 +15,7 @@ void window_run(Ctx& c, const stg_window& w, const stg_config& cfg);
 std::string groupdata_json(Ctx& c, uint32_t parts);
 std::string report_json(Ctx& c);
 std::string report_text_of(Ctx& c);
+std::string flamegraph_svg(Ctx& c, int kind, int32_t rank_a, int32_t rank_b, const stg_svg_options& o);
 std::string waterline_json(Ctx& c);
 void run_resolve(Ctx& c, Result& res, uint64_t n, const uint64_t* pc, const uint16_t* bin, int32_t n_bins,
                  const uint8_t* ids, int mode, uint32_t* out);
@@ -375,3 +376,44 @@ int stg_result_diff_folded(stg_ctx* ctx, int32_t rank_a, int32_t rank_b, char* b
 }
 
 }  // extern "C"
+
+static int svg_out(stg_ctx* ctx, int kind, int32_t a, int32_t b, const stg_svg_options* opts, char* buf, uint64_t cap,
+                   uint64_t* needed) {
+    std::string* text = nullptr;
+    int rc = guard([&] {
+        std::lock_guard<std::mutex> lk(ctx->impl.mu);
+        stg::Result& r = need_result(ctx);
+        stg_svg_options o{1200, 16, 0.001, "flame graph"};
+        if (opts) o = *opts;
+        if (o.width <= 0 || o.row_height <= 0) stg::fail(STG_EINVAL, "svg width and row height must be positive");
+        // the text is rendered once per request and handed out by the second call
+        uint64_t key = 1469598103934665603ull;
+        auto mixin = [&](const void* p, size_t n) {
+            for (size_t i = 0; i < n; ++i) key = (key ^ static_cast<const unsigned char*>(p)[i]) * 1099511628211ull;
+        };
+        mixin(&kind, sizeof kind);
+        mixin(&a, sizeof a);
+        mixin(&b, sizeof b);
+        mixin(&o.width, sizeof o.width);
+        mixin(&o.row_height, sizeof o.row_height);
+        mixin(&o.min_fraction, sizeof o.min_fraction);
+        if (o.title) mixin(o.title, std::strlen(o.title));
+        if (r.svg_key != key) {
+            r.svg_text = stg::flamegraph_svg(ctx->impl, kind, a, b, o);
+            r.svg_key = key;
+        }
+        text = &r.svg_text;
+    });
+    if (rc) return rc;
+    return copy_out(*text, buf, cap, needed);
+}
+
+int stg_result_flamegraph_svg(stg_ctx* ctx, int32_t rank, const stg_svg_options* opts, char* buf, uint64_t cap,
+                              uint64_t* needed) {
+    return svg_out(ctx, 0, rank, 0, opts, buf, cap, needed);
+}
+
+int stg_result_diff_flamegraph_svg(stg_ctx* ctx, int32_t rank_before, int32_t rank_after,
+                                   const stg_svg_options* opts, char* buf, uint64_t cap, uint64_t* needed) {
+    return svg_out(ctx, 1, rank_before, rank_after, opts, buf, cap, needed);
+}

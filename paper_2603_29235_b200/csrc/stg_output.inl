@@ -81,32 +81,201 @@ static void d2h(Ctx& c, T* host, const char* name, size_t n, size_t offset = 0) 
 }
 
 // Lines of CPU rank i: (sequence name keys, count), in folded order.
+// The folded lines of the last window on the host, one bulk download per result.
+static const Result::HostFold& host_fold(Ctx& c) {
+    Result& r = *c.result;
+    Result::HostFold& h = r.hf;
+    if (h.ok) return h;
+    h.lkey.resize(r.n_lines);
+    h.lcount.resize(r.n_lines);
+    h.dense_rep.resize(r.n_seq);
+    h.line_off.assign(size_t(r.n_window_ranks) + 1, 0);
+    if (r.n_lines) {
+        d2h(c, h.lkey.data(), "lkey_s", r.n_lines);
+        d2h(c, h.lcount.data(), "lcount_s", r.n_lines);
+        d2h(c, h.dense_rep.data(), "dense_rep", r.n_seq);
+        h.seq_off.resize(r.n_gid + 1);
+        d2h(c, h.seq_off.data(), "seq_off", r.n_gid + 1);
+        h.arena.resize(h.seq_off[r.n_gid]);
+        d2h(c, h.arena.data(), "arena", h.arena.size());
+        d2h(c, h.line_off.data(), "line_off", h.line_off.size());
+    }
+    h.ok = true;
+    return h;
+}
+
+// Lines of CPU rank i: (sequence name keys, count), in folded order.
 void rank_lines(Ctx& c, uint32_t i, std::vector<uint64_t>& key_off, std::vector<uint32_t>& keys,
                 std::vector<uint64_t>& counts) {
     Result& r = *c.result;
-    uint32_t row = r.cpu_rank_index.at(i);
-    uint64_t lo[2];
-    d2h(c, lo, "line_off", 2, row);
-    uint64_t n = lo[1] - lo[0];
-    std::vector<uint64_t> lk(n);
-    counts.resize(n);
-    d2h(c, lk.data(), "lkey_s", n, lo[0]);
-    d2h(c, counts.data(), "lcount_s", n, lo[0]);
+    const uint32_t row = r.cpu_rank_index.at(i);
+    const Result::HostFold& h = host_fold(c);
     key_off.assign(1, 0);
     keys.clear();
-    for (uint64_t l = 0; l < n; ++l) {
-        uint32_t s = uint32_t(lk[l]);
-        uint32_t g;
-        d2h(c, &g, "dense_rep", 1, s);
-        uint64_t so[2];
-        d2h(c, so, "seq_off", 2, g);
-        size_t base = keys.size();
-        keys.resize(base + (so[1] - so[0]));
-        d2h(c, keys.data() + base, "arena", so[1] - so[0], so[0]);
+    counts.clear();
+    if (!r.n_lines) return;
+    for (uint64_t l = h.line_off[row]; l < h.line_off[row + 1]; ++l) {
+        const uint32_t g = h.dense_rep[uint32_t(h.lkey[l])];
+        keys.insert(keys.end(), h.arena.begin() + h.seq_off[g], h.arena.begin() + h.seq_off[g + 1]);
         key_off.push_back(keys.size());
+        counts.push_back(h.lcount[l]);
     }
 }
 
+// ---- flame graphs (render_flamegraph / render_diff_flamegraph, svg.cpp:157-172)
+// The reference builds a std::map trie of the profile's lines and renders it
+// depth first.  The lines are already in std::map order here, so the trie's
+// pre-order is one pass over them (a new node wherever a line leaves the
+// previous line's prefix, counts summed over the contiguous run of lines that
+// share it), and the layout is the reference's own sequence of double
+// operations (widths and sibling offsets accumulated left to right), printed
+// with the same ostream formatting.
+namespace svg {
+struct Node {
+    uint32_t depth;
+    uint32_t key;
+    uint64_t before, after;
+};
+static std::string escape(const std::string& s) {
+    std::string out;
+    for (char ch : s) {
+        switch (ch) {
+            case '&': out += "&amp;"; break;
+            case '<': out += "&lt;"; break;
+            case '>': out += "&gt;"; break;
+            case '"': out += "&quot;"; break;
+            default: out += ch;
+        }
+    }
+    return out;
+}
+static std::string name_color(const std::string& name) {
+    uint64_t h = 1469598103934665603ull;
+    for (char ch : name) {
+        h ^= uint8_t(ch);
+        h *= 1099511628211ull;
+    }
+    std::ostringstream os;
+    os << "rgb(" << 205 + int(h % 50) << "," << int(h / 50 % 180) << "," << int(h / 9000 % 55) << ")";
+    return os.str();
+}
+static std::string diff_color(uint64_t before, uint64_t after, uint64_t tb, uint64_t ta) {
+    const double fb = tb ? double(before) / double(tb) : 0.0;
+    const double fa = ta ? double(after) / double(ta) : 0.0;
+    const double delta = fa - fb;
+    std::ostringstream os;
+    if (delta > 0.0005) {
+        const int shade = 255 - std::min(155, int(delta * 4000));
+        os << "rgb(255," << shade << "," << shade << ")";
+    } else if (delta < -0.0005) {
+        const int shade = 255 - std::min(155, int(-delta * 4000));
+        os << "rgb(" << shade << "," << shade << ",255)";
+    } else {
+        os << "rgb(224,224,224)";
+    }
+    return os.str();
+}
+}  // namespace svg
+
+// kind 0: one rank's profile; kind 1: diff (before = rank_a, after = rank_b)
+std::string flamegraph_svg(Ctx& c, int kind, int32_t rank_a, int32_t rank_b, const stg_svg_options& o) {
+    Result& r = *c.result;
+    auto index_of = [&](int32_t rank) {
+        auto it = std::lower_bound(r.cpu_rank_ids.begin(), r.cpu_rank_ids.end(), rank);
+        if (it == r.cpu_rank_ids.end() || *it != rank) fail(STG_EINVAL, "unknown rank id: " + std::to_string(rank));
+        return uint32_t(it - r.cpu_rank_ids.begin());
+    };
+    const Result::HostFold& h = host_fold(c);
+    // the (before, after) line list in map order: one rank, or the merge of two
+    // (lines of both ranks carry global sequence ranks, so merging by them is
+    // merging by name sequence)
+    struct Ln { uint32_t seq; uint64_t before, after; };
+    std::vector<Ln> lines;
+    {
+        const uint32_t ra = r.cpu_rank_index[index_of(rank_a)];
+        const uint64_t a0 = h.line_off[ra], a1 = h.line_off[ra + 1];
+        if (kind == 0) {
+            for (uint64_t l = a0; l < a1; ++l) lines.push_back({uint32_t(h.lkey[l]), h.lcount[l], h.lcount[l]});
+        } else {
+            const uint32_t rb = r.cpu_rank_index[index_of(rank_b)];
+            uint64_t i = a0, j = h.line_off[rb];
+            const uint64_t b1 = h.line_off[rb + 1];
+            while (i < a1 || j < b1) {
+                const uint32_t si = i < a1 ? uint32_t(h.lkey[i]) : 0xffffffffu;
+                const uint32_t sj = j < b1 ? uint32_t(h.lkey[j]) : 0xffffffffu;
+                if (si == sj) lines.push_back({si, h.lcount[i++], h.lcount[j++]});
+                else if (si < sj) lines.push_back({si, h.lcount[i++], 0});
+                else lines.push_back({sj, 0, h.lcount[j++]});
+            }
+        }
+    }
+    // trie pre-order from the sorted lines
+    std::vector<svg::Node> nodes;
+    std::vector<size_t> open;  // node index per depth on the current path
+    const uint32_t* prev = nullptr;
+    uint64_t prev_len = 0, max_len = 0, tot_b = 0, tot_a = 0;
+    for (const Ln& ln : lines) {
+        const uint32_t g = h.dense_rep[ln.seq];
+        const uint32_t* k = h.arena.data() + h.seq_off[g];
+        const uint64_t len = h.seq_off[g + 1] - h.seq_off[g];
+        uint64_t p = 0;
+        while (p < len && p < prev_len && k[p] == prev[p]) ++p;
+        open.resize(p);
+        for (size_t d = 0; d < p; ++d) {
+            nodes[open[d]].before += ln.before;
+            nodes[open[d]].after += ln.after;
+        }
+        for (uint64_t d = p; d < len; ++d) {
+            open.push_back(nodes.size());
+            nodes.push_back({uint32_t(d), k[d], ln.before, ln.after});
+        }
+        tot_b += ln.before;
+        tot_a += ln.after;
+        max_len = std::max(max_len, len);
+        prev = k;
+        prev_len = len;
+    }
+    const bool diff = kind == 1;
+    const int height = int(max_len + 2) * o.row_height + 24;
+    std::ostringstream out;
+    out << "<svg xmlns=\"http://www.w3.org/2000/svg\" width=\"" << o.width << "\" height=\"" << height << "\">\n";
+    out << "<rect width=\"100%\" height=\"100%\" fill=\"white\"/>\n";
+    out << "<text x=\"8\" y=\"16\" font-size=\"13\" font-family=\"monospace\">" << svg::escape(o.title ? o.title : "")
+        << "</text>\n";
+    // per depth on the current path: x, width, the parent's count basis, the
+    // next child's x, visible
+    struct Lvl { double x, w, cx; uint64_t basis; bool vis; };
+    std::vector<Lvl> lv;
+    const Lvl root{0.0, double(o.width), 0.0, tot_a, true};
+    for (const svg::Node& n : nodes) {
+        lv.resize(n.depth);
+        const Lvl& par = n.depth ? lv[n.depth - 1] : root;
+        Lvl& pm = n.depth ? lv[n.depth - 1] : const_cast<Lvl&>(root);
+        double w;
+        if (n.depth == 0)
+            w = tot_a ? double(o.width) * double(n.after) / double(tot_a) : 0.0;
+        else
+            w = par.basis ? par.w * double(n.after) / double(par.basis) : 0.0;
+        const double x = pm.cx;
+        pm.cx += w;
+        const bool vis = par.vis && par.basis != 0 && w / o.width >= o.min_fraction && n.after > 0;
+        lv.push_back({x, w, x, n.after, vis});
+        if (!vis) continue;
+        const std::string name = r.name_of(n.key);
+        const int y = height - (int(n.depth) + 2) * o.row_height;
+        out << "<g><title>" << svg::escape(name) << " (" << n.after;
+        if (diff) out << " vs " << n.before;
+        out << ")</title><rect x=\"" << x << "\" y=\"" << y << "\" width=\"" << w << "\" height=\""
+            << o.row_height - 1 << "\" fill=\""
+            << (diff ? svg::diff_color(n.before, n.after, tot_b, tot_a) : svg::name_color(name)) << "\"/>";
+        if (w > 60)
+            out << "<text x=\"" << x + 2 << "\" y=\"" << y + o.row_height - 4
+                << "\" font-size=\"11\" font-family=\"monospace\">" << svg::escape(name) << "</text>";
+        out << "</g>\n";
+    }
+    out << "</svg>\n";
+    return out.str();
+}
 std::string groupdata_json(Ctx& c, uint32_t parts) {
     Result& r = *c.result;
     JsonW j;
@@ -380,6 +549,8 @@ void window_run(Ctx& c, const stg_window& w, const stg_config& cfg) {
     if (!c.result) c.result = std::make_unique<Result>();
     Result& r = *c.result;
     r.render_valid = r.render_unk_ready = false;
+    r.hf = Result::HostFold{};
+    r.svg_key = ~0ull;
     Runner rn(c, w, cfg, r);
     rn.run();
 }

@@ -23,6 +23,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <sstream>
 
 #include "kernels.cuh"
 #include "result.h"

@@ -1,7 +1,9 @@
-"""GPU parity of the folded-text artifacts:
-stg_result_folded_text = FoldedProfile::to_string (folded.cpp:33-43) and
+"""GPU parity of the output artifacts:
+stg_result_folded_text = FoldedProfile::to_string (folded.cpp:33-43),
 stg_result_diff_folded = diff_folded (folded.cpp:83-96), rendered on the device,
-against the reference's own texts (oracle/_ref) and the oracle restatement.
+and the flame graphs stg_result_(diff_)flamegraph_svg = render_flamegraph /
+render_diff_flamegraph (svg.cpp:157-172), against the reference's own texts
+(oracle/_ref) and the oracle restatement.
 Text is bytes: the bar is exact equality.
 """
 import pytest
@@ -24,6 +26,10 @@ def test_artifacts_match_reference(ctx, scenario):
         assert ctx.folded_text(rank) == text, rank
     for a, b, text in art["diffs"]:
         assert ctx.diff_folded(a, b) == text, (a, b)
+    for rank, svg in art["svg"]:
+        assert ctx.flamegraph_svg(rank, title=f"rank {rank}") == svg, rank
+    for a, b, svg in art["svg_diffs"]:
+        assert ctx.diff_flamegraph_svg(a, b, title=f"rank {a} vs rank {b}") == svg, (a, b)
 
 
 def test_artifacts_with_unknown_labels_match_oracle(ctx):
@@ -46,6 +52,24 @@ def test_unknown_rank_is_refused(ctx):
         ctx.folded_text(999)
     with pytest.raises(stg.StgError, match="unknown rank id: 77"):
         ctx.diff_folded(0, 77)
+    with pytest.raises(stg.StgError, match="unknown rank id: 5"):
+        ctx.flamegraph_svg(5)
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+def test_flamegraphs_c1_scale_match_reference(ctx):
+    """Deep, wide profiles (2k distinct stacks per rank, unknown labels, elided
+    narrow frames) render to the reference's exact SVG bytes."""
+    win = small_window(seed=2, ranks=4, samples_per_rank=30_000, slow_rank=1, depth=12, n_sym=2000, pool=2000,
+                       unknown_frac=0.02)
+    r, _, _ = ref.window_run(win, artifacts=True)
+    ctx.window_run(win)
+    art = r["artifacts"]
+    assert art["svg"] and art["svg_diffs"]
+    for rank, svg in art["svg"]:
+        assert ctx.flamegraph_svg(rank, title=f"rank {rank}") == svg, rank
+    for a, b, svg in art["svg_diffs"]:
+        assert ctx.diff_flamegraph_svg(a, b, title=f"rank {a} vs rank {b}") == svg, (a, b)
 
 
 def test_artifacts_large_window_properties(ctx):
