@@ -672,19 +672,28 @@ struct Runner {
         uint32_t unk_cap = uint32_t(std::max<uint64_t>(4096, next_pow2(c_unk_hint())));
         int dev_sms = 148;
         STG_CUDA(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c.device));
-        unsigned long long* d_nin = dev<unsigned long long>("nin", R);
-        int* d_uns = dev<int>("uns", R);
-        unsigned long long* d_eempty = dev<unsigned long long>("eempty", R);
-        int* d_ebin = dev<int>("ebin", 1);
-        unsigned* d_used = dev<unsigned>("tused", R);
-        int* d_ovf = dev<int>("tovf", R);
-        unsigned* d_unk_used = dev<unsigned>("unk_used", 1);
-        int* d_unk_ovf = dev<int>("unk_ovf", 1);
+        // everything the host reads after the kernel, in one block (one download):
+        // stat[2] | n_in[R] | err_empty[R] | unk_used, unk_ovf, ebin, pad | used[R] | ovf[R] | unsorted[R]
+        const size_t so_n = 16 + 16 * size_t(R) + 16 + 12 * size_t(R);
+        uint8_t* so = dev<uint8_t>("s_out", so_n);
+        unsigned long long* d_stat = reinterpret_cast<unsigned long long*>(so);
+        unsigned long long* d_nin = d_stat + 2;
+        unsigned long long* d_eempty = d_nin + R;
+        unsigned* d_unk_used = reinterpret_cast<unsigned*>(d_eempty + R);
+        int* d_unk_ovf = reinterpret_cast<int*>(d_unk_used + 1);
+        int* d_ebin = d_unk_ovf + 1;
+        unsigned* d_used = reinterpret_cast<unsigned*>(d_ebin + 2);
+        int* d_ovf = reinterpret_cast<int*>(d_used + R);
+        int* d_uns = d_ovf + R;
+        s_unk_used = d_unk_used;
+        s_unk_ovf = d_unk_ovf;
+        s_ebin = d_ebin;
+        std::vector<uint8_t> hso(so_n);
+        auto hso_at = [&](const void* dptr) { return hso.data() + (static_cast<const uint8_t*>(dptr) - so); };
         std::vector<uint64_t> tab_off(R);
         // prefix cache: ~4 slots per distinct raw chain of the previous window
         uint32_t pfx_cap = uint32_t(std::min<uint64_t>(1u << 24, std::max<uint64_t>(1u << 16, next_pow2(4 * c.hint_pfx_misses + 1))));
         PfxSlot* pfx = dev<PfxSlot>("pfx", pfx_cap);
-        unsigned long long* d_stat = dev<unsigned long long>("sym_stat", 2);
         AggSlot* slots = nullptr;
         UnkSlot* unk = nullptr;
         std::vector<int> ovf(R);
@@ -724,14 +733,8 @@ struct Runner {
             d_mask = up<uint32_t>("tmask", masks.data(), R);
             unk = dev<UnkSlot>("unk", unk_cap);
             zero(unk, size_t(unk_cap) * sizeof(UnkSlot));
-            zero(d_nin, R * 8);
-            zero(d_uns, R * 4);
+            zero(so, so_n);
             STG_CUDA(cudaMemsetAsync(d_eempty, 0xff, R * 8, st));
-            zero(d_ebin, 4);
-            zero(d_used, R * 4);
-            zero(d_ovf, R * 4);
-            zero(d_unk_used, 4);
-            zero(d_unk_ovf, 4);
             p = AggParams{};
             p.ts = ts;
             p.foff = foff;
@@ -764,7 +767,6 @@ struct Runner {
             p.use_pfx = pass == 0;
             p.weak_pfx = cfg.debug_weak_prefix_key != 0;
             zero(pfx, size_t(pfx_cap) * sizeof(PfxSlot));
-            zero(d_stat, 16);
             // 4 resident CTAs of 8 warps per SM (64 registers), 4 waves' worth of CTAs
             const uint64_t need = ((n_s + 31) / 32 + (kThreads / 32) - 1) / (kThreads / 32);
             unsigned grid = unsigned(dev_sms) * 16;
@@ -777,38 +779,39 @@ struct Runner {
             cudaEventRecord(ev[3], st);
             if (attempt == 0) side_gpu_os();  // host + side-stream work while the kernel streams
             res.agg_attempts = attempt + 1;
-            down(ovf.data(), d_ovf, R);
+            down(hso.data(), so, so_n);
             mark("s:k_sym_agg");
-            down(used.data(), d_used, R);
+            std::memcpy(ovf.data(), hso_at(d_ovf), R * 4);
+            std::memcpy(used.data(), hso_at(d_used), R * 4);
             bool any = false;
             for (int r = 0; r < R; ++r)
                 if (ovf[r] || used[r] > (caps[r] >> 1)) {  // probe cap hit, or past the 50 % load limit
                     caps[r] = caps[r] >= (1u << 30) ? caps[r] : caps[r] * 4;
                     any = true;
                 }
-            bool unk_over = get1(d_unk_ovf) != 0;
+            bool unk_over = *reinterpret_cast<const int*>(hso_at(d_unk_ovf)) != 0;
             if (unk_over) unk_cap = unk_cap >= (1u << 30) ? unk_cap : unk_cap * 4;
             if (!any && !unk_over) break;
             if (attempt > 6) fail(STG_ENOMEM, "aggregation tables kept overflowing");
         }
-        c_set_hints(used, get1(d_unk_used));
+        c_set_hints(used, *reinterpret_cast<const unsigned*>(hso_at(d_unk_used)));
         {
             unsigned long long hm[2];
-            down(hm, d_stat, 2);
+            std::memcpy(hm, hso_at(d_stat), 16);
             res.pfx_hits = hm[0];
             res.pfx_misses = hm[1];
             if (pass == 0) c.hint_pfx_misses = uint32_t(std::min<unsigned long long>(hm[1], 1u << 22));
         }
-        if (get1(d_ebin)) fail(STG_EINVAL, "frame binary index out of range");
+        if (*reinterpret_cast<const int*>(hso_at(d_ebin))) fail(STG_EINVAL, "frame binary index out of range");
         h_n_in.resize(R);
-        down(h_n_in.data(), d_nin, R);
+        std::memcpy(h_n_in.data(), hso_at(d_nin), R * 8);
         // validation in aggregate_samples order (samples.cpp:32-58), ranks ascending;
         // a rank whose in-window samples all have empty stacks has no aggregated
         // sample but still fails like the reference
         std::vector<unsigned long long> eempty(R), ereg(R, ~0ull);
-        down(eempty.data(), d_eempty, R);
+        std::memcpy(eempty.data(), hso_at(d_eempty), R * 8);
         std::vector<int> uns(R);
-        down(uns.data(), d_uns, R);
+        std::memcpy(uns.data(), hso_at(d_uns), R * 4);
         std::vector<int> flagged;
         for (int r = 0; r < R; ++r)
             if (uns[r] && h_n_in[r]) flagged.push_back(r);
@@ -873,6 +876,8 @@ struct Runner {
         return ok;
     }
     bool fold_bad = false;
+    unsigned* s_unk_used = nullptr;  // inside the samples stage's output block
+    int *s_unk_ovf = nullptr, *s_ebin = nullptr;
     int32_t fail_rank = -1;  // rank whose validation failed (distributed error agreement)
 
     // table-capacity hints kept on the context between windows
@@ -1011,9 +1016,9 @@ struct Runner {
         d_seq_off = dev<uint64_t>("seq_off", G + 1);
         excl_sum(seq_len, d_seq_off, uint64_t(G) + 1);
         d_arena = dev<uint32_t>("arena", std::max<uint64_t>(A, 1));
-        unsigned* d_unk_used = static_cast<unsigned*>(c.buf("unk_used").p);
-        int* d_unk_ovf = static_cast<int*>(c.buf("unk_ovf").p);
-        int* d_ebin = static_cast<int*>(c.buf("ebin").p);
+        unsigned* d_unk_used = s_unk_used;
+        int* d_unk_ovf = s_unk_ovf;
+        int* d_ebin = s_ebin;
         UnkSet us{unk, unk_cap - 1, unk_cap - 1, d_unk_used, d_unk_ovf};
         LAUNCH(k_seq_materialize, grid_for(uint64_t(G) * 32), kThreads, G, seq_rep, d_seq_off, foff, pc, bin, d_tabs,
                uint32_t(w.n_bins), cfg.lookup_mode, us, d_ebin, d_arena);

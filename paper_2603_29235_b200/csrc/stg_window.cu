@@ -958,17 +958,31 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
         }
         r_cur = lo;
     }
+    // phase-0 stream values of the next batch, loaded one batch ahead (they are
+    // in flight while the current batch streams its frames and runs its lookups)
+    int64_t nx_t = 0, nx_tp = 0;
+    uint64_t nx_f0 = 0, nx_f1 = 0;
+    auto load0 = [&](uint64_t b) {
+        const uint64_t i = b * 32 + lane;
+        const uint64_t q = i < p.n_samples ? i : p.n_samples - 1;
+        nx_t = __ldcs(p.ts + q);
+        nx_f0 = __ldcs(p.foff + q);
+        nx_f1 = (lane == 31 || i + 1 >= p.n_samples) ? __ldcs(p.foff + q + 1) : 0;
+        nx_tp = lane == 0 && q > 0 ? __ldcs(p.ts + q - 1) : 0;
+    };
+    if (b_begin < b_end) load0(b_begin);
     for (uint64_t bt = b_begin; bt < b_end; bt += b_step) {
-        // ---------------- phase 0: lane s owns sample i; its stream loads are
-        // issued before the rank-dependent ones resolve
+        // ---------------- phase 0: lane s owns sample i; its stream values were
+        // loaded during the previous batch, the next batch's are issued now
         const uint64_t i = bt * 32 + lane;
         const bool valid = i < p.n_samples;
         const uint64_t q = valid ? i : p.n_samples - 1;
-        const int64_t t = __ldcs(p.ts + q);
-        uint64_t f0 = __ldcs(p.foff + q);
+        const int64_t t = nx_t;
+        uint64_t f0 = nx_f0;
         const bool own_next = lane == 31 || i + 1 >= p.n_samples;
-        uint64_t f1 = own_next ? __ldcs(p.foff + q + 1) : 0;
-        const int64_t t_prev = lane == 0 && q > 0 ? __ldcs(p.ts + q - 1) : 0;
+        uint64_t f1 = nx_f1;
+        const int64_t t_prev = nx_tp;
+        if (bt + b_step < b_end) load0(bt + b_step);
         int r = r_cur;
         while (q >= __ldg(p.rank_soff + r + 1)) ++r;
         r_cur = __shfl_sync(0xffffffffu, r, 31);
@@ -1143,11 +1157,20 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
             }
         }
         if (leaf_search) {
-            while (blo < bhi) {
+            // bisection down to <= 4 candidates (the bucket index usually leaves
+            // 1-2), then every candidate's entry in one round trip: the answer is
+            // the last whose start is <= pc (symfile.cpp:54-75)
+            while (bhi - blo > 3) {
                 const uint32_t mid = (blo + bhi + 1) >> 1;
                 if (__ldg(&T->e[mid].x) <= leaf_pc) blo = mid; else bhi = mid - 1;
             }
-            const ulonglong2 e = __ldg(T->e + blo);
+            ulonglong2 e = __ldg(T->e + blo);
+            const ulonglong2 e1 = blo + 1 <= bhi ? __ldg(T->e + blo + 1) : e;
+            const ulonglong2 e2 = blo + 2 <= bhi ? __ldg(T->e + blo + 2) : e;
+            const ulonglong2 e3 = blo + 3 <= bhi ? __ldg(T->e + blo + 3) : e;
+            if (blo + 1 <= bhi && e1.x <= leaf_pc) e = e1;
+            if (blo + 2 <= bhi && e2.x <= leaf_pc) e = e2;
+            if (blo + 3 <= bhi && e3.x <= leaf_pc) e = e3;
             if (p.mode == STG_LOOKUP_NEAREST_LOWER) {
                 leaf_key = uint32_t(e.y >> 32);
             } else {
