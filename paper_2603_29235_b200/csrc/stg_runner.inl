@@ -595,6 +595,8 @@ struct Runner {
 
     // 4 resident CTAs of 8 warps per SM (64 registers); the table staging in
     // shared memory covers up to kMaxSmemBins binaries
+    // 4 resident CTAs of 8 warps per SM (64 registers); the table staging in
+    // shared memory covers up to kMaxSmemBins binaries
     void launch_sym_agg(const AggParams& p, unsigned grid, bool smem_tabs) {
         if (smem_tabs) k_sym_agg<true, 4, 1, 1><<<grid, kThreads, 0, st>>>(p);
         else k_sym_agg<false, 4, 1, 1><<<grid, kThreads, 0, st>>>(p);

@@ -927,7 +927,7 @@ __device__ __forceinline__ void pfx_put(PfxSlot* T, uint32_t mask, uint64_t ha, 
 //           open-addressing table with __match_any pre-aggregation;
 //  misses   the warp symbolizes the missing chains cooperatively and fills
 //           the cache.
-template <bool SMEM_TABS, int MINB, int UB, int UBC>
+template <bool SMEM_TABS, int MINB, int UB, int UBC, bool COOP = true>
 __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
     __shared__ DevTable s_tabs[kMaxSmemBins];
     if (SMEM_TABS) {
@@ -1017,9 +1017,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
             const uint64_t A = __shfl_sync(0xffffffffu, f0, 0);
             const uint32_t d0 = __shfl_sync(0xffffffffu, depth, 0);
             const uint32_t nb = d0 >> 3;
-            coop = __all_sync(0xffffffffu, inwin && depth == d0) && d0 >= 8 && (d0 & 7) == 0 && (A & 7) == 0 &&
-                   nb <= 32 && (nb & (nb - 1)) == 0;
-            if (coop) {
+            coop = COOP && __all_sync(0xffffffffu, inwin && depth == d0) && d0 >= 8 && (d0 & 7) == 0 &&
+                   (A & 7) == 0 && nb <= 32 && (nb & (nb - 1)) == 0;
+            if (COOP && coop) {
                 const int lg = __ffs(nb) - 1;
                 const int wid = threadIdx.x >> 5;
                 // UBC steps per round trip: all their loads are issued before any hashing
