@@ -910,6 +910,11 @@ __device__ __forceinline__ void pfx_put(PfxSlot* T, uint32_t mask, uint64_t ha, 
     }
 }
 
+__device__ __forceinline__ void cp_async8(void* smem, const void* g) {
+    const uint32_t sa = uint32_t(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(g) : "memory");
+}
+
 // The fused hot kernel (stage a+b), one lane per sample.  A warp takes 32
 // consecutive samples — one contiguous block of frames in HBM — and owns a
 // contiguous range of such batches, so its rank only moves forward:
@@ -958,17 +963,19 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
         }
         r_cur = lo;
     }
-    // phase-0 stream values of the next batch, loaded one batch ahead (they are
-    // in flight while the current batch streams its frames and runs its lookups)
-    int64_t nx_t = 0, nx_tp = 0;
-    uint64_t nx_f0 = 0, nx_f1 = 0;
+    // phase-0 stream values of the next batch, copied one batch ahead into
+    // shared memory with asynchronous copies (in flight while the current batch
+    // streams its frames and runs its lookups, and holding no registers)
+    __shared__ uint64_t s_nx[kThreads / 32][4][32];  // ts, frame offset, next frame offset, previous ts
+    uint64_t* nxw = &s_nx[threadIdx.x >> 5][0][0];
     auto load0 = [&](uint64_t b) {
         const uint64_t i = b * 32 + lane;
         const uint64_t q = i < p.n_samples ? i : p.n_samples - 1;
-        nx_t = __ldcs(p.ts + q);
-        nx_f0 = __ldcs(p.foff + q);
-        nx_f1 = (lane == 31 || i + 1 >= p.n_samples) ? __ldcs(p.foff + q + 1) : 0;
-        nx_tp = lane == 0 && q > 0 ? __ldcs(p.ts + q - 1) : 0;
+        cp_async8(nxw + lane, p.ts + q);
+        cp_async8(nxw + 32 + lane, p.foff + q);
+        if (lane == 31 || i + 1 >= p.n_samples) cp_async8(nxw + 64 + lane, p.foff + q + 1);
+        if (lane == 0 && q > 0) cp_async8(nxw + 96, p.ts + q - 1);
+        asm volatile("cp.async.commit_group;" ::: "memory");
     };
     if (b_begin < b_end) load0(b_begin);
     for (uint64_t bt = b_begin; bt < b_end; bt += b_step) {
@@ -977,11 +984,14 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
         const uint64_t i = bt * 32 + lane;
         const bool valid = i < p.n_samples;
         const uint64_t q = valid ? i : p.n_samples - 1;
-        const int64_t t = nx_t;
-        uint64_t f0 = nx_f0;
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
+        const int64_t t = int64_t(nxw[lane]);
+        uint64_t f0 = nxw[32 + lane];
         const bool own_next = lane == 31 || i + 1 >= p.n_samples;
-        uint64_t f1 = nx_f1;
-        const int64_t t_prev = nx_tp;
+        uint64_t f1 = own_next ? nxw[64 + lane] : 0;
+        const int64_t t_prev = lane == 0 && q > 0 ? int64_t(nxw[96]) : 0;
+        __syncwarp();
         if (bt + b_step < b_end) load0(bt + b_step);
         int r = r_cur;
         while (q >= __ldg(p.rank_soff + r + 1)) ++r;
@@ -1157,20 +1167,16 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
             }
         }
         if (leaf_search) {
-            // bisection down to <= 4 candidates (the bucket index usually leaves
-            // 1-2), then every candidate's entry in one round trip: the answer is
+            // bisection down to <= 2 candidates (the bucket index usually leaves
+            // 1-2), then both candidates' entries in one round trip: the answer is
             // the last whose start is <= pc (symfile.cpp:54-75)
-            while (bhi - blo > 3) {
+            while (bhi - blo > 1) {
                 const uint32_t mid = (blo + bhi + 1) >> 1;
                 if (__ldg(&T->e[mid].x) <= leaf_pc) blo = mid; else bhi = mid - 1;
             }
             ulonglong2 e = __ldg(T->e + blo);
-            const ulonglong2 e1 = blo + 1 <= bhi ? __ldg(T->e + blo + 1) : e;
-            const ulonglong2 e2 = blo + 2 <= bhi ? __ldg(T->e + blo + 2) : e;
-            const ulonglong2 e3 = blo + 3 <= bhi ? __ldg(T->e + blo + 3) : e;
-            if (blo + 1 <= bhi && e1.x <= leaf_pc) e = e1;
-            if (blo + 2 <= bhi && e2.x <= leaf_pc) e = e2;
-            if (blo + 3 <= bhi && e3.x <= leaf_pc) e = e3;
+            const ulonglong2 e1 = blo < bhi ? __ldg(T->e + bhi) : e;
+            if (blo < bhi && e1.x <= leaf_pc) e = e1;
             if (p.mode == STG_LOOKUP_NEAREST_LOWER) {
                 leaf_key = uint32_t(e.y >> 32);
             } else {
