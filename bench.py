@@ -92,6 +92,7 @@ class Workload:
         self.iterations = getattr(a, "iterations", 100)
         self.iter_ns = self.span // self.iterations
         self.group_size = world * a.ranks
+        self.world = world
         self.skews_all = rng.integers(-10_000_000, 10_000_001, size=self.group_size).astype(np.int64)
         self.rank_base = shard * a.ranks
         self.skews = self.skews_all[self.rank_base:self.rank_base + a.ranks]
@@ -172,6 +173,12 @@ class Workload:
         w.n_frames_ = ranks * spr * a.depth
         if ranks == a.ranks:
             apply_side(w, self.side, self.group_size)
+            if self.world > 1:  # collectives + GPU/OS streams sharded by rank like the samples
+                from paper_2603_29235_b200.dist import keep_streams
+                lo = self.rank_base if self.rank_base else None
+                hi = self.rank_base + ranks if self.rank_base + ranks < self.group_size else None
+                keep_streams(w, lo, hi, 3)
+                w.shard_rank_lo = self.rank_base
         else:  # bounded sample: keep the side streams of the sampled ranks only
             from tests.synth import side_streams
             rng = np.random.default_rng(a.seed)
@@ -362,8 +369,22 @@ def bench_c4(a, torch, stg, rank, local, world, dist):
     events per GPU (device-resident), NIC-softirq straggler.  Metric: events/s."""
     from tests.synth import c4_window
     ranks = 1024
-    win = c4_window(ranks=ranks, events_per_rank=a.events, seed=1 + rank, device=True, torch=torch)
+    E = a.events
+    sharded = world > 1  # one 1,024-rank window, its ranks' events split over the GPUs (strong scaling)
+    win = c4_window(ranks=ranks, events_per_rank=E, seed=1, device=True, torch=torch)
+    if sharded:
+        from paper_2603_29235_b200.dist import keep_streams, shard_bounds
+        lo, hi = shard_bounds(ranks, world, rank)
+        for f in ("coll_rank", "coll_group", "coll_kind", "coll_entry", "coll_exit", "coll_gpu_dur"):
+            setattr(win, f, getattr(win, f)[lo * E:hi * E].contiguous())  # rank-major events
+        win.n_coll_ = (hi - lo) * E
+        keep_streams(win, lo if rank else None, hi if rank + 1 < world else None, 2)
+        win.shard_streams = 3
+        win.shard_rank_lo = lo
     ctx = stg.Context(local)
+    if sharded:
+        from paper_2603_29235_b200.dist import share_unique_id
+        ctx.dist_init(world, rank, share_unique_id(dist, stg.Context.dist_unique_id, device="cuda"))
     for _ in range(a.warmup):
         s = ctx.window_run(win)
         log(f"[c4 r{rank}] warmup {s['ms_total']:.2f} ms (collectives {s['ms_collectives']:.2f}) "
@@ -385,16 +406,19 @@ def bench_c4(a, torch, stg, rank, local, world, dist):
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    n_ev = ranks * a.events
+    n_ev = ranks * a.events  # events of the whole group per step (sharded) / per GPU (1 GPU)
     cm = float(np.median(coll))
-    algo = 24 * n_ev  # entry+exit read, lateness written (SURVEY.md §8(d) stage d)
+    algo = 24 * n_ev // world  # per GPU: entry+exit read, lateness written (SURVEY.md §8(d) stage d)
     peak = peaks().get("hbm_gbs", 6650.0)
     line = {"metric": "collective events/sec aligned (match+align+lateness+straggler+verdict)",
-            "value": n_ev * world / (ms / 1e3), "unit": "events/s", "n_gpus": world, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "value": n_ev / (ms / 1e3), "unit": "events/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "config": {"workload": f"C4: {ranks} ranks x {a.events} events (AllReduce/AllGather), straggler rank 4",
-                       "inputs": "collective arrays resident in HBM"},
+                       "inputs": "collective arrays resident in HBM",
+                       "parallelism": (f"one {ranks}-rank window, events sharded by rank over {world} GPUs "
+                                       "(STG_SHARD_COLL: per-instance partials over NCCL, straggler sums "
+                                       "chained in rank order)") if sharded else "1 GPU"},
             "verdict": rep["verdict"], "flagged_ranks": rep["flagged_ranks"],
             "stage_ms": {"collectives": cm, "total_device": s["ms_total"]},
             "roofline": {"bound": "hbm", "achieved": round(algo / (cm / 1e3) / 1e9, 1), "peak": peak, "unit": "GB/s",

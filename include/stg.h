@@ -176,7 +176,26 @@ typedef struct stg_window {
     int32_t coll_memory;
     /* stg_memory of the gpu_* and os_* arrays (kernel/counter names stay host) */
     int32_t side_memory;
+
+    /* Distributed mode only (stg_dist_init, world > 1): which per-rank streams
+     * this context holds for its own ranks only, instead of identically on
+     * every context.  Context p owns the ranks in [shard_rank_lo of p,
+     * shard_rank_lo of p+1) (the last context: to infinity); the lower bounds
+     * must increase with the world rank.  STG_SHARD_COLL: coll_* hold only the
+     * owned ranks' events, in LoadedBundle::collectives order (the group's
+     * event order is the contexts' lists concatenated in world-rank order) —
+     * stage d (match_collectives / align_clocks / entry_lateness /
+     * detect_straggler, collective.cpp:29-142, diagnosis.cpp:76-111) then runs
+     * rank-sharded with per-instance partials combined over NCCL, and the
+     * lateness_per_instance of the GroupData holds the owned ranks only.
+     * STG_SHARD_SIDE: gpu_* / os_* likewise (per-rank sums all-reduced).
+     * 0 = replicated. */
+    int32_t shard_streams;
+    int32_t shard_rank_lo;
 } stg_window;
+
+#define STG_SHARD_COLL 1
+#define STG_SHARD_SIDE 2
 
 /* DiagnosisConfig (diagnosis.hpp:203-210) + GpuDiffConfig (:83-92) + OsDiffConfig
  * (:127-132).  stg_config_default() fills the reference defaults. */

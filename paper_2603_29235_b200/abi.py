@@ -88,6 +88,8 @@ class StgWindow(C.Structure):
         ("baseline_iteration_ms", C.c_double),
         ("coll_memory", C.c_int32),
         ("side_memory", C.c_int32),
+        ("shard_streams", C.c_int32),
+        ("shard_rank_lo", C.c_int32),
     ]
 
 
@@ -202,6 +204,8 @@ class StgStream(C.Structure):
 
 
 STG_AGG_FORCE_EXACT = 1
+STG_SHARD_COLL = 1
+STG_SHARD_SIDE = 2
 
 
 class StgBundleInfo(C.Structure):
@@ -257,6 +261,8 @@ class Window:
     memory: int = STG_MEM_HOST
     coll_memory: int = STG_MEM_HOST
     side_memory: int = STG_MEM_HOST
+    shard_streams: int = 0  # STG_SHARD_COLL | STG_SHARD_SIDE (distributed mode)
+    shard_rank_lo: int = 0
     n_gpu_: Optional[int] = None
     n_os_: Optional[int] = None
     n_coll_: Optional[int] = None
@@ -379,6 +385,8 @@ class Window:
         w.baseline_fracs = _ptr(np.array([self.baseline[n] for n in names], np.float64), keep)
         w.has_baseline_iteration = int(self.baseline_iteration_ms is not None)
         w.baseline_iteration_ms = float(self.baseline_iteration_ms or 0.0)
+        w.shard_streams = int(self.shard_streams)
+        w.shard_rank_lo = int(self.shard_rank_lo)
         return w, keep
 
     @staticmethod

@@ -101,7 +101,7 @@ struct Runner {
     // main stream did before k_sym_agg) while k_sym_agg streams, and their host
     // downloads synchronise only the side stream.
     void side_gpu_os() {
-        if (gpu_os_done) return;
+        if (gpu_os_done || side_sharded()) return;  // sharded: main stream, reduced over NCCL after the samples
         if (!c.side) STG_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
         STG_CUDA(cudaStreamWaitEvent(c.side, ev_pre, 0));
         cudaStream_t keep = st;
@@ -246,31 +246,68 @@ struct Runner {
         if (out[0] >= (1 << 24)) fail(STG_EINVAL, "rank ids must be below 2^24");
         span = out[0] + 1;
     }
+    bool coll_sharded() const { return dist() && (w.shard_streams & STG_SHARD_COLL); }
+    bool side_sharded() const { return dist() && (w.shard_streams & STG_SHARD_SIDE); }
+    // shards of a rank-sharded group: context q owns ranks [sh_lo[q], sh_lo[q+1])
+    // and holds sh_n[q] collective events, global event indices from sh_base[q]
+    std::vector<int64_t> sh_lo, sh_n, sh_base;
+    int r_lo = 0, r_hi = 0;  // this context's ranks, clipped to [0, span)
     void rank_span_agree() {
-        if (dist()) {  // every context must index ranks the same way
-            int* d = dev<int>("dx_span", 1);
-            STG_CUDA(cudaMemcpyAsync(d, &span, 4, cudaMemcpyHostToDevice, st));
-            nccl(ncclAllReduce(d, d, 1, ncclInt32, ncclMax, comm(), st));
-            span = get1(d);
+        if (dist()) {  // every context must index ranks (and collective streams) the same way
+            int* d = dev<int>("dx_span", 4);
+            int v[4] = {span, coll_rg[1], coll_rg[2], ~coll_rg[0]};  // max of ~g = ~min g
+            STG_CUDA(cudaMemcpyAsync(d, v, sizeof v, cudaMemcpyHostToDevice, st));
+            nccl(ncclAllReduce(d, d, 4, ncclInt32, ncclMax, comm(), st));
+            down(v, d, 4);
+            span = v[0];
+            if (w.shard_streams & STG_SHARD_COLL) {
+                coll_rg[1] = v[1];
+                coll_rg[2] = v[2];
+                coll_rg[0] = ~v[3];
+            }
         }
         res.rank_span = span;
+        r_lo = 0;
+        r_hi = span;
+        if (!(w.shard_streams & (STG_SHARD_COLL | STG_SHARD_SIDE)) || !dist()) return;
+        const int W = c.world;
+        int64_t* d = dev<int64_t>("dx_shard", 2 * (W + 1));
+        int64_t mine[2] = {int64_t(w.shard_rank_lo), int64_t(w.n_coll)};
+        STG_CUDA(cudaMemcpyAsync(d + 2 * W, mine, 16, cudaMemcpyHostToDevice, st));
+        nccl(ncclAllGather(d + 2 * W, d, 2, ncclInt64, comm(), st));
+        std::vector<int64_t> h(2 * W);
+        down(h.data(), d, 2 * W);
+        sh_lo.assign(W + 1, 0);
+        sh_n.assign(W, 0);
+        sh_base.assign(W + 1, 0);
+        for (int q = 0; q < W; ++q) {
+            sh_lo[q] = h[2 * q];
+            sh_n[q] = h[2 * q + 1];
+            sh_base[q + 1] = sh_base[q] + sh_n[q];
+        }
+        sh_lo[W] = INT64_MAX;
+        for (int q = 1; q < W; ++q)  // identical data on every context: all fail alike
+            if (sh_lo[q] <= sh_lo[q - 1])
+                fail(STG_EINVAL, "stg_window.shard_rank_lo must increase with the world rank");
+        r_lo = int(std::min<int64_t>(std::max<int64_t>(sh_lo[c.wrank], 0), span));
+        r_hi = int(std::min<int64_t>(std::max<int64_t>(sh_lo[c.wrank + 1], 0), span));
     }
 
     // ------------------------------------------------------ collectives
-    void collectives() {
-        // one device block for everything the host reads back at the end (one
-        // download): offsets, straggler statistics, error and count words
+    // one device block for everything the host reads back at the end of stage d
+    // (one download): offsets, straggler statistics, error and count words
+    uint8_t* cb = nullptr;
+    size_t o_ma = 0, o_ml = 0, o_zm = 0, o_fl = 0, o_err = 0, o_cnt = 0, o_has = 0, o_pres = 0, o_hz = 0, o_end = 0;
+    uint64_t n_coll_all = 0;  // events stage d runs over (all of them, or the gathered shards)
+    void coll_result_init() {
         const uint64_t sp = uint64_t(span);
-        const size_t o_ma = 8 * sp, o_ml = 16 * sp, o_zm = 24 * sp, o_fl = 32 * sp, o_err = 40 * sp,
-                     o_cnt = 40 * sp + 16, o_has = 40 * sp + 48, o_pres = 41 * sp + 48, o_hz = 42 * sp + 48,
-                     o_end = 43 * sp + 48;
-        uint8_t* cb = dev<uint8_t>("c_out", o_end);
+        o_ma = 8 * sp, o_ml = 16 * sp, o_zm = 24 * sp, o_fl = 32 * sp, o_err = 40 * sp, o_cnt = 40 * sp + 16,
+        o_has = 40 * sp + 48, o_pres = 41 * sp + 48, o_hz = 42 * sp + 48, o_end = 43 * sp + 48;
+        cb = dev<uint8_t>("c_out", o_end);
         zero(cb, o_end);
         STG_CUDA(cudaMemsetAsync(cb + o_err, 0xff, 16, st));
         d_off = reinterpret_cast<int64_t*>(cb);
         d_has_off = cb + o_has;
-        unsigned long long* errs = reinterpret_cast<unsigned long long*>(cb + o_err);
-        unsigned long long* cnts = reinterpret_cast<unsigned long long*>(cb + o_cnt);  // n_seg, n_st, n_d, n_w
         res.n_instances = res.n_windowed = 0;
         res.iteration_times_ms.clear();
         res.offsets.assign(span, 0);
@@ -282,9 +319,32 @@ struct Runner {
         res.flag_count.assign(span, 0);
         res.has_z.assign(span, 0);
         res.have_offsets = false;
-        const uint64_t n = w.n_coll;
+    }
+    // one download of the result block into the host mirror
+    void coll_result_download() {
+        const uint64_t sp = uint64_t(span);
+        std::vector<uint8_t> h(o_end);
+        down(h.data(), cb, o_end);
+        std::memcpy(res.offsets.data(), h.data(), 8 * sp);
+        std::memcpy(res.mean_lat_all.data(), h.data() + o_ma, 8 * sp);
+        std::memcpy(res.mean_lat_alert.data(), h.data() + o_ml, 8 * sp);
+        std::memcpy(res.z_mean.data(), h.data() + o_zm, 8 * sp);
+        std::memcpy(res.flag_count.data(), h.data() + o_fl, 8 * sp);
+        std::memcpy(res.has_offset.data(), h.data() + o_has, sp);
+        std::memcpy(res.lat_present.data(), h.data() + o_pres, sp);
+        std::memcpy(res.has_z.data(), h.data() + o_hz, sp);
+        unsigned long long nd;
+        std::memcpy(&nd, h.data() + o_cnt + 16, 8);
+        res.have_offsets = nd > 0;
+    }
+    void collectives() {
+        const uint64_t sp = uint64_t(span);
+        unsigned long long* errs = reinterpret_cast<unsigned long long*>(cb + o_err);
+        unsigned long long* cnts = reinterpret_cast<unsigned long long*>(cb + o_cnt);  // n_seg, n_st, n_d, n_w
+        const uint64_t n = n_coll_all;
         if (n == 0) return;
         if (n >= 0xffffffffull) fail(STG_EINVAL, "too many collective events");
+        zero(cnts + 3, 8);  // n_w
         uint64_t* key = dev<uint64_t>("c_key", n);
         uint64_t* key_s = dev<uint64_t>("c_key_s", n);
         uint32_t* idx = dev<uint32_t>("c_idx", n);
@@ -296,8 +356,8 @@ struct Runner {
         const int kbits = std::max(1, bits_for(uint64_t(coll_rg[2])));
         const int gbits = bits_for(uint64_t(int64_t(coll_rg[1]) - coll_rg[0]));
         const uint64_t rmask = (1ull << rbits) - 1;
-        LAUNCH(k_coll_keys, grid_for(n), kThreads, n, cd_rank, cd_group, cd_kind, coll_rg[0], kbits, rbits, key, idx,
-               d_err);
+        LAUNCH(k_coll_keys, grid_for(n), kThreads, n, cd_rank, cd_group, cd_kind, coll_rg[0], kbits, rbits, 0, INT_MAX,
+               key, idx, d_err);
         sort_pairs(key, key_s, idx, idx_s, n, gbits + kbits + rbits);
         int64_t* s_entry = dev<int64_t>("c_sentry", n);
         int64_t* s_exit = dev<int64_t>("c_sexit", n);
@@ -462,90 +522,385 @@ struct Runner {
             double* sg = dev<double>("s_sg", n_w);
             uint32_t* m = dev<uint32_t>("s_m", n_w);
             LAUNCH(k_straggler_inst, grid_for(n_w * 32), kThreads, n_w, span, d_lat, cfg.k, mu, sg, m);
-            LAUNCH(k_straggler_rank, grid_for(sp * 32, kStragWarps * 32), kStragWarps * 32, n_w, span, d_lat, cfg.k, mu,
+            LAUNCH(k_straggler_rank, grid_for(sp * 32, kStragWarps * 32), kStragWarps * 32, n_w, 0, span, d_lat, cfg.k, mu,
                    sg, m, cb + o_pres, reinterpret_cast<double*>(cb + o_ma), reinterpret_cast<double*>(cb + o_ml),
                    reinterpret_cast<double*>(cb + o_zm), reinterpret_cast<uint64_t*>(cb + o_fl), cb + o_hz);
         }
         // one download for offsets, straggler statistics and counts; one for the iteration times
-        std::vector<uint8_t> h(o_end);
         if (n_w > 1) {
             res.iteration_times_ms.resize(n_w - 1);
             STG_CUDA(cudaMemcpyAsync(res.iteration_times_ms.data(), it, (n_w - 1) * 8, cudaMemcpyDeviceToHost, st));
             d2h += (n_w - 1) * 8;
         }
-        down(h.data(), cb, o_end);
-        std::memcpy(res.offsets.data(), h.data(), 8 * sp);
-        std::memcpy(res.mean_lat_all.data(), h.data() + o_ma, 8 * sp);
-        std::memcpy(res.mean_lat_alert.data(), h.data() + o_ml, 8 * sp);
-        std::memcpy(res.z_mean.data(), h.data() + o_zm, 8 * sp);
-        std::memcpy(res.flag_count.data(), h.data() + o_fl, 8 * sp);
-        std::memcpy(res.has_offset.data(), h.data() + o_has, sp);
-        std::memcpy(res.lat_present.data(), h.data() + o_pres, sp);
-        std::memcpy(res.has_z.data(), h.data() + o_hz, sp);
-        unsigned long long nd;
-        std::memcpy(&nd, h.data() + o_cnt + 16, 8);
-        res.have_offsets = nd > 0;
+        coll_result_download();
+    }
+
+    // ---------------------------------------------- rank-sharded stage d
+    // stg_window.shard_streams & STG_SHARD_COLL: every context holds only its
+    // ranks' collective events.  coll_local() (may fail; inside agreed()) sorts
+    // them into (stream, rank) segments and validates them; coll_exchange()
+    // (NCCL, never fails on input) builds the group-wide stream list, proves
+    // the regular case with gathered seed candidates, reduces the per-instance
+    // partials (max exit, group membership, max aligned exit, min adjusted
+    // entry), continues detect_straggler's rank-order sums from context to
+    // context (send/recv chain: the single-GPU rounding sequence), and sums the
+    // per-rank result blocks.  An irregular stream (missing events, late
+    // joiners: the greedy sweep's general case) falls back to gathering every
+    // event and running the replicated stage on each context.
+    struct CLocal {
+        uint64_t n = 0, n_seg = 0, n_st = 0;
+        uint64_t* key_s = nullptr;
+        int64_t *s_entry = nullptr, *s_exit = nullptr;
+        uint32_t *seg_pos = nullptr, *st_pos = nullptr, *stream_of_pos = nullptr, *st_seg = nullptr,
+                 *seg_stream = nullptr;
+        std::vector<uint64_t> skeys;
+        int rbits = 1;
+        uint64_t rmask = 1;
+    } cl;
+    static int bits_for(uint64_t v) {
+        int b = 0;
+        while (b < 64 && (v >> b)) ++b;
+        return b;
+    }
+    void coll_local() {
+        const int W = c.world, P = c.wrank;
+        const uint64_t n = w.n_coll;
+        cl = CLocal{};
+        cl.n = n;
+        cl.rbits = std::max(1, bits_for(uint64_t(span - 1)));
+        cl.rmask = (1ull << cl.rbits) - 1;
+        if (sh_base[W] >= 0xffffffffull) fail(STG_EINVAL, "too many collective events");
+        if (n == 0) return;
+        unsigned long long* errs = reinterpret_cast<unsigned long long*>(cb + o_err);
+        unsigned long long* cnts = reinterpret_cast<unsigned long long*>(cb + o_cnt);
+        const int kbits = std::max(1, bits_for(uint64_t(coll_rg[2])));
+        const int gbits = bits_for(uint64_t(int64_t(coll_rg[1]) - coll_rg[0]));
+        const int rlo = P == 0 ? 0 : int(sh_lo[P]);
+        const int rhi = int(std::min<int64_t>(sh_lo[P + 1], INT_MAX));
+        uint64_t* key = dev<uint64_t>("c_key", n);
+        cl.key_s = dev<uint64_t>("c_key_s", n);
+        uint32_t* idx = dev<uint32_t>("c_idx", n);
+        uint32_t* idx_s = dev<uint32_t>("c_idx_s", n);
+        int* d_err = reinterpret_cast<int*>(cnts + 3);  // n_w word, unused until windowing
+        zero(d_err, sizeof(int));
+        LAUNCH(k_coll_keys, grid_for(n), kThreads, n, cd_rank, cd_group, cd_kind, coll_rg[0], kbits, cl.rbits, rlo, rhi,
+               key, idx, d_err);
+        sort_pairs(key, cl.key_s, idx, idx_s, n, gbits + kbits + cl.rbits);
+        cl.s_entry = dev<int64_t>("c_sentry", n);
+        cl.s_exit = dev<int64_t>("c_sexit", n);
+        uint32_t* seg_flag = dev<uint32_t>("c_segflag", n);
+        uint32_t* stream_flag = dev<uint32_t>("c_stflag", n);
+        LAUNCH(k_coll_gather, grid_for(n), kThreads, n, cl.key_s, idx_s, cd_entry, cd_exit, cl.rbits, cl.s_entry,
+               cl.s_exit, errs, errs + 1, seg_flag, stream_flag);
+        cl.seg_pos = dev<uint32_t>("c_segpos", n + 1);
+        cl.st_pos = dev<uint32_t>("c_stpos", n + 1);
+        {
+            uint32_t* iota = dev<uint32_t>("sel_iota", n);
+            LAUNCH(k_iota, grid_for(n), kThreads, iota, n);
+            size_t tb = 0;
+            STG_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, iota, seg_flag, cl.seg_pos, cnts, n, st));
+            STG_CUDA(cub::DeviceSelect::Flagged(temp(tb), tb, iota, seg_flag, cl.seg_pos, cnts, n, st));
+            STG_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, iota, stream_flag, cl.st_pos, cnts + 1, n, st));
+            STG_CUDA(cub::DeviceSelect::Flagged(temp(tb), tb, iota, stream_flag, cl.st_pos, cnts + 1, n, st));
+            launches += 2;
+        }
+        unsigned long long h[6];  // entry >= exit, order, n_seg, n_st, n_d, out-of-shard flag
+        STG_CUDA(cudaMemcpyAsync(h, errs, 48, cudaMemcpyDeviceToHost, st));
+        STG_CUDA(cudaStreamSynchronize(st));
+        ++syncs;
+        if (uint32_t(h[5])) fail(STG_EINVAL, "collective event rank outside the context's shard (shard_rank_lo)");
+        if (h[0] != ~0ull || h[1] != ~0ull) {  // the group's first bad event in concatenated order
+            fail_rank = int64_t(sh_base[P] + std::min(h[0], h[1]));
+            if (h[0] <= h[1]) fail(STG_EINVAL, "collective event with entry >= exit");
+            fail(STG_EINVAL, "collective events not time-ordered within rank");
+        }
+        cl.n_seg = h[2];
+        cl.n_st = h[3];
+        {
+            const uint32_t nn = uint32_t(n);
+            STG_CUDA(cudaMemcpyAsync(cl.seg_pos + cl.n_seg, &nn, 4, cudaMemcpyHostToDevice, st));
+        }
+        cl.st_seg = dev<uint32_t>("c_stseg", cl.n_st + 1);
+        cl.seg_stream = dev<uint32_t>("c_segstream", cl.n_seg);
+        LAUNCH(k_stream_tables, grid_for(cl.n_seg + cl.n_st + 1), kThreads, cnts, cl.seg_pos, cl.st_pos, cl.st_seg,
+               cl.seg_stream);
+        cl.stream_of_pos = dev<uint32_t>("c_streamofpos", n);
+        incl_sum(stream_flag, cl.stream_of_pos, n);  // 1-based
+        uint64_t* skey = dev<uint64_t>("c_skey", cl.n_st);
+        LAUNCH(k_stream_keys, grid_for(cl.n_st), kThreads, cnts, cl.st_pos, cl.key_s, cl.rbits, skey);
+        cl.skeys.resize(cl.n_st);
+        down(cl.skeys.data(), skey, cl.n_st);
+    }
+
+    void coll_exchange() {
+        const int W = c.world, P = c.wrank;
+        if (sh_base[W] == 0) return;
+        const uint64_t sp = uint64_t(span), n = cl.n, n_st = cl.n_st, n_seg = cl.n_seg;
+        unsigned long long* cnts = reinterpret_cast<unsigned long long*>(cb + o_cnt);
+        // 1. the group's (group, kind) streams: sorted union of every context's
+        std::vector<uint8_t> mine(n_st * 8);
+        if (n_st) std::memcpy(mine.data(), cl.skeys.data(), n_st * 8);
+        std::vector<uint64_t> gs;
+        for (const auto& b : allgather_bytes(mine))
+            for (size_t i = 0; i + 8 <= b.size(); i += 8) {
+                uint64_t v;
+                std::memcpy(&v, b.data() + i, 8);
+                gs.push_back(v);
+            }
+        std::sort(gs.begin(), gs.end());
+        gs.erase(std::unique(gs.begin(), gs.end()), gs.end());
+        const uint64_t n_gs = gs.size();
+        std::vector<uint32_t> lg(n_st);
+        for (uint64_t s = 0; s < n_st; ++s)
+            lg[s] = uint32_t(std::lower_bound(gs.begin(), gs.end(), cl.skeys[s]) - gs.begin());
+        const uint32_t* d_lg = up<uint32_t>("cs_lg", lg.data(), n_st);
+        // 2. per stream: first entry (coarse offsets), per-rank event counts
+        long long* minfirst = dev<long long>("cs_minfirst", n_gs);
+        uint32_t* kk = dev<uint32_t>("cs_kk", 2 * n_gs);
+        LAUNCH(k_fill_i64, grid_for(n_gs), kThreads, minfirst, n_gs, LLONG_MAX);
+        zero(kk, 2 * n_gs * 4);
+        if (n_st)
+            LAUNCH(k_coll_stream_stats, unsigned(n_st), kThreads, int(n_st), cl.st_seg, cl.seg_pos, cl.s_entry, d_lg,
+                   uint32_t(n_gs), minfirst, kk);
+        nccl(ncclGroupStart());
+        nccl(ncclAllReduce(minfirst, minfirst, n_gs, ncclInt64, ncclMin, comm(), st));
+        nccl(ncclAllReduce(kk, kk, 2 * n_gs, ncclUint32, ncclMax, comm(), st));
+        nccl(ncclGroupEnd());
+        int64_t* coarse = dev<int64_t>("c_coarse", n_seg);
+        if (n_seg)
+            LAUNCH(k_coll_coarse, grid_for(n_seg), kThreads, n_seg, cl.seg_pos, cl.seg_stream, d_lg, cl.s_entry,
+                   minfirst, coarse);
+        std::vector<uint32_t> h_kk(2 * n_gs), kmax(n_gs), kmin(n_gs);
+        down(h_kk.data(), kk, 2 * n_gs);
+        for (uint64_t g = 0; g < n_gs; ++g) {
+            kmax[g] = h_kk[g];
+            kmin[g] = ~h_kk[n_gs + g];
+        }
+        // 3. regular-case proof: instance k of a stream = every rank's k-th event
+        std::vector<uint64_t> k_base(n_gs + 1, 0), lk_base(n_st + 1, 0);
+        for (uint64_t g = 0; g < n_gs; ++g) k_base[g + 1] = k_base[g] + kmin[g];
+        for (uint64_t s = 0; s < n_st; ++s) lk_base[s + 1] = lk_base[s] + kmin[lg[s]];
+        const uint64_t K = k_base[n_gs], nk = lk_base[n_st];
+        const uint64_t* d_kbase = up<uint64_t>("cs_kbase", k_base.data(), n_gs + 1);
+        const uint64_t* d_lkbase = up<uint64_t>("cs_lkbase", lk_base.data(), n_st + 1);
+        long long* cand = dev<long long>("cs_cand", 2 * K);
+        long long* cand_all = dev<long long>("cs_cand_all", 2 * K * W);
+        uint32_t* ffail = up<uint32_t>("cs_ffail", kmin.data(), n_gs);
+        if (K) {
+            LAUNCH(k_fill_i64, grid_for(2 * K), kThreads, cand, 2 * K, LLONG_MAX);
+            if (nk)
+                LAUNCH(k_coll_seed_cand, grid_for(nk * 32), kThreads, int(n_st), cl.st_seg, cl.seg_pos, coarse,
+                       cl.s_entry, cl.s_exit, d_lkbase, nk, d_lg, d_kbase, cand);
+            nccl(ncclAllGather(cand, cand_all, 2 * K, ncclInt64, comm(), st));
+            if (nk)
+                LAUNCH(k_coll_regular_sh, grid_for(nk * 32), kThreads, int(n_st), cl.st_seg, cl.seg_pos, coarse,
+                       cl.s_entry, cl.s_exit, d_lkbase, nk, d_lg, d_kbase, K, cand_all, W, w.max_skew_ns, ffail);
+            nccl(ncclAllReduce(ffail, ffail, n_gs, ncclUint32, ncclMin, comm(), st));
+        }
+        std::vector<uint32_t> k0(n_gs);
+        down(k0.data(), ffail, n_gs);
+        for (uint64_t g = 0; g < n_gs; ++g)
+            if (k0[g] < kmax[g]) {  // irregular somewhere: the general greedy sweep over all events
+                coll_gather_all();
+                collectives();
+                return;
+            }
+        // 4. instances (regular: every rank of a stream has k0 events)
+        std::vector<uint64_t> ibase(n_gs + 1, 0);
+        for (uint64_t g = 0; g < n_gs; ++g) ibase[g + 1] = ibase[g] + k0[g];
+        const uint64_t I = ibase[n_gs];
+        res.n_instances = I;
+        std::vector<uint64_t> base1(n_st + 1, 0);  // stream_of_pos is 1-based
+        std::vector<uint32_t> k0l(n_st);
+        for (uint64_t s = 0; s < n_st; ++s) {
+            base1[s + 1] = ibase[lg[s]];
+            k0l[s] = k0[lg[s]];
+        }
+        const uint64_t* d_ibase = up<uint64_t>("c_ibase", base1.data(), n_st + 1);
+        uint32_t* d_k0 = up<uint32_t>("c_k0l", k0l.data(), n_st);
+        uint32_t* inst_local = dev<uint32_t>("c_instlocal", n);
+        if (n_seg)
+            LAUNCH(k_coll_assign_regular, unsigned(std::min<uint64_t>(n_seg, 65535)), 128, int(n_st), cl.st_seg,
+                   cl.seg_pos, cl.seg_stream, uint32_t(n_seg), d_k0, inst_local);
+        std::vector<uint8_t> member(span, 0);
+        unsigned n_group = 0;
+        for (int32_t i = 0; i < w.n_group_ranks; ++i)
+            if (!member[size_t(w.group_ranks[i])]) {
+                member[size_t(w.group_ranks[i])] = 1;
+                ++n_group;
+            }
+        uint8_t* d_member = up<uint8_t>("c_member", member.data(), span);
+        uint32_t* inst_of = dev<uint32_t>("c_instof", n);
+        unsigned long long* imax = dev<unsigned long long>("c_imax", I);
+        unsigned* isize = dev<unsigned>("c_isize", I);
+        unsigned* iing = dev<unsigned>("c_iing", I);
+        LAUNCH(k_fill_i64, grid_for(I), kThreads, (long long*)imax, I, LLONG_MIN);
+        zero(isize, I * sizeof(unsigned));
+        zero(iing, I * sizeof(unsigned));
+        if (n)
+            LAUNCH(k_coll_inst, grid_for(n), kThreads, n, cl.key_s, nullptr, cl.stream_of_pos, d_ibase, inst_local,
+                   cl.s_exit, d_member, inst_of, imax, isize, iing, cl.rmask);
+        nccl(ncclGroupStart());
+        nccl(ncclAllReduce(imax, imax, I, ncclInt64, ncclMax, comm(), st));
+        nccl(ncclAllReduce(iing, iing, I, ncclUint32, ncclSum, comm(), st));
+        nccl(ncclGroupEnd());
+        // 5. align_clocks for this context's ranks (medians are per rank)
+        if (n) {
+            int64_t* dval = dev<int64_t>("c_dval", n);
+            uint32_t* dflag = dev<uint32_t>("c_dflag", n);
+            long long* d_dmin = dev<long long>("c_dmin", 1);
+            zero(d_dmin, 8);
+            LAUNCH(k_coll_deltas, grid_for(n), kThreads, n, inst_of, cl.s_exit, imax, iing, n_group, dval, dflag,
+                   d_dmin);
+            uint32_t* d_segrank = dev<uint32_t>("c_segrank", n_seg);
+            uint32_t* d_segrank_s = dev<uint32_t>("c_segrank_s", n_seg);
+            uint32_t* d_segid = dev<uint32_t>("c_segid", n_seg);
+            uint32_t* d_rsegs = dev<uint32_t>("c_rsegs", std::max<uint64_t>(n_seg, 1));
+            uint32_t* d_rso = dev<uint32_t>("c_rso", sp + 1);
+            LAUNCH(k_seg_rank, grid_for(n_seg), kThreads, n_seg, cl.seg_pos, cl.key_s, cl.rmask, d_segrank);
+            LAUNCH(k_iota, grid_for(n_seg), kThreads, d_segid, n_seg);
+            sort_pairs(d_segrank, d_segrank_s, d_segid, d_rsegs, n_seg, cl.rbits);
+            LAUNCH(k_rank_offsets, grid_for(sp + 1), kThreads, span, d_segrank_s, n_seg, d_rso);
+            const long long dmin = get1(d_dmin);
+            const int dbits = std::max(1, bits_for(uint64_t(-dmin)));
+            LAUNCH(k_coll_median_sel, unsigned(std::min<int64_t>(span, 148 * 16)), 256, int(span), d_rso, d_rsegs,
+                   cl.seg_pos, dval, dflag, dmin, dbits, d_off, d_has_off, cnts + 2);
+        }
+        // 6. windowed complete instances, ordered by the max aligned exit
+        unsigned long long* aexit = dev<unsigned long long>("c_aexit", I);
+        zero(aexit, I * 8);
+        if (n)
+            LAUNCH(k_coll_aligned_exit, grid_for(n), kThreads, n, cl.key_s, inst_of, cl.s_exit, iing, n_group, d_off,
+                   aexit, cl.rmask);
+        nccl(ncclAllReduce(aexit, aexit, I, ncclInt64, ncclMax, comm(), st));
+        uint64_t* wkey = dev<uint64_t>("c_wkey", I);
+        uint64_t* wkey_s = dev<uint64_t>("c_wkey_s", I);
+        uint32_t* winst = dev<uint32_t>("c_winst", I);
+        uint32_t* winst_s = dev<uint32_t>("c_winst_s", I);
+        unsigned long long* nw = cnts + 3;
+        zero(nw, 8);
+        LAUNCH(k_coll_window_select, grid_for(I), kThreads, I, iing, n_group, aexit, w.window_start_ns, wkey, winst,
+               nw);
+        const uint64_t n_w = get1(nw);
+        res.n_windowed = n_w;
+        sort_pairs(wkey, wkey_s, winst, winst_s, n_w);
+        uint32_t* inst_w = dev<uint32_t>("c_instw", I);
+        STG_CUDA(cudaMemsetAsync(inst_w, 0xff, I * sizeof(uint32_t), st));
+        LAUNCH(k_coll_winv, grid_for(n_w), kThreads, n_w, winst_s, inst_w);
+        long long* wmin = dev<long long>("c_wmin", n_w);
+        LAUNCH(k_fill_i64, grid_for(n_w), kThreads, wmin, n_w, LLONG_MAX);
+        if (n)
+            LAUNCH(k_coll_minadj, grid_for(n), kThreads, n, cl.key_s, inst_of, inst_w, cl.s_entry, d_off, wmin,
+                   cl.rmask);
+        nccl(ncclAllReduce(wmin, wmin, n_w, ncclInt64, ncclMin, comm(), st));
+        d_lat = dev<double>("lat", sp * n_w);
+        LAUNCH(k_fill_f64, grid_for(sp * n_w), kThreads, d_lat, sp * n_w, nan(""));
+        if (n)
+            LAUNCH(k_coll_lateness, grid_for(n), kThreads, n, cl.key_s, inst_of, inst_w, cl.s_entry, d_off, wmin, n_w,
+                   d_lat, cl.rmask);
+        double* it = dev<double>("c_it", std::max<uint64_t>(n_w, 1));
+        if (n_w > 1) LAUNCH(k_coll_itertimes, grid_for(n_w), kThreads, n_w, wkey_s, it);
+        // 7. detect_straggler: per-instance sums in rank order, context after context
+        if (n_w) {
+            double* chain = dev<double>("s_chain", 2 * n_w);
+            double* s2 = dev<double>("s_s2", n_w);
+            double* mu = dev<double>("s_mu", n_w);
+            double* sg = dev<double>("s_sg", n_w);
+            uint32_t* m = dev<uint32_t>("s_m", n_w);
+            if (P == 0) zero(chain, 16 * n_w);
+            else nccl(ncclRecv(chain, 2 * n_w, ncclFloat64, P - 1, comm(), st));
+            LAUNCH(k_strag_chain1, grid_for(n_w * 32), kThreads, n_w, r_lo, r_hi, d_lat, chain);
+            if (P + 1 < W) nccl(ncclSend(chain, 2 * n_w, ncclFloat64, P + 1, comm(), st));
+            nccl(ncclBroadcast(chain, chain, 2 * n_w, ncclFloat64, W - 1, comm(), st));
+            LAUNCH(k_strag_mu, grid_for(n_w), kThreads, n_w, chain, mu, m);
+            if (P == 0) zero(s2, 8 * n_w);
+            else nccl(ncclRecv(s2, n_w, ncclFloat64, P - 1, comm(), st));
+            LAUNCH(k_strag_chain2, grid_for(n_w * 32), kThreads, n_w, r_lo, r_hi, d_lat, mu, m, s2);
+            if (P + 1 < W) nccl(ncclSend(s2, n_w, ncclFloat64, P + 1, comm(), st));
+            nccl(ncclBroadcast(s2, s2, n_w, ncclFloat64, W - 1, comm(), st));
+            LAUNCH(k_strag_sigma, grid_for(n_w), kThreads, n_w, s2, m, sg);
+            if (r_hi > r_lo)
+                LAUNCH(k_straggler_rank, grid_for(uint64_t(r_hi - r_lo) * 32, kStragWarps * 32), kStragWarps * 32, n_w,
+                       r_lo, r_hi, d_lat, cfg.k, mu, sg, m, cb + o_pres, reinterpret_cast<double*>(cb + o_ma),
+                       reinterpret_cast<double*>(cb + o_ml), reinterpret_cast<double*>(cb + o_zm),
+                       reinterpret_cast<uint64_t*>(cb + o_fl), cb + o_hz);
+        }
+        // 8. per-rank blocks (offsets, straggler statistics): each rank's row is
+        //    non-zero on its owner only, so sums rebuild the single-context block
+        nccl(ncclGroupStart());
+        nccl(ncclAllReduce(cb, cb, sp, ncclInt64, ncclSum, comm(), st));
+        nccl(ncclAllReduce(cb + o_ma, cb + o_ma, 3 * sp, ncclFloat64, ncclSum, comm(), st));
+        nccl(ncclAllReduce(cb + o_fl, cb + o_fl, sp, ncclUint64, ncclSum, comm(), st));
+        nccl(ncclAllReduce(cb + o_has, cb + o_has, 3 * sp, ncclUint8, ncclSum, comm(), st));
+        nccl(ncclAllReduce(cnts + 2, cnts + 2, 1, ncclUint64, ncclSum, comm(), st));
+        nccl(ncclGroupEnd());
+        if (n_w > 1) {
+            res.iteration_times_ms.resize(n_w - 1);
+            STG_CUDA(cudaMemcpyAsync(res.iteration_times_ms.data(), it, (n_w - 1) * 8, cudaMemcpyDeviceToHost, st));
+            d2h += (n_w - 1) * 8;
+        }
+        coll_result_download();
+    }
+
+    // Irregular fallback: every context gathers the group's events (its own
+    // list concatenated in world-rank order = the group's event order).
+    void coll_gather_all() {
+        const int W = c.world;
+        const uint64_t N = sh_base[W], n = w.n_coll;
+        uint64_t mx = 1;
+        for (int q = 0; q < W; ++q) mx = std::max<uint64_t>(mx, uint64_t(sh_n[q]));
+        auto gather = [&](const void* src, size_t esz, const char* nm_send, const char* nm_pad, const char* nm_out) {
+            uint8_t* snd = dev<uint8_t>(nm_send, mx * esz);
+            uint8_t* pad = dev<uint8_t>(nm_pad, mx * esz * W);
+            uint8_t* out = dev<uint8_t>(nm_out, N * esz);
+            if (n) STG_CUDA(cudaMemcpyAsync(snd, src, n * esz, cudaMemcpyDeviceToDevice, st));
+            nccl(ncclAllGather(snd, pad, mx * esz, ncclUint8, comm(), st));
+            for (int q = 0; q < W; ++q)
+                if (sh_n[q])
+                    STG_CUDA(cudaMemcpyAsync(out + sh_base[q] * esz, pad + q * mx * esz, sh_n[q] * esz,
+                                             cudaMemcpyDeviceToDevice, st));
+            return static_cast<const void*>(out);
+        };
+        cd_rank = static_cast<const int32_t*>(gather(cd_rank, 4, "cg_snd_r", "cg_pad_r", "cg_rank"));
+        cd_group = static_cast<const int32_t*>(gather(cd_group, 4, "cg_snd_g", "cg_pad_g", "cg_group"));
+        cd_kind = static_cast<const uint8_t*>(gather(cd_kind, 1, "cg_snd_k", "cg_pad_k", "cg_kind"));
+        cd_entry = static_cast<const int64_t*>(gather(cd_entry, 8, "cg_snd_e", "cg_pad_e", "cg_entry"));
+        cd_exit = static_cast<const int64_t*>(gather(cd_exit, 8, "cg_snd_x", "cg_pad_x", "cg_exit"));
+        n_coll_all = N;
     }
 
     // ------------------------------------------------------------ gpu/os
+    // Per-rank GPU kernel time and OS counter sums (build_group_data
+    // bundle.cpp:302-320) in device buffers, validated; the host maps are read
+    // back by gpu_os_collect().  With sharded side streams every context holds
+    // the same buffers (its own ranks' rows filled) and gpu_os_reduce() sums
+    // them over the group first.
     void gpu_os() {
         res.gpu.clear();
         res.os.clear();
-        if (w.n_gpu) {
+        const bool shard = side_sharded();
+        const bool sdev = w.side_memory == STG_MEM_DEVICE;
+        if (w.n_gpu || (shard && w.n_kernel_names)) {
             const uint64_t n = w.n_gpu, K = w.n_kernel_names;
-            const bool sdev = w.side_memory == STG_MEM_DEVICE;
-            const int32_t* d_rank = sdev ? w.gpu_rank : static_cast<const int32_t*>(c.buf("gpu_rank").p);
-            const uint32_t* d_k = sdev ? w.gpu_kernel : up<uint32_t>("gpu_k", w.gpu_kernel, n);
-            const int64_t* d_s = sdev ? w.gpu_start : up<int64_t>("gpu_s", w.gpu_start, n);
-            const int64_t* d_d = sdev ? w.gpu_dur : up<int64_t>("gpu_d", w.gpu_dur, n);
             unsigned long long* sums = dev<unsigned long long>("gpu_sums", span * K);
             uint8_t* pres = dev<uint8_t>("gpu_pres", span * K);
-            int* err = dev<int>("gpu_err", 1);
             zero(sums, span * K * 8);
             zero(pres, span * K);
-            zero(err, 4);
-            LAUNCH(k_gpu_sums, grid_for(n), kThreads, n, d_rank, d_k, d_s, d_d, d_off, w.window_start_ns, uint32_t(K),
-                   sums, pres, err);
-            if (get1(err)) fail(STG_EINVAL, "gpu event kernel index out of range");
-            std::vector<unsigned long long> hs(span * K);
-            std::vector<uint8_t> hp(span * K);
-            down(hs.data(), sums, span * K);
-            down(hp.data(), pres, span * K);
-            for (int32_t r = 0; r < span; ++r)
-                for (uint64_t k = 0; k < K; ++k)
-                    if (hp[r * K + k]) res.gpu[r][w.kernel_names[k]] += int64_t(hs[r * K + k]);
-        }
-        if (w.n_os) {
-            const uint64_t n = w.n_os, C = std::max<uint32_t>(w.n_counter_names, 1);
-            const bool sdev = w.side_memory == STG_MEM_DEVICE;
-            const int32_t* d_rank = sdev ? w.os_rank : static_cast<const int32_t*>(c.buf("os_rank").p);
-            const int64_t *ws, *p50, *p99, *mig, *ival, *sval;
-            const uint64_t *ioff, *soff;
-            const uint32_t *ikey, *skey;
-            if (sdev) {
-                ws = w.os_window_start;
-                p50 = w.os_p50;
-                p99 = w.os_p99;
-                mig = w.os_migrations;
-                ioff = w.os_irq_off;
-                ikey = w.os_irq_key;
-                ival = w.os_irq_val;
-                soff = w.os_sirq_off;
-                skey = w.os_sirq_key;
-                sval = w.os_sirq_val;
-            } else {
-                ws = up<int64_t>("os_ws", w.os_window_start, n);
-                p50 = up<int64_t>("os_p50", w.os_p50, n);
-                p99 = up<int64_t>("os_p99", w.os_p99, n);
-                mig = up<int64_t>("os_mig", w.os_migrations, n);
-                ioff = up<uint64_t>("os_ioff", w.os_irq_off, n + 1);
-                const uint64_t ni = w.os_irq_off[n], ns = w.os_sirq_off[n];
-                ikey = up<uint32_t>("os_ikey", w.os_irq_key, ni);
-                ival = up<int64_t>("os_ival", w.os_irq_val, ni);
-                soff = up<uint64_t>("os_soff", w.os_sirq_off, n + 1);
-                skey = up<uint32_t>("os_skey", w.os_sirq_key, ns);
-                sval = up<int64_t>("os_sval", w.os_sirq_val, ns);
+            if (n) {
+                const int32_t* d_rank = sdev ? w.gpu_rank : static_cast<const int32_t*>(c.buf("gpu_rank").p);
+                const uint32_t* d_k = sdev ? w.gpu_kernel : up<uint32_t>("gpu_k", w.gpu_kernel, n);
+                const int64_t* d_s = sdev ? w.gpu_start : up<int64_t>("gpu_s", w.gpu_start, n);
+                const int64_t* d_d = sdev ? w.gpu_dur : up<int64_t>("gpu_d", w.gpu_dur, n);
+                int* err = dev<int>("gpu_err", 1);
+                zero(err, 4);
+                LAUNCH(k_gpu_sums, grid_for(n), kThreads, n, d_rank, d_k, d_s, d_d, d_off, w.window_start_ns,
+                       uint32_t(K), sums, pres, err);
+                if (get1(err)) fail(STG_EINVAL, "gpu event kernel index out of range");
             }
+            gpu_bufs = true;
+        }
+        if (w.n_os || shard) {
+            const uint64_t n = w.n_os, C = std::max<uint32_t>(w.n_counter_names, 1);
             auto irq = dev<unsigned long long>("os_irq", span * C);
             auto irqp = dev<uint8_t>("os_irqp", span * C);
             auto sirq = dev<unsigned long long>("os_sirq", span * C);
@@ -554,7 +909,6 @@ struct Runner {
             auto mp99 = dev<long long>("os_mp99", span);
             auto migs = dev<unsigned long long>("os_migs", span);
             auto pres = dev<uint8_t>("os_pres", span);
-            int* err = dev<int>("os_err", 1);
             zero(irq, span * C * 8);
             zero(irqp, span * C);
             zero(sirq, span * C * 8);
@@ -563,22 +917,102 @@ struct Runner {
             zero(mp99, span * 8);
             zero(migs, span * 8);
             zero(pres, span);
-            zero(err, 4);
-            LAUNCH(k_os_sums, grid_for(n), kThreads, n, d_rank, ws, p50, p99, mig, ioff, ikey, ival, soff, skey, sval,
-                   d_off, w.window_start_ns, uint32_t(w.n_counter_names), irq, irqp, sirq, sirqp, mp50, mp99, migs,
-                   pres, err);
-            if (get1(err)) fail(STG_EINVAL, "os counter key index out of range");
+            if (n) {
+                const int32_t* d_rank = sdev ? w.os_rank : static_cast<const int32_t*>(c.buf("os_rank").p);
+                const int64_t *ws, *p50, *p99, *mig, *ival, *sval;
+                const uint64_t *ioff, *soff;
+                const uint32_t *ikey, *skey;
+                if (sdev) {
+                    ws = w.os_window_start;
+                    p50 = w.os_p50;
+                    p99 = w.os_p99;
+                    mig = w.os_migrations;
+                    ioff = w.os_irq_off;
+                    ikey = w.os_irq_key;
+                    ival = w.os_irq_val;
+                    soff = w.os_sirq_off;
+                    skey = w.os_sirq_key;
+                    sval = w.os_sirq_val;
+                } else {
+                    ws = up<int64_t>("os_ws", w.os_window_start, n);
+                    p50 = up<int64_t>("os_p50", w.os_p50, n);
+                    p99 = up<int64_t>("os_p99", w.os_p99, n);
+                    mig = up<int64_t>("os_mig", w.os_migrations, n);
+                    ioff = up<uint64_t>("os_ioff", w.os_irq_off, n + 1);
+                    const uint64_t ni = w.os_irq_off[n], ns = w.os_sirq_off[n];
+                    ikey = up<uint32_t>("os_ikey", w.os_irq_key, ni);
+                    ival = up<int64_t>("os_ival", w.os_irq_val, ni);
+                    soff = up<uint64_t>("os_soff", w.os_sirq_off, n + 1);
+                    skey = up<uint32_t>("os_skey", w.os_sirq_key, ns);
+                    sval = up<int64_t>("os_sval", w.os_sirq_val, ns);
+                }
+                int* err = dev<int>("os_err", 1);
+                zero(err, 4);
+                LAUNCH(k_os_sums, grid_for(n), kThreads, n, d_rank, ws, p50, p99, mig, ioff, ikey, ival, soff, skey,
+                       sval, d_off, w.window_start_ns, uint32_t(w.n_counter_names), irq, irqp, sirq, sirqp, mp50, mp99,
+                       migs, pres, err);
+                if (get1(err)) fail(STG_EINVAL, "os counter key index out of range");
+            }
+            os_bufs = true;
+        }
+        if (!shard) gpu_os_collect();
+    }
+    bool gpu_bufs = false, os_bufs = false;
+    // sharded side streams: each rank's sums live on the context that owns it
+    // (zeros elsewhere; p50 / p99 are maxima of non-negative values), so a sum
+    // over the group reproduces the single-context arrays
+    void gpu_os_reduce() {
+        const uint64_t K = w.n_kernel_names, C = std::max<uint32_t>(w.n_counter_names, 1), sp = uint64_t(span);
+        nccl(ncclGroupStart());
+        if (gpu_bufs) {
+            auto sums = dev<unsigned long long>("gpu_sums", sp * K);
+            auto pres = dev<uint8_t>("gpu_pres", sp * K);
+            nccl(ncclAllReduce(sums, sums, sp * K, ncclUint64, ncclSum, comm(), st));
+            nccl(ncclAllReduce(pres, pres, sp * K, ncclUint8, ncclMax, comm(), st));
+        }
+        if (os_bufs) {
+            for (const char* nm : {"os_irq", "os_sirq"}) {
+                auto p = dev<unsigned long long>(nm, sp * C);
+                nccl(ncclAllReduce(p, p, sp * C, ncclUint64, ncclSum, comm(), st));
+            }
+            for (const char* nm : {"os_irqp", "os_sirqp"}) {
+                auto p = dev<uint8_t>(nm, sp * C);
+                nccl(ncclAllReduce(p, p, sp * C, ncclUint8, ncclMax, comm(), st));
+            }
+            for (const char* nm : {"os_mp50", "os_mp99", "os_migs"}) {
+                auto p = dev<long long>(nm, sp);
+                nccl(ncclAllReduce(p, p, sp, ncclInt64, ncclSum, comm(), st));
+            }
+            auto pres = dev<uint8_t>("os_pres", sp);
+            nccl(ncclAllReduce(pres, pres, sp, ncclUint8, ncclMax, comm(), st));
+        }
+        nccl(ncclGroupEnd());
+        gpu_os_collect();
+    }
+    void gpu_os_collect() {
+        if (gpu_bufs) {
+            const uint64_t K = w.n_kernel_names;
+            std::vector<unsigned long long> hs(span * K);
+            std::vector<uint8_t> hp(span * K);
+            down(hs.data(), dev<unsigned long long>("gpu_sums", span * K), span * K);
+            down(hp.data(), dev<uint8_t>("gpu_pres", span * K), span * K);
+            for (int32_t r = 0; r < span; ++r)
+                for (uint64_t k = 0; k < K; ++k)
+                    if (hp[r * K + k]) res.gpu[r][w.kernel_names[k]] += int64_t(hs[r * K + k]);
+        }
+        if (os_bufs) {
+            const uint64_t C = std::max<uint32_t>(w.n_counter_names, 1);
             std::vector<unsigned long long> hi(span * C), hs(span * C), hm(span);
             std::vector<uint8_t> hip(span * C), hsp(span * C), hp(span);
             std::vector<long long> h50(span), h99(span);
-            down(hi.data(), irq, span * C);
-            down(hs.data(), sirq, span * C);
-            down(hip.data(), irqp, span * C);
-            down(hsp.data(), sirqp, span * C);
-            down(hp.data(), pres, span);
-            down(h50.data(), mp50, span);
-            down(h99.data(), mp99, span);
-            down(hm.data(), migs, span);
+            down(hi.data(), dev<unsigned long long>("os_irq", span * C), span * C);
+            down(hs.data(), dev<unsigned long long>("os_sirq", span * C), span * C);
+            down(hip.data(), dev<uint8_t>("os_irqp", span * C), span * C);
+            down(hsp.data(), dev<uint8_t>("os_sirqp", span * C), span * C);
+            down(hp.data(), dev<uint8_t>("os_pres", span), span);
+            down(h50.data(), dev<long long>("os_mp50", span), span);
+            down(h99.data(), dev<long long>("os_mp99", span), span);
+            down(hm.data(), dev<unsigned long long>("os_migs", span), span);
             for (int32_t r = 0; r < span; ++r) {
                 if (!hp[r]) continue;
                 OsAcc& a = res.os[r];
@@ -597,9 +1031,20 @@ struct Runner {
     // shared memory covers up to kMaxSmemBins binaries
     // 4 resident CTAs of 8 warps per SM (64 registers); the table staging in
     // shared memory covers up to kMaxSmemBins binaries
+    // Shallow windows (<= 14 frames per sample on average, the C1/C3 shapes)
+    // take the staged form: each batch's frames arrive in shared memory by one
+    // bulk copy issued during the previous batch's lookups.
     void launch_sym_agg(const AggParams& p, unsigned grid, bool smem_tabs) {
-        if (smem_tabs) k_sym_agg<true, 4, 1, 1><<<grid, kThreads, 0, st>>>(p);
-        else k_sym_agg<false, 4, 1, 1><<<grid, kThreads, 0, st>>>(p);
+        const bool stage = smem_tabs && p.n_frames <= 14 * p.n_samples;
+        if (stage) {
+            STG_CUDA(cudaFuncSetAttribute(k_sym_agg<true, 4, 1, 1, false, true>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kStageSmem));
+            k_sym_agg<true, 4, 1, 1, false, true><<<grid, kThreads, kStageSmem, st>>>(p);
+        } else if (smem_tabs) {
+            k_sym_agg<true, 4, 1, 1><<<grid, kThreads, 0, st>>>(p);
+        } else {
+            k_sym_agg<false, 4, 1, 1><<<grid, kThreads, 0, st>>>(p);
+        }
     }
 
     // ---------------------------------------------------------- samples
@@ -880,7 +1325,7 @@ struct Runner {
     bool fold_bad = false;
     unsigned* s_unk_used = nullptr;  // inside the samples stage's output block
     int *s_unk_ovf = nullptr, *s_ebin = nullptr;
-    int32_t fail_rank = -1;  // rank whose validation failed (distributed error agreement)
+    int64_t fail_rank = -1;  // rank (or group event index) whose validation failed (distributed error agreement)
 
     // table-capacity hints kept on the context between windows
     uint64_t c_cap_hint(int r, uint64_t nr) {
@@ -2142,9 +2587,18 @@ struct Runner {
         agreed([&] { rank_space(); });
         rank_span_agree();
         mark("rank_space");
+        agreed([&] { coll_result_init(); });
+        n_coll_all = w.n_coll;
+        if (coll_sharded()) {  // local half may fail (agreed), the exchange does not
+            agreed([&] {
+                err_stage = 0;
+                coll_local();
+            });
+            coll_exchange();
+        }
         agreed([&] {
             err_stage = 0;
-            collectives();
+            if (!coll_sharded()) collectives();
             cudaEventRecord(ev[1], st);
             mark("collectives");
             err_stage = 1;
@@ -2152,6 +2606,7 @@ struct Runner {
             err_stage = 2;
             if (!gpu_os_done) gpu_os();
         });
+        if (side_sharded()) gpu_os_reduce();
         mark("samples+fold");
         if (ev_unset_fold()) {
             cudaEventRecord(ev[2], st);

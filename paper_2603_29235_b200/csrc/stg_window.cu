@@ -113,12 +113,14 @@ __global__ void k_coll_ranges(uint64_t n, const int32_t* group, const uint8_t* k
 // key = (group - gmin) << (kbits + rbits) | kind << rbits | rank: a stable sort
 // on it splits events into (group, kind) streams and per-rank runs while keeping
 // each rank's input order (collective.cpp:33-43).
+// err_rank: set when an event's rank lies outside [rlo, rhi) (a sharded
+// context's own ranks; [0, 2^24) otherwise).
 __global__ void k_coll_keys(uint64_t n, const int32_t* rank, const int32_t* group, const uint8_t* kind, int gmin,
-                            int kbits, int rbits, uint64_t* key, uint32_t* idx, int* err_rank) {
+                            int kbits, int rbits, int rlo, int rhi, uint64_t* key, uint32_t* idx, int* err_rank) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x) {
         int32_t r = rank[i];
-        if (r < 0 || r >= (1 << 24)) *err_rank = 1;
+        if (r < rlo || r >= rhi || r >= (1 << 24)) *err_rank = 1;
         key[i] = (uint64_t(uint32_t(group[i] - gmin)) << (kbits + rbits)) | (uint64_t(kind[i]) << rbits) |
                  uint64_t(uint32_t(r) & 0xffffffu);
         idx[i] = uint32_t(i);
@@ -595,14 +597,14 @@ __global__ void k_straggler_inst(uint64_t n_w, int rank_span, const double* lat,
 constexpr int kStragChunk = 256;
 constexpr int kStragWarps = 8;
 __global__ void __launch_bounds__(kStragWarps * 32) k_straggler_rank(
-    uint64_t n_w, int rank_span, const double* lat, double k, const double* mu_w, const double* sigma_w,
+    uint64_t n_w, int r_lo, int r_hi, const double* lat, double k, const double* mu_w, const double* sigma_w,
     const uint32_t* m_w, uint8_t* present, double* mean_all, double* mean_alert, double* z_mean, uint64_t* flags,
     uint8_t* has_z) {
     __shared__ double s_val[kStragWarps][kStragChunk];
     __shared__ double s_z[kStragWarps][kStragChunk];
     __shared__ uint8_t s_bits[kStragWarps][kStragChunk];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int r = int((blockIdx.x * blockDim.x + threadIdx.x) >> 5); r < rank_span;
+    for (int r = r_lo + int((blockIdx.x * blockDim.x + threadIdx.x) >> 5); r < r_hi;
          r += int((gridDim.x * blockDim.x) >> 5)) {
         double acc = 0.0;  // lane 0: Σ all present, lane 1: Σ alert, lane 2: Σ z of flagged
         uint64_t n_all = 0, n2 = 0, nz = 0;
@@ -653,6 +655,194 @@ __global__ void __launch_bounds__(kStragWarps * 32) k_straggler_rank(
             has_z[r] = nz > 0;
         }
     }
+}
+
+// ------------------------------------------------ rank-sharded stage d
+// When the collective events are sharded by rank over the GPUs of one group
+// (stg_window.shard_streams & STG_SHARD_COLL), each GPU runs the kernels above
+// on its own ranks' (stream, rank) segments; what crosses GPUs are the
+// per-stream and per-instance partials below (reduced / gathered over NCCL).
+
+// Per local stream: min first entry, min / max per-rank event count, written
+// at the stream's global index (each global stream is at most one local one).
+__global__ void k_coll_stream_stats(int n_streams, const uint32_t* st_seg, const uint32_t* seg_pos,
+                                    const int64_t* s_entry, const uint32_t* lg, uint32_t n_gs, long long* min_first,
+                                    uint32_t* kk /* [0, n_gs): kmax, [n_gs, 2 n_gs): ~kmin */) {
+    const int s = blockIdx.x;
+    if (s >= n_streams) return;
+    const uint32_t a = st_seg[s], b = st_seg[s + 1];
+    __shared__ long long s_min;
+    __shared__ unsigned s_kmin, s_kmax;
+    if (threadIdx.x == 0) {
+        s_min = LLONG_MAX;
+        s_kmin = 0xffffffffu;
+        s_kmax = 0;
+    }
+    __syncthreads();
+    for (uint32_t j = a + threadIdx.x; j < b; j += blockDim.x) {
+        atomicMin(&s_min, (long long)s_entry[seg_pos[j]]);
+        const uint32_t len = seg_pos[j + 1] - seg_pos[j];
+        atomicMin(&s_kmin, len);
+        atomicMax(&s_kmax, len);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t g = lg[s];
+        min_first[g] = s_min;
+        kk[g] = s_kmax;
+        kk[n_gs + g] = ~s_kmin;
+    }
+}
+
+// coarse pre-alignment of each local segment against the group-wide first entry
+__global__ void k_coll_coarse(uint64_t n_seg, const uint32_t* seg_pos, const uint32_t* seg_stream, const uint32_t* lg,
+                              const int64_t* s_entry, const long long* min_first, int64_t* coarse) {
+    for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < n_seg; j += uint64_t(gridDim.x) * blockDim.x)
+        coarse[j] = s_entry[seg_pos[j]] - min_first[lg[seg_stream[j]]];
+}
+
+// Work item t of the local regular proof -> (local stream, k); lk_base over
+// local streams is the prefix sum of the streams' global min counts.
+__device__ __forceinline__ int local_stream_of(const uint64_t* lk_base, int n_streams, uint64_t t) {
+    int lo = 0, hi = n_streams - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (lk_base[mid] <= t) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// Seed candidate of instance (stream, k) from this GPU's ranks: the lowest
+// pre-aligned entry (ties to the lowest rank) and that event's exit.  Candidates
+// of all GPUs are gathered; the seed is the first minimum in world-rank order,
+// which is the lowest rank because the shards are ascending rank intervals.
+__global__ void k_coll_seed_cand(int n_streams, const uint32_t* st_seg, const uint32_t* seg_pos,
+                                 const int64_t* coarse, const int64_t* s_entry, const int64_t* s_exit,
+                                 const uint64_t* lk_base, uint64_t n_k, const uint32_t* lg, const uint64_t* k_base,
+                                 long long* cand /* [K][2] */) {
+    const int lane = threadIdx.x & 31;
+    for (uint64_t t = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; t < n_k;
+         t += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+        const int s = local_stream_of(lk_base, n_streams, t);
+        const uint32_t k = uint32_t(t - lk_base[s]);
+        const uint32_t a = st_seg[s], b = st_seg[s + 1];
+        long long best = LLONG_MAX;
+        uint32_t bj = 0xffffffffu;
+        for (uint32_t j = a + lane; j < b; j += 32) {
+            const long long e = s_entry[seg_pos[j] + k] - coarse[j];
+            if (e < best) {
+                best = e;
+                bj = j;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const long long ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const uint32_t oj = __shfl_xor_sync(0xffffffffu, bj, o);
+            if (ob < best || (ob == best && oj < bj)) {
+                best = ob;
+                bj = oj;
+            }
+        }
+        if (lane == 0) {
+            const uint64_t gi = k_base[lg[s]] + k;
+            cand[2 * gi] = best;
+            cand[2 * gi + 1] = s_exit[seg_pos[bj] + k] - coarse[bj];
+        }
+    }
+}
+
+// The regular-case proof on this GPU's heads against the group-wide seed.
+__global__ void k_coll_regular_sh(int n_streams, const uint32_t* st_seg, const uint32_t* seg_pos,
+                                  const int64_t* coarse, const int64_t* s_entry, const int64_t* s_exit,
+                                  const uint64_t* lk_base, uint64_t n_k, const uint32_t* lg, const uint64_t* k_base,
+                                  uint64_t K, const long long* cand_all, int world, int64_t skew,
+                                  uint32_t* first_fail /* global stream index */) {
+    const int lane = threadIdx.x & 31;
+    for (uint64_t t = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; t < n_k;
+         t += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+        const int s = local_stream_of(lk_base, n_streams, t);
+        const uint32_t k = uint32_t(t - lk_base[s]);
+        const uint64_t gi = k_base[lg[s]] + k;
+        long long best = LLONG_MAX, best_exit = 0;
+        for (int q = 0; q < world; ++q) {  // first minimum in world order
+            const long long e = cand_all[(uint64_t(q) * K + gi) * 2];
+            if (e < best) {
+                best = e;
+                best_exit = cand_all[(uint64_t(q) * K + gi) * 2 + 1];
+            }
+        }
+        const uint32_t a = st_seg[s], b = st_seg[s + 1];
+        bool ok = true;
+        for (uint32_t j = a + lane; j < b && ok; j += 32) {
+            const uint64_t p = seg_pos[j] + k;
+            const long long e = s_entry[p] - coarse[j], x = s_exit[p] - coarse[j];
+            ok = e <= best_exit + skew && x + skew >= best;
+        }
+        ok = __all_sync(0xffffffffu, ok);
+        if (!ok && lane == 0) atomicMin(first_fail + lg[s], k);
+    }
+}
+
+// detect_straggler's per-instance sums (diagnosis.cpp:82-96) split along the
+// rank order: each GPU continues the chains of the GPUs before it over its
+// own ranks [r0, r1) — the same sequence of double roundings as one pass over
+// all ranks.  Pass 1: (Σ l, count) per instance; pass 2: Σ (l - μ)².
+__global__ void k_strag_chain1(uint64_t n_w, int r0, int r1, const double* lat, double* chain /* [n_w][2] */) {
+    const int lane = threadIdx.x & 31;
+    for (uint64_t w = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; w < n_w;
+         w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+        double acc = chain[2 * w];
+        uint32_t m = 0;
+        for (int rb = r0; rb < r1; rb += 32) {
+            const int r = rb + lane;
+            const double l = r < r1 ? lat[uint64_t(r) * n_w + w] : nan("");
+            const unsigned pres = __ballot_sync(0xffffffffu, l == l);
+            m += __popc(pres);
+            for (unsigned q = pres; q; q &= q - 1) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, l, __ffs(q) - 1));
+        }
+        if (lane == 0) {
+            chain[2 * w] = acc;
+            chain[2 * w + 1] += double(m);
+        }
+    }
+}
+__global__ void k_strag_mu(uint64_t n_w, const double* chain, double* mu_w, uint32_t* m_w) {
+    for (uint64_t w = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; w < n_w; w += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t m = uint32_t(chain[2 * w + 1]);
+        m_w[w] = m;
+        mu_w[w] = m >= 2 ? __ddiv_rn(chain[2 * w], double(m)) : 0.0;
+    }
+}
+__global__ void k_strag_chain2(uint64_t n_w, int r0, int r1, const double* lat, const double* mu_w,
+                               const uint32_t* m_w, double* s2_w) {
+    const int lane = threadIdx.x & 31;
+    for (uint64_t w = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; w < n_w;
+         w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+        if (m_w[w] < 2) continue;
+        const double mu = mu_w[w];
+        double s2 = s2_w[w];
+        for (int rb = r0; rb < r1; rb += 32) {
+            const int r = rb + lane;
+            const double l = r < r1 ? lat[uint64_t(r) * n_w + w] : nan("");
+            const double d = __dsub_rn(l, mu);
+            const double dd = __dmul_rn(d, d);
+            for (unsigned q = __ballot_sync(0xffffffffu, l == l); q; q &= q - 1)
+                s2 = __dadd_rn(s2, __shfl_sync(0xffffffffu, dd, __ffs(q) - 1));
+        }
+        if (lane == 0) s2_w[w] = s2;
+    }
+}
+__global__ void k_strag_sigma(uint64_t n_w, const double* s2_w, const uint32_t* m_w, double* sigma_w) {
+    for (uint64_t w = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; w < n_w; w += uint64_t(gridDim.x) * blockDim.x)
+        if (m_w[w] >= 2) sigma_w[w] = __dsqrt_rn(__ddiv_rn(s2_w[w], double(m_w[w])));
+}
+// local stream keys (group, kind) for the global stream union
+__global__ void k_stream_keys(const unsigned long long* counts, const uint32_t* st_pos, const uint64_t* key, int rbits,
+                              uint64_t* skey) {
+    const uint64_t n_st = counts[1];
+    for (uint64_t s = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; s < n_st; s += uint64_t(gridDim.x) * blockDim.x)
+        skey[s] = key[st_pos[s]] >> rbits;
 }
 
 __global__ void k_fill_f64(double* p, uint64_t n, double v) {
@@ -915,6 +1105,36 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* g) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(g) : "memory");
 }
 
+// Bulk (TMA) copies global -> shared with mbarrier completion, for the staged
+// form of k_sym_agg: one lane issues the copy of a whole batch's frames.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+// staged form: per-warp shared memory = frames of one batch (pcs, bins) + the
+// phase-0 values of two batches (ts[32], foff[32], next foff, previous ts) + mbarrier
+constexpr int kStageFrames = 512;
+constexpr int kStageNx = 66;
+constexpr int kStageWarpBytes = kStageFrames * 10 + 2 * kStageNx * 8 + 64;  // 6240, a multiple of 16
+constexpr int kStageSmem = (kThreads / 32) * kStageWarpBytes;
+
 // The fused hot kernel (stage a+b), one lane per sample.  A warp takes 32
 // consecutive samples — one contiguous block of frames in HBM — and owns a
 // contiguous range of such batches, so its rank only moves forward:
@@ -932,14 +1152,19 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* g) {
 //           open-addressing table with __match_any pre-aggregation;
 //  misses   the warp symbolizes the missing chains cooperatively and fills
 //           the cache.
-template <bool SMEM_TABS, int MINB, int UB, int UBC, bool COOP = true>
+//  STAGE    shallow windows (C1/C3 shapes, <= kStageFrames frames per batch):
+//           phase 1 reads from shared memory, where one lane's bulk (TMA) copy
+//           put the batch's whole frame range while the previous batch ran its
+//           lookups, so the frame stream leaves the per-batch chain of
+//           dependent round trips; phase-0 values come two batches ahead.
+template <bool SMEM_TABS, int MINB, int UB, int UBC, bool COOP = true, bool STAGE = false>
 __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
     __shared__ DevTable s_tabs[kMaxSmemBins];
     if (SMEM_TABS) {
         for (uint32_t i = threadIdx.x; i < p.n_bins; i += blockDim.x) s_tabs[i] = p.tabs[i];
         __syncthreads();
     }
-    __shared__ ulonglong4 s_acc[kThreads / 32][32];  // cooperative phase 1: (Σa, Σb, leaf pc, leaf bin) per sample
+    __shared__ ulonglong4 s_acc[COOP ? kThreads / 32 : 1][32];  // cooperative phase 1: (Σa, Σb, leaf pc, leaf bin) per sample
     const DevTable* tabs = SMEM_TABS ? s_tabs : p.tabs;
     const int lane = threadIdx.x & 31;
     const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
@@ -966,8 +1191,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
     // phase-0 stream values of the next batch, copied one batch ahead into
     // shared memory with asynchronous copies (in flight while the current batch
     // streams its frames and runs its lookups, and holding no registers)
-    __shared__ uint64_t s_nx[kThreads / 32][4][32];  // ts, frame offset, next frame offset, previous ts
-    uint64_t* nxw = &s_nx[threadIdx.x >> 5][0][0];
+    __shared__ uint64_t s_nx[STAGE ? 1 : kThreads / 32][4][32];  // ts, frame offset, next frame offset, previous ts
+    uint64_t* nxw = &s_nx[STAGE ? 0 : threadIdx.x >> 5][0][0];
     auto load0 = [&](uint64_t b) {
         const uint64_t i = b * 32 + lane;
         const uint64_t q = i < p.n_samples ? i : p.n_samples - 1;
@@ -977,22 +1202,90 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
         if (lane == 0 && q > 0) cp_async8(nxw + 96, p.ts + q - 1);
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    if (b_begin < b_end) load0(b_begin);
+    // staged form: per-warp region of the dynamic shared memory
+    extern __shared__ __align__(128) unsigned char s_dyn[];
+    unsigned char* sw = s_dyn + size_t(threadIdx.x >> 5) * kStageWarpBytes;
+    uint64_t* s_pc = reinterpret_cast<uint64_t*>(sw);
+    uint16_t* s_bin = reinterpret_cast<uint16_t*>(sw + kStageFrames * 8);
+    uint64_t* s_nx2 = reinterpret_cast<uint64_t*>(sw + kStageFrames * 10);  // [2][kStageNx]
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(sw + kStageFrames * 10 + 2 * kStageNx * 8);
+    auto load0s = [&](uint64_t b) {  // ts[32], foff[32], foff after the batch, ts before it
+        uint64_t* d = s_nx2 + (b & 1) * kStageNx;
+        const uint64_t i = b * 32 + lane;
+        const uint64_t q = i < p.n_samples ? i : p.n_samples - 1;
+        cp_async8(d + lane, p.ts + q);
+        cp_async8(d + 32 + lane, p.foff + q);
+        if (lane == 31 || i + 1 == p.n_samples) cp_async8(d + 64, p.foff + q + 1);
+        if (lane == 0 && q > 0) cp_async8(d + 65, p.ts + q - 1);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    // issue the bulk copy of batch b's aligned frame range [A, E); false when it
+    // does not fit (the batch then streams its frames from global memory)
+    uint64_t st_base = 0;
+    auto stage_issue = [&](uint64_t b) -> bool {
+        const uint64_t* d = s_nx2 + (b & 1) * kStageNx;
+        const uint64_t F0 = d[32], F1 = d[64];
+        const uint64_t A = F0 & ~7ull, E = (F1 + 7) & ~7ull;
+        if (!(F1 > F0 && E - A <= uint64_t(kStageFrames) && E <= (p.n_frames & ~7ull))) return false;
+        if (lane == 0) {
+            mbar_expect_tx(s_bar, unsigned(E - A) * 10u);
+            bulk_g2s(s_pc, p.pc + A, unsigned(E - A) * 8u, s_bar, pol);
+            bulk_g2s(s_bin, p.bin + A, unsigned(E - A) * 2u, s_bar, pol);
+        }
+        st_base = A;
+        return true;
+    };
+    unsigned st_phase = 0;
+    bool staged = false;
+    if (STAGE) {
+        if (lane == 0) mbar_init(s_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        __syncwarp();
+        if (b_begin < b_end) {
+            load0s(b_begin);
+            if (b_begin + 1 < b_end) {
+                load0s(b_begin + 1);
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+            } else {
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+            }
+            __syncwarp();
+            staged = stage_issue(b_begin);
+        }
+    } else if (b_begin < b_end) {
+        load0(b_begin);
+    }
     for (uint64_t bt = b_begin; bt < b_end; bt += b_step) {
         // ---------------- phase 0: lane s owns sample i; its stream values were
         // loaded during the previous batch, the next batch's are issued now
         const uint64_t i = bt * 32 + lane;
         const bool valid = i < p.n_samples;
         const uint64_t q = valid ? i : p.n_samples - 1;
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        __syncwarp();
-        const int64_t t = int64_t(nxw[lane]);
-        uint64_t f0 = nxw[32 + lane];
+        int64_t t, t_prev;
+        uint64_t f0, f1;
         const bool own_next = lane == 31 || i + 1 >= p.n_samples;
-        uint64_t f1 = own_next ? nxw[64 + lane] : 0;
-        const int64_t t_prev = lane == 0 && q > 0 ? int64_t(nxw[96]) : 0;
-        __syncwarp();
-        if (bt + b_step < b_end) load0(bt + b_step);
+        if (STAGE) {
+            // groups in flight: bt, bt + 1 (issued at bt - 1)
+            if (bt + 1 < b_end) asm volatile("cp.async.wait_group 1;" ::: "memory");
+            else asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncwarp();
+            const uint64_t* d = s_nx2 + (bt & 1) * kStageNx;
+            t = int64_t(d[lane]);
+            f0 = d[32 + lane];
+            f1 = own_next ? d[64] : 0;
+            t_prev = lane == 0 && q > 0 ? int64_t(d[65]) : 0;
+            __syncwarp();
+            if (bt + 2 < b_end) load0s(bt + 2);
+        } else {
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncwarp();
+            t = int64_t(nxw[lane]);
+            f0 = nxw[32 + lane];
+            f1 = own_next ? nxw[64 + lane] : 0;
+            t_prev = lane == 0 && q > 0 ? int64_t(nxw[96]) : 0;
+            __syncwarp();
+            if (bt + b_step < b_end) load0(bt + b_step);
+        }
         int r = r_cur;
         while (q >= __ldg(p.rank_soff + r + 1)) ++r;
         r_cur = __shfl_sync(0xffffffffu, r, 31);
@@ -1070,8 +1363,58 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
                 __syncwarp();
             }
         }
+        // ---------------- phase 1, staged form: this lane's frames from shared memory
+        bool from_smem = false;
+        if (STAGE && staged) {
+            mbar_wait(s_bar, st_phase);
+            st_phase ^= 1u;
+            from_smem = true;
+            if (inwin) {
+                const uint64_t a0 = f0 & ~7ull;
+                for (uint64_t bb = a0; bb < f1; bb += 8) {
+                    const uint64_t o = bb - st_base;
+                    const ulonglong2* sp2 = reinterpret_cast<const ulonglong2*>(s_pc + o);
+                    const ulonglong2 v0 = sp2[0], v1 = sp2[1], v2 = sp2[2], v3 = sp2[3];
+                    uint64_t pcs[8] = {v0.x, v0.y, v1.x, v1.y, v2.x, v2.y, v3.x, v3.y};
+                    uint4 bq = *reinterpret_cast<const uint4*>(s_bin + o);
+                    if (!(bb > f0 && bb + 8 <= f1)) {  // boundary block: take the leaf, zero the rest
+                        uint32_t bw[4] = {bq.x, bq.y, bq.z, bq.w};
+#pragma unroll
+                        for (int tt = 0; tt < 8; ++tt) {
+                            const uint64_t j = bb + tt;
+                            const uint32_t bv = (bw[tt >> 1] >> (16 * (tt & 1))) & 0xffffu;
+                            if (j == f0) {
+                                leaf_pc = pcs[tt];
+                                leaf_bin = bv;
+                            }
+                            if (!(j > f0 && j < f1)) {
+                                pcs[tt] = 0;
+                                bw[tt >> 1] &= ~(0xffffu << (16 * (tt & 1)));
+                            }
+                        }
+                        bq = make_uint4(bw[0], bw[1], bw[2], bw[3]);
+                    }
+                    raw_block(pcs, uint64_t(bq.x) | (uint64_t(bq.y) << 32), uint64_t(bq.z) | (uint64_t(bq.w) << 32),
+                              (bb - a0) >> 3, p.salt, ha, hb);
+                }
+            }
+        }
+        if (STAGE) {  // the buffer is free: stage the next batch under this batch's lookups
+            if (from_smem) {
+                __syncwarp();
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            }
+            staged = false;
+            if (bt + 1 < b_end) {
+                // groups in flight: bt + 1, bt + 2
+                if (bt + 2 < b_end) asm volatile("cp.async.wait_group 1;" ::: "memory");
+                else asm volatile("cp.async.wait_group 0;" ::: "memory");
+                __syncwarp();
+                staged = stage_issue(bt + 1);
+            }
+        }
         // ---------------- phase 1, per-lane form: this lane's frames, 8 per step
-        if (inwin && !coop) {
+        if (inwin && !coop && !from_smem) {
             const uint64_t a0 = f0 & ~7ull;
             for (uint64_t bs = a0; bs < f1; bs += 8 * UB) {
                 // UB blocks per step: all their loads are issued before any hashing

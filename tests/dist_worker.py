@@ -20,6 +20,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", required=True)
     ap.add_argument("--case", required=True)
+    ap.add_argument("--shard", type=int, default=0, help="stg_window.shard_streams (1 coll, 2 side)")
     a = ap.parse_args()
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -29,7 +30,7 @@ def main():
     ctx = stg.Context(local)
     ctx.dist_init(world, rank, share_unique_id(dist, stg.Context.dist_unique_id, device="cuda"))
     try:
-        ctx.window_run(shard_window(win, world, rank), cfg={"want_waterline": 1})
+        ctx.window_run(shard_window(win, world, rank, streams=a.shard), cfg={"want_waterline": 1})
         out = {"report": ctx.report(), "groupdata": ctx.groupdata(), "waterline": ctx.waterline()}
     except stg.StgError as e:  # every process must fail with the same error (no hang)
         out = {"error": str(e)}
