@@ -487,7 +487,7 @@ struct Runner {
         LAUNCH(k_rank_offsets, grid_for(sp + 1), kThreads, span, d_segrank_s, n_seg, d_rso);
         const long long dmin = get1(d_dmin);
         const int dbits = std::max(1, bits_for(uint64_t(-dmin)));
-        LAUNCH(k_coll_median_sel, unsigned(std::min<int64_t>(span, 148 * 16)), 256, int(span), d_rso, d_rsegs, seg_pos,
+        LAUNCH(k_coll_median_sel, unsigned(std::min<int64_t>(span, 148 * 4)), kMedThreads, int(span), d_rso, d_rsegs, seg_pos,
                dval, dflag, dmin, dbits, d_off, d_has_off, cnts + 2);
         // windowed complete instances ordered by max aligned exit
         unsigned long long* aexit = dev<unsigned long long>("c_aexit", I);
@@ -521,7 +521,14 @@ struct Runner {
             double* mu = dev<double>("s_mu", n_w);
             double* sg = dev<double>("s_sg", n_w);
             uint32_t* m = dev<uint32_t>("s_m", n_w);
-            LAUNCH(k_straggler_inst, grid_for(n_w * 32), kThreads, n_w, span, d_lat, cfg.k, mu, sg, m);
+            double* chain = dev<double>("s_chain", 2 * n_w);
+            double* s2 = dev<double>("s_s2", n_w);
+            zero(chain, 16 * n_w);
+            zero(s2, 8 * n_w);
+            strag_chain1(n_w, 0, span, chain);
+            LAUNCH(k_strag_mu, grid_for(n_w), kThreads, n_w, chain, mu, m);
+            strag_chain2(n_w, 0, span, mu, m, s2);
+            LAUNCH(k_strag_sigma, grid_for(n_w), kThreads, n_w, s2, m, sg);
             LAUNCH(k_straggler_rank, grid_for(sp * 32, kStragWarps * 32), kStragWarps * 32, n_w, 0, span, d_lat, cfg.k, mu,
                    sg, m, cb + o_pres, reinterpret_cast<double*>(cb + o_ma), reinterpret_cast<double*>(cb + o_ml),
                    reinterpret_cast<double*>(cb + o_zm), reinterpret_cast<uint64_t*>(cb + o_fl), cb + o_hz);
@@ -533,6 +540,19 @@ struct Runner {
             d2h += (n_w - 1) * 8;
         }
         coll_result_download();
+    }
+
+    // detect_straggler's per-instance sums (diagnosis.cpp:82-96) over the ranks
+    // [r0, r1) in rank order, continuing the chains they are given: a warp per
+    // instance for few instances, a thread per instance (coalesced rank rows)
+    // for many
+    void strag_chain1(uint64_t n_w, int r0, int r1, double* chain) {
+        if (n_w >= 4096) LAUNCH(k_strag_chain1_t, grid_for(n_w), kThreads, n_w, r0, r1, d_lat, chain);
+        else LAUNCH(k_strag_chain1, grid_for(n_w * 32), kThreads, n_w, r0, r1, d_lat, chain);
+    }
+    void strag_chain2(uint64_t n_w, int r0, int r1, const double* mu, const uint32_t* m, double* s2) {
+        if (n_w >= 4096) LAUNCH(k_strag_chain2_t, grid_for(n_w), kThreads, n_w, r0, r1, d_lat, mu, m, s2);
+        else LAUNCH(k_strag_chain2, grid_for(n_w * 32), kThreads, n_w, r0, r1, d_lat, mu, m, s2);
     }
 
     // ---------------------------------------------- rank-sharded stage d
@@ -763,7 +783,7 @@ struct Runner {
             LAUNCH(k_rank_offsets, grid_for(sp + 1), kThreads, span, d_segrank_s, n_seg, d_rso);
             const long long dmin = get1(d_dmin);
             const int dbits = std::max(1, bits_for(uint64_t(-dmin)));
-            LAUNCH(k_coll_median_sel, unsigned(std::min<int64_t>(span, 148 * 16)), 256, int(span), d_rso, d_rsegs,
+            LAUNCH(k_coll_median_sel, unsigned(std::min<int64_t>(span, 148 * 4)), kMedThreads, int(span), d_rso, d_rsegs,
                    cl.seg_pos, dval, dflag, dmin, dbits, d_off, d_has_off, cnts + 2);
         }
         // 6. windowed complete instances, ordered by the max aligned exit
@@ -809,13 +829,13 @@ struct Runner {
             uint32_t* m = dev<uint32_t>("s_m", n_w);
             if (P == 0) zero(chain, 16 * n_w);
             else nccl(ncclRecv(chain, 2 * n_w, ncclFloat64, P - 1, comm(), st));
-            LAUNCH(k_strag_chain1, grid_for(n_w * 32), kThreads, n_w, r_lo, r_hi, d_lat, chain);
+            strag_chain1(n_w, r_lo, r_hi, chain);
             if (P + 1 < W) nccl(ncclSend(chain, 2 * n_w, ncclFloat64, P + 1, comm(), st));
             nccl(ncclBroadcast(chain, chain, 2 * n_w, ncclFloat64, W - 1, comm(), st));
             LAUNCH(k_strag_mu, grid_for(n_w), kThreads, n_w, chain, mu, m);
             if (P == 0) zero(s2, 8 * n_w);
             else nccl(ncclRecv(s2, n_w, ncclFloat64, P - 1, comm(), st));
-            LAUNCH(k_strag_chain2, grid_for(n_w * 32), kThreads, n_w, r_lo, r_hi, d_lat, mu, m, s2);
+            strag_chain2(n_w, r_lo, r_hi, mu, m, s2);
             if (P + 1 < W) nccl(ncclSend(s2, n_w, ncclFloat64, P + 1, comm(), st));
             nccl(ncclBroadcast(s2, s2, n_w, ncclFloat64, W - 1, comm(), st));
             LAUNCH(k_strag_sigma, grid_for(n_w), kThreads, n_w, s2, m, sg);
@@ -1031,16 +1051,8 @@ struct Runner {
     // shared memory covers up to kMaxSmemBins binaries
     // 4 resident CTAs of 8 warps per SM (64 registers); the table staging in
     // shared memory covers up to kMaxSmemBins binaries
-    // Shallow windows (<= 14 frames per sample on average, the C1/C3 shapes)
-    // take the staged form: each batch's frames arrive in shared memory by one
-    // bulk copy issued during the previous batch's lookups.
     void launch_sym_agg(const AggParams& p, unsigned grid, bool smem_tabs) {
-        const bool stage = smem_tabs && p.n_frames <= 14 * p.n_samples;
-        if (stage) {
-            STG_CUDA(cudaFuncSetAttribute(k_sym_agg<true, 4, 1, 1, false, true>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kStageSmem));
-            k_sym_agg<true, 4, 1, 1, false, true><<<grid, kThreads, kStageSmem, st>>>(p);
-        } else if (smem_tabs) {
+        if (smem_tabs) {
             k_sym_agg<true, 4, 1, 1><<<grid, kThreads, 0, st>>>(p);
         } else {
             k_sym_agg<false, 4, 1, 1><<<grid, kThreads, 0, st>>>(p);
@@ -1101,6 +1113,7 @@ struct Runner {
             t.nb = h.nb;
             t.n = h.n;
             t.valid = 1;
+            t.line = h.d_line;
         }
         DevTable* d_tabs = up<DevTable>("tabs", tabs.data(), tabs.size());
         uint64_t* d_rsoff = up<uint64_t>("rsoff", w.rank_sample_off, R + 1);

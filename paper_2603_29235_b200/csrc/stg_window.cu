@@ -89,6 +89,32 @@ __global__ void k_build_buckets(const ulonglong2* e, uint32_t n, uint64_t base, 
     }
 }
 
+// Bucket lines (DevTable::line): the answer of every offset in bucket b is the
+// last entry whose start <= offset, i.e. a = bucket[b] (covers the bucket
+// start) or one of the entries starting strictly inside the bucket.  With none
+// or one such entry c, the line holds {a, c} (c = a when none) and a lookup is
+// one 32-byte read; with more it holds the search range.
+__global__ void k_build_lines(const ulonglong2* e, const uint32_t* bucket, uint64_t base, uint32_t shift, uint32_t nb,
+                              ulonglong4* line) {
+    for (uint64_t b = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; b < nb; b += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t a = bucket[b], nx = bucket[b + 1];
+        const uint64_t step = uint64_t(1) << shift;
+        const uint64_t key1 = base + (b + 1) * step;  // first offset of bucket b + 1
+        const bool wrap = key1 < base;                // past the top of the address space
+        uint32_t interior = nx - a;
+        if (nx > a && !wrap && e[nx].x == key1) --interior;
+        const ulonglong2 ea = e[a];
+        if (interior == 0) {
+            line[b] = make_ulonglong4(ea.x, ea.y, ea.x, ea.y);
+        } else if (interior == 1) {
+            const ulonglong2 ec = e[a + 1];
+            line[b] = make_ulonglong4(ea.x, ea.y, ec.x, ec.y);
+        } else {
+            line[b] = make_ulonglong4(uint64_t(a) | (uint64_t(nx) << 32), ~0ull, 0, 0);
+        }
+    }
+}
+
 // ========================================================= collectives
 // Group/kind ranges, so the stream key uses only the bits it needs.
 __global__ void k_coll_ranges(uint64_t n, const int32_t* group, const uint8_t* kind, int* gmin, int* gmax, int* kmax) {
@@ -397,81 +423,94 @@ __global__ void k_seg_rank(uint64_t n_seg, const uint32_t* seg_pos, const uint64
     for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < n_seg; j += uint64_t(gridDim.x) * blockDim.x)
         seg_rank[j] = uint32_t(key[seg_pos[j]] & rmask);
 }
-__global__ void __launch_bounds__(256) k_coll_median_sel(int rank_span, const uint32_t* rso, const uint32_t* rsegs,
-                                                        const uint32_t* seg_pos, const int64_t* dval,
-                                                        const uint32_t* dflag, long long dmin, int dbits,
-                                                        int64_t* off, uint8_t* has_off, unsigned long long* n_total) {
+constexpr int kMedThreads = 1024;
+__global__ void __launch_bounds__(kMedThreads) k_coll_median_sel(int rank_span, const uint32_t* rso, const uint32_t* rsegs,
+                                                                 const uint32_t* seg_pos, const int64_t* dval,
+                                                                 const uint32_t* dflag, long long dmin, int dbits,
+                                                                 int64_t* off, uint8_t* has_off,
+                                                                 unsigned long long* n_total) {
     __shared__ unsigned hist[2][256];
     __shared__ unsigned long long s_pref[2], s_k[2], s_cnt;
     const int lane = threadIdx.x & 31;
+    constexpr int U = 4;  // elements per thread per step: U loads in flight
     for (int r = blockIdx.x; r < rank_span; r += gridDim.x) {
         const uint32_t j0 = rso[r], j1 = rso[r + 1];
-        // pass 0: count the rank's flagged deltas
-        unsigned long long c = 0;
-        for (uint32_t j = j0; j < j1; ++j)
-            for (uint32_t q = seg_pos[rsegs[j]] + threadIdx.x; q < seg_pos[rsegs[j] + 1]; q += blockDim.x) c += dflag[q];
-        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-        if (threadIdx.x == 0) s_cnt = 0;
-        __syncthreads();
-        if (lane == 0 && c) atomicAdd(&s_cnt, c);
-        __syncthreads();
-        const unsigned long long cnt = s_cnt;
-        if (cnt == 0) {
-            if (threadIdx.x == 0) {
-                has_off[r] = 0;
-                off[r] = 0;
-            }
-            __syncthreads();
-            continue;
-        }
         if (threadIdx.x == 0) {
             s_pref[0] = s_pref[1] = 0;
-            s_k[0] = (cnt - 1) / 2;
-            s_k[1] = cnt / 2;
-            atomicAdd(n_total, cnt);
+            s_cnt = 0;
         }
+        bool first = true;
         for (int sh = ((dbits + 7) / 8 - 1) * 8; sh >= 0; sh -= 8) {
             for (int t = threadIdx.x; t < 512; t += blockDim.x) (&hist[0][0])[t] = 0;
             __syncthreads();
             const unsigned long long p0 = s_pref[0] >> sh >> 8, p1 = s_pref[1] >> sh >> 8;
+            unsigned long long c = 0;
             for (uint32_t j = j0; j < j1; ++j) {
                 const uint32_t a = seg_pos[rsegs[j]], b = seg_pos[rsegs[j] + 1];
-                for (uint32_t q0 = a; q0 < b; q0 += blockDim.x) {  // warp-uniform trip count
-                    const uint32_t q = q0 + threadIdx.x;
-                    unsigned d0 = 0xffffffffu, d1 = 0xffffffffu;
-                    if (q < b && dflag[q]) {
-                        const unsigned long long v = (unsigned long long)(dval[q] - dmin);
-                        const unsigned long long hi = v >> sh >> 8;
-                        const unsigned dg = unsigned(v >> sh) & 255u;
-                        if (hi == p0) d0 = dg;
-                        if (hi == p1) d1 = dg;
+                for (uint32_t q0 = a; q0 < b; q0 += U * kMedThreads) {  // warp-uniform trip count
+                    int64_t v[U];
+                    uint32_t fl[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const uint32_t q = q0 + u * kMedThreads + threadIdx.x;
+                        fl[u] = q < b ? dflag[q] : 0u;
+                        v[u] = q < b ? dval[q] : 0;
                     }
-                    const unsigned m0 = __match_any_sync(0xffffffffu, d0);
-                    if (d0 != 0xffffffffu && (__ffs(m0) - 1) == lane) atomicAdd(&hist[0][d0], __popc(m0));
-                    const unsigned m1 = __match_any_sync(0xffffffffu, d1);
-                    if (d1 != 0xffffffffu && (__ffs(m1) - 1) == lane) atomicAdd(&hist[1][d1], __popc(m1));
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        unsigned d0 = 0xffffffffu, d1 = 0xffffffffu;
+                        if (fl[u]) {
+                            ++c;
+                            const unsigned long long x = (unsigned long long)(v[u] - dmin);
+                            const unsigned long long hi = x >> sh >> 8;
+                            const unsigned dg = unsigned(x >> sh) & 255u;
+                            if (hi == p0) d0 = dg;
+                            if (hi == p1) d1 = dg;
+                        }
+                        const unsigned m0 = __match_any_sync(0xffffffffu, d0);
+                        if (d0 != 0xffffffffu && (__ffs(m0) - 1) == lane) atomicAdd(&hist[0][d0], __popc(m0));
+                        if (first) continue;  // both order statistics share the first digit's histogram
+                        const unsigned m1 = __match_any_sync(0xffffffffu, d1);
+                        if (d1 != 0xffffffffu && (__ffs(m1) - 1) == lane) atomicAdd(&hist[1][d1], __popc(m1));
+                    }
                 }
             }
+            if (first) {  // the count of the rank's complete-instance deltas comes with the first pass
+                for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+                if (lane == 0 && c) atomicAdd(&s_cnt, c);
+            }
             __syncthreads();
+            const unsigned long long cnt = s_cnt;
+            if (cnt == 0) break;
             if (threadIdx.x < 2) {
                 const int T = threadIdx.x;
+                if (first) s_k[T] = T == 0 ? (cnt - 1) / 2 : cnt / 2;
+                const unsigned* h = hist[first ? 0 : T];
                 unsigned long long k = s_k[T], cum = 0;
                 for (int bn = 0; bn < 256; ++bn) {
-                    const unsigned h = hist[T][bn];
-                    if (cum + h > k) {
+                    const unsigned hv = h[bn];
+                    if (cum + hv > k) {
                         s_pref[T] |= (unsigned long long)bn << sh;
                         s_k[T] = k - cum;
                         break;
                     }
-                    cum += h;
+                    cum += hv;
                 }
             }
+            first = false;
             __syncthreads();
         }
         if (threadIdx.x == 0) {
-            const int64_t lo = int64_t(s_pref[0]) + dmin, hi = int64_t(s_pref[1]) + dmin;
-            has_off[r] = 1;
-            off[r] = cnt % 2 ? hi : (lo + hi) / 2;
+            const unsigned long long cnt = s_cnt;
+            if (cnt == 0) {
+                has_off[r] = 0;
+                off[r] = 0;
+            } else {
+                const int64_t lo = int64_t(s_pref[0]) + dmin, hi = int64_t(s_pref[1]) + dmin;
+                has_off[r] = 1;
+                off[r] = cnt % 2 ? hi : (lo + hi) / 2;
+                atomicAdd(n_total, cnt);
+            }
         }
         __syncthreads();
     }
@@ -545,46 +584,6 @@ __global__ void k_coll_itertimes(uint64_t n_w, const uint64_t* wkey_sorted, doub
     }
 }
 
-// detect_straggler, per instance (diagnosis.cpp:82-96), in the reference's exact
-// floating-point order: Σ over ranks ascending, then /n; Σ (l-μ)² ascending.
-__global__ void k_straggler_inst(uint64_t n_w, int rank_span, const double* lat, double k,
-                                 double* mu_w, double* sigma_w, uint32_t* m_w) {
-    // one warp per instance: lanes load 32 ranks at a time, lane 0 adds them in
-    // rank order (the reference's sequence of roundings)
-    const int lane = threadIdx.x & 31;
-    for (uint64_t w = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; w < n_w;
-         w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
-        double acc = 0.0;
-        uint32_t m = 0;
-        for (int r0 = 0; r0 < rank_span; r0 += 32) {
-            const int r = r0 + lane;
-            const double l = r < rank_span ? lat[uint64_t(r) * n_w + w] : nan("");
-            const unsigned pres = __ballot_sync(0xffffffffu, l == l);
-            m += __popc(pres);
-            for (unsigned q = pres; q; q &= q - 1) {
-                const double v = __shfl_sync(0xffffffffu, l, __ffs(q) - 1);
-                acc = __dadd_rn(acc, v);
-            }
-        }
-        if (lane == 0) m_w[w] = m;
-        if (m < 2) continue;
-        const double mu = __ddiv_rn(acc, double(m));
-        double s2 = 0.0;
-        for (int r0 = 0; r0 < rank_span; r0 += 32) {
-            const int r = r0 + lane;
-            const double l = r < rank_span ? lat[uint64_t(r) * n_w + w] : nan("");
-            const double d = __dsub_rn(l, mu);
-            const double dd = __dmul_rn(d, d);
-            for (unsigned q = __ballot_sync(0xffffffffu, l == l); q; q &= q - 1)
-                s2 = __dadd_rn(s2, __shfl_sync(0xffffffffu, dd, __ffs(q) - 1));
-        }
-        if (lane == 0) {
-            mu_w[w] = mu;
-            sigma_w[w] = __dsqrt_rn(__ddiv_rn(s2, double(m)));
-        }
-    }
-}
-
 // Per rank: flags, mean lateness (alert: over >=2-rank instances; median
 // reference: over all), mean z over flagged — each summed in instance order
 // (diagnosis.cpp:97-110, bit-exact: the same sequence of double roundings).
@@ -594,8 +593,9 @@ __global__ void k_straggler_inst(uint64_t n_w, int rank_span, const double* lat,
 // run the three in-order add chains side by side over the chunk (lane 0: all
 // present, lane 1: present in >= 2-rank instances, lane 2: z of flagged), one
 // dependent add per element per chain and no shuffles.
-constexpr int kStragChunk = 256;
+constexpr int kStragChunk = 128;
 constexpr int kStragWarps = 8;
+constexpr int kStragPer = kStragChunk / 32;
 __global__ void __launch_bounds__(kStragWarps * 32) k_straggler_rank(
     uint64_t n_w, int r_lo, int r_hi, const double* lat, double k, const double* mu_w, const double* sigma_w,
     const uint32_t* m_w, uint8_t* present, double* mean_all, double* mean_alert, double* z_mean, uint64_t* flags,
@@ -609,39 +609,70 @@ __global__ void __launch_bounds__(kStragWarps * 32) k_straggler_rank(
         double acc = 0.0;  // lane 0: Σ all present, lane 1: Σ alert, lane 2: Σ z of flagged
         uint64_t n_all = 0, n2 = 0, nz = 0;
         const double* row = lat + uint64_t(r) * n_w;
-        for (uint64_t c0 = 0; c0 < n_w; c0 += kStragChunk) {
-            const uint32_t cn = uint32_t(n_w - c0 < kStragChunk ? n_w - c0 : kStragChunk);
-            for (uint32_t j = lane; j < kStragChunk; j += 32) {
-                const uint64_t w = c0 + j;
-                double l = nan(""), z = 0.0;
-                bool two = false, fl = false;
-                if (j < cn) {
-                    l = row[w];
-                    two = m_w[w] >= 2;
+        // chunk c's row values and instance statistics are loaded into registers
+        // before chunk c-1's add chains run, so the loads are in flight meanwhile
+        double l_n[kStragPer], mu_n[kStragPer], sg_n[kStragPer];
+        uint32_t m_n[kStragPer];
+        auto fetch = [&](uint64_t c0) {
+#pragma unroll
+            for (int u = 0; u < kStragPer; ++u) {
+                const uint64_t w = c0 + u * 32 + lane;
+                const bool in = w < n_w;
+                l_n[u] = in ? row[w] : nan("");
+                m_n[u] = in ? m_w[w] : 0u;
+                mu_n[u] = in ? mu_w[w] : 0.0;
+                sg_n[u] = in ? sigma_w[w] : 0.0;
+            }
+        };
+        uint32_t cn_prev = 0;
+        if (n_w) fetch(0);
+        for (uint64_t c0 = 0; c0 < n_w + kStragChunk; c0 += kStragChunk) {
+            const bool have = c0 < n_w;
+            const uint32_t cn = have ? uint32_t(n_w - c0 < kStragChunk ? n_w - c0 : kStragChunk) : 0;
+            double lv[kStragPer], zv[kStragPer];
+            uint8_t bits[kStragPer];
+            if (have) {  // decide presence / alert / flag and z of chunk c (registers)
+#pragma unroll
+                for (int u = 0; u < kStragPer; ++u) {
+                    const double l = l_n[u];
+                    const bool two = m_n[u] >= 2;
+                    bool fl = false;
+                    double z = 0.0;
                     if (l == l && two) {
-                        const double mu = mu_w[w], sg = sigma_w[w];
+                        const double mu = mu_n[u], sg = sg_n[u];
                         fl = sg > 0.0 && l > __dadd_rn(mu, __dmul_rn(k, sg));
                         if (fl) z = __ddiv_rn(__dsub_rn(l, mu), sg);
                     }
+                    const bool pres = l == l;
+                    n_all += __popc(__ballot_sync(0xffffffffu, pres));
+                    n2 += __popc(__ballot_sync(0xffffffffu, pres && two));
+                    nz += __popc(__ballot_sync(0xffffffffu, fl));
+                    lv[u] = l;
+                    zv[u] = z;
+                    bits[u] = uint8_t((pres ? 1 : 0) | (pres && two ? 2 : 0) | (fl ? 4 : 0));
                 }
-                const bool pres = l == l;
-                n_all += __popc(__ballot_sync(0xffffffffu, pres));
-                n2 += __popc(__ballot_sync(0xffffffffu, pres && two));
-                nz += __popc(__ballot_sync(0xffffffffu, fl));
-                s_val[wid][j] = l;
-                s_z[wid][j] = z;
-                s_bits[wid][j] = uint8_t((pres ? 1 : 0) | (pres && two ? 2 : 0) | (fl ? 4 : 0));
+                if (c0 + kStragChunk < n_w) fetch(c0 + kStragChunk);
             }
-            __syncwarp();
-            if (lane < 3) {
+            // chains of chunk c-1 (staged in shared memory by the previous step)
+            if (cn_prev && lane < 3) {
                 const double* src = lane == 2 ? s_z[wid] : s_val[wid];
 #pragma unroll 8
-                for (uint32_t j = 0; j < cn; ++j) {
+                for (uint32_t j = 0; j < cn_prev; ++j) {
                     const double v = src[j];
                     if ((s_bits[wid][j] >> lane) & 1) acc = __dadd_rn(acc, v);
                 }
             }
             __syncwarp();
+            if (have) {
+#pragma unroll
+                for (int u = 0; u < kStragPer; ++u) {
+                    s_val[wid][u * 32 + lane] = lv[u];
+                    s_z[wid][u * 32 + lane] = zv[u];
+                    s_bits[wid][u * 32 + lane] = (u * 32 + lane) < int(cn) ? bits[u] : 0;
+                }
+            }
+            __syncwarp();
+            cn_prev = cn;
         }
         const double s_all = __shfl_sync(0xffffffffu, acc, 0);
         const double s2 = __shfl_sync(0xffffffffu, acc, 1);
@@ -837,6 +868,66 @@ __global__ void k_strag_sigma(uint64_t n_w, const double* s2_w, const uint32_t* 
     for (uint64_t w = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; w < n_w; w += uint64_t(gridDim.x) * blockDim.x)
         if (m_w[w] >= 2) sigma_w[w] = __dsqrt_rn(__ddiv_rn(s2_w[w], double(m_w[w])));
 }
+// The same chains with one thread per instance, for many instances (C4:
+// 50k): the warp's 32 instances are adjacent in each rank row, so every step
+// of the rank loop is one coalesced 256 B read; the chain stays in the thread.
+constexpr int kChainU = 8;
+__global__ void k_strag_chain1_t(uint64_t n_w, int r0, int r1, const double* lat, double* chain) {
+    for (uint64_t w = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; w < n_w; w += uint64_t(gridDim.x) * blockDim.x) {
+        double acc = chain[2 * w];
+        uint32_t m = 0;
+        int r = r0;
+        for (; r + kChainU <= r1; r += kChainU) {
+            double v[kChainU];
+#pragma unroll
+            for (int u = 0; u < kChainU; ++u) v[u] = __ldcs(lat + uint64_t(r + u) * n_w + w);
+#pragma unroll
+            for (int u = 0; u < kChainU; ++u)
+                if (v[u] == v[u]) {
+                    acc = __dadd_rn(acc, v[u]);
+                    ++m;
+                }
+        }
+        for (; r < r1; ++r) {
+            const double l = lat[uint64_t(r) * n_w + w];
+            if (l == l) {
+                acc = __dadd_rn(acc, l);
+                ++m;
+            }
+        }
+        chain[2 * w] = acc;
+        chain[2 * w + 1] += double(m);
+    }
+}
+__global__ void k_strag_chain2_t(uint64_t n_w, int r0, int r1, const double* lat, const double* mu_w,
+                                 const uint32_t* m_w, double* s2_w) {
+    for (uint64_t w = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; w < n_w; w += uint64_t(gridDim.x) * blockDim.x) {
+        if (m_w[w] < 2) continue;
+        const double mu = mu_w[w];
+        double s2 = s2_w[w];
+        int r = r0;
+        for (; r + kChainU <= r1; r += kChainU) {
+            double v[kChainU];
+#pragma unroll
+            for (int u = 0; u < kChainU; ++u) v[u] = __ldcs(lat + uint64_t(r + u) * n_w + w);
+#pragma unroll
+            for (int u = 0; u < kChainU; ++u)
+                if (v[u] == v[u]) {
+                    const double d = __dsub_rn(v[u], mu);
+                    s2 = __dadd_rn(s2, __dmul_rn(d, d));
+                }
+        }
+        for (; r < r1; ++r) {
+            const double l = lat[uint64_t(r) * n_w + w];
+            if (l == l) {
+                const double d = __dsub_rn(l, mu);
+                s2 = __dadd_rn(s2, __dmul_rn(d, d));
+            }
+        }
+        s2_w[w] = s2;
+    }
+}
+
 // local stream keys (group, kind) for the global stream union
 __global__ void k_stream_keys(const unsigned long long* counts, const uint32_t* st_pos, const uint64_t* key, int rbits,
                               uint64_t* skey) {
@@ -1105,35 +1196,6 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* g) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(g) : "memory");
 }
 
-// Bulk (TMA) copies global -> shared with mbarrier completion, for the staged
-// form of k_sym_agg: one lane issues the copy of a whole batch's frames.
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned cnt) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(cnt) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
-    asm volatile(
-        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
-            smem_u32(bar)),
-        "r"(phase)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar, uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-        : "memory");
-}
-// staged form: per-warp shared memory = frames of one batch (pcs, bins) + the
-// phase-0 values of two batches (ts[32], foff[32], next foff, previous ts) + mbarrier
-constexpr int kStageFrames = 512;
-constexpr int kStageNx = 66;
-constexpr int kStageWarpBytes = kStageFrames * 10 + 2 * kStageNx * 8 + 64;  // 6240, a multiple of 16
-constexpr int kStageSmem = (kThreads / 32) * kStageWarpBytes;
 
 // The fused hot kernel (stage a+b), one lane per sample.  A warp takes 32
 // consecutive samples — one contiguous block of frames in HBM — and owns a
@@ -1152,19 +1214,14 @@ constexpr int kStageSmem = (kThreads / 32) * kStageWarpBytes;
 //           open-addressing table with __match_any pre-aggregation;
 //  misses   the warp symbolizes the missing chains cooperatively and fills
 //           the cache.
-//  STAGE    shallow windows (C1/C3 shapes, <= kStageFrames frames per batch):
-//           phase 1 reads from shared memory, where one lane's bulk (TMA) copy
-//           put the batch's whole frame range while the previous batch ran its
-//           lookups, so the frame stream leaves the per-batch chain of
-//           dependent round trips; phase-0 values come two batches ahead.
-template <bool SMEM_TABS, int MINB, int UB, int UBC, bool COOP = true, bool STAGE = false>
+template <bool SMEM_TABS, int MINB, int UB, int UBC, bool COOP = true>
 __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
     __shared__ DevTable s_tabs[kMaxSmemBins];
     if (SMEM_TABS) {
         for (uint32_t i = threadIdx.x; i < p.n_bins; i += blockDim.x) s_tabs[i] = p.tabs[i];
         __syncthreads();
     }
-    __shared__ ulonglong4 s_acc[COOP ? kThreads / 32 : 1][32];  // cooperative phase 1: (Σa, Σb, leaf pc, leaf bin) per sample
+    __shared__ ulonglong4 s_acc[kThreads / 32][32];  // cooperative phase 1: (Σa, Σb, leaf pc, leaf bin) per sample
     const DevTable* tabs = SMEM_TABS ? s_tabs : p.tabs;
     const int lane = threadIdx.x & 31;
     const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
@@ -1191,8 +1248,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
     // phase-0 stream values of the next batch, copied one batch ahead into
     // shared memory with asynchronous copies (in flight while the current batch
     // streams its frames and runs its lookups, and holding no registers)
-    __shared__ uint64_t s_nx[STAGE ? 1 : kThreads / 32][4][32];  // ts, frame offset, next frame offset, previous ts
-    uint64_t* nxw = &s_nx[STAGE ? 0 : threadIdx.x >> 5][0][0];
+    __shared__ uint64_t s_nx[kThreads / 32][4][32];  // ts, frame offset, next frame offset, previous ts
+    uint64_t* nxw = &s_nx[threadIdx.x >> 5][0][0];
     auto load0 = [&](uint64_t b) {
         const uint64_t i = b * 32 + lane;
         const uint64_t q = i < p.n_samples ? i : p.n_samples - 1;
@@ -1202,90 +1259,22 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
         if (lane == 0 && q > 0) cp_async8(nxw + 96, p.ts + q - 1);
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    // staged form: per-warp region of the dynamic shared memory
-    extern __shared__ __align__(128) unsigned char s_dyn[];
-    unsigned char* sw = s_dyn + size_t(threadIdx.x >> 5) * kStageWarpBytes;
-    uint64_t* s_pc = reinterpret_cast<uint64_t*>(sw);
-    uint16_t* s_bin = reinterpret_cast<uint16_t*>(sw + kStageFrames * 8);
-    uint64_t* s_nx2 = reinterpret_cast<uint64_t*>(sw + kStageFrames * 10);  // [2][kStageNx]
-    uint64_t* s_bar = reinterpret_cast<uint64_t*>(sw + kStageFrames * 10 + 2 * kStageNx * 8);
-    auto load0s = [&](uint64_t b) {  // ts[32], foff[32], foff after the batch, ts before it
-        uint64_t* d = s_nx2 + (b & 1) * kStageNx;
-        const uint64_t i = b * 32 + lane;
-        const uint64_t q = i < p.n_samples ? i : p.n_samples - 1;
-        cp_async8(d + lane, p.ts + q);
-        cp_async8(d + 32 + lane, p.foff + q);
-        if (lane == 31 || i + 1 == p.n_samples) cp_async8(d + 64, p.foff + q + 1);
-        if (lane == 0 && q > 0) cp_async8(d + 65, p.ts + q - 1);
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    // issue the bulk copy of batch b's aligned frame range [A, E); false when it
-    // does not fit (the batch then streams its frames from global memory)
-    uint64_t st_base = 0;
-    auto stage_issue = [&](uint64_t b) -> bool {
-        const uint64_t* d = s_nx2 + (b & 1) * kStageNx;
-        const uint64_t F0 = d[32], F1 = d[64];
-        const uint64_t A = F0 & ~7ull, E = (F1 + 7) & ~7ull;
-        if (!(F1 > F0 && E - A <= uint64_t(kStageFrames) && E <= (p.n_frames & ~7ull))) return false;
-        if (lane == 0) {
-            mbar_expect_tx(s_bar, unsigned(E - A) * 10u);
-            bulk_g2s(s_pc, p.pc + A, unsigned(E - A) * 8u, s_bar, pol);
-            bulk_g2s(s_bin, p.bin + A, unsigned(E - A) * 2u, s_bar, pol);
-        }
-        st_base = A;
-        return true;
-    };
-    unsigned st_phase = 0;
-    bool staged = false;
-    if (STAGE) {
-        if (lane == 0) mbar_init(s_bar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        __syncwarp();
-        if (b_begin < b_end) {
-            load0s(b_begin);
-            if (b_begin + 1 < b_end) {
-                load0s(b_begin + 1);
-                asm volatile("cp.async.wait_group 1;" ::: "memory");
-            } else {
-                asm volatile("cp.async.wait_group 0;" ::: "memory");
-            }
-            __syncwarp();
-            staged = stage_issue(b_begin);
-        }
-    } else if (b_begin < b_end) {
-        load0(b_begin);
-    }
+    if (b_begin < b_end) load0(b_begin);
     for (uint64_t bt = b_begin; bt < b_end; bt += b_step) {
         // ---------------- phase 0: lane s owns sample i; its stream values were
         // loaded during the previous batch, the next batch's are issued now
         const uint64_t i = bt * 32 + lane;
         const bool valid = i < p.n_samples;
         const uint64_t q = valid ? i : p.n_samples - 1;
-        int64_t t, t_prev;
-        uint64_t f0, f1;
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
+        const int64_t t = int64_t(nxw[lane]);
+        uint64_t f0 = nxw[32 + lane];
         const bool own_next = lane == 31 || i + 1 >= p.n_samples;
-        if (STAGE) {
-            // groups in flight: bt, bt + 1 (issued at bt - 1)
-            if (bt + 1 < b_end) asm volatile("cp.async.wait_group 1;" ::: "memory");
-            else asm volatile("cp.async.wait_group 0;" ::: "memory");
-            __syncwarp();
-            const uint64_t* d = s_nx2 + (bt & 1) * kStageNx;
-            t = int64_t(d[lane]);
-            f0 = d[32 + lane];
-            f1 = own_next ? d[64] : 0;
-            t_prev = lane == 0 && q > 0 ? int64_t(d[65]) : 0;
-            __syncwarp();
-            if (bt + 2 < b_end) load0s(bt + 2);
-        } else {
-            asm volatile("cp.async.wait_all;" ::: "memory");
-            __syncwarp();
-            t = int64_t(nxw[lane]);
-            f0 = nxw[32 + lane];
-            f1 = own_next ? nxw[64 + lane] : 0;
-            t_prev = lane == 0 && q > 0 ? int64_t(nxw[96]) : 0;
-            __syncwarp();
-            if (bt + b_step < b_end) load0(bt + b_step);
-        }
+        uint64_t f1 = own_next ? nxw[64 + lane] : 0;
+        const int64_t t_prev = lane == 0 && q > 0 ? int64_t(nxw[96]) : 0;
+        __syncwarp();
+        if (bt + b_step < b_end) load0(bt + b_step);
         int r = r_cur;
         while (q >= __ldg(p.rank_soff + r + 1)) ++r;
         r_cur = __shfl_sync(0xffffffffu, r, 31);
@@ -1363,58 +1352,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
                 __syncwarp();
             }
         }
-        // ---------------- phase 1, staged form: this lane's frames from shared memory
-        bool from_smem = false;
-        if (STAGE && staged) {
-            mbar_wait(s_bar, st_phase);
-            st_phase ^= 1u;
-            from_smem = true;
-            if (inwin) {
-                const uint64_t a0 = f0 & ~7ull;
-                for (uint64_t bb = a0; bb < f1; bb += 8) {
-                    const uint64_t o = bb - st_base;
-                    const ulonglong2* sp2 = reinterpret_cast<const ulonglong2*>(s_pc + o);
-                    const ulonglong2 v0 = sp2[0], v1 = sp2[1], v2 = sp2[2], v3 = sp2[3];
-                    uint64_t pcs[8] = {v0.x, v0.y, v1.x, v1.y, v2.x, v2.y, v3.x, v3.y};
-                    uint4 bq = *reinterpret_cast<const uint4*>(s_bin + o);
-                    if (!(bb > f0 && bb + 8 <= f1)) {  // boundary block: take the leaf, zero the rest
-                        uint32_t bw[4] = {bq.x, bq.y, bq.z, bq.w};
-#pragma unroll
-                        for (int tt = 0; tt < 8; ++tt) {
-                            const uint64_t j = bb + tt;
-                            const uint32_t bv = (bw[tt >> 1] >> (16 * (tt & 1))) & 0xffffu;
-                            if (j == f0) {
-                                leaf_pc = pcs[tt];
-                                leaf_bin = bv;
-                            }
-                            if (!(j > f0 && j < f1)) {
-                                pcs[tt] = 0;
-                                bw[tt >> 1] &= ~(0xffffu << (16 * (tt & 1)));
-                            }
-                        }
-                        bq = make_uint4(bw[0], bw[1], bw[2], bw[3]);
-                    }
-                    raw_block(pcs, uint64_t(bq.x) | (uint64_t(bq.y) << 32), uint64_t(bq.z) | (uint64_t(bq.w) << 32),
-                              (bb - a0) >> 3, p.salt, ha, hb);
-                }
-            }
-        }
-        if (STAGE) {  // the buffer is free: stage the next batch under this batch's lookups
-            if (from_smem) {
-                __syncwarp();
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            }
-            staged = false;
-            if (bt + 1 < b_end) {
-                // groups in flight: bt + 1, bt + 2
-                if (bt + 2 < b_end) asm volatile("cp.async.wait_group 1;" ::: "memory");
-                else asm volatile("cp.async.wait_group 0;" ::: "memory");
-                __syncwarp();
-                staged = stage_issue(bt + 1);
-            }
-        }
         // ---------------- phase 1, per-lane form: this lane's frames, 8 per step
-        if (inwin && !coop && !from_smem) {
+        if (inwin && !coop) {
             const uint64_t a0 = f0 & ~7ull;
             for (uint64_t bs = a0; bs < f1; bs += 8 * UB) {
                 // UB blocks per step: all their loads are issued before any hashing
@@ -1470,8 +1409,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
             pb = __ldcg(reinterpret_cast<const ulonglong2*>(p.pfx + pslot) + 1);
         }
         uint32_t leaf_key = kUnknownBit;
-        bool leaf_search = false;
+        bool leaf_search = false, leaf_line = false;
         uint32_t blo = 0, bhi = 0;
+        ulonglong4 Lk = make_ulonglong4(0, 0, 0, 0);
         const DevTable* T = nullptr;
         if (inwin) {
             if (leaf_bin < p.n_bins) {
@@ -1480,6 +1420,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
                     const uint64_t bk = (leaf_pc - T->base) >> T->shift;
                     if (bk >= T->nb) {
                         blo = bhi = T->n - 1;
+                    } else if (T->line) {  // the bucket line: usually the answer itself
+                        Lk = ld_line(T->line + bk);
+                        leaf_line = true;
                     } else {
                         blo = __ldg(T->bucket + bk);
                         bhi = __ldg(T->bucket + bk + 1);
@@ -1510,16 +1453,26 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
             }
         }
         if (leaf_search) {
-            // bisection down to <= 2 candidates (the bucket index usually leaves
-            // 1-2), then both candidates' entries in one round trip: the answer is
-            // the last whose start is <= pc (symfile.cpp:54-75)
-            while (bhi - blo > 1) {
-                const uint32_t mid = (blo + bhi + 1) >> 1;
-                if (__ldg(&T->e[mid].x) <= leaf_pc) blo = mid; else bhi = mid - 1;
+            // the bucket line holds the answer unless the bucket has several
+            // interior starts; then bisection down to <= 2 candidates, and both
+            // candidates' entries in one round trip: the answer is the last
+            // whose start is <= pc (symfile.cpp:54-75)
+            ulonglong2 e;
+            if (leaf_line && Lk.y != ~0ull) {
+                e = Lk.z <= leaf_pc ? make_ulonglong2(Lk.z, Lk.w) : make_ulonglong2(Lk.x, Lk.y);
+            } else {
+                if (leaf_line) {
+                    blo = uint32_t(Lk.x);
+                    bhi = uint32_t(Lk.x >> 32);
+                }
+                while (bhi - blo > 1) {
+                    const uint32_t mid = (blo + bhi + 1) >> 1;
+                    if (__ldg(&T->e[mid].x) <= leaf_pc) blo = mid; else bhi = mid - 1;
+                }
+                e = __ldg(T->e + blo);
+                const ulonglong2 e1 = blo < bhi ? __ldg(T->e + bhi) : e;
+                if (blo < bhi && e1.x <= leaf_pc) e = e1;
             }
-            ulonglong2 e = __ldg(T->e + blo);
-            const ulonglong2 e1 = blo < bhi ? __ldg(T->e + bhi) : e;
-            if (blo < bhi && e1.x <= leaf_pc) e = e1;
             if (p.mode == STG_LOOKUP_NEAREST_LOWER) {
                 leaf_key = uint32_t(e.y >> 32);
             } else {
@@ -2514,6 +2467,10 @@ __global__ void k_clk_of_cpu(int R, const int32_t* rank_ids, const int64_t* off,
 
 }  // namespace
 
+void launch_build_lines(const ulonglong2* e, const uint32_t* bucket, uint64_t base, uint32_t shift, uint32_t nb,
+                        ulonglong4* line, cudaStream_t s) {
+    if (nb) k_build_lines<<<grid_for(nb), kThreads, 0, s>>>(e, bucket, base, shift, nb, line);
+}
 void launch_build_buckets(const ulonglong2* e, uint32_t n, uint64_t base, uint32_t shift, uint32_t nb,
                           uint32_t* bucket, cudaStream_t s) {
     k_build_buckets<<<grid_for(uint64_t(nb) + 1), kThreads, 0, s>>>(e, n, base, shift, nb, bucket);
