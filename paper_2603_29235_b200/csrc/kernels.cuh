@@ -77,49 +77,27 @@ __device__ __forceinline__ uint32_t unk_get(const UnkSet& u, uint32_t bin, uint6
     return 0;
 }
 
-// 32-byte read-only load (one bucket line, LDG.E.ENL2.256)
-__device__ __forceinline__ ulonglong4 ld_line(const ulonglong4* p) {
-    ulonglong4 v;
-    asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(v.x), "=l"(v.y), "=l"(v.z), "=l"(v.w) : "l"(p));
-    return v;
-}
-
 // SymbolFile::lookup (symfile.cpp:54-75) on a staged table: greatest entry with
 // start <= pc, then the exact-range / nearest-lower check.  Returns the name
 // rank, or kUnknownBit when the frame does not resolve.
-
 __device__ __forceinline__ uint32_t table_lookup(const DevTable& t, uint64_t pc, int mode) {
     if (!t.valid || pc < t.base) return kUnknownBit;  // below first entry (lo == 0)
+    uint32_t i;
     uint64_t b = (pc - t.base) >> t.shift;
-    ulonglong2 e;
     if (b >= t.nb) {
-        e = __ldg(t.e + (t.n - 1));
+        i = t.n - 1;
     } else {
-        uint32_t lo, hi;
-        bool done = false;
-        if (t.line) {  // one read answers buckets with at most one interior start
-            const ulonglong4 L = ld_line(t.line + b);
-            if (L.y != ~0ull) {
-                e = L.z <= pc ? make_ulonglong2(L.z, L.w) : make_ulonglong2(L.x, L.y);
-                done = true;
-            }
-            lo = uint32_t(L.x);
-            hi = uint32_t(L.x >> 32);
-        } else {
-            lo = __ldg(t.bucket + b);
-            hi = __ldg(t.bucket + b + 1);
+        uint32_t lo = __ldg(t.bucket + b), hi = __ldg(t.bucket + b + 1);
+        while (lo < hi) {
+            uint32_t mid = (lo + hi + 1) >> 1;
+            if (__ldg(&t.e[mid].x) <= pc)
+                lo = mid;
+            else
+                hi = mid - 1;
         }
-        if (!done) {
-            while (lo < hi) {
-                uint32_t mid = (lo + hi + 1) >> 1;
-                if (__ldg(&t.e[mid].x) <= pc)
-                    lo = mid;
-                else
-                    hi = mid - 1;
-            }
-            e = __ldg(t.e + lo);
-        }
+        i = lo;
     }
+    ulonglong2 e = __ldg(t.e + i);
     if (mode == STG_LOOKUP_NEAREST_LOWER) return uint32_t(e.y >> 32);
     uint32_t size = uint32_t(e.y);
     bool in = size == 0 ? pc == e.x : pc < e.x + uint64_t(size);

@@ -35,11 +35,7 @@ struct Error : std::runtime_error {
 // e[i] = {start, size (low 32 bits) | name rank (high 32 bits)}, 16 bytes, so a
 // probe and the final entry fetch are single 16-byte loads.  bucket[b] is the
 // index of the last entry whose start <= base + (b << shift); the search for an
-// offset in bucket b is confined to [bucket[b], bucket[b+1]].  line[b] (32 B)
-// answers most lookups in one read: for a bucket with at most one entry
-// starting strictly inside it, {entry covering the bucket start, the interior
-// entry (or the same one again)}; otherwise {bucket[b] | bucket[b+1] << 32, ~0}
-// (the search range) — see k_build_lines.
+// offset in bucket b is confined to [bucket[b], bucket[b+1]].
 struct DevTable {
     const ulonglong2* e;
     const uint32_t* bucket;
@@ -49,7 +45,6 @@ struct DevTable {
     uint32_t nb;
     uint32_t n;
     uint32_t valid;
-    const ulonglong4* line;
 };
 
 constexpr uint32_t kUnknownBit = 0x80000000u;
@@ -98,7 +93,6 @@ struct HostTable {
     uint32_t* d_name_len = nullptr;
     ulonglong2* d_e = nullptr;        // {start, size | name_rank << 32}
     uint32_t* d_bucket = nullptr;
-    ulonglong4* d_line = nullptr;     // one-read bucket lines (rebuilt with the name ranks)
     uint32_t shift = 0, nb = 0;
     uint64_t dict_version = ~0ull;    // dictionary the ranks in d_e refer to
     HostTable() = default;
@@ -199,8 +193,6 @@ std::string hex_id(const uint8_t* id);
 std::string unknown_label(const uint8_t* id, uint64_t off);
 
 // device helpers implemented in stg_window.cu
-void launch_build_lines(const ulonglong2* e, const uint32_t* bucket, uint64_t base, uint32_t shift, uint32_t nb,
-                        ulonglong4* line, cudaStream_t s);
 void launch_build_buckets(const ulonglong2* e, uint32_t n, uint64_t base, uint32_t shift,
                           uint32_t nb, uint32_t* bucket, cudaStream_t s);
 

@@ -24,7 +24,7 @@ void run_resolve(Ctx& c, Result& res, uint64_t n, const uint64_t* pc, const uint
         if (it == c.table_by_id.end()) continue;
         HostTable& h = *c.tables[it->second];
         if (h.n == 0) continue;
-        t = DevTable{h.d_e, h.d_bucket, h.first_start, h.last_start, h.shift, h.nb, h.n, 1, h.d_line};
+        t = DevTable{h.d_e, h.d_bucket, h.first_start, h.last_start, h.shift, h.nb, h.n, 1};
     }
     DevTable* d_tabs = rn.up<DevTable>("rv_tabs", tabs.data(), tabs.size());
     const uint64_t* d_pc = rn.up<uint64_t>("rv_pc", pc, n);

@@ -1113,7 +1113,6 @@ struct Runner {
             t.nb = h.nb;
             t.n = h.n;
             t.valid = 1;
-            t.line = h.d_line;
         }
         DevTable* d_tabs = up<DevTable>("tabs", tabs.data(), tabs.size());
         uint64_t* d_rsoff = up<uint64_t>("rsoff", w.rank_sample_off, R + 1);

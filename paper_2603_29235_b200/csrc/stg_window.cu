@@ -89,32 +89,6 @@ __global__ void k_build_buckets(const ulonglong2* e, uint32_t n, uint64_t base, 
     }
 }
 
-// Bucket lines (DevTable::line): the answer of every offset in bucket b is the
-// last entry whose start <= offset, i.e. a = bucket[b] (covers the bucket
-// start) or one of the entries starting strictly inside the bucket.  With none
-// or one such entry c, the line holds {a, c} (c = a when none) and a lookup is
-// one 32-byte read; with more it holds the search range.
-__global__ void k_build_lines(const ulonglong2* e, const uint32_t* bucket, uint64_t base, uint32_t shift, uint32_t nb,
-                              ulonglong4* line) {
-    for (uint64_t b = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; b < nb; b += uint64_t(gridDim.x) * blockDim.x) {
-        const uint32_t a = bucket[b], nx = bucket[b + 1];
-        const uint64_t step = uint64_t(1) << shift;
-        const uint64_t key1 = base + (b + 1) * step;  // first offset of bucket b + 1
-        const bool wrap = key1 < base;                // past the top of the address space
-        uint32_t interior = nx - a;
-        if (nx > a && !wrap && e[nx].x == key1) --interior;
-        const ulonglong2 ea = e[a];
-        if (interior == 0) {
-            line[b] = make_ulonglong4(ea.x, ea.y, ea.x, ea.y);
-        } else if (interior == 1) {
-            const ulonglong2 ec = e[a + 1];
-            line[b] = make_ulonglong4(ea.x, ea.y, ec.x, ec.y);
-        } else {
-            line[b] = make_ulonglong4(uint64_t(a) | (uint64_t(nx) << 32), ~0ull, 0, 0);
-        }
-    }
-}
-
 // ========================================================= collectives
 // Group/kind ranges, so the stream key uses only the bits it needs.
 __global__ void k_coll_ranges(uint64_t n, const int32_t* group, const uint8_t* kind, int* gmin, int* gmax, int* kmax) {
@@ -1409,9 +1383,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
             pb = __ldcg(reinterpret_cast<const ulonglong2*>(p.pfx + pslot) + 1);
         }
         uint32_t leaf_key = kUnknownBit;
-        bool leaf_search = false, leaf_line = false;
+        bool leaf_search = false;
         uint32_t blo = 0, bhi = 0;
-        ulonglong4 Lk = make_ulonglong4(0, 0, 0, 0);
         const DevTable* T = nullptr;
         if (inwin) {
             if (leaf_bin < p.n_bins) {
@@ -1420,9 +1393,6 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
                     const uint64_t bk = (leaf_pc - T->base) >> T->shift;
                     if (bk >= T->nb) {
                         blo = bhi = T->n - 1;
-                    } else if (T->line) {  // the bucket line: usually the answer itself
-                        Lk = ld_line(T->line + bk);
-                        leaf_line = true;
                     } else {
                         blo = __ldg(T->bucket + bk);
                         bhi = __ldg(T->bucket + bk + 1);
@@ -1453,26 +1423,16 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
             }
         }
         if (leaf_search) {
-            // the bucket line holds the answer unless the bucket has several
-            // interior starts; then bisection down to <= 2 candidates, and both
-            // candidates' entries in one round trip: the answer is the last
-            // whose start is <= pc (symfile.cpp:54-75)
-            ulonglong2 e;
-            if (leaf_line && Lk.y != ~0ull) {
-                e = Lk.z <= leaf_pc ? make_ulonglong2(Lk.z, Lk.w) : make_ulonglong2(Lk.x, Lk.y);
-            } else {
-                if (leaf_line) {
-                    blo = uint32_t(Lk.x);
-                    bhi = uint32_t(Lk.x >> 32);
-                }
-                while (bhi - blo > 1) {
-                    const uint32_t mid = (blo + bhi + 1) >> 1;
-                    if (__ldg(&T->e[mid].x) <= leaf_pc) blo = mid; else bhi = mid - 1;
-                }
-                e = __ldg(T->e + blo);
-                const ulonglong2 e1 = blo < bhi ? __ldg(T->e + bhi) : e;
-                if (blo < bhi && e1.x <= leaf_pc) e = e1;
+            // bisection down to <= 2 candidates (the bucket index usually leaves
+            // 1-2), then both candidates' entries in one round trip: the answer is
+            // the last whose start is <= pc (symfile.cpp:54-75)
+            while (bhi - blo > 1) {
+                const uint32_t mid = (blo + bhi + 1) >> 1;
+                if (__ldg(&T->e[mid].x) <= leaf_pc) blo = mid; else bhi = mid - 1;
             }
+            ulonglong2 e = __ldg(T->e + blo);
+            const ulonglong2 e1 = blo < bhi ? __ldg(T->e + bhi) : e;
+            if (blo < bhi && e1.x <= leaf_pc) e = e1;
             if (p.mode == STG_LOOKUP_NEAREST_LOWER) {
                 leaf_key = uint32_t(e.y >> 32);
             } else {
@@ -2467,10 +2427,6 @@ __global__ void k_clk_of_cpu(int R, const int32_t* rank_ids, const int64_t* off,
 
 }  // namespace
 
-void launch_build_lines(const ulonglong2* e, const uint32_t* bucket, uint64_t base, uint32_t shift, uint32_t nb,
-                        ulonglong4* line, cudaStream_t s) {
-    if (nb) k_build_lines<<<grid_for(nb), kThreads, 0, s>>>(e, bucket, base, shift, nb, line);
-}
 void launch_build_buckets(const ulonglong2* e, uint32_t n, uint64_t base, uint32_t shift, uint32_t nb,
                           uint32_t* bucket, cudaStream_t s) {
     k_build_buckets<<<grid_for(uint64_t(nb) + 1), kThreads, 0, s>>>(e, n, base, shift, nb, bucket);

@@ -203,7 +203,6 @@ size_t Dict::lower_bound(std::string_view s) const {
 HostTable::~HostTable() {
     if (d_e) cudaFree(d_e);
     if (d_bucket) cudaFree(d_bucket);
-    if (d_line) cudaFree(d_line);
     if (d_payload) cudaFree(d_payload);
     if (d_name_off) cudaFree(d_name_off);
     if (d_name_len) cudaFree(d_name_len);
@@ -338,14 +337,6 @@ void symtab_refresh_dictionary(Ctx& c) {
         d.blob.resize(d.off[U]);
         if (d.off[U]) STG_CUDA(cudaMemcpyAsync(d.blob.data(), blob, d.off[U], cudaMemcpyDeviceToHost, st));
         STG_CUDA(cudaStreamSynchronize(st));
-    }
-    // bucket lines carry whole entries (name ranks included): rebuilt here
-    for (auto& tp : c.tables) {
-        HostTable& t = *tp;
-        if (t.n == 0 || !t.d_bucket) continue;
-        if (!t.d_line) STG_CUDA(cudaMalloc(&t.d_line, size_t(t.nb) * sizeof(ulonglong4)));
-        launch_build_lines(t.d_e, t.d_bucket, t.first_start, t.shift, t.nb, t.d_line, st);
-        STG_CUDA(cudaGetLastError());
     }
     c.dict_version++;
     for (auto& tp : c.tables) tp->dict_version = c.dict_version;
