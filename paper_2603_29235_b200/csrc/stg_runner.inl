@@ -197,6 +197,7 @@ struct Runner {
     const uint8_t* cd_kind = nullptr;
     const int64_t *cd_entry = nullptr, *cd_exit = nullptr;
     int coll_rg[3] = {0, 0, 0};  // min group, max group, max kind
+    bool coll_rank_sorted = false;  // event ranks non-decreasing in input order
     void rank_space() {
         int mx = -1, mn = 0;
         for (int32_t i = 0; i < w.n_ranks; ++i) {
@@ -209,8 +210,8 @@ struct Runner {
             mx = std::max(mx, w.group_ranks[i]);
             mn = std::min(mn, w.group_ranks[i]);
         }
-        int* d_mm = dev<int>("mm", 5);  // max rank, min rank, min group, max group, max kind
-        int init[5] = {mx, mn, INT_MAX, INT_MIN, 0};
+        int* d_mm = dev<int>("mm", 6);  // max rank, min rank, min group, max group, max kind, ranks unsorted
+        int init[6] = {mx, mn, INT_MAX, INT_MIN, 0, 0};
         STG_CUDA(cudaMemcpyAsync(d_mm, init, sizeof init, cudaMemcpyHostToDevice, st));
         auto scan = [&](const int32_t* host, uint64_t n, const char* nm) {
             if (!n) return;
@@ -229,6 +230,7 @@ struct Runner {
         if (nc) {
             LAUNCH(k_max_rank, grid_for(nc), kThreads, nc, cd_rank, d_mm, d_mm + 1);
             LAUNCH(k_coll_ranges, grid_for(nc), kThreads, nc, cd_group, cd_kind, d_mm + 2, d_mm + 3, d_mm + 4);
+            LAUNCH(k_rank_unsorted, grid_for(nc), kThreads, nc, cd_rank, d_mm + 5);
         }
         if (w.side_memory == STG_MEM_DEVICE) {
             if (w.n_gpu) LAUNCH(k_max_rank, grid_for(w.n_gpu), kThreads, w.n_gpu, w.gpu_rank, d_mm, d_mm + 1);
@@ -237,8 +239,9 @@ struct Runner {
             scan(w.gpu_rank, w.n_gpu, "gpu_rank");
             scan(w.os_rank, w.n_os, "os_rank");
         }
-        int out[5];
-        down(out, d_mm, 5);
+        int out[6];
+        down(out, d_mm, 6);
+        coll_rank_sorted = out[5] == 0;
         coll_rg[0] = out[2];
         coll_rg[1] = out[3];
         coll_rg[2] = out[4];
@@ -337,6 +340,29 @@ struct Runner {
         std::memcpy(&nd, h.data() + o_cnt + 16, 8);
         res.have_offsets = nd > 0;
     }
+    // column items (regular streams): (stream, chunk of <= kColChunk segments),
+    // K[s] events per rank, instance ids from ib[s]
+    ColItems col_items(const std::vector<uint32_t>& st_seg_h, const std::vector<uint32_t>& K,
+                       const std::vector<uint64_t>& ib) {
+        std::vector<uint64_t> off{0}, b;
+        std::vector<uint32_t> j0, j1;
+        for (size_t s = 0; s + 1 < st_seg_h.size(); ++s)
+            for (uint32_t j = st_seg_h[s]; j < st_seg_h[s + 1]; j += kColChunk) {
+                j0.push_back(j);
+                j1.push_back(std::min<uint32_t>(j + kColChunk, st_seg_h[s + 1]));
+                b.push_back(ib[s]);
+                off.push_back(off.back() + K[s]);
+            }
+        ColItems c{};
+        c.M = uint32_t(j0.size());
+        c.total = off.back();
+        if (!c.M) return c;
+        c.off = up<uint64_t>("cl_off", off.data(), off.size());
+        c.j0 = up<uint32_t>("cl_j0", j0.data(), j0.size());
+        c.j1 = up<uint32_t>("cl_j1", j1.data(), j1.size());
+        c.ib = up<uint64_t>("cl_ib", b.data(), b.size());
+        return c;
+    }
     void collectives() {
         const uint64_t sp = uint64_t(span);
         unsigned long long* errs = reinterpret_cast<unsigned long long*>(cb + o_err);
@@ -358,7 +384,7 @@ struct Runner {
         const uint64_t rmask = (1ull << rbits) - 1;
         LAUNCH(k_coll_keys, grid_for(n), kThreads, n, cd_rank, cd_group, cd_kind, coll_rg[0], kbits, rbits, 0, INT_MAX,
                key, idx, d_err);
-        sort_pairs(key, key_s, idx, idx_s, n, gbits + kbits + rbits);
+        sort_pairs(key, key_s, idx, idx_s, n, gbits + kbits + rbits, coll_rank_sorted ? rbits : 0);
         int64_t* s_entry = dev<int64_t>("c_sentry", n);
         int64_t* s_exit = dev<int64_t>("c_sexit", n);
         uint32_t* seg_flag = dev<uint32_t>("c_segflag", n);
@@ -418,12 +444,11 @@ struct Runner {
         if (k_base[n_st])
             LAUNCH(k_coll_regular, grid_for(k_base[n_st] * 32), kThreads, int(n_st), d_st_seg, seg_pos, coarse, s_entry,
                    s_exit, kmin, d_kbase, k_base[n_st], w.max_skew_ns, first_fail);
-        std::vector<uint32_t> k0(n_st);
+        std::vector<uint32_t> k0(n_st), st_seg_h(n_st + 1);
+        STG_CUDA(cudaMemcpyAsync(st_seg_h.data(), d_st_seg, (n_st + 1) * 4, cudaMemcpyDeviceToHost, st));
         down(k0.data(), first_fail, n_st);
         uint32_t* inst_local = dev<uint32_t>("c_instlocal", n);
         uint32_t* d_k0 = first_fail;  // = k0 on the device
-        LAUNCH(k_coll_assign_regular, unsigned(std::min<uint64_t>(n_seg, 65535)), 128, int(n_st), d_st_seg, seg_pos,
-               d_seg_stream, uint32_t(n_seg), d_k0, inst_local);
         std::vector<int> irregular;
         std::vector<uint32_t> n_inst(n_st);
         for (uint64_t s = 0; s < n_st; ++s) {
@@ -432,7 +457,10 @@ struct Runner {
             else
                 n_inst[s] = k0[s];
         }
-        if (!irregular.empty()) {
+        const bool col = irregular.empty();  // all regular: column form, no per-event ids
+        if (!col) {
+            LAUNCH(k_coll_assign_regular, unsigned(std::min<uint64_t>(n_seg, 65535)), 128, int(n_st), d_st_seg,
+                   seg_pos, d_seg_stream, uint32_t(n_seg), d_k0, inst_local);
             int* d_irr = up<int>("c_irr", irregular.data(), irregular.size());
             uint32_t* head = dev<uint32_t>("c_head", n_seg);
             uint32_t* d_ninst = dev<uint32_t>("c_ninst", n_st);
@@ -467,33 +495,53 @@ struct Runner {
         LAUNCH(k_fill_i64, grid_for(I), kThreads, (long long*)imax, I, LLONG_MIN);
         zero(isize, I * sizeof(unsigned));
         zero(iing, I * sizeof(unsigned));
-        LAUNCH(k_coll_inst, grid_for(n), kThreads, n, key_s, nullptr, stream_of_pos, d_ibase, inst_local, s_exit,
-               d_member, inst_of, imax, isize, iing, rmask);
+        uint32_t* d_segrank = dev<uint32_t>("c_segrank", n_seg);
+        LAUNCH(k_seg_rank, grid_for(n_seg), kThreads, n_seg, seg_pos, key_s, rmask, d_segrank);
+        ColItems ci{};
+        if (col) {
+            std::vector<uint64_t> ib(n_st);
+            for (uint64_t s = 0; s < n_st; ++s) ib[s] = base1[s + 1];
+            ci = col_items(st_seg_h, k0, ib);
+            if (ci.total)
+                LAUNCH(k_col_inst, grid_for(ci.total), kThreads, ci, seg_pos, d_segrank, s_exit, d_member, imax, iing);
+        } else {
+            LAUNCH(k_coll_inst, grid_for(n), kThreads, n, key_s, nullptr, stream_of_pos, d_ibase, inst_local, s_exit,
+                   d_member, inst_of, imax, isize, iing, rmask);
+        }
         // align_clocks: deltas of complete-instance events, per-rank radix select
         int64_t* dval = dev<int64_t>("c_dval", n);
-        uint32_t* dflag = dev<uint32_t>("c_dflag", n);
         long long* d_dmin = dev<long long>("c_dmin", 1);
         zero(d_dmin, 8);
-        LAUNCH(k_coll_deltas, grid_for(n), kThreads, n, inst_of, s_exit, imax, iing, n_group, dval, dflag, d_dmin);
+        if (col) {
+            if (ci.total)
+                LAUNCH(k_col_deltas, grid_for(ci.total), kThreads, ci, seg_pos, s_exit, imax, iing, n_group, dval,
+                       d_dmin);
+        } else {
+            LAUNCH(k_coll_deltas, grid_for(n), kThreads, n, inst_of, s_exit, imax, iing, n_group, dval, d_dmin);
+        }
         // per-rank segment lists on the device: segments sorted by their rank
-        uint32_t* d_segrank = dev<uint32_t>("c_segrank", n_seg);
         uint32_t* d_segrank_s = dev<uint32_t>("c_segrank_s", n_seg);
         uint32_t* d_segid = dev<uint32_t>("c_segid", n_seg);
         uint32_t* d_rsegs = dev<uint32_t>("c_rsegs", std::max<uint64_t>(n_seg, 1));
         uint32_t* d_rso = dev<uint32_t>("c_rso", sp + 1);
-        LAUNCH(k_seg_rank, grid_for(n_seg), kThreads, n_seg, seg_pos, key_s, rmask, d_segrank);
         LAUNCH(k_iota, grid_for(n_seg), kThreads, d_segid, n_seg);
         sort_pairs(d_segrank, d_segrank_s, d_segid, d_rsegs, n_seg, rbits);
         LAUNCH(k_rank_offsets, grid_for(sp + 1), kThreads, span, d_segrank_s, n_seg, d_rso);
         const long long dmin = get1(d_dmin);
         const int dbits = std::max(1, bits_for(uint64_t(-dmin)));
         LAUNCH(k_coll_median_sel, unsigned(std::min<int64_t>(span, 148 * 4)), kMedThreads, int(span), d_rso, d_rsegs, seg_pos,
-               dval, dflag, dmin, dbits, d_off, d_has_off, cnts + 2);
+               dval, dmin, dbits, d_off, d_has_off, cnts + 2);
         // windowed complete instances ordered by max aligned exit
         unsigned long long* aexit = dev<unsigned long long>("c_aexit", I);
         zero(aexit, I * 8);  // int64 0: build_group_data initialises max_exit to 0
-        LAUNCH(k_coll_aligned_exit, grid_for(n), kThreads, n, key_s, inst_of, s_exit, iing, n_group, d_off, aexit,
-               rmask);
+        if (col) {
+            if (ci.total)
+                LAUNCH(k_col_aligned_exit, grid_for(ci.total), kThreads, ci, seg_pos, d_segrank, s_exit, iing, n_group,
+                       d_off, aexit);
+        } else {
+            LAUNCH(k_coll_aligned_exit, grid_for(n), kThreads, n, key_s, inst_of, s_exit, iing, n_group, d_off, aexit,
+                   rmask);
+        }
         uint64_t* wkey = dev<uint64_t>("c_wkey", I);
         uint64_t* wkey_s = dev<uint64_t>("c_wkey_s", I);
         uint32_t* winst = dev<uint32_t>("c_winst", I);
@@ -509,11 +557,19 @@ struct Runner {
         LAUNCH(k_coll_winv, grid_for(n_w), kThreads, n_w, winst_s, inst_w);
         long long* wmin = dev<long long>("c_wmin", n_w);
         LAUNCH(k_fill_i64, grid_for(n_w), kThreads, wmin, n_w, LLONG_MAX);
-        LAUNCH(k_coll_minadj, grid_for(n), kThreads, n, key_s, inst_of, inst_w, s_entry, d_off, wmin, rmask);
         d_lat = dev<double>("lat", sp * n_w);
         LAUNCH(k_fill_f64, grid_for(sp * n_w), kThreads, d_lat, sp * n_w, nan(""));
-        LAUNCH(k_coll_lateness, grid_for(n), kThreads, n, key_s, inst_of, inst_w, s_entry, d_off, wmin, n_w, d_lat,
-               rmask);
+        if (col) {
+            if (ci.total) {
+                LAUNCH(k_col_minadj, grid_for(ci.total), kThreads, ci, seg_pos, d_segrank, s_entry, inst_w, d_off, wmin);
+                LAUNCH(k_col_lateness, grid_for(ci.total), kThreads, ci, seg_pos, d_segrank, s_entry, inst_w, d_off,
+                       wmin, n_w, d_lat);
+            }
+        } else {
+            LAUNCH(k_coll_minadj, grid_for(n), kThreads, n, key_s, inst_of, inst_w, s_entry, d_off, wmin, rmask);
+            LAUNCH(k_coll_lateness, grid_for(n), kThreads, n, key_s, inst_of, inst_w, s_entry, d_off, wmin, n_w, d_lat,
+                   rmask);
+        }
         double* it = dev<double>("c_it", std::max<uint64_t>(n_w, 1));
         if (n_w > 1) LAUNCH(k_coll_itertimes, grid_for(n_w), kThreads, n_w, wkey_s, it);
         // detect_straggler statistics
@@ -605,7 +661,7 @@ struct Runner {
         zero(d_err, sizeof(int));
         LAUNCH(k_coll_keys, grid_for(n), kThreads, n, cd_rank, cd_group, cd_kind, coll_rg[0], kbits, cl.rbits, rlo, rhi,
                key, idx, d_err);
-        sort_pairs(key, cl.key_s, idx, idx_s, n, gbits + kbits + cl.rbits);
+        sort_pairs(key, cl.key_s, idx, idx_s, n, gbits + kbits + cl.rbits, coll_rank_sorted ? cl.rbits : 0);
         cl.s_entry = dev<int64_t>("c_sentry", n);
         cl.s_exit = dev<int64_t>("c_sexit", n);
         uint32_t* seg_flag = dev<uint32_t>("c_segflag", n);
@@ -736,12 +792,14 @@ struct Runner {
             base1[s + 1] = ibase[lg[s]];
             k0l[s] = k0[lg[s]];
         }
-        const uint64_t* d_ibase = up<uint64_t>("c_ibase", base1.data(), n_st + 1);
-        uint32_t* d_k0 = up<uint32_t>("c_k0l", k0l.data(), n_st);
-        uint32_t* inst_local = dev<uint32_t>("c_instlocal", n);
-        if (n_seg)
-            LAUNCH(k_coll_assign_regular, unsigned(std::min<uint64_t>(n_seg, 65535)), 128, int(n_st), cl.st_seg,
-                   cl.seg_pos, cl.seg_stream, uint32_t(n_seg), d_k0, inst_local);
+        // column items over the local segments (every stream is regular here)
+        std::vector<uint32_t> st_seg_h(n_st + 1, 0);
+        if (n_st) down(st_seg_h.data(), cl.st_seg, n_st + 1);
+        std::vector<uint64_t> ib(n_st);
+        for (uint64_t s = 0; s < n_st; ++s) ib[s] = base1[s + 1];
+        const ColItems ci = col_items(st_seg_h, k0l, ib);
+        uint32_t* d_segrank = dev<uint32_t>("c_segrank", n_seg);
+        if (n_seg) LAUNCH(k_seg_rank, grid_for(n_seg), kThreads, n_seg, cl.seg_pos, cl.key_s, cl.rmask, d_segrank);
         std::vector<uint8_t> member(span, 0);
         unsigned n_group = 0;
         for (int32_t i = 0; i < w.n_group_ranks; ++i)
@@ -750,16 +808,13 @@ struct Runner {
                 ++n_group;
             }
         uint8_t* d_member = up<uint8_t>("c_member", member.data(), span);
-        uint32_t* inst_of = dev<uint32_t>("c_instof", n);
         unsigned long long* imax = dev<unsigned long long>("c_imax", I);
-        unsigned* isize = dev<unsigned>("c_isize", I);
         unsigned* iing = dev<unsigned>("c_iing", I);
         LAUNCH(k_fill_i64, grid_for(I), kThreads, (long long*)imax, I, LLONG_MIN);
-        zero(isize, I * sizeof(unsigned));
         zero(iing, I * sizeof(unsigned));
-        if (n)
-            LAUNCH(k_coll_inst, grid_for(n), kThreads, n, cl.key_s, nullptr, cl.stream_of_pos, d_ibase, inst_local,
-                   cl.s_exit, d_member, inst_of, imax, isize, iing, cl.rmask);
+        if (ci.total)
+            LAUNCH(k_col_inst, grid_for(ci.total), kThreads, ci, cl.seg_pos, d_segrank, cl.s_exit, d_member, imax,
+                   iing);
         nccl(ncclGroupStart());
         nccl(ncclAllReduce(imax, imax, I, ncclInt64, ncclMax, comm(), st));
         nccl(ncclAllReduce(iing, iing, I, ncclUint32, ncclSum, comm(), st));
@@ -767,31 +822,29 @@ struct Runner {
         // 5. align_clocks for this context's ranks (medians are per rank)
         if (n) {
             int64_t* dval = dev<int64_t>("c_dval", n);
-            uint32_t* dflag = dev<uint32_t>("c_dflag", n);
             long long* d_dmin = dev<long long>("c_dmin", 1);
             zero(d_dmin, 8);
-            LAUNCH(k_coll_deltas, grid_for(n), kThreads, n, inst_of, cl.s_exit, imax, iing, n_group, dval, dflag,
-                   d_dmin);
-            uint32_t* d_segrank = dev<uint32_t>("c_segrank", n_seg);
+            if (ci.total)
+                LAUNCH(k_col_deltas, grid_for(ci.total), kThreads, ci, cl.seg_pos, cl.s_exit, imax, iing, n_group,
+                       dval, d_dmin);
             uint32_t* d_segrank_s = dev<uint32_t>("c_segrank_s", n_seg);
             uint32_t* d_segid = dev<uint32_t>("c_segid", n_seg);
             uint32_t* d_rsegs = dev<uint32_t>("c_rsegs", std::max<uint64_t>(n_seg, 1));
             uint32_t* d_rso = dev<uint32_t>("c_rso", sp + 1);
-            LAUNCH(k_seg_rank, grid_for(n_seg), kThreads, n_seg, cl.seg_pos, cl.key_s, cl.rmask, d_segrank);
             LAUNCH(k_iota, grid_for(n_seg), kThreads, d_segid, n_seg);
             sort_pairs(d_segrank, d_segrank_s, d_segid, d_rsegs, n_seg, cl.rbits);
             LAUNCH(k_rank_offsets, grid_for(sp + 1), kThreads, span, d_segrank_s, n_seg, d_rso);
             const long long dmin = get1(d_dmin);
             const int dbits = std::max(1, bits_for(uint64_t(-dmin)));
             LAUNCH(k_coll_median_sel, unsigned(std::min<int64_t>(span, 148 * 4)), kMedThreads, int(span), d_rso, d_rsegs,
-                   cl.seg_pos, dval, dflag, dmin, dbits, d_off, d_has_off, cnts + 2);
+                   cl.seg_pos, dval, dmin, dbits, d_off, d_has_off, cnts + 2);
         }
         // 6. windowed complete instances, ordered by the max aligned exit
         unsigned long long* aexit = dev<unsigned long long>("c_aexit", I);
         zero(aexit, I * 8);
-        if (n)
-            LAUNCH(k_coll_aligned_exit, grid_for(n), kThreads, n, cl.key_s, inst_of, cl.s_exit, iing, n_group, d_off,
-                   aexit, cl.rmask);
+        if (ci.total)
+            LAUNCH(k_col_aligned_exit, grid_for(ci.total), kThreads, ci, cl.seg_pos, d_segrank, cl.s_exit, iing,
+                   n_group, d_off, aexit);
         nccl(ncclAllReduce(aexit, aexit, I, ncclInt64, ncclMax, comm(), st));
         uint64_t* wkey = dev<uint64_t>("c_wkey", I);
         uint64_t* wkey_s = dev<uint64_t>("c_wkey_s", I);
@@ -809,15 +862,15 @@ struct Runner {
         LAUNCH(k_coll_winv, grid_for(n_w), kThreads, n_w, winst_s, inst_w);
         long long* wmin = dev<long long>("c_wmin", n_w);
         LAUNCH(k_fill_i64, grid_for(n_w), kThreads, wmin, n_w, LLONG_MAX);
-        if (n)
-            LAUNCH(k_coll_minadj, grid_for(n), kThreads, n, cl.key_s, inst_of, inst_w, cl.s_entry, d_off, wmin,
-                   cl.rmask);
+        if (ci.total)
+            LAUNCH(k_col_minadj, grid_for(ci.total), kThreads, ci, cl.seg_pos, d_segrank, cl.s_entry, inst_w, d_off,
+                   wmin);
         nccl(ncclAllReduce(wmin, wmin, n_w, ncclInt64, ncclMin, comm(), st));
         d_lat = dev<double>("lat", sp * n_w);
         LAUNCH(k_fill_f64, grid_for(sp * n_w), kThreads, d_lat, sp * n_w, nan(""));
-        if (n)
-            LAUNCH(k_coll_lateness, grid_for(n), kThreads, n, cl.key_s, inst_of, inst_w, cl.s_entry, d_off, wmin, n_w,
-                   d_lat, cl.rmask);
+        if (ci.total)
+            LAUNCH(k_col_lateness, grid_for(ci.total), kThreads, ci, cl.seg_pos, d_segrank, cl.s_entry, inst_w, d_off,
+                   wmin, n_w, d_lat);
         double* it = dev<double>("c_it", std::max<uint64_t>(n_w, 1));
         if (n_w > 1) LAUNCH(k_coll_itertimes, grid_for(n_w), kThreads, n_w, wkey_s, it);
         // 7. detect_straggler: per-instance sums in rank order, context after context
@@ -887,6 +940,7 @@ struct Runner {
         cd_entry = static_cast<const int64_t*>(gather(cd_entry, 8, "cg_snd_e", "cg_pad_e", "cg_entry"));
         cd_exit = static_cast<const int64_t*>(gather(cd_exit, 8, "cg_snd_x", "cg_pad_x", "cg_exit"));
         n_coll_all = N;
+        coll_rank_sorted = false;  // the other shards were not checked here
     }
 
     // ------------------------------------------------------------ gpu/os

@@ -371,18 +371,19 @@ __global__ void k_coll_inst(uint64_t n, const uint64_t* key, const uint32_t* seg
 
 // align_clocks (collective.cpp:105-125) inputs: delta = exit - max exit for
 // events of complete instances (flag = 1), min delta for the key width.
+// dval = exit - max exit (<= 0) for events of complete instances, +1 for the
+// others (the median select skips positive values); min delta for the key width.
 __global__ void k_coll_deltas(uint64_t n, const uint32_t* inst_of, const int64_t* s_exit,
                               const unsigned long long* inst_max_exit, const unsigned* inst_ingroup, unsigned n_group,
-                              int64_t* dval, uint32_t* dflag, long long* dmin) {
+                              int64_t* dval, long long* dmin) {
     long long lo = 0;
     for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < n;
          p += uint64_t(gridDim.x) * blockDim.x) {
         const uint32_t g = inst_of[p];
         const bool ok = inst_ingroup[g] >= n_group;
-        const int64_t d = ok ? s_exit[p] - (long long)inst_max_exit[g] : 0;
+        const int64_t d = ok ? s_exit[p] - (long long)inst_max_exit[g] : 1;
         dval[p] = d;
-        dflag[p] = ok;
-        lo = min(lo, (long long)d);
+        if (ok) lo = min(lo, (long long)d);
     }
     for (int o = 16; o > 0; o >>= 1) lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
     if ((threadIdx.x & 31) == 0) atomicMin(dmin, lo);
@@ -398,15 +399,51 @@ __global__ void k_seg_rank(uint64_t n_seg, const uint32_t* seg_pos, const uint64
         seg_rank[j] = uint32_t(key[seg_pos[j]] & rmask);
 }
 constexpr int kMedThreads = 1024;
+constexpr int kMedBits = 11, kMedBins = 1 << kMedBits;  // 2 x 8 KB histograms, 2 bins per thread
+// block-wide exclusive scan of two counters per thread (1,024 threads)
+__device__ __forceinline__ void med_scan2(unsigned a, unsigned b, unsigned& ea, unsigned& eb, unsigned (*ws)[32]) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned ia = a, ib = b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned ta = __shfl_up_sync(0xffffffffu, ia, o), tb = __shfl_up_sync(0xffffffffu, ib, o);
+        if (lane >= o) {
+            ia += ta;
+            ib += tb;
+        }
+    }
+    if (lane == 31) {
+        ws[0][wid] = ia;
+        ws[1][wid] = ib;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        unsigned xa = ws[0][lane], xb = ws[1][lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned ta = __shfl_up_sync(0xffffffffu, xa, o), tb = __shfl_up_sync(0xffffffffu, xb, o);
+            if (lane >= o) {
+                xa += ta;
+                xb += tb;
+            }
+        }
+        ws[0][lane] = xa;
+        ws[1][lane] = xb;
+    }
+    __syncthreads();
+    ea = ia - a + (wid ? ws[0][wid - 1] : 0u);
+    eb = ib - b + (wid ? ws[1][wid - 1] : 0u);
+}
 __global__ void __launch_bounds__(kMedThreads) k_coll_median_sel(int rank_span, const uint32_t* rso, const uint32_t* rsegs,
                                                                  const uint32_t* seg_pos, const int64_t* dval,
-                                                                 const uint32_t* dflag, long long dmin, int dbits,
-                                                                 int64_t* off, uint8_t* has_off,
-                                                                 unsigned long long* n_total) {
-    __shared__ unsigned hist[2][256];
+                                                                 long long dmin, int dbits, int64_t* off,
+                                                                 uint8_t* has_off, unsigned long long* n_total) {
+    __shared__ unsigned hist[2][kMedBins];
+    __shared__ unsigned s_ws[2][32];
     __shared__ unsigned long long s_pref[2], s_k[2], s_cnt;
     const int lane = threadIdx.x & 31;
     constexpr int U = 4;  // elements per thread per step: U loads in flight
+    const int nd = (dbits + kMedBits - 1) / kMedBits;
     for (int r = blockIdx.x; r < rank_span; r += gridDim.x) {
         const uint32_t j0 = rso[r], j1 = rso[r + 1];
         if (threadIdx.x == 0) {
@@ -414,32 +451,29 @@ __global__ void __launch_bounds__(kMedThreads) k_coll_median_sel(int rank_span, 
             s_cnt = 0;
         }
         bool first = true;
-        for (int sh = ((dbits + 7) / 8 - 1) * 8; sh >= 0; sh -= 8) {
-            for (int t = threadIdx.x; t < 512; t += blockDim.x) (&hist[0][0])[t] = 0;
+        for (int sh = (nd - 1) * kMedBits; sh >= 0; sh -= kMedBits) {
+            for (int t = threadIdx.x; t < 2 * kMedBins; t += blockDim.x) (&hist[0][0])[t] = 0;
             __syncthreads();
-            const unsigned long long p0 = s_pref[0] >> sh >> 8, p1 = s_pref[1] >> sh >> 8;
+            const unsigned long long p0 = (s_pref[0] >> sh) >> kMedBits, p1 = (s_pref[1] >> sh) >> kMedBits;
             unsigned long long c = 0;
             for (uint32_t j = j0; j < j1; ++j) {
                 const uint32_t a = seg_pos[rsegs[j]], b = seg_pos[rsegs[j] + 1];
                 for (uint32_t q0 = a; q0 < b; q0 += U * kMedThreads) {  // warp-uniform trip count
                     int64_t v[U];
-                    uint32_t fl[U];
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         const uint32_t q = q0 + u * kMedThreads + threadIdx.x;
-                        fl[u] = q < b ? dflag[q] : 0u;
-                        v[u] = q < b ? dval[q] : 0;
+                        v[u] = q < b ? dval[q] : 1;
                     }
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         unsigned d0 = 0xffffffffu, d1 = 0xffffffffu;
-                        if (fl[u]) {
+                        if (v[u] <= 0) {  // a delta of a complete instance
                             ++c;
-                            const unsigned long long x = (unsigned long long)(v[u] - dmin);
-                            const unsigned long long hi = x >> sh >> 8;
-                            const unsigned dg = unsigned(x >> sh) & 255u;
-                            if (hi == p0) d0 = dg;
-                            if (hi == p1) d1 = dg;
+                            const unsigned long long x = (unsigned long long)(v[u] - dmin) >> sh;
+                            const unsigned dg = unsigned(x) & (kMedBins - 1);
+                            if ((x >> kMedBits) == p0) d0 = dg;
+                            if ((x >> kMedBits) == p1) d1 = dg;
                         }
                         const unsigned m0 = __match_any_sync(0xffffffffu, d0);
                         if (d0 != 0xffffffffu && (__ffs(m0) - 1) == lane) atomicAdd(&hist[0][d0], __popc(m0));
@@ -456,20 +490,22 @@ __global__ void __launch_bounds__(kMedThreads) k_coll_median_sel(int rank_span, 
             __syncthreads();
             const unsigned long long cnt = s_cnt;
             if (cnt == 0) break;
-            if (threadIdx.x < 2) {
-                const int T = threadIdx.x;
-                if (first) s_k[T] = T == 0 ? (cnt - 1) / 2 : cnt / 2;
-                const unsigned* h = hist[first ? 0 : T];
-                unsigned long long k = s_k[T], cum = 0;
-                for (int bn = 0; bn < 256; ++bn) {
-                    const unsigned hv = h[bn];
-                    if (cum + hv > k) {
-                        s_pref[T] |= (unsigned long long)bn << sh;
-                        s_k[T] = k - cum;
-                        break;
-                    }
-                    cum += hv;
-                }
+            // digit of each order statistic: a block scan over the bins (two per thread)
+            const unsigned long long k0 = first ? (cnt - 1) / 2 : s_k[0], k1 = first ? cnt / 2 : s_k[1];
+            const unsigned* h1 = hist[first ? 0 : 1];
+            const unsigned a0 = hist[0][2 * threadIdx.x], b0 = hist[0][2 * threadIdx.x + 1];
+            const unsigned a1 = h1[2 * threadIdx.x], b1 = h1[2 * threadIdx.x + 1];
+            unsigned e0, e1;
+            med_scan2(a0 + b0, a1 + b1, e0, e1, s_ws);
+            if (k0 >= e0 && k0 < e0 + a0 + b0) {
+                const bool lo = k0 < e0 + a0;
+                s_pref[0] |= (unsigned long long)(2 * threadIdx.x + (lo ? 0 : 1)) << sh;
+                s_k[0] = k0 - e0 - (lo ? 0 : a0);
+            }
+            if (k1 >= e1 && k1 < e1 + a1 + b1) {
+                const bool lo = k1 < e1 + a1;
+                s_pref[1] |= (unsigned long long)(2 * threadIdx.x + (lo ? 0 : 1)) << sh;
+                s_k[1] = k1 - e1 - (lo ? 0 : a1);
             }
             first = false;
             __syncthreads();
@@ -658,6 +694,115 @@ __global__ void __launch_bounds__(kStragWarps * 32) k_straggler_rank(
             z_mean[r] = nz ? __ddiv_rn(sz, double(nz)) : 0.0;
             flags[r] = nz;
             has_z[r] = nz > 0;
+        }
+    }
+}
+
+// ------------------------------------------- regular streams, column form
+// When every stream is regular (instance k of a stream = the k-th event of each
+// of its ranks), the per-instance reductions are column reductions over the
+// stream's [rank][k] event matrix: one thread per (k, chunk of up to kColChunk
+// rank segments) reads its column with coalesced loads (consecutive k are
+// adjacent in every segment), reduces in registers and issues one atomic per
+// chunk; ranks and instances are implicit (no per-event key or instance id).
+constexpr uint32_t kColChunk = 64;
+struct ColItems {
+    const uint64_t* off;   // [M+1] prefix of the items' k counts
+    const uint32_t* j0;    // [M] first segment of the chunk
+    const uint32_t* j1;    // [M] end segment
+    const uint64_t* ib;    // [M] instance id of k = 0
+    uint32_t M;
+    uint64_t total;
+};
+__device__ __forceinline__ bool col_item(const ColItems& c, uint64_t t, uint32_t& m, uint32_t& k) {
+    if (t >= c.total) return false;
+    uint32_t lo = 0, hi = c.M - 1;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (c.off[mid] <= t) lo = mid; else hi = mid - 1;
+    }
+    m = lo;
+    k = uint32_t(t - c.off[lo]);
+    return true;
+}
+__global__ void k_col_inst(ColItems c, const uint32_t* seg_pos, const uint32_t* seg_rank, const int64_t* s_exit,
+                           const uint8_t* member, unsigned long long* imax, unsigned* iing) {
+    for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < c.total; t += uint64_t(gridDim.x) * blockDim.x) {
+        uint32_t m, k;
+        col_item(c, t, m, k);
+        long long mx = LLONG_MIN;
+        unsigned ing = 0;
+#pragma unroll 4
+        for (uint32_t j = c.j0[m]; j < c.j1[m]; ++j) {
+            mx = max(mx, (long long)s_exit[seg_pos[j] + k]);
+            ing += member[seg_rank[j]];
+        }
+        const uint64_t g = c.ib[m] + k;
+        atomicMax((long long*)&imax[g], mx);
+        if (ing) atomicAdd(&iing[g], ing);
+    }
+}
+__global__ void k_col_deltas(ColItems c, const uint32_t* seg_pos, const int64_t* s_exit,
+                             const unsigned long long* imax, const unsigned* iing, unsigned n_group, int64_t* dval,
+                             long long* dmin) {
+    long long lo = 0;
+    for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < c.total; t += uint64_t(gridDim.x) * blockDim.x) {
+        uint32_t m, k;
+        col_item(c, t, m, k);
+        const uint64_t g = c.ib[m] + k;
+        const bool ok = iing[g] >= n_group;
+        const long long mx = (long long)imax[g];
+#pragma unroll 4
+        for (uint32_t j = c.j0[m]; j < c.j1[m]; ++j) {
+            const uint64_t p = seg_pos[j] + k;
+            const int64_t d = ok ? s_exit[p] - mx : 1;
+            dval[p] = d;
+            if (ok) lo = min(lo, (long long)d);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    if ((threadIdx.x & 31) == 0) atomicMin(dmin, lo);
+}
+__global__ void k_col_aligned_exit(ColItems c, const uint32_t* seg_pos, const uint32_t* seg_rank, const int64_t* s_exit,
+                                   const unsigned* iing, unsigned n_group, const int64_t* off,
+                                   unsigned long long* aexit) {
+    for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < c.total; t += uint64_t(gridDim.x) * blockDim.x) {
+        uint32_t m, k;
+        col_item(c, t, m, k);
+        const uint64_t g = c.ib[m] + k;
+        if (iing[g] < n_group) continue;
+        long long mx = LLONG_MIN;
+#pragma unroll 4
+        for (uint32_t j = c.j0[m]; j < c.j1[m]; ++j) mx = max(mx, (long long)(s_exit[seg_pos[j] + k] - off[seg_rank[j]]));
+        atomicMax((long long*)&aexit[g], mx);
+    }
+}
+__global__ void k_col_minadj(ColItems c, const uint32_t* seg_pos, const uint32_t* seg_rank, const int64_t* s_entry,
+                             const uint32_t* inst_w, const int64_t* off, long long* wmin) {
+    for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < c.total; t += uint64_t(gridDim.x) * blockDim.x) {
+        uint32_t m, k;
+        col_item(c, t, m, k);
+        const uint32_t w = inst_w[c.ib[m] + k];
+        if (w == 0xffffffffu) continue;
+        long long mn = LLONG_MAX;
+#pragma unroll 4
+        for (uint32_t j = c.j0[m]; j < c.j1[m]; ++j) mn = min(mn, (long long)(s_entry[seg_pos[j] + k] - off[seg_rank[j]]));
+        atomicMin(&wmin[w], mn);
+    }
+}
+__global__ void k_col_lateness(ColItems c, const uint32_t* seg_pos, const uint32_t* seg_rank, const int64_t* s_entry,
+                               const uint32_t* inst_w, const int64_t* off, const long long* wmin, uint64_t n_w,
+                               double* lat) {
+    for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < c.total; t += uint64_t(gridDim.x) * blockDim.x) {
+        uint32_t m, k;
+        col_item(c, t, m, k);
+        const uint32_t w = inst_w[c.ib[m] + k];
+        if (w == 0xffffffffu) continue;
+        const long long base = wmin[w];
+#pragma unroll 4
+        for (uint32_t j = c.j0[m]; j < c.j1[m]; ++j) {
+            const uint32_t r = seg_rank[j];
+            lat[uint64_t(r) * n_w + w] = __ddiv_rn(__ll2double_rn(s_entry[seg_pos[j] + k] - off[r] - base), 1e6);
         }
     }
 }
@@ -930,6 +1075,14 @@ __global__ void k_max_rank(uint64_t n, const int32_t* r, int* mx, int* mn) {
     }
     atomicMax(mx, a);
     atomicMin(mn, b);
+}
+
+// flag = 1 unless the events' ranks are non-decreasing in input order (the
+// common rank-major layout): then a stable sort on the stream bits alone
+// already yields (stream, rank, input order)
+__global__ void k_rank_unsorted(uint64_t n, const int32_t* r, int* flag) {
+    for (uint64_t i = 1 + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        if (r[i] < r[i - 1]) *flag = 1;
 }
 
 // ================================================================ gpu / os
