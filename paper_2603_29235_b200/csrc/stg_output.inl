@@ -455,7 +455,7 @@ static std::string waterline_json_dist(Ctx& c) {
         if (!first) j.raw(", ");
         first = false;
         j.raw("[");
-        j.str(r.gname(uint32_t(g)));
+        j.str(r.gname(r.wl_ukeys[g]));
         j.raw(", ");
         j.num(hm[g]);
         j.raw(", ");

@@ -945,160 +945,132 @@ struct Runner {
 
     // ------------------------------------------------------------ gpu/os
     // Per-rank GPU kernel time and OS counter sums (build_group_data
-    // bundle.cpp:302-320) in device buffers, validated; the host maps are read
-    // back by gpu_os_collect().  With sharded side streams every context holds
-    // the same buffers (its own ranks' rows filled) and gpu_os_reduce() sums
-    // them over the group first.
+    // bundle.cpp:302-320) in one device block — 8-byte sums / maxima and error
+    // flags, then 1-byte presence flags — read back with one download.  With
+    // sharded side streams every context fills its own ranks' rows and the
+    // block is summed over the group (gpu_os_reduce) before it is read.
+    struct SideBlock {
+        uint64_t K = 0, C = 1, n8 = 0, n1 = 0;
+        size_t o_gs = 0, o_irq = 0, o_sirq = 0, o_p50 = 0, o_p99 = 0, o_mig = 0, o_err = 0;  // in 8-byte words
+        size_t o_gp = 0, o_irqp = 0, o_sirqp = 0, o_op = 0;                                 // in bytes after them
+        uint8_t* d = nullptr;
+        bool gpu = false, os = false;
+    } sb;
     void gpu_os() {
         res.gpu.clear();
         res.os.clear();
         const bool shard = side_sharded();
         const bool sdev = w.side_memory == STG_MEM_DEVICE;
-        if (w.n_gpu || (shard && w.n_kernel_names)) {
-            const uint64_t n = w.n_gpu, K = w.n_kernel_names;
-            unsigned long long* sums = dev<unsigned long long>("gpu_sums", span * K);
-            uint8_t* pres = dev<uint8_t>("gpu_pres", span * K);
-            zero(sums, span * K * 8);
-            zero(pres, span * K);
-            if (n) {
-                const int32_t* d_rank = sdev ? w.gpu_rank : static_cast<const int32_t*>(c.buf("gpu_rank").p);
-                const uint32_t* d_k = sdev ? w.gpu_kernel : up<uint32_t>("gpu_k", w.gpu_kernel, n);
-                const int64_t* d_s = sdev ? w.gpu_start : up<int64_t>("gpu_s", w.gpu_start, n);
-                const int64_t* d_d = sdev ? w.gpu_dur : up<int64_t>("gpu_d", w.gpu_dur, n);
-                int* err = dev<int>("gpu_err", 1);
-                zero(err, 4);
-                LAUNCH(k_gpu_sums, grid_for(n), kThreads, n, d_rank, d_k, d_s, d_d, d_off, w.window_start_ns,
-                       uint32_t(K), sums, pres, err);
-                if (get1(err)) fail(STG_EINVAL, "gpu event kernel index out of range");
-            }
-            gpu_bufs = true;
+        const uint64_t sp = uint64_t(span);
+        sb = SideBlock{};
+        sb.K = w.n_kernel_names;
+        sb.C = std::max<uint32_t>(w.n_counter_names, 1);
+        sb.gpu = w.n_gpu || (shard && sb.K);
+        sb.os = w.n_os || shard;
+        if (!sb.gpu && !sb.os) return;
+        size_t q = 0;
+        sb.o_gs = q, q += sp * sb.K;
+        sb.o_irq = q, q += sp * sb.C;
+        sb.o_sirq = q, q += sp * sb.C;
+        sb.o_p50 = q, q += sp;
+        sb.o_p99 = q, q += sp;
+        sb.o_mig = q, q += sp;
+        sb.o_err = q, q += 2;
+        sb.n8 = q;
+        size_t b = 0;
+        sb.o_gp = b, b += sp * sb.K;
+        sb.o_irqp = b, b += sp * sb.C;
+        sb.o_sirqp = b, b += sp * sb.C;
+        sb.o_op = b, b += sp;
+        sb.n1 = b;
+        sb.d = dev<uint8_t>("side_block", sb.n8 * 8 + sb.n1);
+        zero(sb.d, sb.n8 * 8 + sb.n1);
+        auto w8 = [&](size_t o) { return reinterpret_cast<unsigned long long*>(sb.d) + o; };
+        uint8_t* d1 = sb.d + sb.n8 * 8;
+        if (w.n_gpu) {
+            const uint64_t n = w.n_gpu;
+            const int32_t* d_rank = sdev ? w.gpu_rank : static_cast<const int32_t*>(c.buf("gpu_rank").p);
+            const uint32_t* d_k = sdev ? w.gpu_kernel : up<uint32_t>("gpu_k", w.gpu_kernel, n);
+            const int64_t* d_s = sdev ? w.gpu_start : up<int64_t>("gpu_s", w.gpu_start, n);
+            const int64_t* d_d = sdev ? w.gpu_dur : up<int64_t>("gpu_d", w.gpu_dur, n);
+            LAUNCH(k_gpu_sums, grid_for(n), kThreads, n, d_rank, d_k, d_s, d_d, d_off, w.window_start_ns,
+                   uint32_t(sb.K), w8(sb.o_gs), d1 + sb.o_gp, reinterpret_cast<int*>(w8(sb.o_err)));
         }
-        if (w.n_os || shard) {
-            const uint64_t n = w.n_os, C = std::max<uint32_t>(w.n_counter_names, 1);
-            auto irq = dev<unsigned long long>("os_irq", span * C);
-            auto irqp = dev<uint8_t>("os_irqp", span * C);
-            auto sirq = dev<unsigned long long>("os_sirq", span * C);
-            auto sirqp = dev<uint8_t>("os_sirqp", span * C);
-            auto mp50 = dev<long long>("os_mp50", span);
-            auto mp99 = dev<long long>("os_mp99", span);
-            auto migs = dev<unsigned long long>("os_migs", span);
-            auto pres = dev<uint8_t>("os_pres", span);
-            zero(irq, span * C * 8);
-            zero(irqp, span * C);
-            zero(sirq, span * C * 8);
-            zero(sirqp, span * C);
-            zero(mp50, span * 8);
-            zero(mp99, span * 8);
-            zero(migs, span * 8);
-            zero(pres, span);
-            if (n) {
-                const int32_t* d_rank = sdev ? w.os_rank : static_cast<const int32_t*>(c.buf("os_rank").p);
-                const int64_t *ws, *p50, *p99, *mig, *ival, *sval;
-                const uint64_t *ioff, *soff;
-                const uint32_t *ikey, *skey;
-                if (sdev) {
-                    ws = w.os_window_start;
-                    p50 = w.os_p50;
-                    p99 = w.os_p99;
-                    mig = w.os_migrations;
-                    ioff = w.os_irq_off;
-                    ikey = w.os_irq_key;
-                    ival = w.os_irq_val;
-                    soff = w.os_sirq_off;
-                    skey = w.os_sirq_key;
-                    sval = w.os_sirq_val;
-                } else {
-                    ws = up<int64_t>("os_ws", w.os_window_start, n);
-                    p50 = up<int64_t>("os_p50", w.os_p50, n);
-                    p99 = up<int64_t>("os_p99", w.os_p99, n);
-                    mig = up<int64_t>("os_mig", w.os_migrations, n);
-                    ioff = up<uint64_t>("os_ioff", w.os_irq_off, n + 1);
-                    const uint64_t ni = w.os_irq_off[n], ns = w.os_sirq_off[n];
-                    ikey = up<uint32_t>("os_ikey", w.os_irq_key, ni);
-                    ival = up<int64_t>("os_ival", w.os_irq_val, ni);
-                    soff = up<uint64_t>("os_soff", w.os_sirq_off, n + 1);
-                    skey = up<uint32_t>("os_skey", w.os_sirq_key, ns);
-                    sval = up<int64_t>("os_sval", w.os_sirq_val, ns);
-                }
-                int* err = dev<int>("os_err", 1);
-                zero(err, 4);
-                LAUNCH(k_os_sums, grid_for(n), kThreads, n, d_rank, ws, p50, p99, mig, ioff, ikey, ival, soff, skey,
-                       sval, d_off, w.window_start_ns, uint32_t(w.n_counter_names), irq, irqp, sirq, sirqp, mp50, mp99,
-                       migs, pres, err);
-                if (get1(err)) fail(STG_EINVAL, "os counter key index out of range");
+        if (w.n_os) {
+            const uint64_t n = w.n_os;
+            const int32_t* d_rank = sdev ? w.os_rank : static_cast<const int32_t*>(c.buf("os_rank").p);
+            const int64_t *ws, *p50, *p99, *mig, *ival, *sval;
+            const uint64_t *ioff, *soff;
+            const uint32_t *ikey, *skey;
+            if (sdev) {
+                ws = w.os_window_start;
+                p50 = w.os_p50;
+                p99 = w.os_p99;
+                mig = w.os_migrations;
+                ioff = w.os_irq_off;
+                ikey = w.os_irq_key;
+                ival = w.os_irq_val;
+                soff = w.os_sirq_off;
+                skey = w.os_sirq_key;
+                sval = w.os_sirq_val;
+            } else {
+                ws = up<int64_t>("os_ws", w.os_window_start, n);
+                p50 = up<int64_t>("os_p50", w.os_p50, n);
+                p99 = up<int64_t>("os_p99", w.os_p99, n);
+                mig = up<int64_t>("os_mig", w.os_migrations, n);
+                ioff = up<uint64_t>("os_ioff", w.os_irq_off, n + 1);
+                const uint64_t ni = w.os_irq_off[n], ns = w.os_sirq_off[n];
+                ikey = up<uint32_t>("os_ikey", w.os_irq_key, ni);
+                ival = up<int64_t>("os_ival", w.os_irq_val, ni);
+                soff = up<uint64_t>("os_soff", w.os_sirq_off, n + 1);
+                skey = up<uint32_t>("os_skey", w.os_sirq_key, ns);
+                sval = up<int64_t>("os_sval", w.os_sirq_val, ns);
             }
-            os_bufs = true;
+            LAUNCH(k_os_sums, grid_for(n), kThreads, n, d_rank, ws, p50, p99, mig, ioff, ikey, ival, soff, skey, sval,
+                   d_off, w.window_start_ns, uint32_t(w.n_counter_names), w8(sb.o_irq), d1 + sb.o_irqp, w8(sb.o_sirq),
+                   d1 + sb.o_sirqp, reinterpret_cast<long long*>(w8(sb.o_p50)),
+                   reinterpret_cast<long long*>(w8(sb.o_p99)), w8(sb.o_mig), d1 + sb.o_op,
+                   reinterpret_cast<int*>(w8(sb.o_err + 1)));
         }
         if (!shard) gpu_os_collect();
     }
-    bool gpu_bufs = false, os_bufs = false;
     // sharded side streams: each rank's sums live on the context that owns it
     // (zeros elsewhere; p50 / p99 are maxima of non-negative values), so a sum
-    // over the group reproduces the single-context arrays
+    // over the group reproduces the single-context block; the error flags are
+    // summed too, so every context sees the same validation result
     void gpu_os_reduce() {
-        const uint64_t K = w.n_kernel_names, C = std::max<uint32_t>(w.n_counter_names, 1), sp = uint64_t(span);
+        if (!sb.gpu && !sb.os) return;
         nccl(ncclGroupStart());
-        if (gpu_bufs) {
-            auto sums = dev<unsigned long long>("gpu_sums", sp * K);
-            auto pres = dev<uint8_t>("gpu_pres", sp * K);
-            nccl(ncclAllReduce(sums, sums, sp * K, ncclUint64, ncclSum, comm(), st));
-            nccl(ncclAllReduce(pres, pres, sp * K, ncclUint8, ncclMax, comm(), st));
-        }
-        if (os_bufs) {
-            for (const char* nm : {"os_irq", "os_sirq"}) {
-                auto p = dev<unsigned long long>(nm, sp * C);
-                nccl(ncclAllReduce(p, p, sp * C, ncclUint64, ncclSum, comm(), st));
-            }
-            for (const char* nm : {"os_irqp", "os_sirqp"}) {
-                auto p = dev<uint8_t>(nm, sp * C);
-                nccl(ncclAllReduce(p, p, sp * C, ncclUint8, ncclMax, comm(), st));
-            }
-            for (const char* nm : {"os_mp50", "os_mp99", "os_migs"}) {
-                auto p = dev<long long>(nm, sp);
-                nccl(ncclAllReduce(p, p, sp, ncclInt64, ncclSum, comm(), st));
-            }
-            auto pres = dev<uint8_t>("os_pres", sp);
-            nccl(ncclAllReduce(pres, pres, sp, ncclUint8, ncclMax, comm(), st));
-        }
+        nccl(ncclAllReduce(sb.d, sb.d, sb.n8, ncclInt64, ncclSum, comm(), st));
+        nccl(ncclAllReduce(sb.d + sb.n8 * 8, sb.d + sb.n8 * 8, sb.n1, ncclUint8, ncclMax, comm(), st));
         nccl(ncclGroupEnd());
         gpu_os_collect();
     }
     void gpu_os_collect() {
-        if (gpu_bufs) {
-            const uint64_t K = w.n_kernel_names;
-            std::vector<unsigned long long> hs(span * K);
-            std::vector<uint8_t> hp(span * K);
-            down(hs.data(), dev<unsigned long long>("gpu_sums", span * K), span * K);
-            down(hp.data(), dev<uint8_t>("gpu_pres", span * K), span * K);
+        if (!sb.gpu && !sb.os) return;
+        std::vector<uint8_t> h(sb.n8 * 8 + sb.n1);
+        down(h.data(), sb.d, h.size());
+        const int64_t* h8 = reinterpret_cast<const int64_t*>(h.data());
+        const uint8_t* h1 = h.data() + sb.n8 * 8;
+        if (int32_t(h8[sb.o_err])) fail(STG_EINVAL, "gpu event kernel index out of range");
+        if (int32_t(h8[sb.o_err + 1])) fail(STG_EINVAL, "os counter key index out of range");
+        const uint64_t K = sb.K, C = sb.C;
+        if (sb.gpu)
             for (int32_t r = 0; r < span; ++r)
                 for (uint64_t k = 0; k < K; ++k)
-                    if (hp[r * K + k]) res.gpu[r][w.kernel_names[k]] += int64_t(hs[r * K + k]);
-        }
-        if (os_bufs) {
-            const uint64_t C = std::max<uint32_t>(w.n_counter_names, 1);
-            std::vector<unsigned long long> hi(span * C), hs(span * C), hm(span);
-            std::vector<uint8_t> hip(span * C), hsp(span * C), hp(span);
-            std::vector<long long> h50(span), h99(span);
-            down(hi.data(), dev<unsigned long long>("os_irq", span * C), span * C);
-            down(hs.data(), dev<unsigned long long>("os_sirq", span * C), span * C);
-            down(hip.data(), dev<uint8_t>("os_irqp", span * C), span * C);
-            down(hsp.data(), dev<uint8_t>("os_sirqp", span * C), span * C);
-            down(hp.data(), dev<uint8_t>("os_pres", span), span);
-            down(h50.data(), dev<long long>("os_mp50", span), span);
-            down(h99.data(), dev<long long>("os_mp99", span), span);
-            down(hm.data(), dev<unsigned long long>("os_migs", span), span);
+                    if (h1[sb.o_gp + r * K + k]) res.gpu[r][w.kernel_names[k]] += h8[sb.o_gs + r * K + k];
+        if (sb.os)
             for (int32_t r = 0; r < span; ++r) {
-                if (!hp[r]) continue;
+                if (!h1[sb.o_op + r]) continue;
                 OsAcc& a = res.os[r];
                 for (uint32_t k = 0; k < w.n_counter_names; ++k) {
-                    if (hip[r * C + k]) a.interrupts[w.counter_names[k]] += int64_t(hi[r * C + k]);
-                    if (hsp[r * C + k]) a.softirqs[w.counter_names[k]] += int64_t(hs[r * C + k]);
+                    if (h1[sb.o_irqp + r * C + k]) a.interrupts[w.counter_names[k]] += h8[sb.o_irq + r * C + k];
+                    if (h1[sb.o_sirqp + r * C + k]) a.softirqs[w.counter_names[k]] += h8[sb.o_sirq + r * C + k];
                 }
-                a.p50 = h50[r];
-                a.p99 = h99[r];
-                a.migrations = int64_t(hm[r]);
+                a.p50 = h8[sb.o_p50 + r];
+                a.p99 = h8[sb.o_p99 + r];
+                a.migrations = h8[sb.o_mig + r];
             }
-        }
     }
 
     // 4 resident CTAs of 8 warps per SM (64 registers); the table staging in
@@ -2509,19 +2481,38 @@ struct Runner {
             res.waterline_json = "{\"error\": \"waterline requires at least 2 ranks\"}";
             return;
         }
-        const uint64_t NG = c.dict.size() + gn.lab.size();
+        // per-name sums only over the names some GPU's profiles use: the sorted
+        // union of the contexts' global keys (not the whole dictionary)
+        std::vector<uint32_t> gk(F);
+        if (F) {
+            dense_name(0);
+            for (uint64_t f = 0; f < F; ++f) gk[f] = to_global(h_dense_final[f]);
+        }
+        std::vector<uint32_t> uk;
+        {
+            std::vector<uint32_t> mine(gk);
+            std::sort(mine.begin(), mine.end());
+            mine.erase(std::unique(mine.begin(), mine.end()), mine.end());
+            std::vector<uint8_t> b(mine.size() * 4);
+            if (!mine.empty()) std::memcpy(b.data(), mine.data(), b.size());
+            for (const auto& v : allgather_bytes(b)) {
+                const size_t m = v.size() / 4, o = uk.size();
+                uk.resize(o + m);
+                if (m) std::memcpy(uk.data() + o, v.data(), m * 4);
+                std::inplace_merge(uk.begin(), uk.begin() + o, uk.end());
+            }
+            uk.erase(std::unique(uk.begin(), uk.end()), uk.end());
+        }
+        std::vector<uint32_t> cix(F);
+        for (uint64_t f = 0; f < F; ++f) cix[f] = uint32_t(std::lower_bound(uk.begin(), uk.end(), gk[f]) - uk.begin());
+        const uint64_t NG = std::max<uint64_t>(uk.size(), 1);
         double* s1 = dev<double>("wl_s1", NG);
         unsigned* np = dev<unsigned>("wl_np", NG);
         double* s2 = dev<double>("wl_s2", NG);
         zero(s1, NG * 8);
         zero(np, NG * 4);
         zero(s2, NG * 8);
-        std::vector<uint32_t> gk(F);
-        if (F) {
-            dense_name(0);
-            for (uint64_t f = 0; f < F; ++f) gk[f] = to_global(h_dense_final[f]);
-        }
-        uint32_t* d_gk = up<uint32_t>("wl_gkey", gk.data(), std::max<uint64_t>(F, 1));
+        uint32_t* d_gk = up<uint32_t>("wl_gkey", cix.data(), std::max<uint64_t>(F, 1));
         uint32_t* rows = up<uint32_t>("wl_rows", res.cpu_rank_index.data(), std::max<size_t>(nr, 1));
         if (F && nr) LAUNCH(k_wl_pass1, grid_for(F * 32), kThreads, F, rows, int(nr), d_incl, d_totals, d_gk, s1, np);
         nccl(ncclAllReduce(s1, s1, NG, ncclFloat64, ncclSum, comm(), st));
@@ -2544,7 +2535,8 @@ struct Runner {
         res.wl_flags = std::min<uint64_t>(get1(n_out), cap);
         res.wl_F = F;
         res.wl_dist = true;
-        res.wl_NG = NG;
+        res.wl_NG = uk.size();
+        res.wl_ukeys = std::move(uk);
         res.g_lab_final = gn.lab_final;
         res.g_lab = gn.lab;
         res.wl_gkey = gk;
