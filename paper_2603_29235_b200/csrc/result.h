@@ -91,7 +91,7 @@ struct Result {
     std::vector<uint64_t> g_lab_final;
     std::vector<std::string> g_lab;
     std::vector<uint32_t> wl_gkey;  // dense name -> global key
-    std::vector<uint32_t> wl_ukeys;  // global keys of the waterline's names (sorted union over the group)
+    uint64_t wl_NGF = 0;  // global name space; device byte map "wl_umap" marks the waterline's names
     std::string gname(uint32_t g) const {
         auto it = std::lower_bound(g_lab_final.begin(), g_lab_final.end(), uint64_t(g));
         if (it != g_lab_final.end() && *it == g) return g_lab[size_t(it - g_lab_final.begin())];

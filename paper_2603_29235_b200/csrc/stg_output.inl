@@ -434,6 +434,13 @@ std::string groupdata_json(Ctx& c, uint32_t parts) {
 static std::string waterline_json_dist(Ctx& c) {
     Result& r = *c.result;
     const uint64_t NG = r.wl_NG, nf = r.wl_flags;
+    std::vector<uint32_t> ukeys;  // global keys of the waterline's names (set in the byte map)
+    {
+        std::vector<uint8_t> um(r.wl_NGF);
+        d2h(c, um.data(), "wl_umap", r.wl_NGF);
+        for (uint64_t g = 0; g < r.wl_NGF; ++g)
+            if (um[g]) ukeys.push_back(uint32_t(g));
+    }
     std::vector<double> hm(NG), hs(NG);
     std::vector<unsigned> hnp(NG);
     d2h(c, hm.data(), "wlg_mean", NG);
@@ -455,7 +462,7 @@ static std::string waterline_json_dist(Ctx& c) {
         if (!first) j.raw(", ");
         first = false;
         j.raw("[");
-        j.str(r.gname(r.wl_ukeys[g]));
+        j.str(r.gname(ukeys[g]));
         j.raw(", ");
         j.num(hm[g]);
         j.raw(", ");

@@ -1956,15 +1956,17 @@ struct Runner {
         std::vector<std::pair<std::string, uint32_t>> all;
         auto gathered = allgather_bytes(mine);
         mark("g:allgather");
-        for (const auto& b : gathered) {
+        for (const auto& b : gathered) {  // each context's labels arrive sorted: merge
             const uint8_t* p = b.data();
             uint32_t n = b.empty() ? 0 : get<uint32_t>(p);
+            const size_t o = all.size();
             for (uint32_t i = 0; i < n; ++i) {
                 uint32_t pos = get<uint32_t>(p);
                 all.emplace_back(get_str(p), pos);
             }
+            if (!std::is_sorted(all.begin() + o, all.end())) std::sort(all.begin() + o, all.end());
+            std::inplace_merge(all.begin(), all.begin() + o, all.end());
         }
-        std::sort(all.begin(), all.end());
         all.erase(std::unique(all.begin(), all.end(),
                               [](const auto& a, const auto& b) { return a.first == b.first; }),
                   all.end());
@@ -2488,31 +2490,29 @@ struct Runner {
             dense_name(0);
             for (uint64_t f = 0; f < F; ++f) gk[f] = to_global(h_dense_final[f]);
         }
-        std::vector<uint32_t> uk;
-        {
-            std::vector<uint32_t> mine(gk);
-            std::sort(mine.begin(), mine.end());
-            mine.erase(std::unique(mine.begin(), mine.end()), mine.end());
-            std::vector<uint8_t> b(mine.size() * 4);
-            if (!mine.empty()) std::memcpy(b.data(), mine.data(), b.size());
-            for (const auto& v : allgather_bytes(b)) {
-                const size_t m = v.size() / 4, o = uk.size();
-                uk.resize(o + m);
-                if (m) std::memcpy(uk.data() + o, v.data(), m * 4);
-                std::inplace_merge(uk.begin(), uk.begin() + o, uk.end());
-            }
-            uk.erase(std::unique(uk.begin(), uk.end()), uk.end());
-        }
-        std::vector<uint32_t> cix(F);
-        for (uint64_t f = 0; f < F; ++f) cix[f] = uint32_t(std::lower_bound(uk.begin(), uk.end(), gk[f]) - uk.begin());
-        const uint64_t NG = std::max<uint64_t>(uk.size(), 1);
+        // used-name byte map over the global name space, OR-ed over the group
+        // (all-reduce max), scanned into compact indices on the device
+        const uint64_t NGF = c.dict.size() + gn.lab.size();
+        uint8_t* umap = dev<uint8_t>("wl_umap", NGF);
+        zero(umap, NGF);
+        uint32_t* d_gkey = up<uint32_t>("wl_gkey_g", gk.data(), std::max<uint64_t>(F, 1));
+        if (F) LAUNCH(k_mark_u8, grid_for(F), kThreads, F, d_gkey, umap);
+        nccl(ncclAllReduce(umap, umap, NGF, ncclUint8, ncclMax, comm(), st));
+        uint32_t* u32 = dev<uint32_t>("wl_u32", NGF + 1);
+        uint32_t* uscan = dev<uint32_t>("wl_uscan", NGF + 1);
+        LAUNCH(k_u8_to_u32, grid_for(NGF + 1), kThreads, NGF, umap, u32);
+        excl_sum(u32, uscan, NGF + 1);
+        const uint64_t NU = get1(uscan + NGF);
+        uint32_t* d_gk = dev<uint32_t>("wl_gkey", std::max<uint64_t>(F, 1));
+        if (F) LAUNCH(k_gather_u32, grid_for(F), kThreads, F, d_gkey, uscan, d_gk);
+        const uint64_t NG = std::max<uint64_t>(NU, 1);
         double* s1 = dev<double>("wl_s1", NG);
         unsigned* np = dev<unsigned>("wl_np", NG);
         double* s2 = dev<double>("wl_s2", NG);
         zero(s1, NG * 8);
         zero(np, NG * 4);
         zero(s2, NG * 8);
-        uint32_t* d_gk = up<uint32_t>("wl_gkey", cix.data(), std::max<uint64_t>(F, 1));
+
         uint32_t* rows = up<uint32_t>("wl_rows", res.cpu_rank_index.data(), std::max<size_t>(nr, 1));
         if (F && nr) LAUNCH(k_wl_pass1, grid_for(F * 32), kThreads, F, rows, int(nr), d_incl, d_totals, d_gk, s1, np);
         nccl(ncclAllReduce(s1, s1, NG, ncclFloat64, ncclSum, comm(), st));
@@ -2535,8 +2535,8 @@ struct Runner {
         res.wl_flags = std::min<uint64_t>(get1(n_out), cap);
         res.wl_F = F;
         res.wl_dist = true;
-        res.wl_NG = uk.size();
-        res.wl_ukeys = std::move(uk);
+        res.wl_NG = NU;
+        res.wl_NGF = NGF;
         res.g_lab_final = gn.lab_final;
         res.g_lab = gn.lab;
         res.wl_gkey = gk;

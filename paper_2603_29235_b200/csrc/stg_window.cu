@@ -2562,6 +2562,14 @@ __global__ void k_flag_g(uint64_t F, const uint32_t* rows, int R, const unsigned
     }
 }
 
+__global__ void k_mark_u8(uint64_t n, const uint32_t* idx, uint8_t* map) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        map[idx[i]] = 1;
+}
+__global__ void k_u8_to_u32(uint64_t n, const uint8_t* a, uint32_t* b) {  // b[n] = 0
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i <= n; i += uint64_t(gridDim.x) * blockDim.x)
+        b[i] = i < n ? a[i] : 0u;
+}
 __global__ void k_scatter_add(uint64_t n, const uint32_t* to, const unsigned long long* v, unsigned long long* out) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
         atomicAdd(out + to[i], v[i]);
