@@ -14,9 +14,12 @@ resident in HBM (84 GB per GPU >> 126 MB L2, so no L2 flush is needed).
                   [--ranks R] [--spr S] [--no-e2e] [--no-cpu-baseline]
 
 N > 1: launched by torchrun, one process per GPU; the N GPUs analyse ONE
-communication group of N x 128 ranks, each GPU holding the sample streams of
-its 128 ranks (weak scaling: 128 M samples per GPU), with libstg's NCCL
-exchange inside the window; timing is the max over ranks.
+communication group of N x 128 ranks, each GPU holding the sample streams,
+collective events and GPU / OS records of its own 128 ranks (weak scaling:
+128 M samples per GPU; stg_window.shard_streams = STG_SHARD_COLL |
+STG_SHARD_SIDE), with libstg's NCCL exchange inside the window; timing is the
+max over ranks.  --config c3 / c4 shard one fixed 1,024-rank window over the
+GPUs instead (strong scaling).
 """
 from __future__ import annotations
 

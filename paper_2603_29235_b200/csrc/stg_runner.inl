@@ -527,10 +527,8 @@ struct Runner {
         LAUNCH(k_iota, grid_for(n_seg), kThreads, d_segid, n_seg);
         sort_pairs(d_segrank, d_segrank_s, d_segid, d_rsegs, n_seg, rbits);
         LAUNCH(k_rank_offsets, grid_for(sp + 1), kThreads, span, d_segrank_s, n_seg, d_rso);
-        const long long dmin = get1(d_dmin);
-        const int dbits = std::max(1, bits_for(uint64_t(-dmin)));
         LAUNCH(k_coll_median_sel, unsigned(std::min<int64_t>(span, 148 * 4)), kMedThreads, int(span), d_rso, d_rsegs, seg_pos,
-               dval, dmin, dbits, d_off, d_has_off, cnts + 2);
+               dval, d_dmin, d_off, d_has_off, cnts + 2);
         // windowed complete instances ordered by max aligned exit
         unsigned long long* aexit = dev<unsigned long long>("c_aexit", I);
         zero(aexit, I * 8);  // int64 0: build_group_data initialises max_exit to 0
@@ -834,10 +832,8 @@ struct Runner {
             LAUNCH(k_iota, grid_for(n_seg), kThreads, d_segid, n_seg);
             sort_pairs(d_segrank, d_segrank_s, d_segid, d_rsegs, n_seg, cl.rbits);
             LAUNCH(k_rank_offsets, grid_for(sp + 1), kThreads, span, d_segrank_s, n_seg, d_rso);
-            const long long dmin = get1(d_dmin);
-            const int dbits = std::max(1, bits_for(uint64_t(-dmin)));
             LAUNCH(k_coll_median_sel, unsigned(std::min<int64_t>(span, 148 * 4)), kMedThreads, int(span), d_rso, d_rsegs,
-                   cl.seg_pos, dval, dmin, dbits, d_off, d_has_off, cnts + 2);
+                   cl.seg_pos, dval, d_dmin, d_off, d_has_off, cnts + 2);
         }
         // 6. windowed complete instances, ordered by the max aligned exit
         unsigned long long* aexit = dev<unsigned long long>("c_aexit", I);
@@ -2479,6 +2475,7 @@ struct Runner {
         STG_CUDA(cudaMemcpyAsync(drt, &nrl, 8, cudaMemcpyHostToDevice, st));
         nccl(ncclAllReduce(drt, drt, 1, ncclUint64, ncclSum, comm(), st));
         const uint64_t RT = get1(drt);
+        mark("w:ranks");
         if (RT < 2) {
             res.waterline_json = "{\"error\": \"waterline requires at least 2 ranks\"}";
             return;
@@ -2503,6 +2500,7 @@ struct Runner {
         LAUNCH(k_u8_to_u32, grid_for(NGF + 1), kThreads, NGF, umap, u32);
         excl_sum(u32, uscan, NGF + 1);
         const uint64_t NU = get1(uscan + NGF);
+        mark("w:union");
         uint32_t* d_gk = dev<uint32_t>("wl_gkey", std::max<uint64_t>(F, 1));
         if (F) LAUNCH(k_gather_u32, grid_for(F), kThreads, F, d_gkey, uscan, d_gk);
         const uint64_t NG = std::max<uint64_t>(NU, 1);
@@ -2519,6 +2517,7 @@ struct Runner {
         nccl(ncclAllReduce(np, np, NG, ncclUint32, ncclSum, comm(), st));
         if (F && nr) LAUNCH(k_wl_pass2, grid_for(F * 32), kThreads, F, rows, int(nr), d_incl, d_totals, d_gk, s1, np, double(RT), s2);
         nccl(ncclAllReduce(s2, s2, NG, ncclFloat64, ncclSum, comm(), st));
+        mark("w:sums");
         double* mean = dev<double>("wlg_mean", NG);
         double* sd = dev<double>("wlg_sd", NG);
         LAUNCH(k_wl_final, grid_for(NG), kThreads, NG, s1, np, s2, double(RT), mean, sd);

@@ -436,13 +436,15 @@ __device__ __forceinline__ void med_scan2(unsigned a, unsigned b, unsigned& ea, 
 }
 __global__ void __launch_bounds__(kMedThreads) k_coll_median_sel(int rank_span, const uint32_t* rso, const uint32_t* rsegs,
                                                                  const uint32_t* seg_pos, const int64_t* dval,
-                                                                 long long dmin, int dbits, int64_t* off,
+                                                                 const long long* dmin_p, int64_t* off,
                                                                  uint8_t* has_off, unsigned long long* n_total) {
     __shared__ unsigned hist[2][kMedBins];
     __shared__ unsigned s_ws[2][32];
     __shared__ unsigned long long s_pref[2], s_k[2], s_cnt;
     const int lane = threadIdx.x & 31;
     constexpr int U = 4;  // elements per thread per step: U loads in flight
+    const long long dmin = *dmin_p;  // min delta (<= 0): the keys are v - dmin in [0, -dmin]
+    const int dbits = dmin < 0 ? 64 - __clzll((unsigned long long)(-dmin)) : 1;
     const int nd = (dbits + kMedBits - 1) / kMedBits;
     for (int r = blockIdx.x; r < rank_span; r += gridDim.x) {
         const uint32_t j0 = rso[r], j1 = rso[r + 1];

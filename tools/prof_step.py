@@ -1,6 +1,7 @@
 import sys, time
+from pathlib import Path
 sys.argv = ["bench.py", "--ranks", "128", "--no-e2e", "--no-cpu-baseline"]
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import bench, torch, ctypes as C
 import paper_2603_29235_b200 as stg
 from paper_2603_29235_b200.abi import STG_MEM_DEVICE, config_struct, StgRunStats
