@@ -339,9 +339,10 @@ def reference_arm(a, wl, torch, threads: int, steps: int = 1, warmup: int = 0):
         tot_n += n
         print(f"[bench ref] step {i}: {n} samples in {t:.2f}s ({w:.2f}s wall)", file=sys.stderr, flush=True)
     return {"value": tot_n / tot_t, "unit": UNIT, "cores": ranks, "kind": "reference",
-            "sample": f"{max(1, steps)} x ({ranks} ranks x {k} samples) of the C2 workload (64-frame stacks, "
-                      f"3x{a.nsym}-symbol tables), build_group_data+diagnose in {tot_t:.2f}s; the reference reloads "
-                      "the 1M-entry SYMR tables once per aggregated record (resolve_stack cache is per call)",
+            "sample": f"{max(1, steps)} x ({ranks} ranks x {k} samples) of the {a.config.upper()} workload "
+                      f"({a.depth}-frame stacks, 3x{a.nsym}-symbol tables), build_group_data+diagnose in "
+                      f"{tot_t:.2f}s; the reference reloads the {a.nsym}-entry SYMR tables once per aggregated "
+                      "record (resolve_stack cache is per call)",
             "verdict": res["report"]["verdict"]}
 
 
@@ -768,7 +769,9 @@ def main():
     peak = pk.get("hbm_gbs", 6650.0)
     achieved = algo_bytes / (k_ms / 1e3) / 1e9
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": ncu_traffic("k_sym_agg", algo_bytes), "kernel": "k_sym_agg",
+            "frac": round(achieved / peak, 4),
+            "traffic": ncu_traffic("k_sym_agg_c3" if a.config == "c3" else "k_sym_agg", algo_bytes),
+            "kernel": "k_sym_agg",
             "kernel_ms": round(k_ms, 3), "algorithmic_bytes": algo_bytes,
             "pipeline_frac": round(algo_bytes / (ms / 1e3) / 1e9 / peak, 4),
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback 6.65 TB/s"}
