@@ -2009,6 +2009,36 @@ struct Runner {
     }
     // this context's exact fractions of CPU rank `rank` as (global key, value),
     // plus the dense index of each key for local follow-ups
+    std::vector<std::pair<uint32_t, double>> rank_fracs_global(int rank, std::vector<uint32_t>* dense_of) {
+        int i = cpu_index(rank);
+        uint64_t lo[2];
+        down(lo, d_line_off + i, 2);
+        auto fr = exact_fractions(lo[0], lo[1] - lo[0], h_n_in[i], false);
+        dense_name(0);  // ensure h_dense_final
+        std::vector<std::pair<uint32_t, double>> out;
+        for (const auto& [f, v] : fr) {
+            uint32_t g = to_global(h_dense_final[f]);
+            out.emplace_back(g, v);
+            if (dense_of) dense_of->push_back(f);  // parallel to out (keys ascending)
+        }
+        return out;
+    }
+    std::vector<std::pair<uint32_t, double>> bcast_fracs(std::vector<std::pair<uint32_t, double>> v, int root) {
+        std::vector<uint8_t> b;
+        if (c.wrank == root)
+            for (const auto& [k, x] : v) {
+                put<uint32_t>(b, k);
+                put<double>(b, x);
+            }
+        b = bcast_bytes(std::move(b), root);
+        std::vector<std::pair<uint32_t, double>> out;
+        for (const uint8_t* p = b.data(); p < b.data() + b.size();) {
+            uint32_t k = get<uint32_t>(p);
+            double x = get<double>(p);
+            out.emplace_back(k, x);
+        }
+        return out;
+    }
     std::vector<std::string> bcast_path(std::vector<std::string> path, int root) {
         std::vector<uint8_t> b;
         if (c.wrank == root)
@@ -2223,115 +2253,41 @@ struct Runner {
                 mark("d:owners");
                 const int os_ = cpu_owner[size_t(strag)], oq = cpu_owner[size_t(ref)];
                 if (os_ >= 0 && oq >= 0) {
-                    // cpu_diff across owners, candidates first (as on one GPU): the
-                    // reference's owner sends its inclusive counts by global key;
-                    // the straggler's owner keeps the names whose estimated
-                    // difference can pass delta (the margin bounds both sequential
-                    // sums) and sums their exact fractions in line order; the
-                    // reference's owner adds the exact fractions of those names.
-                    inclusive_counts();
-                    if (F) dense_name(0);  // h_dense_final
-                    auto gkey = [&](uint32_t f) { return to_global(h_dense_final[f]); };
-                    auto row_of = [&](int ri, std::vector<unsigned long long>& row, uint64_t (&lo)[2]) {
-                        row.assign(F, 0);
-                        if (F) down(row.data(), d_incl + uint64_t(ri) * F, F);
-                        down(lo, d_line_off + ri, 2);
-                    };
-                    std::vector<uint8_t> bA;
-                    if (c.wrank == oq) {
-                        const int ri = cpu_index(ref);
-                        std::vector<unsigned long long> row;
-                        uint64_t lo[2];
-                        row_of(ri, row, lo);
-                        put<uint64_t>(bA, h_n_in[size_t(ri)]);
-                        put<uint64_t>(bA, lo[1] - lo[0]);
-                        for (uint64_t f = 0; f < F; ++f)
-                            if (row[f]) {
-                                put<uint32_t>(bA, gkey(uint32_t(f)));
-                                put<uint64_t>(bA, row[f]);
+                    std::vector<uint32_t> dense_of;
+                    std::vector<std::pair<uint32_t, double>> fs_, fr_;
+                    if (c.wrank == os_) fs_ = rank_fracs_global(strag, &dense_of);
+                    if (c.wrank == oq) fr_ = rank_fracs_global(ref, nullptr);
+                    mark("d:fracs");
+                    {  // one all-gather carries both lists from their owners
+                        std::vector<uint8_t> mine;
+                        auto pack = [&](const std::vector<std::pair<uint32_t, double>>& v) {
+                            put<uint64_t>(mine, v.size());
+                            for (const auto& [k, x] : v) {
+                                put<uint32_t>(mine, k);
+                                put<double>(mine, x);
                             }
-                    }
-                    bA = bcast_bytes(std::move(bA), oq);
-                    mark("d:refcounts");
-                    std::vector<std::pair<uint32_t, uint64_t>> rc;  // reference: (global key, inclusive count)
-                    uint64_t tot_r = 0, nl_r = 0;
-                    {
-                        const uint8_t* p = bA.data();
-                        tot_r = get<uint64_t>(p);
-                        nl_r = get<uint64_t>(p);
-                        while (p < bA.data() + bA.size()) {
-                            const uint32_t k = get<uint32_t>(p);
-                            rc.emplace_back(k, get<uint64_t>(p));
-                        }
-                        std::sort(rc.begin(), rc.end());
-                    }
-                    std::vector<uint8_t> bB;
-                    std::vector<uint32_t> dense_of;  // straggler owner: candidate -> dense name
-                    uint64_t slo[2] = {0, 0};
-                    if (c.wrank == os_) {
-                        const int si = cpu_index(strag);
-                        std::vector<unsigned long long> row;
-                        row_of(si, row, slo);
-                        const double ts = double(h_n_in[size_t(si)]), tr = double(tot_r);
-                        const double margin = double((slo[1] - slo[0]) + nl_r + 8) * std::ldexp(1.0, -50);
-                        std::vector<uint8_t> want(std::max<uint64_t>(F, 1), 0);
-                        for (uint64_t f = 0; f < F; ++f) {
-                            if (!row[f]) continue;
-                            const uint32_t k = gkey(uint32_t(f));
-                            auto it = std::lower_bound(rc.begin(), rc.end(), std::make_pair(k, uint64_t(0)));
-                            const double fr = it != rc.end() && it->first == k ? double(it->second) / tr : 0.0;
-                            want[f] = double(row[f]) / ts - fr > cfg.delta - margin;
-                        }
-                        const uint8_t* d_want = up<uint8_t>("xf_want", want.data(), want.size());
-                        auto fr2 = exact_fractions2(slo[0], slo[1] - slo[0], h_n_in[size_t(si)], 0, 0, 0, false,
-                                                    nullptr, nullptr, nullptr, d_want);
-                        for (const auto& [f, v] : fr2[0]) {
-                            put<uint32_t>(bB, gkey(f));
-                            put<double>(bB, v);
-                            dense_of.push_back(f);
-                        }
-                    }
-                    bB = bcast_bytes(std::move(bB), os_);
-                    std::vector<std::pair<uint32_t, double>> fs_;
-                    for (const uint8_t* p = bB.data(); p < bB.data() + bB.size();) {
-                        const uint32_t k = get<uint32_t>(p);
-                        fs_.emplace_back(k, get<double>(p));
-                    }
-                    mark("d:fracs_s");
-                    std::vector<uint8_t> bC;
-                    if (c.wrank == oq) {
-                        const int ri = cpu_index(ref);
-                        std::vector<std::pair<uint32_t, uint32_t>> kf(F);  // (global key, dense name)
-                        for (uint64_t f = 0; f < F; ++f) kf[f] = {gkey(uint32_t(f)), uint32_t(f)};
-                        std::sort(kf.begin(), kf.end());
-                        std::vector<uint8_t> want(std::max<uint64_t>(F, 1), 0);
-                        bool any = false;
-                        for (const auto& [k, v] : fs_) {
-                            auto it = std::lower_bound(kf.begin(), kf.end(), std::make_pair(k, uint32_t(0)));
-                            if (it != kf.end() && it->first == k) {
-                                want[it->second] = 1;
-                                any = true;
+                        };
+                        pack(fs_);
+                        pack(fr_);
+                        auto all = allgather_bytes(mine);
+                        auto unpack = [&](const std::vector<uint8_t>& b, int which) {
+                            const uint8_t* p = b.data();
+                            std::vector<std::pair<uint32_t, double>> v;
+                            for (int w = 0; w <= which; ++w) {
+                                uint64_t n = get<uint64_t>(p);
+                                v.clear();
+                                for (uint64_t i = 0; i < n; ++i) {
+                                    uint32_t k = get<uint32_t>(p);
+                                    double x = get<double>(p);
+                                    v.emplace_back(k, x);
+                                }
                             }
-                        }
-                        if (any) {
-                            uint64_t lo[2];
-                            down(lo, d_line_off + ri, 2);
-                            const uint8_t* d_want = up<uint8_t>("xf_want", want.data(), want.size());
-                            auto fr2 = exact_fractions2(lo[0], lo[1] - lo[0], h_n_in[size_t(ri)], 0, 0, 0, false,
-                                                        nullptr, nullptr, nullptr, d_want);
-                            for (const auto& [f, v] : fr2[0]) {
-                                put<uint32_t>(bC, gkey(f));
-                                put<double>(bC, v);
-                            }
-                        }
+                            return v;
+                        };
+                        fs_ = unpack(all[size_t(os_)], 0);
+                        fr_ = unpack(all[size_t(oq)], 1);
                     }
-                    bC = bcast_bytes(std::move(bC), oq);
-                    std::vector<std::pair<uint32_t, double>> fr_;
-                    for (const uint8_t* p = bC.data(); p < bC.data() + bC.size();) {
-                        const uint32_t k = get<uint32_t>(p);
-                        fr_.emplace_back(k, get<double>(p));
-                    }
-                    mark("d:fracs_r");
+                    mark("d:bcast");
                     struct Cand { std::string fn; double fs, fr, d; uint32_t key; };
                     std::vector<Cand> cands;
                     size_t j = 0;
@@ -2349,8 +2305,10 @@ struct Runner {
                         concluded = STG_VERDICT_CPU_INTERFERENCE;
                         std::vector<std::string> path;
                         if (c.wrank == os_) {
+                            uint64_t lo[2];
+                            down(lo, d_line_off + is, 2);
                             auto it = std::lower_bound(fs_.begin(), fs_.end(), std::make_pair(cands.front().key, -1e300));
-                            path = hottest(slo[0], slo[1], dense_of[size_t(it - fs_.begin())], false);
+                            path = hottest(lo[0], lo[1], dense_of[size_t(it - fs_.begin())], false);
                         }
                         rep.top_path = bcast_path(std::move(path), os_);
                         mark("d:path");
