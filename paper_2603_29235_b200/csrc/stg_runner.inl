@@ -1073,12 +1073,8 @@ struct Runner {
     // shared memory covers up to kMaxSmemBins binaries
     // 4 resident CTAs of 8 warps per SM (64 registers); the table staging in
     // shared memory covers up to kMaxSmemBins binaries
-    // Shallow windows (<= 16 frames per sample on average: C1, C3) take the
-    // instance with the coalesced any-depth phase 1; deep ones (C2) the other.
     void launch_sym_agg(const AggParams& p, unsigned grid, bool smem_tabs) {
-        if (smem_tabs && p.n_frames <= 16 * p.n_samples) {
-            k_sym_agg<true, 4, 1, 1, false, true><<<grid, kThreads, 0, st>>>(p);
-        } else if (smem_tabs) {
+        if (smem_tabs) {
             k_sym_agg<true, 4, 1, 1><<<grid, kThreads, 0, st>>>(p);
         } else {
             k_sym_agg<false, 4, 1, 1><<<grid, kThreads, 0, st>>>(p);

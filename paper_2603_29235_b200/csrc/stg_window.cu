@@ -1343,9 +1343,7 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* g) {
 //           open-addressing table with __match_any pre-aggregation;
 //  misses   the warp symbolizes the missing chains cooperatively and fills
 //           the cache.
-//  GCOOP    shallow / ragged windows (host-selected instance): the coalesced
-//           phase 1 for any depth, below.
-template <bool SMEM_TABS, int MINB, int UB, int UBC, bool COOP = true, bool GCOOP = false>
+template <bool SMEM_TABS, int MINB, int UB, int UBC, bool COOP = true>
 __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
     __shared__ DevTable s_tabs[kMaxSmemBins];
     if (SMEM_TABS) {
@@ -1353,7 +1351,6 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
         __syncthreads();
     }
     __shared__ ulonglong4 s_acc[kThreads / 32][32];  // cooperative phase 1: (Σa, Σb, leaf pc, leaf bin) per sample
-    __shared__ uint64_t s_gf0[GCOOP ? kThreads / 32 : 1][33];  // shallow cooperative form: the batch's CSR bounds
     const DevTable* tabs = SMEM_TABS ? s_tabs : p.tabs;
     const int lane = threadIdx.x & 31;
     const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
@@ -1423,7 +1420,6 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
             atomicMin(p.err_empty + r, (unsigned long long)(i - rs));
             inwin = false;
         }
-        const uint64_t f0r = f0, f1r_all = f1;  // the CSR bounds before out-of-window samples are emptied
         if (!inwin) f0 = f1 = 0;
         const uint32_t depth = uint32_t(f1 - f0);
         uint64_t leaf_pc = 0, ha = 0, hb = 0;
@@ -1485,75 +1481,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sym_agg(AggParams p) {
                 __syncwarp();
             }
         }
-        // ---------------- phase 1, cooperative form for shallow / ragged batches
-        // (<= 64 aligned blocks per batch, e.g. C1 / C3): lane l loads block l of
-        // each 256-frame step of the batch's contiguous range (coalesced), and
-        // adds, for every in-window sample the block intersects, that sample's
-        // raw_block term (its frames outside the non-leaf range zeroed, the
-        // block position counted from the sample's own aligned start) to the
-        // sample's sums in shared memory; the block holding a sample's first
-        // frame also hands over its leaf.  Same terms, same sums as the
-        // per-lane form: every block intersecting [f0, f1) contributes once.
-        bool gcoop = false;
-        if (GCOOP && !coop) {
-            const unsigned inm = __ballot_sync(0xffffffffu, inwin);
-            const int last = int(min(uint64_t(31), p.n_samples - 1 - bt * 32));
-            const uint64_t A8 = __shfl_sync(0xffffffffu, f0r, 0) & ~7ull;
-            uint64_t Bend = __shfl_sync(0xffffffffu, f1r_all, last);
-            gcoop = inm != 0 && Bend > A8 && Bend - A8 <= 512;
-            if (gcoop) {
-                const int wid = threadIdx.x >> 5;
-                uint64_t* sf = s_gf0[wid];
-                sf[lane] = lane <= last ? f0r : Bend;
-                if (lane == 31) sf[32] = Bend;
-                s_acc[wid][lane] = make_ulonglong4(0, 0, 0, 0);
-                __syncwarp();
-                for (uint64_t bb = A8 + 8ull * lane; bb < Bend; bb += 256) {
-                    uint64_t pcs[8];
-                    uint4 bq;
-                    load_block<0>(p.pc, p.bin, p.n_frames, bb, pcs, bq);
-                    int s = 0;  // last sample starting at or before bb
-#pragma unroll
-                    for (int st = 16; st > 0; st >>= 1)
-                        if (s + st < 32 && sf[s + st] <= bb) s += st;
-                    for (; s < 32 && sf[s] < bb + 8; ++s) {
-                        const uint64_t g0 = sf[s], g1 = sf[s + 1];
-                        if (!((inm >> s) & 1) || g1 <= bb) continue;
-                        uint64_t q[8];
-                        uint32_t bw[4] = {bq.x, bq.y, bq.z, bq.w};
-#pragma unroll
-                        for (int t = 0; t < 8; ++t) {
-                            const uint64_t j = bb + t;
-                            q[t] = pcs[t];
-                            if (j == g0) {
-                                s_acc[wid][s].z = pcs[t];
-                                s_acc[wid][s].w = (bw[t >> 1] >> (16 * (t & 1))) & 0xffffu;
-                            }
-                            if (!(j > g0 && j < g1)) {
-                                q[t] = 0;
-                                bw[t >> 1] &= ~(0xffffu << (16 * (t & 1)));
-                            }
-                        }
-                        uint64_t xa = 0, xb = 0;
-                        raw_block(q, uint64_t(bw[0]) | (uint64_t(bw[1]) << 32), uint64_t(bw[2]) | (uint64_t(bw[3]) << 32),
-                                  (bb - (g0 & ~7ull)) >> 3, p.salt, xa, xb);
-                        atomicAdd(&s_acc[wid][s].x, xa);
-                        atomicAdd(&s_acc[wid][s].y, xb);
-                    }
-                }
-                __syncwarp();
-                const ulonglong4 v = s_acc[wid][lane];
-                if (inwin) {
-                    ha = v.x;
-                    hb = v.y;
-                    leaf_pc = v.z;
-                    leaf_bin = uint32_t(v.w);
-                }
-                __syncwarp();
-            }
-        }
         // ---------------- phase 1, per-lane form: this lane's frames, 8 per step
-        if (inwin && !coop && !gcoop) {
+        if (inwin && !coop) {
             const uint64_t a0 = f0 & ~7ull;
             for (uint64_t bs = a0; bs < f1; bs += 8 * UB) {
                 // UB blocks per step: all their loads are issued before any hashing
