@@ -1248,9 +1248,13 @@ struct Runner {
             p.use_pfx = pass == 0;
             p.weak_pfx = cfg.debug_weak_prefix_key != 0;
             zero(pfx, size_t(pfx_cap) * sizeof(PfxSlot));
-            // 4 resident CTAs of 8 warps per SM (64 registers), 4 waves' worth of CTAs
+            // 4 resident CTAs of 8 warps per SM (64 registers), 16 waves' worth of
+            // CTAs: each warp owns a contiguous batch range, so the CTAs in flight
+            // cover a narrow slice of the rank-major samples — few ranks' hash
+            // tables are hot in L2 at a time (C2: 17.5 -> 16.2 ms against 4 waves,
+            // profiles/r2e_grid_sweep.md) and the last wave's tail is short
             const uint64_t need = ((n_s + 31) / 32 + (kThreads / 32) - 1) / (kThreads / 32);
-            unsigned grid = unsigned(dev_sms) * 16;
+            unsigned grid = unsigned(dev_sms) * 64;
             if (need < grid) grid = unsigned(std::max<uint64_t>(need, 1));
             cudaEventRecord(ev[2], st);
             if (attempt == 0 && pass == 0) cudaEventRecord(ev_pre, st);
