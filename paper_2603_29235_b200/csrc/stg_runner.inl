@@ -2009,35 +2009,29 @@ struct Runner {
     }
     // this context's exact fractions of CPU rank `rank` as (global key, value),
     // plus the dense index of each key for local follow-ups
-    std::vector<std::pair<uint32_t, double>> rank_fracs_global(int rank, std::vector<uint32_t>* dense_of) {
-        int i = cpu_index(rank);
-        uint64_t lo[2];
-        down(lo, d_line_off + i, 2);
-        auto fr = exact_fractions(lo[0], lo[1] - lo[0], h_n_in[i], false);
-        dense_name(0);  // ensure h_dense_final
-        std::vector<std::pair<uint32_t, double>> out;
-        for (const auto& [f, v] : fr) {
-            uint32_t g = to_global(h_dense_final[f]);
-            out.emplace_back(g, v);
-            if (dense_of) dense_of->push_back(f);  // parallel to out (keys ascending)
-        }
-        return out;
-    }
-    std::vector<std::pair<uint32_t, double>> bcast_fracs(std::vector<std::pair<uint32_t, double>> v, int root) {
-        std::vector<uint8_t> b;
-        if (c.wrank == root)
-            for (const auto& [k, x] : v) {
-                put<uint32_t>(b, k);
-                put<double>(b, x);
+    // dense name of a global key on this context (-1: not used here): the
+    // inverse of to_global, checked by the round trip
+    int64_t dense_of_global(uint32_t g) const {
+        uint64_t fin;
+        auto it = std::lower_bound(gn.lab_final.begin(), gn.lab_final.end(), uint64_t(g));
+        if (it != gn.lab_final.end() && *it == g) {  // a label: find it among this context's labels
+            const std::string& lab = gn.lab[size_t(it - gn.lab_final.begin())];
+            auto lt = std::lower_bound(res.unk_labels.begin(), res.unk_labels.end(), lab);
+            if (lt == res.unk_labels.end() || *lt != lab) return -1;
+            fin = res.unk_final[size_t(lt - res.unk_labels.begin())];
+        } else {  // a dictionary name: i, shifted by this context's labels sorting before it
+            const uint64_t i = g - uint64_t(it - gn.lab_final.begin());
+            uint64_t lo = 0, hi = res.unk_final.size();  // labels whose dictionary position <= i
+            while (lo < hi) {
+                const uint64_t mid = (lo + hi) / 2;
+                if (res.unk_final[mid] - mid <= i) lo = mid + 1; else hi = mid;
             }
-        b = bcast_bytes(std::move(b), root);
-        std::vector<std::pair<uint32_t, double>> out;
-        for (const uint8_t* p = b.data(); p < b.data() + b.size();) {
-            uint32_t k = get<uint32_t>(p);
-            double x = get<double>(p);
-            out.emplace_back(k, x);
+            fin = i + lo;
         }
-        return out;
+        auto dt = std::lower_bound(h_dense_final.begin(), h_dense_final.end(), uint32_t(fin));
+        if (dt == h_dense_final.end() || *dt != fin) return -1;
+        const uint32_t f = uint32_t(dt - h_dense_final.begin());
+        return to_global(h_dense_final[f]) == g ? int64_t(f) : -1;
     }
     std::vector<std::string> bcast_path(std::vector<std::string> path, int root) {
         std::vector<uint8_t> b;
@@ -2253,39 +2247,65 @@ struct Runner {
                 mark("d:owners");
                 const int os_ = cpu_owner[size_t(strag)], oq = cpu_owner[size_t(ref)];
                 if (os_ >= 0 && oq >= 0) {
+                    // candidates first (as on one GPU): d = fs - fr <= fs, so the
+                    // straggler's owner sums exact fractions only for names whose
+                    // own estimate can exceed delta; the reference's owner then adds
+                    // the exact fractions of those names; both lists are small
+                    inclusive_counts();
+                    if (F) dense_name(0);  // h_dense_final
                     std::vector<uint32_t> dense_of;
                     std::vector<std::pair<uint32_t, double>> fs_, fr_;
-                    if (c.wrank == os_) fs_ = rank_fracs_global(strag, &dense_of);
-                    if (c.wrank == oq) fr_ = rank_fracs_global(ref, nullptr);
+                    std::vector<uint8_t> bS, bR;
+                    if (c.wrank == os_) {
+                        const int si = cpu_index(strag);
+                        uint64_t lo[2];
+                        down(lo, d_line_off + si, 2);
+                        const double margin = double(lo[1] - lo[0] + 8) * std::ldexp(1.0, -50);
+                        uint8_t* want = dev<uint8_t>("xf_want", std::max<uint64_t>(F, 1));
+                        if (F)
+                            LAUNCH(k_frac_want, grid_for(F), kThreads, F, d_incl + uint64_t(si) * F,
+                                   double(h_n_in[size_t(si)]), cfg.delta - margin, want);
+                        auto fr2 = exact_fractions2(lo[0], lo[1] - lo[0], h_n_in[size_t(si)], 0, 0, 0, false, nullptr,
+                                                    nullptr, nullptr, want);
+                        for (const auto& [f, v] : fr2[0]) {
+                            put<uint32_t>(bS, to_global(h_dense_final[f]));
+                            put<double>(bS, v);
+                            dense_of.push_back(f);
+                        }
+                    }
+                    bS = bcast_bytes(std::move(bS), os_);
+                    for (const uint8_t* p = bS.data(); p < bS.data() + bS.size();) {
+                        const uint32_t k = get<uint32_t>(p);
+                        fs_.emplace_back(k, get<double>(p));
+                    }
                     mark("d:fracs");
-                    {  // one all-gather carries both lists from their owners
-                        std::vector<uint8_t> mine;
-                        auto pack = [&](const std::vector<std::pair<uint32_t, double>>& v) {
-                            put<uint64_t>(mine, v.size());
-                            for (const auto& [k, x] : v) {
-                                put<uint32_t>(mine, k);
-                                put<double>(mine, x);
+                    if (c.wrank == oq) {
+                        const int ri = cpu_index(ref);
+                        std::vector<uint8_t> want(std::max<uint64_t>(F, 1), 0);
+                        bool any = false;
+                        for (const auto& [g, v] : fs_) {
+                            const int64_t f = dense_of_global(g);
+                            if (f >= 0) {
+                                want[size_t(f)] = 1;
+                                any = true;
                             }
-                        };
-                        pack(fs_);
-                        pack(fr_);
-                        auto all = allgather_bytes(mine);
-                        auto unpack = [&](const std::vector<uint8_t>& b, int which) {
-                            const uint8_t* p = b.data();
-                            std::vector<std::pair<uint32_t, double>> v;
-                            for (int w = 0; w <= which; ++w) {
-                                uint64_t n = get<uint64_t>(p);
-                                v.clear();
-                                for (uint64_t i = 0; i < n; ++i) {
-                                    uint32_t k = get<uint32_t>(p);
-                                    double x = get<double>(p);
-                                    v.emplace_back(k, x);
-                                }
+                        }
+                        if (any) {
+                            uint64_t lo[2];
+                            down(lo, d_line_off + ri, 2);
+                            const uint8_t* d_want = up<uint8_t>("xf_want", want.data(), want.size());
+                            auto fr2 = exact_fractions2(lo[0], lo[1] - lo[0], h_n_in[size_t(ri)], 0, 0, 0, false,
+                                                        nullptr, nullptr, nullptr, d_want);
+                            for (const auto& [f, v] : fr2[0]) {
+                                put<uint32_t>(bR, to_global(h_dense_final[f]));
+                                put<double>(bR, v);
                             }
-                            return v;
-                        };
-                        fs_ = unpack(all[size_t(os_)], 0);
-                        fr_ = unpack(all[size_t(oq)], 1);
+                        }
+                    }
+                    bR = bcast_bytes(std::move(bR), oq);
+                    for (const uint8_t* p = bR.data(); p < bR.data() + bR.size();) {
+                        const uint32_t k = get<uint32_t>(p);
+                        fr_.emplace_back(k, get<double>(p));
                     }
                     mark("d:bcast");
                     struct Cand { std::string fn; double fs, fr, d; uint32_t key; };

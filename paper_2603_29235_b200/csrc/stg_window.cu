@@ -2385,6 +2385,14 @@ __global__ void k_pair_emit(uint64_t n, uint64_t n0, const uint64_t* lkey0, cons
 // d = fs - fr > delta only if its exact-integer estimate passes delta - margin,
 // margin bounding the rounding of the reference's sequential sums (see
 // Runner::diagnose); those names alone get the exact line-order sums.
+// names of one rank whose own inclusive fraction can exceed lim (a name's
+// cpu_diff d = fs - fr <= fs, so only these can pass delta)
+__global__ void k_frac_want(uint64_t F, const unsigned long long* row, double total, double lim, uint8_t* want) {
+    for (uint64_t f = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; f < F; f += uint64_t(gridDim.x) * blockDim.x) {
+        const unsigned long long c = row[f];
+        want[f] = c && __ddiv_rn(__ull2double_rn(c), total) > lim;
+    }
+}
 __global__ void k_diff_cands(uint64_t F, const unsigned long long* incl, uint32_t R, uint32_t is, uint32_t iq,
                              double ts, double tr, double lim, uint8_t* want) {
     for (uint64_t f = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; f < F; f += uint64_t(gridDim.x) * blockDim.x) {
