@@ -90,7 +90,6 @@ struct Result {
     uint64_t wl_NG = 0;
     std::vector<uint64_t> g_lab_final;
     std::vector<std::string> g_lab;
-    std::vector<uint32_t> wl_gkey;  // dense name -> global key
     uint64_t wl_NGF = 0;  // global name space; device byte map "wl_umap" marks the waterline's names
     std::string gname(uint32_t g) const {
         auto it = std::lower_bound(g_lab_final.begin(), g_lab_final.end(), uint64_t(g));

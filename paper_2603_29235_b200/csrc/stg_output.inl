@@ -454,6 +454,8 @@ static std::string waterline_json_dist(Ctx& c) {
     d2h(c, fth.data(), "wl_oth", nf);
     std::vector<int32_t> rids(r.n_window_ranks);
     d2h(c, rids.data(), "rids", r.n_window_ranks);
+    std::vector<uint32_t> gkey(r.wl_F);  // dense name -> global key
+    d2h(c, gkey.data(), "wl_gkey_g", r.wl_F);
     JsonW j;
     j.raw("{\"functions\": [");
     bool first = true;
@@ -481,7 +483,7 @@ static std::string waterline_json_dist(Ctx& c) {
         j.raw("[");
         j.num(int64_t(rids[fr[k]]));
         j.raw(", ");
-        j.str(r.gname(r.wl_gkey[ff[k]]));
+        j.str(r.gname(gkey[ff[k]]));
         j.raw(", ");
         j.num(ffr[k]);
         j.raw(", ");

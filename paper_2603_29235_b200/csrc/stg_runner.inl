@@ -2506,17 +2506,20 @@ struct Runner {
         }
         // per-name sums only over the names some GPU's profiles use: the sorted
         // union of the contexts' global keys (not the whole dictionary)
-        std::vector<uint32_t> gk(F);
+        // dense name -> global key on the device (to_global, one thread per name)
+        uint32_t* d_gkey = dev<uint32_t>("wl_gkey_g", std::max<uint64_t>(F, 1));
         if (F) {
-            dense_name(0);
-            for (uint64_t f = 0; f < F; ++f) gk[f] = to_global(h_dense_final[f]);
+            const uint64_t nl = gn.loc_final.size(), ng = gn.pos.size();
+            const uint64_t* d_lf = up<uint64_t>("tg_lf", gn.loc_final.data(), std::max<uint64_t>(nl, 1));
+            const uint32_t* d_lg = up<uint32_t>("tg_lg", gn.loc_global.data(), std::max<uint64_t>(nl, 1));
+            const uint32_t* d_ps = up<uint32_t>("tg_ps", gn.pos.data(), std::max<uint64_t>(ng, 1));
+            LAUNCH(k_to_global, grid_for(F), kThreads, F, d_dense_final, d_lf, d_lg, nl, d_ps, ng, d_gkey);
         }
         // used-name byte map over the global name space, OR-ed over the group
         // (all-reduce max), scanned into compact indices on the device
         const uint64_t NGF = c.dict.size() + gn.lab.size();
         uint8_t* umap = dev<uint8_t>("wl_umap", NGF);
         zero(umap, NGF);
-        uint32_t* d_gkey = up<uint32_t>("wl_gkey_g", gk.data(), std::max<uint64_t>(F, 1));
         if (F) LAUNCH(k_mark_u8, grid_for(F), kThreads, F, d_gkey, umap);
         nccl(ncclAllReduce(umap, umap, NGF, ncclUint8, ncclMax, comm(), st));
         uint32_t* u32 = dev<uint32_t>("wl_u32", NGF + 1);
@@ -2562,7 +2565,6 @@ struct Runner {
         res.wl_NGF = NGF;
         res.g_lab_final = gn.lab_final;
         res.g_lab = gn.lab;
-        res.wl_gkey = gk;
         res.waterline_json.clear();  // rendered on request
     }
 

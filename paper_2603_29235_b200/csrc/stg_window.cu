@@ -2572,6 +2572,30 @@ __global__ void k_flag_g(uint64_t F, const uint32_t* rows, int R, const unsigned
     }
 }
 
+// Runner::to_global on the device: a local label maps through its global key,
+// a dictionary name i to i + (global labels whose dictionary position <= i)
+__global__ void k_to_global(uint64_t F, const uint32_t* dense_final, const uint64_t* loc_final,
+                            const uint32_t* loc_global, uint64_t nl, const uint32_t* pos, uint64_t ng, uint32_t* out) {
+    for (uint64_t f = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; f < F; f += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t fin = dense_final[f];
+        uint64_t lo = 0, hi = nl;  // lower_bound(loc_final, fin)
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (loc_final[mid] < fin) lo = mid + 1; else hi = mid;
+        }
+        if (lo < nl && loc_final[lo] == fin) {
+            out[f] = loc_global[lo];
+            continue;
+        }
+        const uint64_t i = fin - lo;
+        uint64_t a = 0, b = ng;  // upper_bound(pos, i)
+        while (a < b) {
+            const uint64_t mid = (a + b) >> 1;
+            if (pos[mid] <= i) a = mid + 1; else b = mid;
+        }
+        out[f] = uint32_t(i + a);
+    }
+}
 __global__ void k_mark_u8(uint64_t n, const uint32_t* idx, uint8_t* map) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
         map[idx[i]] = 1;
