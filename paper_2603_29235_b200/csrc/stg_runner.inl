@@ -529,6 +529,10 @@ struct Runner {
         LAUNCH(k_rank_offsets, grid_for(sp + 1), kThreads, span, d_segrank_s, n_seg, d_rso);
         LAUNCH(k_coll_median_sel, unsigned(std::min<int64_t>(span, 148 * 4)), kMedThreads, int(span), d_rso, d_rsegs, seg_pos,
                dval, d_dmin, d_off, d_has_off, cnts + 2);
+        // The clock offsets are all the samples stage needs; the rest of stage d
+        // (windowing, lateness, straggler statistics) feeds only the decision
+        // ladder, so it runs on the side stream under k_sym_agg (side_coll_tail).
+        coll_tail = [=]() {
         // windowed complete instances ordered by max aligned exit
         unsigned long long* aexit = dev<unsigned long long>("c_aexit", I);
         zero(aexit, I * 8);  // int64 0: build_group_data initialises max_exit to 0
@@ -594,6 +598,31 @@ struct Runner {
             d2h += (n_w - 1) * 8;
         }
         coll_result_download();
+        };
+    }
+    std::function<void()> coll_tail;  // the deferred rest of the replicated stage d
+    // run the deferred part of stage d on the side stream (after everything the
+    // main stream did before k_sym_agg), or on the main stream when no samples
+    // stage gave it a kernel to hide under
+    void side_coll_tail(bool side = true) {
+        if (!coll_tail) return;
+        auto f = std::move(coll_tail);
+        coll_tail = nullptr;
+        if (!side) {
+            f();
+            return;
+        }
+        if (!c.side) STG_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+        STG_CUDA(cudaStreamWaitEvent(c.side, ev_pre, 0));
+        cudaStream_t keep = st;
+        st = c.side;
+        try {
+            f();
+        } catch (...) {
+            st = keep;
+            throw;
+        }
+        st = keep;
     }
 
     // detect_straggler's per-instance sums (diagnosis.cpp:82-96) over the ranks
@@ -1262,7 +1291,10 @@ struct Runner {
             STG_CUDA(cudaGetLastError());
             ++launches;
             cudaEventRecord(ev[3], st);
-            if (attempt == 0) side_gpu_os();  // host + side-stream work while the kernel streams
+            if (attempt == 0) {  // host + side-stream work while the kernel streams
+                side_gpu_os();
+                side_coll_tail();
+            }
             res.agg_attempts = attempt + 1;
             down(hso.data(), so, so_n);
             mark("s:k_sym_agg");
@@ -2689,6 +2721,7 @@ struct Runner {
             err_stage = 2;
             if (!gpu_os_done) gpu_os();
         });
+        side_coll_tail(false);  // no samples stage ran it
         if (side_sharded()) gpu_os_reduce();
         mark("samples+fold");
         if (ev_unset_fold()) {

@@ -13,6 +13,7 @@
 //      temporal_diff; the decision ladder of diagnose (diagnosis.cpp:301-432) runs
 //      on the host over these device-side summaries.
 #include <cub/cub.cuh>
+#include <functional>
 #include <nccl.h>
 
 #include <algorithm>
