@@ -604,13 +604,13 @@ struct Runner {
     // run the deferred part of stage d on the side stream (after everything the
     // main stream did before k_sym_agg), or on the main stream when no samples
     // stage gave it a kernel to hide under
-    void side_coll_tail(bool side = true) {
-        if (!coll_tail) return;
+    bool side_coll_tail(bool side = true) {
+        if (!coll_tail) return false;
         auto f = std::move(coll_tail);
         coll_tail = nullptr;
         if (!side) {
             f();
-            return;
+            return true;
         }
         if (!c.side) STG_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
         STG_CUDA(cudaStreamWaitEvent(c.side, ev_pre, 0));
@@ -623,6 +623,7 @@ struct Runner {
             throw;
         }
         st = keep;
+        return true;
     }
 
     // detect_straggler's per-instance sums (diagnosis.cpp:82-96) over the ranks
@@ -2721,7 +2722,7 @@ struct Runner {
             err_stage = 2;
             if (!gpu_os_done) gpu_os();
         });
-        side_coll_tail(false);  // no samples stage ran it
+        if (side_coll_tail(false)) cudaEventRecord(ev[1], st);  // no samples stage: stage d ends here
         if (side_sharded()) gpu_os_reduce();
         mark("samples+fold");
         if (ev_unset_fold()) {
