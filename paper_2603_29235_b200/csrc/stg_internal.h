@@ -26,8 +26,10 @@ struct Error : std::runtime_error {
 #define STG_CUDA(x)                                                                   \
     do {                                                                              \
         cudaError_t e_ = (x);                                                         \
-        if (e_ != cudaSuccess)                                                        \
+        if (e_ != cudaSuccess) {                                                      \
+            cudaGetLastError(); /* leave no error state behind for the host app */   \
             ::stg::fail(STG_ECUDA, std::string(#x " -> ") + cudaGetErrorString(e_));  \
+        }                                                                             \
     } while (0)
 
 // --------------------------------------------------------- device tables

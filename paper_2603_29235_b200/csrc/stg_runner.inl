@@ -2543,9 +2543,10 @@ struct Runner {
         uint32_t* d_gkey = dev<uint32_t>("wl_gkey_g", std::max<uint64_t>(F, 1));
         if (F) {
             const uint64_t nl = gn.loc_final.size(), ng = gn.pos.size();
-            const uint64_t* d_lf = up<uint64_t>("tg_lf", gn.loc_final.data(), std::max<uint64_t>(nl, 1));
-            const uint32_t* d_lg = up<uint32_t>("tg_lg", gn.loc_global.data(), std::max<uint64_t>(nl, 1));
-            const uint32_t* d_ps = up<uint32_t>("tg_ps", gn.pos.data(), std::max<uint64_t>(ng, 1));
+            // (empty label lists: nothing is copied, the kernel does not read them)
+            const uint64_t* d_lf = up<uint64_t>("tg_lf", gn.loc_final.data(), nl);
+            const uint32_t* d_lg = up<uint32_t>("tg_lg", gn.loc_global.data(), nl);
+            const uint32_t* d_ps = up<uint32_t>("tg_ps", gn.pos.data(), ng);
             LAUNCH(k_to_global, grid_for(F), kThreads, F, d_dense_final, d_lf, d_lg, nl, d_ps, ng, d_gkey);
         }
         // used-name byte map over the global name space, OR-ed over the group
@@ -2571,7 +2572,7 @@ struct Runner {
         zero(np, NG * 4);
         zero(s2, NG * 8);
 
-        uint32_t* rows = up<uint32_t>("wl_rows", res.cpu_rank_index.data(), std::max<size_t>(nr, 1));
+        uint32_t* rows = up<uint32_t>("wl_rows", res.cpu_rank_index.data(), nr);
         if (F && nr) LAUNCH(k_wl_pass1, grid_for(F * 32), kThreads, F, rows, int(nr), d_incl, d_totals, d_gk, s1, np);
         nccl(ncclAllReduce(s1, s1, NG, ncclFloat64, ncclSum, comm(), st));
         nccl(ncclAllReduce(np, np, NG, ncclUint32, ncclSum, comm(), st));
