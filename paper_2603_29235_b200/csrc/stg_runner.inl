@@ -100,9 +100,17 @@ struct Runner {
     // the sample stream: they run on a side stream (ordered after everything the
     // main stream did before k_sym_agg) while k_sym_agg streams, and their host
     // downloads synchronise only the side stream.
+    // The side stream has the highest priority: its few small kernels are
+    // scheduled ahead of k_sym_agg's remaining CTAs instead of after them.
+    void ensure_side() {
+        if (c.side) return;
+        int lo = 0, hi = 0;
+        STG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        STG_CUDA(cudaStreamCreateWithPriority(&c.side, cudaStreamNonBlocking, hi));
+    }
     void side_gpu_os() {
         if (gpu_os_done || side_sharded()) return;  // sharded: main stream, reduced over NCCL after the samples
-        if (!c.side) STG_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+        ensure_side();
         STG_CUDA(cudaStreamWaitEvent(c.side, ev_pre, 0));
         cudaStream_t keep = st;
         st = c.side;
@@ -612,7 +620,7 @@ struct Runner {
             f();
             return true;
         }
-        if (!c.side) STG_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+        ensure_side();
         STG_CUDA(cudaStreamWaitEvent(c.side, ev_pre, 0));
         cudaStream_t keep = st;
         st = c.side;
