@@ -1,4 +1,5 @@
-# final validation of the committed head (2 GPUs: the dist tests run too)
+# Full GPU validation of the committed head on a 2-GPU box: pytest -m gpu (incl. the 2-GPU tests), smoke, the driver's bench lines.
+# usage: gpurun --gpus 2 -- bash tools/gpu_validate.sh   (outputs in gpurun_out/s22_*)
 timeout 1800 python -m pytest tests -m gpu -q -x --durations=10 > gpurun_out/s22_gputest.log 2>&1; echo rc=$? >> gpurun_out/s22_gputest.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/s22_smoke.log 2>&1
 timeout 600 python bench.py > gpurun_out/s22_bench.json 2> gpurun_out/s22_bench.err
