@@ -786,8 +786,11 @@ def main():
                        "inputs": f"resident in HBM, {(10 * win.n_frames + 16 * win.n_samples) / 1e9:.1f} GB/GPU "
                                  "> L2 (no flush needed)",
                        "group_ranks": wl.group_size,
-                       "parallelism": f"one {wl.group_size}-rank group sharded by rank over {world} GPU(s), "
-                                      "NCCL exchange of straggler/reference fractions + waterline all-reduce"},
+                       "parallelism": (f"one {wl.group_size}-rank group sharded by rank over {world} GPUs "
+                                       "(samples, collectives, GPU / OS streams); NCCL inside libstg: stage-d "
+                                       "partials and straggler chains, cpu_diff fractions from their owners, "
+                                       "waterline reductions") if world > 1 else
+                                      f"one {wl.group_size}-rank group on 1 GPU"},
             "verdict": rep["verdict"], "flagged_ranks": rep["flagged_ranks"],
             "prefix_cache": {"hits": s["prefix_hits"], "misses": s["prefix_misses"]},
             "stage_ms": {"total_device": float(np.median(tot_ms)), "symbolize_aggregate": k_ms,
